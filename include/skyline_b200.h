@@ -1,0 +1,181 @@
+/*
+ * skyline_b200.h — C ABI of the B200-native two-phase parallel skyline engine.
+ *
+ * This is the drop-in boundary for the reference engine's hot path
+ * (arxiv 2411.14968 artifact, /root/reference/proj). Every entry point below
+ * names the reference interface it replaces. Plain pointers and sizes only;
+ * no C++ or torch types cross this boundary.
+ *
+ *   reference                                   this ABI
+ *   ------------------------------------------  --------------------------------
+ *   skyline::run            engine.hpp:88        sky_run
+ *   skyline::EngineConfig   engine.hpp:30-38     sky_config
+ *   skyline::PartitionConfig partition.hpp:21-27 sky_config.{strategy,p,m,seed,slice_dim}
+ *   skyline::RunResult/PhaseMetrics engine.hpp:40-57  sky_result
+ *   skyline::make_assignment partition.hpp:102   sky_assign
+ *   skyline::snap_slices    partition.hpp:99     sky_snap_slices
+ *   skyline::relative_skyline core.hpp:79        sky_relative_skyline
+ *   skyline::sfs / skyline_bruteforce            sky_skyline
+ *     (sequential.hpp:29, core.hpp:75)
+ *   skyline::select_representatives_sorted +     sky_representatives
+ *     prune_dominated_reps (filter.hpp:46,67)
+ *   exception taxonomy core.hpp:13-34            sky_status codes
+ *
+ * Coordinates are float32, row-major n x d, ids are 0-based row indices
+ * (core.cpp:43). The reference stores doubles; float32 -> double is exact,
+ * so every comparison made here is the comparison the reference makes on the
+ * upcast input.
+ */
+#ifndef SKYLINE_B200_H
+#define SKYLINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SKY_API __attribute__((visibility("default")))
+#else
+#define SKY_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKY_ABI_VERSION 1
+
+/* Return codes mirror the reference's exception classes (core.hpp:13-34). */
+typedef enum sky_status {
+    SKY_OK = 0,
+    SKY_E_CONFIG = 1,        /* ConfigError        core.hpp:25 */
+    SKY_E_DIMENSION = 2,     /* DimensionError     core.hpp:17 */
+    SKY_E_NORMALIZATION = 3, /* NormalizationError core.hpp:21 */
+    SKY_E_DATA = 4,          /* DataError          core.hpp:29 */
+    SKY_E_IO = 5,            /* IoError            core.hpp:32 */
+    SKY_E_CUDA = 10,         /* CUDA runtime failure (no reference analogue) */
+    SKY_E_NCCL = 11,         /* NCCL failure */
+    SKY_E_INTERNAL = 12
+} sky_status;
+
+/* Strategy (partition.hpp:14-19). */
+enum { SKY_RANDOM = 0, SKY_GRID = 1, SKY_ANGULAR = 2, SKY_SLICED = 3 };
+/* FilterKind (engine.hpp:19-23). */
+enum { SKY_FILTER_NONE = 0, SKY_FILTER_GRID = 1, SKY_FILTER_REPRESENTATIVE = 2 };
+/* RepSelection (filter.hpp:21-25); only Sorted is on the hot path (Region and
+ * Random return SKY_E_CONFIG; SURVEY.md 8(f) ranks them "next"). */
+enum { SKY_REPS_SORTED = 0, SKY_REPS_REGION = 1, SKY_REPS_RANDOM = 2 };
+/* MergeKind (engine.hpp:25-28). */
+enum { SKY_MERGE_SEQUENTIAL = 0, SKY_MERGE_NOSEQ = 1 };
+/* Local algorithm (new: the reference has SFS only). */
+enum { SKY_LOCAL_SFS = 0, SKY_LOCAL_BNL = 1 };
+
+typedef struct sky_config {
+    /* PartitionConfig (partition.hpp:21-27) */
+    int32_t strategy;
+    uint64_t p;          /* target partition count */
+    uint64_t m;          /* slices per dimension (grid/angular); 0 = snap from p */
+    uint64_t seed;       /* random partitioning seed */
+    uint64_t slice_dim;  /* sliced only */
+    /* EngineConfig (engine.hpp:30-38) */
+    int32_t filter;
+    int32_t rep_selection;
+    uint64_t rep_q;      /* default 5 (engine.hpp:34) */
+    int32_t merge;
+    uint64_t workers;    /* kept for validation parity (engine.cpp:20); must be >= 1 */
+    /* B200 extensions */
+    int32_t local_algo;       /* SKY_LOCAL_SFS | SKY_LOCAL_BNL */
+    uint32_t bnl_window_cap;  /* BNL window capacity in points (0 -> 4096) */
+    int32_t count_tests;      /* nonzero: kernels count dominance tests */
+} sky_config;
+
+/* RunResult + PhaseMetrics (engine.hpp:40-57). Owned by the library until
+ * sky_result_free. */
+typedef struct sky_result {
+    int64_t* ids;               /* skyline ids, ascending (engine.cpp:132) */
+    uint64_t n_ids;
+    uint64_t effective_p;       /* RunResult::effective_p */
+    uint64_t input_size, input_dim;
+    uint64_t union_size;        /* PhaseMetrics::union_size */
+    uint64_t filtered_count;    /* PhaseMetrics::filtered_count */
+    uint64_t final_size;        /* PhaseMetrics::final_size */
+    uint64_t* local_skyline_sizes; /* [effective_p] */
+    double partition_ms, local_ms, merge_ms; /* device-timed phase durations */
+    double total_ms;            /* device time of the whole run */
+    uint64_t tests_reps, tests_local, tests_merge; /* executed dominance tests */
+    uint64_t n_reps;            /* representatives after pruning */
+    uint64_t angular_host_fixups; /* points whose angular slice sat on a boundary */
+    uint64_t h2d_bytes, d2h_bytes;
+    uint32_t kernel_launches;   /* kernels this library launched for the run */
+} sky_result;
+
+typedef struct sky_ctx sky_ctx;
+
+/* Context: one CUDA device, one stream, a grow-only device arena and pinned
+ * staging buffers. One call in flight per context. */
+SKY_API int sky_ctx_create(int device, sky_ctx** out);
+SKY_API void sky_ctx_destroy(sky_ctx* ctx);
+SKY_API const char* sky_last_error(const sky_ctx* ctx);
+/* Optional external stream (cudaStream_t passed as void*); NULL restores the
+ * context's own stream. */
+SKY_API int sky_ctx_set_stream(sky_ctx* ctx, void* stream);
+
+SKY_API void sky_config_default(sky_config* cfg);
+
+/* skyline::run (engine.hpp:88). `points` is a host pointer when
+ * points_on_device == 0 (copied H2D inside the call) or a device pointer on
+ * the context's device otherwise. */
+SKY_API int sky_run(sky_ctx* ctx, const float* points, uint64_t n, uint32_t d,
+            int normalized, int points_on_device, const sky_config* cfg,
+            sky_result* out);
+SKY_API void sky_result_free(sky_result* r);
+
+/* skyline::make_assignment (partition.hpp:102-103): partition_of[n] on the
+ * host, effective partition count in *effective_p. */
+SKY_API int sky_assign(sky_ctx* ctx, const float* points, uint64_t n, uint32_t d,
+               int normalized, const sky_config* cfg, uint64_t* partition_of,
+               uint64_t* effective_p);
+
+/* skyline::snap_slices (partition.hpp:99). Host only. */
+SKY_API int sky_snap_slices(uint64_t target_p, uint64_t k, uint64_t* out_m);
+
+/* skyline::relative_skyline (core.hpp:79): keep[i] = 1 iff no row of c
+ * dominates row i of r. Host arrays. */
+SKY_API int sky_relative_skyline(sky_ctx* ctx, const float* r, uint64_t nr,
+                         const float* c, uint64_t nc, uint32_t d,
+                         uint8_t* keep, uint64_t* tests);
+
+/* skyline::sfs / skyline_bruteforce (sequential.hpp:29, core.hpp:75): the
+ * skyline ids of one relation, ascending. *out_ids is malloc'ed; free with
+ * sky_free. */
+SKY_API int sky_skyline(sky_ctx* ctx, const float* points, uint64_t n, uint32_t d,
+                int64_t** out_ids, uint64_t* n_out, uint64_t* tests);
+
+/* select_representatives_sorted + prune_dominated_reps (filter.cpp:66-86,
+ * 139-145) over the partitions given by partition_of: rep ids ascending. */
+SKY_API int sky_representatives(sky_ctx* ctx, const float* points, uint64_t n,
+                        uint32_t d, const uint64_t* partition_of, uint64_t p,
+                        uint64_t q, int64_t** out_ids, uint64_t* n_out);
+
+SKY_API void sky_free(void* ptr);
+
+/* Host-side synthetic generators for the five BASELINE configs (not part of
+ * the reference API; used by bench and tests). kind: 1 uniform, 2/4
+ * anticorrelated (s~N(0.5,0.0625) + rejection), 3 correlated, 5 ints [0,16).
+ * Deterministic for (kind, n, d, seed) regardless of thread count. */
+SKY_API int sky_generate(int kind, uint64_t n, uint32_t d, uint64_t seed, float* out);
+
+/* Multi-rank planning helpers (host-only, pure functions; used by the
+ * NCCL path and by the gloo tests). Longest-processing-time assignment of
+ * `count` weighted units to `ranks` owners; owner[count]. */
+SKY_API int sky_plan_lpt(const uint64_t* weights, uint64_t count, int ranks, int32_t* owner);
+/* Balanced contiguous split of `count` candidates with per-candidate cost
+ * prefix sums: bounds[ranks+1]. */
+SKY_API int sky_plan_split(const uint64_t* cost_prefix, uint64_t count, int ranks, uint64_t* bounds);
+
+SKY_API int sky_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKYLINE_B200_H */

@@ -1,0 +1,195 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points over the UNMODIFIED reference engine
+// (/root/reference/proj/src/*.cpp, compiled in place by oracle/Makefile into
+// oracle/_ref/libskyref.so). Used by tests to pin oracle/sky_oracle.c, by
+// tests/golden/make_golden.py to produce fixtures, and by bench.py's
+// `--impl reference` arm to time the reference's own CPU path.
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "skyline/core.hpp"
+#include "skyline/engine.hpp"
+#include "skyline/filter.hpp"
+#include "skyline/partition.hpp"
+#include "skyline/sequential.hpp"
+#include "../include/skyline_b200.h"
+
+using namespace skyline;
+
+namespace {
+
+Dataset to_dataset(const float* pts, uint64_t n, uint32_t d, int normalized) {
+    Dataset r;
+    r.d = d;
+    r.normalized = normalized != 0;
+    r.points.resize(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        r.points[i].coords.assign(pts + i * d, pts + (i + 1) * d);  // float -> double, exact
+        r.points[i].id = static_cast<PointId>(i);
+    }
+    return r;
+}
+
+EngineConfig to_engine(const sky_config* c) {
+    EngineConfig e;
+    e.partition.strategy = static_cast<Strategy>(c->strategy);
+    e.partition.p = c->p;
+    e.partition.m = c->m;
+    e.partition.seed = c->seed;
+    e.partition.slice_dim = c->slice_dim;
+    e.filter = static_cast<FilterKind>(c->filter);
+    e.rep_selection = static_cast<RepSelection>(c->rep_selection);
+    e.rep_q = c->rep_q;
+    e.merge = static_cast<MergeKind>(c->merge);
+    e.workers = c->workers;
+    e.seed = c->seed;
+    return e;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SKY_OK;
+    } catch (const ConfigError&) {
+        return SKY_E_CONFIG;
+    } catch (const DimensionError&) {
+        return SKY_E_DIMENSION;
+    } catch (const NormalizationError&) {
+        return SKY_E_NORMALIZATION;
+    } catch (const DataError&) {
+        return SKY_E_DATA;
+    } catch (const IoError&) {
+        return SKY_E_IO;
+    } catch (...) {
+        return SKY_E_INTERNAL;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+struct skyref_result {
+    int64_t* ids;
+    uint64_t n_ids;
+    uint64_t effective_p;
+    uint64_t union_size, filtered_count, final_size, n_reps;
+    uint64_t* local_skyline_sizes;
+    double partition_ms, local_ms, merge_ms, run_ms;
+};
+
+int skyref_hardware_concurrency(void) {
+    unsigned n = std::thread::hardware_concurrency();
+    return n ? static_cast<int>(n) : 1;
+}
+
+// skyline::run on float32 rows upcast to double. run_ms is the steady_clock
+// time of run() alone (engine.cpp:144-194 phase timers summed by the caller).
+int skyref_run(const float* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+               skyref_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    return guarded([&] {
+        const Dataset r = to_dataset(pts, n, d, normalized);
+        const EngineConfig e = to_engine(cfg);
+        auto t0 = std::chrono::steady_clock::now();
+        RunResult res = run(r, e);
+        auto t1 = std::chrono::steady_clock::now();
+        out->run_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        out->n_ids = res.skyline.size();
+        out->ids = static_cast<int64_t*>(std::malloc((out->n_ids ? out->n_ids : 1) * sizeof(int64_t)));
+        for (uint64_t i = 0; i < out->n_ids; ++i) out->ids[i] = res.skyline.points[i].id;
+        out->effective_p = res.effective_p;
+        out->union_size = res.metrics.union_size;
+        out->filtered_count = res.metrics.filtered_count;
+        out->final_size = res.metrics.final_size;
+        const auto& ls = res.metrics.local_skyline_sizes;
+        out->local_skyline_sizes =
+            static_cast<uint64_t*>(std::malloc((ls.size() ? ls.size() : 1) * sizeof(uint64_t)));
+        for (size_t i = 0; i < ls.size(); ++i) out->local_skyline_sizes[i] = ls[i];
+        out->partition_ms = res.metrics.partition_ms;
+        out->local_ms = res.metrics.local_ms;
+        out->merge_ms = res.metrics.merge_ms;
+    });
+}
+
+void skyref_result_free(skyref_result* r) {
+    std::free(r->ids);
+    std::free(r->local_skyline_sizes);
+    std::memset(r, 0, sizeof(*r));
+}
+
+int skyref_assign(const float* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+                  uint64_t* partition_of, uint64_t* count) {
+    return guarded([&] {
+        const Dataset r = to_dataset(pts, n, d, normalized);
+        PartitionAssignment a = make_assignment(r, to_engine(cfg).partition);
+        for (uint64_t i = 0; i < n; ++i) partition_of[i] = a.partition_of[i];
+        *count = a.partition_count;
+    });
+}
+
+uint64_t skyref_bruteforce(const float* pts, uint64_t n, uint32_t d, int64_t* out) {
+    const Dataset r = to_dataset(pts, n, d, 0);
+    SkylineSet s = skyline_bruteforce(r);
+    for (size_t i = 0; i < s.size(); ++i) out[i] = s.points[i].id;
+    return s.size();
+}
+
+uint64_t skyref_sfs(const float* pts, uint64_t n, uint32_t d, int64_t* out) {
+    const Dataset r = to_dataset(pts, n, d, 0);
+    SkylineSet s = sfs(r);
+    for (size_t i = 0; i < s.size(); ++i) out[i] = s.points[i].id;
+    return s.size();
+}
+
+void skyref_relative_skyline(const float* rp, uint64_t nr, const float* cp, uint64_t nc, uint32_t d,
+                             uint8_t* keep) {
+    const Dataset r = to_dataset(rp, nr, d, 0);
+    Dataset c = to_dataset(cp, nc, d, 0);
+    for (auto& pt : c.points) pt.id += static_cast<PointId>(nr);
+    Dataset k = relative_skyline(r, c);
+    std::memset(keep, 0, nr);
+    for (const Point& t : k.points) keep[t.id] = 1;
+}
+
+uint64_t skyref_snap_slices(uint64_t target_p, uint64_t k) {
+    uint64_t m = 0;
+    guarded([&] { m = snap_slices(target_p, k); });
+    return m;
+}
+
+uint64_t skyref_angular_index(const float* x, uint32_t d, uint64_t m) {
+    Point t;
+    t.coords.assign(x, x + d);
+    return angular_index(t, m);
+}
+
+uint64_t skyref_grid_index(const float* x, uint32_t d, uint64_t m) {
+    Point t;
+    t.coords.assign(x, x + d);
+    uint64_t g = UINT64_MAX;
+    guarded([&] { g = grid_index(t, m); });
+    return g;
+}
+
+uint64_t skyref_representatives(const float* pts, uint64_t n, uint32_t d, const uint64_t* partition_of,
+                                uint64_t p, uint64_t q, int64_t* out) {
+    const Dataset r = to_dataset(pts, n, d, 0);
+    std::vector<Dataset> parts(p);
+    for (auto& part : parts) part.d = d;
+    for (uint64_t i = 0; i < n; ++i) parts[partition_of[i]].points.push_back(r.points[i]);
+    Representatives reps = select_representatives_sorted(parts, q, 1);
+    std::vector<int64_t> ids;
+    for (const Point& t : reps.points) ids.push_back(t.id);
+    std::sort(ids.begin(), ids.end());
+    for (size_t i = 0; i < ids.size(); ++i) out[i] = ids[i];
+    return ids.size();
+}
+
+}  // extern "C"

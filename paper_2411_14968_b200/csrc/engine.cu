@@ -1,0 +1,1118 @@
+// engine.cu — host orchestration of the two-phase skyline on one B200 and the
+// C ABI (include/skyline_b200.h).
+//
+// Mirrors skyline::run (reference engine.cpp:136-204) phase by phase:
+//   partition   make_assignment + split      -> k_prep (+ sliced rank sort), one
+//                                                radix sort by (pid, sum key)
+//   local       select_representatives_sorted -> k_rep_pick, prune via k_relsky
+//               rep_prefilter                 -> k_relsky over all rows (indirect)
+//               sfs / sfs_presorted           -> block skylines + in-partition
+//                                                relative skyline (k_relsky), or
+//                                                BNL (k_bnl)
+//   merge       merge_sequential / merge_noseq -> k_relsky against the union
+//               + potential_dominators           (or per-strategy pd segments)
+// The host side plans work items from partition offsets (one device->host
+// read per phase); all dominance tests run on the GPU.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace sky;
+
+struct sky_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    Arena dev;
+    PinnedArena pin;
+    int sm_count = 148;
+    int smem_optin = 0;
+    cudaEvent_t ev[6] = {};
+    uint32_t launches = 0;
+};
+
+namespace {
+
+enum Slot {
+    S_PTS, S_KEY_A, S_KEY_B, S_IDX_A, S_IDX_B, S_SK_A, S_SK_B, S_PID, S_MISC, S_AMB, S_OFF_A, S_OFF_B,
+    S_DEAD, S_POS, S_CUB, S_ITEMS, S_RANGES, S_REPCAND, S_REPROWS, S_RUNS,
+    S_SET0, S_SET0_K, S_SET0_I, S_SET1, S_SET1_K, S_SET1_I, S_SET2, S_SET2_K, S_SET2_I,
+    S_SET3, S_SET3_K, S_SET3_I, S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
+    S_OVF, S_SKTMP, S_COUNT
+};
+// pinned slots
+enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
+
+constexpr int kTile = 512;          // candidates per relsky item (RS_THREADS * RS_K)
+constexpr uint32_t kChunk = 8192;   // comparators per relsky item before bounding
+constexpr uint32_t kBlock = 512;    // local block-skyline size
+
+// misc device words
+enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_TESTS = 8 /* 4 x u64 */ };
+
+uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
+    uint64_t r = 1;
+    for (uint64_t i = 0; i < e; ++i) {
+        if (r > kMaxPartitions) return kMaxPartitions + 1;
+        r *= base;
+    }
+    return r;
+}
+
+uint64_t snap_slices(uint64_t target_p, uint64_t k) {  // partition.cpp:220-231
+    if (target_p < 1) throw Error(SKY_E_CONFIG, "target partition count must be >= 1");
+    if (k < 1) throw Error(SKY_E_CONFIG, "snap exponent must be >= 1");
+    uint64_t hi = 1;
+    while (checked_pow(hi, k) < target_p && checked_pow(hi, k) <= kMaxPartitions) ++hi;
+    if (hi == 1) return 1;
+    if (checked_pow(hi, k) < target_p) return hi;
+    const uint64_t lo = hi - 1;
+    const uint64_t above = checked_pow(hi, k) - target_p;
+    const uint64_t below = target_p - checked_pow(lo, k);
+    return above < below ? hi : lo;
+}
+
+// Rng::below + shuffle (rng.hpp:40-60) with std::mt19937_64, the engine the
+// reference pins; partition_of[perm[i]] = i mod p (partition.cpp:36-54).
+void random_partition_of(uint64_t n, uint64_t p, uint64_t seed, uint32_t* pid) {
+    std::vector<uint32_t> perm(n);
+    for (uint64_t i = 0; i < n; ++i) perm[i] = (uint32_t)i;
+    std::mt19937_64 eng(seed);
+    for (uint64_t i = n; i > 1; --i) {
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % i;
+        uint64_t x;
+        do {
+            x = eng();
+        } while (x >= limit);
+        std::swap(perm[i - 1], perm[x % i]);
+    }
+    for (uint64_t i = 0; i < n; ++i) pid[perm[i]] = (uint32_t)(i % p);
+}
+
+// hyperspherical_angles + angular_index (partition.cpp:118-148) on the host's
+// libm for boundary points.
+uint64_t angular_index_host(const float* x, uint32_t d, uint64_t m) {
+    std::vector<double> ang(d - 1);
+    double tail_sq = (double)x[d - 1] * (double)x[d - 1];
+    for (uint32_t i = d - 1; i-- > 0;) {
+        ang[i] = std::atan2(std::sqrt(tail_sq), (double)x[i]);
+        tail_sq += (double)x[i] * (double)x[i];
+    }
+    uint64_t index = 0, stride = 1;
+    for (double phi : ang) {
+        uint64_t slice = (uint64_t)(2.0 * phi / 3.14159265358979323846 * (double)m);
+        if (slice >= m) slice = m - 1;
+        index += slice * stride;
+        stride *= m;
+    }
+    return index;
+}
+
+struct Plan {
+    std::vector<Item> items;
+    std::vector<uint2> ranges;
+    std::vector<uint32_t> group;  // item wave (comparator chunk index)
+    std::vector<uint64_t> work;
+
+    // candidates [cb,ce) vs comparator ranges, split into groups of at most
+    // kChunk comparators; items of group g launch after those of group g-1.
+    void add(uint32_t cb, uint32_t ce, const std::vector<uint2>& comps, uint32_t chunk = kChunk) {
+        uint32_t g = 0, acc = 0;
+        uint32_t lb = (uint32_t)ranges.size();
+        auto flush = [&](bool force) {
+            if ((uint32_t)ranges.size() > lb || force) {
+                if ((uint32_t)ranges.size() > lb) {
+                    items.push_back(Item{cb, ce, lb, (uint32_t)ranges.size()});
+                    group.push_back(g);
+                    work.push_back((uint64_t)acc * (ce - cb));
+                    ++g;
+                }
+                lb = (uint32_t)ranges.size();
+                acc = 0;
+            }
+        };
+        for (uint2 r : comps) {
+            uint32_t b = r.x;
+            while (b < r.y) {
+                const uint32_t take = std::min(r.y - b, chunk - acc);
+                ranges.push_back(make_uint2(b, b + take));
+                b += take;
+                acc += take;
+                if (acc >= chunk) flush(false);
+            }
+        }
+        flush(false);
+    }
+
+    // Launch order: by wave, then by descending work inside a wave.
+    void order() {
+        std::vector<uint32_t> ix(items.size());
+        for (uint32_t i = 0; i < ix.size(); ++i) ix[i] = i;
+        std::stable_sort(ix.begin(), ix.end(), [&](uint32_t a, uint32_t b) {
+            if (group[a] != group[b]) return group[a] < group[b];
+            return work[a] > work[b];
+        });
+        std::vector<Item> it2(items.size());
+        for (uint32_t i = 0; i < ix.size(); ++i) it2[i] = items[ix[i]];
+        items.swap(it2);
+    }
+};
+
+class Runner {
+   public:
+    Runner(sky_ctx* c) : c_(c), st_(c->stream) {}
+
+    // --------------------------------------------------------------- utils
+    template <class T>
+    T* dev(int slot, size_t n) { return c_->dev.as<T>(slot, n ? n : 1); }
+    template <class T>
+    T* pin(int slot, size_t n) { return c_->pin.as<T>(slot, n ? n : 1); }
+    void sync() { SKY_CUDA(cudaStreamSynchronize(st_)); }
+    void count(int k = 1) { c_->launches += k; }
+
+    DevSet set(int base, uint32_t n, int D) {
+        DevSet s;
+        const int D4 = (D + 3) / 4 * 4;
+        s.xyz = dev<float>(base, (size_t)n * D4);
+        s.skey = dev<uint32_t>(base + 1, n);
+        s.id = dev<uint32_t>(base + 2, n);
+        s.n = n;
+        return s;
+    }
+
+    template <class K, class V>
+    void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint32_t n, int bb, int eb) {
+        if (!n) return;
+        size_t bytes = 0;
+        SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, bb, eb, st_));
+        void* tmp = c_->dev.get(S_CUB, bytes);
+        SKY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, bb, eb, st_));
+        count(4);
+    }
+    template <class K>
+    void sort_keys(const K* kin, K* kout, uint32_t n) {
+        if (!n) return;
+        size_t bytes = 0;
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kin, kout, (int)n, 0, (int)(8 * sizeof(K)), st_));
+        void* tmp = c_->dev.get(S_CUB, bytes);
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, kin, kout, (int)n, 0, (int)(8 * sizeof(K)), st_));
+        count(4);
+    }
+    struct NotDead {
+        __host__ __device__ uint32_t operator()(uint8_t x) const { return x ? 0u : 1u; }
+    };
+    // pos[i] = number of live entries before i
+    void scan_live(const uint8_t* dead, uint32_t* pos, uint32_t n) {
+        if (!n) return;
+        cub::TransformInputIterator<uint32_t, NotDead, const uint8_t*> it(dead, NotDead());
+        size_t bytes = 0;
+        SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, pos, (int)n, st_));
+        void* tmp = c_->dev.get(S_CUB, bytes);
+        SKY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, it, pos, (int)n, st_));
+        count(2);
+    }
+
+    // Keep the live rows of `in` (segments off_in[P+1]) into `out_base`;
+    // new offsets land in off_out (device) and off_host. Synchronizes.
+    DevSet compact(const DevSet& in, const uint8_t* dead, const uint32_t* off_in, uint32_t P, int out_base,
+                   uint32_t* off_out, std::vector<uint32_t>& off_host, int D) {
+        uint32_t* pos = dev<uint32_t>(S_POS, in.n);
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        scan_live(dead, pos, in.n);
+        launch_count_total(pos, dead, in.n, misc + M_TOTAL, st_);
+        count();
+        launch_remap_offsets(off_in, P, pos, dead, in.n, off_out, st_);
+        count();
+        uint32_t* h = pin<uint32_t>(P_OFF, P + 2);
+        SKY_CUDA(cudaMemcpyAsync(h, off_out, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        sync();
+        const uint32_t total = in.n ? h[P + 1] : 0;
+        off_host.assign(h, h + P + 1);
+        DevSet out = set(out_base, total, D);
+        launch_scatter_direct(D, in, dead, pos, out, st_);
+        count();
+        return out;
+    }
+
+    void relsky(int D, const Plan& plan, const RelskyArgs& base) {
+        if (plan.items.empty()) return;
+        Item* hi = pin<Item>(P_ITEMS, plan.items.size());
+        uint2* hr = pin<uint2>(P_RANGES, plan.ranges.size());
+        std::memcpy(hi, plan.items.data(), plan.items.size() * sizeof(Item));
+        std::memcpy(hr, plan.ranges.data(), plan.ranges.size() * sizeof(uint2));
+        Item* di = dev<Item>(S_ITEMS, plan.items.size());
+        uint2* dr = dev<uint2>(S_RANGES, plan.ranges.size());
+        SKY_CUDA(cudaMemcpyAsync(di, hi, plan.items.size() * sizeof(Item), cudaMemcpyHostToDevice, st_));
+        SKY_CUDA(cudaMemcpyAsync(dr, hr, plan.ranges.size() * sizeof(uint2), cudaMemcpyHostToDevice, st_));
+        RelskyArgs a = base;
+        a.items = di;
+        a.ranges = dr;
+        a.n_items = (uint32_t)plan.items.size();
+        launch_relsky(D, a, st_);
+        count();
+        // the pinned staging buffers are reused by the next call: make sure
+        // the copies have consumed them first
+        sync();
+    }
+
+    unsigned long long* tests(int k) {
+        return reinterpret_cast<unsigned long long*>(dev<uint32_t>(S_MISC, 64) + M_TESTS) + k;
+    }
+
+    // ------------------------------------------------------ local skylines
+    // SFS restated for the GPU: the partition is already in (sum key) order;
+    // (1) every block of kBlock rows keeps the rows no earlier-or-equal-key
+    // row of the block dominates; (2) each block survivor is tested against
+    // all block survivors of its partition with key <= its own. The result is
+    // exactly the partition's local skyline (sfs, sequential.cpp:48-60).
+    DevSet local_sfs(int D, const DevSet& s0, const std::vector<uint32_t>& off0, uint32_t* off0_dev, uint32_t P,
+                     uint32_t* off_u_dev, std::vector<uint32_t>& off_u, bool count_tests) {
+        uint8_t* dead = dev<uint8_t>(S_DEAD, s0.n);
+        launch_fill_u8(dead, 0, s0.n, st_);
+        Plan blocks;
+        for (uint32_t p = 0; p < P; ++p)
+            for (uint32_t b = off0[p]; b < off0[p + 1]; b += kBlock) {
+                const uint32_t e = std::min(b + kBlock, off0[p + 1]);
+                blocks.add(b, e, {make_uint2(b, e)});
+            }
+        RelskyArgs a{};
+        a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
+        a.sxyz = s0.xyz; a.sskey = s0.skey; a.bounded = true; a.dead = dead;
+        a.tests = count_tests ? tests(1) : nullptr;
+        relsky(D, blocks, a);
+        std::vector<uint32_t> off1;
+        uint32_t* off1_dev = dev<uint32_t>(S_OFF_B, P + 1);
+        DevSet s1 = compact(s0, dead, off0_dev, P, S_SET1, off1_dev, off1, D);
+
+        uint8_t* dead1 = dev<uint8_t>(S_DEAD, s1.n);
+        launch_fill_u8(dead1, 0, s1.n, st_);
+        Plan loc;
+        for (uint32_t p = 0; p < P; ++p) {
+            const uint32_t b0 = off1[p], e0 = off1[p + 1];
+            for (uint32_t b = b0; b < e0; b += kTile) {
+                const uint32_t e = std::min(b + (uint32_t)kTile, e0);
+                loc.add(b, e, {make_uint2(b0, e0)});
+            }
+        }
+        loc.order();
+        a.cxyz = s1.xyz; a.cskey = s1.skey; a.sxyz = s1.xyz; a.sskey = s1.skey; a.dead = dead1;
+        relsky(D, loc, a);
+        return compact(s1, dead1, off1_dev, P, S_SET2, off_u_dev, off_u, D);
+    }
+
+    // BNL local skylines (k_bnl), window capped at cfg.bnl_window_cap.
+    DevSet local_bnl(int D, const DevSet& s0, uint32_t* off0_dev, uint32_t P, uint32_t window, uint32_t* off_u_dev,
+                     std::vector<uint32_t>& off_u, bool count_tests, uint32_t* used_window) {
+        uint8_t* dead = dev<uint8_t>(S_DEAD, s0.n);
+        launch_fill_u8(dead, 1, s0.n, st_);
+        const uint32_t cap = bnl_window_fit(D, window ? window : 4096, c_->smem_optin);
+        *used_window = cap;
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(P, (uint32_t)c_->sm_count));
+        uint32_t* wpos = dev<uint32_t>(S_BNL_POS, (size_t)grid * cap);
+        uint32_t* wmeta = dev<uint32_t>(S_BNL_META, (size_t)grid * cap);
+        uint32_t* ovf = dev<uint32_t>(S_OVF, s0.n);
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        SKY_CUDA(cudaMemsetAsync(misc + M_BNLCTR, 0, sizeof(uint32_t), st_));
+        BnlArgs b{};
+        b.xyz = s0.xyz;
+        b.seg_off = off0_dev;
+        b.P = P;
+        b.window = cap;
+        b.dead = dead;
+        b.overflow = ovf;
+        b.tests = count_tests ? tests(1) : nullptr;
+        if (s0.n) {
+            launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
+            count();
+        }
+        return compact(s0, dead, off0_dev, P, S_SET2, off_u_dev, off_u, D);
+    }
+
+   public:
+    sky_ctx* c_;
+    cudaStream_t st_;
+};
+
+void validate(uint64_t n, uint32_t d, const sky_config* c) {  // engine.cpp:19-32
+    if (c->workers < 1) throw Error(SKY_E_CONFIG, "worker count must be >= 1");
+    if (c->p < 1) throw Error(SKY_E_CONFIG, "partition count must be >= 1");
+    if (c->filter == SKY_FILTER_GRID && c->strategy != SKY_GRID)
+        throw Error(SKY_E_CONFIG, "grid filtering requires the grid partitioning strategy");
+    if (c->filter == SKY_FILTER_REPRESENTATIVE && c->rep_q < 1)
+        throw Error(SKY_E_CONFIG, "representative count q must be >= 1");
+    if (c->strategy == SKY_ANGULAR && n > 0 && d < 2) throw Error(SKY_E_DIMENSION, "angular partitioning needs d >= 2");
+    if (c->strategy < 0 || c->strategy > 3) throw Error(SKY_E_CONFIG, "unknown partitioning strategy");
+    if (c->filter < 0 || c->filter > 2) throw Error(SKY_E_CONFIG, "unknown filter kind");
+    if (c->merge < 0 || c->merge > 1) throw Error(SKY_E_CONFIG, "unknown merge kind");
+    if (c->local_algo < 0 || c->local_algo > 1) throw Error(SKY_E_CONFIG, "unknown local algorithm");
+    if (c->filter == SKY_FILTER_REPRESENTATIVE && c->rep_selection != SKY_REPS_SORTED)
+        throw Error(SKY_E_CONFIG, "only sorted representative selection is implemented on the GPU path");
+}
+
+// Effective partition count and slices (make_assignment, partition.cpp:233-251).
+void resolve_partitions(uint64_t n, uint32_t d, const sky_config* c, uint64_t* P, uint64_t* m) {
+    *m = 0;
+    switch (c->strategy) {
+        case SKY_RANDOM:
+            *P = c->p;
+            break;
+        case SKY_GRID: {
+            *m = c->m > 0 ? c->m : snap_slices(c->p, d);
+            if (*m < 1) throw Error(SKY_E_CONFIG, "slices per dimension must be >= 1");
+            if (d < 1) throw Error(SKY_E_DIMENSION, "grid partitioning needs d >= 1");
+            *P = checked_pow(*m, d);
+            if (*P > kMaxPartitions) throw Error(SKY_E_CONFIG, "grid partition count m^d exceeds the supported maximum");
+            break;
+        }
+        case SKY_ANGULAR: {
+            if (d < 2) throw Error(SKY_E_DIMENSION, "angular partitioning needs d >= 2");
+            *m = c->m > 0 ? c->m : snap_slices(c->p, d - 1);
+            if (*m < 1) throw Error(SKY_E_CONFIG, "slices per dimension must be >= 1");
+            *P = checked_pow(*m, d - 1);
+            if (*P > kMaxPartitions)
+                throw Error(SKY_E_CONFIG, "angular partition count m^(d-1) exceeds the supported maximum");
+            break;
+        }
+        case SKY_SLICED:
+            if (n > 0 && c->slice_dim >= d) throw Error(SKY_E_CONFIG, "slice dimension out of range");
+            *P = c->p;
+            break;
+        default:
+            throw Error(SKY_E_CONFIG, "unknown partitioning strategy");
+    }
+    if (*P > 0xFFFFFFF0ull) throw Error(SKY_E_CONFIG, "partition count too large");
+}
+
+// weak_grid_dominates over decoded cells (partition.cpp:87-116)
+bool weak_grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d) {
+    bool equal = true;
+    for (uint32_t j = 0; j < d; ++j) {
+        const uint64_t ca = a % m, cb = b % m;
+        if (ca > cb) return false;
+        if (ca != cb) equal = false;
+        a /= m;
+        b /= m;
+    }
+    return !equal;
+}
+bool grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d) {
+    for (uint32_t j = 0; j < d; ++j) {
+        if (a % m >= b % m) return false;
+        a /= m;
+        b /= m;
+    }
+    return true;
+}
+
+struct PartitionOut {
+    uint64_t* key64;   // sorted (pid << 32 | skey)
+    uint32_t* idx;     // row of each sorted position
+    uint32_t* off;     // device offsets [P+1]
+};
+
+// Phase 1a: partition ids, sum keys, validation, sort into partitions.
+PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d, int normalized, int strategy,
+                             uint64_t P, uint64_t m, const sky_config* cfg, std::thread* host_perm,
+                             uint32_t* host_pid, uint64_t* fixups) {
+    cudaStream_t st = R.st_;
+    uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, n);
+    uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, n);
+    uint32_t* idxA = R.dev<uint32_t>(S_IDX_A, n);
+    uint32_t* idxB = R.dev<uint32_t>(S_IDX_B, n);
+    uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
+    uint32_t* pid_in = nullptr;
+    if (strategy == SKY_RANDOM) {
+        if (host_perm) host_perm->join();
+        pid_in = R.dev<uint32_t>(S_PID, n);
+        SKY_CUDA(cudaMemcpyAsync(pid_in, host_pid, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    }
+    const uint32_t amb_cap = 1u << 16;
+    uint32_t* amb = R.dev<uint32_t>(S_AMB, amb_cap);
+    uint32_t* skA = nullptr;
+    if (strategy == SKY_SLICED) skA = R.dev<uint32_t>(S_SK_A, n);
+    PrepArgs pa{pts, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA, idxA, skA,
+                misc + M_ERR, misc + M_AMB, amb, amb_cap};
+    launch_prep(pa, st);
+    R.count();
+
+    // errors + angular boundary points (one host round trip)
+    uint32_t* hm = R.pin<uint32_t>(P_MISC, 8);
+    SKY_CUDA(cudaMemcpyAsync(hm, misc, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    R.sync();
+    const uint32_t err = hm[M_ERR];
+    if (err & kErrNonFinite) throw Error(SKY_E_DATA, "coordinate must be finite and >= 0");
+    if (err & kErrAboveOne) throw Error(SKY_E_DATA, "normalized dataset has coordinate > 1");
+    if (err & kErrGridRange) throw Error(SKY_E_NORMALIZATION, "grid index needs coordinates in [0,1]");
+    if (strategy == SKY_ANGULAR && hm[M_AMB]) {
+        const uint32_t na = hm[M_AMB];
+        if (na > amb_cap) throw Error(SKY_E_INTERNAL, "too many angular boundary points");
+        uint32_t* ha = R.pin<uint32_t>(P_AMB, 3 * (size_t)na + 1);
+        SKY_CUDA(cudaMemcpyAsync(ha, amb, na * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        // fetch the rows and recompute with the host libm
+        std::vector<float> row(d);
+        uint32_t* hp = ha + na;
+        float* hrows = reinterpret_cast<float*>(ha + 2 * (size_t)na);
+        (void)hrows;
+        for (uint32_t k = 0; k < na; ++k) {
+            SKY_CUDA(cudaMemcpy(row.data(), pts + (size_t)ha[k] * d, d * sizeof(float), cudaMemcpyDeviceToHost));
+            hp[k] = (uint32_t)angular_index_host(row.data(), d, m);
+        }
+        uint32_t* dp = amb + na;  // reuse tail of the amb buffer for pids (cap >= 2*na checked below)
+        if (2 * (size_t)na > amb_cap) dp = R.dev<uint32_t>(S_RUNS, na);
+        SKY_CUDA(cudaMemcpyAsync(dp, hp, na * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        launch_patch_pid(keyA, amb, dp, na, st);
+        R.count();
+        *fixups = na;
+    }
+
+    if (strategy == SKY_SLICED && n > 0) {
+        // rank order by (x[k], row): radix sort of the canonical float bits
+        uint32_t* skB = R.dev<uint32_t>(S_SK_B, n);
+        uint32_t* rankA = R.dev<uint32_t>(S_PERM_A, n);
+        uint32_t* rankB = R.dev<uint32_t>(S_PERM_B, n);
+        R.sort_pairs(skA, skB, idxA, rankA, n, 0, 32);
+        // tie runs straddling slice boundaries need the (lex, id) order
+        const uint32_t run_cap = (uint32_t)std::min<uint64_t>(P, 1u << 20);
+        uint32_t* runs = R.dev<uint32_t>(S_RUNS, 2 * (size_t)run_cap);
+        SKY_CUDA(cudaMemsetAsync(misc + M_RUNS, 0, sizeof(uint32_t), st));
+        launch_slice_runs(skB, n, P, runs, misc + M_RUNS, run_cap, st);
+        R.count();
+        SKY_CUDA(cudaMemcpyAsync(hm, misc + M_RUNS, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        const uint32_t nruns = std::min(hm[0], run_cap);
+        uint64_t cost = 0;
+        uint32_t max_len = 0;
+        std::vector<uint32_t> hr;
+        if (nruns) {
+            uint32_t* h = R.pin<uint32_t>(P_RUNS, 2 * (size_t)nruns);
+            SKY_CUDA(cudaMemcpyAsync(h, runs, 2 * (size_t)nruns * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            R.sync();
+            for (uint32_t k = 0; k < nruns; ++k) {
+                const uint64_t L = h[2 * k + 1] - h[2 * k];
+                cost += L * L;
+                max_len = std::max<uint32_t>(max_len, (uint32_t)L);
+            }
+        }
+        if (cost <= (uint64_t)1e9) {
+            launch_slice_assign(rankA, n, P, keyA, st);
+            R.count();
+            launch_slice_fix_runs(pts, d, rankA, n, P, runs, nruns, max_len, keyA, st);
+            if (nruns) R.count();
+        } else {
+            // full (x[k], x[0..d-1], row) order by LSD passes over the rows
+            uint32_t* cur = rankB;
+            uint32_t* other = rankA;
+            SKY_CUDA(cudaMemcpyAsync(cur, idxA, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+            for (int j = (int)d - 1; j >= -1; --j) {
+                const uint32_t col = j < 0 ? (uint32_t)cfg->slice_dim : (uint32_t)j;
+                launch_gather_coord_key(pts, d, col, cur, n, skA, st);
+                R.count();
+                R.sort_pairs(skA, skB, cur, other, n, 0, 32);
+                std::swap(cur, other);
+            }
+            launch_slice_assign(cur, n, P, keyA, st);
+            R.count();
+        }
+    }
+
+    // one radix sort by (pid, sum key); stable, so ties keep row order
+    const int end_bit = 32 + std::max(1, bits_for(P));
+    R.sort_pairs(keyA, keyB, idxA, idxB, n, 0, std::min(64, end_bit));
+    uint32_t* off = R.dev<uint32_t>(S_OFF_A, P + 1);
+    launch_seg_offsets(keyB, n, (uint32_t)P, off, st);
+    R.count();
+    return PartitionOut{keyB, idxB, off};
+}
+
+void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int normalized, int on_device,
+              const sky_config* cfg, sky_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    validate(n64, d, cfg);
+    uint64_t P64 = 0, m = 0;
+    resolve_partitions(n64, d, cfg, &P64, &m);
+    if (n64 >= 0xFFFFFFF0ull) throw Error(SKY_E_DATA, "at most 2^32-16 points per run");
+    const uint32_t n = (uint32_t)n64;
+    const uint32_t P = (uint32_t)P64;
+    out->effective_p = P;
+    out->input_size = n;
+    out->input_dim = d;
+    out->local_skyline_sizes = static_cast<uint64_t*>(std::calloc(P ? P : 1, sizeof(uint64_t)));
+    c->launches = 0;
+    const bool count_tests = cfg->count_tests != 0;
+
+    if (n == 0 || d == 0) {
+        // d == 0: no coordinate can be strictly better, nothing is dominated
+        // (dominates_raw core.hpp:89-96); every row is its own local skyline.
+        out->ids = static_cast<int64_t*>(std::malloc((n ? n : 1) * sizeof(int64_t)));
+        for (uint32_t i = 0; i < n; ++i) out->ids[i] = i;
+        out->n_ids = out->final_size = out->union_size = n;
+        if (n && cfg->strategy == SKY_RANDOM) {
+            std::vector<uint32_t> pid(n);
+            random_partition_of(n, P, cfg->seed, pid.data());
+            for (uint32_t i = 0; i < n; ++i) out->local_skyline_sizes[pid[i]]++;
+        } else if (n) {
+            out->local_skyline_sizes[0] = n;
+        }
+        return;
+    }
+    const int D = padded_dim(d);
+    if (!D) throw Error(SKY_E_DIMENSION, "the GPU engine supports d <= 32");
+
+    Runner R(c);
+    cudaStream_t st = c->stream;
+
+    // random partitioning: the permutation is seeded host work; overlap it
+    // with the upload and the prep pass of the other fields
+    uint32_t* host_pid = nullptr;
+    std::thread perm_thread;
+    if (cfg->strategy == SKY_RANDOM) {
+        host_pid = R.pin<uint32_t>(P_PID, n);
+        perm_thread = std::thread(random_partition_of, (uint64_t)n, (uint64_t)P, cfg->seed, host_pid);
+    }
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() { if (t.joinable()) t.join(); }
+    } joiner{perm_thread};
+
+    SKY_CUDA(cudaEventRecord(c->ev[0], st));
+    uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
+    SKY_CUDA(cudaMemsetAsync(misc, 0, 64 * sizeof(uint32_t), st));
+    const float* pts = points;
+    if (!on_device) {
+        float* dp = R.dev<float>(S_PTS, (size_t)n * d);
+        SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, st));
+        pts = dp;
+        out->h2d_bytes += (uint64_t)n * d * sizeof(float);
+    }
+    if (cfg->strategy == SKY_RANDOM) out->h2d_bytes += (uint64_t)n * sizeof(uint32_t);
+
+    PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg,
+                                      cfg->strategy == SKY_RANDOM ? &perm_thread : nullptr, host_pid,
+                                      &out->angular_host_fixups);
+
+    std::vector<uint32_t> off0(P + 1);
+    uint8_t* dead = R.dev<uint8_t>(S_DEAD, n);
+    uint64_t grid_filtered = 0;
+    bool any_dead = false;
+    if (cfg->filter == SKY_FILTER_GRID) {
+        // grid_filter over non-empty cells (filter.cpp:37-50, engine.cpp:150-163)
+        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 2);
+        SKY_CUDA(cudaMemcpyAsync(h, po.off, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        std::vector<uint32_t> nonempty;
+        for (uint32_t p = 0; p < P; ++p)
+            if (h[p + 1] > h[p]) nonempty.push_back(p);
+        uint8_t* cd = R.pin<uint8_t>(P_PCOUNT, P);
+        std::memset(cd, 0, P);
+        for (uint32_t a : nonempty)
+            for (uint32_t b : nonempty)
+                if (grid_dom(b, a, m, d)) {
+                    cd[a] = 1;
+                    grid_filtered += h[a + 1] - h[a];
+                    break;
+                }
+        uint8_t* cdd = R.dev<uint8_t>(S_CELLDEAD, P);
+        SKY_CUDA(cudaMemcpyAsync(cdd, cd, P, cudaMemcpyHostToDevice, st));
+        launch_mark_cells_dead(po.key64, n, cdd, dead, st);
+        R.count();
+        any_dead = grid_filtered > 0;
+        R.sync();
+    } else {
+        launch_fill_u8(dead, 0, n, st);
+    }
+    SKY_CUDA(cudaEventRecord(c->ev[1], st));
+
+    // ---------------------------------------------- representatives + filter
+    uint64_t rep_filtered = 0;
+    if (cfg->filter == SKY_FILTER_REPRESENTATIVE) {
+        const uint32_t q = (uint32_t)std::min<uint64_t>(cfg->rep_q, n);
+        uint32_t* cand = R.dev<uint32_t>(S_REPCAND, (size_t)P * q);
+        // filtered (grid) partitions are empty for the reps; here only the
+        // representative filter is active, so every partition participates
+        launch_rep_pick(po.key64, po.idx, po.off, P, pts, d, q, cand, st);
+        R.count();
+        // compact the candidate rows on the host side (P*q is small)
+        uint32_t* hc = R.pin<uint32_t>(P_IDS, (size_t)P * q);
+        SKY_CUDA(cudaMemcpyAsync(hc, cand, (size_t)P * q * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        std::vector<uint32_t> rows;
+        rows.reserve((size_t)P * q);
+        for (size_t k = 0; k < (size_t)P * q; ++k)
+            if (hc[k] != kNone) rows.push_back(hc[k]);
+        const uint32_t nc = (uint32_t)rows.size();
+        uint32_t* drows = R.dev<uint32_t>(S_REPROWS, nc);
+        std::memcpy(hc, rows.data(), nc * sizeof(uint32_t));
+        SKY_CUDA(cudaMemcpyAsync(drows, hc, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        DevSet cs = R.set(S_SET3, nc, D);
+        launch_gather_rows(D, pts, d, drows, nc, cs, nullptr, st);
+        R.count();
+        // sort candidates by sum key, prune to an antichain (prune_dominated_reps)
+        DevSet css = R.set(S_SET1, nc, D);
+        {
+            uint32_t* iota = R.dev<uint32_t>(S_PERM_A, nc);
+            uint32_t* perm = R.dev<uint32_t>(S_PERM_B, nc);
+            std::vector<uint32_t> io(nc);
+            for (uint32_t k = 0; k < nc; ++k) io[k] = k;
+            uint32_t* hio = R.pin<uint32_t>(P_RUNS, nc);
+            std::memcpy(hio, io.data(), nc * sizeof(uint32_t));
+            SKY_CUDA(cudaMemcpyAsync(iota, hio, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            uint32_t* sk2 = R.dev<uint32_t>(S_SKTMP, nc);
+            R.sort_pairs(cs.skey, sk2, iota, perm, nc, 0, 32);
+            launch_gather_set(D, cs, perm, css, st);
+            R.count();
+        }
+        uint8_t* cdead = R.dev<uint8_t>(S_CELLDEAD, nc);
+        launch_fill_u8(cdead, 0, nc, st);
+        Plan pp;
+        for (uint32_t b = 0; b < nc; b += kTile) pp.add(b, std::min(nc, b + (uint32_t)kTile), {make_uint2(0, nc)});
+        RelskyArgs ra{};
+        ra.cxyz = css.xyz; ra.cskey = css.skey; ra.sxyz = css.xyz; ra.sskey = css.skey;
+        ra.bounded = true; ra.dead = cdead; ra.tests = count_tests ? R.tests(0) : nullptr;
+        R.relsky(D, pp, ra);
+        std::vector<uint32_t> roff;
+        uint32_t zero_off[2] = {0, nc};
+        uint32_t* doff = R.dev<uint32_t>(S_OFF_B, 2);
+        uint32_t* hz = R.pin<uint32_t>(P_MISC, 8);
+        hz[4] = zero_off[0];
+        hz[5] = zero_off[1];
+        SKY_CUDA(cudaMemcpyAsync(doff, hz + 4, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        uint32_t* doff2 = R.dev<uint32_t>(S_OFF_B, 4) + 2;
+        DevSet reps = R.compact(css, cdead, doff, 1, S_SET3, doff2, roff, D);
+        out->n_reps = reps.n;
+
+        // rep_prefilter over every row, in partition/sum order (indirect)
+        if (reps.n > 0) {
+            Plan pf;
+            for (uint32_t b = 0; b < n; b += kTile) pf.add(b, std::min(n, b + (uint32_t)kTile), {make_uint2(0, reps.n)});
+            RelskyArgs fa{};
+            fa.cxyz = pts; fa.cskey = reinterpret_cast<const uint32_t*>(po.key64); fa.cidx = po.idx; fa.cd = d;
+            fa.indirect = true; fa.sxyz = reps.xyz; fa.sskey = reps.skey; fa.bounded = true; fa.dead = dead;
+            fa.tests = count_tests ? R.tests(1) : nullptr;
+            R.relsky(D, pf, fa);
+            any_dead = true;
+        }
+    }
+
+    // materialize the surviving rows in (pid, sum key) order
+    std::vector<uint32_t> off1;
+    uint32_t* off1_dev = R.dev<uint32_t>(S_OFF_B, P + 1);
+    DevSet s0;
+    {
+        uint32_t* pos = R.dev<uint32_t>(S_POS, n);
+        R.scan_live(dead, pos, n);
+        launch_count_total(pos, dead, n, misc + M_TOTAL, st);
+        launch_remap_offsets(po.off, P, pos, dead, n, off1_dev, st);
+        R.count(2);
+        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 2);
+        SKY_CUDA(cudaMemcpyAsync(h, off1_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        off1.assign(h, h + P + 1);
+        const uint32_t total = h[P + 1];
+        s0 = R.set(S_SET0, total, D);
+        launch_scatter_indirect(D, pts, d, po.idx, po.key64, n, any_dead ? dead : nullptr, any_dead ? pos : nullptr,
+                                s0, st);
+        R.count();
+        rep_filtered = (uint64_t)n - total - grid_filtered;
+    }
+    out->filtered_count = grid_filtered + rep_filtered;
+
+    // ----------------------------------------------------- local skylines
+    std::vector<uint32_t> offu;
+    uint32_t* offu_dev = R.dev<uint32_t>(S_OFF_A, P + 1);  // partition offsets no longer needed
+    DevSet U;
+    if (cfg->local_algo == SKY_LOCAL_BNL) {
+        uint32_t used = 0;
+        U = R.local_bnl(D, s0, off1_dev, P, cfg->bnl_window_cap, offu_dev, offu, count_tests, &used);
+    } else {
+        U = R.local_sfs(D, s0, off1, off1_dev, P, offu_dev, offu, count_tests);
+    }
+    SKY_CUDA(cudaEventRecord(c->ev[2], st));
+    for (uint32_t p = 0; p < P; ++p) out->local_skyline_sizes[p] = offu[p + 1] - offu[p];
+    out->union_size = U.n;
+
+    // ---------------------------------------------------------------- merge
+    uint8_t* fdead = R.dev<uint8_t>(S_CELLDEAD, U.n);
+    launch_fill_u8(fdead, 0, U.n, st);
+    RelskyArgs ma{};
+    ma.cxyz = U.xyz; ma.cskey = U.skey; ma.bounded = true; ma.dead = fdead;
+    ma.tests = count_tests ? R.tests(2) : nullptr;
+    Plan mp;
+    const bool all_mode = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
+                          cfg->strategy == SKY_ANGULAR;
+    DevSet US;
+    if (all_mode && P > 1) {
+        // Sky(U) against the whole union sorted by sum key: for random and
+        // angular pd_i is every other local (engine.cpp:98-103) and u_i is an
+        // antichain, so testing against all of U is the same relation;
+        // merge_sequential (engine.cpp:65-72) is Sky(U) by definition.
+        US = R.set(S_SET3, U.n, D);
+        uint32_t* iota = R.dev<uint32_t>(S_PERM_A, U.n);
+        uint32_t* perm = R.dev<uint32_t>(S_PERM_B, U.n);
+        uint32_t* sk2 = R.dev<uint32_t>(S_SKTMP, U.n);
+        {
+            // iota on device via the id array trick: pos = exclusive scan of
+            // all-live flags
+            uint8_t* z = R.dev<uint8_t>(S_DEAD, U.n);
+            launch_fill_u8(z, 0, U.n, st);
+            R.scan_live(z, iota, U.n);
+        }
+        R.sort_pairs(U.skey, sk2, iota, perm, U.n, 0, 32);
+        launch_gather_set(D, U, perm, US, st);
+        R.count();
+        for (uint32_t p = 0; p < P; ++p)
+            for (uint32_t b = offu[p]; b < offu[p + 1]; b += kTile)
+                mp.add(b, std::min(offu[p + 1], b + (uint32_t)kTile), {make_uint2(0, U.n)});
+        ma.sxyz = US.xyz; ma.sskey = US.skey;
+    } else if (P > 1) {
+        ma.sxyz = U.xyz; ma.sskey = U.skey;
+        std::vector<uint32_t> nonempty;
+        for (uint32_t p = 0; p < P; ++p)
+            if (offu[p + 1] > offu[p]) nonempty.push_back(p);
+        std::vector<uint2> comps;
+        for (uint32_t i : nonempty) {
+            comps.clear();
+            if (cfg->strategy == SKY_SLICED) {  // pd_i = u_j, j < i (engine.cpp:106-108)
+                if (offu[i] > 0) comps.push_back(make_uint2(0, offu[i]));
+                // split per slice so each range stays sum-sorted
+                comps.clear();
+                for (uint32_t j : nonempty) {
+                    if (j >= i) break;
+                    comps.push_back(make_uint2(offu[j], offu[j + 1]));
+                }
+            } else {  // grid: weakly dominating non-empty cells (engine.cpp:92-104)
+                for (uint32_t j : nonempty)
+                    if (j != i && weak_grid_dom(j, i, m, d)) comps.push_back(make_uint2(offu[j], offu[j + 1]));
+            }
+            if (comps.empty()) continue;
+            for (uint32_t b = offu[i]; b < offu[i + 1]; b += kTile)
+                mp.add(b, std::min(offu[i + 1], b + (uint32_t)kTile), comps);
+        }
+    }
+    mp.order();
+    R.relsky(D, mp, ma);
+
+    // surviving ids, ascending (engine.cpp:128-133)
+    uint32_t* pos = R.dev<uint32_t>(S_POS, U.n);
+    R.scan_live(fdead, pos, U.n);
+    launch_count_total(pos, fdead, U.n, misc + M_TOTAL, st);
+    R.count();
+    uint32_t* hm = R.pin<uint32_t>(P_MISC, 16);
+    SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    R.sync();
+    const uint32_t nf = U.n ? hm[0] : 0;
+    uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, nf);
+    uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, nf);
+    launch_compact_ids(U.id, fdead, pos, U.n, idsA, st);
+    R.count();
+    R.sort_keys(idsA, idsB, nf);
+    SKY_CUDA(cudaEventRecord(c->ev[3], st));
+    uint32_t* hid = R.pin<uint32_t>(P_IDS, nf);
+    SKY_CUDA(cudaMemcpyAsync(hid, idsB, (size_t)nf * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    unsigned long long* ht = reinterpret_cast<unsigned long long*>(hm + 4);
+    SKY_CUDA(cudaMemcpyAsync(ht, R.tests(0), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SKY_CUDA(cudaEventRecord(c->ev[4], st));
+    R.sync();
+    out->d2h_bytes += (uint64_t)nf * sizeof(uint32_t);
+    out->ids = static_cast<int64_t*>(std::malloc((nf ? nf : 1) * sizeof(int64_t)));
+    for (uint32_t i = 0; i < nf; ++i) out->ids[i] = hid[i];
+    out->n_ids = out->final_size = nf;
+    out->tests_reps = ht[0];
+    out->tests_local = ht[1];
+    out->tests_merge = ht[2];
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    out->partition_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+    out->local_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    out->merge_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
+    out->total_ms = ms;
+    out->kernel_launches = c->launches;
+}
+
+template <class F>
+int guarded(sky_ctx* c, F&& f) {
+    try {
+        if (c) SKY_CUDA(cudaSetDevice(c->device));
+        f();
+        if (c) c->err.clear();
+        return SKY_OK;
+    } catch (const Error& e) {
+        if (c) c->err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        if (c) c->err = "host out of memory";
+        return SKY_E_INTERNAL;
+    } catch (const std::exception& e) {
+        if (c) c->err = e.what();
+        return SKY_E_INTERNAL;
+    }
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int sky_abi_version(void) { return SKY_ABI_VERSION; }
+
+void sky_config_default(sky_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->strategy = SKY_RANDOM;
+    cfg->p = 1;
+    cfg->rep_q = 5;  // engine.hpp:34
+    cfg->merge = SKY_MERGE_SEQUENTIAL;
+    cfg->workers = 1;
+    cfg->local_algo = SKY_LOCAL_SFS;
+    cfg->bnl_window_cap = 4096;
+    cfg->count_tests = 1;
+}
+
+int sky_ctx_create(int device, sky_ctx** out) {
+    *out = nullptr;
+    sky_ctx* c = new sky_ctx();
+    c->device = device;
+    int rc = guarded(c, [&] {
+        SKY_CUDA(cudaSetDevice(device));
+        SKY_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        c->stream = c->own;
+        SKY_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        SKY_CUDA(cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        for (auto& e : c->ev) SKY_CUDA(cudaEventCreate(&e));
+    });
+    if (rc != SKY_OK) {
+        static thread_local std::string last;
+        last = c->err;
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return SKY_OK;
+}
+
+void sky_ctx_destroy(sky_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    c->dev.release();
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+}
+
+const char* sky_last_error(const sky_ctx* c) { return c ? c->err.c_str() : "no context"; }
+
+int sky_ctx_set_stream(sky_ctx* c, void* stream) {
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+    return SKY_OK;
+}
+
+int sky_run(sky_ctx* c, const float* points, uint64_t n, uint32_t d, int normalized, int on_device,
+            const sky_config* cfg, sky_result* out) {
+    return guarded(c, [&] {
+        try {
+            run_impl(c, points, n, d, normalized, on_device, cfg, out);
+        } catch (...) {
+            sky_result_free(out);
+            throw;
+        }
+    });
+}
+
+void sky_result_free(sky_result* r) {
+    if (!r) return;
+    std::free(r->ids);
+    std::free(r->local_skyline_sizes);
+    r->ids = nullptr;
+    r->local_skyline_sizes = nullptr;
+}
+
+int sky_snap_slices(uint64_t target_p, uint64_t k, uint64_t* out_m) {
+    return guarded(nullptr, [&] { *out_m = snap_slices(target_p, k); });
+}
+
+int sky_assign(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int normalized, const sky_config* cfg,
+               uint64_t* partition_of, uint64_t* effective_p) {
+    return guarded(c, [&] {
+        if (cfg->p < 1) throw Error(SKY_E_CONFIG, "partition count must be >= 1");
+        uint64_t P64, m;
+        resolve_partitions(n64, d, cfg, &P64, &m);
+        *effective_p = P64;
+        if (n64 == 0) return;
+        if (d == 0) throw Error(SKY_E_DIMENSION, "assignment needs d >= 1");
+        const uint32_t n = (uint32_t)n64;
+        Runner R(c);
+        float* dp = R.dev<float>(S_PTS, (size_t)n * d);
+        SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        uint32_t* host_pid = nullptr;
+        if (cfg->strategy == SKY_RANDOM) {
+            host_pid = R.pin<uint32_t>(P_PID, n);
+            random_partition_of(n, P64, cfg->seed, host_pid);
+        }
+        uint64_t fix = 0;
+        PartitionOut po = partition_phase(R, dp, n, d, normalized, cfg->strategy, P64, m, cfg, nullptr, host_pid, &fix);
+        std::vector<uint64_t> key(n);
+        std::vector<uint32_t> idx(n);
+        SKY_CUDA(cudaMemcpyAsync(key.data(), po.key64, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        SKY_CUDA(cudaMemcpyAsync(idx.data(), po.idx, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        R.sync();
+        for (uint32_t i = 0; i < n; ++i) partition_of[idx[i]] = key[i] >> 32;
+    });
+}
+
+int sky_relative_skyline(sky_ctx* c, const float* r, uint64_t nr64, const float* cp, uint64_t nc64, uint32_t d,
+                         uint8_t* keep, uint64_t* tests_out) {
+    return guarded(c, [&] {
+        const uint32_t nr = (uint32_t)nr64, nc = (uint32_t)nc64;
+        if (tests_out) *tests_out = 0;
+        std::memset(keep, 1, nr);
+        if (nr == 0 || nc == 0 || d == 0) return;  // relative_skyline (core.cpp:81-84)
+        const int D = padded_dim(d);
+        if (!D) throw Error(SKY_E_DIMENSION, "the GPU engine supports d <= 32");
+        Runner R(c);
+        cudaStream_t st = c->stream;
+        // rows of r then c in one upload
+        float* dp = R.dev<float>(S_PTS, (size_t)(nr + nc) * d);
+        SKY_CUDA(cudaMemcpyAsync(dp, r, (size_t)nr * d * sizeof(float), cudaMemcpyHostToDevice, st));
+        SKY_CUDA(cudaMemcpyAsync(dp + (size_t)nr * d, cp, (size_t)nc * d * sizeof(float), cudaMemcpyHostToDevice, st));
+        uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
+        SKY_CUDA(cudaMemsetAsync(misc, 0, 64 * sizeof(uint32_t), st));
+        uint64_t* key = R.dev<uint64_t>(S_KEY_A, nr + nc);
+        uint32_t* idx = R.dev<uint32_t>(S_IDX_A, nr + nc);
+        PrepArgs pa{dp, nr + nc, d, SKY_SLICED + 100, 0, 0, nullptr, 0, key, idx, nullptr, misc + M_ERR,
+                    misc + M_AMB, nullptr, 0};
+        launch_prep(pa, st);
+        // comparators sorted by sum key
+        uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, nc);
+        uint32_t* idxB = R.dev<uint32_t>(S_IDX_B, nc);
+        R.sort_pairs(key + nr, keyB, idx + nr, idxB, nc, 0, 32);
+        DevSet S = R.set(S_SET1, nc, D);
+        launch_scatter_indirect(D, dp, d, idxB, keyB, nc, nullptr, nullptr, S, st);
+        DevSet T = R.set(S_SET0, nr, D);
+        launch_scatter_indirect(D, dp, d, idx, key, nr, nullptr, nullptr, T, st);
+        uint8_t* dead = R.dev<uint8_t>(S_DEAD, nr);
+        launch_fill_u8(dead, 0, nr, st);
+        Plan pl;
+        for (uint32_t b = 0; b < nr; b += kTile) pl.add(b, std::min(nr, b + (uint32_t)kTile), {make_uint2(0, nc)});
+        pl.order();
+        RelskyArgs a{};
+        a.cxyz = T.xyz; a.cskey = T.skey; a.sxyz = S.xyz; a.sskey = S.skey; a.bounded = false; a.dead = dead;
+        a.tests = R.tests(0);
+        // per-candidate bounds need sorted candidates; without sorting use the
+        // exact tile maximum (bounded=true is still sound on any order)
+        a.bounded = true;
+        R.relsky(D, pl, a);
+        std::vector<uint8_t> h(nr);
+        unsigned long long t = 0;
+        SKY_CUDA(cudaMemcpyAsync(h.data(), dead, nr, cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(&t, R.tests(0), sizeof(t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        for (uint32_t i = 0; i < nr; ++i) keep[i] = h[i] ? 0 : 1;
+        if (tests_out) *tests_out = t;
+    });
+}
+
+int sky_skyline(sky_ctx* c, const float* points, uint64_t n, uint32_t d, int64_t** out_ids, uint64_t* n_out,
+                uint64_t* tests_out) {
+    return guarded(c, [&] {
+        // one partition: Sky(r) is the local skyline of the only partition
+        sky_config cfg;
+        sky_config_default(&cfg);
+        cfg.strategy = SKY_SLICED;
+        cfg.p = 1;
+        sky_result r;
+        run_impl(c, points, n, d, 0, 0, &cfg, &r);
+        *out_ids = r.ids;
+        *n_out = r.n_ids;
+        if (tests_out) *tests_out = r.tests_local + r.tests_merge;
+        r.ids = nullptr;
+        sky_result_free(&r);
+    });
+}
+
+int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, const uint64_t* partition_of,
+                        uint64_t p, uint64_t q, int64_t** out_ids, uint64_t* n_out) {
+    return guarded(c, [&] {
+        *out_ids = nullptr;
+        *n_out = 0;
+        if (q < 1) throw Error(SKY_E_CONFIG, "representative count q must be >= 1");
+        const uint32_t n = (uint32_t)n64;
+        if (n == 0) {
+            *out_ids = static_cast<int64_t*>(std::malloc(sizeof(int64_t)));
+            return;
+        }
+        const int D = padded_dim(d);
+        if (!D) throw Error(SKY_E_DIMENSION, "the GPU engine supports 1 <= d <= 32");
+        // run the partition + reps steps through the engine with a host-given
+        // assignment (random strategy with an explicit partition_of)
+        Runner R(c);
+        cudaStream_t st = c->stream;
+        float* dp = R.dev<float>(S_PTS, (size_t)n * d);
+        SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, st));
+        uint32_t* hp = R.pin<uint32_t>(P_PID, n);
+        for (uint32_t i = 0; i < n; ++i) hp[i] = (uint32_t)partition_of[i];
+        uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
+        SKY_CUDA(cudaMemsetAsync(misc, 0, 64 * sizeof(uint32_t), st));
+        sky_config cfg;
+        sky_config_default(&cfg);
+        cfg.p = p;
+        uint64_t fix = 0;
+        PartitionOut po = partition_phase(R, dp, n, d, 0, SKY_RANDOM, p, 0, &cfg, nullptr, hp, &fix);
+        const uint32_t qq = (uint32_t)std::min<uint64_t>(q, n);
+        uint32_t* cand = R.dev<uint32_t>(S_REPCAND, (size_t)p * qq);
+        launch_rep_pick(po.key64, po.idx, po.off, (uint32_t)p, dp, d, qq, cand, st);
+        std::vector<uint32_t> hc((size_t)p * qq);
+        SKY_CUDA(cudaMemcpyAsync(hc.data(), cand, hc.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        std::vector<float> rows;
+        std::vector<int64_t> ids;
+        for (uint32_t v : hc)
+            if (v != kNone) {
+                ids.push_back(v);
+                rows.insert(rows.end(), points + (size_t)v * d, points + (size_t)(v + 1) * d);
+            }
+        // prune: the skyline of the candidates (prune_dominated_reps)
+        int64_t* sk = nullptr;
+        uint64_t ns = 0;
+        if (!ids.empty()) {
+            sky_config c2;
+            sky_config_default(&c2);
+            c2.strategy = SKY_SLICED;
+            c2.p = 1;
+            sky_result r;
+            run_impl(c, rows.data(), ids.size(), d, 0, 0, &c2, &r);
+            sk = r.ids;
+            ns = r.n_ids;
+            r.ids = nullptr;
+            sky_result_free(&r);
+        }
+        std::vector<int64_t> outv;
+        for (uint64_t k = 0; k < ns; ++k) outv.push_back(ids[sk[k]]);
+        std::free(sk);
+        std::sort(outv.begin(), outv.end());
+        *out_ids = static_cast<int64_t*>(std::malloc((outv.size() ? outv.size() : 1) * sizeof(int64_t)));
+        std::memcpy(*out_ids, outv.data(), outv.size() * sizeof(int64_t));
+        *n_out = outv.size();
+    });
+}
+
+void sky_free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,976 @@
+// kernels.cu — sm_100a kernels of the skyline engine.
+//
+// HBM-bound passes (prep, scatter/gather, offsets) are written for coalesced
+// row streams; the dominance core (k_relsky) and the BNL window kernel are
+// compare-issue bound: comparator tiles are staged in shared memory and
+// broadcast to every thread, each thread keeps RS_K candidates in registers,
+// and warps leave a tile as soon as their coordinate-sum bound is passed or
+// all their candidates are dominated.
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace sky {
+
+int padded_dim(uint32_t d) {
+    static const int widths[] = {2, 3, 4, 5, 6, 8, 10, 12, 16, 24, 32};
+    for (int w : widths)
+        if ((int)d <= w) return w;
+    return 0;
+}
+
+#define SKY_DISPATCH_D(D, ...)                                  \
+    switch (D) {                                                \
+        case 2: { constexpr int DT = 2; __VA_ARGS__; break; }   \
+        case 3: { constexpr int DT = 3; __VA_ARGS__; break; }   \
+        case 4: { constexpr int DT = 4; __VA_ARGS__; break; }   \
+        case 5: { constexpr int DT = 5; __VA_ARGS__; break; }   \
+        case 6: { constexpr int DT = 6; __VA_ARGS__; break; }   \
+        case 8: { constexpr int DT = 8; __VA_ARGS__; break; }   \
+        case 10: { constexpr int DT = 10; __VA_ARGS__; break; } \
+        case 12: { constexpr int DT = 12; __VA_ARGS__; break; } \
+        case 16: { constexpr int DT = 16; __VA_ARGS__; break; } \
+        case 24: { constexpr int DT = 24; __VA_ARGS__; break; } \
+        case 32: { constexpr int DT = 32; __VA_ARGS__; break; } \
+        default: throw Error(SKY_E_DIMENSION, "unsupported padded dimension"); \
+    }
+
+template <int D>
+struct Dims {
+    static constexpr int D4 = (D + 3) / 4 * 4;
+    static constexpr int V = D4 / 4;  // float4 per row
+};
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t canon_bits(float v) {
+    return v == 0.0f ? 0u : __float_as_uint(v);  // -0.0 and +0.0 compare equal
+}
+
+// ------------------------------------------------------------------ prep
+// One thread per row: FP64 coordinate sum (core.hpp:103-107, left to right,
+// no FMA), input validation (core.cpp:21-46, partition.cpp:26-29), partition
+// id for grid (partition.cpp:66-75) and angular (partition.cpp:118-148), and
+// the slicing key for sliced.
+__global__ void k_prep(PrepArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const float* x = a.pts + (size_t)i * a.d;
+    double sum = 0.0;
+    uint32_t err = 0;
+    uint64_t pid = 0;
+    if (a.strategy == SKY_GRID) {
+        uint64_t stride = 1;
+        for (uint32_t j = 0; j < a.d; ++j) {
+            const float v = x[j];
+            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+            if (!(v >= 0.0f && v <= 1.0f)) err |= kErrGridRange;
+            sum = __dadd_rn(sum, (double)v);
+            uint64_t cell = (uint64_t)__dmul_rn((double)v, (double)a.m);
+            if (cell >= a.m) cell = a.m - 1;
+            pid += cell * stride;
+            stride *= a.m;
+        }
+    } else if (a.strategy == SKY_ANGULAR) {
+        for (uint32_t j = 0; j < a.d; ++j) {
+            const float v = x[j];
+            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+            sum = __dadd_rn(sum, (double)v);
+        }
+        // hyperspherical_angles: tail sums of squares back to front.
+        const double PI = 3.14159265358979323846;
+        double tail = __dmul_rn((double)x[a.d - 1], (double)x[a.d - 1]);
+        uint64_t stride_i = 1;
+        for (uint32_t k = 0; k + 1 < a.d; ++k) stride_i *= a.m;  // m^(d-2) for i = d-2
+        bool ambiguous = false;
+        for (uint32_t ii = a.d - 1; ii-- > 0;) {
+            const double xi = (double)x[ii];
+            const double phi = atan2(sqrt(tail), xi);
+            tail = __dadd_rn(tail, __dmul_rn(xi, xi));
+            const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
+            uint64_t slice = (uint64_t)v;
+            if (slice >= a.m) slice = a.m - 1;
+            // CUDA's atan2 may differ from the host libm by an ulp or two; a
+            // value this close to an interior slice boundary is resolved on
+            // the host with the reference's own formula.
+            const double r = rint(v);
+            if (r >= 1.0 && r <= (double)(a.m - 1) && fabs(v - r) <= 1e-9 * fmax(1.0, v)) ambiguous = true;
+            stride_i /= a.m;
+            pid += slice * (stride_i ? stride_i : 1);
+        }
+        if (ambiguous) {
+            const uint32_t k = atomicAdd(a.amb_count, 1u);
+            if (k < a.amb_cap) a.amb_list[k] = i;
+        }
+    } else {
+        for (uint32_t j = 0; j < a.d; ++j) {
+            const float v = x[j];
+            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+            sum = __dadd_rn(sum, (double)v);
+        }
+        if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
+        if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(x[a.slice_dim]);
+    }
+    if (err) atomicOr(a.err, err);
+    const uint32_t skey = __float_as_uint(__double2float_rn(sum));  // monotone in sum
+    a.key64[i] = (pid << 32) | skey;
+    a.idx[i] = i;
+}
+
+void launch_prep(const PrepArgs& a, cudaStream_t st) {
+    if (a.n == 0) return;
+    k_prep<<<ceil_div(a.n, 256), 256, 0, st>>>(a);
+    SKY_LAUNCH_CHECK();
+}
+
+// The angular stride loop above walks i = d-2 .. 0 with stride m^i.
+// (stride_i starts at m^(d-1) and is divided before use.)
+
+__global__ void k_seg_offsets(const uint64_t* __restrict__ key64, uint32_t n, uint32_t P, uint32_t* off) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = (uint32_t)(key64[i] >> 32);
+    const int64_t prev = i ? (int64_t)(key64[i - 1] >> 32) : -1;
+    for (int64_t q = prev + 1; q <= (int64_t)p; ++q) off[q] = i;
+    if (i == n - 1)
+        for (uint32_t q = p + 1; q <= P; ++q) off[q] = n;
+}
+
+void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t* off, cudaStream_t st) {
+    if (n == 0) {
+        SKY_CUDA(cudaMemsetAsync(off, 0, (P + 1) * sizeof(uint32_t), st));
+        return;
+    }
+    k_seg_offsets<<<ceil_div(n, 256), 256, 0, st>>>(key64, n, P, off);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_patch_pid(uint64_t* key64, const uint32_t* rows, const uint32_t* pids, uint32_t count) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t r = rows[i];
+    key64[r] = ((uint64_t)pids[i] << 32) | (key64[r] & 0xFFFFFFFFull);
+}
+
+void launch_patch_pid(uint64_t* key64, const uint32_t* rows, const uint32_t* pids, uint32_t count,
+                      cudaStream_t st) {
+    if (!count) return;
+    k_patch_pid<<<ceil_div(count, 256), 256, 0, st>>>(key64, rows, pids, count);
+    SKY_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- sliced
+// rank -> partition (partition.cpp:212-216)
+__device__ __forceinline__ uint32_t slice_of_rank(uint64_t rank, uint64_t n, uint64_t p) {
+    uint64_t index = n > 1 ? rank * p / (n - 1) : 0;
+    return (uint32_t)(index >= p ? p - 1 : index);
+}
+
+// First rank belonging to slice b (b >= 1): smallest r with r*p/(n-1) >= b.
+__device__ __forceinline__ uint64_t first_rank_of_slice(uint64_t b, uint64_t n, uint64_t p) {
+    return (b * (n - 1) + p - 1) / p;
+}
+
+// For each slice boundary whose two sides share x[k], record the tie run
+// [ra, rc) once (by the first boundary inside it).
+__global__ void k_slice_runs(const uint32_t* __restrict__ key, uint32_t n, uint64_t p, uint32_t* runs,
+                             uint32_t* run_count, uint32_t run_cap) {
+    const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (b >= p || n < 2) return;
+    const uint64_t r = first_rank_of_slice(b, n, p);
+    if (r == 0 || r >= n) return;
+    if (key[r - 1] != key[r]) return;
+    const uint32_t v = key[r];
+    // run bounds by binary search
+    uint64_t lo = 0, hi = r;  // first index with key == v
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) / 2;
+        if (key[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t ra = lo;
+    lo = r; hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) / 2;
+        if (key[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t rc = lo;
+    // owner: no earlier boundary inside [ra, rc)
+    if (b > 1) {
+        const uint64_t rp = first_rank_of_slice(b - 1, n, p);
+        if (rp > ra) return;
+    }
+    const uint32_t k = atomicAdd(run_count, 1u);
+    if (k < run_cap) {
+        runs[2 * k] = (uint32_t)ra;
+        runs[2 * k + 1] = (uint32_t)rc;
+    }
+}
+
+void launch_slice_runs(const uint32_t* sorted_key, uint32_t n, uint64_t p, uint32_t* runs, uint32_t* run_count,
+                       uint32_t run_cap, cudaStream_t st) {
+    if (p < 2 || n < 2) return;
+    k_slice_runs<<<ceil_div(p - 1, 256), 256, 0, st>>>(sorted_key, n, p, runs, run_count, run_cap);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_slice_assign(const uint32_t* __restrict__ rank_idx, uint32_t n, uint64_t p, uint64_t* key64) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t row = rank_idx[r];
+    key64[row] = ((uint64_t)slice_of_rank(r, n, p) << 32) | (key64[row] & 0xFFFFFFFFull);
+}
+
+void launch_slice_assign(const uint32_t* rank_idx, uint32_t n, uint64_t p, uint64_t* key64, cudaStream_t st) {
+    if (!n) return;
+    k_slice_assign<<<ceil_div(n, 256), 256, 0, st>>>(rank_idx, n, p, key64);
+    SKY_LAUNCH_CHECK();
+}
+
+// coords_then_id_less (core.cpp:10-17) on float rows (exact: float order ==
+// double order of the upcast values).
+__device__ __forceinline__ bool lex_less(const float* pts, uint32_t d, uint32_t a, uint32_t b) {
+    const float* pa = pts + (size_t)a * d;
+    const float* pb = pts + (size_t)b * d;
+    for (uint32_t j = 0; j < d; ++j) {
+        const float x = pa[j], y = pb[j];
+        if (x < y) return true;
+        if (x > y) return false;
+    }
+    return a < b;
+}
+
+// Exact rank of each member inside its straddling tie run, then its slice.
+__global__ void k_slice_fix_runs(const float* __restrict__ pts, uint32_t d, const uint32_t* __restrict__ rank_idx,
+                                 uint32_t n, uint64_t p, const uint32_t* __restrict__ runs, uint64_t* key64) {
+    const uint32_t ra = runs[2 * blockIdx.y], rc = runs[2 * blockIdx.y + 1];
+    const uint32_t e = ra + blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rc) return;
+    const uint32_t row = rank_idx[e];
+    uint32_t rank = 0;
+    for (uint32_t f = ra; f < rc; ++f)
+        if (f != e && lex_less(pts, d, rank_idx[f], row)) ++rank;
+    key64[row] = ((uint64_t)slice_of_rank(ra + rank, n, p) << 32) | (key64[row] & 0xFFFFFFFFull);
+}
+
+void launch_slice_fix_runs(const float* pts, uint32_t d, const uint32_t* rank_idx, uint32_t n, uint64_t p,
+                           const uint32_t* runs, uint32_t n_runs, uint32_t max_len, uint64_t* key64,
+                           cudaStream_t st) {
+    if (!n_runs) return;
+    dim3 grid(ceil_div(max_len, 256), n_runs);
+    k_slice_fix_runs<<<grid, 256, 0, st>>>(pts, d, rank_idx, n, p, runs, key64);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_gather_coord_key(const float* __restrict__ pts, uint32_t d, uint32_t j,
+                                   const uint32_t* __restrict__ idx, uint32_t n, uint32_t* key) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = canon_bits(pts[(size_t)idx[i] * d + j]);
+}
+
+void launch_gather_coord_key(const float* pts, uint32_t d, uint32_t j, const uint32_t* idx, uint32_t n,
+                             uint32_t* key, cudaStream_t st) {
+    if (!n) return;
+    k_gather_coord_key<<<ceil_div(n, 256), 256, 0, st>>>(pts, d, j, idx, n, key);
+    SKY_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------- representatives
+__device__ double row_sum(const float* pts, uint32_t d, uint32_t r) {
+    const float* x = pts + (size_t)r * d;
+    double s = 0.0;
+    for (uint32_t j = 0; j < d; ++j) s = __dadd_rn(s, (double)x[j]);
+    return s;
+}
+
+// (coord_sum, coords_then_id_less) total order of filter.cpp:74-79.
+__device__ bool rep_less(const float* pts, uint32_t d, uint32_t a, uint32_t b) {
+    const double sa = row_sum(pts, d, a), sb = row_sum(pts, d, b);
+    if (sa != sb) return sa < sb;
+    return lex_less(pts, d, a, b);
+}
+
+// One CTA per partition. Rows are sorted by (pid, skey, row); skey ties can
+// hide (sum, lex, id) order, so the tie run that straddles position q-1 is
+// resolved exactly by repeated block-wide argmin.
+__global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* __restrict__ idx,
+                           const uint32_t* __restrict__ off, const float* __restrict__ pts, uint32_t d,
+                           uint32_t q, uint32_t* cand) {
+    const uint32_t p = blockIdx.x;
+    const uint32_t a = off[p], b = off[p + 1];
+    uint32_t* out = cand + (size_t)p * q;
+    const uint32_t size = b - a;
+    const uint32_t take = size < q ? size : q;
+    for (uint32_t k = threadIdx.x; k < q; k += blockDim.x) out[k] = kNone;
+    if (take == 0) return;
+    const uint32_t v = (uint32_t)key64[a + take - 1];
+    // run [ra, rb) of skey == v inside the partition
+    __shared__ uint32_t s_ra, s_rb;
+    if (threadIdx.x == 0) {
+        uint32_t lo = a, hi = a + take - 1;
+        while (lo < hi) {
+            uint32_t mid = (lo + hi) / 2;
+            if ((uint32_t)key64[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        s_ra = lo;
+        lo = a + take - 1; hi = b;
+        while (lo < hi) {
+            uint32_t mid = (lo + hi) / 2;
+            if ((uint32_t)key64[mid] <= v) lo = mid + 1; else hi = mid;
+        }
+        s_rb = lo;
+    }
+    __syncthreads();
+    const uint32_t ra = s_ra, rb = s_rb;
+    for (uint32_t k = threadIdx.x; k < ra - a; k += blockDim.x) out[k] = idx[a + k];
+    const uint32_t need = take - (ra - a);
+    if (rb - ra == need) {
+        for (uint32_t k = threadIdx.x; k < need; k += blockDim.x) out[ra - a + k] = idx[ra + k];
+        return;
+    }
+    // select `need` smallest of the run under the exact order
+    __shared__ uint32_t s_best[32];
+    uint32_t last = kNone;
+    for (uint32_t r = 0; r < need; ++r) {
+        uint32_t best = kNone;
+        for (uint32_t e = ra + threadIdx.x; e < rb; e += blockDim.x) {
+            const uint32_t row = idx[e];
+            if (last != kNone && !rep_less(pts, d, last, row)) continue;  // already taken
+            if (best == kNone || rep_less(pts, d, row, best)) best = row;
+        }
+        // warp reduce
+        for (int o = 16; o > 0; o >>= 1) {
+            uint32_t other = __shfl_down_sync(0xffffffffu, best, o);
+            if (other != kNone && (best == kNone || rep_less(pts, d, other, best))) best = other;
+        }
+        if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t bb = kNone;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+                const uint32_t o = s_best[w];
+                if (o != kNone && (bb == kNone || rep_less(pts, d, o, bb))) bb = o;
+            }
+            s_best[0] = bb;
+            out[ra - a + r] = bb;
+        }
+        __syncthreads();
+        last = s_best[0];
+        __syncthreads();
+    }
+}
+
+void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
+                     const float* pts, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st) {
+    if (!P) return;
+    k_rep_pick<<<P, 128, 0, st>>>(key64, idx, off, pts, d, q, cand);
+    SKY_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ compaction
+template <int D>
+__global__ void k_scatter_direct(DevSet in, const uint8_t* __restrict__ dead, const uint32_t* __restrict__ pos,
+                                 DevSet out) {
+    constexpr int V = Dims<D>::V;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= in.n || dead[i]) return;
+    const uint32_t o = pos[i];
+    const float4* src = reinterpret_cast<const float4*>(in.xyz) + (size_t)i * V;
+    float4* dst = reinterpret_cast<float4*>(out.xyz) + (size_t)o * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) dst[v] = src[v];
+    out.skey[o] = in.skey[i];
+    out.id[o] = in.id[i];
+}
+
+void launch_scatter_direct(int D, const DevSet& in, const uint8_t* dead, const uint32_t* pos, DevSet out,
+                           cudaStream_t st) {
+    if (!in.n) return;
+    SKY_DISPATCH_D(D, (k_scatter_direct<DT><<<ceil_div(in.n, 256), 256, 0, st>>>(in, dead, pos, out)));
+    SKY_LAUNCH_CHECK();
+}
+
+template <int D>
+__global__ void k_scatter_indirect(const float* __restrict__ pts, uint32_t d, const uint32_t* __restrict__ idx,
+                                   const uint64_t* __restrict__ key64, uint32_t n,
+                                   const uint8_t* __restrict__ dead, const uint32_t* __restrict__ pos,
+                                   DevSet out) {
+    constexpr int D4 = Dims<D>::D4;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || (dead && dead[i])) return;
+    const uint32_t o = pos ? pos[i] : i;
+    const uint32_t row = idx[i];
+    const float* x = pts + (size_t)row * d;
+    float* dst = out.xyz + (size_t)o * D4;
+#pragma unroll
+    for (int j = 0; j < D4; ++j) dst[j] = (uint32_t)j < d ? x[j] : 0.0f;
+    out.skey[o] = (uint32_t)key64[i];
+    out.id[o] = row;
+}
+
+void launch_scatter_indirect(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64,
+                             uint32_t n, const uint8_t* dead, const uint32_t* pos, DevSet out, cudaStream_t st) {
+    if (!n) return;
+    SKY_DISPATCH_D(D, (k_scatter_indirect<DT><<<ceil_div(n, 256), 256, 0, st>>>(pts, d, idx, key64, n, dead,
+                                                                               pos, out)));
+    SKY_LAUNCH_CHECK();
+}
+
+// Rows of the input -> DevSet (reps, small sets). skey recomputed when
+// skey_src is null.
+template <int D>
+__global__ void k_gather_rows(const float* __restrict__ pts, uint32_t d, const uint32_t* __restrict__ rows,
+                              uint32_t n, DevSet out) {
+    constexpr int D4 = Dims<D>::D4;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t row = rows[i];
+    const float* x = pts + (size_t)row * d;
+    float* dst = out.xyz + (size_t)i * D4;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < D4; ++j) {
+        const float v = (uint32_t)j < d ? x[j] : 0.0f;
+        dst[j] = v;
+        if ((uint32_t)j < d) s = __dadd_rn(s, (double)v);
+    }
+    out.skey[i] = __float_as_uint(__double2float_rn(s));
+    out.id[i] = row;
+}
+
+void launch_gather_rows(int D, const float* pts, uint32_t d, const uint32_t* rows, uint32_t n, DevSet out,
+                        const uint32_t* skey_src, cudaStream_t st) {
+    (void)skey_src;
+    if (!n) return;
+    SKY_DISPATCH_D(D, (k_gather_rows<DT><<<ceil_div(n, 256), 256, 0, st>>>(pts, d, rows, n, out)));
+    SKY_LAUNCH_CHECK();
+}
+
+template <int D>
+__global__ void k_gather_set(DevSet in, const uint32_t* __restrict__ perm, uint32_t n, DevSet out) {
+    constexpr int V = Dims<D>::V;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t s = perm[i];
+    const float4* src = reinterpret_cast<const float4*>(in.xyz) + (size_t)s * V;
+    float4* dst = reinterpret_cast<float4*>(out.xyz) + (size_t)i * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) dst[v] = src[v];
+    out.skey[i] = in.skey[s];
+    out.id[i] = in.id[s];
+}
+
+void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st) {
+    if (!in.n) return;
+    SKY_DISPATCH_D(D, (k_gather_set<DT><<<ceil_div(in.n, 256), 256, 0, st>>>(in, perm, in.n, out)));
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_remap_offsets(const uint32_t* __restrict__ off_old, uint32_t P, const uint32_t* __restrict__ pos,
+                                const uint8_t* __restrict__ dead, uint32_t n, uint32_t* off_new) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > P) return;
+    const uint32_t o = off_old[p];
+    off_new[p] = o < n ? pos[o] : (n ? pos[n - 1] + (dead[n - 1] ? 0u : 1u) : 0u);
+}
+
+void launch_remap_offsets(const uint32_t* off_old, uint32_t P, const uint32_t* pos, const uint8_t* dead,
+                          uint32_t n, uint32_t* off_new, cudaStream_t st) {
+    k_remap_offsets<<<ceil_div(P + 1, 256), 256, 0, st>>>(off_old, P, pos, dead, n, off_new);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, uint32_t* total) {
+    *total = n ? pos[n - 1] + (dead[n - 1] ? 0u : 1u) : 0u;
+}
+
+void launch_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, uint32_t* total, cudaStream_t st) {
+    k_count_total<<<1, 1, 0, st>>>(pos, dead, n, total);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_compact_ids(const uint32_t* __restrict__ id, const uint8_t* __restrict__ dead,
+                              const uint32_t* __restrict__ pos, uint32_t n, uint32_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || dead[i]) return;
+    out[pos[i]] = id[i];
+}
+
+void launch_compact_ids(const uint32_t* id, const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t* out,
+                        cudaStream_t st) {
+    if (!n) return;
+    k_compact_ids<<<ceil_div(n, 256), 256, 0, st>>>(id, dead, pos, n, out);
+    SKY_LAUNCH_CHECK();
+}
+
+void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st) {
+    if (n) SKY_CUDA(cudaMemsetAsync(p, v, n, st));
+}
+
+__global__ void k_mark_cells_dead(const uint64_t* __restrict__ key64, uint32_t n, const uint8_t* __restrict__ cell_dead,
+                                  uint8_t* dead) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    dead[i] = cell_dead[(uint32_t)(key64[i] >> 32)];
+}
+
+void launch_mark_cells_dead(const uint64_t* key64, uint32_t n, const uint8_t* cell_dead, uint8_t* dead,
+                            cudaStream_t st) {
+    if (!n) return;
+    k_mark_cells_dead<<<ceil_div(n, 256), 256, 0, st>>>(key64, n, cell_dead, dead);
+    SKY_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------- dominance core
+constexpr int RS_THREADS = 128;
+constexpr int RS_K = 4;
+constexpr int RS_TILE = 256;
+
+// s dominates t on D coordinates (core.hpp:89-96): s <= t everywhere and
+// s < t somewhere. The <=-chain is the hot path; strictness is only checked
+// on a hit.
+template <int D>
+__device__ __forceinline__ bool dominates_f(const float (&s)[D], const float (&t)[D]) {
+    bool gt = false;
+#pragma unroll
+    for (int j = 0; j < D; ++j) gt |= s[j] > t[j];
+    if (gt) return false;
+    bool lt = false;
+#pragma unroll
+    for (int j = 0; j < D; ++j) lt |= s[j] < t[j];
+    return lt;
+}
+
+template <int D, bool INDIRECT>
+__global__ void __launch_bounds__(RS_THREADS) k_relsky(RelskyArgs a) {
+    constexpr int V = Dims<D>::V;
+    __shared__ float4 s_xyz[RS_TILE * V];
+    __shared__ uint32_t s_key[RS_TILE];
+    __shared__ uint32_t s_red[RS_THREADS / 32];
+    __shared__ uint32_t s_end;
+
+    const Item it = a.items[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    float t[RS_K][D];
+    uint32_t tk[RS_K];
+    bool alive[RS_K];
+    const uint32_t pos0 = it.cb + tid * RS_K;
+    uint32_t my_max = 0;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < RS_K; ++k) {
+        const uint32_t pos = pos0 + k;
+        alive[k] = pos < it.ce && !a.dead[pos];
+        tk[k] = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) t[k][j] = 0.0f;
+        if (alive[k]) {
+            if (INDIRECT) {
+                const float* x = a.cxyz + (size_t)a.cidx[pos] * a.cd;
+#pragma unroll
+                for (int j = 0; j < D; ++j) t[k][j] = (uint32_t)j < a.cd ? x[j] : 0.0f;
+                tk[k] = a.cskey[2 * (size_t)pos];  // low word of key64
+            } else {
+                const float4* x = reinterpret_cast<const float4*>(a.cxyz) + (size_t)pos * V;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const float4 q = x[v];
+                    if (4 * v + 0 < D) t[k][4 * v + 0] = q.x;
+                    if (4 * v + 1 < D) t[k][4 * v + 1] = q.y;
+                    if (4 * v + 2 < D) t[k][4 * v + 2] = q.z;
+                    if (4 * v + 3 < D) t[k][4 * v + 3] = q.w;
+                }
+                tk[k] = a.cskey[pos];
+            }
+            my_max = max(my_max, tk[k]);
+            any = true;
+        }
+    }
+    bool initially[RS_K];
+#pragma unroll
+    for (int k = 0; k < RS_K; ++k) initially[k] = alive[k];
+
+    uint32_t warp_max = __reduce_max_sync(0xffffffffu, my_max);
+    if (lane == 0) s_red[warp] = warp_max;
+    __syncthreads();
+    uint32_t cta_max = 0;
+#pragma unroll
+    for (int w = 0; w < RS_THREADS / 32; ++w) cta_max = max(cta_max, s_red[w]);
+    if (!a.bounded) warp_max = cta_max = 0xFFFFFFFFu;
+    bool warp_alive = __any_sync(0xffffffffu, any);
+    if (!__syncthreads_or(any)) return;
+
+    unsigned long long ntests = 0;
+    for (uint32_t r = it.lb; r < it.le; ++r) {
+        const uint2 rg = a.ranges[r];
+        uint32_t sb = rg.x, se = rg.y;
+        if (a.bounded) {
+            if (tid == 0) {
+                uint32_t lo = sb, hi = se;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (a.sskey[mid] <= cta_max) lo = mid + 1; else hi = mid;
+                }
+                s_end = lo;
+            }
+            __syncthreads();
+            se = s_end;
+        }
+        bool warp_range_live = warp_alive;
+        for (uint32_t base = sb; base < se; base += RS_TILE) {
+            const uint32_t len = min((uint32_t)RS_TILE, se - base);
+            __syncthreads();
+            const float4* src = reinterpret_cast<const float4*>(a.sxyz) + (size_t)base * V;
+            for (uint32_t i = tid; i < len * V; i += RS_THREADS) s_xyz[i] = src[i];
+            for (uint32_t i = tid; i < len; i += RS_THREADS) s_key[i] = a.sskey[base + i];
+            __syncthreads();
+            if (warp_range_live) {
+                uint32_t i = 0;
+                for (; i < len; ++i) {
+                    if (s_key[i] > warp_max) break;  // warp-uniform: sorted comparators
+                    float s[D];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const float4 q = s_xyz[i * V + v];
+                        if (4 * v + 0 < D) s[4 * v + 0] = q.x;
+                        if (4 * v + 1 < D) s[4 * v + 1] = q.y;
+                        if (4 * v + 2 < D) s[4 * v + 2] = q.z;
+                        if (4 * v + 3 < D) s[4 * v + 3] = q.w;
+                    }
+#pragma unroll
+                    for (int k = 0; k < RS_K; ++k) {
+                        if (alive[k] && dominates_f<D>(s, t[k])) {
+                            alive[k] = false;
+                            ntests += i + 1;
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, alive[0] | alive[1] | alive[2] | alive[3])) {
+                        ++i;
+                        break;
+                    }
+                }
+                int nal = 0;
+#pragma unroll
+                for (int k = 0; k < RS_K; ++k) nal += alive[k];
+                ntests += (unsigned long long)nal * i;
+                if (i < len) warp_range_live = false;
+                warp_alive = __any_sync(0xffffffffu, alive[0] | alive[1] | alive[2] | alive[3]);
+                if (!warp_alive) warp_range_live = false;
+            }
+            if (!__syncthreads_or(warp_range_live)) break;
+        }
+        if (!__syncthreads_or(warp_alive)) break;
+    }
+#pragma unroll
+    for (int k = 0; k < RS_K; ++k)
+        if (initially[k] && !alive[k]) a.dead[pos0 + k] = 1;
+    if (a.tests) {
+        ntests = warp_sum_u64(ntests);
+        if (lane == 0 && ntests) atomicAdd(a.tests, ntests);
+    }
+}
+
+void launch_relsky(int D, const RelskyArgs& a, cudaStream_t st) {
+    if (!a.n_items) return;
+    if (a.indirect) {
+        SKY_DISPATCH_D(D, (k_relsky<DT, true><<<a.n_items, RS_THREADS, 0, st>>>(a)));
+    } else {
+        SKY_DISPATCH_D(D, (k_relsky<DT, false><<<a.n_items, RS_THREADS, 0, st>>>(a)));
+    }
+    SKY_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------- BNL
+// Block-nested-loops (Börzsönyi et al., ICDE 2001) with a shared-memory
+// window of at most `cap` points, restated for a CTA: the partition is
+// consumed in batches of BNL_B tuples (one per thread); each batch is
+// compared with the window in both directions (window tuples a batch tuple
+// dominates are evicted) and with itself; survivors enter the window while it
+// has room and spill to an overflow list otherwise. Window tuples carry
+// (pass, timestamp = overflow length at insertion); a tuple inserted in pass
+// p is confirmed once pass p+1 has consumed that many overflow tuples.
+constexpr int BNL_B = 256;
+
+template <int D>
+__global__ void __launch_bounds__(BNL_B) k_bnl(BnlArgs a, uint32_t cap, uint32_t* win_pos_g, uint32_t* win_meta_g,
+                                                 uint32_t* work_counter) {
+    constexpr int V = Dims<D>::V;
+    extern __shared__ float4 smem[];
+    float4* w_xyz = smem;                                        // cap * V
+    float4* b_xyz = w_xyz + (size_t)cap * V;                     // BNL_B * V
+    uint8_t* w_kill = reinterpret_cast<uint8_t*>(b_xyz + BNL_B * V);  // cap
+    __shared__ uint32_t s_wn, s_ovf_w, s_part, s_scan[BNL_B / 32], s_bn;
+    __shared__ int s_pass;
+
+    uint32_t* win_pos = win_pos_g + (size_t)blockIdx.x * cap;
+    uint32_t* win_meta = win_meta_g + (size_t)blockIdx.x * cap;  // (pass << 24) | ts (ts < 2^24)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long ntests = 0;
+
+    for (;;) {
+        if (tid == 0) s_part = atomicAdd(work_counter, 1u);
+        __syncthreads();
+        const uint32_t part = s_part;
+        if (part >= a.P) break;
+        const uint32_t seg_b = a.seg_off[part], seg_e = a.seg_off[part + 1];
+        if (seg_b == seg_e) { __syncthreads(); continue; }
+        uint32_t* ovf = a.overflow + seg_b;  // in-place overflow list (positions)
+        if (tid == 0) { s_wn = 0; s_pass = 0; }
+        __syncthreads();
+        uint32_t in_n = seg_e - seg_b;  // pass 0 input = the segment itself
+        bool first = true;
+        while (in_n > 0 || s_wn > 0) {
+            const int pass = s_pass;
+            if (tid == 0) s_ovf_w = 0;
+            __syncthreads();
+            for (uint32_t k0 = 0; k0 < in_n || k0 == 0; k0 += BNL_B) {
+                // confirm window tuples of the previous pass whose timestamp
+                // has been reached (they have now met every tuple)
+                if (!first) {
+                    const uint32_t wn = s_wn;
+                    for (uint32_t w = tid; w < wn; w += BNL_B) {
+                        const uint32_t meta = win_meta[w];
+                        const bool prev = (int)(meta >> 24) == pass - 1;
+                        w_kill[w] = (prev && (meta & 0xFFFFFFu) <= k0) ? 2 : 0;
+                    }
+                } else {
+                    for (uint32_t w = tid; w < s_wn; w += BNL_B) w_kill[w] = 0;
+                }
+                __syncthreads();
+                if (in_n == 0) break;
+                // load batch
+                const uint32_t bn = min((uint32_t)BNL_B, in_n - k0);
+                uint32_t mypos = kNone;
+                float t[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) t[j] = 0.0f;
+                if ((uint32_t)tid < bn) {
+                    mypos = first ? seg_b + k0 + tid : ovf[k0 + tid];
+                    const float4* x = reinterpret_cast<const float4*>(a.xyz) + (size_t)mypos * V;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const float4 q = x[v];
+                        b_xyz[tid * V + v] = q;
+                        if (4 * v + 0 < D) t[4 * v + 0] = q.x;
+                        if (4 * v + 1 < D) t[4 * v + 1] = q.y;
+                        if (4 * v + 2 < D) t[4 * v + 2] = q.z;
+                        if (4 * v + 3 < D) t[4 * v + 3] = q.w;
+                    }
+                }
+                __syncthreads();
+                bool alive = (uint32_t)tid < bn;
+                // batch vs window (both directions)
+                const uint32_t wn = s_wn;
+                if (__syncthreads_or(alive)) {
+                    for (uint32_t w = 0; w < wn; ++w) {
+                        if (w_kill[w] == 1) continue;
+                        float s[D];
+#pragma unroll
+                        for (int v = 0; v < V; ++v) {
+                            const float4 q = w_xyz[w * V + v];
+                            if (4 * v + 0 < D) s[4 * v + 0] = q.x;
+                            if (4 * v + 1 < D) s[4 * v + 1] = q.y;
+                            if (4 * v + 2 < D) s[4 * v + 2] = q.z;
+                            if (4 * v + 3 < D) s[4 * v + 3] = q.w;
+                        }
+                        if (alive) {
+                            bool gt = false, lt = false;
+#pragma unroll
+                            for (int j = 0; j < D; ++j) {
+                                gt |= s[j] > t[j];
+                                lt |= s[j] < t[j];
+                            }
+                            ntests += 2;  // both directions
+                            if (!gt && lt) alive = false;              // window dominates t
+                            else if (gt && !lt) w_kill[w] = 1;          // t dominates window tuple
+                        }
+                    }
+                }
+                // batch vs batch
+                for (uint32_t b = 0; b < bn; ++b) {
+                    if (!alive) break;
+                    if (b == (uint32_t)tid) continue;
+                    float s[D];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const float4 q = b_xyz[b * V + v];
+                        if (4 * v + 0 < D) s[4 * v + 0] = q.x;
+                        if (4 * v + 1 < D) s[4 * v + 1] = q.y;
+                        if (4 * v + 2 < D) s[4 * v + 2] = q.z;
+                        if (4 * v + 3 < D) s[4 * v + 3] = q.w;
+                    }
+                    ++ntests;
+                    if (dominates_f<D>(s, t)) alive = false;
+                }
+                __syncthreads();
+                // remove killed (1) and confirmed (2) window tuples; compact
+                {
+                    const uint32_t wn0 = s_wn;
+                    uint32_t kept_before = 0;
+                    for (uint32_t c0 = 0; c0 < wn0; c0 += BNL_B) {
+                        const uint32_t w = c0 + tid;
+                        const bool in = w < wn0;
+                        const uint8_t kill = in ? w_kill[w] : 0;
+                        const bool keep = in && kill == 0;
+                        float4 q[V];
+                        uint32_t pos = 0, meta = 0;
+                        if (keep) {
+#pragma unroll
+                            for (int v = 0; v < V; ++v) q[v] = w_xyz[w * V + v];
+                            pos = win_pos[w];
+                            meta = win_meta[w];
+                        }
+                        if (in && kill == 2) a.dead[win_pos[w]] = 0;  // confirmed skyline tuple
+                        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                        if (lane == 0) s_scan[warp] = __popc(bal);
+                        __syncthreads();
+                        uint32_t off = kept_before;
+                        for (int ww = 0; ww < warp; ++ww) off += s_scan[ww];
+                        off += __popc(bal & ((1u << lane) - 1u));
+                        uint32_t tot = 0;
+                        for (int ww = 0; ww < BNL_B / 32; ++ww) tot += s_scan[ww];
+                        __syncthreads();
+                        if (keep) {
+#pragma unroll
+                            for (int v = 0; v < V; ++v) w_xyz[off * V + v] = q[v];
+                            win_pos[off] = pos;
+                            win_meta[off] = meta;
+                        }
+                        kept_before += tot;
+                        __syncthreads();
+                    }
+                    if (tid == 0) s_wn = kept_before;
+                    __syncthreads();
+                }
+                // insert survivors (batch order) or spill them
+                {
+                    const unsigned bal = __ballot_sync(0xffffffffu, alive);
+                    if (lane == 0) s_scan[warp] = __popc(bal);
+                    __syncthreads();
+                    uint32_t rank = __popc(bal & ((1u << lane) - 1u));
+                    for (int ww = 0; ww < warp; ++ww) rank += s_scan[ww];
+                    const uint32_t wn1 = s_wn, ow = s_ovf_w;
+                    uint32_t room = cap - wn1;
+                    if (alive) {
+                        if (rank < room) {
+                            const uint32_t slot = wn1 + rank;
+#pragma unroll
+                            for (int v = 0; v < V; ++v) w_xyz[slot * V + v] = b_xyz[tid * V + v];
+                            win_pos[slot] = mypos;
+                            // timestamp: overflow writes in this pass so far
+                            win_meta[slot] = ((uint32_t)pass << 24) | min(ow, 0xFFFFFFu);
+                        } else {
+                            ovf[ow + (rank - room)] = mypos;  // ow + ... <= k0 + tid (in place)
+                        }
+                    }
+                    uint32_t tot = 0;
+                    for (int ww = 0; ww < BNL_B / 32; ++ww) tot += s_scan[ww];
+                    __syncthreads();
+                    if (tid == 0) {
+                        const uint32_t ins = min(tot, room);
+                        s_wn = wn1 + ins;
+                        s_ovf_w = ow + (tot - ins);
+                    }
+                    __syncthreads();
+                }
+            }
+            // end of pass: window tuples inserted before any overflow in
+            // this pass (ts == 0) are confirmed; when no overflow was written
+            // every window tuple is confirmed.
+            {
+                const uint32_t ovf_n = s_ovf_w;
+                const uint32_t wn0 = s_wn;
+                for (uint32_t w = tid; w < wn0; w += BNL_B) {
+                    const uint32_t meta = win_meta[w];
+                    const bool cur = (int)(meta >> 24) == pass;
+                    const bool confirm = ovf_n == 0 || (cur && (meta & 0xFFFFFFu) == 0) ||
+                                         (!cur && (int)(meta >> 24) == pass - 1);
+                    w_kill[w] = confirm ? 2 : 0;
+                }
+                __syncthreads();
+                uint32_t kept_before = 0;
+                for (uint32_t c0 = 0; c0 < wn0; c0 += BNL_B) {
+                    const uint32_t w = c0 + tid;
+                    const bool in = w < wn0;
+                    const bool keep = in && w_kill[w] == 0;
+                    float4 q[V];
+                    uint32_t pos = 0, meta = 0;
+                    if (keep) {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) q[v] = w_xyz[w * V + v];
+                        pos = win_pos[w];
+                        meta = win_meta[w];
+                    }
+                    if (in && !keep) a.dead[win_pos[w]] = 0;
+                    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                    if (lane == 0) s_scan[warp] = __popc(bal);
+                    __syncthreads();
+                    uint32_t off = kept_before + __popc(bal & ((1u << lane) - 1u));
+                    for (int ww = 0; ww < warp; ++ww) off += s_scan[ww];
+                    uint32_t tot = 0;
+                    for (int ww = 0; ww < BNL_B / 32; ++ww) tot += s_scan[ww];
+                    __syncthreads();
+                    if (keep) {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) w_xyz[off * V + v] = q[v];
+                        win_pos[off] = pos;
+                        win_meta[off] = meta;
+                    }
+                    kept_before += tot;
+                    __syncthreads();
+                }
+                if (tid == 0) {
+                    s_wn = kept_before;
+                    s_pass = pass + 1;
+                    s_bn = ovf_n;
+                }
+                __syncthreads();
+                in_n = s_bn;
+                first = false;
+            }
+        }
+        __syncthreads();
+    }
+    if (a.tests) {
+        ntests = warp_sum_u64(ntests);
+        if (lane == 0 && ntests) atomicAdd(a.tests, ntests);
+    }
+}
+
+template <int D>
+size_t bnl_smem_bytes(uint32_t cap) {
+    constexpr int V = Dims<D>::V;
+    return (size_t)cap * V * 16 + (size_t)BNL_B * V * 16 + cap + 64;
+}
+
+template <int D>
+void launch_bnl_impl(const BnlArgs& a, uint32_t cap, uint32_t grid, uint32_t* win_pos, uint32_t* win_meta,
+                     uint32_t* counter, cudaStream_t st) {
+    const size_t smem = bnl_smem_bytes<D>(cap);
+    SKY_CUDA(cudaFuncSetAttribute(k_bnl<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bnl<D><<<grid, BNL_B, smem, st>>>(a, cap, win_pos, win_meta, counter);
+    SKY_LAUNCH_CHECK();
+}
+
+uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin) {
+    uint32_t cap = want;
+    SKY_DISPATCH_D(D, {
+        while (cap > 32 && bnl_smem_bytes<DT>(cap) + 1024 > (size_t)smem_optin) cap -= 32;
+    });
+    return cap;
+}
+
+void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint32_t* win_pos, uint32_t* win_meta,
+                     uint32_t* counter, cudaStream_t st) {
+    SKY_DISPATCH_D(D, (launch_bnl_impl<DT>(a, cap, grid, win_pos, win_meta, counter, st)));
+}
+
+}  // namespace sky

@@ -1,0 +1,118 @@
+// kernels.cuh — launch wrappers for the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace sky {
+
+// Internal dimensionality: d is padded with zero coordinates up to one of
+// the instantiated widths (zeros never change a dominance outcome).
+int padded_dim(uint32_t d);  // 0 if unsupported (d > 32)
+
+// Point set on the device in dominance-friendly layout: AoS coords with
+// stride round4(D) floats (16-byte aligned rows), plus the 32-bit sort key
+// (float32 image of the FP64 coordinate sum, monotone) and the input row id.
+struct DevSet {
+    float* xyz = nullptr;
+    uint32_t* skey = nullptr;
+    uint32_t* id = nullptr;
+    uint32_t n = 0;
+};
+
+struct PrepArgs {
+    const float* pts;
+    uint32_t n, d;
+    int strategy;
+    uint64_t m;
+    int normalized;
+    const uint32_t* pid_in;  // random: host-computed partition_of
+    uint32_t slice_dim;
+    uint64_t* key64;         // out: (pid << 32) | skey
+    uint32_t* idx;           // out: identity
+    uint32_t* slice_key;     // out (sliced): canonical bits of x[slice_dim]
+    uint32_t* err;           // out: error bits
+    uint32_t* amb_count;     // out (angular): boundary points
+    uint32_t* amb_list;
+    uint32_t amb_cap;
+};
+void launch_prep(const PrepArgs& a, cudaStream_t st);
+
+// Partition boundaries of a (pid << 32 | skey)-sorted key array: off[P+1].
+void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t* off, cudaStream_t st);
+
+// Patch pid bits of key64 for rows listed in (rows, pids).
+void launch_patch_pid(uint64_t* key64, const uint32_t* rows, const uint32_t* pids, uint32_t count,
+                      cudaStream_t st);
+
+// Sliced: pid of each row from its rank in the (x[k], lex, id) order.
+//   rank_idx: rows sorted by x[k] (ties by row id); run list: tie runs that
+//   straddle slice boundaries, resolved by exact lexicographic rank.
+void launch_slice_runs(const uint32_t* sorted_key, uint32_t n, uint64_t p, uint32_t* runs,
+                       uint32_t* run_count, uint32_t run_cap, cudaStream_t st);
+void launch_slice_assign(const uint32_t* rank_idx, uint32_t n, uint64_t p, uint64_t* key64,
+                         cudaStream_t st);
+void launch_slice_fix_runs(const float* pts, uint32_t d, const uint32_t* rank_idx, uint32_t n, uint64_t p,
+                           const uint32_t* runs, uint32_t n_runs, uint32_t max_len, uint64_t* key64,
+                           cudaStream_t st);
+void launch_gather_coord_key(const float* pts, uint32_t d, uint32_t j, const uint32_t* idx, uint32_t n,
+                             uint32_t* key, cudaStream_t st);
+
+// Exact top-q per partition under (FP64 sum, lex coords, id) (filter.cpp:66-86).
+void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
+                     const float* pts, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st);
+
+// Compaction plumbing.
+void launch_scatter_direct(int D, const DevSet& in, const uint8_t* dead, const uint32_t* pos, DevSet out,
+                           cudaStream_t st);
+void launch_scatter_indirect(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64,
+                             uint32_t n, const uint8_t* dead, const uint32_t* pos, DevSet out, cudaStream_t st);
+void launch_gather_rows(int D, const float* pts, uint32_t d, const uint32_t* rows, uint32_t n, DevSet out,
+                        const uint32_t* skey_src, cudaStream_t st);
+void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st);
+void launch_remap_offsets(const uint32_t* off_old, uint32_t P, const uint32_t* pos, const uint8_t* dead,
+                          uint32_t n, uint32_t* off_new, cudaStream_t st);
+void launch_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, uint32_t* total, cudaStream_t st);
+void launch_compact_ids(const uint32_t* id, const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t* out,
+                        cudaStream_t st);
+void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st);
+void launch_mark_cells_dead(const uint64_t* key64, uint32_t n, const uint8_t* cell_dead, uint8_t* dead,
+                            cudaStream_t st);
+
+// The dominance core: for each item, candidates [cb,ce) vs every comparator
+// range in ranges[lb,le). Sets dead[c] = 1 for each candidate dominated by
+// some comparator with skey <= the candidate tile's key bound.
+struct RelskyArgs {
+    // candidates: direct (AoS DevSet) or indirect (row-major pts via idx)
+    const float* cxyz;
+    const uint32_t* cskey;   // direct: skey[]; indirect: key64 viewed as u32 pairs
+    const uint32_t* cidx;    // indirect only
+    uint32_t cd;             // indirect only: row-major stride
+    bool indirect;
+    const float* sxyz;
+    const uint32_t* sskey;
+    const Item* items;
+    uint32_t n_items;
+    const uint2* ranges;
+    bool bounded;
+    uint8_t* dead;
+    unsigned long long* tests;
+};
+void launch_relsky(int D, const RelskyArgs& a, cudaStream_t st);
+
+// BNL local skylines: one CTA per partition segment, window capped at
+// `window` points in shared memory; partition input in scan order.
+struct BnlArgs {
+    const float* xyz;
+    const uint32_t* seg_off;  // [P+1]
+    uint32_t P;
+    uint32_t window;
+    uint8_t* dead;            // out: 1 = dominated within its partition
+    uint32_t* overflow;       // scratch: n entries
+    unsigned long long* tests;
+};
+// Largest window <= want whose shared-memory footprint fits smem_optin.
+uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin);
+void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint32_t* win_pos, uint32_t* win_meta,
+                     uint32_t* counter, cudaStream_t st);
+
+}  // namespace sky

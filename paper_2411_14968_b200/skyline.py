@@ -1,0 +1,361 @@
+"""Host-side mirror of the reference engine API (reference
+proj/include/skyline/{engine,partition,filter,core}.hpp) over the C ABI.
+
+Names, argument meanings and error behaviour follow the reference:
+
+    reference (C++)                          here
+    ---------------------------------------  ----------------------------------
+    skyline::Strategy        partition.hpp:14  Strategy
+    skyline::PartitionConfig partition.hpp:21  PartitionConfig
+    skyline::FilterKind      engine.hpp:19     FilterKind
+    skyline::RepSelection    filter.hpp:21     RepSelection
+    skyline::MergeKind       engine.hpp:25     MergeKind
+    skyline::EngineConfig    engine.hpp:30     EngineConfig (+ local_algo, bnl_window_cap)
+    skyline::PhaseMetrics    engine.hpp:40     PhaseMetrics
+    skyline::RunResult       engine.hpp:50     RunResult
+    skyline::run             engine.hpp:88     Engine.run / run
+    skyline::make_assignment partition.hpp:102 Engine.make_assignment
+    skyline::snap_slices     partition.hpp:99  snap_slices
+    skyline::relative_skyline core.hpp:79      Engine.relative_skyline
+    skyline::sfs             sequential.hpp:29 Engine.sfs
+    select_representatives_sorted filter.hpp:46 Engine.select_representatives_sorted
+    SkylineError hierarchy   core.hpp:13-34    SkylineError, ConfigError, ...
+
+Every call runs on the GPU through libskyline_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import abi
+
+
+# ----------------------------------------------------------------- errors
+class SkylineError(RuntimeError):
+    code = 12
+
+
+class ConfigError(SkylineError):
+    code = 1
+
+
+class DimensionError(SkylineError):
+    code = 2
+
+
+class NormalizationError(SkylineError):
+    code = 3
+
+
+class DataError(SkylineError):
+    code = 4
+
+
+class IoError(SkylineError):
+    code = 5
+
+
+class CudaError(SkylineError):
+    code = 10
+
+
+class NcclError(SkylineError):
+    code = 11
+
+
+_ERRORS = {1: ConfigError, 2: DimensionError, 3: NormalizationError, 4: DataError, 5: IoError,
+           10: CudaError, 11: NcclError, 12: SkylineError}
+
+
+def _raise(rc: int, msg: str = ""):
+    if rc != abi.SKY_OK:
+        raise _ERRORS.get(rc, SkylineError)(msg or abi.STATUS_NAMES.get(rc, str(rc)))
+
+
+# ------------------------------------------------------------------ enums
+class Strategy(enum.IntEnum):
+    Random = 0
+    Grid = 1
+    Angular = 2
+    Sliced = 3
+
+
+class FilterKind(enum.IntEnum):
+    None_ = 0
+    GridFilter = 1
+    Representative = 2
+
+
+class RepSelection(enum.IntEnum):
+    Sorted = 0
+    Region = 1
+    Random = 2
+
+
+class MergeKind(enum.IntEnum):
+    Sequential = 0
+    NoSeq = 1
+
+
+class LocalAlgo(enum.IntEnum):
+    SFS = 0
+    BNL = 1
+
+
+@dataclass
+class PartitionConfig:
+    strategy: Strategy = Strategy.Random
+    p: int = 1
+    m: int = 0
+    seed: int = 0
+    slice_dim: int = 0
+
+
+@dataclass
+class EngineConfig:
+    partition: PartitionConfig = field(default_factory=PartitionConfig)
+    filter: FilterKind = FilterKind.None_
+    rep_selection: RepSelection = RepSelection.Sorted
+    rep_q: int = 5
+    merge: MergeKind = MergeKind.Sequential
+    workers: int = 1
+    seed: int = 0
+    local_algo: LocalAlgo = LocalAlgo.SFS
+    bnl_window_cap: int = 4096
+    count_tests: bool = True
+
+    def to_c(self) -> abi.SkyConfig:
+        p = self.partition
+        return abi.SkyConfig.make(
+            strategy=int(p.strategy), p=int(p.p), m=int(p.m), seed=int(p.seed), slice_dim=int(p.slice_dim),
+            filter=int(self.filter), rep_selection=int(self.rep_selection), rep_q=int(self.rep_q),
+            merge=int(self.merge), workers=int(self.workers), local_algo=int(self.local_algo),
+            bnl_window_cap=int(self.bnl_window_cap), count_tests=int(bool(self.count_tests)))
+
+
+@dataclass
+class PhaseMetrics:
+    partition_ms: float = 0.0
+    local_ms: float = 0.0
+    merge_ms: float = 0.0
+    local_skyline_sizes: List[int] = field(default_factory=list)
+    union_size: int = 0
+    filtered_count: int = 0
+    final_size: int = 0
+    # B200 extensions
+    total_ms: float = 0.0
+    tests_reps: int = 0
+    tests_local: int = 0
+    tests_merge: int = 0
+    n_reps: int = 0
+    angular_host_fixups: int = 0
+    kernel_launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+    @property
+    def tests_total(self) -> int:
+        return self.tests_reps + self.tests_local + self.tests_merge
+
+
+@dataclass
+class RunResult:
+    skyline: np.ndarray  # int64 ids, ascending
+    metrics: PhaseMetrics
+    config: EngineConfig
+    effective_p: int
+    input_size: int
+    input_dim: int
+
+
+def snap_slices(target_p: int, k: int) -> int:
+    out = C.c_uint64(0)
+    _raise(abi.load().sky_snap_slices(target_p, k, C.byref(out)))
+    return int(out.value)
+
+
+def _as_points(points) -> np.ndarray:
+    a = np.ascontiguousarray(points, dtype=np.float32)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1) if a.size else a.reshape(0, 0)
+    if a.ndim != 2:
+        raise DimensionError("points must be a 2-D array (n x d)")
+    return a
+
+
+class Engine:
+    """One GPU context (device, stream, device arena). Not thread-safe: one
+    call in flight per Engine, as in the C ABI."""
+
+    def __init__(self, device: int = 0):
+        self._lib = abi.load()
+        h = C.c_void_p()
+        rc = self._lib.sky_ctx_create(device, C.byref(h))
+        _raise(rc, "sky_ctx_create failed (is a CUDA device visible?)")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sky_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _err(self, rc):
+        if rc != abi.SKY_OK:
+            msg = self._lib.sky_last_error(self._h)
+            _raise(rc, msg.decode() if msg else "")
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        self._lib.sky_ctx_set_stream(self._h, C.c_void_p(stream_ptr or 0))
+
+    # skyline::run (engine.hpp:88)
+    def run(self, points, config: EngineConfig, normalized: bool = True, *, device_ptr: Optional[int] = None,
+            n: Optional[int] = None, d: Optional[int] = None) -> RunResult:
+        """Run the engine. `points` is an (n, d) float32 host array, or pass
+        device_ptr/n/d for rows already resident on the GPU."""
+        cfg = config.to_c()
+        res = abi.SkyResult()
+        if device_ptr is not None:
+            rc = self._lib.sky_run(self._h, C.c_void_p(device_ptr), n, d, int(normalized), 1, C.byref(cfg),
+                                   C.byref(res))
+        else:
+            a = _as_points(points)
+            n, d = a.shape
+            rc = self._lib.sky_run(self._h, a.ctypes.data_as(C.c_void_p), n, d, int(normalized), 0,
+                                   C.byref(cfg), C.byref(res))
+        self._err(rc)
+        try:
+            ids = np.ctypeslib.as_array(res.ids, shape=(res.n_ids,)).copy() if res.n_ids else np.zeros(0, np.int64)
+            P = int(res.effective_p)
+            sizes = (np.ctypeslib.as_array(res.local_skyline_sizes, shape=(P,)).astype(np.int64).tolist()
+                     if P else [])
+            m = PhaseMetrics(
+                partition_ms=res.partition_ms, local_ms=res.local_ms, merge_ms=res.merge_ms,
+                local_skyline_sizes=sizes, union_size=int(res.union_size),
+                filtered_count=int(res.filtered_count), final_size=int(res.final_size),
+                total_ms=res.total_ms, tests_reps=int(res.tests_reps), tests_local=int(res.tests_local),
+                tests_merge=int(res.tests_merge), n_reps=int(res.n_reps),
+                angular_host_fixups=int(res.angular_host_fixups), kernel_launches=int(res.kernel_launches),
+                h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes))
+            return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
+        finally:
+            self._lib.sky_result_free(C.byref(res))
+
+    # skyline::make_assignment (partition.hpp:102)
+    def make_assignment(self, points, partition: PartitionConfig, normalized: bool = True):
+        a = _as_points(points)
+        n, d = a.shape
+        cfg = EngineConfig(partition=partition).to_c()
+        out = np.zeros(max(n, 1), np.uint64)
+        P = C.c_uint64(0)
+        rc = self._lib.sky_assign(self._h, a.ctypes.data_as(C.POINTER(C.c_float)), n, d, int(normalized),
+                                  C.byref(cfg), out.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(P))
+        self._err(rc)
+        return out[:n], int(P.value)
+
+    # skyline::relative_skyline (core.hpp:79): boolean keep mask over r
+    def relative_skyline(self, r, c):
+        ra = _as_points(r)
+        ca = _as_points(c)
+        d = ra.shape[1] if ra.size else (ca.shape[1] if ca.size else 0)
+        if ra.size and ca.size and ra.shape[1] != ca.shape[1]:
+            raise DimensionError("relative skyline over relations of unequal dimensionality")
+        keep = np.ones(max(len(ra), 1), np.uint8)
+        tests = C.c_uint64(0)
+        rc = self._lib.sky_relative_skyline(self._h, ra.ctypes.data_as(C.POINTER(C.c_float)), len(ra),
+                                            ca.ctypes.data_as(C.POINTER(C.c_float)), len(ca), d,
+                                            keep.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(tests))
+        self._err(rc)
+        return keep[: len(ra)].astype(bool)
+
+    # skyline::sfs / skyline_bruteforce: skyline ids ascending
+    def sfs(self, points) -> np.ndarray:
+        a = _as_points(points)
+        n, d = a.shape
+        ptr = C.POINTER(C.c_int64)()
+        k = C.c_uint64(0)
+        t = C.c_uint64(0)
+        rc = self._lib.sky_skyline(self._h, a.ctypes.data_as(C.POINTER(C.c_float)), n, d, C.byref(ptr),
+                                   C.byref(k), C.byref(t))
+        self._err(rc)
+        try:
+            return np.ctypeslib.as_array(ptr, shape=(k.value,)).copy() if k.value else np.zeros(0, np.int64)
+        finally:
+            self._lib.sky_free(ptr)
+
+    skyline = sfs
+
+    # select_representatives_sorted + prune_dominated_reps (filter.hpp:46,67)
+    def select_representatives_sorted(self, points, partition_of, p: int, q: int) -> np.ndarray:
+        a = _as_points(points)
+        n, d = a.shape
+        po = np.ascontiguousarray(partition_of, dtype=np.uint64)
+        ptr = C.POINTER(C.c_int64)()
+        k = C.c_uint64(0)
+        rc = self._lib.sky_representatives(self._h, a.ctypes.data_as(C.POINTER(C.c_float)), n, d,
+                                           po.ctypes.data_as(C.POINTER(C.c_uint64)), p, q, C.byref(ptr),
+                                           C.byref(k))
+        self._err(rc)
+        try:
+            return np.ctypeslib.as_array(ptr, shape=(k.value,)).copy() if k.value else np.zeros(0, np.int64)
+        finally:
+            self._lib.sky_free(ptr)
+
+
+_default: Optional[Engine] = None
+
+
+def default_engine() -> Engine:
+    global _default
+    if _default is None:
+        _default = Engine(0)
+    return _default
+
+
+def run(points, config: EngineConfig, normalized: bool = True) -> RunResult:
+    """skyline::run on the default GPU context."""
+    return default_engine().run(points, config, normalized)
+
+
+def generate(kind: int, n: int, d: int, seed: int) -> np.ndarray:
+    """Synthetic BASELINE inputs (host, deterministic): kind 1 uniform,
+    2/4 anti-correlated, 3 correlated, 5 integers in [0,16)."""
+    out = np.empty((n, d), np.float32)
+    rc = abi.load().sky_generate(kind, n, d, seed, out.ctypes.data_as(C.POINTER(C.c_float)))
+    _raise(rc)
+    return out
+
+
+def plan_lpt(weights, ranks: int) -> np.ndarray:
+    w = np.ascontiguousarray(weights, dtype=np.uint64)
+    owner = np.zeros(max(len(w), 1), np.int32)
+    _raise(abi.load().sky_plan_lpt(w.ctypes.data_as(C.POINTER(C.c_uint64)), len(w), ranks,
+                                   owner.ctypes.data_as(C.POINTER(C.c_int32))))
+    return owner[: len(w)]
+
+
+def plan_split(cost, ranks: int) -> np.ndarray:
+    c = np.ascontiguousarray(cost, dtype=np.uint64)
+    prefix = np.zeros(len(c) + 1, np.uint64)
+    np.cumsum(c, out=prefix[1:])
+    bounds = np.zeros(ranks + 1, np.uint64)
+    _raise(abi.load().sky_plan_split(prefix.ctypes.data_as(C.POINTER(C.c_uint64)), len(c), ranks,
+                                     bounds.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return bounds

@@ -1,0 +1,182 @@
+"""Generate the golden fixtures from the REFERENCE ITSELF.
+
+Runs the unmodified reference engine (oracle/_ref/libskyref.so, compiled in
+place from /root/reference by `make -C oracle ref`) on:
+  * the known-answer literals of the reference's own unit tests
+    (proj/tests/test_core.cpp, test_partition.cpp, test_filter.cpp,
+    test_sequential.cpp, test_engine.cpp), and
+  * the five BASELINE configs at reduced N on sky_generate inputs
+    (SHA-256 of the float32 input recorded),
+and writes tests/golden/golden.json + tests/golden/configs.npz.
+
+Usage (in the build container, where /root/reference exists):
+    python tests/golden/make_golden.py
+"""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle as O  # noqa: E402
+from paper_2411_14968_b200.abi import SkyConfig  # noqa: E402
+from paper_2411_14968_b200.configs import make_config  # noqa: E402
+from paper_2411_14968_b200.skyline import generate  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# reduced sizes: the single-threaded oracle must finish each in seconds
+REDUCED_N = {1: 100_000, 2: 100_000, 3: 1_000_000, 4: 40_000, 5: 500_000}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, np.float32).tobytes()).hexdigest()
+
+
+def known_answers():
+    L = []
+
+    def sky(rows, src):
+        x = np.array(rows, np.float32)
+        L.append({"kind": "skyline", "src": src, "points": x.tolist(),
+                  "expect": O.bruteforce(x, ref=True).tolist()})
+
+    sky([[1, 2], [2, 1], [2, 2]], "test_core.cpp:65-67")
+    sky([[3, 3]], "test_core.cpp:72-74")
+    sky([[1, 1], [1, 1], [2, 2]], "test_core.cpp:75-78")
+    sky([[0.5, 0.5], [0.5, 0.5]], "test_sequential.cpp:54-56")
+
+    def rel(r, c, src):
+        r = np.array(r, np.float32)
+        c = np.array(c, np.float32)
+        L.append({"kind": "relative", "src": src, "r": r.tolist(), "c": c.tolist(),
+                  "expect": O.relative_skyline(r, c, ref=True).astype(int).tolist()})
+
+    rel([[2, 2], [3, 1]], [[1, 1]], "test_core.cpp:83-86")
+    rel([[1, 2], [2, 1]], [[1, 2], [2, 1]], "test_core.cpp:91-94")
+    rel([[2, 2], [0.5, 3]], [[1, 1]], "test_filter.cpp:136-141")
+    rel([[2, 2], [1, 3]], [[2, 2], [1, 3]], "test_filter.cpp:147-153")
+
+    ref = O.ref_lib()
+    for pt, m, src in [([0.3, 0.7], 2, "test_partition.cpp:53"), ([0.0, 0.0], 2, "test_partition.cpp:54"),
+                       ([0.0, 0.0], 5, "test_partition.cpp:55"), ([1.0, 1.0], 2, "test_partition.cpp:56")]:
+        x = np.array(pt, np.float32)
+        L.append({"kind": "grid_index", "src": src, "x": x.tolist(), "m": m,
+                  "expect": int(ref.skyref_grid_index(x.ctypes.data_as(O._f32p), len(x), m))})
+    for pt, m, src in [([1, 1], 4, "test_partition.cpp:137"), ([1, 0], 4, "test_partition.cpp:138"),
+                       ([0, 1], 4, "test_partition.cpp:139")]:
+        x = np.array(pt, np.float32)
+        L.append({"kind": "angular_index", "src": src, "x": x.tolist(), "m": m,
+                  "expect": int(ref.skyref_angular_index(x.ctypes.data_as(O._f32p), len(x), m))})
+    for tp, k in [(16, 4), (120, 4), (120, 3), (120, 2), (120, 1), (1, 3), (64, 5), (256, 8)]:
+        L.append({"kind": "snap", "src": "test_partition.cpp:228-234", "p": tp, "k": k,
+                  "expect": int(ref.skyref_snap_slices(tp, k))})
+    # sliced rank formula on rows (i/100, 0.5)
+    x = np.array([[i / 100.0, 0.5] for i in range(100)], np.float32)
+    po, cnt = O.oracle_assign(x, SkyConfig.make(strategy=3, p=4), True, ref=True)
+    L.append({"kind": "assign", "src": "test_partition.cpp:153-162", "points": x.tolist(),
+              "cfg": {"strategy": 3, "p": 4}, "normalized": True, "expect": po.astype(int).tolist(),
+              "count": cnt})
+    # grid engine example (test_engine.cpp:140-149)
+    x = np.array([[0.1, 0.1], [0.6, 0.6], [0.7, 0.2], [0.2, 0.8]], np.float32)
+    for strat, p in [(1, 4), (0, 2), (2, 4), (3, 3)]:
+        for merge in (0, 1):
+            cfg = SkyConfig.make(strategy=strat, p=p, seed=3, merge=merge)
+            r = O.ref_run(x, cfg, True)
+            L.append({"kind": "run", "src": "test_engine.cpp:140-149", "points": x.tolist(), "normalized": True,
+                      "cfg": cfg.as_dict(), "expect": r["ids"].tolist(),
+                      "local_skyline_sizes": r["local_skyline_sizes"].astype(int).tolist()})
+    # reps (test_filter.cpp:68-85)
+    x = np.array([[1, 2], [2, 1], [3, 3]], np.float32)
+    L.append({"kind": "reps", "src": "test_filter.cpp:70-73", "points": x.tolist(), "partition_of": [0, 0, 0],
+              "p": 1, "q": 2, "expect": O.representatives(x, [0, 0, 0], 1, 2, ref=True).tolist()})
+    x = np.array([[1, 1], [2, 2]], np.float32)
+    L.append({"kind": "reps", "src": "test_filter.cpp:79-82", "points": x.tolist(), "partition_of": [0, 1],
+              "p": 2, "q": 1, "expect": O.representatives(x, [0, 1], 2, 1, ref=True).tolist()})
+    return L
+
+
+def lattice(n, d, levels, seed):
+    """test_support.hpp:46-60 style lattice data (ties and duplicates)."""
+    rng = np.random.default_rng(seed)
+    return (rng.integers(0, levels + 1, (n, d)) / levels).astype(np.float32)
+
+
+def plane():
+    """A slice of the reference's configuration plane (test_engine.cpp:16-46,
+    acceptance.cpp:54-114) on smooth and lattice data."""
+    out = []
+    arrays = {}
+    k = 0
+    for dist in ("uniform", "lattice", "ints"):
+        for d in (2, 3, 5, 8):
+            for n in (60, 700):
+                rng = np.random.default_rng(1000 + 10 * d + n)
+                if dist == "uniform":
+                    x = rng.random((n, d), dtype=np.float32)
+                elif dist == "lattice":
+                    x = lattice(n, d, 4, 2000 + d + n)
+                else:
+                    x = rng.integers(0, 6, (n, d)).astype(np.float32)
+                norm = dist != "ints"
+                for strat in (0, 1, 2, 3):
+                    if strat == 1 and not norm:
+                        continue
+                    filters = (0, 2, 1) if strat == 1 else (0, 2)
+                    for filt in filters:
+                        for merge in (0, 1):
+                            for q in ((3,) if filt == 2 else (5,)):
+                                cfg = SkyConfig.make(strategy=strat, p=7, seed=11, slice_dim=d - 1, filter=filt,
+                                                     rep_q=q, merge=merge, workers=4)
+                                r = O.ref_run(x, cfg, norm)
+                                key = f"plane{k}"
+                                arrays[key + "_x"] = x
+                                arrays[key + "_ids"] = r["ids"]
+                                arrays[key + "_lss"] = r["local_skyline_sizes"].astype(np.int64)
+                                out.append({"key": key, "dist": dist, "n": n, "d": d, "normalized": norm,
+                                            "cfg": cfg.as_dict(), "effective_p": r["effective_p"],
+                                            "union_size": r["union_size"], "filtered_count": r["filtered_count"],
+                                            "final_size": r["final_size"]})
+                                k += 1
+    return out, arrays
+
+
+def configs():
+    out = []
+    arrays = {}
+    for i in range(1, 6):
+        w = make_config(i, REDUCED_N[i])
+        x = generate(w.kind, w.n, w.d, 42)
+        cfg = w.config.to_c()
+        cfg.workers = 8
+        r = O.ref_run(x, cfg, w.normalized)
+        arrays[f"c{i}_ids"] = r["ids"]
+        arrays[f"c{i}_lss"] = r["local_skyline_sizes"].astype(np.int64)
+        out.append({"config": i, "name": w.name, "n": w.n, "d": w.d, "kind": w.kind, "seed": 42,
+                    "normalized": w.normalized, "sha256": sha(x), "cfg": cfg.as_dict(),
+                    "effective_p": r["effective_p"], "union_size": r["union_size"],
+                    "filtered_count": r["filtered_count"], "final_size": r["final_size"],
+                    "ref_run_ms": r["run_ms"]})
+        print(w.name, r["final_size"], r["union_size"], r["filtered_count"], f"{r['run_ms']:.0f} ms", flush=True)
+    return out, arrays
+
+
+def main():
+    O.build(ref=True)
+    ka = known_answers()
+    pl, pl_arr = plane()
+    cf, cf_arr = configs()
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump({"generator": "tests/golden/make_golden.py", "source": "oracle/_ref/libskyref.so "
+                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "configs": cf}, f)
+    np.savez_compressed(os.path.join(HERE, "plane.npz"), **pl_arr)
+    np.savez_compressed(os.path.join(HERE, "configs.npz"), **cf_arr)
+    print(len(ka), "known answers;", len(pl), "plane cases;", len(cf), "configs")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the reference
+goldens and the oracle. Integer/index work, so every check is bit-exact:
+skyline id sets, effective_p, union_size, filtered_count, final_size and
+local_skyline_sizes."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2411_14968_b200 import (ConfigError, DataError, DimensionError, EngineConfig, FilterKind, LocalAlgo,
+                                   MergeKind, NormalizationError, PartitionConfig, Strategy, generate)
+from paper_2411_14968_b200.abi import SkyConfig
+from paper_2411_14968_b200.configs import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+def to_engine_config(d):
+    return EngineConfig(partition=PartitionConfig(Strategy(d["strategy"]), d["p"], d["m"], d["seed"], d["slice_dim"]),
+                        filter=FilterKind(d["filter"]), rep_q=d["rep_q"], merge=MergeKind(d["merge"]),
+                        workers=max(1, d["workers"]), local_algo=LocalAlgo(d.get("local_algo", 0)),
+                        bnl_window_cap=d.get("bnl_window_cap", 4096) or 4096)
+
+
+def check_metrics(res, exp, tag):
+    m = res.metrics
+    assert res.effective_p == exp["effective_p"], tag
+    assert m.union_size == exp["union_size"], (tag, m.union_size, exp["union_size"])
+    assert m.filtered_count == exp["filtered_count"], (tag, m.filtered_count, exp["filtered_count"])
+    assert m.final_size == exp["final_size"], tag
+
+
+def test_known_answers(engine, golden):
+    for ka in golden["known_answers"]:
+        k = ka["kind"]
+        if k == "skyline":
+            got = engine.sfs(np.array(ka["points"], np.float32)).tolist()
+        elif k == "relative":
+            got = engine.relative_skyline(np.array(ka["r"], np.float32), np.array(ka["c"], np.float32)).astype(int).tolist()
+        elif k in ("grid_index", "angular_index"):
+            x = np.array([ka["x"]], np.float32)
+            strat = Strategy.Grid if k == "grid_index" else Strategy.Angular
+            po, _ = engine.make_assignment(x, PartitionConfig(strat, p=1, m=ka["m"]))
+            got = int(po[0])
+        elif k == "snap":
+            from paper_2411_14968_b200 import snap_slices
+            got = snap_slices(ka["p"], ka["k"])
+        elif k == "assign":
+            c = ka["cfg"]
+            po, cnt = engine.make_assignment(np.array(ka["points"], np.float32),
+                                             PartitionConfig(Strategy(c["strategy"]), p=c["p"]), ka["normalized"])
+            got = po.astype(int).tolist()
+            assert cnt == ka["count"]
+        elif k == "run":
+            r = engine.run(np.array(ka["points"], np.float32), to_engine_config(ka["cfg"]), ka["normalized"])
+            got = r.skyline.tolist()
+            assert r.metrics.local_skyline_sizes == ka["local_skyline_sizes"], ka["src"]
+        elif k == "reps":
+            got = engine.select_representatives_sorted(np.array(ka["points"], np.float32), ka["partition_of"],
+                                                       ka["p"], ka["q"]).tolist()
+        else:
+            raise AssertionError(k)
+        assert got == ka["expect"], (ka["src"], got, ka["expect"])
+
+
+@pytest.mark.parametrize("local_algo", [LocalAlgo.SFS, LocalAlgo.BNL])
+def test_plane_matches_reference(engine, golden, local_algo):
+    arr = golden["plane_arrays"]
+    for case in golden["plane"]:
+        key = case["key"]
+        cfg = to_engine_config(case["cfg"])
+        cfg.local_algo = local_algo
+        cfg.bnl_window_cap = 64  # small window: forces overflow passes
+        r = engine.run(arr[key + "_x"], cfg, case["normalized"])
+        assert np.array_equal(r.skyline, arr[key + "_ids"]), key
+        assert r.metrics.local_skyline_sizes == arr[key + "_lss"].tolist(), key
+        check_metrics(r, case, key)
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4, 5])
+def test_baseline_configs_reduced(engine, golden, cfg_idx):
+    c = [c for c in golden["configs"] if c["config"] == cfg_idx][0]
+    arr = golden["config_arrays"]
+    x = generate(c["kind"], c["n"], c["d"], c["seed"])
+    assert hashlib.sha256(x.tobytes()).hexdigest() == c["sha256"]
+    w = make_config(cfg_idx)
+    for algo in (w.config.local_algo, LocalAlgo.SFS if w.config.local_algo == LocalAlgo.BNL else LocalAlgo.BNL):
+        w.config.local_algo = algo
+        r = engine.run(x, w.config, c["normalized"])
+        assert np.array_equal(r.skyline, arr[f"c{cfg_idx}_ids"]), (cfg_idx, algo)
+        assert r.metrics.local_skyline_sizes == arr[f"c{cfg_idx}_lss"].tolist(), (cfg_idx, algo)
+        check_metrics(r, c, cfg_idx)
+
+
+def test_random_configs_vs_oracle(engine):
+    rng = np.random.default_rng(11)
+    for it in range(120):
+        d = int(rng.integers(1, 13))
+        n = int(rng.integers(0, 3000))
+        kind = it % 4
+        if kind == 0:
+            x = rng.random((n, d), dtype=np.float32)
+        elif kind == 1:
+            x = (rng.integers(0, 5, (n, d)) / 4).astype(np.float32)
+        elif kind == 2:
+            x = rng.integers(0, 7, (n, d)).astype(np.float32)
+        else:
+            x = generate(2, max(n, 1), d, it)[:n] if d > 1 else rng.random((n, d), dtype=np.float32)
+        norm = kind != 2
+        strat = int(rng.integers(0, 4))
+        filt = int(rng.choice([0, 2] + ([1] if strat == 1 else [])))
+        cfg = SkyConfig.make(strategy=strat, p=int(rng.integers(1, 40)), seed=int(rng.integers(0, 1000)),
+                             slice_dim=int(rng.integers(0, d)), filter=filt, rep_q=int(rng.integers(1, 9)),
+                             merge=int(rng.integers(0, 2)), workers=1)
+        ecfg = to_engine_config(cfg.as_dict())
+        ecfg.local_algo = LocalAlgo(it % 2)
+        ecfg.bnl_window_cap = int(rng.choice([32, 256, 4096]))
+        try:
+            exp = O.oracle_run(x, cfg, norm)
+        except O.CpuError as e:
+            with pytest.raises(Exception) as ei:
+                engine.run(x, ecfg, norm)
+            assert getattr(ei.value, "code", None) == e.code, (it, e.code, ei.value)
+            continue
+        r = engine.run(x, ecfg, norm)
+        tag = (it, n, d, strat, filt, cfg.merge, ecfg.local_algo)
+        assert np.array_equal(r.skyline, exp["ids"]), tag
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+        check_metrics(r, exp, tag)
+
+
+def test_skyline_and_relative_vs_oracle(engine):
+    rng = np.random.default_rng(5)
+    for it in range(30):
+        d = int(rng.integers(1, 11))
+        x = (rng.integers(0, 6, (int(rng.integers(1, 5000)), d)) / 5).astype(np.float32) if it % 2 else \
+            rng.random((int(rng.integers(1, 5000)), d), dtype=np.float32)
+        assert np.array_equal(engine.sfs(x), O.bruteforce(x) if len(x) < 1500 else O.oracle_run(
+            x, SkyConfig.make(strategy=3, p=1), True)["ids"])
+        c = x[rng.integers(0, len(x), int(rng.integers(1, 300)))] * np.float32(0.9)
+        assert np.array_equal(engine.relative_skyline(x, c), O.relative_skyline(x, c))
+
+
+def test_edge_cases(engine):
+    cfg = EngineConfig(partition=PartitionConfig(Strategy.Sliced, p=4))
+    r = engine.run(np.zeros((0, 3), np.float32), cfg)
+    assert r.skyline.size == 0 and r.effective_p == 4
+    one = np.array([[0.5, 0.5]], np.float32)
+    for s in (Strategy.Random, Strategy.Grid, Strategy.Sliced, Strategy.Angular):
+        assert engine.run(one, EngineConfig(partition=PartitionConfig(s, p=3))).skyline.tolist() == [0]
+    dup = np.ones((1000, 4), np.float32) * 0.25
+    assert engine.run(dup, EngineConfig(partition=PartitionConfig(Strategy.Random, p=7),
+                                        filter=FilterKind.Representative, merge=MergeKind.NoSeq)).skyline.size == 1000
+    # errors (engine.cpp:19-32, core.cpp:21-46, partition.cpp:26-29)
+    x = np.random.default_rng(0).random((10, 2), dtype=np.float32)
+    with pytest.raises(ConfigError):
+        engine.run(x, EngineConfig(workers=0))
+    with pytest.raises(ConfigError):
+        engine.run(x, EngineConfig(partition=PartitionConfig(p=0)))
+    with pytest.raises(ConfigError):
+        engine.run(x, EngineConfig(partition=PartitionConfig(Strategy.Sliced), filter=FilterKind.GridFilter))
+    with pytest.raises(ConfigError):
+        engine.run(x, EngineConfig(filter=FilterKind.Representative, rep_q=0))
+    with pytest.raises(DimensionError):
+        engine.run(x[:, :1], EngineConfig(partition=PartitionConfig(Strategy.Angular)))
+    with pytest.raises(NormalizationError):
+        engine.run(np.array([[3.0, 1.0], [0.5, 2.0]], np.float32), EngineConfig(partition=PartitionConfig(Strategy.Grid)),
+                   normalized=False)
+    with pytest.raises(DataError):
+        engine.run(np.array([[-1.0, 1.0]], np.float32), EngineConfig())
+    with pytest.raises(DataError):
+        engine.run(np.array([[np.nan, 1.0]], np.float32), EngineConfig())
+    with pytest.raises(DataError):
+        engine.run(np.array([[0.5, 1.5]], np.float32), EngineConfig(), normalized=True)
+
+
+def _dominated_by_any(x, t):
+    return bool(np.any(np.all(x <= t, axis=1) & np.any(x < t, axis=1)))
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4, 5])
+def test_full_size_properties(engine, cfg_idx):
+    """BASELINE sizes: output is sorted, unique, an antichain on a sample, no
+    sampled output row is dominated by any input row, and sampled
+    non-output rows are dominated by some output row."""
+    w = make_config(cfg_idx)
+    x = generate(w.kind, w.n, w.d, 42)
+    r = engine.run(x, w.config, w.normalized)
+    ids = r.skyline
+    assert ids.size > 0 and np.all(np.diff(ids) > 0)
+    assert r.metrics.final_size == ids.size <= r.metrics.union_size
+    assert r.metrics.union_size == sum(r.metrics.local_skyline_sizes)
+    assert r.metrics.union_size <= w.n - r.metrics.filtered_count
+    rng = np.random.default_rng(cfg_idx)
+    sky = x[ids]
+    for t in rng.choice(ids, min(25, ids.size), replace=False):
+        assert not _dominated_by_any(x, x[t]), t
+    mask = np.ones(w.n, bool)
+    mask[ids] = False
+    others = np.flatnonzero(mask)
+    for t in rng.choice(others, min(200, others.size), replace=False):
+        assert _dominated_by_any(sky, x[t]), t
+    # determinism (workers-invariance analogue, test_engine.cpp:246-258)
+    r2 = engine.run(x, w.config, w.normalized)
+    assert np.array_equal(r2.skyline, ids)
+    assert r2.metrics.local_skyline_sizes == r.metrics.local_skyline_sizes
+
+
+def test_full_c1_vs_oracle(engine):
+    w = make_config(1)
+    x = generate(w.kind, w.n, w.d, 42)
+    exp = O.oracle_run(x, w.config.to_c(), w.normalized)
+    r = engine.run(x, w.config, w.normalized)
+    assert np.array_equal(r.skyline, exp["ids"])
+    assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist()
+    check_metrics(r, exp, "c1")
