@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark: skyline input points/s (+ dominance tests/s) on B200 vs the
+reference CPU engine.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A step is one complete skyline query (sky_run: partition -> representatives
+-> local skylines -> merge -> ascending ids on the host) over the config's
+synthetic input. Default workload: BASELINE configs[1] (anti-correlated
+N=1M d=6, angular 64->32, q=8, NoSeq). Inputs (24 MB) fit in L2, so a
+512 MiB buffer is written between timed steps (L2 flush), outside the
+timed region.
+
+`value` is device-resident (inputs already in HBM); `e2e` goes through the
+public API with pinned host buffers (H2D of the rows and D2H of the ids
+inside the timed region). Multi-GPU: one process per GPU under torchrun;
+timing is the max over ranks of CUDA-event time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "skyline input points/sec + dominance tests/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "input points/s"
+COMPARES_PER_CLK_PER_SM = 64  # FP32 compare issue (CUDA C++ guide throughput table)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE config 1..5 (default 2 = configs[1])")
+    ap.add_argument("--n", type=int, default=None, help="override N (parity/debug only)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
+                 str(self.device), "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_run(x, w, workers: int):
+    """One run of the reference engine (oracle/_ref) or, if it was not built,
+    the C restatement (oracle), on the host cores. Returns (seconds, kind)."""
+    import oracle
+    cfg = w.config.to_c()
+    cfg.workers = workers
+    if oracle.ref_available():
+        r = oracle.ref_run(x, cfg, w.normalized)
+        return r["run_ms"] / 1e3, "reference", r
+    t0 = time.perf_counter()
+    r = oracle.oracle_run(x, cfg, w.normalized)
+    return time.perf_counter() - t0, "port", r
+
+
+def run_reference_arm(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2411_14968_b200.configs import make_config
+    from paper_2411_14968_b200.skyline import generate
+    w = make_config(args.config, args.n)
+    x = generate(w.kind, w.n, w.d, 42)
+    cores = os.cpu_count() or 1
+    if oracle.ref_available():
+        cores = oracle.ref_lib().skyref_hardware_concurrency()
+    times = []
+    kind = None
+    for i in range(args.warmup + args.steps):
+        t, kind, r = cpu_reference_run(x, w, cores)
+        if i >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = w.n * len(times) / total
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (sky_generate, seed 42)",
+        "config": {"workload": w.name, "n": w.n, "d": w.d, "description": w.description},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"full workload (N={w.n}), {len(times)} timed runs of skyline::run"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "skyline_size": int(r["final_size"]),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_14968_b200 import Engine
+    from paper_2411_14968_b200.configs import make_config
+    from paper_2411_14968_b200.skyline import generate
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = make_config(args.config, args.n)
+    x = generate(w.kind, w.n, w.d, 42)
+    x_pin = torch.from_numpy(x).pin_memory()
+    x_host = x_pin.numpy()  # pinned view
+    x_dev = x_pin.to(f"cuda:{local}")
+    eng = Engine(local)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    n, d = x.shape
+
+    def step_dev():
+        return eng.run(None, w.config, w.normalized, device_ptr=x_dev.data_ptr(), n=n, d=d)
+
+    def step_e2e():
+        return eng.run(x_host, w.config, w.normalized)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        r = step_dev()
+    if not args.no_e2e:
+        step_e2e()
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        ms = []
+        res = []
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)  # > L2: evicts the previous step's lines
+            torch.cuda.synchronize()
+            barrier()
+            ev0.record(stream)
+            res.append(fn())
+            ev1.record(stream)
+            ev1.synchronize()
+            ms.append(ev0.elapsed_time(ev1))
+            barrier()
+        torch.cuda.synchronize()
+        return ms, res
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    dev_ms, dev_res = timed(step_dev)
+    e2e_ms, e2e_res = (None, None) if args.no_e2e else timed(step_e2e)
+    clk = clocks.stop()
+
+    total_dev = sum(dev_ms)
+    total_e2e = sum(e2e_ms) if e2e_ms else None
+    if world > 1:
+        t = torch.tensor([total_dev, total_e2e or 0.0], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_dev, total_e2e = float(t[0]), (float(t[1]) if total_e2e is not None else None)
+
+    # every rank runs the whole query (multi-GPU sharding of the query is
+    # not in this build: N GPUs are N independent replicas)
+    jobs = world
+    r = dev_res[-1]
+    m = r.metrics
+    for rr in dev_res:
+        assert np.array_equal(rr.skyline, r.skyline), "non-deterministic skyline across steps"
+    value = w.n * args.steps * jobs / (total_dev / 1e3)
+    tests_per_step = statistics.mean(rr.metrics.tests_total for rr in dev_res)
+    dom_ms = statistics.mean(rr.metrics.dom_kernel_ms for rr in dev_res)
+    dom_tests = statistics.mean(rr.metrics.dom_tests for rr in dev_res)
+    launches = sum(rr.metrics.kernel_launches for rr in dev_res)
+
+    peaks = measured_peaks()
+    props = torch.cuda.get_device_properties(local)
+    n_sm = props.multi_processor_count
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    achieved = dom_tests * d / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0  # Gcompares/s
+    peak = n_sm * COMPARES_PER_CLK_PER_SM * sm_max * 1e6 / 1e9
+    roofline = {
+        "bound": "alu", "kernel": "k_relsky + k_bnl (dominance tests)", "achieved": achieved, "peak": peak,
+        "unit": "Gcompare/s", "frac": achieved / peak if peak else None, "traffic": None,
+        "algorithmic_unit": f"1 dominance test = d = {d} FP32 compares",
+        "peak_source": f"{n_sm} SM x {COMPARES_PER_CLK_PER_SM} FP32 compare/clk x sm_max_mhz {sm_max} "
+                       f"(MEASURED_PEAKS.json); ALU compare issue, no HBM/tensor term",
+        "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / statistics.mean(dev_ms),
+        "tests_per_step": dom_tests,
+    }
+
+    line = {
+        "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": total_dev / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (sky_generate, seed 42)",
+        "config": {"workload": w.name, "n": w.n, "d": w.d, "description": w.description,
+                   "effective_p": r.effective_p, "l2": "512 MiB buffer written between timed steps",
+                   "parallelism": "replicas" if world > 1 else "single-gpu"},
+        "tests_per_s": tests_per_step * args.steps * jobs / (total_dev / 1e3),
+        "skyline_size": int(r.skyline.size), "union_size": m.union_size, "filtered_count": m.filtered_count,
+        "phase_ms": {"partition": m.partition_ms, "local": m.local_ms, "merge": m.merge_ms},
+        "roofline": roofline,
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    if total_e2e is not None:
+        e0 = e2e_res[-1]
+        assert np.array_equal(e0.skyline, r.skyline)
+        line["e2e"] = {"value": w.n * args.steps * jobs / (total_e2e / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": int(e0.metrics.h2d_bytes), "d2h_bytes_per_step": int(e0.metrics.d2h_bytes),
+                       "ms_per_step": total_e2e / args.steps}
+    if rank == 0 and not args.no_cpu_baseline:
+        t, kind, rr = cpu_reference_run(x, w, os.cpu_count() or 1)
+        cores = os.cpu_count() or 1
+        if kind == "reference":
+            import oracle
+            cores = oracle.ref_lib().skyref_hardware_concurrency()
+        assert np.array_equal(rr["ids"], r.skyline), "GPU skyline differs from the CPU reference"
+        line["cpu_baseline"] = {"value": w.n / t, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": f"full workload (N={w.n}), 1 run of skyline::run, workers={cores}",
+                                "ms": t * 1e3, "parity": "ids identical"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -106,6 +106,9 @@ typedef struct sky_result {
     uint64_t angular_host_fixups; /* points whose angular slice sat on a boundary */
     uint64_t h2d_bytes, d2h_bytes;
     uint32_t kernel_launches;   /* kernels this library launched for the run */
+    uint32_t dom_launches;      /* dominance-kernel (k_relsky/k_bnl) launches */
+    double dom_kernel_ms;       /* summed CUDA-event time of those launches */
+    uint64_t dom_tests;         /* dominance tests they executed */
 } sky_result;
 
 typedef struct sky_ctx sky_ctx;

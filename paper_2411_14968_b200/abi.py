@@ -72,6 +72,9 @@ class SkyResult(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint32),
+        ("dom_launches", C.c_uint32),
+        ("dom_kernel_ms", C.c_double),
+        ("dom_tests", C.c_uint64),
     ]
 
 

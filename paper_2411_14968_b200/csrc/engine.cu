@@ -40,7 +40,10 @@ struct sky_ctx {
     int sm_count = 148;
     int smem_optin = 0;
     cudaEvent_t ev[6] = {};
+    cudaEvent_t dom_ev[2] = {};
     uint32_t launches = 0;
+    uint32_t dom_launches = 0;
+    double dom_ms = 0.0;
 };
 
 namespace {
@@ -261,11 +264,23 @@ class Runner {
         a.items = di;
         a.ranges = dr;
         a.n_items = (uint32_t)plan.items.size();
+        SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
         launch_relsky(D, a, st_);
+        SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));
         count();
+        dom_done();
         // the pinned staging buffers are reused by the next call: make sure
         // the copies have consumed them first
         sync();
+    }
+
+    // accumulate the CUDA-event time of the dominance launch just issued
+    void dom_done() {
+        SKY_CUDA(cudaEventSynchronize(c_->dom_ev[1]));
+        float ms = 0.f;
+        SKY_CUDA(cudaEventElapsedTime(&ms, c_->dom_ev[0], c_->dom_ev[1]));
+        c_->dom_ms += ms;
+        c_->dom_launches += 1;
     }
 
     unsigned long long* tests(int k) {
@@ -335,8 +350,11 @@ class Runner {
         b.overflow = ovf;
         b.tests = count_tests ? tests(1) : nullptr;
         if (s0.n) {
+            SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
             launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
+            SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));
             count();
+            dom_done();
         }
         return compact(s0, dead, off0_dev, P, S_SET2, off_u_dev, off_u, D);
     }
@@ -552,6 +570,8 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     out->input_dim = d;
     out->local_skyline_sizes = static_cast<uint64_t*>(std::calloc(P ? P : 1, sizeof(uint64_t)));
     c->launches = 0;
+    c->dom_launches = 0;
+    c->dom_ms = 0.0;
     const bool count_tests = cfg->count_tests != 0;
 
     if (n == 0 || d == 0) {
@@ -844,6 +864,9 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
     out->total_ms = ms;
     out->kernel_launches = c->launches;
+    out->dom_launches = c->dom_launches;
+    out->dom_kernel_ms = c->dom_ms;
+    out->dom_tests = ht[0] + ht[1] + ht[2];
 }
 
 template <class F>
@@ -895,6 +918,7 @@ int sky_ctx_create(int device, sky_ctx** out) {
         SKY_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         SKY_CUDA(cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         for (auto& e : c->ev) SKY_CUDA(cudaEventCreate(&e));
+        for (auto& e : c->dom_ev) SKY_CUDA(cudaEventCreate(&e));
     });
     if (rc != SKY_OK) {
         static thread_local std::string last;
@@ -911,6 +935,8 @@ void sky_ctx_destroy(sky_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->dom_ev)
         if (e) cudaEventDestroy(e);
     c->dev.release();
     if (c->own) cudaStreamDestroy(c->own);

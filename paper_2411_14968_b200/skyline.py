@@ -157,6 +157,9 @@ class PhaseMetrics:
     kernel_launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    dom_launches: int = 0
+    dom_kernel_ms: float = 0.0
+    dom_tests: int = 0
 
     @property
     def tests_total(self) -> int:
@@ -253,7 +256,9 @@ class Engine:
                 total_ms=res.total_ms, tests_reps=int(res.tests_reps), tests_local=int(res.tests_local),
                 tests_merge=int(res.tests_merge), n_reps=int(res.n_reps),
                 angular_host_fixups=int(res.angular_host_fixups), kernel_launches=int(res.kernel_launches),
-                h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes))
+                h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
+                dom_launches=int(res.dom_launches), dom_kernel_ms=float(res.dom_kernel_ms),
+                dom_tests=int(res.dom_tests))
             return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
         finally:
             self._lib.sky_result_free(C.byref(res))
