@@ -51,9 +51,10 @@ namespace {
 enum Slot {
     S_PTS, S_KEY_A, S_KEY_B, S_IDX_A, S_IDX_B, S_SK_A, S_SK_B, S_PID, S_MISC, S_AMB, S_OFF_A, S_OFF_B,
     S_DEAD, S_POS, S_CUB, S_ITEMS, S_RANGES, S_REPCAND, S_REPROWS, S_RUNS,
-    S_SET0, S_SET0_K, S_SET0_I, S_SET1, S_SET1_K, S_SET1_I, S_SET2, S_SET2_K, S_SET2_I,
-    S_SET3, S_SET3_K, S_SET3_I, S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
-    S_OVF, S_SKTMP, S_COUNT
+    S_SET0, S_SET0_K, S_SET0_I, S_SET0_Q, S_SET1, S_SET1_K, S_SET1_I, S_SET1_Q,
+    S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
+    S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
+    S_OVF, S_SKTMP, S_THR, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -63,7 +64,8 @@ constexpr uint32_t kChunk = 8192;   // comparators per relsky item before boundi
 constexpr uint32_t kBlock = 512;    // local block-skyline size
 
 // misc device words
-enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_TESTS = 8 /* 4 x u64 */ };
+enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_TESTS = 8 /* 4 x u64 */,
+       M_HITS = 16 /* u64 */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;
@@ -124,6 +126,7 @@ uint64_t angular_index_host(const float* x, uint32_t d, uint64_t m) {
 }
 
 struct Plan {
+    uint32_t tile = kTile;  // candidates per item
     std::vector<Item> items;
     std::vector<uint2> ranges;
     std::vector<uint32_t> group;  // item wave (comparator chunk index)
@@ -191,8 +194,19 @@ class Runner {
         s.xyz = dev<float>(base, (size_t)n * D4);
         s.skey = dev<uint32_t>(base + 1, n);
         s.id = dev<uint32_t>(base + 2, n);
+        if (D <= 16) s.qc = dev<uint2>(base + 3, n);
         s.n = n;
         return s;
+    }
+
+    // Packed monotone codes for a set whose comparators and candidates share
+    // one quantization (thresholds from a sample of `s`).
+    void encode(int D, DevSet& s) {
+        if (D > 16 || !s.n) return;
+        float* thr = dev<float>(S_THR, (size_t)D * (kCodeLevels - 1));
+        launch_thresholds(D, s, thr, st_);
+        launch_encode(D, s, thr, st_);
+        count(2);
     }
 
     template <class K, class V>
@@ -250,7 +264,8 @@ class Runner {
         return out;
     }
 
-    void relsky(int D, const Plan& plan, const RelskyArgs& base) {
+    void relsky(int D, const Plan& plan, const RelskyArgs& base, const uint2* cq = nullptr,
+                const uint2* sq = nullptr) {
         if (plan.items.empty()) return;
         Item* hi = pin<Item>(P_ITEMS, plan.items.size());
         uint2* hr = pin<uint2>(P_RANGES, plan.ranges.size());
@@ -265,7 +280,20 @@ class Runner {
         a.ranges = dr;
         a.n_items = (uint32_t)plan.items.size();
         SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
-        launch_relsky(D, a, st_);
+        if (D <= 16 && cq && sq && !a.indirect) {
+            uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+            SKY_CUDA(cudaMemsetAsync(misc + M_WORK, 0, sizeof(uint32_t), st_));
+            Relsky2Args b{};
+            b.cxyz = a.cxyz; b.cskey = a.cskey; b.cqc = cq;
+            b.sxyz = a.sxyz; b.sskey = a.sskey; b.sqc = sq;
+            b.items = di; b.n_items = a.n_items; b.ranges = dr; b.bounded = a.bounded; b.dead = a.dead;
+            b.tests = a.tests; b.counter = misc + M_WORK;
+            b.coarse_hits = reinterpret_cast<unsigned long long*>(misc + M_HITS);
+            launch_relsky2(D, (int)plan.tile, b, c_->sm_count, st_);
+        } else {
+            if (plan.tile != (uint32_t)kTile) throw Error(SKY_E_INTERNAL, "v1 relsky needs 512-candidate tiles");
+            launch_relsky(D, a, st_);
+        }
         SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));
         count();
         dom_done();
@@ -281,6 +309,13 @@ class Runner {
         SKY_CUDA(cudaEventElapsedTime(&ms, c_->dom_ev[0], c_->dom_ev[1]));
         c_->dom_ms += ms;
         c_->dom_launches += 1;
+    }
+
+    // candidates per relsky item: big tiles amortize comparator staging,
+    // small ones keep enough items in flight on 148 SMs
+    uint32_t pick_tile(int D, uint64_t n_cands) const {
+        if (D > 16) return kTile;
+        return n_cands >= (uint64_t)c_->sm_count * 4 * 1024 ? 1024u : (uint32_t)kTile;
     }
 
     unsigned long long* tests(int k) {
@@ -307,7 +342,7 @@ class Runner {
         a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
         a.sxyz = s0.xyz; a.sskey = s0.skey; a.bounded = true; a.dead = dead;
         a.tests = count_tests ? tests(1) : nullptr;
-        relsky(D, blocks, a);
+        relsky(D, blocks, a, s0.qc, s0.qc);
         std::vector<uint32_t> off1;
         uint32_t* off1_dev = dev<uint32_t>(S_OFF_B, P + 1);
         DevSet s1 = compact(s0, dead, off0_dev, P, S_SET1, off1_dev, off1, D);
@@ -315,16 +350,17 @@ class Runner {
         uint8_t* dead1 = dev<uint8_t>(S_DEAD, s1.n);
         launch_fill_u8(dead1, 0, s1.n, st_);
         Plan loc;
+        loc.tile = pick_tile(D, s1.n);
         for (uint32_t p = 0; p < P; ++p) {
             const uint32_t b0 = off1[p], e0 = off1[p + 1];
-            for (uint32_t b = b0; b < e0; b += kTile) {
-                const uint32_t e = std::min(b + (uint32_t)kTile, e0);
+            for (uint32_t b = b0; b < e0; b += loc.tile) {
+                const uint32_t e = std::min(b + loc.tile, e0);
                 loc.add(b, e, {make_uint2(b0, e0)});
             }
         }
         loc.order();
         a.cxyz = s1.xyz; a.cskey = s1.skey; a.sxyz = s1.xyz; a.sskey = s1.skey; a.dead = dead1;
-        relsky(D, loc, a);
+        relsky(D, loc, a, s1.qc, s1.qc);
         return compact(s1, dead1, off1_dev, P, S_SET2, off_u_dev, off_u, D);
     }
 
@@ -748,6 +784,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
                                 s0, st);
         R.count();
         rep_filtered = (uint64_t)n - total - grid_filtered;
+        R.encode(D, s0);
     }
     out->filtered_count = grid_filtered + rep_filtered;
 
@@ -772,6 +809,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     ma.cxyz = U.xyz; ma.cskey = U.skey; ma.bounded = true; ma.dead = fdead;
     ma.tests = count_tests ? R.tests(2) : nullptr;
     Plan mp;
+    mp.tile = R.pick_tile(D, U.n);
     const bool all_mode = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
                           cfg->strategy == SKY_ANGULAR;
     DevSet US;
@@ -795,8 +833,8 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         launch_gather_set(D, U, perm, US, st);
         R.count();
         for (uint32_t p = 0; p < P; ++p)
-            for (uint32_t b = offu[p]; b < offu[p + 1]; b += kTile)
-                mp.add(b, std::min(offu[p + 1], b + (uint32_t)kTile), {make_uint2(0, U.n)});
+            for (uint32_t b = offu[p]; b < offu[p + 1]; b += mp.tile)
+                mp.add(b, std::min(offu[p + 1], b + mp.tile), {make_uint2(0, U.n)});
         ma.sxyz = US.xyz; ma.sskey = US.skey;
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
@@ -807,9 +845,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         for (uint32_t i : nonempty) {
             comps.clear();
             if (cfg->strategy == SKY_SLICED) {  // pd_i = u_j, j < i (engine.cpp:106-108)
-                if (offu[i] > 0) comps.push_back(make_uint2(0, offu[i]));
-                // split per slice so each range stays sum-sorted
-                comps.clear();
+                // one range per slice so each range stays sum-key sorted
                 for (uint32_t j : nonempty) {
                     if (j >= i) break;
                     comps.push_back(make_uint2(offu[j], offu[j + 1]));
@@ -819,12 +855,12 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
                     if (j != i && weak_grid_dom(j, i, m, d)) comps.push_back(make_uint2(offu[j], offu[j + 1]));
             }
             if (comps.empty()) continue;
-            for (uint32_t b = offu[i]; b < offu[i + 1]; b += kTile)
-                mp.add(b, std::min(offu[i + 1], b + (uint32_t)kTile), comps);
+            for (uint32_t b = offu[i]; b < offu[i + 1]; b += mp.tile)
+                mp.add(b, std::min(offu[i + 1], b + mp.tile), comps);
         }
     }
     mp.order();
-    R.relsky(D, mp, ma);
+    R.relsky(D, mp, ma, U.qc, all_mode && P > 1 ? US.qc : U.qc);
 
     // surviving ids, ascending (engine.cpp:128-133)
     uint32_t* pos = R.dev<uint32_t>(S_POS, U.n);

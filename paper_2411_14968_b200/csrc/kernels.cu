@@ -388,6 +388,7 @@ __global__ void k_scatter_direct(DevSet in, const uint8_t* __restrict__ dead, co
     for (int v = 0; v < V; ++v) dst[v] = src[v];
     out.skey[o] = in.skey[i];
     out.id[o] = in.id[i];
+    if (in.qc && out.qc) out.qc[o] = in.qc[i];
 }
 
 void launch_scatter_direct(int D, const DevSet& in, const uint8_t* dead, const uint32_t* pos, DevSet out,
@@ -465,6 +466,7 @@ __global__ void k_gather_set(DevSet in, const uint32_t* __restrict__ perm, uint3
     for (int v = 0; v < V; ++v) dst[v] = src[v];
     out.skey[i] = in.skey[s];
     out.id[i] = in.id[s];
+    if (in.qc && out.qc) out.qc[i] = in.qc[s];
 }
 
 void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st) {

@@ -16,6 +16,7 @@ struct DevSet {
     float* xyz = nullptr;
     uint32_t* skey = nullptr;
     uint32_t* id = nullptr;
+    uint2* qc = nullptr;  // packed monotone codes, two words (D <= 16), optional
     uint32_t n = 0;
 };
 
@@ -98,6 +99,33 @@ struct RelskyArgs {
     unsigned long long* tests;
 };
 void launch_relsky(int D, const RelskyArgs& a, cudaStream_t st);
+
+// ---- packed-code dominance core (kernels_dom.cu), D <= 16 -----------------
+// Per-dimension monotone codes q(x) = #{quantile thresholds <= x}: q(s_j) >
+// q(t_j) proves s_j > t_j, so a guarded lane-wise subtraction over two packed
+// words rules out most non-dominating pairs; pairs that pass are confirmed
+// with the exact float test.
+constexpr int kCodeLevels = 128;
+void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st);   // thr[D][127]
+void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st);  // fills s.qc
+struct Relsky2Args {
+    const float* cxyz;
+    const uint32_t* cskey;
+    const uint2* cqc;
+    const float* sxyz;
+    const uint32_t* sskey;
+    const uint2* sqc;
+    const Item* items;
+    uint32_t n_items;
+    const uint2* ranges;
+    bool bounded;
+    uint8_t* dead;
+    unsigned long long* tests;
+    uint32_t* counter;   // zeroed work counter (persistent CTAs fetch items)
+    unsigned long long* coarse_hits;  // optional: exact checks performed
+};
+// tile = candidates per item (<= 128 * 8); picks K from it.
+void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);
 
 // BNL local skylines: one CTA per partition segment, window capped at
 // `window` points in shared memory; partition input in scan order.
