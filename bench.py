@@ -282,7 +282,8 @@ def run_ours(args):
         "tests_per_s": tests_per_step * args.steps * jobs / (total_dev / 1e3),
         "skyline_size": int(r.skyline.size), "union_size": m.union_size, "filtered_count": m.filtered_count,
         "phase_ms": {"partition": m.partition_ms, "local": m.local_ms, "merge": m.merge_ms},
-        "tests_per_step": {"reps_prefilter": m.tests_reps, "local": m.tests_local, "merge": m.tests_merge},
+        "tests_per_step": {"reps_prefilter": m.tests_reps, "local": m.tests_local, "merge": m.tests_merge,
+                           "exact_checks": m.dom_exact_checks},
         "roofline": roofline,
         "clocks": clk,
         "gpu_launches": launches,

@@ -109,6 +109,8 @@ typedef struct sky_result {
     uint32_t dom_launches;      /* dominance-kernel (k_relsky/k_bnl) launches */
     double dom_kernel_ms;       /* summed CUDA-event time of those launches */
     uint64_t dom_tests;         /* dominance tests they executed */
+    uint64_t dom_exact_checks;  /* pairs the packed codes could not rule out */
+    uint64_t exact_checks_merge;
 } sky_result;
 
 typedef struct sky_ctx sky_ctx;

@@ -75,6 +75,8 @@ class SkyResult(C.Structure):
         ("dom_launches", C.c_uint32),
         ("dom_kernel_ms", C.c_double),
         ("dom_tests", C.c_uint64),
+        ("dom_exact_checks", C.c_uint64),
+        ("exact_checks_merge", C.c_uint64),
     ]
 
 

@@ -65,7 +65,7 @@ constexpr uint32_t kBlock = 512;    // local block-skyline size
 
 // misc device words
 enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_TESTS = 8 /* 4 x u64 */,
-       M_HITS = 16 /* u64 */ };
+       M_HITS = 16 /* 4 x u64, per phase */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;
@@ -200,13 +200,17 @@ class Runner {
     }
 
     // Packed monotone codes for a set whose comparators and candidates share
-    // one quantization (thresholds from a sample of `s`).
-    void encode(int D, DevSet& s) {
+    // one quantization (thresholds from a sample of `s`; `also` reuses them).
+    void encode(int D, DevSet& s, DevSet* also = nullptr) {
         if (D > 16 || !s.n) return;
         float* thr = dev<float>(S_THR, (size_t)D * (kCodeLevels - 1));
         launch_thresholds(D, s, thr, st_);
         launch_encode(D, s, thr, st_);
         count(2);
+        if (also && also->n) {
+            launch_encode(D, *also, thr, st_);
+            count();
+        }
     }
 
     template <class K, class V>
@@ -288,7 +292,8 @@ class Runner {
             b.sxyz = a.sxyz; b.sskey = a.sskey; b.sqc = sq;
             b.items = di; b.n_items = a.n_items; b.ranges = dr; b.bounded = a.bounded; b.dead = a.dead;
             b.tests = a.tests; b.counter = misc + M_WORK;
-            b.coarse_hits = reinterpret_cast<unsigned long long*>(misc + M_HITS);
+            const int phase = a.tests ? (int)(a.tests - tests(0)) : 3;
+            b.coarse_hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + phase;
             launch_relsky2(D, (int)plan.tile, b, c_->sm_count, st_);
         } else {
             if (plan.tile != (uint32_t)kTile) throw Error(SKY_E_INTERNAL, "v1 relsky needs 512-candidate tiles");
@@ -315,7 +320,7 @@ class Runner {
     // small ones keep enough items in flight on 148 SMs
     uint32_t pick_tile(int D, uint64_t n_cands) const {
         if (D > 16) return kTile;
-        return n_cands >= (uint64_t)c_->sm_count * 4 * 1024 ? 1024u : (uint32_t)kTile;
+        return n_cands >= (uint64_t)c_->sm_count * 8 * 256 ? 256u : 128u;
     }
 
     unsigned long long* tests(int k) {
@@ -333,10 +338,11 @@ class Runner {
         uint8_t* dead = dev<uint8_t>(S_DEAD, s0.n);
         launch_fill_u8(dead, 0, s0.n, st_);
         Plan blocks;
+        blocks.tile = D <= 16 ? 256u : (uint32_t)kTile;
         for (uint32_t p = 0; p < P; ++p)
             for (uint32_t b = off0[p]; b < off0[p + 1]; b += kBlock) {
                 const uint32_t e = std::min(b + kBlock, off0[p + 1]);
-                blocks.add(b, e, {make_uint2(b, e)});
+                for (uint32_t c = b; c < e; c += blocks.tile) blocks.add(c, std::min(e, c + blocks.tile), {make_uint2(b, e)});
             }
         RelskyArgs a{};
         a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
@@ -860,6 +866,25 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         }
     }
     mp.order();
+    if (const char* dump = std::getenv("SKY_DEBUG_DUMP")) {
+        // debug aid: union set + codes + thresholds as raw little-endian arrays
+        R.sync();
+        const int D4 = (D + 3) / 4 * 4;
+        std::vector<float> hx((size_t)U.n * D4), ht((size_t)D * (kCodeLevels - 1));
+        std::vector<uint32_t> hk(U.n), hq(2 * (size_t)U.n);
+        SKY_CUDA(cudaMemcpy(hx.data(), U.xyz, hx.size() * 4, cudaMemcpyDeviceToHost));
+        SKY_CUDA(cudaMemcpy(hk.data(), U.skey, hk.size() * 4, cudaMemcpyDeviceToHost));
+        if (U.qc) SKY_CUDA(cudaMemcpy(hq.data(), U.qc, hq.size() * 4, cudaMemcpyDeviceToHost));
+        SKY_CUDA(cudaMemcpy(ht.data(), R.dev<float>(S_THR, ht.size()), ht.size() * 4, cudaMemcpyDeviceToHost));
+        FILE* f = std::fopen(dump, "wb");
+        uint32_t hdr[3] = {U.n, (uint32_t)D, (uint32_t)D4};
+        std::fwrite(hdr, 4, 3, f);
+        std::fwrite(hx.data(), 4, hx.size(), f);
+        std::fwrite(hk.data(), 4, hk.size(), f);
+        std::fwrite(hq.data(), 4, hq.size(), f);
+        std::fwrite(ht.data(), 4, ht.size(), f);
+        std::fclose(f);
+    }
     R.relsky(D, mp, ma, U.qc, all_mode && P > 1 ? US.qc : U.qc);
 
     // surviving ids, ascending (engine.cpp:128-133)
@@ -867,7 +892,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     R.scan_live(fdead, pos, U.n);
     launch_count_total(pos, fdead, U.n, misc + M_TOTAL, st);
     R.count();
-    uint32_t* hm = R.pin<uint32_t>(P_MISC, 16);
+    uint32_t* hm = R.pin<uint32_t>(P_MISC, 32);
     SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     R.sync();
     const uint32_t nf = U.n ? hm[0] : 0;
@@ -881,6 +906,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     SKY_CUDA(cudaMemcpyAsync(hid, idsB, (size_t)nf * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     unsigned long long* ht = reinterpret_cast<unsigned long long*>(hm + 4);
     SKY_CUDA(cudaMemcpyAsync(ht, R.tests(0), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SKY_CUDA(cudaMemcpyAsync(ht + 3, misc + M_HITS, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SKY_CUDA(cudaEventRecord(c->ev[4], st));
     R.sync();
     out->d2h_bytes += (uint64_t)nf * sizeof(uint32_t);
@@ -903,6 +929,8 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     out->dom_launches = c->dom_launches;
     out->dom_kernel_ms = c->dom_ms;
     out->dom_tests = ht[0] + ht[1] + ht[2];
+    out->dom_exact_checks = ht[3] + ht[4] + ht[5] + ht[6];
+    out->exact_checks_merge = ht[5];
 }
 
 template <class F>
@@ -1071,23 +1099,28 @@ int sky_relative_skyline(sky_ctx* c, const float* r, uint64_t nr64, const float*
         launch_scatter_indirect(D, dp, d, idx, key, nr, nullptr, nullptr, T, st);
         uint8_t* dead = R.dev<uint8_t>(S_DEAD, nr);
         launch_fill_u8(dead, 0, nr, st);
+        R.encode(D, S, &T);
         Plan pl;
-        for (uint32_t b = 0; b < nr; b += kTile) pl.add(b, std::min(nr, b + (uint32_t)kTile), {make_uint2(0, nc)});
+        pl.tile = D <= 16 ? 128u : (uint32_t)kTile;
+        for (uint32_t b = 0; b < nr; b += pl.tile) pl.add(b, std::min(nr, b + pl.tile), {make_uint2(0, nc)});
         pl.order();
         RelskyArgs a{};
-        a.cxyz = T.xyz; a.cskey = T.skey; a.sxyz = S.xyz; a.sskey = S.skey; a.bounded = false; a.dead = dead;
+        a.cxyz = T.xyz; a.cskey = T.skey; a.sxyz = S.xyz; a.sskey = S.skey; a.dead = dead;
         a.tests = R.tests(0);
-        // per-candidate bounds need sorted candidates; without sorting use the
-        // exact tile maximum (bounded=true is still sound on any order)
+        // candidates are in input order, so the key bound is per warp (still
+        // sound on any order: a dominator never has a larger key)
         a.bounded = true;
-        R.relsky(D, pl, a);
+        R.relsky(D, pl, a, T.qc, S.qc);
         std::vector<uint8_t> h(nr);
-        unsigned long long t = 0;
+        unsigned long long t[5] = {0, 0, 0, 0, 0};
         SKY_CUDA(cudaMemcpyAsync(h.data(), dead, nr, cudaMemcpyDeviceToHost, st));
-        SKY_CUDA(cudaMemcpyAsync(&t, R.tests(0), sizeof(t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(t, R.tests(0), sizeof(t[0]), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(t + 1, R.dev<uint32_t>(S_MISC, 64) + M_HITS, 4 * sizeof(t[0]),
+                                 cudaMemcpyDeviceToHost, st));
         R.sync();
+        if (std::getenv("SKY_DEBUG_HITS")) std::fprintf(stderr, "relsky tests=%llu exact_checks=%llu\n", t[0], t[1]);
         for (uint32_t i = 0; i < nr; ++i) keep[i] = h[i] ? 0 : 1;
-        if (tests_out) *tests_out = t;
+        if (tests_out) *tests_out = t[0];
     });
 }
 

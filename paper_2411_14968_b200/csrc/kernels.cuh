@@ -121,10 +121,11 @@ struct Relsky2Args {
     bool bounded;
     uint8_t* dead;
     unsigned long long* tests;
-    uint32_t* counter;   // zeroed work counter (persistent CTAs fetch items)
+    uint32_t* counter;   // zeroed work counter (persistent warps fetch items)
+    const uint32_t* wcount;  // window lengths for dynamic ranges (y has bit 31 set)
     unsigned long long* coarse_hits;  // optional: exact checks performed
 };
-// tile = candidates per item (<= 128 * 8); picks K from it.
+// tile = candidates per item (<= 32 * 8, one warp); picks K from it.
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);
 
 // BNL local skylines: one CTA per partition segment, window capped at

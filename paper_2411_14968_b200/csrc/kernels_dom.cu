@@ -13,11 +13,8 @@
 // LOP3 and one predicate-accumulating ISETP (ALU pipe), instead of D FP32
 // compares on the ALU pipe.
 //
-// Work distribution: persistent CTAs pull host-planned items (candidate tile
-// x comparator ranges) from an atomic counter in launch order; comparator
-// tiles are staged in shared memory and broadcast; every warp stops a range
-// at its own coordinate-sum-key bound (a warp-uniform binary search per tile)
-// and as soon as all its candidates are dominated.
+// Work distribution: persistent warps pull host-planned items (<= 256
+// candidates x comparator ranges) from an atomic counter in launch order.
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -38,16 +35,20 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 }
 
 // Two-word code layout for D dimensions (see the file comment).
+// Bit 31 of both words is never part of a lane; in word 0 it is the "alive"
+// guard: set in t' while the candidate is alive, cleared when it is dominated
+// (or the slot is empty), so a dead slot can never pass the coarse test.
 template <int D>
 struct CodeLayout {
     static constexpr int L = (D + 1) / 2;                     // lanes per word
-    static constexpr int LW = 32 / L;                          // lane width in bits
+    static constexpr int LW = 31 / L;                          // lane width in bits
     static constexpr int B = (LW - 1) < 7 ? (LW - 1) : 7;      // code bits
-    static constexpr uint32_t G = [] {                         // guard bits
+    static constexpr uint32_t G = [] {                         // lane guard bits
         uint32_t g = 0;
         for (int i = 0; i < L; ++i) g |= 1u << (i * LW + LW - 1);
         return g;
     }();
+    static constexpr uint32_t ALIVE = 0x80000000u;
 };
 
 constexpr int kSample = 4096;
@@ -128,14 +129,16 @@ __global__ void __launch_bounds__(256) k_encode(DevSet s, const float* __restric
     s.qc[i] = make_uint2(w[0], w[1]);
 }
 
-// q(s_j) <= q(t_j) on every lane of both words (t' carries the guard bits)
+// q(s_j) <= q(t_j) on every lane of both words, and t alive (t' carries the
+// lane guards in both words and the alive guard in word 0)
 template <uint32_t G>
 __device__ __forceinline__ bool coarse_pass(const uint32_t (&t)[2], const uint2& s) {
-    return ((t[0] - s.x) & (t[1] - s.y) & G) == G;
+    constexpr uint32_t GA = G | 0x80000000u;  // t'[1] always carries bit 31
+    return ((t[0] - s.x) & (t[1] - s.y) & GA) == GA;
 }
 
-constexpr int RS2_THREADS = 128;
-constexpr int RS2_TILE = 128;  // comparators per shared-memory tile
+constexpr int RS3_WARPS = 8;
+constexpr int RS3_THREADS = RS3_WARPS * 32;
 
 template <int D>
 __device__ __forceinline__ bool dominates_exact(const float4* __restrict__ s, const float4* __restrict__ t) {
@@ -150,139 +153,142 @@ __device__ __forceinline__ bool dominates_exact(const float4* __restrict__ s, co
     return !gt && lt;
 }
 
+// Comparator range end: plain, or (flag bit) the current length of a
+// device-side window counter (windowed SFS).
+__device__ __forceinline__ uint32_t range_end(const Relsky2Args& a, uint2 rg) {
+    return (rg.y & 0x80000000u) ? rg.x + a.wcount[rg.y & 0x7FFFFFFFu] : rg.y;
+}
+
+// Warp-autonomous dominance core: every warp fetches its own item
+// (<= 32*K candidates, lane l owns candidates cb + 32k + l), streams the
+// comparator ranges 32 at a time through its private shared-memory slot
+// (codes, keys and coordinates of the next batch are prefetched into
+// registers while the current one is tested), stops a range when a ballot
+// shows the sorted keys passed the warp's bound and leaves the item once every
+// candidate is dominated. Exact checks read both points from shared memory.
+// No CTA barriers.
 template <int D, int K>
-__global__ void __launch_bounds__(RS2_THREADS) k_relsky2(Relsky2Args a, int tile) {
+struct Relsky3Smem {
+    static constexpr int V = Dims2<D>::V;
+    float4 cand[K][V][32];  // [k][v][lane]: conflict-free per-lane reads
+    float4 comp[32][V];     // current comparator batch (broadcast reads)
+    uint2 code[32];
+};
+
+template <int D, int K>
+__global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
     constexpr int W = Dims2<D>::V;
     constexpr uint32_t G = CodeLayout<D>::G;
-    __shared__ float4 s_xyz[RS2_TILE * W];
-    __shared__ uint2 s_code[RS2_TILE];
-    __shared__ uint32_t s_key[RS2_TILE];
-    __shared__ uint32_t s_red[RS2_THREADS / 32];
-    __shared__ uint32_t s_item, s_end;
+    constexpr uint32_t FULL = 0xffffffffu;
+    extern __shared__ float4 smem_raw[];
+    using S = Relsky3Smem<D, K>;
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per_warp = (tile + 3) / 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    S& sm = reinterpret_cast<S*>(smem_raw)[warp];
     unsigned long long ntests = 0, nhits = 0;
 
     for (;;) {
-        if (tid == 0) s_item = atomicAdd(a.counter, 1u);
-        __syncthreads();
-        const uint32_t item = s_item;
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(a.counter, 1u);
+        item = __shfl_sync(FULL, item, 0);
         if (item >= a.n_items) break;
         const Item it = a.items[item];
 
-        // ---- candidates: warp w owns [w*per_warp, (w+1)*per_warp) of the tile
         uint32_t T[K][2];
         uint32_t alive = 0, my_max = 0;
-        const uint32_t wbase = it.cb + warp * per_warp;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const uint32_t off = k * 32 + lane;
-            const uint32_t c = wbase + off;
-            T[k][0] = T[k][1] = 0;
-            if ((int)off < per_warp && c < it.ce && !a.dead[c]) {
+            const uint32_t c = it.cb + k * 32 + lane;
+            // empty / dead slot: lane guards set (no borrow can reach bit 31),
+            // alive guard clear -> never passes
+            T[k][0] = G;
+            T[k][1] = G | 0x80000000u;
+            if (c < it.ce && !a.dead[c]) {
                 alive |= 1u << k;
                 const uint2 q = a.cqc[c];
-                T[k][0] = q.x | G;
-                T[k][1] = q.y | G;
+                T[k][0] = q.x | G | CodeLayout<D>::ALIVE;
+                T[k][1] = q.y | G | 0x80000000u;
                 my_max = max(my_max, a.cskey[c]);
+                const float4* x = reinterpret_cast<const float4*>(a.cxyz) + (size_t)c * W;
+#pragma unroll
+                for (int v = 0; v < W; ++v) sm.cand[k][v][lane] = x[v];
             }
         }
         const uint32_t initial = alive;
-        uint32_t warp_max = __reduce_max_sync(0xffffffffu, my_max);
-        if (lane == 0) s_red[warp] = warp_max;
-        __syncthreads();
-        uint32_t cta_max = 0;
-#pragma unroll
-        for (int w = 0; w < RS2_THREADS / 32; ++w) cta_max = max(cta_max, s_red[w]);
-        if (!a.bounded) warp_max = cta_max = 0xFFFFFFFFu;
-        bool warp_alive = __any_sync(0xffffffffu, alive != 0);
+        const uint32_t bound = a.bounded ? __reduce_max_sync(FULL, my_max) : 0xFFFFFFFFu;
+        bool live = __any_sync(FULL, alive != 0);
 
-        if (__syncthreads_or(alive != 0)) {
-            for (uint32_t r = it.lb; r < it.le; ++r) {
-                const uint2 rg = a.ranges[r];
-                uint32_t sb = rg.x, se = rg.y;
-                if (a.bounded) {
-                    if (tid == 0) {
-                        uint32_t lo = sb, hi = se;
-                        while (lo < hi) {
-                            const uint32_t mid = (lo + hi) >> 1;
-                            if (a.sskey[mid] <= cta_max) lo = mid + 1; else hi = mid;
-                        }
-                        s_end = lo;
-                    }
-                    __syncthreads();
-                    se = s_end;
+        for (uint32_t r = it.lb; live && r < it.le; ++r) {
+            const uint2 rg = a.ranges[r];
+            const uint32_t sb = rg.x, se = range_end(a, rg);
+            // prefetch the first batch
+            uint32_t idx = sb + lane;
+            uint2 nq = make_uint2(0, 0);
+            uint32_t nk = 0xFFFFFFFFu;
+            float4 nx[W];
+            if (idx < se) {
+                nq = a.sqc[idx];
+                nk = a.sskey[idx];
+                const float4* x = reinterpret_cast<const float4*>(a.sxyz) + (size_t)idx * W;
+#pragma unroll
+                for (int v = 0; v < W; ++v) nx[v] = x[v];
+            }
+            for (uint32_t base = sb; base < se; base += 32) {
+                const uint32_t inb = __ballot_sync(FULL, nk <= bound);  // prefix (keys sorted)
+                const uint32_t lim = __popc(inb);
+                __syncwarp();
+                sm.code[lane] = nq;
+#pragma unroll
+                for (int v = 0; v < W; ++v) sm.comp[lane][v] = nx[v];
+                __syncwarp();
+                idx = base + 32 + lane;
+                if (lim == 32 && idx < se) {
+                    nq = a.sqc[idx];
+                    nk = a.sskey[idx];
+                    const float4* x = reinterpret_cast<const float4*>(a.sxyz) + (size_t)idx * W;
+#pragma unroll
+                    for (int v = 0; v < W; ++v) nx[v] = x[v];
+                } else {
+                    nk = 0xFFFFFFFFu;
                 }
-                bool warp_live = warp_alive;
-                for (uint32_t base = sb; base < se; base += RS2_TILE) {
-                    const uint32_t len = min((uint32_t)RS2_TILE, se - base);
-                    __syncthreads();
-                    {
-                        const float4* src = reinterpret_cast<const float4*>(a.sxyz) + (size_t)base * W;
-                        for (uint32_t i = tid; i < len * W; i += RS2_THREADS) s_xyz[i] = src[i];
-                        for (uint32_t i = tid; i < len; i += RS2_THREADS) {
-                            s_code[i] = a.sqc[base + i];
-                            s_key[i] = a.sskey[base + i];
-                        }
-                    }
-                    __syncthreads();
-                    if (warp_live) {
-                        // comparators of this tile inside the warp's key bound
-                        uint32_t lo = 0, hi = len;
-                        while (lo < hi) {
-                            const uint32_t mid = (lo + hi) >> 1;
-                            if (s_key[mid] <= warp_max) lo = mid + 1; else hi = mid;
-                        }
-                        const uint32_t lim = lo;
-                        uint32_t i = 0;
-                        const uint2* __restrict__ sc = s_code;
-                        for (; i < lim; ++i) {
-                            const uint2 q = sc[i];
-                            // all guard bits set <=> (t' - s) | ~M == 0xFFFFFFFF in every word
-                            bool none = true;
+                for (uint32_t i = 0; i < lim; ++i) {
+                    const uint2 q = sm.code[i];
+                    bool none = true;
 #pragma unroll
-                            for (int k = 0; k < K; ++k) none &= !coarse_pass<G>(T[k], q);
-                            if (!none) {
-                                // exact test (core.hpp:89-96) for the pairs the codes could not rule out
-                                const float4* sx = s_xyz + i * W;
+                    for (int k = 0; k < K; ++k) none &= !coarse_pass<G>(T[k], q);
+                    if (!none) {
+                        // exact test (core.hpp:89-96) where the codes could not rule s out
 #pragma unroll
-                                for (int k = 0; k < K; ++k) {
-                                    if ((alive >> k) & 1u) {
-                                        if (coarse_pass<G>(T[k], q)) {
-                                            ++nhits;
-                                            const uint32_t c = wbase + k * 32 + lane;
-                                            const float4* tx = reinterpret_cast<const float4*>(a.cxyz) + (size_t)c * W;
-                                            if (dominates_exact<D>(sx, tx)) {
-                                                alive &= ~(1u << k);
-                                                ntests += i + 1;
-                                            }
-                                        }
-                                    }
+                        for (int k = 0; k < K; ++k) {
+                            if (coarse_pass<G>(T[k], q)) {
+                                ++nhits;
+                                bool gt = false, lt = false;
+#pragma unroll
+                                for (int v = 0; v < W; ++v) {
+                                    const float4 sa = sm.comp[i][v], tb = sm.cand[k][v][lane];
+                                    gt |= (sa.x > tb.x) | (sa.y > tb.y) | (sa.z > tb.z) | (sa.w > tb.w);
+                                    lt |= (sa.x < tb.x) | (sa.y < tb.y) | (sa.z < tb.z) | (sa.w < tb.w);
+                                }
+                                if (!gt && lt) {
+                                    alive &= ~(1u << k);
+                                    T[k][0] &= ~CodeLayout<D>::ALIVE;
+                                    ntests += i + 1;
                                 }
                             }
-                            if ((i & 15) == 15 && !__any_sync(0xffffffffu, alive != 0)) {
-                                ++i;
-                                break;
-                            }
                         }
-                        ntests += (unsigned long long)__popc(alive) * i;
-                        if (i < len) warp_live = false;  // key bound reached (sorted range)
-                        warp_alive = __any_sync(0xffffffffu, alive != 0);
-                        if (!warp_alive) warp_live = false;
                     }
-                    if (!__syncthreads_or(warp_live)) break;
                 }
-                if (!__syncthreads_or(warp_alive)) break;
+                ntests += (unsigned long long)__popc(alive) * lim;
+                live = __any_sync(FULL, alive != 0);
+                if (!live || lim < 32) break;  // all dominated, or past the key bound
             }
         }
         uint32_t killed = initial & ~alive;
         while (killed) {
             const int k = __ffs(killed) - 1;
             killed &= killed - 1;
-            a.dead[wbase + k * 32 + lane] = 1;
+            a.dead[it.cb + k * 32 + lane] = 1;
         }
-        __syncthreads();  // s_item / s_red reuse
     }
     if (a.tests) {
         ntests = warp_sum(ntests);
@@ -309,14 +315,17 @@ __global__ void __launch_bounds__(RS2_THREADS) k_relsky2(Relsky2Args a, int tile
     }
 
 template <int D, int K>
-void launch_k(const Relsky2Args& a, int tile, int sm_count, cudaStream_t st) {
+void launch_k(const Relsky2Args& a, int sm_count, cudaStream_t st) {
     static int per_sm = 0;
+    const size_t smem = sizeof(Relsky3Smem<D, K>) * RS3_WARPS;
     if (!per_sm) {
-        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_relsky2<D, K>, RS2_THREADS, 0));
+        SKY_CUDA(cudaFuncSetAttribute(k_relsky3<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_relsky3<D, K>, RS3_THREADS, smem));
         if (per_sm < 1) per_sm = 1;
     }
-    const uint32_t grid = (uint32_t)std::min<uint64_t>(a.n_items, (uint64_t)per_sm * sm_count);
-    k_relsky2<D, K><<<grid, RS2_THREADS, 0, st>>>(a, tile);
+    const uint64_t warps = std::min<uint64_t>(a.n_items, (uint64_t)per_sm * sm_count * RS3_WARPS);
+    const uint32_t grid = (uint32_t)((warps + RS3_WARPS - 1) / RS3_WARPS);
+    k_relsky3<D, K><<<grid, RS3_THREADS, smem, st>>>(a);
     SKY_LAUNCH_CHECK();
 }
 
@@ -336,10 +345,12 @@ void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st) {
 
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st) {
     if (!a.n_items) return;
-    if (tile <= 4 * 32 * 4) {
-        SKY_DISPATCH_D16(D, (launch_k<DT, 4>(a, tile, sm_count, st)));
+    if (tile <= 4 * 32) {
+        SKY_DISPATCH_D16(D, (launch_k<DT, 4>(a, sm_count, st)));
+    } else if (tile <= 8 * 32) {
+        SKY_DISPATCH_D16(D, (launch_k<DT, 8>(a, sm_count, st)));
     } else {
-        SKY_DISPATCH_D16(D, (launch_k<DT, 8>(a, tile, sm_count, st)));
+        throw Error(SKY_E_INTERNAL, "relsky item larger than one warp's candidates");
     }
 }
 

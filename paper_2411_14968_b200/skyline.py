@@ -160,6 +160,7 @@ class PhaseMetrics:
     dom_launches: int = 0
     dom_kernel_ms: float = 0.0
     dom_tests: int = 0
+    dom_exact_checks: int = 0
 
     @property
     def tests_total(self) -> int:
@@ -258,7 +259,7 @@ class Engine:
                 angular_host_fixups=int(res.angular_host_fixups), kernel_launches=int(res.kernel_launches),
                 h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
                 dom_launches=int(res.dom_launches), dom_kernel_ms=float(res.dom_kernel_ms),
-                dom_tests=int(res.dom_tests))
+                dom_tests=int(res.dom_tests), dom_exact_checks=int(res.dom_exact_checks))
             return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
         finally:
             self._lib.sky_result_free(C.byref(res))
