@@ -375,7 +375,9 @@ class Runner {
                      std::vector<uint32_t>& off_u, bool count_tests, uint32_t* used_window) {
         uint8_t* dead = dev<uint8_t>(S_DEAD, s0.n);
         launch_fill_u8(dead, 1, s0.n, st_);
-        const uint32_t cap = bnl_window_fit(D, window ? window : 4096, c_->smem_optin);
+        const bool packed = D <= 16 && s0.qc;
+        const uint32_t want = window ? window : 4096;
+        const uint32_t cap = packed ? bnl2_window_fit(D, want, c_->smem_optin) : bnl_window_fit(D, want, c_->smem_optin);
         *used_window = cap;
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(P, (uint32_t)c_->sm_count));
         uint32_t* wpos = dev<uint32_t>(S_BNL_POS, (size_t)grid * cap);
@@ -393,7 +395,10 @@ class Runner {
         b.tests = count_tests ? tests(1) : nullptr;
         if (s0.n) {
             SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
-            launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
+            if (packed)
+                launch_bnl2(D, b, s0.qc, cap, grid, misc + M_BNLCTR, st_);
+            else
+                launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
             SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));
             count();
             dom_done();

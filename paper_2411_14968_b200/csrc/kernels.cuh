@@ -144,4 +144,9 @@ uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint32_t* win_pos, uint32_t* win_meta,
                      uint32_t* counter, cudaStream_t st);
 
+// Packed-code BNL (D <= 16): window codes + metadata in shared memory.
+uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin);
+void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
+                 cudaStream_t st);
+
 }  // namespace sky

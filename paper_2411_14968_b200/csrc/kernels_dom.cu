@@ -300,6 +300,284 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
     }
 }
 
+// ------------------------------------------------------------------ BNL
+// Block-nested-loops (Borzsonyi et al., ICDE 2001; the reference has no BNL,
+// SPEC.md:157) for one partition per CTA with a shared-memory window of at
+// most `cap` tuples. The partition is consumed in batches of BNL2_B tuples
+// (one per thread). Each batch tuple t is compared with every window tuple w
+// in both directions (w may dominate t: t dies; t may dominate w: w is
+// evicted) and with the other batch tuples, all through the packed codes with
+// exact confirmation. Survivors enter the window while it has room and spill
+// to an in-place overflow list otherwise. A window tuple carries (pass,
+// timestamp = overflow length when it entered); it is output once it has met
+// every tuple: at the end of its pass if nothing spilled before it, else when
+// the next pass has consumed that many overflow tuples.
+constexpr int BNL2_B = 512;
+
+template <int D>
+size_t bnl2_smem(uint32_t cap) {
+    constexpr int V = Dims2<D>::V;
+    return (size_t)cap * 16 + (size_t)BNL2_B * V * 16 + (size_t)BNL2_B * 8 + (size_t)cap * 8 + 2 * (size_t)cap + 64;
+}
+
+template <int D>
+__device__ __forceinline__ bool dom_f4(const float4* __restrict__ s, const float4* __restrict__ t) {
+    constexpr int V = Dims2<D>::V;
+    bool gt = false, lt = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const float4 a = s[v], b = t[v];
+        gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
+        lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
+    }
+    return !gt && lt;
+}
+
+template <int D>
+__global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restrict__ qc, uint32_t cap,
+                                                 uint32_t* work_counter) {
+    constexpr int V = Dims2<D>::V;
+    constexpr uint32_t G = CodeLayout<D>::G;
+    constexpr uint32_t GA = G | 0x80000000u;
+    constexpr uint32_t ALIVE = CodeLayout<D>::ALIVE;
+    extern __shared__ uint4 sm4[];
+    uint4* w_code = sm4;                                                   // (w.x, w.y, w'.x, w'.y)
+    float4* b_xyz = reinterpret_cast<float4*>(w_code + cap);               // batch coords [B][V]
+    uint2* b_code = reinterpret_cast<uint2*>(b_xyz + BNL2_B * V);          // batch codes
+    uint32_t* w_pos = reinterpret_cast<uint32_t*>(b_code + BNL2_B);        // window -> set position
+    uint32_t* w_ts = w_pos + cap;                                          // overflow length at entry
+    uint8_t* w_pass = reinterpret_cast<uint8_t*>(w_ts + cap);              // pass of entry (mod 256)
+    uint8_t* w_kill = w_pass + cap;                                        // 1 evicted, 2 confirmed
+    __shared__ uint32_t s_wn, s_ovf_w, s_part, s_scan[BNL2_B / 32], s_next;
+    __shared__ int s_pass;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float4* __restrict__ xyz = reinterpret_cast<const float4*>(a.xyz);
+    unsigned long long ntests = 0;
+
+    // stable compaction of the window: drop entries with w_kill != 0
+    // (confirmed ones are output first)
+    auto compact_window = [&]() {
+        const uint32_t wn0 = s_wn;
+        uint32_t kept_before = 0;
+        for (uint32_t c0 = 0; c0 < wn0; c0 += BNL2_B) {
+            const uint32_t w = c0 + tid;
+            const bool in = w < wn0;
+            const uint8_t kill = in ? w_kill[w] : 0;
+            const bool keep = in && kill == 0;
+            uint4 q = make_uint4(0, 0, 0, 0);
+            uint32_t pos = 0, ts = 0;
+            uint8_t ps = 0;
+            if (in) pos = w_pos[w];
+            if (keep) {
+                q = w_code[w];
+                ts = w_ts[w];
+                ps = w_pass[w];
+            }
+            if (in && kill == 2) a.dead[pos] = 0;  // confirmed skyline tuple
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) s_scan[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t off = kept_before + __popc(bal & ((1u << lane) - 1u));
+            uint32_t tot = 0;
+#pragma unroll
+            for (int ww = 0; ww < BNL2_B / 32; ++ww) {
+                if (ww < warp) off += s_scan[ww];
+                tot += s_scan[ww];
+            }
+            __syncthreads();
+            if (keep) {
+                w_code[off] = q;
+                w_pos[off] = pos;
+                w_ts[off] = ts;
+                w_pass[off] = ps;
+                w_kill[off] = 0;
+            }
+            kept_before += tot;
+            __syncthreads();
+        }
+        if (tid == 0) s_wn = kept_before;
+        __syncthreads();
+    };
+
+    for (;;) {
+        if (tid == 0) s_part = atomicAdd(work_counter, 1u);
+        __syncthreads();
+        const uint32_t part = s_part;
+        if (part >= a.P) break;
+        const uint32_t seg_b = a.seg_off[part], seg_e = a.seg_off[part + 1];
+        if (seg_b == seg_e) {
+            __syncthreads();
+            continue;
+        }
+        uint32_t* ovf = a.overflow + seg_b;
+        if (tid == 0) {
+            s_wn = 0;
+            s_pass = 0;
+        }
+        __syncthreads();
+        uint32_t in_n = seg_e - seg_b;
+        bool first = true;
+        for (;;) {
+            const uint32_t wn_start = s_wn;
+            if (in_n == 0 && wn_start == 0) break;
+            const int pass = s_pass;
+            const uint8_t prev_pass = (uint8_t)(pass - 1);
+            if (tid == 0) s_ovf_w = 0;
+            __syncthreads();
+            for (uint32_t k0 = 0;; k0 += BNL2_B) {
+                // confirm window tuples of the previous pass whose timestamp is reached
+                {
+                    bool any = false;
+                    const uint32_t wn = s_wn;
+                    for (uint32_t w = tid; w < wn; w += BNL2_B) {
+                        const bool c = !first && w_pass[w] == prev_pass && w_ts[w] <= k0;
+                        w_kill[w] = c ? 2 : 0;
+                        any |= c;
+                    }
+                    if (__syncthreads_or(any)) compact_window();
+                }
+                if (k0 >= in_n) break;
+                const uint32_t bn = min((uint32_t)BNL2_B, in_n - k0);
+                const bool valid = (uint32_t)tid < bn;
+                uint32_t mypos = 0;
+                float4 t[V];
+                uint2 tq = make_uint2(0, 0);
+                if (valid) {
+                    mypos = first ? seg_b + k0 + tid : ovf[k0 + tid];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        t[v] = xyz[(size_t)mypos * V + v];
+                        b_xyz[tid * V + v] = t[v];
+                    }
+                    tq = qc[mypos];
+                    b_code[tid] = tq;
+                }
+                __syncthreads();
+                uint32_t T0 = valid ? (tq.x | G | ALIVE) : G;
+                const uint32_t T1 = (valid ? tq.y : 0u) | G | 0x80000000u;
+                bool alive = valid;
+                // batch x window, both directions
+                const uint32_t wn = s_wn;
+                bool killed_any = false;
+                auto slow = [&](uint32_t w, bool d1, bool d2) {
+                    const float4* wx = xyz + (size_t)w_pos[w] * V;
+                    float4 wv[V];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) wv[v] = wx[v];
+                    if (d1 && dom_f4<D>(wv, t)) {
+                        alive = false;
+                        T0 &= ~ALIVE;
+                    }
+                    if (d2 && dom_f4<D>(t, wv)) {
+                        w_kill[w] = 1;
+                        killed_any = true;
+                    }
+                };
+                uint32_t w = 0;
+                for (; w + 4 <= wn; w += 4) {
+                    // four independent entries per step: loads issue back to back
+                    uint4 q[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) q[u] = w_code[w + u];
+                    bool d1[4], d2[4];
+                    bool any = false;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        d1[u] = ((T0 - q[u].x) & (T1 - q[u].y) & GA) == GA;            // w may dominate t
+                        d2[u] = valid && ((q[u].z - tq.x) & (q[u].w - tq.y) & GA) == GA;  // t may dominate w
+                        any |= d1[u] | d2[u];
+                    }
+                    if (any) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (d1[u] | d2[u]) slow(w + u, d1[u], d2[u]);
+                    }
+                }
+                for (; w < wn; ++w) {
+                    const uint4 q = w_code[w];
+                    const bool d1 = ((T0 - q.x) & (T1 - q.y) & GA) == GA;
+                    const bool d2 = valid && ((q.z - tq.x) & (q.w - tq.y) & GA) == GA;
+                    if (d1 | d2) slow(w, d1, d2);
+                }
+                if (valid) ntests += 2ull * wn;
+                // batch x batch: is t dominated by another batch tuple?
+                for (uint32_t u = 0; u < bn; ++u) {
+                    const uint2 uq = b_code[u];
+                    if (u != (uint32_t)tid && ((T0 - uq.x) & (T1 - uq.y) & GA) == GA) {
+                        if (dom_f4<D>(b_xyz + u * V, t)) {
+                            alive = false;
+                            T0 &= ~ALIVE;
+                        }
+                    }
+                }
+                if (valid) ntests += bn - 1;
+                if (__syncthreads_or(killed_any)) compact_window();
+                // survivors enter the window in batch order, or spill
+                {
+                    const unsigned bal = __ballot_sync(0xffffffffu, alive);
+                    if (lane == 0) s_scan[warp] = __popc(bal);
+                    __syncthreads();
+                    uint32_t rank = __popc(bal & ((1u << lane) - 1u));
+                    uint32_t tot = 0;
+#pragma unroll
+                    for (int ww = 0; ww < BNL2_B / 32; ++ww) {
+                        if (ww < warp) rank += s_scan[ww];
+                        tot += s_scan[ww];
+                    }
+                    const uint32_t wn1 = s_wn, ow = s_ovf_w;
+                    const uint32_t room = cap - wn1;
+                    if (alive) {
+                        if (rank < room) {
+                            const uint32_t slot = wn1 + rank;
+                            w_code[slot] = make_uint4(tq.x, tq.y, tq.x | G | 0x80000000u, tq.y | G | 0x80000000u);
+                            w_pos[slot] = mypos;
+                            w_ts[slot] = ow;  // overflow tuples written in this pass so far
+                            w_pass[slot] = (uint8_t)pass;
+                            w_kill[slot] = 0;
+                        } else {
+                            ovf[ow + (rank - room)] = mypos;  // in place: ow + spilled <= k0 + bn
+                        }
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        const uint32_t ins = min(tot, room);
+                        s_wn = wn1 + ins;
+                        s_ovf_w = ow + (tot - ins);
+                    }
+                    __syncthreads();
+                }
+            }
+            // end of pass: tuples that entered before any spill of this pass,
+            // and every tuple of the previous pass, have met every tuple;
+            // with no spill at all the whole window is final.
+            {
+                const uint32_t ovf_n = s_ovf_w;
+                const uint32_t wn = s_wn;
+                for (uint32_t w = tid; w < wn; w += BNL2_B) {
+                    const bool cur = w_pass[w] == (uint8_t)pass;
+                    const bool confirm = ovf_n == 0 || (cur && w_ts[w] == 0) || (!cur && w_pass[w] == prev_pass);
+                    w_kill[w] = confirm ? 2 : 0;
+                }
+                __syncthreads();
+                compact_window();
+                if (tid == 0) {
+                    s_pass = pass + 1;
+                    s_next = ovf_n;
+                }
+                __syncthreads();
+                in_n = s_next;
+                first = false;
+            }
+        }
+        __syncthreads();
+    }
+    if (a.tests) {
+        ntests = warp_sum(ntests);
+        if (lane == 0 && ntests) atomicAdd(a.tests, ntests);
+    }
+}
+
 #define SKY_DISPATCH_D16(D, ...)                                \
     switch (D) {                                                \
         case 2: { constexpr int DT = 2; __VA_ARGS__; break; }   \
@@ -329,7 +607,29 @@ void launch_k(const Relsky2Args& a, int sm_count, cudaStream_t st) {
     SKY_LAUNCH_CHECK();
 }
 
+template <int D>
+void launch_bnl2_impl(const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
+                      cudaStream_t st) {
+    const size_t smem = bnl2_smem<D>(cap);
+    SKY_CUDA(cudaFuncSetAttribute(k_bnl2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bnl2<D><<<grid, BNL2_B, smem, st>>>(a, qc, cap, counter);
+    SKY_LAUNCH_CHECK();
+}
+
 }  // namespace
+
+uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin) {
+    uint32_t cap = want;
+    SKY_DISPATCH_D16(D, {
+        while (cap > 32 && bnl2_smem<DT>(cap) + 2048 > (size_t)smem_optin) cap -= 32;
+    });
+    return cap;
+}
+
+void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
+                 cudaStream_t st) {
+    SKY_DISPATCH_D16(D, (launch_bnl2_impl<DT>(a, qc, cap, grid, counter, st)));
+}
 
 void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st) {
     if (!s.n) return;
