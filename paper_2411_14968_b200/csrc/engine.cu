@@ -54,7 +54,7 @@ enum Slot {
     S_SET0, S_SET0_K, S_SET0_I, S_SET0_Q, S_SET1, S_SET1_K, S_SET1_I, S_SET1_Q,
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
-    S_OVF, S_SKTMP, S_THR, S_COUNT
+    S_OVF, S_SKTMP, S_THR, S_RAND, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -323,6 +323,22 @@ class Runner {
         return n_cands >= (uint64_t)c_->sm_count * 8 * 256 ? 256u : 128u;
     }
 
+    // partition_of of assign_random (partition.cpp:36-54) on the device; the
+    // host reproduces it only if a draw would have been rejected.
+    uint32_t* random_pids(uint32_t n, uint64_t P, uint64_t seed) {
+        uint32_t* pid = dev<uint32_t>(S_PID, n);
+        void* scratch = c_->dev.get(S_RAND, random_scratch_bytes(n));
+        const size_t cb = random_cub_bytes(n);
+        void* ct = c_->dev.get(S_CUB, cb);
+        if (!random_partition_gpu(n, P, seed, pid, scratch, ct, cb, c_->sm_count, st_, &c_->launches)) {
+            uint32_t* h = pin<uint32_t>(P_PID, n);
+            random_partition_of(n, P, seed, h);
+            SKY_CUDA(cudaMemcpyAsync(pid, h, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+            sync();
+        }
+        return pid;
+    }
+
     unsigned long long* tests(int k) {
         return reinterpret_cast<unsigned long long*>(dev<uint32_t>(S_MISC, 64) + M_TESTS) + k;
     }
@@ -490,20 +506,16 @@ struct PartitionOut {
 
 // Phase 1a: partition ids, sum keys, validation, sort into partitions.
 PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d, int normalized, int strategy,
-                             uint64_t P, uint64_t m, const sky_config* cfg, std::thread* host_perm,
-                             uint32_t* host_pid, uint64_t* fixups) {
+                             uint64_t P, uint64_t m, const sky_config* cfg, const uint32_t* pid_dev,
+                             uint64_t* fixups) {
     cudaStream_t st = R.st_;
     uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, n);
     uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, n);
     uint32_t* idxA = R.dev<uint32_t>(S_IDX_A, n);
     uint32_t* idxB = R.dev<uint32_t>(S_IDX_B, n);
     uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
-    uint32_t* pid_in = nullptr;
-    if (strategy == SKY_RANDOM) {
-        if (host_perm) host_perm->join();
-        pid_in = R.dev<uint32_t>(S_PID, n);
-        SKY_CUDA(cudaMemcpyAsync(pid_in, host_pid, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    }
+    const uint32_t* pid_in = strategy == SKY_RANDOM ? pid_dev : nullptr;
+    if (strategy == SKY_RANDOM && !pid_in && n) throw Error(SKY_E_INTERNAL, "random strategy without partition ids");
     const uint32_t amb_cap = 1u << 16;
     uint32_t* amb = R.dev<uint32_t>(S_AMB, amb_cap);
     uint32_t* skA = nullptr;
@@ -642,19 +654,6 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     Runner R(c);
     cudaStream_t st = c->stream;
 
-    // random partitioning: the permutation is seeded host work; overlap it
-    // with the upload and the prep pass of the other fields
-    uint32_t* host_pid = nullptr;
-    std::thread perm_thread;
-    if (cfg->strategy == SKY_RANDOM) {
-        host_pid = R.pin<uint32_t>(P_PID, n);
-        perm_thread = std::thread(random_partition_of, (uint64_t)n, (uint64_t)P, cfg->seed, host_pid);
-    }
-    struct Joiner {
-        std::thread& t;
-        ~Joiner() { if (t.joinable()) t.join(); }
-    } joiner{perm_thread};
-
     SKY_CUDA(cudaEventRecord(c->ev[0], st));
     uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
     SKY_CUDA(cudaMemsetAsync(misc, 0, 64 * sizeof(uint32_t), st));
@@ -665,10 +664,8 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         pts = dp;
         out->h2d_bytes += (uint64_t)n * d * sizeof(float);
     }
-    if (cfg->strategy == SKY_RANDOM) out->h2d_bytes += (uint64_t)n * sizeof(uint32_t);
-
-    PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg,
-                                      cfg->strategy == SKY_RANDOM ? &perm_thread : nullptr, host_pid,
+    const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed) : nullptr;
+    PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
                                       &out->angular_host_fixups);
 
     std::vector<uint32_t> off0(P + 1);
@@ -1056,13 +1053,9 @@ int sky_assign(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int no
         Runner R(c);
         float* dp = R.dev<float>(S_PTS, (size_t)n * d);
         SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-        uint32_t* host_pid = nullptr;
-        if (cfg->strategy == SKY_RANDOM) {
-            host_pid = R.pin<uint32_t>(P_PID, n);
-            random_partition_of(n, P64, cfg->seed, host_pid);
-        }
+        const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P64, cfg->seed) : nullptr;
         uint64_t fix = 0;
-        PartitionOut po = partition_phase(R, dp, n, d, normalized, cfg->strategy, P64, m, cfg, nullptr, host_pid, &fix);
+        PartitionOut po = partition_phase(R, dp, n, d, normalized, cfg->strategy, P64, m, cfg, pid_dev, &fix);
         std::vector<uint64_t> key(n);
         std::vector<uint32_t> idx(n);
         SKY_CUDA(cudaMemcpyAsync(key.data(), po.key64, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -1173,8 +1166,10 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
         sky_config cfg;
         sky_config_default(&cfg);
         cfg.p = p;
+        uint32_t* pd = R.dev<uint32_t>(S_PID, n);
+        SKY_CUDA(cudaMemcpyAsync(pd, hp, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
         uint64_t fix = 0;
-        PartitionOut po = partition_phase(R, dp, n, d, 0, SKY_RANDOM, p, 0, &cfg, nullptr, hp, &fix);
+        PartitionOut po = partition_phase(R, dp, n, d, 0, SKY_RANDOM, p, 0, &cfg, pd, &fix);
         const uint32_t qq = (uint32_t)std::min<uint64_t>(q, n);
         uint32_t* cand = R.dev<uint32_t>(S_REPCAND, (size_t)p * qq);
         launch_rep_pick(po.key64, po.idx, po.off, (uint32_t)p, dp, d, qq, cand, st);

@@ -149,4 +149,10 @@ uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
                  cudaStream_t st);
 
+// Random partitioner (kernels_rand.cu): bit-exact assign_random on the GPU.
+size_t random_scratch_bytes(uint32_t n);
+size_t random_cub_bytes(uint32_t n);
+bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, void* scratch, void* cub_tmp,
+                          size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches);
+
 }  // namespace sky

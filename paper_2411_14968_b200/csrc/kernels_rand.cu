@@ -1,0 +1,264 @@
+// kernels_rand.cu — the reference's random partitioner on the GPU, bit-exact.
+//
+// assign_random (partition.cpp:36-54) shuffles 0..n-1 with Fisher-Yates
+// driven by Rng(seed) = std::mt19937_64 (rng.hpp:15-60): for i = n..2,
+// j_i = below(i) (rejection sampling, x % i), swap(v[i-1], v[j_i]); then
+// partition_of[perm[k]] = k mod p. Here:
+//   1. one CTA produces the mt19937_64 output stream (the twist runs as two
+//      156-wide dependent phases; the standard's published parameters);
+//   2. j_i = x_k % i for k = n - i, in parallel; a draw that the reference
+//      would reject (x >= 2^64 - 2^64 mod i, probability ~n^2/2^65) raises a
+//      flag and the caller reproduces the shuffle on the host instead;
+//   3. the swap sequence is resolved without executing it: let S_p be the
+//      steps with j_i = p. Position i-1 is final after step i, so
+//      perm[i-1] = g(i), the value at j_i just before step i, and the value
+//      at position p just before step i is f(i*) for the next-larger step i*
+//      in S_p (or p itself), where f(i) = value at i-1 just before step i
+//      follows the same rule on S_{i-1}. Sorting (j_i, i) gives every S_p; f
+//      is resolved by pointer jumping (pointers only increase), g and the
+//      partition ids in one final pass.
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace sky {
+
+namespace {
+
+constexpr int MT_N = 312, MT_M = 156;
+constexpr uint64_t MT_UM = 0xFFFFFFFF80000000ull, MT_LM = 0x7FFFFFFFull;
+
+__device__ __forceinline__ uint64_t mt_tw(uint64_t a, uint64_t b) {
+    const uint64_t x = (a & MT_UM) | (b & MT_LM);
+    return (x >> 1) ^ ((x & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+}
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
+    x ^= (x >> 29) & 0x5555555555555555ull;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+    x ^= (x << 37) & 0xFFF7EEE000000000ull;
+    x ^= x >> 43;
+    return x;
+}
+
+// Untempered mt19937_64(seed) state sequence -> out[0..count): the state
+// words form one sequence x[m] = x[m-156] ^ tw(x[m-312], x[m-311])
+// (x[0..311] = seeded state; output k = temper(x[312+k]), applied by the
+// parallel consumer). Terms m0+t and m0+156+t (t < 156) depend only on
+// earlier groups, except that m0+311 needs x[m0], which thread 155
+// recomputes; so a 624-term ring needs one barrier per 312 outputs.
+__global__ void __launch_bounds__(160) k_mt64(uint64_t seed, uint32_t count, uint64_t* __restrict__ out) {
+    constexpr uint32_t R = 2 * MT_N;
+    __shared__ uint64_t x[R];
+    const uint32_t t = threadIdx.x;
+    if (t == 0) {
+        x[0] = seed;
+        for (int i = 1; i < MT_N; ++i) x[i] = 6364136223846793005ull * (x[i - 1] ^ (x[i - 1] >> 62)) + (uint64_t)i;
+    }
+    __syncthreads();
+    uint32_t r0 = MT_N;  // ring position of m0
+    for (uint32_t k0 = 0; k0 < count; k0 += MT_N) {
+        uint64_t v0 = 0, v1 = 0;
+        uint32_t p0 = 0, p1 = 0;
+        if (t < MT_M) {
+            auto at = [&](uint32_t back) {  // x[m0 + t - back]
+                uint32_t q = r0 + t + R - back;
+                while (q >= R) q -= R;
+                return x[q];
+            };
+            const uint64_t a = at(MT_M), b = at(MT_N), c = at(MT_N - 1);
+            v0 = a ^ mt_tw(b, c);                              // x[m0 + t]
+            uint64_t c2;                                       // x[m0 + t - 155]
+            if (t + 1 < MT_M) {
+                c2 = at(MT_M - 1);
+            } else {                                           // x[m0], recomputed
+                uint32_t q0 = r0 + R - MT_M, q1 = r0 + R - MT_N, q2 = r0 + R - MT_N + 1;
+                while (q0 >= R) q0 -= R;
+                while (q1 >= R) q1 -= R;
+                while (q2 >= R) q2 -= R;
+                c2 = x[q0] ^ mt_tw(x[q1], x[q2]);
+            }
+            v1 = v0 ^ mt_tw(a, c2);                            // x[m0 + 156 + t]
+            p0 = r0 + t;
+            if (p0 >= R) p0 -= R;
+            p1 = p0 + MT_M;
+            if (p1 >= R) p1 -= R;
+        }
+        __syncthreads();  // every read of the previous groups is done
+        if (t < MT_M) {
+            x[p0] = v0;
+            x[p1] = v1;
+            if (k0 + t < count) out[k0 + t] = v0;
+            if (k0 + MT_M + t < count) out[k0 + MT_M + t] = v1;
+        }
+        r0 += MT_N;
+        if (r0 >= R) r0 -= R;
+        __syncthreads();
+    }
+}
+
+// step i = n - k: j_i = x_k mod i, key (j_i << 32 | i); flag a rejected draw
+__global__ void k_fy_draws(const uint64_t* __restrict__ x, uint32_t n, uint64_t* __restrict__ key,
+                           uint32_t* __restrict__ jv, uint32_t* flag) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k + 1 >= n) return;  // n-1 steps
+    const uint64_t i = (uint64_t)n - k;
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % i;
+    const uint64_t v = mt_temper(x[k]);
+    if (v >= limit) atomicOr(flag, 1u);
+    const uint32_t j = (uint32_t)(v % i);
+    jv[k] = j;
+    key[k] = ((uint64_t)j << 32) | (uint32_t)i;
+}
+
+__global__ void k_fy_heads(const uint64_t* __restrict__ key, uint32_t m, uint32_t* __restrict__ head) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    const uint32_t p = (uint32_t)(key[q] >> 32);
+    if (q == 0 || (uint32_t)(key[q - 1] >> 32) != p) head[p] = q;
+}
+
+// gnext[i]: next larger step in S_{j_i}; f pointers for every step i.
+__global__ void k_fy_ptrs(const uint64_t* __restrict__ key, uint32_t m, const uint32_t* __restrict__ head, uint32_t n,
+                          uint32_t* __restrict__ gnext, uint32_t* __restrict__ fptr, uint32_t* __restrict__ fval) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < m) {
+        const uint32_t p = (uint32_t)(key[q] >> 32), i = (uint32_t)key[q];
+        gnext[i] = (q + 1 < m && (uint32_t)(key[q + 1] >> 32) == p) ? (uint32_t)key[q + 1] : kNone;
+    }
+    const uint32_t i = q + 2;  // steps 2..n
+    if (i <= n) {
+        const uint32_t h = head[i - 1];
+        uint32_t v = kNone;
+        if (h != kNone) {
+            v = (uint32_t)key[h];
+            if (v == i) {
+                const uint32_t h2 = h + 1;
+                v = (h2 < m && (uint32_t)(key[h2] >> 32) == i - 1) ? (uint32_t)key[h2] : kNone;
+            }
+        }
+        if (v == kNone) {
+            fval[i] = i - 1;  // position i-1 untouched before step i
+            fptr[i] = kNone;
+        } else {
+            fval[i] = kNone;
+            fptr[i] = v;
+        }
+    }
+}
+
+// pointer jumping until every f is resolved (cooperative: grid-wide sync)
+__global__ void k_fy_jump(uint32_t n, uint32_t* __restrict__ fptr, uint32_t* __restrict__ fval, uint32_t* pending) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (int round = 0; round < 64; ++round) {
+        uint32_t local = 0;
+        for (uint32_t i = 2 + blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
+            if (fval[i] != kNone) continue;
+            const uint32_t j = fptr[i];
+            const uint32_t vj = ((volatile uint32_t*)fval)[j];
+            if (vj != kNone) {
+                fval[i] = vj;
+            } else {
+                fptr[i] = ((volatile uint32_t*)fptr)[j];
+                ++local;
+            }
+        }
+        local = __reduce_add_sync(0xffffffffu, local);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(pending + (round & 1), local);
+        grid.sync();
+        const uint32_t left = pending[round & 1];
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) pending[(round + 1) & 1] = 0;
+        if (left == 0) break;
+        grid.sync();
+    }
+}
+
+// perm[k] (k >= 1) = g(k+1); perm[0] = value at 0 after its last touch.
+__global__ void k_fy_final(uint32_t n, uint64_t p, const uint32_t* __restrict__ jv, const uint32_t* __restrict__ gnext,
+                           const uint32_t* __restrict__ fval, const uint32_t* __restrict__ head,
+                           const uint64_t* __restrict__ key, uint32_t* __restrict__ pid) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    uint32_t v;
+    if (k == 0) {
+        const uint32_t h = head[0];
+        v = h == kNone ? 0u : fval[(uint32_t)key[h]];
+    } else {
+        const uint32_t i = k + 1;
+        const uint32_t gn = gnext[i];
+        v = gn != kNone ? fval[gn] : jv[n - i];
+    }
+    pid[v] = (uint32_t)(k % p);
+}
+
+}  // namespace
+
+size_t random_scratch_bytes(uint32_t n) {
+    // x (8n) + key (8n) + key2 (8n) + jv (4n) + head (4n) + gnext/fptr/fval (12(n+1)) + pending
+    return (size_t)n * 44 + 64;
+}
+
+// Partition ids of the reference's random assignment, on `st`. Returns false
+// (nothing written) when a draw would have been rejected; the caller then
+// reproduces the shuffle on the host. Synchronizes once to read the flag.
+bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, void* scratch, void* cub_tmp,
+                          size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches) {
+    if (n == 0) return true;
+    if (n == 1) {
+        SKY_CUDA(cudaMemsetAsync(pid, 0, sizeof(uint32_t), st));
+        return true;
+    }
+    char* s = static_cast<char*>(scratch);
+    uint64_t* x = reinterpret_cast<uint64_t*>(s);
+    uint64_t* key = x + n;
+    uint64_t* key2 = key + n;
+    uint32_t* jv = reinterpret_cast<uint32_t*>(key2 + n);
+    uint32_t* head = jv + n;
+    uint32_t* gnext = head + n;
+    uint32_t* fptr = gnext + (n + 1);
+    uint32_t* fval = fptr + (n + 1);
+    uint32_t* misc = fval + (n + 1);  // flag, pending[2]
+    const uint32_t m = n - 1;
+    SKY_CUDA(cudaMemsetAsync(misc, 0, 4 * sizeof(uint32_t), st));
+    SKY_CUDA(cudaMemsetAsync(head, 0xFF, (size_t)n * sizeof(uint32_t), st));
+    k_mt64<<<1, 160, 0, st>>>(seed, m, x);
+    k_fy_draws<<<ceil_div(m, 256), 256, 0, st>>>(x, n, key, jv, misc);
+    int end_bit = 32;
+    while (end_bit < 64 && (uint64_t{1} << (end_bit - 32)) < n) ++end_bit;
+    size_t need = 0;
+    SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, key, key2, (int)m, 0, end_bit, st));
+    if (need > cub_bytes) throw Error(SKY_E_INTERNAL, "cub scratch too small for the random partitioner");
+    SKY_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, need, key, key2, (int)m, 0, end_bit, st));
+    k_fy_heads<<<ceil_div(m, 256), 256, 0, st>>>(key2, m, head);
+    k_fy_ptrs<<<ceil_div(n, 256), 256, 0, st>>>(key2, m, head, n, gnext, fptr, fval);
+    {
+        int per_sm = 0;
+        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fy_jump, 256, 0));
+        const int grid = std::max(1, std::min(per_sm * sm_count, (int)ceil_div(n, 256)));
+        uint32_t nn = n;
+        uint32_t* pending = misc + 1;
+        void* args[] = {&nn, &fptr, &fval, &pending};
+        SKY_CUDA(cudaLaunchCooperativeKernel((void*)k_fy_jump, grid, 256, args, 0, st));
+    }
+    k_fy_final<<<ceil_div(n, 256), 256, 0, st>>>(n, p, jv, gnext, fval, head, key2, pid);
+    SKY_LAUNCH_CHECK();
+    if (launches) *launches += 7 + 4;
+    uint32_t flag = 0;
+    SKY_CUDA(cudaMemcpyAsync(&flag, misc, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    SKY_CUDA(cudaStreamSynchronize(st));
+    return flag == 0;
+}
+
+size_t random_cub_bytes(uint32_t n) {
+    if (n < 2) return 16;
+    size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)(n - 1), 0, 64,
+                                   (cudaStream_t)0);
+    return need;
+}
+
+}  // namespace sky

@@ -215,3 +215,17 @@ def test_full_c1_vs_oracle(engine):
     assert np.array_equal(r.skyline, exp["ids"])
     assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist()
     check_metrics(r, exp, "c1")
+
+
+@pytest.mark.parametrize("n,p,seed", [(2, 1, 0), (3, 2, 5), (1000, 7, 42), (65_537, 32, 42), (2_000_000, 32, 42),
+                                      (100_000, 8, 42), (300_001, 5, 123456789)])
+def test_random_assignment_matches_reference_shuffle(engine, n, p, seed):
+    """assign_random (partition.cpp:36-54) resolved on the GPU must equal the
+    sequential Fisher-Yates with mt19937_64 (rng.hpp:40-60)."""
+    x = np.zeros((n, 2), np.float32)
+    po, cnt = engine.make_assignment(x, PartitionConfig(Strategy.Random, p=p, seed=seed))
+    perm = O.random_permutation(n, seed)
+    exp = np.empty(n, np.uint64)
+    exp[perm] = np.arange(n, dtype=np.uint64) % p
+    assert cnt == p
+    assert np.array_equal(po, exp)
