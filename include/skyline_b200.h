@@ -119,6 +119,13 @@ typedef struct sky_ctx sky_ctx;
  * staging buffers. One call in flight per context. */
 SKY_API int sky_ctx_create(int device, sky_ctx** out);
 SKY_API void sky_ctx_destroy(sky_ctx* ctx);
+/* Multi-GPU: one rank per process. Rank 0 creates the NCCL unique id
+ * (128 bytes), every rank passes it with (rank, world); sky_run on such a
+ * context shards the local and merge phases over the ranks and returns the
+ * full result on every rank (parallel_for fan-out of parallel.cpp:11-43
+ * replaced by NCCL over NVLink). */
+SKY_API int sky_nccl_unique_id(uint8_t* out, uint64_t size);
+SKY_API int sky_ctx_create_dist(int device, int rank, int world, const uint8_t* unique_id, sky_ctx** out);
 SKY_API const char* sky_last_error(const sky_ctx* ctx);
 /* Optional external stream (cudaStream_t passed as void*); NULL restores the
  * context's own stream. */
@@ -176,6 +183,13 @@ SKY_API int sky_plan_lpt(const uint64_t* weights, uint64_t count, int ranks, int
 /* Balanced contiguous split of `count` candidates with per-candidate cost
  * prefix sums: bounds[ranks+1]. */
 SKY_API int sky_plan_split(const uint64_t* cost_prefix, uint64_t count, int ranks, uint64_t* bounds);
+/* The shard plans sky_run uses on a multi-rank context: local phase =
+ * contiguous partition ranges of the filtered set (offsets off[P+1]),
+ * merge phase = contiguous candidate-partition ranges of the union
+ * (offsets offu[P+1]); bounds[world+1]. m = slices per dimension (grid). */
+SKY_API int sky_plan_local_shards(const uint32_t* off, uint64_t P, int world, uint32_t* bounds);
+SKY_API int sky_plan_merge_shards(const uint32_t* offu, uint64_t P, int world, const sky_config* cfg,
+                                  uint32_t d, uint64_t m, uint32_t* bounds);
 
 SKY_API int sky_abi_version(void);
 

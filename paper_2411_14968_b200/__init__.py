@@ -7,6 +7,7 @@ package is the host-side mirror of the reference's engine API.
 from .skyline import (  # noqa: F401
     ConfigError, CudaError, DataError, DimensionError, Engine, EngineConfig, FilterKind, IoError, LocalAlgo,
     MergeKind, NcclError, NormalizationError, PartitionConfig, PhaseMetrics, RepSelection, RunResult,
-    SkylineError, Strategy, default_engine, generate, plan_lpt, plan_split, run, snap_slices,
+    SkylineError, Strategy, default_engine, generate, nccl_unique_id, plan_local_shards, plan_lpt, plan_merge_shards,
+    plan_split, run, snap_slices,
 )
 from .configs import BASELINE_CONFIGS, make_config  # noqa: F401

@@ -83,11 +83,12 @@ class SkyResult(C.Structure):
 # Every symbol include/skyline_b200.h declares; tests check the library
 # exports all of them.
 EXPORTED = [
-    "sky_ctx_create", "sky_ctx_destroy", "sky_last_error", "sky_ctx_set_stream",
+    "sky_ctx_create", "sky_ctx_destroy", "sky_nccl_unique_id", "sky_ctx_create_dist",
+    "sky_last_error", "sky_ctx_set_stream",
     "sky_config_default", "sky_run", "sky_result_free", "sky_assign",
     "sky_snap_slices", "sky_relative_skyline", "sky_skyline",
     "sky_representatives", "sky_free", "sky_generate", "sky_plan_lpt",
-    "sky_plan_split", "sky_abi_version",
+    "sky_plan_split", "sky_plan_local_shards", "sky_plan_merge_shards", "sky_abi_version",
 ]
 
 _lib = None
@@ -110,6 +111,8 @@ def load():
     vp = C.c_void_p
     lib.sky_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
     lib.sky_ctx_destroy.argtypes = [vp]
+    lib.sky_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8), C.c_uint64]
+    lib.sky_ctx_create_dist.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(vp)]
     lib.sky_last_error.argtypes = [vp]
     lib.sky_last_error.restype = C.c_char_p
     lib.sky_ctx_set_stream.argtypes = [vp, vp]
@@ -127,6 +130,10 @@ def load():
     lib.sky_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, _f32p]
     lib.sky_plan_lpt.argtypes = [_u64p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]
     lib.sky_plan_split.argtypes = [_u64p, C.c_uint64, C.c_int, _u64p]
+    _u32p = C.POINTER(C.c_uint32)
+    lib.sky_plan_local_shards.argtypes = [_u32p, C.c_uint64, C.c_int, _u32p]
+    lib.sky_plan_merge_shards.argtypes = [_u32p, C.c_uint64, C.c_int, C.POINTER(SkyConfig), C.c_uint32, C.c_uint64,
+                                          _u32p]
     lib.sky_abi_version.restype = C.c_int
     _lib = lib
     return lib

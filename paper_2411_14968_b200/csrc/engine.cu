@@ -26,9 +26,20 @@
 #include <thread>
 #include <vector>
 
+#include <nccl.h>
+
 #include "kernels.cuh"
 
 using namespace sky;
+
+extern "C" int sky_plan_split(const uint64_t* cost_prefix, uint64_t count, int ranks, uint64_t* bounds);
+
+#define SKY_NCCL(call)                                                                   \
+    do {                                                                                 \
+        ncclResult_t r_ = (call);                                                        \
+        if (r_ != ncclSuccess)                                                           \
+            throw ::sky::Error(SKY_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
 
 struct sky_ctx {
     int device = 0;
@@ -44,6 +55,9 @@ struct sky_ctx {
     uint32_t launches = 0;
     uint32_t dom_launches = 0;
     double dom_ms = 0.0;
+    // multi-GPU: one rank per process, NCCL over NVLink/NVSwitch
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
 };
 
 namespace {
@@ -54,7 +68,7 @@ enum Slot {
     S_SET0, S_SET0_K, S_SET0_I, S_SET0_Q, S_SET1, S_SET1_K, S_SET1_I, S_SET1_Q,
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
-    S_OVF, S_SKTMP, S_THR, S_RAND, S_COUNT
+    S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -123,6 +137,69 @@ uint64_t angular_index_host(const float* x, uint32_t d, uint64_t m) {
         stride *= m;
     }
     return index;
+}
+
+// Contiguous ranges of P units over `ranks` owners with balanced weight
+// (sky_plan_split); bounds[r]..bounds[r+1] belong to rank r.
+template <class F>
+std::vector<uint32_t> plan_ranges(const std::vector<uint32_t>& off, uint32_t P, int ranks, F weight) {
+    (void)off;
+    std::vector<uint32_t> b(ranks + 1, 0);
+    b[ranks] = P;
+    if (ranks == 1) return b;
+    std::vector<uint64_t> prefix(P + 1, 0);
+    for (uint32_t p = 0; p < P; ++p) prefix[p + 1] = prefix[p] + weight(p);
+    std::vector<uint64_t> bounds(ranks + 1);
+    sky_plan_split(prefix.data(), P, ranks, bounds.data());
+    for (int r = 0; r <= ranks; ++r) b[r] = (uint32_t)bounds[r];
+    return b;
+}
+
+// Local-phase shards: contiguous partition ranges balanced by |r_i|^2 (the
+// SFS/BNL cost of a partition).
+std::vector<uint32_t> plan_local_shards(const std::vector<uint32_t>& off, uint32_t P, int W) {
+    return plan_ranges(off, P, W, [&](uint32_t p) {
+        const uint64_t np = off[p + 1] - off[p];
+        return np * np + np;
+    });
+}
+
+bool weak_grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d);
+
+// Potential dominators of partition i (engine.cpp:74-114) as ranges of the
+// union (partition order); empty for strategies merged against all of U.
+void pd_ranges(const std::vector<uint32_t>& offu, const std::vector<uint32_t>& nonempty, uint32_t i, int strategy,
+               uint64_t m, uint32_t d, std::vector<uint2>& comps) {
+    comps.clear();
+    if (strategy == SKY_SLICED) {  // pd_i = u_j, j < i (engine.cpp:106-108)
+        for (uint32_t j : nonempty) {  // one range per slice: each stays sum-key sorted
+            if (j >= i) break;
+            comps.push_back(make_uint2(offu[j], offu[j + 1]));
+        }
+    } else if (strategy == SKY_GRID) {  // weakly dominating non-empty cells (engine.cpp:92-104)
+        for (uint32_t j : nonempty)
+            if (j != i && weak_grid_dom(j, i, m, d)) comps.push_back(make_uint2(offu[j], offu[j + 1]));
+    }
+}
+
+// Merge-phase shards: contiguous candidate-partition ranges balanced by the
+// number of candidate x potential-dominator pairs.
+std::vector<uint32_t> plan_merge_shards(const std::vector<uint32_t>& offu, uint32_t P, int W, bool all_mode,
+                                        int strategy, uint64_t m, uint32_t d) {
+    std::vector<uint32_t> nonempty;
+    for (uint32_t p = 0; p < P; ++p)
+        if (offu[p + 1] > offu[p]) nonempty.push_back(p);
+    std::vector<uint2> comps;
+    const uint64_t U = offu[P];
+    return plan_ranges(offu, P, W, [&](uint32_t i) -> uint64_t {
+        const uint64_t ni = offu[i + 1] - offu[i];
+        if (!ni) return 0;
+        if (all_mode) return ni * U;
+        pd_ranges(offu, nonempty, i, strategy, m, d, comps);
+        uint64_t cmp = 0;
+        for (uint2 r : comps) cmp += r.y - r.x;
+        return ni * (cmp + 1);
+    });
 }
 
 struct Plan {
@@ -321,6 +398,79 @@ class Runner {
     uint32_t pick_tile(int D, uint64_t n_cands) const {
         if (D > 16) return kTile;
         return n_cands >= (uint64_t)c_->sm_count * 8 * 256 ? 256u : 128u;
+    }
+
+    // ----------------------------------------------------------- NCCL
+    // Local skylines of all ranks in partition order on every rank: sizes by
+    // all-reduce, rows by one grouped broadcast per owner (an all-gather-v).
+    DevSet gather_union(int D, const DevSet& Um, const std::vector<uint32_t>& offum, const std::vector<uint32_t>& pr,
+                        uint32_t P, std::vector<uint32_t>& offu, uint32_t* offu_dev) {
+        const int W = c_->world, rank = c_->rank;
+        const uint32_t pb = pr[rank], pe = pr[rank + 1];
+        uint32_t* sizes = dev<uint32_t>(S_SIZES, P);
+        uint32_t* h = pin<uint32_t>(P_OFF, P + 2);
+        std::memset(h, 0, P * sizeof(uint32_t));
+        for (uint32_t p = pb; p < pe; ++p) h[p] = offum[p - pb + 1] - offum[p - pb];
+        SKY_CUDA(cudaMemcpyAsync(sizes, h, P * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        SKY_NCCL(ncclAllReduce(sizes, sizes, P, ncclUint32, ncclSum, c_->comm, st_));
+        SKY_CUDA(cudaMemcpyAsync(h, sizes, P * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        sync();
+        offu.assign(P + 1, 0);
+        for (uint32_t p = 0; p < P; ++p) offu[p + 1] = offu[p] + h[p];
+        std::memcpy(h, offu.data(), (P + 1) * sizeof(uint32_t));
+        SKY_CUDA(cudaMemcpyAsync(offu_dev, h, (P + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        DevSet Ug = set(S_SET1, offu[P], D);
+        const size_t D4 = (size_t)(D + 3) / 4 * 4;
+        SKY_NCCL(ncclGroupStart());
+        for (int q = 0; q < W; ++q) {
+            const uint32_t lo = offu[pr[q]], cnt = offu[pr[q + 1]] - lo;
+            if (!cnt) continue;
+            const bool me = q == rank;
+            SKY_NCCL(ncclBroadcast(me ? (const void*)Um.xyz : Ug.xyz + lo * D4, Ug.xyz + lo * D4, cnt * D4,
+                                   ncclFloat32, q, c_->comm, st_));
+            SKY_NCCL(ncclBroadcast(me ? (const void*)Um.skey : Ug.skey + lo, Ug.skey + lo, cnt, ncclUint32, q,
+                                   c_->comm, st_));
+            SKY_NCCL(ncclBroadcast(me ? (const void*)Um.id : Ug.id + lo, Ug.id + lo, cnt, ncclUint32, q, c_->comm,
+                                   st_));
+            if (Ug.qc)
+                SKY_NCCL(ncclBroadcast(me ? (const void*)Um.qc : Ug.qc + lo, Ug.qc + lo, 2 * (size_t)cnt, ncclUint32,
+                                       q, c_->comm, st_));
+        }
+        SKY_NCCL(ncclGroupEnd());
+        return Ug;
+    }
+
+    // All ranks' survivor ids (each rank's list from its candidate range),
+    // concatenated and sorted ascending into `out`; returns the count.
+    uint32_t gather_ids(const uint32_t* mine, uint32_t nmine, uint32_t* out) {
+        const int W = c_->world, rank = c_->rank;
+        uint32_t* cnt = dev<uint32_t>(S_GCOUNT, W + 1);
+        uint32_t* h = pin<uint32_t>(P_RUNS, W + 1);
+        h[0] = nmine;
+        SKY_CUDA(cudaMemcpyAsync(cnt + W, h, sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        SKY_NCCL(ncclAllGather(cnt + W, cnt, 1, ncclUint32, c_->comm, st_));
+        SKY_CUDA(cudaMemcpyAsync(h, cnt, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        sync();
+        std::vector<uint32_t> displ(W + 1, 0);
+        for (int q = 0; q < W; ++q) displ[q + 1] = displ[q] + h[q];
+        const uint32_t total = displ[W];
+        uint32_t* all = dev<uint32_t>(S_PERM_A, total);
+        SKY_NCCL(ncclGroupStart());
+        for (int q = 0; q < W; ++q) {
+            if (!h[q]) continue;
+            SKY_NCCL(ncclBroadcast(q == rank ? (const void*)mine : all + displ[q], all + displ[q], h[q], ncclUint32, q,
+                                   c_->comm, st_));
+        }
+        SKY_NCCL(ncclGroupEnd());
+        sort_keys(all, out, total);
+        return total;
+    }
+
+    // dominance-test and exact-check counters summed over ranks
+    void reduce_counters() {
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        SKY_NCCL(ncclAllReduce(misc + M_TESTS, misc + M_TESTS, 3, ncclUint64, ncclSum, c_->comm, st_));
+        SKY_NCCL(ncclAllReduce(misc + M_HITS, misc + M_HITS, 4, ncclUint64, ncclSum, c_->comm, st_));
     }
 
     // partition_of of assign_random (partition.cpp:36-54) on the device; the
@@ -797,14 +947,51 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     out->filtered_count = grid_filtered + rep_filtered;
 
     // ----------------------------------------------------- local skylines
+    // Multi-GPU: every rank holds the same s0 (phase 1a above is replicated);
+    // the local phase is sharded by contiguous, cost-balanced partition
+    // ranges, and the local skylines are all-gathered over NCCL.
+    const int W = c->world, rank = c->rank;
+    std::vector<uint32_t> pr = plan_local_shards(off1, P, W);
+    const uint32_t pb = pr[rank], pe = pr[rank + 1];
     std::vector<uint32_t> offu;
-    uint32_t* offu_dev = R.dev<uint32_t>(S_OFF_A, P + 1);  // partition offsets no longer needed
+    uint32_t* offu_dev = R.dev<uint32_t>(S_OFF_A, P + 1);
     DevSet U;
-    if (cfg->local_algo == SKY_LOCAL_BNL) {
-        uint32_t used = 0;
-        U = R.local_bnl(D, s0, off1_dev, P, cfg->bnl_window_cap, offu_dev, offu, count_tests, &used);
-    } else {
-        U = R.local_sfs(D, s0, off1, off1_dev, P, offu_dev, offu, count_tests);
+    {
+        // view of this rank's partitions
+        const uint32_t base = off1[pb], cnt = off1[pe] - base;
+        const int D4 = (D + 3) / 4 * 4;
+        DevSet mine = s0;
+        if (W > 1) {
+            mine.xyz = s0.xyz + (size_t)base * D4;
+            mine.skey = s0.skey + base;
+            mine.id = s0.id + base;
+            mine.qc = s0.qc ? s0.qc + base : nullptr;
+            mine.n = cnt;
+        }
+        const uint32_t Pm = pe - pb;
+        std::vector<uint32_t> offm(Pm + 1);
+        for (uint32_t k = 0; k <= Pm; ++k) offm[k] = off1[pb + k] - base;
+        uint32_t* offm_dev = off1_dev;
+        if (W > 1) {
+            offm_dev = R.dev<uint32_t>(S_OFF_C, Pm + 1);
+            uint32_t* h = R.pin<uint32_t>(P_OFF, Pm + 1);
+            std::memcpy(h, offm.data(), (Pm + 1) * sizeof(uint32_t));
+            SKY_CUDA(cudaMemcpyAsync(offm_dev, h, (Pm + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        }
+        std::vector<uint32_t> offum;
+        DevSet Um;
+        if (cfg->local_algo == SKY_LOCAL_BNL) {
+            uint32_t used = 0;
+            Um = R.local_bnl(D, mine, offm_dev, Pm, cfg->bnl_window_cap, offu_dev, offum, count_tests, &used);
+        } else {
+            Um = R.local_sfs(D, mine, offm, offm_dev, Pm, offu_dev, offum, count_tests);
+        }
+        if (W == 1) {
+            U = Um;
+            offu = offum;
+        } else {
+            U = R.gather_union(D, Um, offum, pr, P, offu, offu_dev);
+        }
     }
     SKY_CUDA(cudaEventRecord(c->ev[2], st));
     for (uint32_t p = 0; p < P; ++p) out->local_skyline_sizes[p] = offu[p + 1] - offu[p];
@@ -817,9 +1004,15 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     ma.cxyz = U.xyz; ma.cskey = U.skey; ma.bounded = true; ma.dead = fdead;
     ma.tests = count_tests ? R.tests(2) : nullptr;
     Plan mp;
-    mp.tile = R.pick_tile(D, U.n);
+    mp.tile = R.pick_tile(D, W > 1 ? U.n / W : U.n);
     const bool all_mode = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
                           cfg->strategy == SKY_ANGULAR;
+    std::vector<uint32_t> nonempty;
+    for (uint32_t p = 0; p < P; ++p)
+        if (offu[p + 1] > offu[p]) nonempty.push_back(p);
+    // the merge is sharded by candidate partitions, balanced by test volume
+    const std::vector<uint32_t> mr = plan_merge_shards(offu, P, W, all_mode, cfg->strategy, m, d);
+    const uint32_t qb = mr[rank], qe = mr[rank + 1];
     DevSet US;
     if (all_mode && P > 1) {
         // Sky(U) against the whole union sorted by sum key: for random and
@@ -831,8 +1024,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         uint32_t* perm = R.dev<uint32_t>(S_PERM_B, U.n);
         uint32_t* sk2 = R.dev<uint32_t>(S_SKTMP, U.n);
         {
-            // iota on device via the id array trick: pos = exclusive scan of
-            // all-live flags
+            // iota on device: exclusive scan of all-live flags
             uint8_t* z = R.dev<uint8_t>(S_DEAD, U.n);
             launch_fill_u8(z, 0, U.n, st);
             R.scan_live(z, iota, U.n);
@@ -840,72 +1032,50 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         R.sort_pairs(U.skey, sk2, iota, perm, U.n, 0, 32);
         launch_gather_set(D, U, perm, US, st);
         R.count();
-        for (uint32_t p = 0; p < P; ++p)
+        for (uint32_t p = qb; p < qe; ++p)
             for (uint32_t b = offu[p]; b < offu[p + 1]; b += mp.tile)
                 mp.add(b, std::min(offu[p + 1], b + mp.tile), {make_uint2(0, U.n)});
         ma.sxyz = US.xyz; ma.sskey = US.skey;
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
-        std::vector<uint32_t> nonempty;
-        for (uint32_t p = 0; p < P; ++p)
-            if (offu[p + 1] > offu[p]) nonempty.push_back(p);
         std::vector<uint2> comps;
         for (uint32_t i : nonempty) {
-            comps.clear();
-            if (cfg->strategy == SKY_SLICED) {  // pd_i = u_j, j < i (engine.cpp:106-108)
-                // one range per slice so each range stays sum-key sorted
-                for (uint32_t j : nonempty) {
-                    if (j >= i) break;
-                    comps.push_back(make_uint2(offu[j], offu[j + 1]));
-                }
-            } else {  // grid: weakly dominating non-empty cells (engine.cpp:92-104)
-                for (uint32_t j : nonempty)
-                    if (j != i && weak_grid_dom(j, i, m, d)) comps.push_back(make_uint2(offu[j], offu[j + 1]));
-            }
+            if (i < qb || i >= qe) continue;
+            pd_ranges(offu, nonempty, i, cfg->strategy, m, d, comps);
             if (comps.empty()) continue;
             for (uint32_t b = offu[i]; b < offu[i + 1]; b += mp.tile)
                 mp.add(b, std::min(offu[i + 1], b + mp.tile), comps);
         }
     }
     mp.order();
-    if (const char* dump = std::getenv("SKY_DEBUG_DUMP")) {
-        // debug aid: union set + codes + thresholds as raw little-endian arrays
-        R.sync();
-        const int D4 = (D + 3) / 4 * 4;
-        std::vector<float> hx((size_t)U.n * D4), ht((size_t)D * (kCodeLevels - 1));
-        std::vector<uint32_t> hk(U.n), hq(2 * (size_t)U.n);
-        SKY_CUDA(cudaMemcpy(hx.data(), U.xyz, hx.size() * 4, cudaMemcpyDeviceToHost));
-        SKY_CUDA(cudaMemcpy(hk.data(), U.skey, hk.size() * 4, cudaMemcpyDeviceToHost));
-        if (U.qc) SKY_CUDA(cudaMemcpy(hq.data(), U.qc, hq.size() * 4, cudaMemcpyDeviceToHost));
-        SKY_CUDA(cudaMemcpy(ht.data(), R.dev<float>(S_THR, ht.size()), ht.size() * 4, cudaMemcpyDeviceToHost));
-        FILE* f = std::fopen(dump, "wb");
-        uint32_t hdr[3] = {U.n, (uint32_t)D, (uint32_t)D4};
-        std::fwrite(hdr, 4, 3, f);
-        std::fwrite(hx.data(), 4, hx.size(), f);
-        std::fwrite(hk.data(), 4, hk.size(), f);
-        std::fwrite(hq.data(), 4, hq.size(), f);
-        std::fwrite(ht.data(), 4, ht.size(), f);
-        std::fclose(f);
-    }
     R.relsky(D, mp, ma, U.qc, all_mode && P > 1 ? US.qc : U.qc);
 
-    // surviving ids, ascending (engine.cpp:128-133)
-    uint32_t* pos = R.dev<uint32_t>(S_POS, U.n);
-    R.scan_live(fdead, pos, U.n);
-    launch_count_total(pos, fdead, U.n, misc + M_TOTAL, st);
+    // surviving ids of this rank's candidates, ascending (engine.cpp:128-133)
+    const uint32_t cb = offu[qb], cn = offu[qe] - cb;
+    uint32_t* pos = R.dev<uint32_t>(S_POS, cn);
+    R.scan_live(fdead + cb, pos, cn);
+    launch_count_total(pos, fdead + cb, cn, misc + M_TOTAL, st);
     R.count();
     uint32_t* hm = R.pin<uint32_t>(P_MISC, 32);
     SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     R.sync();
-    const uint32_t nf = U.n ? hm[0] : 0;
-    uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, nf);
-    uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, nf);
-    launch_compact_ids(U.id, fdead, pos, U.n, idsA, st);
+    const uint32_t nmine = cn ? hm[0] : 0;
+    uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, std::max<uint32_t>(nmine, U.n));
+    uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, std::max<uint32_t>(nmine, U.n));
+    launch_compact_ids(U.id + cb, fdead + cb, pos, cn, idsA, st);
     R.count();
-    R.sort_keys(idsA, idsB, nf);
+    uint32_t nf = nmine;
+    uint32_t* final_ids = idsB;
+    if (W == 1) {
+        R.sort_keys(idsA, idsB, nf);
+    } else {
+        nf = R.gather_ids(idsA, nmine, idsB);  // all ranks' survivors, then sorted
+        final_ids = idsB;
+        R.reduce_counters();
+    }
     SKY_CUDA(cudaEventRecord(c->ev[3], st));
     uint32_t* hid = R.pin<uint32_t>(P_IDS, nf);
-    SKY_CUDA(cudaMemcpyAsync(hid, idsB, (size_t)nf * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    SKY_CUDA(cudaMemcpyAsync(hid, final_ids, (size_t)nf * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     unsigned long long* ht = reinterpret_cast<unsigned long long*>(hm + 4);
     SKY_CUDA(cudaMemcpyAsync(ht, R.tests(0), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SKY_CUDA(cudaMemcpyAsync(ht + 3, misc + M_HITS, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -996,9 +1166,40 @@ int sky_ctx_create(int device, sky_ctx** out) {
     return SKY_OK;
 }
 
+int sky_nccl_unique_id(uint8_t* out, uint64_t size) {
+    return guarded(nullptr, [&] {
+        if (size < sizeof(ncclUniqueId)) throw Error(SKY_E_CONFIG, "unique id buffer too small");
+        ncclUniqueId id;
+        SKY_NCCL(ncclGetUniqueId(&id));
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int sky_ctx_create_dist(int device, int rank, int world, const uint8_t* unique_id, sky_ctx** out) {
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return SKY_E_CONFIG;
+    sky_ctx* c = nullptr;
+    int rc = sky_ctx_create(device, &c);
+    if (rc != SKY_OK) return rc;
+    rc = guarded(c, [&] {
+        c->rank = rank;
+        c->world = world;
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        SKY_NCCL(ncclCommInitRank(&c->comm, world, id, rank));
+    });
+    if (rc != SKY_OK) {
+        sky_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return SKY_OK;
+}
+
 void sky_ctx_destroy(sky_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->comm) ncclCommDestroy(c->comm);
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -1209,5 +1410,26 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
 }
 
 void sky_free(void* p) { std::free(p); }
+
+int sky_plan_local_shards(const uint32_t* off, uint64_t P, int world, uint32_t* bounds) {
+    return guarded(nullptr, [&] {
+        if (world < 1) throw Error(SKY_E_CONFIG, "world must be >= 1");
+        std::vector<uint32_t> o(off, off + P + 1);
+        const auto b = plan_local_shards(o, (uint32_t)P, world);
+        std::memcpy(bounds, b.data(), (world + 1) * sizeof(uint32_t));
+    });
+}
+
+int sky_plan_merge_shards(const uint32_t* offu, uint64_t P, int world, const sky_config* cfg, uint32_t d,
+                          uint64_t m, uint32_t* bounds) {
+    return guarded(nullptr, [&] {
+        if (world < 1) throw Error(SKY_E_CONFIG, "world must be >= 1");
+        std::vector<uint32_t> o(offu, offu + P + 1);
+        const bool all_mode = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
+                              cfg->strategy == SKY_ANGULAR;
+        const auto b = plan_merge_shards(o, (uint32_t)P, world, all_mode, cfg->strategy, m, d);
+        std::memcpy(bounds, b.data(), (world + 1) * sizeof(uint32_t));
+    });
+}
 
 }  // extern "C"

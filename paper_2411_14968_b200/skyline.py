@@ -204,6 +204,21 @@ class Engine:
         self._h = h
         self.device = device
 
+    @classmethod
+    def distributed(cls, device: int, rank: int, world: int, unique_id: bytes) -> "Engine":
+        """A rank of a multi-GPU engine (one process per GPU): every rank
+        calls run() on the same input; the local and merge phases are
+        sharded over the ranks with NCCL and every rank gets the result."""
+        self = cls.__new__(cls)
+        self._lib = abi.load()
+        h = C.c_void_p()
+        buf = (C.c_uint8 * len(unique_id)).from_buffer_copy(unique_id)
+        rc = self._lib.sky_ctx_create_dist(device, rank, world, buf, C.byref(h))
+        _raise(rc, "sky_ctx_create_dist failed")
+        self._h = h
+        self.device = device
+        return self
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.sky_ctx_destroy(self._h)
@@ -347,6 +362,31 @@ def generate(kind: int, n: int, d: int, seed: int) -> np.ndarray:
     rc = abi.load().sky_generate(kind, n, d, seed, out.ctypes.data_as(C.POINTER(C.c_float)))
     _raise(rc)
     return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _raise(abi.load().sky_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def plan_local_shards(off, ranks: int) -> np.ndarray:
+    """Partition ranges per rank for the local phase (what sky_run uses)."""
+    o = np.ascontiguousarray(off, dtype=np.uint32)
+    b = np.zeros(ranks + 1, np.uint32)
+    _raise(abi.load().sky_plan_local_shards(o.ctypes.data_as(C.POINTER(C.c_uint32)), len(o) - 1, ranks,
+                                            b.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return b
+
+
+def plan_merge_shards(offu, ranks: int, config: EngineConfig, d: int, m: int = 0) -> np.ndarray:
+    """Candidate-partition ranges per rank for the merge phase."""
+    o = np.ascontiguousarray(offu, dtype=np.uint32)
+    b = np.zeros(ranks + 1, np.uint32)
+    cfg = config.to_c()
+    _raise(abi.load().sky_plan_merge_shards(o.ctypes.data_as(C.POINTER(C.c_uint32)), len(o) - 1, ranks,
+                                            C.byref(cfg), d, m, b.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return b
 
 
 def plan_lpt(weights, ranks: int) -> np.ndarray:

@@ -229,3 +229,20 @@ def test_random_assignment_matches_reference_shuffle(engine, n, p, seed):
     exp[perm] = np.arange(n, dtype=np.uint64) % p
     assert cnt == p
     assert np.array_equal(po, exp)
+
+
+def test_distributed_context_single_rank():
+    """The NCCL-backed context (world = 1 on this box) runs the same path and
+    returns the reference result."""
+    from paper_2411_14968_b200 import Engine, nccl_unique_id
+    eng = Engine.distributed(0, 0, 1, nccl_unique_id())
+    try:
+        for idx, n in ((2, 30_000), (4, 8_000), (3, 200_000)):
+            w = make_config(idx, n)
+            x = generate(w.kind, w.n, w.d, 42)
+            exp = O.oracle_run(x, w.config.to_c(), w.normalized)
+            r = eng.run(x, w.config, w.normalized)
+            assert np.array_equal(r.skyline, exp["ids"])
+            assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist()
+    finally:
+        eng.close()
