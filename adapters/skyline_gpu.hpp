@@ -1,0 +1,104 @@
+// skyline_gpu.hpp — drop-in adapter: the reference engine API (skyline::run,
+// /root/reference/proj/include/skyline/engine.hpp:88) served by the B200
+// engine through the C ABI in include/skyline_b200.h.
+//
+// A maintainer of the reference adds this header next to engine.hpp and calls
+// skyline::gpu::run(dataset, config) where skyline::run was called; the
+// returned RunResult carries the same skyline (id-sorted Points) and the same
+// PhaseMetrics fields (engine.hpp:40-57). Errors come back as the reference's
+// exception classes (core.hpp:13-34).
+//
+// Requirements: coordinates exactly representable in float32 (the GPU engine
+// compares float32; the BASELINE inputs are float32), d <= 32, and one
+// sky_ctx per thread.
+#pragma once
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "skyline/core.hpp"
+#include "skyline/engine.hpp"
+#include "skyline_b200.h"
+
+namespace skyline::gpu {
+
+inline void throw_status(int rc, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (rc) {
+        case SKY_OK: return;
+        case SKY_E_CONFIG: throw ConfigError(m);
+        case SKY_E_DIMENSION: throw DimensionError(m);
+        case SKY_E_NORMALIZATION: throw NormalizationError(m);
+        case SKY_E_DATA: throw DataError(m);
+        case SKY_E_IO: throw IoError(m);
+        default: throw SkylineError("skyline_b200: " + m);
+    }
+}
+
+struct Context {
+    sky_ctx* ctx = nullptr;
+    explicit Context(int device = 0) { throw_status(sky_ctx_create(device, &ctx), "sky_ctx_create failed"); }
+    ~Context() { sky_ctx_destroy(ctx); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+};
+
+inline sky_config to_sky(const EngineConfig& e) {
+    sky_config c;
+    sky_config_default(&c);
+    c.strategy = static_cast<int32_t>(e.partition.strategy);
+    c.p = e.partition.p;
+    c.m = e.partition.m;
+    c.seed = e.partition.seed;
+    c.slice_dim = e.partition.slice_dim;
+    c.filter = static_cast<int32_t>(e.filter);
+    c.rep_selection = static_cast<int32_t>(e.rep_selection);
+    c.rep_q = e.rep_q;
+    c.merge = static_cast<int32_t>(e.merge);
+    c.workers = e.workers;
+    return c;
+}
+
+// skyline::run on the GPU (engine.hpp:88). Ids of the input points are
+// preserved (core.cpp:43 assigns them in row order; Dataset ids are used as
+// given here).
+inline RunResult run(Context& g, const Dataset& r, const EngineConfig& config) {
+    const size_t n = r.size(), d = r.d;
+    std::vector<float> rows(n * d);
+    for (size_t i = 0; i < n; ++i) {
+        const Point& t = r.points[i];
+        if (t.dim() != d) throw DimensionError("ragged dataset");
+        for (size_t j = 0; j < d; ++j) {
+            const float f = static_cast<float>(t.coords[j]);
+            if (static_cast<double>(f) != t.coords[j] && std::isfinite(t.coords[j]))
+                throw DataError("coordinate not representable in float32");
+            rows[i * d + j] = f;
+        }
+    }
+    const sky_config c = to_sky(config);
+    sky_result res;
+    throw_status(sky_run(g.ctx, rows.data(), n, static_cast<uint32_t>(d), r.normalized ? 1 : 0, 0, &c, &res),
+                 sky_last_error(g.ctx));
+    RunResult out;
+    out.config = config;
+    out.effective_p = res.effective_p;
+    out.input_size = n;
+    out.input_dim = d;
+    out.skyline.points.reserve(res.n_ids);
+    for (uint64_t k = 0; k < res.n_ids; ++k) out.skyline.points.push_back(r.points[res.ids[k]]);
+    PhaseMetrics& m = out.metrics;
+    m.partition_ms = res.partition_ms;
+    m.local_ms = res.local_ms;
+    m.merge_ms = res.merge_ms;
+    m.local_skyline_sizes.assign(res.local_skyline_sizes, res.local_skyline_sizes + res.effective_p);
+    m.union_size = res.union_size;
+    m.filtered_count = res.filtered_count;
+    m.final_size = res.final_size;
+    sky_result_free(&res);
+    return out;
+}
+
+}  // namespace skyline::gpu

@@ -1,0 +1,39 @@
+"""The drop-in adapter (adapters/skyline_gpu.hpp) compiles against the
+reference's own headers and links against libskyline_b200.so (CPU-side
+check; needs /root/reference, present only in the build container)."""
+import os
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_INC = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not present")
+def test_adapter_compiles_and_links_against_reference_headers():
+    from paper_2411_14968_b200 import abi
+    abi.load()
+    src = r'''
+#include "skyline_gpu.hpp"
+int main(int argc, char**) {
+    if (argc > 1) {  // never executed here: no GPU in the build container
+        skyline::gpu::Context g(0);
+        skyline::Dataset r;
+        skyline::EngineConfig c;
+        auto res = skyline::gpu::run(g, r, c);
+        return (int)res.skyline.size();
+    }
+    return 0;
+}
+'''
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "a.cpp")
+        open(p, "w").write(src)
+        exe = os.path.join(td, "a")
+        libdir = os.path.join(ROOT, "paper_2411_14968_b200")
+        subprocess.run(["g++", "-std=c++20", "-I", REF_INC, "-I", os.path.join(ROOT, "include"),
+                        "-I", os.path.join(ROOT, "adapters"), p, "-L", libdir, "-lskyline_b200",
+                        f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+        assert subprocess.run([exe]).returncode == 0
