@@ -203,52 +203,51 @@ std::vector<uint32_t> plan_merge_shards(const std::vector<uint32_t>& offu, uint3
 }
 
 struct Plan {
-    uint32_t tile = kTile;  // candidates per item
+    uint32_t tile = kTile;    // candidates per item
+    uint32_t chunk = kChunk;  // comparators per item before the key bound
     std::vector<Item> items;
     std::vector<uint2> ranges;
     std::vector<uint32_t> group;  // item wave (comparator chunk index)
-    std::vector<uint64_t> work;
 
     // candidates [cb,ce) vs comparator ranges, split into groups of at most
-    // kChunk comparators; items of group g launch after those of group g-1.
-    void add(uint32_t cb, uint32_t ce, const std::vector<uint2>& comps, uint32_t chunk = kChunk) {
+    // `chunk` comparators; items of group g launch after those of group g-1
+    // (so dominated candidates found by earlier chunks are skipped later).
+    void add(uint32_t cb, uint32_t ce, const std::vector<uint2>& comps, uint32_t ch = 0) {
+        if (!ch) ch = chunk;
         uint32_t g = 0, acc = 0;
         uint32_t lb = (uint32_t)ranges.size();
-        auto flush = [&](bool force) {
-            if ((uint32_t)ranges.size() > lb || force) {
-                if ((uint32_t)ranges.size() > lb) {
-                    items.push_back(Item{cb, ce, lb, (uint32_t)ranges.size()});
-                    group.push_back(g);
-                    work.push_back((uint64_t)acc * (ce - cb));
-                    ++g;
-                }
-                lb = (uint32_t)ranges.size();
-                acc = 0;
+        auto flush = [&]() {
+            if ((uint32_t)ranges.size() > lb) {
+                items.push_back(Item{cb, ce, lb, (uint32_t)ranges.size()});
+                group.push_back(g);
+                ++g;
             }
+            lb = (uint32_t)ranges.size();
+            acc = 0;
         };
         for (uint2 r : comps) {
             uint32_t b = r.x;
             while (b < r.y) {
-                const uint32_t take = std::min(r.y - b, chunk - acc);
+                const uint32_t take = std::min(r.y - b, ch - acc);
                 ranges.push_back(make_uint2(b, b + take));
                 b += take;
                 acc += take;
-                if (acc >= chunk) flush(false);
+                if (acc >= ch) flush();
             }
         }
-        flush(false);
+        flush();
     }
 
-    // Launch order: by wave, then by descending work inside a wave.
+    // Launch order by wave: a stable counting pass over the group index.
     void order() {
-        std::vector<uint32_t> ix(items.size());
-        for (uint32_t i = 0; i < ix.size(); ++i) ix[i] = i;
-        std::stable_sort(ix.begin(), ix.end(), [&](uint32_t a, uint32_t b) {
-            if (group[a] != group[b]) return group[a] < group[b];
-            return work[a] > work[b];
-        });
+        if (items.empty()) return;
+        uint32_t G = 0;
+        for (uint32_t g : group) G = std::max(G, g + 1);
+        std::vector<uint32_t> start(G + 1, 0);
+        for (uint32_t g : group) ++start[g + 1];
+        for (uint32_t g = 0; g < G; ++g) start[g + 1] += start[g];
         std::vector<Item> it2(items.size());
-        for (uint32_t i = 0; i < ix.size(); ++i) it2[i] = items[ix[i]];
+        for (size_t i = 0; i < items.size(); ++i) it2[start[group[i]]++] = items[i];
         items.swap(it2);
     }
 };
@@ -348,6 +347,20 @@ class Runner {
     void relsky(int D, const Plan& plan, const RelskyArgs& base, const uint2* cq = nullptr,
                 const uint2* sq = nullptr) {
         if (plan.items.empty()) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        struct Report {
+            const Plan& p;
+            std::chrono::steady_clock::time_point t0;
+            sky_ctx* c;
+            ~Report() {
+                if (std::getenv("SKY_PROFILE_HOST")) {
+                    const double ms =
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                    std::fprintf(stderr, "relsky items=%zu ranges=%zu tile=%u chunk=%u host+wait=%.3f ms dom_total=%.3f\n",
+                                 p.items.size(), p.ranges.size(), p.tile, p.chunk, ms, c->dom_ms);
+                }
+            }
+        } report{plan, t0, c_};
         Item* hi = pin<Item>(P_ITEMS, plan.items.size());
         uint2* hr = pin<uint2>(P_RANGES, plan.ranges.size());
         std::memcpy(hi, plan.items.data(), plan.items.size() * sizeof(Item));
@@ -393,11 +406,26 @@ class Runner {
         c_->dom_launches += 1;
     }
 
-    // candidates per relsky item: big tiles amortize comparator staging,
-    // small ones keep enough items in flight on 148 SMs
-    uint32_t pick_tile(int D, uint64_t n_cands) const {
-        if (D > 16) return kTile;
-        return n_cands >= (uint64_t)c_->sm_count * 8 * 256 ? 256u : 128u;
+    // Item granularity: candidates per item (one warp, 32*K) and comparators
+    // per item before the key bound. Big items amortize comparator staging;
+    // small ones keep ~16 items per resident warp slot so 148 SMs stay busy
+    // and load balances. `pairs` = candidate x comparator pairs of the launch
+    // (before bounding).
+    void pick_grain(int D, uint64_t n_cands, uint64_t pairs, uint32_t* tile, uint32_t* chunk) const {
+        if (D > 16) {
+            *tile = kTile;
+            *chunk = kChunk;
+            return;
+        }
+        // ~4 items per resident CTA (8 warps share an item's comparators);
+        // shrink the comparator chunk first (keeps 256-candidate tiles), the
+        // candidate tile only when candidates are few
+        const uint64_t target = (uint64_t)c_->sm_count * 2 * 4;
+        uint32_t t = 256, ch = 16384;
+        while (ch > 2048 && n_cands && pairs / ((uint64_t)t * ch) < target) ch /= 2;
+        while (t > 32 && n_cands && n_cands / t < (uint64_t)c_->sm_count * 2) t /= 2;
+        *tile = t;
+        *chunk = ch;
     }
 
     // ----------------------------------------------------------- NCCL
@@ -522,12 +550,16 @@ class Runner {
         uint8_t* dead1 = dev<uint8_t>(S_DEAD, s1.n);
         launch_fill_u8(dead1, 0, s1.n, st_);
         Plan loc;
-        loc.tile = pick_tile(D, s1.n);
+        {
+            uint64_t pairs = 0;
+            for (uint32_t p = 0; p < P; ++p) pairs += (uint64_t)(off1[p + 1] - off1[p]) * (off1[p + 1] - off1[p]) / 2;
+            pick_grain(D, s1.n, pairs, &loc.tile, &loc.chunk);
+        }
         for (uint32_t p = 0; p < P; ++p) {
             const uint32_t b0 = off1[p], e0 = off1[p + 1];
             for (uint32_t b = b0; b < e0; b += loc.tile) {
                 const uint32_t e = std::min(b + loc.tile, e0);
-                loc.add(b, e, {make_uint2(b0, e0)});
+                loc.add(b, e, {make_uint2(b0, e0)}, loc.chunk);
             }
         }
         loc.order();
@@ -891,12 +923,16 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         }
         uint8_t* cdead = R.dev<uint8_t>(S_CELLDEAD, nc);
         launch_fill_u8(cdead, 0, nc, st);
-        Plan pp;
-        for (uint32_t b = 0; b < nc; b += kTile) pp.add(b, std::min(nc, b + (uint32_t)kTile), {make_uint2(0, nc)});
-        RelskyArgs ra{};
-        ra.cxyz = css.xyz; ra.cskey = css.skey; ra.sxyz = css.xyz; ra.sskey = css.skey;
-        ra.bounded = true; ra.dead = cdead; ra.tests = count_tests ? R.tests(0) : nullptr;
-        R.relsky(D, pp, ra);
+        if (launch_small_skyline(D, css.xyz, nc, cdead, count_tests ? R.tests(0) : nullptr, c->smem_optin, st)) {
+            R.count();
+        } else {
+            Plan pp;
+            for (uint32_t b = 0; b < nc; b += kTile) pp.add(b, std::min(nc, b + (uint32_t)kTile), {make_uint2(0, nc)});
+            RelskyArgs ra{};
+            ra.cxyz = css.xyz; ra.cskey = css.skey; ra.sxyz = css.xyz; ra.sskey = css.skey;
+            ra.bounded = true; ra.dead = cdead; ra.tests = count_tests ? R.tests(0) : nullptr;
+            R.relsky(D, pp, ra);
+        }
         std::vector<uint32_t> roff;
         uint32_t zero_off[2] = {0, nc};
         uint32_t* doff = R.dev<uint32_t>(S_OFF_B, 2);
@@ -909,7 +945,11 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         out->n_reps = reps.n;
 
         // rep_prefilter over every row, in partition/sum order (indirect)
-        if (reps.n > 0) {
+        if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, po.key64, n, reps.xyz, reps.skey, reps.n, dead,
+                                           count_tests ? R.tests(1) : nullptr, c->smem_optin, st)) {
+            R.count();
+            any_dead = true;
+        } else if (reps.n > 0) {
             Plan pf;
             for (uint32_t b = 0; b < n; b += kTile) pf.add(b, std::min(n, b + (uint32_t)kTile), {make_uint2(0, reps.n)});
             RelskyArgs fa{};
@@ -1004,7 +1044,6 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     ma.cxyz = U.xyz; ma.cskey = U.skey; ma.bounded = true; ma.dead = fdead;
     ma.tests = count_tests ? R.tests(2) : nullptr;
     Plan mp;
-    mp.tile = R.pick_tile(D, W > 1 ? U.n / W : U.n);
     const bool all_mode = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
                           cfg->strategy == SKY_ANGULAR;
     std::vector<uint32_t> nonempty;
@@ -1013,6 +1052,21 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     // the merge is sharded by candidate partitions, balanced by test volume
     const std::vector<uint32_t> mr = plan_merge_shards(offu, P, W, all_mode, cfg->strategy, m, d);
     const uint32_t qb = mr[rank], qe = mr[rank + 1];
+    {
+        uint64_t pairs = 0, cands = offu[qe] - offu[qb];
+        std::vector<uint2> comps;
+        for (uint32_t i = qb; i < qe; ++i) {
+            const uint64_t ni = offu[i + 1] - offu[i];
+            if (!ni) continue;
+            if (all_mode) {
+                pairs += ni * (uint64_t)U.n / 2;
+            } else {
+                pd_ranges(offu, nonempty, i, cfg->strategy, m, d, comps);
+                for (uint2 r : comps) pairs += ni * (r.y - r.x) / 2;
+            }
+        }
+        R.pick_grain(D, cands, pairs, &mp.tile, &mp.chunk);
+    }
     DevSet US;
     if (all_mode && P > 1) {
         // Sky(U) against the whole union sorted by sum key: for random and
@@ -1034,7 +1088,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         R.count();
         for (uint32_t p = qb; p < qe; ++p)
             for (uint32_t b = offu[p]; b < offu[p + 1]; b += mp.tile)
-                mp.add(b, std::min(offu[p + 1], b + mp.tile), {make_uint2(0, U.n)});
+                mp.add(b, std::min(offu[p + 1], b + mp.tile), {make_uint2(0, U.n)}, mp.chunk);
         ma.sxyz = US.xyz; ma.sskey = US.skey;
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
@@ -1044,7 +1098,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
             pd_ranges(offu, nonempty, i, cfg->strategy, m, d, comps);
             if (comps.empty()) continue;
             for (uint32_t b = offu[i]; b < offu[i + 1]; b += mp.tile)
-                mp.add(b, std::min(offu[i + 1], b + mp.tile), comps);
+                mp.add(b, std::min(offu[i + 1], b + mp.tile), comps, mp.chunk);
         }
     }
     mp.order();

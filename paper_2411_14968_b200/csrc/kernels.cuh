@@ -149,6 +149,14 @@ uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
                  cudaStream_t st);
 
+// Streaming representative prefilter (false: not applicable, use k_relsky).
+bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64, uint32_t n,
+                      const float* rep_xyz, const uint32_t* rep_key, uint32_t nrep, uint8_t* dead,
+                      unsigned long long* tests, int smem_optin, cudaStream_t st);
+// Skyline of one small set in one CTA (false: too big, use k_relsky).
+bool launch_small_skyline(int D, const float* xyz, uint32_t n, uint8_t* dead, unsigned long long* tests,
+                          int smem_optin, cudaStream_t st);
+
 // Random partitioner (kernels_rand.cu): bit-exact assign_random on the GPU.
 size_t random_scratch_bytes(uint32_t n);
 size_t random_cub_bytes(uint32_t n);

@@ -13,8 +13,10 @@
 // LOP3 and one predicate-accumulating ISETP (ALU pipe), instead of D FP32
 // compares on the ALU pipe.
 //
-// Work distribution: persistent warps pull host-planned items (<= 256
+// Work distribution: persistent CTAs pull host-planned items (<= 256
 // candidates x comparator ranges) from an atomic counter in launch order.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -54,40 +56,29 @@ struct CodeLayout {
 constexpr int kSample = 4096;
 constexpr int kThr = kCodeLevels - 1;  // 127 thresholds per dimension
 
-// One CTA per dimension: sort a strided sample of the column and keep 127
-// quantiles as thresholds.
+// One CTA per dimension: block radix sort of a strided sample of the column
+// (2048 rows), keep 127 quantiles as thresholds.
+constexpr int kThrThreads = 512, kThrItems = 4;
 template <int D>
-__global__ void __launch_bounds__(512) k_thresholds(DevSet s, float* thr) {
+__global__ void __launch_bounds__(kThrThreads) k_thresholds(DevSet s, float* thr) {
     constexpr int D4 = Dims2<D>::V * 4;
-    __shared__ float v[kSample];
+    constexpr int SMP = kThrThreads * kThrItems;
+    using Sort = cub::BlockRadixSort<float, kThrThreads, kThrItems>;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ float v[SMP];
     const int j = blockIdx.x;
-    const uint32_t S = s.n < (uint32_t)kSample ? s.n : (uint32_t)kSample;
-    for (int i = threadIdx.x; i < kSample; i += blockDim.x) {
-        float x = __int_as_float(0x7f800000);  // +inf padding
-        if ((uint32_t)i < S) {
-            const uint64_t row = (uint64_t)i * s.n / S;
-            x = s.xyz[row * D4 + j];
-        }
-        v[i] = x;
+    const uint32_t S = s.n < (uint32_t)SMP ? s.n : (uint32_t)SMP;
+    float keys[kThrItems];
+#pragma unroll
+    for (int k = 0; k < kThrItems; ++k) {
+        const uint32_t i = threadIdx.x * kThrItems + k;
+        keys[k] = __int_as_float(0x7f800000);  // +inf padding sorts last
+        if (i < S) keys[k] = s.xyz[((uint64_t)i * s.n / S) * D4 + j];
     }
+    Sort(tmp).Sort(keys);
+#pragma unroll
+    for (int k = 0; k < kThrItems; ++k) v[threadIdx.x * kThrItems + k] = keys[k];
     __syncthreads();
-    // bitonic sort of kSample floats
-    for (int k = 2; k <= kSample; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < kSample; i += blockDim.x) {
-                const int p = i ^ jj;
-                if (p > i) {
-                    const float a = v[i], b = v[p];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        v[i] = b;
-                        v[p] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
     for (int k = threadIdx.x; k < kThr; k += blockDim.x) {
         uint32_t idx = S ? (uint32_t)(((uint64_t)(k + 1) * S) / kCodeLevels) : 0;
         if (idx >= S) idx = S ? S - 1 : 0;
@@ -159,20 +150,24 @@ __device__ __forceinline__ uint32_t range_end(const Relsky2Args& a, uint2 rg) {
     return (rg.y & 0x80000000u) ? rg.x + a.wcount[rg.y & 0x7FFFFFFFu] : rg.y;
 }
 
-// Warp-autonomous dominance core: every warp fetches its own item
-// (<= 32*K candidates, lane l owns candidates cb + 32k + l), streams the
-// comparator ranges 32 at a time through its private shared-memory slot
-// (codes, keys and coordinates of the next batch are prefetched into
-// registers while the current one is tested), stops a range when a ballot
-// shows the sorted keys passed the warp's bound and leaves the item once every
-// candidate is dominated. Exact checks read both points from shared memory.
-// No CTA barriers.
+// Dominance core. A CTA of RS3_WARPS warps takes one item: <= 32*K candidates
+// (lane l of every warp holds candidates cb + 32k + l as packed codes in
+// registers) against a list of comparator ranges, each sorted by sum key.
+// The warps split the comparator stream: warp w handles batches w, w+8, ...
+// of 32 comparators (codes, keys and coordinates of its next batch are
+// prefetched into registers while the current one is tested) and stops a
+// range once a ballot shows the sorted keys passed the item's bound. A kill
+// is published in a shared-memory mask that every warp folds into its alive
+// bits before each batch, so no warp keeps testing a dominated candidate.
+// Exact checks read both points from shared memory.
 template <int D, int K>
 struct Relsky3Smem {
     static constexpr int V = Dims2<D>::V;
-    float4 cand[K][V][32];  // [k][v][lane]: conflict-free per-lane reads
-    float4 comp[32][V];     // current comparator batch (broadcast reads)
-    uint2 code[32];
+    float4 cand[K][V][32];             // [k][v][lane]: conflict-free per-lane reads
+    float4 comp[RS3_WARPS][32][V];     // each warp's current batch (broadcast reads)
+    uint2 code[RS3_WARPS][32];
+    uint32_t deadmask[32];             // bit k of word l: candidate (k, l) dominated
+    uint32_t item, bound;
 };
 
 template <int D, int K>
@@ -182,15 +177,16 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
     constexpr uint32_t FULL = 0xffffffffu;
     extern __shared__ float4 smem_raw[];
     using S = Relsky3Smem<D, K>;
+    S& sm = *reinterpret_cast<S*>(smem_raw);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    S& sm = reinterpret_cast<S*>(smem_raw)[warp];
     unsigned long long ntests = 0, nhits = 0;
 
     for (;;) {
-        uint32_t item = 0;
-        if (lane == 0) item = atomicAdd(a.counter, 1u);
-        item = __shfl_sync(FULL, item, 0);
+        if (threadIdx.x == 0) sm.item = atomicAdd(a.counter, 1u);
+        if (threadIdx.x < 32) sm.deadmask[threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t item = sm.item;
         if (item >= a.n_items) break;
         const Item it = a.items[item];
 
@@ -209,20 +205,25 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                 T[k][0] = q.x | G | CodeLayout<D>::ALIVE;
                 T[k][1] = q.y | G | 0x80000000u;
                 my_max = max(my_max, a.cskey[c]);
-                const float4* x = reinterpret_cast<const float4*>(a.cxyz) + (size_t)c * W;
+                if (warp == 0) {
+                    const float4* x = reinterpret_cast<const float4*>(a.cxyz) + (size_t)c * W;
 #pragma unroll
-                for (int v = 0; v < W; ++v) sm.cand[k][v][lane] = x[v];
+                    for (int v = 0; v < W; ++v) sm.cand[k][v][lane] = x[v];
+                }
             }
         }
         const uint32_t initial = alive;
         const uint32_t bound = a.bounded ? __reduce_max_sync(FULL, my_max) : 0xFFFFFFFFu;
+        __syncthreads();  // candidate coordinates staged
         bool live = __any_sync(FULL, alive != 0);
 
         for (uint32_t r = it.lb; live && r < it.le; ++r) {
             const uint2 rg = a.ranges[r];
             const uint32_t sb = rg.x, se = range_end(a, rg);
-            // prefetch the first batch
-            uint32_t idx = sb + lane;
+            uint32_t base = sb + warp * 32;
+            if (base >= se) continue;
+            // prefetch this warp's first batch
+            uint32_t idx = base + lane;
             uint2 nq = make_uint2(0, 0);
             uint32_t nk = 0xFFFFFFFFu;
             float4 nx[W];
@@ -233,15 +234,23 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 #pragma unroll
                 for (int v = 0; v < W; ++v) nx[v] = x[v];
             }
-            for (uint32_t base = sb; base < se; base += 32) {
+            for (; base < se; base += 32 * RS3_WARPS) {
+                // fold in kills published by the other warps
+                const uint32_t dm = sm.deadmask[lane];
+                if (dm & alive) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if ((dm >> k) & 1u) T[k][0] &= ~CodeLayout<D>::ALIVE;
+                    alive &= ~dm;
+                }
                 const uint32_t inb = __ballot_sync(FULL, nk <= bound);  // prefix (keys sorted)
                 const uint32_t lim = __popc(inb);
                 __syncwarp();
-                sm.code[lane] = nq;
+                sm.code[warp][lane] = nq;
 #pragma unroll
-                for (int v = 0; v < W; ++v) sm.comp[lane][v] = nx[v];
+                for (int v = 0; v < W; ++v) sm.comp[warp][lane][v] = nx[v];
                 __syncwarp();
-                idx = base + 32 + lane;
+                idx = base + 32 * RS3_WARPS + lane;
                 if (lim == 32 && idx < se) {
                     nq = a.sqc[idx];
                     nk = a.sskey[idx];
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                     nk = 0xFFFFFFFFu;
                 }
                 for (uint32_t i = 0; i < lim; ++i) {
-                    const uint2 q = sm.code[i];
+                    const uint2 q = sm.code[warp][i];
                     bool none = true;
 #pragma unroll
                     for (int k = 0; k < K; ++k) none &= !coarse_pass<G>(T[k], q);
@@ -265,13 +274,14 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                                 bool gt = false, lt = false;
 #pragma unroll
                                 for (int v = 0; v < W; ++v) {
-                                    const float4 sa = sm.comp[i][v], tb = sm.cand[k][v][lane];
+                                    const float4 sa = sm.comp[warp][i][v], tb = sm.cand[k][v][lane];
                                     gt |= (sa.x > tb.x) | (sa.y > tb.y) | (sa.z > tb.z) | (sa.w > tb.w);
                                     lt |= (sa.x < tb.x) | (sa.y < tb.y) | (sa.z < tb.z) | (sa.w < tb.w);
                                 }
                                 if (!gt && lt) {
                                     alive &= ~(1u << k);
                                     T[k][0] &= ~CodeLayout<D>::ALIVE;
+                                    atomicOr(&sm.deadmask[lane], 1u << k);
                                     ntests += i + 1;
                                 }
                             }
@@ -283,12 +293,16 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                 if (!live || lim < 32) break;  // all dominated, or past the key bound
             }
         }
-        uint32_t killed = initial & ~alive;
-        while (killed) {
-            const int k = __ffs(killed) - 1;
-            killed &= killed - 1;
-            a.dead[it.cb + k * 32 + lane] = 1;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t killed = initial & (sm.deadmask[lane] | ~alive);
+            while (killed) {
+                const int k = __ffs(killed) - 1;
+                killed &= killed - 1;
+                a.dead[it.cb + k * 32 + lane] = 1;
+            }
         }
+        __syncthreads();
     }
     if (a.tests) {
         ntests = warp_sum(ntests);
@@ -578,6 +592,91 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
     }
 }
 
+// ------------------------------------------------------------ prefilter
+// rep_prefilter (filter.cpp:147-159) over every row: one row per thread
+// (read through the sorted index, so a warp's rows have close keys), the
+// representatives resident in shared memory sorted by key; a row stops at its
+// first dominating representative, a warp at its key bound or when all its
+// rows are dominated.
+template <int D>
+__global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts, uint32_t d,
+                                                   const uint32_t* __restrict__ idx, const uint64_t* __restrict__ key64,
+                                                   uint32_t n, const float4* __restrict__ rep_xyz,
+                                                   const uint32_t* __restrict__ rep_key, uint32_t nrep,
+                                                   uint8_t* __restrict__ dead, unsigned long long* tests) {
+    constexpr int V = Dims2<D>::V;
+    extern __shared__ float4 s_rep[];
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_rep + (size_t)nrep * V);
+    for (uint32_t i = threadIdx.x; i < nrep * V; i += blockDim.x) s_rep[i] = rep_xyz[i];
+    for (uint32_t i = threadIdx.x; i < nrep; i += blockDim.x) s_key[i] = rep_key[i];
+    __syncthreads();
+    const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = pos < n && !dead[pos];
+    float t[4 * V];
+#pragma unroll
+    for (int j = 0; j < 4 * V; ++j) t[j] = 0.0f;
+    uint32_t tk = 0;
+    if (valid) {
+        const float* x = pts + (size_t)idx[pos] * d;
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if ((uint32_t)j < d) t[j] = x[j];
+        tk = (uint32_t)key64[pos];
+    }
+    bool alive = valid;
+    const uint32_t bound = __reduce_max_sync(0xffffffffu, alive ? tk : 0u);
+    uint32_t r = 0;
+    unsigned long long nt = 0;
+    if (__any_sync(0xffffffffu, alive)) {
+        for (; r < nrep; ++r) {
+            if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
+            const float4* sx = s_rep + r * V;
+            bool gt = false, lt = false;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const float4 a = sx[v];
+                gt |= (a.x > t[4 * v]) | (a.y > t[4 * v + 1]) | (a.z > t[4 * v + 2]) | (a.w > t[4 * v + 3]);
+                lt |= (a.x < t[4 * v]) | (a.y < t[4 * v + 1]) | (a.z < t[4 * v + 2]) | (a.w < t[4 * v + 3]);
+            }
+            if (alive) {
+                ++nt;
+                if (!gt && lt) alive = false;
+            }
+            if ((r & 7) == 7 && !__any_sync(0xffffffffu, alive)) break;
+        }
+    }
+    if (valid && !alive) dead[pos] = 1;
+    if (tests) {
+        nt = warp_sum(nt);
+        if ((threadIdx.x & 31) == 0 && nt) atomicAdd(tests, nt);
+    }
+}
+
+// skyline_bruteforce (core.cpp:56-73) of one small set (prune_dominated_reps,
+// filter.cpp:139-145): the set in shared memory, every thread tests its
+// points against all others.
+template <int D>
+__global__ void __launch_bounds__(1024) k_small_skyline(const float4* __restrict__ xyz, uint32_t n,
+                                                        uint8_t* __restrict__ dead, unsigned long long* tests) {
+    constexpr int V = Dims2<D>::V;
+    extern __shared__ float4 s_pts[];
+    for (uint32_t i = threadIdx.x; i < n * V; i += blockDim.x) s_pts[i] = xyz[i];
+    __syncthreads();
+    unsigned long long nt = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        bool dom = false;
+        for (uint32_t j = 0; j < n && !dom; ++j) {
+            ++nt;
+            if (j != i && dom_f4<D>(s_pts + j * V, s_pts + i * V)) dom = true;
+        }
+        dead[i] = dom ? 1 : 0;
+    }
+    if (tests) {
+        nt = warp_sum(nt);
+        if ((threadIdx.x & 31) == 0 && nt) atomicAdd(tests, nt);
+    }
+}
+
 #define SKY_DISPATCH_D16(D, ...)                                \
     switch (D) {                                                \
         case 2: { constexpr int DT = 2; __VA_ARGS__; break; }   \
@@ -595,14 +694,13 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
 template <int D, int K>
 void launch_k(const Relsky2Args& a, int sm_count, cudaStream_t st) {
     static int per_sm = 0;
-    const size_t smem = sizeof(Relsky3Smem<D, K>) * RS3_WARPS;
+    const size_t smem = sizeof(Relsky3Smem<D, K>);
     if (!per_sm) {
         SKY_CUDA(cudaFuncSetAttribute(k_relsky3<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_relsky3<D, K>, RS3_THREADS, smem));
         if (per_sm < 1) per_sm = 1;
     }
-    const uint64_t warps = std::min<uint64_t>(a.n_items, (uint64_t)per_sm * sm_count * RS3_WARPS);
-    const uint32_t grid = (uint32_t)((warps + RS3_WARPS - 1) / RS3_WARPS);
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(a.n_items, (uint64_t)per_sm * sm_count);
     k_relsky3<D, K><<<grid, RS3_THREADS, smem, st>>>(a);
     SKY_LAUNCH_CHECK();
 }
@@ -631,9 +729,40 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_
     SKY_DISPATCH_D16(D, (launch_bnl2_impl<DT>(a, qc, cap, grid, counter, st)));
 }
 
+bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64, uint32_t n,
+                      const float* rep_xyz, const uint32_t* rep_key, uint32_t nrep, uint8_t* dead,
+                      unsigned long long* tests, int smem_optin, cudaStream_t st) {
+    if (D > 16) return false;
+    const size_t smem = (size_t)nrep * ((D + 3) / 4) * 16 + (size_t)nrep * 4 + 16;
+    if (smem + 1024 > (size_t)smem_optin) return false;
+    if (!n) return true;
+    SKY_DISPATCH_D16(D, {
+        SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_prefilter<DT><<<ceil_div(n, 256), 256, smem, st>>>(pts, d, idx, key64, n,
+                                                            reinterpret_cast<const float4*>(rep_xyz), rep_key, nrep,
+                                                            dead, tests);
+    });
+    SKY_LAUNCH_CHECK();
+    return true;
+}
+
+bool launch_small_skyline(int D, const float* xyz, uint32_t n, uint8_t* dead, unsigned long long* tests,
+                          int smem_optin, cudaStream_t st) {
+    if (D > 16 || n > 4096) return false;
+    const size_t smem = (size_t)n * ((D + 3) / 4) * 16 + 16;
+    if (smem + 1024 > (size_t)smem_optin) return false;
+    if (!n) return true;
+    SKY_DISPATCH_D16(D, {
+        SKY_CUDA(cudaFuncSetAttribute(k_small_skyline<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_small_skyline<DT><<<1, 1024, smem, st>>>(reinterpret_cast<const float4*>(xyz), n, dead, tests);
+    });
+    SKY_LAUNCH_CHECK();
+    return true;
+}
+
 void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st) {
     if (!s.n) return;
-    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, 512, 0, st>>>(s, thr)));
+    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(s, thr)));
     SKY_LAUNCH_CHECK();
 }
 
@@ -645,7 +774,11 @@ void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st) {
 
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st) {
     if (!a.n_items) return;
-    if (tile <= 4 * 32) {
+    if (tile <= 1 * 32) {
+        SKY_DISPATCH_D16(D, (launch_k<DT, 1>(a, sm_count, st)));
+    } else if (tile <= 2 * 32) {
+        SKY_DISPATCH_D16(D, (launch_k<DT, 2>(a, sm_count, st)));
+    } else if (tile <= 4 * 32) {
         SKY_DISPATCH_D16(D, (launch_k<DT, 4>(a, sm_count, st)));
     } else if (tile <= 8 * 32) {
         SKY_DISPATCH_D16(D, (launch_k<DT, 8>(a, sm_count, st)));
