@@ -68,7 +68,7 @@ enum Slot {
     S_SET0, S_SET0_K, S_SET0_I, S_SET0_Q, S_SET1, S_SET1_K, S_SET1_I, S_SET1_Q,
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
-    S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_COUNT
+    S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -171,14 +171,30 @@ bool weak_grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d);
 void pd_ranges(const std::vector<uint32_t>& offu, const std::vector<uint32_t>& nonempty, uint32_t i, int strategy,
                uint64_t m, uint32_t d, std::vector<uint2>& comps) {
     comps.clear();
+    // Nearest potential dominators first: a dominated candidate usually has
+    // its dominator in an adjacent slice / cell, so scanning those first lets
+    // it leave early (the set, hence the result, is the reference's pd_i).
     if (strategy == SKY_SLICED) {  // pd_i = u_j, j < i (engine.cpp:106-108)
-        for (uint32_t j : nonempty) {  // one range per slice: each stays sum-key sorted
-            if (j >= i) break;
+        for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it) {  // one range per slice (sorted by key)
+            const uint32_t j = *it;
+            if (j >= i) continue;
             comps.push_back(make_uint2(offu[j], offu[j + 1]));
         }
     } else if (strategy == SKY_GRID) {  // weakly dominating non-empty cells (engine.cpp:92-104)
-        for (uint32_t j : nonempty)
-            if (j != i && weak_grid_dom(j, i, m, d)) comps.push_back(make_uint2(offu[j], offu[j + 1]));
+        std::vector<std::pair<uint64_t, uint32_t>> cells;
+        for (uint32_t j : nonempty) {
+            if (j == i || !weak_grid_dom(j, i, m, d)) continue;
+            uint64_t sum = 0, x = j;
+            for (uint32_t k = 0; k < d; ++k) {
+                sum += x % m;
+                x /= m;
+            }
+            cells.push_back({sum, j});
+        }
+        std::sort(cells.begin(), cells.end(), [](const auto& a, const auto& b) {
+            return a.first != b.first ? a.first > b.first : a.second > b.second;
+        });
+        for (const auto& c : cells) comps.push_back(make_uint2(offu[c.second], offu[c.second + 1]));
     }
 }
 
@@ -261,7 +277,16 @@ class Runner {
     T* dev(int slot, size_t n) { return c_->dev.as<T>(slot, n ? n : 1); }
     template <class T>
     T* pin(int slot, size_t n) { return c_->pin.as<T>(slot, n ? n : 1); }
-    void sync() { SKY_CUDA(cudaStreamSynchronize(st_)); }
+    void sync() {
+        SKY_CUDA(cudaStreamSynchronize(st_));
+        if (prof_) {
+            const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start_).count();
+            std::fprintf(stderr, "  sync #%d at %.3f ms\n", ++n_sync_, t);
+        }
+    }
+    bool prof_ = std::getenv("SKY_PROFILE_HOST") != nullptr;
+    int n_sync_ = 0;
+    std::chrono::steady_clock::time_point t_start_ = std::chrono::steady_clock::now();
     void count(int k = 1) { c_->launches += k; }
 
     DevSet set(int base, uint32_t n, int D) {
@@ -345,7 +370,7 @@ class Runner {
     }
 
     void relsky(int D, const Plan& plan, const RelskyArgs& base, const uint2* cq = nullptr,
-                const uint2* sq = nullptr) {
+                const uint2* sq = nullptr, const uint32_t* dense = nullptr) {
         if (plan.items.empty()) return;
         const auto t0 = std::chrono::steady_clock::now();
         struct Report {
@@ -378,6 +403,7 @@ class Runner {
             uint32_t* misc = dev<uint32_t>(S_MISC, 64);
             SKY_CUDA(cudaMemsetAsync(misc + M_WORK, 0, sizeof(uint32_t), st_));
             Relsky2Args b{};
+            b.cidx = dense;
             b.cxyz = a.cxyz; b.cskey = a.cskey; b.cqc = cq;
             b.sxyz = a.sxyz; b.sskey = a.sskey; b.sqc = sq;
             b.items = di; b.n_items = a.n_items; b.ranges = dr; b.bounded = a.bounded; b.dead = a.dead;
@@ -395,6 +421,82 @@ class Runner {
         // the pinned staging buffers are reused by the next call: make sure
         // the copies have consumed them first
         sync();
+    }
+
+    // Two-wave relative skyline of the candidates of partitions [qb, qe)
+    // (positions offc[p]..offc[p+1] of `C`) against their comparator ranges
+    // (comps_of(p), most likely dominators first). Wave A: every candidate vs
+    // the first `head` comparators of its list. The surviving candidates are
+    // then compacted into dense per-partition lists, so wave B (the rest of
+    // the list) runs full tiles of live candidates instead of tiles whose
+    // dominated slots still burn test issue.
+    template <class CompsOf>
+    void relsky_waves(int D, const std::vector<uint32_t>& offc, uint32_t qb, uint32_t qe, CompsOf comps_of,
+                      const RelskyArgs& base, const uint2* cq, const uint2* sq, uint32_t tile, uint32_t chunk,
+                      uint32_t head) {
+        if (qb >= qe) return;
+        std::vector<std::vector<uint2>> rest(qe - qb);
+        std::vector<uint2> comps, first;
+        Plan A;
+        A.tile = tile;
+        A.chunk = chunk;
+        uint64_t rest_total = 0;
+        for (uint32_t p = qb; p < qe; ++p) {
+            if (offc[p + 1] == offc[p]) continue;
+            comps_of(p, comps);
+            first.clear();
+            uint32_t budget = head;
+            size_t r = 0;
+            for (; r < comps.size() && budget; ++r) {
+                const uint32_t len = comps[r].y - comps[r].x;
+                if (len <= budget) {
+                    first.push_back(comps[r]);
+                    budget -= len;
+                } else {
+                    first.push_back(make_uint2(comps[r].x, comps[r].x + budget));
+                    rest[p - qb].push_back(make_uint2(comps[r].x + budget, comps[r].y));
+                    budget = 0;
+                }
+            }
+            for (; r < comps.size(); ++r) rest[p - qb].push_back(comps[r]);
+            for (const uint2& x : rest[p - qb]) rest_total += x.y - x.x;
+            if (first.empty()) continue;
+            for (uint32_t b = offc[p]; b < offc[p + 1]; b += tile) A.add(b, std::min(offc[p + 1], b + tile), first);
+        }
+        A.order();
+        relsky(D, A, base, cq, sq);
+        if (!rest_total) return;
+        // dense lists of the live candidates, per partition
+        const uint32_t cb = offc[qb], cn = offc[qe] - cb;
+        uint32_t* pos = dev<uint32_t>(S_POS, cn);
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        scan_live(base.dead + cb, pos, cn);
+        launch_count_total(pos, base.dead + cb, cn, misc + M_TOTAL, st_);
+        const uint32_t np = qe - qb;
+        uint32_t* hrel = pin<uint32_t>(P_OFF, np + 2);
+        for (uint32_t p = qb; p <= qe; ++p) hrel[p - qb] = offc[p] - cb;
+        uint32_t* drel = dev<uint32_t>(S_OFF_C, np + 1);
+        uint32_t* dnew = dev<uint32_t>(S_SIZES, np + 1);
+        SKY_CUDA(cudaMemcpyAsync(drel, hrel, (np + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        launch_remap_offsets(drel, np, pos, base.dead + cb, cn, dnew, st_);
+        uint32_t* dense = dev<uint32_t>(S_DENSE, cn);
+        launch_compact_pos(base.dead + cb, pos, cn, cb, dense, st_);
+        count(4);
+        uint32_t* hnew = pin<uint32_t>(P_RUNS, np + 1);
+        SKY_CUDA(cudaMemcpyAsync(hnew, dnew, (np + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        sync();
+        std::vector<uint32_t> doff(hnew, hnew + np + 1);
+        Plan B;
+        B.tile = tile;
+        B.chunk = chunk;
+        for (uint32_t p = qb; p < qe; ++p) {
+            const auto& rr = rest[p - qb];
+            if (rr.empty()) continue;
+            const uint32_t b0 = doff[p - qb], e0 = doff[p - qb + 1];
+            for (uint32_t b = b0; b < e0; b += tile) B.add(b, std::min(e0, b + tile), rr);
+        }
+        B.order();
+        relsky(D, B, base, cq, sq, dense);
     }
 
     // accumulate the CUDA-event time of the dominance launch just issued
@@ -549,22 +651,25 @@ class Runner {
 
         uint8_t* dead1 = dev<uint8_t>(S_DEAD, s1.n);
         launch_fill_u8(dead1, 0, s1.n, st_);
-        Plan loc;
-        {
+        RelskyArgs b2 = a;
+        b2.cxyz = s1.xyz; b2.cskey = s1.skey; b2.sxyz = s1.xyz; b2.sskey = s1.skey; b2.dead = dead1;
+        if (D <= 16 && s1.qc) {
             uint64_t pairs = 0;
             for (uint32_t p = 0; p < P; ++p) pairs += (uint64_t)(off1[p + 1] - off1[p]) * (off1[p + 1] - off1[p]) / 2;
-            pick_grain(D, s1.n, pairs, &loc.tile, &loc.chunk);
-        }
-        for (uint32_t p = 0; p < P; ++p) {
-            const uint32_t b0 = off1[p], e0 = off1[p + 1];
-            for (uint32_t b = b0; b < e0; b += loc.tile) {
-                const uint32_t e = std::min(b + loc.tile, e0);
-                loc.add(b, e, {make_uint2(b0, e0)}, loc.chunk);
+            uint32_t tile, chunk;
+            pick_grain(D, s1.n, pairs, &tile, &chunk);
+            relsky_waves(D, off1, 0, P, [&](uint32_t p, std::vector<uint2>& c) {
+                c.assign(1, make_uint2(off1[p], off1[p + 1]));
+            }, b2, s1.qc, s1.qc, tile, chunk, 2048);
+        } else {
+            Plan loc;
+            for (uint32_t p = 0; p < P; ++p) {
+                const uint32_t b0 = off1[p], e0 = off1[p + 1];
+                for (uint32_t b = b0; b < e0; b += loc.tile) loc.add(b, std::min(b + loc.tile, e0), {make_uint2(b0, e0)});
             }
+            loc.order();
+            relsky(D, loc, b2);
         }
-        loc.order();
-        a.cxyz = s1.xyz; a.cskey = s1.skey; a.sxyz = s1.xyz; a.sskey = s1.skey; a.dead = dead1;
-        relsky(D, loc, a, s1.qc, s1.qc);
         return compact(s1, dead1, off1_dev, P, S_SET2, off_u_dev, off_u, D);
     }
 
@@ -945,8 +1050,17 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         out->n_reps = reps.n;
 
         // rep_prefilter over every row, in partition/sum order (indirect)
-        if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, po.key64, n, reps.xyz, reps.skey, reps.n, dead,
-                                           count_tests ? R.tests(1) : nullptr, c->smem_optin, st)) {
+        float* pthr = nullptr;
+        if (reps.n >= 32 && D <= 16 && reps.qc) {
+            // one quantization for rows and representatives: quantiles of the input
+            pthr = R.dev<float>(S_PTHR, (size_t)D * (kCodeLevels - 1));
+            launch_thresholds_rows(D, pts, d, n, pthr, st);
+            launch_encode(D, reps, pthr, st);
+            R.count(2);
+        }
+        uint8_t* dead_row = R.dev<uint8_t>(S_DEADROW, n);
+        if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.n,
+                                           pthr, dead_row, dead, count_tests ? R.tests(1) : nullptr, c->smem_optin, st)) {
             R.count();
             any_dead = true;
         } else if (reps.n > 0) {
@@ -1086,23 +1200,42 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         R.sort_pairs(U.skey, sk2, iota, perm, U.n, 0, 32);
         launch_gather_set(D, U, perm, US, st);
         R.count();
-        for (uint32_t p = qb; p < qe; ++p)
-            for (uint32_t b = offu[p]; b < offu[p + 1]; b += mp.tile)
-                mp.add(b, std::min(offu[p + 1], b + mp.tile), {make_uint2(0, U.n)}, mp.chunk);
         ma.sxyz = US.xyz; ma.sskey = US.skey;
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
-        std::vector<uint2> comps;
-        for (uint32_t i : nonempty) {
-            if (i < qb || i >= qe) continue;
-            pd_ranges(offu, nonempty, i, cfg->strategy, m, d, comps);
-            if (comps.empty()) continue;
-            for (uint32_t b = offu[i]; b < offu[i + 1]; b += mp.tile)
-                mp.add(b, std::min(offu[i + 1], b + mp.tile), comps, mp.chunk);
+    }
+    if (P > 1) {
+        const uint2* sq = all_mode ? US.qc : U.qc;
+        auto comps_of = [&](uint32_t i, std::vector<uint2>& c) {
+            if (all_mode)
+                c.assign(1, make_uint2(0, U.n));
+            else
+                pd_ranges(offu, nonempty, i, cfg->strategy, m, d, c);
+        };
+        if (D <= 16 && U.qc) {
+            // wave A: the nearest slice / cell (or the strongest keys of the
+            // union), wave B: the rest over dense tiles of survivors
+            std::vector<uint2> c0;
+            uint32_t head = 4096;
+            if (!all_mode)
+                for (uint32_t i = qb; i < qe; ++i) {
+                    comps_of(i, c0);
+                    if (!c0.empty()) head = std::max(head, c0[0].y - c0[0].x);
+                }
+            R.relsky_waves(D, offu, qb, qe, comps_of, ma, U.qc, sq, mp.tile, mp.chunk, head);
+        } else {
+            std::vector<uint2> comps;
+            for (uint32_t i = qb; i < qe; ++i) {
+                if (offu[i + 1] == offu[i]) continue;
+                comps_of(i, comps);
+                if (comps.empty()) continue;
+                for (uint32_t b = offu[i]; b < offu[i + 1]; b += mp.tile)
+                    mp.add(b, std::min(offu[i + 1], b + mp.tile), comps, mp.chunk);
+            }
+            mp.order();
+            R.relsky(D, mp, ma);
         }
     }
-    mp.order();
-    R.relsky(D, mp, ma, U.qc, all_mode && P > 1 ? US.qc : U.qc);
 
     // surviving ids of this rank's candidates, ascending (engine.cpp:128-133)
     const uint32_t cb = offu[qb], cn = offu[qe] - cb;

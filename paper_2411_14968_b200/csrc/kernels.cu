@@ -512,6 +512,20 @@ void launch_compact_ids(const uint32_t* id, const uint8_t* dead, const uint32_t*
     SKY_LAUNCH_CHECK();
 }
 
+__global__ void k_compact_pos(const uint8_t* __restrict__ dead, const uint32_t* __restrict__ pos, uint32_t n,
+                              uint32_t base, uint32_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || dead[i]) return;
+    out[pos[i]] = base + i;
+}
+
+void launch_compact_pos(const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t base, uint32_t* out,
+                        cudaStream_t st) {
+    if (!n) return;
+    k_compact_pos<<<ceil_div(n, 256), 256, 0, st>>>(dead, pos, n, base, out);
+    SKY_LAUNCH_CHECK();
+}
+
 void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st) {
     if (n) SKY_CUDA(cudaMemsetAsync(p, v, n, st));
 }

@@ -76,6 +76,9 @@ void launch_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, ui
 void launch_compact_ids(const uint32_t* id, const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t* out,
                         cudaStream_t st);
 void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st);
+// out[pos[i]] = base + i for live i (dense list of live positions)
+void launch_compact_pos(const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t base, uint32_t* out,
+                        cudaStream_t st);
 void launch_mark_cells_dead(const uint64_t* key64, uint32_t n, const uint8_t* cell_dead, uint8_t* dead,
                             cudaStream_t st);
 
@@ -109,6 +112,7 @@ constexpr int kCodeLevels = 128;
 void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st);   // thr[D][127]
 void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st);  // fills s.qc
 struct Relsky2Args {
+    const uint32_t* cidx;  // optional: item candidate slots index this list of set positions
     const float* cxyz;
     const uint32_t* cskey;
     const uint2* cqc;
@@ -150,9 +154,13 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_
                  cudaStream_t st);
 
 // Streaming representative prefilter (false: not applicable, use k_relsky).
-bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64, uint32_t n,
-                      const float* rep_xyz, const uint32_t* rep_key, uint32_t nrep, uint8_t* dead,
-                      unsigned long long* tests, int smem_optin, cudaStream_t st);
+// Rows are tested in input order (dead_row), then folded into the sorted
+// positions (dead_pos[i] |= dead_row[idx[i]]).
+bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
+                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const float* thr, uint8_t* dead_row,
+                      uint8_t* dead_pos, unsigned long long* tests, int smem_optin, cudaStream_t st);
+// Quantization thresholds from a strided sample of row-major input rows.
+void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st);
 // Skyline of one small set in one CTA (false: too big, use k_relsky).
 bool launch_small_skyline(int D, const float* xyz, uint32_t n, uint8_t* dead, unsigned long long* tests,
                           int smem_optin, cudaStream_t st);

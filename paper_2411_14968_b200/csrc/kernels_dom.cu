@@ -60,20 +60,20 @@ constexpr int kThr = kCodeLevels - 1;  // 127 thresholds per dimension
 // (2048 rows), keep 127 quantiles as thresholds.
 constexpr int kThrThreads = 512, kThrItems = 4;
 template <int D>
-__global__ void __launch_bounds__(kThrThreads) k_thresholds(DevSet s, float* thr) {
-    constexpr int D4 = Dims2<D>::V * 4;
+__global__ void __launch_bounds__(kThrThreads) k_thresholds(const float* __restrict__ src, uint32_t stride, uint32_t ncols,
+                                                           uint32_t n, float* thr) {
     constexpr int SMP = kThrThreads * kThrItems;
     using Sort = cub::BlockRadixSort<float, kThrThreads, kThrItems>;
     __shared__ typename Sort::TempStorage tmp;
     __shared__ float v[SMP];
     const int j = blockIdx.x;
-    const uint32_t S = s.n < (uint32_t)SMP ? s.n : (uint32_t)SMP;
+    const uint32_t S = n < (uint32_t)SMP ? n : (uint32_t)SMP;
     float keys[kThrItems];
 #pragma unroll
     for (int k = 0; k < kThrItems; ++k) {
         const uint32_t i = threadIdx.x * kThrItems + k;
         keys[k] = __int_as_float(0x7f800000);  // +inf padding sorts last
-        if (i < S) keys[k] = s.xyz[((uint64_t)i * s.n / S) * D4 + j];
+        if (i < S) keys[k] = (uint32_t)j < ncols ? src[((uint64_t)i * n / S) * stride + j] : 0.0f;
     }
     Sort(tmp).Sort(keys);
 #pragma unroll
@@ -126,6 +126,26 @@ template <uint32_t G>
 __device__ __forceinline__ bool coarse_pass(const uint32_t (&t)[2], const uint2& s) {
     constexpr uint32_t GA = G | 0x80000000u;  // t'[1] always carries bit 31
     return ((t[0] - s.x) & (t[1] - s.y) & GA) == GA;
+}
+
+// Missing guard bits of the coarse test (0 <=> pass): 2 IMAD + 1 LOP3; the
+// K candidates of a lane fold with 3-input mins (VIMNMX3) into one compare.
+template <uint32_t G>
+__device__ __forceinline__ uint32_t coarse_miss(const uint32_t (&t)[2], const uint2& s) {
+    constexpr uint32_t GA = G | 0x80000000u;
+    return ~((t[0] - s.x) & (t[1] - s.y)) & GA;
+}
+
+template <uint32_t G, int K>
+__device__ __forceinline__ bool any_coarse_pass(const uint32_t (&T)[K][2], const uint2& q) {
+    uint32_t f[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) f[k] = coarse_miss<G>(T[k], q);
+    uint32_t m = f[0];
+#pragma unroll
+    for (int k = 1; k + 1 < K; k += 2) m = min(m, min(f[k], f[k + 1]));
+    if (K % 2 == 0 && K > 1) m = min(m, f[K - 1]);
+    return m == 0;
 }
 
 constexpr int RS3_WARPS = 8;
@@ -194,12 +214,13 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
         uint32_t alive = 0, my_max = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const uint32_t c = it.cb + k * 32 + lane;
+            const uint32_t slot = it.cb + k * 32 + lane;
             // empty / dead slot: lane guards set (no borrow can reach bit 31),
             // alive guard clear -> never passes
             T[k][0] = G;
             T[k][1] = G | 0x80000000u;
-            if (c < it.ce && !a.dead[c]) {
+            const uint32_t c = (slot < it.ce && a.cidx) ? a.cidx[slot] : slot;  // dense candidate lists
+            if (slot < it.ce && !a.dead[c]) {
                 alive |= 1u << k;
                 const uint2 q = a.cqc[c];
                 T[k][0] = q.x | G | CodeLayout<D>::ALIVE;
@@ -260,33 +281,41 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                 } else {
                     nk = 0xFFFFFFFFu;
                 }
-                for (uint32_t i = 0; i < lim; ++i) {
-                    const uint2 q = sm.code[warp][i];
-                    bool none = true;
+                auto exact = [&](uint32_t i, const uint2 q) {
+                    // exact test (core.hpp:89-96) where the codes could not rule s out
 #pragma unroll
-                    for (int k = 0; k < K; ++k) none &= !coarse_pass<G>(T[k], q);
-                    if (!none) {
-                        // exact test (core.hpp:89-96) where the codes could not rule s out
+                    for (int k = 0; k < K; ++k) {
+                        if (coarse_pass<G>(T[k], q)) {
+                            ++nhits;
+                            bool gt = false, lt = false;
 #pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            if (coarse_pass<G>(T[k], q)) {
-                                ++nhits;
-                                bool gt = false, lt = false;
-#pragma unroll
-                                for (int v = 0; v < W; ++v) {
-                                    const float4 sa = sm.comp[warp][i][v], tb = sm.cand[k][v][lane];
-                                    gt |= (sa.x > tb.x) | (sa.y > tb.y) | (sa.z > tb.z) | (sa.w > tb.w);
-                                    lt |= (sa.x < tb.x) | (sa.y < tb.y) | (sa.z < tb.z) | (sa.w < tb.w);
-                                }
-                                if (!gt && lt) {
-                                    alive &= ~(1u << k);
-                                    T[k][0] &= ~CodeLayout<D>::ALIVE;
-                                    atomicOr(&sm.deadmask[lane], 1u << k);
-                                    ntests += i + 1;
-                                }
+                            for (int v = 0; v < W; ++v) {
+                                const float4 sa = sm.comp[warp][i][v], tb = sm.cand[k][v][lane];
+                                gt |= (sa.x > tb.x) | (sa.y > tb.y) | (sa.z > tb.z) | (sa.w > tb.w);
+                                lt |= (sa.x < tb.x) | (sa.y < tb.y) | (sa.z < tb.z) | (sa.w < tb.w);
+                            }
+                            if (!gt && lt) {
+                                alive &= ~(1u << k);
+                                T[k][0] &= ~CodeLayout<D>::ALIVE;
+                                atomicOr(&sm.deadmask[lane], 1u << k);
+                                ntests += i + 1;
                             }
                         }
                     }
+                };
+                uint32_t i = 0;
+                for (; i + 2 <= lim; i += 2) {
+                    const uint2 q0 = sm.code[warp][i], q1 = sm.code[warp][i + 1];
+                    const bool p0 = any_coarse_pass<G, K>(T, q0);
+                    const bool p1 = any_coarse_pass<G, K>(T, q1);
+                    if (p0 | p1) {
+                        if (p0) exact(i, q0);
+                        if (p1) exact(i + 1, q1);
+                    }
+                }
+                if (i < lim) {
+                    const uint2 q = sm.code[warp][i];
+                    if (any_coarse_pass<G, K>(T, q)) exact(i, q);
                 }
                 ntests += (unsigned long long)__popc(alive) * lim;
                 live = __any_sync(FULL, alive != 0);
@@ -299,7 +328,8 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
             while (killed) {
                 const int k = __ffs(killed) - 1;
                 killed &= killed - 1;
-                a.dead[it.cb + k * 32 + lane] = 1;
+                const uint32_t slot = it.cb + k * 32 + lane;
+                a.dead[a.cidx ? a.cidx[slot] : slot] = 1;
             }
         }
         __syncthreads();
@@ -594,62 +624,103 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
 
 // ------------------------------------------------------------ prefilter
 // rep_prefilter (filter.cpp:147-159) over every row: one row per thread
-// (read through the sorted index, so a warp's rows have close keys), the
-// representatives resident in shared memory sorted by key; a row stops at its
-// first dominating representative, a warp at its key bound or when all its
-// rows are dominated.
-template <int D>
-__global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts, uint32_t d,
-                                                   const uint32_t* __restrict__ idx, const uint64_t* __restrict__ key64,
-                                                   uint32_t n, const float4* __restrict__ rep_xyz,
-                                                   const uint32_t* __restrict__ rep_key, uint32_t nrep,
-                                                   uint8_t* __restrict__ dead, unsigned long long* tests) {
+// (read through the sorted index, so a warp's rows have close keys). The
+// representatives sit in shared memory sorted by key with their packed codes
+// (quantization thresholds from a sample of the input); each row encodes
+// itself from the thresholds and runs the coarse test against every
+// representative with key <= the warp's bound, the exact test only where the
+// codes pass. A row stops at its first dominator, a warp when all its rows
+// are dominated.
+template <int D, bool CODES>
+__global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts, uint32_t d, uint32_t n,
+                                                   const float4* __restrict__ rep_xyz,
+                                                   const uint32_t* __restrict__ rep_key, const uint2* __restrict__ rep_qc,
+                                                   uint32_t nrep, const float* __restrict__ thr,
+                                                   uint8_t* __restrict__ dead_row, unsigned long long* tests) {
     constexpr int V = Dims2<D>::V;
+    constexpr uint32_t G = CodeLayout<D>::G;
+    constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
     extern __shared__ float4 s_rep[];
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_rep + (size_t)nrep * V);
+    uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)nrep * V);
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_code + nrep);
+    float* s_thr = reinterpret_cast<float*>(s_key + nrep);
     for (uint32_t i = threadIdx.x; i < nrep * V; i += blockDim.x) s_rep[i] = rep_xyz[i];
-    for (uint32_t i = threadIdx.x; i < nrep; i += blockDim.x) s_key[i] = rep_key[i];
+    for (uint32_t i = threadIdx.x; i < nrep; i += blockDim.x) {
+        if (CODES) s_code[i] = rep_qc[i];
+        s_key[i] = rep_key[i];
+    }
+    if (CODES)
+        for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
     __syncthreads();
-    const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = pos < n && !dead[pos];
-    float t[4 * V];
-#pragma unroll
-    for (int j = 0; j < 4 * V; ++j) t[j] = 0.0f;
+    const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;  // row order: coalesced reads
+    const bool valid = row < n;
+    float4 t[V];
     uint32_t tk = 0;
-    if (valid) {
-        const float* x = pts + (size_t)idx[pos] * d;
+    uint32_t T0 = G, T1 = G | 0x80000000u;  // never passes unless set below
+    {
+        float xs[4 * V];
+        const float* x = pts + (size_t)row * d;
+        double sum = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j)
-            if ((uint32_t)j < d) t[j] = x[j];
-        tk = (uint32_t)key64[pos];
+        for (int j = 0; j < 4 * V; ++j) {
+            xs[j] = (valid && j < D && (uint32_t)j < d) ? x[j] : 0.0f;
+            if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)xs[j]);  // same key as k_prep
+        }
+        tk = __float_as_uint(__double2float_rn(sum));
+        if (CODES && valid) {
+            uint32_t w[2] = {0, 0};
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const float* tj = s_thr + j * kThr;
+                int lo = 0, hi = kThr;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (tj[mid] <= xs[j]) lo = mid + 1; else hi = mid;
+                }
+                w[j / L] |= ((uint32_t)lo >> (7 - B)) << (LW * (j % L));
+            }
+            T0 = w[0] | G | CodeLayout<D>::ALIVE;
+            T1 = w[1] | G | 0x80000000u;
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) t[v] = make_float4(xs[4 * v], xs[4 * v + 1], xs[4 * v + 2], xs[4 * v + 3]);
     }
     bool alive = valid;
     const uint32_t bound = __reduce_max_sync(0xffffffffu, alive ? tk : 0u);
-    uint32_t r = 0;
     unsigned long long nt = 0;
     if (__any_sync(0xffffffffu, alive)) {
+        uint32_t r = 0;
         for (; r < nrep; ++r) {
             if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
-            const float4* sx = s_rep + r * V;
-            bool gt = false, lt = false;
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const float4 a = sx[v];
-                gt |= (a.x > t[4 * v]) | (a.y > t[4 * v + 1]) | (a.z > t[4 * v + 2]) | (a.w > t[4 * v + 3]);
-                lt |= (a.x < t[4 * v]) | (a.y < t[4 * v + 1]) | (a.z < t[4 * v + 2]) | (a.w < t[4 * v + 3]);
+            bool maybe = alive;
+            if (CODES) {
+                const uint2 q = s_code[r];
+                constexpr uint32_t GA = G | 0x80000000u;
+                maybe = ((T0 - q.x) & (T1 - q.y) & GA) == GA;
             }
-            if (alive) {
-                ++nt;
-                if (!gt && lt) alive = false;
+            if (maybe && s_key[r] <= tk && dom_f4<D>(s_rep + r * V, t)) {
+                alive = false;
+                nt += r + 1;
+                T0 &= ~CodeLayout<D>::ALIVE;
             }
-            if ((r & 7) == 7 && !__any_sync(0xffffffffu, alive)) break;
+            if ((r & 15) == 15 && !__any_sync(0xffffffffu, alive)) {
+                ++r;
+                break;
+            }
         }
+        if (alive) nt += r;
     }
-    if (valid && !alive) dead[pos] = 1;
+    if (valid) dead_row[row] = alive ? 0 : 1;
     if (tests) {
         nt = warp_sum(nt);
         if ((threadIdx.x & 31) == 0 && nt) atomicAdd(tests, nt);
     }
+}
+
+__global__ void k_gather_dead(const uint32_t* __restrict__ idx, const uint8_t* __restrict__ dead_row, uint32_t n,
+                              uint8_t* __restrict__ dead_pos) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dead_pos[i] |= dead_row[idx[i]];
 }
 
 // skyline_bruteforce (core.cpp:56-73) of one small set (prune_dominated_reps,
@@ -729,19 +800,27 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_
     SKY_DISPATCH_D16(D, (launch_bnl2_impl<DT>(a, qc, cap, grid, counter, st)));
 }
 
-bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64, uint32_t n,
-                      const float* rep_xyz, const uint32_t* rep_key, uint32_t nrep, uint8_t* dead,
-                      unsigned long long* tests, int smem_optin, cudaStream_t st) {
+bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
+                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const float* thr, uint8_t* dead_row,
+                      uint8_t* dead_pos, unsigned long long* tests, int smem_optin, cudaStream_t st) {
     if (D > 16) return false;
-    const size_t smem = (size_t)nrep * ((D + 3) / 4) * 16 + (size_t)nrep * 4 + 16;
+    const bool codes = rep_qc && thr && nrep >= 32;
+    const size_t smem = (size_t)nrep * ((D + 3) / 4) * 16 + (size_t)nrep * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64;
     if (smem + 1024 > (size_t)smem_optin) return false;
     if (!n) return true;
     SKY_DISPATCH_D16(D, {
-        SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_prefilter<DT><<<ceil_div(n, 256), 256, smem, st>>>(pts, d, idx, key64, n,
-                                                            reinterpret_cast<const float4*>(rep_xyz), rep_key, nrep,
-                                                            dead, tests);
+        if (codes) {
+            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_prefilter<DT, true><<<ceil_div(n, 256), 256, smem, st>>>(
+                pts, d, n, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, nrep, thr, dead_row, tests);
+        } else {
+            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_prefilter<DT, false><<<ceil_div(n, 256), 256, smem, st>>>(
+                pts, d, n, reinterpret_cast<const float4*>(rep_xyz), rep_key, nullptr, nrep, nullptr, dead_row, tests);
+        }
     });
+    SKY_LAUNCH_CHECK();
+    k_gather_dead<<<ceil_div(n, 256), 256, 0, st>>>(idx, dead_row, n, dead_pos);
     SKY_LAUNCH_CHECK();
     return true;
 }
@@ -762,7 +841,13 @@ bool launch_small_skyline(int D, const float* xyz, uint32_t n, uint8_t* dead, un
 
 void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st) {
     if (!s.n) return;
-    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(s, thr)));
+    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(s.xyz, (DT + 3) / 4 * 4, DT, s.n, thr)));
+    SKY_LAUNCH_CHECK();
+}
+
+void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st) {
+    if (!n) return;
+    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(pts, d, d, n, thr)));
     SKY_LAUNCH_CHECK();
 }
 
