@@ -696,10 +696,11 @@ class Runner {
         b.dead = dead;
         b.overflow = ovf;
         b.tests = count_tests ? tests(1) : nullptr;
+        b.hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + 1;
         if (s0.n) {
             SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
             if (packed)
-                launch_bnl2(D, b, s0.qc, cap, grid, misc + M_BNLCTR, st_);
+                launch_bnl2(D, b, s0.qc, s0.skey, cap & ~3u, grid, misc + M_BNLCTR, st_);
             else
                 launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
             SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));

@@ -142,6 +142,7 @@ struct BnlArgs {
     uint8_t* dead;            // out: 1 = dominated within its partition
     uint32_t* overflow;       // scratch: n entries
     unsigned long long* tests;
+    unsigned long long* hits;  // optional: exact checks performed
 };
 // Largest window <= want whose shared-memory footprint fits smem_optin.
 uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin);
@@ -150,8 +151,8 @@ void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint3
 
 // Packed-code BNL (D <= 16): window codes + metadata in shared memory.
 uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin);
-void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
-                 cudaStream_t st);
+void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey, uint32_t cap, uint32_t grid,
+                 uint32_t* counter, cudaStream_t st);
 
 // Streaming representative prefilter (false: not applicable, use k_relsky).
 // Rows are tested in input order (dead_row), then folded into the sorted

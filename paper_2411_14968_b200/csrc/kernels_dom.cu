@@ -356,12 +356,14 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 // timestamp = overflow length when it entered); it is output once it has met
 // every tuple: at the end of its pass if nothing spilled before it, else when
 // the next pass has consumed that many overflow tuples.
-constexpr int BNL2_B = 512;
+constexpr int BNL2_B = 1024;
 
 template <int D>
 size_t bnl2_smem(uint32_t cap) {
     constexpr int V = Dims2<D>::V;
-    return (size_t)cap * 16 + (size_t)BNL2_B * V * 16 + (size_t)BNL2_B * 8 + (size_t)cap * 8 + 2 * (size_t)cap + 64;
+    // window: codes (8) + key (4) + pos (4) + ts (4) + pass (1) + kill (1)
+    // batch: coords (16V) + codes (8) + key (4)
+    return (size_t)cap * 22 + (size_t)BNL2_B * (V * 16 + 12) + 256;
 }
 
 template <int D>
@@ -378,26 +380,30 @@ __device__ __forceinline__ bool dom_f4(const float4* __restrict__ s, const float
 }
 
 template <int D>
-__global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restrict__ qc, uint32_t cap,
+__global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restrict__ qc,
+                                                 const uint32_t* __restrict__ skey, uint32_t cap,
                                                  uint32_t* work_counter) {
     constexpr int V = Dims2<D>::V;
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr uint32_t GA = G | 0x80000000u;
     constexpr uint32_t ALIVE = CodeLayout<D>::ALIVE;
+    constexpr int NW = BNL2_B / 32;
     extern __shared__ uint4 sm4[];
-    uint4* w_code = sm4;                                                   // (w.x, w.y, w'.x, w'.y)
-    float4* b_xyz = reinterpret_cast<float4*>(w_code + cap);               // batch coords [B][V]
-    uint2* b_code = reinterpret_cast<uint2*>(b_xyz + BNL2_B * V);          // batch codes
-    uint32_t* w_pos = reinterpret_cast<uint32_t*>(b_code + BNL2_B);        // window -> set position
-    uint32_t* w_ts = w_pos + cap;                                          // overflow length at entry
-    uint8_t* w_pass = reinterpret_cast<uint8_t*>(w_ts + cap);              // pass of entry (mod 256)
-    uint8_t* w_kill = w_pass + cap;                                        // 1 evicted, 2 confirmed
-    __shared__ uint32_t s_wn, s_ovf_w, s_part, s_scan[BNL2_B / 32], s_next;
+    float4* b_xyz = reinterpret_cast<float4*>(sm4);                          // batch coords [B][V]
+    uint2* w_code = reinterpret_cast<uint2*>(b_xyz + BNL2_B * V);            // window codes
+    uint2* b_code = w_code + cap;                                            // batch codes
+    uint32_t* w_key = reinterpret_cast<uint32_t*>(b_code + BNL2_B);          // window keys
+    uint32_t* b_key = w_key + cap;                                           // batch keys
+    uint32_t* w_pos = b_key + BNL2_B;                                        // window -> set position
+    uint32_t* w_ts = w_pos + cap;                                            // overflow length at entry
+    uint8_t* w_pass = reinterpret_cast<uint8_t*>(w_ts + cap);                // pass of entry (mod 256)
+    uint8_t* w_kill = w_pass + cap;                                          // 1 evicted, 2 confirmed
+    __shared__ uint32_t s_wn, s_ovf_w, s_part, s_scan[NW], s_next;
     __shared__ int s_pass;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float4* __restrict__ xyz = reinterpret_cast<const float4*>(a.xyz);
-    unsigned long long ntests = 0;
+    unsigned long long ntests = 0, nhits = 0;
 
     // stable compaction of the window: drop entries with w_kill != 0
     // (confirmed ones are output first)
@@ -409,12 +415,13 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
             const bool in = w < wn0;
             const uint8_t kill = in ? w_kill[w] : 0;
             const bool keep = in && kill == 0;
-            uint4 q = make_uint4(0, 0, 0, 0);
-            uint32_t pos = 0, ts = 0;
+            uint2 q = make_uint2(0, 0);
+            uint32_t pos = 0, ts = 0, key = 0;
             uint8_t ps = 0;
             if (in) pos = w_pos[w];
             if (keep) {
                 q = w_code[w];
+                key = w_key[w];
                 ts = w_ts[w];
                 ps = w_pass[w];
             }
@@ -425,13 +432,14 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
             uint32_t off = kept_before + __popc(bal & ((1u << lane) - 1u));
             uint32_t tot = 0;
 #pragma unroll
-            for (int ww = 0; ww < BNL2_B / 32; ++ww) {
+            for (int ww = 0; ww < NW; ++ww) {
                 if (ww < warp) off += s_scan[ww];
                 tot += s_scan[ww];
             }
             __syncthreads();
             if (keep) {
                 w_code[off] = q;
+                w_key[off] = key;
                 w_pos[off] = pos;
                 w_ts[off] = ts;
                 w_pass[off] = ps;
@@ -484,7 +492,7 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                 if (k0 >= in_n) break;
                 const uint32_t bn = min((uint32_t)BNL2_B, in_n - k0);
                 const bool valid = (uint32_t)tid < bn;
-                uint32_t mypos = 0;
+                uint32_t mypos = 0, tkey = 0;
                 float4 t[V];
                 uint2 tq = make_uint2(0, 0);
                 if (valid) {
@@ -495,16 +503,26 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                         b_xyz[tid * V + v] = t[v];
                     }
                     tq = qc[mypos];
+                    tkey = skey[mypos];
                     b_code[tid] = tq;
+                    b_key[tid] = tkey;
                 }
                 __syncthreads();
                 uint32_t T0 = valid ? (tq.x | G | ALIVE) : G;
                 const uint32_t T1 = (valid ? tq.y : 0u) | G | 0x80000000u;
+                // a window tuple can only be dominated by t if its key is >= t's
+                // (dominance implies a smaller or equal coordinate sum)
+                const uint32_t rkey = valid ? tkey : 0xFFFFFFFFu;
                 bool alive = valid;
-                // batch x window, both directions
                 const uint32_t wn = s_wn;
                 bool killed_any = false;
-                auto slow = [&](uint32_t w, bool d1, bool d2) {
+                auto slow = [&](uint32_t w) {
+                    const uint2 q = w_code[w];
+                    const bool d1 = ((T0 - q.x) & (T1 - q.y) & GA) == GA;  // w may dominate t
+                    const bool d2 = w_key[w] >= rkey &&                     // t may dominate w
+                                    (((q.x | G | 0x80000000u) - tq.x) & ((q.y | G | 0x80000000u) - tq.y) & GA) == GA;
+                    if (!(d1 | d2)) return;
+                    ++nhits;
                     const float4* wx = xyz + (size_t)w_pos[w] * V;
                     float4 wv[V];
 #pragma unroll
@@ -520,33 +538,29 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                 };
                 uint32_t w = 0;
                 for (; w + 4 <= wn; w += 4) {
-                    // four independent entries per step: loads issue back to back
-                    uint4 q[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) q[u] = w_code[w + u];
-                    bool d1[4], d2[4];
-                    bool any = false;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        d1[u] = ((T0 - q[u].x) & (T1 - q[u].y) & GA) == GA;            // w may dominate t
-                        d2[u] = valid && ((q[u].z - tq.x) & (q[u].w - tq.y) & GA) == GA;  // t may dominate w
-                        any |= d1[u] | d2[u];
-                    }
-                    if (any) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (d1[u] | d2[u]) slow(w + u, d1[u], d2[u]);
+                    // four entries per step: forward coarse misses fold with
+                    // 3-input mins, the reverse test is gated by the keys
+                    const uint4 qa = *reinterpret_cast<const uint4*>(w_code + w);
+                    const uint4 qb = *reinterpret_cast<const uint4*>(w_code + w + 2);
+                    const uint4 kk = *reinterpret_cast<const uint4*>(w_key + w);
+                    const uint32_t f0 = ~((T0 - qa.x) & (T1 - qa.y)) & GA;
+                    const uint32_t f1 = ~((T0 - qa.z) & (T1 - qa.w)) & GA;
+                    const uint32_t f2 = ~((T0 - qb.x) & (T1 - qb.y)) & GA;
+                    const uint32_t f3 = ~((T0 - qb.z) & (T1 - qb.w)) & GA;
+                    const uint32_t fm = min(min(f0, f1), min(f2, f3));
+                    const uint32_t km = max(max(kk.x, kk.y), max(kk.z, kk.w));
+                    if (fm == 0 || km >= rkey) {
+                        slow(w);
+                        slow(w + 1);
+                        slow(w + 2);
+                        slow(w + 3);
                     }
                 }
-                for (; w < wn; ++w) {
-                    const uint4 q = w_code[w];
-                    const bool d1 = ((T0 - q.x) & (T1 - q.y) & GA) == GA;
-                    const bool d2 = valid && ((q.z - tq.x) & (q.w - tq.y) & GA) == GA;
-                    if (d1 | d2) slow(w, d1, d2);
-                }
+                for (; w < wn; ++w) slow(w);
                 if (valid) ntests += 2ull * wn;
-                // batch x batch: is t dominated by another batch tuple?
+                // batch x batch: is t dominated by an earlier-or-equal-key batch tuple?
                 for (uint32_t u = 0; u < bn; ++u) {
+                    if (b_key[u] > tkey) continue;  // sorted batches: a dominator has key <= tkey
                     const uint2 uq = b_code[u];
                     if (u != (uint32_t)tid && ((T0 - uq.x) & (T1 - uq.y) & GA) == GA) {
                         if (dom_f4<D>(b_xyz + u * V, t)) {
@@ -565,7 +579,7 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                     uint32_t rank = __popc(bal & ((1u << lane) - 1u));
                     uint32_t tot = 0;
 #pragma unroll
-                    for (int ww = 0; ww < BNL2_B / 32; ++ww) {
+                    for (int ww = 0; ww < NW; ++ww) {
                         if (ww < warp) rank += s_scan[ww];
                         tot += s_scan[ww];
                     }
@@ -574,7 +588,8 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                     if (alive) {
                         if (rank < room) {
                             const uint32_t slot = wn1 + rank;
-                            w_code[slot] = make_uint4(tq.x, tq.y, tq.x | G | 0x80000000u, tq.y | G | 0x80000000u);
+                            w_code[slot] = tq;
+                            w_key[slot] = tkey;
                             w_pos[slot] = mypos;
                             w_ts[slot] = ow;  // overflow tuples written in this pass so far
                             w_pass[slot] = (uint8_t)pass;
@@ -777,11 +792,12 @@ void launch_k(const Relsky2Args& a, int sm_count, cudaStream_t st) {
 }
 
 template <int D>
-void launch_bnl2_impl(const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
-                      cudaStream_t st) {
+void launch_bnl2_impl(const BnlArgs& a, const uint2* qc, const uint32_t* skey, uint32_t cap, uint32_t grid,
+                      uint32_t* counter, cudaStream_t st) {
+    cap &= ~3u;  // 4-entry loads of codes / keys
     const size_t smem = bnl2_smem<D>(cap);
     SKY_CUDA(cudaFuncSetAttribute(k_bnl2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bnl2<D><<<grid, BNL2_B, smem, st>>>(a, qc, cap, counter);
+    k_bnl2<D><<<grid, BNL2_B, smem, st>>>(a, qc, skey, cap, counter);
     SKY_LAUNCH_CHECK();
 }
 
@@ -795,9 +811,9 @@ uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin) {
     return cap;
 }
 
-void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, uint32_t cap, uint32_t grid, uint32_t* counter,
-                 cudaStream_t st) {
-    SKY_DISPATCH_D16(D, (launch_bnl2_impl<DT>(a, qc, cap, grid, counter, st)));
+void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey, uint32_t cap, uint32_t grid,
+                 uint32_t* counter, cudaStream_t st) {
+    SKY_DISPATCH_D16(D, (launch_bnl2_impl<DT>(a, qc, skey, cap, grid, counter, st)));
 }
 
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
