@@ -32,7 +32,15 @@ sys.path.insert(0, ROOT)
 
 BASELINE_METRIC = "skyline input points/sec + dominance tests/sec at 1/2/4/8 B200 vs CPU ref"
 UNIT = "input points/s"
-COMPARES_PER_CLK_PER_SM = 64  # FP32 compare issue (CUDA C++ guide throughput table)
+# Issue cost of one pair test on an SM (4 SMSPs; fma and alu pipes each take
+# 2 cycles per warp instruction, B300_MICROARCH.md "Pipe rates"):
+#  - d <= 16, packed monotone codes: 2 word subtractions (IMAD, fma pipe) +
+#    1 LOP3 + 1/2 VIMNMX3 fold (alu pipe) per test -> fma pipe bound,
+#    4 cycles per 32 tests per SMSP -> 32 tests/clk/SM;
+#  - d > 16, FP32 coordinates: d FSETP-class compares on the alu pipe ->
+#    64/d tests/clk/SM.
+PACKED_TESTS_PER_CLK_PER_SM = 32
+FP32_COMPARES_PER_CLK_PER_SM = 64
 
 
 def parse():
@@ -266,14 +274,21 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(local)
     n_sm = props.multi_processor_count
     sm_max = peaks.get("sm_max_mhz", 1965.0)
-    achieved = dom_tests * d / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0  # Gcompares/s
-    peak = n_sm * COMPARES_PER_CLK_PER_SM * sm_max * 1e6 / 1e9
+    achieved = dom_tests / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0  # Gtest/s
+    if d <= 16:
+        per_clk = PACKED_TESTS_PER_CLK_PER_SM
+        unit_desc = ("1 dominance (pair) test on packed 2x32-bit monotone codes: 2 IMAD (fma pipe) + "
+                     "1 LOP3 + 1/2 VIMNMX3 (alu pipe); exact FP32 re-checks counted separately")
+    else:
+        per_clk = FP32_COMPARES_PER_CLK_PER_SM / d
+        unit_desc = f"1 dominance (pair) test = d = {d} FP32 compares"
+    peak = n_sm * per_clk * sm_max * 1e6 / 1e9
     roofline = {
-        "bound": "alu", "kernel": "k_relsky + k_bnl (dominance tests)", "achieved": achieved, "peak": peak,
-        "unit": "Gcompare/s", "frac": achieved / peak if peak else None, "traffic": None,
-        "algorithmic_unit": f"1 dominance test = d = {d} FP32 compares",
-        "peak_source": f"{n_sm} SM x {COMPARES_PER_CLK_PER_SM} FP32 compare/clk x sm_max_mhz {sm_max} "
-                       f"(MEASURED_PEAKS.json); ALU compare issue, no HBM/tensor term",
+        "bound": "alu", "kernel": "k_relsky3 + k_bnl2 (dominance tests)", "achieved": achieved, "peak": peak,
+        "unit": "Gtest/s", "frac": achieved / peak if peak else None, "traffic": None,
+        "algorithmic_unit": unit_desc,
+        "peak_source": f"{n_sm} SM x {per_clk:g} tests/clk x sm_max_mhz {sm_max} (MEASURED_PEAKS.json clock); "
+                       "fma/alu pipe issue, no HBM/tensor term (operands live in shared memory)",
         "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / statistics.mean(dev_ms),
         "tests_per_step": dom_tests,
     }

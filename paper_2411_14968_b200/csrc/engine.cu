@@ -51,7 +51,12 @@ struct sky_ctx {
     int sm_count = 148;
     int smem_optin = 0;
     cudaEvent_t ev[6] = {};
-    cudaEvent_t dom_ev[2] = {};
+    std::vector<cudaEvent_t> dom_ev;  // (start, end) pairs, one per dominance launch of a run
+    uint32_t dom_used = 0;
+    // pinned staging for async H2D copies: bump-allocated per run, never
+    // reused within a run, so no launch has to wait for its copy to drain
+    std::vector<std::pair<char*, size_t>> stage;
+    size_t stage_cur = 0, stage_off = 0;
     uint32_t launches = 0;
     uint32_t dom_launches = 0;
     double dom_ms = 0.0;
@@ -78,7 +83,7 @@ constexpr uint32_t kChunk = 8192;   // comparators per relsky item before boundi
 constexpr uint32_t kBlock = 512;    // local block-skyline size
 
 // misc device words
-enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_TESTS = 8 /* 4 x u64 */,
+enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_TESTS = 8 /* 4 x u64 */,
        M_HITS = 16 /* 4 x u64, per phase */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
@@ -270,7 +275,34 @@ struct Plan {
 
 class Runner {
    public:
-    Runner(sky_ctx* c) : c_(c), st_(c->stream) {}
+    // Every API call ends with the stream drained (its results are read on
+    // the host), so a new Runner may recycle the staging and event pools.
+    Runner(sky_ctx* c) : c_(c), st_(c->stream) {
+        c->stage_cur = c->stage_off = 0;
+        c->dom_used = 0;
+    }
+
+    // Pinned bytes that stay untouched until the stream drains.
+    template <class T>
+    T* stage(size_t n) {
+        const size_t bytes = (n ? n : 1) * sizeof(T) + 16;
+        auto& v = c_->stage;
+        while (true) {
+            if (c_->stage_cur >= v.size()) {
+                const size_t cap = std::max<size_t>(bytes, (size_t)4 << 20);
+                char* p = nullptr;
+                SKY_CUDA(cudaMallocHost(&p, cap));
+                v.emplace_back(p, cap);
+            }
+            size_t off = (c_->stage_off + 15) & ~size_t{15};
+            if (off + bytes <= v[c_->stage_cur].second) {
+                c_->stage_off = off + bytes;
+                return reinterpret_cast<T*>(v[c_->stage_cur].first + off);
+            }
+            ++c_->stage_cur;
+            c_->stage_off = 0;
+        }
+    }
 
     // --------------------------------------------------------------- utils
     template <class T>
@@ -386,8 +418,8 @@ class Runner {
                 }
             }
         } report{plan, t0, c_};
-        Item* hi = pin<Item>(P_ITEMS, plan.items.size());
-        uint2* hr = pin<uint2>(P_RANGES, plan.ranges.size());
+        Item* hi = stage<Item>(plan.items.size());
+        uint2* hr = stage<uint2>(plan.ranges.size());
         std::memcpy(hi, plan.items.data(), plan.items.size() * sizeof(Item));
         std::memcpy(hr, plan.ranges.data(), plan.ranges.size() * sizeof(uint2));
         Item* di = dev<Item>(S_ITEMS, plan.items.size());
@@ -398,7 +430,7 @@ class Runner {
         a.items = di;
         a.ranges = dr;
         a.n_items = (uint32_t)plan.items.size();
-        SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
+        dom_begin();
         if (D <= 16 && cq && sq && !a.indirect) {
             uint32_t* misc = dev<uint32_t>(S_MISC, 64);
             SKY_CUDA(cudaMemsetAsync(misc + M_WORK, 0, sizeof(uint32_t), st_));
@@ -415,12 +447,8 @@ class Runner {
             if (plan.tile != (uint32_t)kTile) throw Error(SKY_E_INTERNAL, "v1 relsky needs 512-candidate tiles");
             launch_relsky(D, a, st_);
         }
-        SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));
+        dom_end();
         count();
-        dom_done();
-        // the pinned staging buffers are reused by the next call: make sure
-        // the copies have consumed them first
-        sync();
     }
 
     // Two-wave relative skyline of the candidates of partitions [qb, qe)
@@ -473,7 +501,7 @@ class Runner {
         scan_live(base.dead + cb, pos, cn);
         launch_count_total(pos, base.dead + cb, cn, misc + M_TOTAL, st_);
         const uint32_t np = qe - qb;
-        uint32_t* hrel = pin<uint32_t>(P_OFF, np + 2);
+        uint32_t* hrel = stage<uint32_t>(np + 2);
         for (uint32_t p = qb; p <= qe; ++p) hrel[p - qb] = offc[p] - cb;
         uint32_t* drel = dev<uint32_t>(S_OFF_C, np + 1);
         uint32_t* dnew = dev<uint32_t>(S_SIZES, np + 1);
@@ -499,13 +527,28 @@ class Runner {
         relsky(D, B, base, cq, sq, dense);
     }
 
-    // accumulate the CUDA-event time of the dominance launch just issued
-    void dom_done() {
-        SKY_CUDA(cudaEventSynchronize(c_->dom_ev[1]));
-        float ms = 0.f;
-        SKY_CUDA(cudaEventElapsedTime(&ms, c_->dom_ev[0], c_->dom_ev[1]));
-        c_->dom_ms += ms;
+    // CUDA events around each dominance launch; summed once the run drained
+    void dom_begin() {
+        auto& e = c_->dom_ev;
+        while (e.size() < 2 * (size_t)(c_->dom_used + 1)) {
+            cudaEvent_t ev;
+            SKY_CUDA(cudaEventCreate(&ev));
+            e.push_back(ev);
+        }
+        SKY_CUDA(cudaEventRecord(e[2 * c_->dom_used], st_));
+    }
+    void dom_end() {
+        SKY_CUDA(cudaEventRecord(c_->dom_ev[2 * c_->dom_used + 1], st_));
+        ++c_->dom_used;
         c_->dom_launches += 1;
+    }
+    void dom_collect() {
+        for (uint32_t k = 0; k < c_->dom_used; ++k) {
+            float ms = 0.f;
+            SKY_CUDA(cudaEventElapsedTime(&ms, c_->dom_ev[2 * k], c_->dom_ev[2 * k + 1]));
+            c_->dom_ms += ms;
+        }
+        c_->dom_used = 0;
     }
 
     // Item granularity: candidates per item (one warp, 32*K) and comparators
@@ -567,6 +610,7 @@ class Runner {
                                        q, c_->comm, st_));
         }
         SKY_NCCL(ncclGroupEnd());
+        sync();  // the pinned offsets above are reused by the next planner
         return Ug;
     }
 
@@ -698,14 +742,13 @@ class Runner {
         b.tests = count_tests ? tests(1) : nullptr;
         b.hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + 1;
         if (s0.n) {
-            SKY_CUDA(cudaEventRecord(c_->dom_ev[0], st_));
+            dom_begin();
             if (packed)
                 launch_bnl2(D, b, s0.qc, s0.skey, cap & ~3u, grid, misc + M_BNLCTR, st_);
             else
                 launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
-            SKY_CUDA(cudaEventRecord(c_->dom_ev[1], st_));
+            dom_end();
             count();
-            dom_done();
         }
         return compact(s0, dead, off0_dev, P, S_SET2, off_u_dev, off_u, D);
     }
@@ -786,6 +829,15 @@ bool grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d) {
     return true;
 }
 
+struct RedoEager {};  // angular boundary points seen by a deferred prep
+
+void check_prep(uint32_t err, uint32_t amb, int strategy, bool eager) {
+    if (err & kErrNonFinite) throw Error(SKY_E_DATA, "coordinate must be finite and >= 0");
+    if (err & kErrAboveOne) throw Error(SKY_E_DATA, "normalized dataset has coordinate > 1");
+    if (err & kErrGridRange) throw Error(SKY_E_NORMALIZATION, "grid index needs coordinates in [0,1]");
+    if (!eager && strategy == SKY_ANGULAR && amb) throw RedoEager{};
+}
+
 struct PartitionOut {
     uint64_t* key64;   // sorted (pid << 32 | skey)
     uint32_t* idx;     // row of each sorted position
@@ -795,7 +847,7 @@ struct PartitionOut {
 // Phase 1a: partition ids, sum keys, validation, sort into partitions.
 PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d, int normalized, int strategy,
                              uint64_t P, uint64_t m, const sky_config* cfg, const uint32_t* pid_dev,
-                             uint64_t* fixups) {
+                             uint64_t* fixups, bool eager = true) {
     cudaStream_t st = R.st_;
     uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, n);
     uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, n);
@@ -813,15 +865,17 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     launch_prep(pa, st);
     R.count();
 
-    // errors + angular boundary points (one host round trip)
+    // errors + angular boundary points (one host round trip). Deferred mode
+    // skips the round trip: the caller checks M_ERR/M_AMB at its first sync
+    // (check_prep) and reruns eagerly when angular boundary points need the
+    // host libm. Kernels downstream tolerate a failed prep (pids clamped).
     uint32_t* hm = R.pin<uint32_t>(P_MISC, 8);
-    SKY_CUDA(cudaMemcpyAsync(hm, misc, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    R.sync();
-    const uint32_t err = hm[M_ERR];
-    if (err & kErrNonFinite) throw Error(SKY_E_DATA, "coordinate must be finite and >= 0");
-    if (err & kErrAboveOne) throw Error(SKY_E_DATA, "normalized dataset has coordinate > 1");
-    if (err & kErrGridRange) throw Error(SKY_E_NORMALIZATION, "grid index needs coordinates in [0,1]");
-    if (strategy == SKY_ANGULAR && hm[M_AMB]) {
+    if (eager || strategy == SKY_SLICED) {
+        SKY_CUDA(cudaMemcpyAsync(hm, misc, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        check_prep(hm[M_ERR], 0, strategy, true);
+    }
+    if (eager && strategy == SKY_ANGULAR && hm[M_AMB]) {
         const uint32_t na = hm[M_AMB];
         if (na > amb_cap) throw Error(SKY_E_INTERNAL, "too many angular boundary points");
         uint32_t* ha = R.pin<uint32_t>(P_AMB, 3 * (size_t)na + 1);
@@ -903,8 +957,62 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     return PartitionOut{keyB, idxB, off};
 }
 
+// Representative selection finished on the host side: compact the picked
+// rows, sort them by sum key and prune them to an antichain
+// (select_representatives_sorted + prune_dominated_reps, filter.cpp). Used
+// when the P*q candidate slots do not fit the one-CTA k_rep_finalize.
+DevSet host_reps(Runner& R, sky_ctx* c, int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d,
+                 bool count_tests) {
+    cudaStream_t st = R.st_;
+    uint32_t* hc = R.pin<uint32_t>(P_IDS, slots);
+    SKY_CUDA(cudaMemcpyAsync(hc, cand, (size_t)slots * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    R.sync();
+    std::vector<uint32_t> rows;
+    rows.reserve(slots);
+    for (size_t k = 0; k < slots; ++k)
+        if (hc[k] != kNone) rows.push_back(hc[k]);
+    const uint32_t nc = (uint32_t)rows.size();
+    uint32_t* drows = R.dev<uint32_t>(S_REPROWS, nc);
+    std::memcpy(hc, rows.data(), nc * sizeof(uint32_t));
+    SKY_CUDA(cudaMemcpyAsync(drows, hc, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    DevSet cs = R.set(S_SET3, nc, D);
+    launch_gather_rows(D, pts, d, drows, nc, cs, nullptr, st);
+    R.count();
+    DevSet css = R.set(S_SET1, nc, D);
+    {
+        uint32_t* iota = R.dev<uint32_t>(S_PERM_A, nc);
+        uint32_t* perm = R.dev<uint32_t>(S_PERM_B, nc);
+        uint32_t* hio = R.pin<uint32_t>(P_RUNS, nc);
+        for (uint32_t k = 0; k < nc; ++k) hio[k] = k;
+        SKY_CUDA(cudaMemcpyAsync(iota, hio, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        uint32_t* sk2 = R.dev<uint32_t>(S_SKTMP, nc);
+        R.sort_pairs(cs.skey, sk2, iota, perm, nc, 0, 32);
+        launch_gather_set(D, cs, perm, css, st);
+        R.count();
+    }
+    uint8_t* cdead = R.dev<uint8_t>(S_CELLDEAD, nc);
+    launch_fill_u8(cdead, 0, nc, st);
+    if (launch_small_skyline(D, css.xyz, nc, cdead, count_tests ? R.tests(0) : nullptr, c->smem_optin, st)) {
+        R.count();
+    } else {
+        Plan pp;
+        for (uint32_t b = 0; b < nc; b += kTile) pp.add(b, std::min(nc, b + (uint32_t)kTile), {make_uint2(0, nc)});
+        RelskyArgs ra{};
+        ra.cxyz = css.xyz; ra.cskey = css.skey; ra.sxyz = css.xyz; ra.sskey = css.skey;
+        ra.bounded = true; ra.dead = cdead; ra.tests = count_tests ? R.tests(0) : nullptr;
+        R.relsky(D, pp, ra);
+    }
+    std::vector<uint32_t> roff;
+    uint32_t* doff = R.dev<uint32_t>(S_OFF_B, 4);
+    uint32_t* hz = R.pin<uint32_t>(P_MISC, 8);
+    hz[4] = 0;
+    hz[5] = nc;
+    SKY_CUDA(cudaMemcpyAsync(doff, hz + 4, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    return R.compact(css, cdead, doff, 1, S_SET3, doff + 2, roff, D);
+}
+
 void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int normalized, int on_device,
-              const sky_config* cfg, sky_result* out) {
+              const sky_config* cfg, sky_result* out, bool eager = false) {
     std::memset(out, 0, sizeof(*out));
     validate(n64, d, cfg);
     uint64_t P64 = 0, m = 0;
@@ -954,7 +1062,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     }
     const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed) : nullptr;
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
-                                      &out->angular_host_fixups);
+                                      &out->angular_host_fixups, eager);
 
     std::vector<uint32_t> off0(P + 1);
     uint8_t* dead = R.dev<uint8_t>(S_DEAD, n);
@@ -997,58 +1105,18 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         // representative filter is active, so every partition participates
         launch_rep_pick(po.key64, po.idx, po.off, P, pts, d, q, cand, st);
         R.count();
-        // compact the candidate rows on the host side (P*q is small)
-        uint32_t* hc = R.pin<uint32_t>(P_IDS, (size_t)P * q);
-        SKY_CUDA(cudaMemcpyAsync(hc, cand, (size_t)P * q * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        R.sync();
-        std::vector<uint32_t> rows;
-        rows.reserve((size_t)P * q);
-        for (size_t k = 0; k < (size_t)P * q; ++k)
-            if (hc[k] != kNone) rows.push_back(hc[k]);
-        const uint32_t nc = (uint32_t)rows.size();
-        uint32_t* drows = R.dev<uint32_t>(S_REPROWS, nc);
-        std::memcpy(hc, rows.data(), nc * sizeof(uint32_t));
-        SKY_CUDA(cudaMemcpyAsync(drows, hc, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        DevSet cs = R.set(S_SET3, nc, D);
-        launch_gather_rows(D, pts, d, drows, nc, cs, nullptr, st);
-        R.count();
-        // sort candidates by sum key, prune to an antichain (prune_dominated_reps)
-        DevSet css = R.set(S_SET1, nc, D);
-        {
-            uint32_t* iota = R.dev<uint32_t>(S_PERM_A, nc);
-            uint32_t* perm = R.dev<uint32_t>(S_PERM_B, nc);
-            std::vector<uint32_t> io(nc);
-            for (uint32_t k = 0; k < nc; ++k) io[k] = k;
-            uint32_t* hio = R.pin<uint32_t>(P_RUNS, nc);
-            std::memcpy(hio, io.data(), nc * sizeof(uint32_t));
-            SKY_CUDA(cudaMemcpyAsync(iota, hio, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-            uint32_t* sk2 = R.dev<uint32_t>(S_SKTMP, nc);
-            R.sort_pairs(cs.skey, sk2, iota, perm, nc, 0, 32);
-            launch_gather_set(D, cs, perm, css, st);
-            R.count();
-        }
-        uint8_t* cdead = R.dev<uint8_t>(S_CELLDEAD, nc);
-        launch_fill_u8(cdead, 0, nc, st);
-        if (launch_small_skyline(D, css.xyz, nc, cdead, count_tests ? R.tests(0) : nullptr, c->smem_optin, st)) {
+        const uint32_t slots = P * q;
+        DevSet reps = R.set(S_SET3, slots, D);  // reps.n: upper bound until the count is read back
+        uint32_t* nrep_dev = misc + M_NREP;
+        if (launch_rep_finalize(D, cand, slots, pts, d, reps, nrep_dev, count_tests ? R.tests(0) : nullptr,
+                                c->smem_optin, st)) {
+            // compact + sort + prune in one CTA; the count stays on the device
             R.count();
         } else {
-            Plan pp;
-            for (uint32_t b = 0; b < nc; b += kTile) pp.add(b, std::min(nc, b + (uint32_t)kTile), {make_uint2(0, nc)});
-            RelskyArgs ra{};
-            ra.cxyz = css.xyz; ra.cskey = css.skey; ra.sxyz = css.xyz; ra.sskey = css.skey;
-            ra.bounded = true; ra.dead = cdead; ra.tests = count_tests ? R.tests(0) : nullptr;
-            R.relsky(D, pp, ra);
+            reps = host_reps(R, c, D, cand, slots, pts, d, count_tests);
+            SKY_CUDA(cudaMemcpyAsync(nrep_dev, &reps.n, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            R.sync();  // &reps.n is pageable stack memory
         }
-        std::vector<uint32_t> roff;
-        uint32_t zero_off[2] = {0, nc};
-        uint32_t* doff = R.dev<uint32_t>(S_OFF_B, 2);
-        uint32_t* hz = R.pin<uint32_t>(P_MISC, 8);
-        hz[4] = zero_off[0];
-        hz[5] = zero_off[1];
-        SKY_CUDA(cudaMemcpyAsync(doff, hz + 4, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        uint32_t* doff2 = R.dev<uint32_t>(S_OFF_B, 4) + 2;
-        DevSet reps = R.compact(css, cdead, doff, 1, S_SET3, doff2, roff, D);
-        out->n_reps = reps.n;
 
         // rep_prefilter over every row, in partition/sum order (indirect)
         float* pthr = nullptr;
@@ -1056,15 +1124,21 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
             // one quantization for rows and representatives: quantiles of the input
             pthr = R.dev<float>(S_PTHR, (size_t)D * (kCodeLevels - 1));
             launch_thresholds_rows(D, pts, d, n, pthr, st);
-            launch_encode(D, reps, pthr, st);
+            launch_encode(D, reps, pthr, st, nrep_dev);
             R.count(2);
         }
         uint8_t* dead_row = R.dev<uint8_t>(S_DEADROW, n);
         if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.n,
-                                           pthr, dead_row, dead, count_tests ? R.tests(1) : nullptr, c->smem_optin, st)) {
+                                           nrep_dev, pthr, dead_row, dead, count_tests ? R.tests(1) : nullptr,
+                                           c->smem_optin, st)) {
             R.count();
             any_dead = true;
         } else if (reps.n > 0) {
+            // generic relsky fallback needs the exact count on the host
+            uint32_t* hn = R.pin<uint32_t>(P_MISC, 8);
+            SKY_CUDA(cudaMemcpyAsync(hn, nrep_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            R.sync();
+            reps.n = hn[0];
             Plan pf;
             for (uint32_t b = 0; b < n; b += kTile) pf.add(b, std::min(n, b + (uint32_t)kTile), {make_uint2(0, reps.n)});
             RelskyArgs fa{};
@@ -1086,12 +1160,15 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         launch_count_total(pos, dead, n, misc + M_TOTAL, st);
         launch_remap_offsets(po.off, P, pos, dead, n, off1_dev, st);
         R.count(2);
-        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 2);
+        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 8);
         SKY_CUDA(cudaMemcpyAsync(h, off1_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         R.sync();
+        const uint32_t* hmisc = h + P + 1;
+        check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
+        if (cfg->filter == SKY_FILTER_REPRESENTATIVE) out->n_reps = hmisc[M_NREP];
         off1.assign(h, h + P + 1);
-        const uint32_t total = h[P + 1];
+        const uint32_t total = hmisc[M_TOTAL];
         s0 = R.set(S_SET0, total, D);
         launch_scatter_indirect(D, pts, d, po.idx, po.key64, n, any_dead ? dead : nullptr, any_dead ? pos : nullptr,
                                 s0, st);
@@ -1129,7 +1206,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         uint32_t* offm_dev = off1_dev;
         if (W > 1) {
             offm_dev = R.dev<uint32_t>(S_OFF_C, Pm + 1);
-            uint32_t* h = R.pin<uint32_t>(P_OFF, Pm + 1);
+            uint32_t* h = R.stage<uint32_t>(Pm + 1);
             std::memcpy(h, offm.data(), (Pm + 1) * sizeof(uint32_t));
             SKY_CUDA(cudaMemcpyAsync(offm_dev, h, (Pm + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
         }
@@ -1287,6 +1364,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     out->total_ms = ms;
     out->kernel_launches = c->launches;
     out->dom_launches = c->dom_launches;
+    R.dom_collect();
     out->dom_kernel_ms = c->dom_ms;
     out->dom_tests = ht[0] + ht[1] + ht[2];
     out->dom_exact_checks = ht[3] + ht[4] + ht[5] + ht[6];
@@ -1342,7 +1420,6 @@ int sky_ctx_create(int device, sky_ctx** out) {
         SKY_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         SKY_CUDA(cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         for (auto& e : c->ev) SKY_CUDA(cudaEventCreate(&e));
-        for (auto& e : c->dom_ev) SKY_CUDA(cudaEventCreate(&e));
     });
     if (rc != SKY_OK) {
         static thread_local std::string last;
@@ -1393,6 +1470,7 @@ void sky_ctx_destroy(sky_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& e : c->dom_ev)
         if (e) cudaEventDestroy(e);
+    for (auto& b : c->stage) cudaFreeHost(b.first);
     c->dev.release();
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -1409,7 +1487,12 @@ int sky_run(sky_ctx* c, const float* points, uint64_t n, uint32_t d, int normali
             const sky_config* cfg, sky_result* out) {
     return guarded(c, [&] {
         try {
-            run_impl(c, points, n, d, normalized, on_device, cfg, out);
+            try {
+                run_impl(c, points, n, d, normalized, on_device, cfg, out);
+            } catch (const RedoEager&) {
+                sky_result_free(out);
+                run_impl(c, points, n, d, normalized, on_device, cfg, out, true);
+            }
         } catch (...) {
             sky_result_free(out);
             throw;

@@ -118,7 +118,10 @@ __global__ void k_prep(PrepArgs a) {
         if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
         if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(x[a.slice_dim]);
     }
-    if (err) atomicOr(a.err, err);
+    if (err) {
+        atomicOr(a.err, err);
+        pid = 0;  // the run fails at its next host check; keep every index in bounds
+    }
     const uint32_t skey = __float_as_uint(__double2float_rn(sum));  // monotone in sum
     a.key64[i] = (pid << 32) | skey;
     a.idx[i] = i;
@@ -372,6 +375,137 @@ void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t*
     if (!P) return;
     k_rep_pick<<<P, 128, 0, st>>>(key64, idx, off, pts, d, q, cand);
     SKY_LAUNCH_CHECK();
+}
+
+// select_representatives_sorted + prune_dominated_reps (filter.cpp:15-33,
+// 66-86, 139-145) finished in one CTA: compact the per-partition picks, sort
+// them by sum key, keep the antichain (brute force, as the reference does),
+// emit them key-sorted with their count in device memory.
+constexpr int REPF_THREADS = 1024, REPF_ITEMS = 2, REPF_MAX = REPF_THREADS * REPF_ITEMS;
+
+template <int D>
+__global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* __restrict__ cand, uint32_t slots,
+                                                               const float* __restrict__ pts, uint32_t d, DevSet out,
+                                                               uint32_t* out_count, unsigned long long* tests) {
+    constexpr int V = Dims<D>::V;
+    using Scan = cub::BlockScan<uint32_t, REPF_THREADS>;
+    using Sort = cub::BlockRadixSort<uint32_t, REPF_THREADS, REPF_ITEMS, uint32_t>;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename Sort::TempStorage sort;
+    } tmp;
+    extern __shared__ float4 s_xyz[];  // [REPF_MAX][V], then rows, keys, order, dead flags
+    uint32_t* s_row = reinterpret_cast<uint32_t*>(s_xyz + (size_t)REPF_MAX * V);
+    uint32_t* s_key = s_row + REPF_MAX;
+    uint32_t* s_ord = s_key + REPF_MAX;
+    uint8_t* s_dead = reinterpret_cast<uint8_t*>(s_ord + REPF_MAX);
+    __shared__ uint32_t s_n;
+    const int t = threadIdx.x;
+    // 1. compact the picks (slot order = partition order)
+    uint32_t flags[REPF_ITEMS], rows[REPF_ITEMS];
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) {
+        const uint32_t sl = t * REPF_ITEMS + k;
+        rows[k] = sl < slots ? cand[sl] : kNone;
+        flags[k] = rows[k] != kNone;
+    }
+    uint32_t offs[REPF_ITEMS], total;
+    Scan(tmp.scan).ExclusiveSum(flags, offs, total);
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k)
+        if (flags[k]) s_row[offs[k]] = rows[k];
+    if (t == 0) s_n = total;
+    __syncthreads();
+    const uint32_t n = s_n;
+    // 2. coordinates and FP64-sum keys
+    for (uint32_t i = t; i < n; i += REPF_THREADS) {
+        const float* x = pts + (size_t)s_row[i] * d;
+        float4* dst = s_xyz + (size_t)i * V;
+        double sum = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            float c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t j = 4 * v + q;
+                c[q] = j < d ? x[j] : 0.0f;
+                if (j < d) sum = __dadd_rn(sum, (double)c[q]);
+            }
+            dst[v] = make_float4(c[0], c[1], c[2], c[3]);
+        }
+        s_key[i] = __float_as_uint(__double2float_rn(sum));
+    }
+    __syncthreads();
+    // 3. key order
+    uint32_t keys[REPF_ITEMS], vals[REPF_ITEMS];
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) {
+        const uint32_t i = t * REPF_ITEMS + k;
+        keys[k] = i < n ? s_key[i] : 0xFFFFFFFFu;
+        vals[k] = i;
+    }
+    __syncthreads();
+    Sort(tmp.sort).Sort(keys, vals);
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) s_ord[t * REPF_ITEMS + k] = vals[k];
+    __syncthreads();
+    // 4. antichain: brute force over all candidates
+    unsigned long long nt = 0;
+    for (uint32_t i = t; i < n; i += REPF_THREADS) {
+        const float4* ti = s_xyz + (size_t)i * V;
+        bool dom = false;
+        for (uint32_t j = 0; j < n && !dom; ++j) {
+            if (j == i) continue;
+            ++nt;
+            const float4* sj = s_xyz + (size_t)j * V;
+            bool gt = false, lt = false;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const float4 a = sj[v], b = ti[v];
+                gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
+                lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
+            }
+            dom = !gt && lt;
+        }
+        s_dead[i] = dom;
+    }
+    __syncthreads();
+    // 5. survivors in key order
+    uint32_t keep[REPF_ITEMS], kpos[REPF_ITEMS], ktot;
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) {
+        const uint32_t p = t * REPF_ITEMS + k;
+        keep[k] = p < n && !s_dead[s_ord[p]];
+    }
+    Scan(tmp.scan).ExclusiveSum(keep, kpos, ktot);
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) {
+        if (!keep[k]) continue;
+        const uint32_t i = s_ord[t * REPF_ITEMS + k], o = kpos[k];
+        float4* dst = reinterpret_cast<float4*>(out.xyz) + (size_t)o * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) dst[v] = s_xyz[(size_t)i * V + v];
+        out.skey[o] = s_key[i];
+        out.id[o] = s_row[i];
+    }
+    if (t == 0) *out_count = ktot;
+    if (tests) {
+        nt = warp_sum_u64(nt);
+        if ((t & 31) == 0 && nt) atomicAdd(tests, nt);
+    }
+}
+
+bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
+                         uint32_t* out_count, unsigned long long* tests, int smem_optin, cudaStream_t st) {
+    if (slots > (uint32_t)REPF_MAX) return false;
+    const size_t smem = (size_t)REPF_MAX * ((D + 3) / 4) * 16 + (size_t)REPF_MAX * 13 + 64;
+    if (smem + 48 * 1024 > (size_t)smem_optin) return false;
+    SKY_DISPATCH_D(D, {
+        SKY_CUDA(cudaFuncSetAttribute(k_rep_finalize<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_rep_finalize<DT><<<1, REPF_THREADS, smem, st>>>(cand, slots, pts, d, out, out_count, tests);
+    });
+    SKY_LAUNCH_CHECK();
+    return true;
 }
 
 // ------------------------------------------------------------ compaction

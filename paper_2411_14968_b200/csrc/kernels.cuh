@@ -62,6 +62,11 @@ void launch_gather_coord_key(const float* pts, uint32_t d, uint32_t j, const uin
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
                      const float* pts, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st);
 
+// Representative finish on the device (<= 2048 picks): key-sorted antichain
+// into `out`, count in *out_count. false: too many picks (host path).
+bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
+                         uint32_t* out_count, unsigned long long* tests, int smem_optin, cudaStream_t st);
+
 // Compaction plumbing.
 void launch_scatter_direct(int D, const DevSet& in, const uint8_t* dead, const uint32_t* pos, DevSet out,
                            cudaStream_t st);
@@ -110,7 +115,8 @@ void launch_relsky(int D, const RelskyArgs& a, cudaStream_t st);
 // with the exact float test.
 constexpr int kCodeLevels = 128;
 void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st);   // thr[D][127]
-void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st);  // fills s.qc
+// fills s.qc; n_dev: optional device-side row count (s.n is then an upper bound)
+void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st, const uint32_t* n_dev = nullptr);
 struct Relsky2Args {
     const uint32_t* cidx;  // optional: item candidate slots index this list of set positions
     const float* cxyz;
@@ -157,9 +163,11 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey,
 // Streaming representative prefilter (false: not applicable, use k_relsky).
 // Rows are tested in input order (dead_row), then folded into the sorted
 // positions (dead_pos[i] |= dead_row[idx[i]]).
+// nrep: host upper bound (shared-memory sizing); nrep_dev: optional device count.
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
-                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const float* thr, uint8_t* dead_row,
-                      uint8_t* dead_pos, unsigned long long* tests, int smem_optin, cudaStream_t st);
+                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const uint32_t* nrep_dev,
+                      const float* thr, uint8_t* dead_row, uint8_t* dead_pos, unsigned long long* tests, int smem_optin,
+                      cudaStream_t st);
 // Quantization thresholds from a strided sample of row-major input rows.
 void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st);
 // Skyline of one small set in one CTA (false: too big, use k_relsky).

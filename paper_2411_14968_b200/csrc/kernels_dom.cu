@@ -87,13 +87,13 @@ __global__ void __launch_bounds__(kThrThreads) k_thresholds(const float* __restr
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_encode(DevSet s, const float* __restrict__ thr) {
+__global__ void __launch_bounds__(256) k_encode(DevSet s, const float* __restrict__ thr, const uint32_t* n_dev) {
     constexpr int V = Dims2<D>::V;
     __shared__ float t[D * kThr];
     for (int i = threadIdx.x; i < D * kThr; i += blockDim.x) t[i] = thr[i];
     __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= s.n) return;
+    if (i >= (n_dev ? *n_dev : s.n)) return;
     const float4* x4 = reinterpret_cast<const float4*>(s.xyz) + (size_t)i * V;
     float x[4 * V];
 #pragma unroll
@@ -646,19 +646,26 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
 // representative with key <= the warp's bound, the exact test only where the
 // codes pass. A row stops at its first dominator, a warp when all its rows
 // are dominated.
-template <int D, bool CODES>
+// POSORDER: thread i takes sorted position i (row idx[i]; a warp's rows then
+// share a partition and have neighbouring keys, so they finish together) and
+// writes dead_pos[i]; otherwise thread i takes row i (coalesced stream) and
+// writes dead_row[i].
+template <int D, bool CODES, bool POSORDER>
 __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts, uint32_t d, uint32_t n,
+                                                   const uint32_t* __restrict__ idx,
                                                    const float4* __restrict__ rep_xyz,
                                                    const uint32_t* __restrict__ rep_key, const uint2* __restrict__ rep_qc,
-                                                   uint32_t nrep, const float* __restrict__ thr,
+                                                   uint32_t nrep_max, const uint32_t* nrep_dev,
+                                                   const float* __restrict__ thr,
                                                    uint8_t* __restrict__ dead_row, unsigned long long* tests) {
     constexpr int V = Dims2<D>::V;
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
+    const uint32_t nrep = nrep_dev ? min(*nrep_dev, nrep_max) : nrep_max;
     extern __shared__ float4 s_rep[];
-    uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)nrep * V);
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_code + nrep);
-    float* s_thr = reinterpret_cast<float*>(s_key + nrep);
+    uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)nrep_max * V);
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_code + nrep_max);
+    float* s_thr = reinterpret_cast<float*>(s_key + nrep_max);
     for (uint32_t i = threadIdx.x; i < nrep * V; i += blockDim.x) s_rep[i] = rep_xyz[i];
     for (uint32_t i = threadIdx.x; i < nrep; i += blockDim.x) {
         if (CODES) s_code[i] = rep_qc[i];
@@ -667,8 +674,9 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     if (CODES)
         for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
     __syncthreads();
-    const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;  // row order: coalesced reads
-    const bool valid = row < n;
+    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = slot < n && (!POSORDER || !dead_row[slot]);
+    const uint32_t row = (POSORDER && slot < n) ? idx[slot] : slot;
     float4 t[V];
     uint32_t tk = 0;
     uint32_t T0 = G, T1 = G | 0x80000000u;  // never passes unless set below
@@ -725,7 +733,11 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         }
         if (alive) nt += r;
     }
-    if (valid) dead_row[row] = alive ? 0 : 1;
+    if (POSORDER) {
+        if (valid && !alive) dead_row[slot] = 1;
+    } else if (valid) {
+        dead_row[row] = alive ? 0 : 1;
+    }
     if (tests) {
         nt = warp_sum(nt);
         if ((threadIdx.x & 31) == 0 && nt) atomicAdd(tests, nt);
@@ -817,8 +829,9 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey,
 }
 
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
-                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const float* thr, uint8_t* dead_row,
-                      uint8_t* dead_pos, unsigned long long* tests, int smem_optin, cudaStream_t st) {
+                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const uint32_t* nrep_dev,
+                      const float* thr, uint8_t* dead_row, uint8_t* dead_pos, unsigned long long* tests, int smem_optin,
+                      cudaStream_t st) {
     if (D > 16) return false;
     const bool codes = rep_qc && thr && nrep >= 32;
     const size_t smem = (size_t)nrep * ((D + 3) / 4) * 16 + (size_t)nrep * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64;
@@ -826,16 +839,22 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
     if (!n) return true;
     SKY_DISPATCH_D16(D, {
         if (codes) {
-            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_prefilter<DT, true><<<ceil_div(n, 256), 256, smem, st>>>(
-                pts, d, n, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, nrep, thr, dead_row, tests);
+            // many representatives: sorted positions, flags written in place
+            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            k_prefilter<DT, true, true><<<ceil_div(n, 256), 256, smem, st>>>(
+                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, nrep, nrep_dev, thr, dead_pos,
+                tests);
         } else {
-            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_prefilter<DT, false><<<ceil_div(n, 256), 256, smem, st>>>(
-                pts, d, n, reinterpret_cast<const float4*>(rep_xyz), rep_key, nullptr, nrep, nullptr, dead_row, tests);
+            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            k_prefilter<DT, false, false><<<ceil_div(n, 256), 256, smem, st>>>(
+                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, nullptr, nrep, nrep_dev, nullptr,
+                dead_row, tests);
         }
     });
     SKY_LAUNCH_CHECK();
+    if (codes) return true;
     k_gather_dead<<<ceil_div(n, 256), 256, 0, st>>>(idx, dead_row, n, dead_pos);
     SKY_LAUNCH_CHECK();
     return true;
@@ -867,9 +886,9 @@ void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, flo
     SKY_LAUNCH_CHECK();
 }
 
-void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st) {
+void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st, const uint32_t* n_dev) {
     if (!s.n) return;
-    SKY_DISPATCH_D16(D, (k_encode<DT><<<ceil_div(s.n, 256), 256, 0, st>>>(s, thr)));
+    SKY_DISPATCH_D16(D, (k_encode<DT><<<ceil_div(s.n, 256), 256, 0, st>>>(s, thr, n_dev)));
     SKY_LAUNCH_CHECK();
 }
 
