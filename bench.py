@@ -274,21 +274,28 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(local)
     n_sm = props.multi_processor_count
     sm_max = peaks.get("sm_max_mhz", 1965.0)
-    achieved = dom_tests / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0  # Gtest/s
-    if d <= 16:
-        per_clk = PACKED_TESTS_PER_CLK_PER_SM
-        unit_desc = ("1 dominance (pair) test on packed 2x32-bit monotone codes: 2 IMAD (fma pipe) + "
-                     "1 LOP3 + 1/2 VIMNMX3 (alu pipe); exact FP32 re-checks counted separately")
-    else:
-        per_clk = FP32_COMPARES_PER_CLK_PER_SM / d
-        unit_desc = f"1 dominance (pair) test = d = {d} FP32 compares"
-    peak = n_sm * per_clk * sm_max * 1e6 / 1e9
+    # 1 dominance test = d FP32 compares, peak 64 compares/clk/SM.
+    # The packed-code test evaluates d attributes in ~3.5 instructions, so this
+    # ratio may exceed 1 (SURVEY 8(d) anticipates it); `packed_issue` is the
+    # hardware-honest fraction against the packed test's own issue peak.
+    tests_s = dom_tests / (dom_ms / 1e3) if dom_ms > 0 else 0.0
+    achieved = tests_s * d / 1e9  # Gcompare/s
+    peak = n_sm * FP32_COMPARES_PER_CLK_PER_SM * sm_max * 1e6 / 1e9
+    per_clk = PACKED_TESTS_PER_CLK_PER_SM if d <= 16 else FP32_COMPARES_PER_CLK_PER_SM / d
+    ipeak = n_sm * per_clk * sm_max * 1e6
     roofline = {
         "bound": "alu", "kernel": "k_relsky3 + k_bnl2 (dominance tests)", "achieved": achieved, "peak": peak,
-        "unit": "Gtest/s", "frac": achieved / peak if peak else None, "traffic": None,
-        "algorithmic_unit": unit_desc,
-        "peak_source": f"{n_sm} SM x {per_clk:g} tests/clk x sm_max_mhz {sm_max} (MEASURED_PEAKS.json clock); "
-                       "fma/alu pipe issue, no HBM/tensor term (operands live in shared memory)",
+        "unit": "Gcompare/s", "frac": achieved / peak if peak else None, "traffic": None,
+        "algorithmic_unit": f"1 dominance (pair) test = d = {d} FP32 compares (SURVEY 8(d))",
+        "peak_source": f"{n_sm} SM x {FP32_COMPARES_PER_CLK_PER_SM} FP32 compare/clk x sm_max_mhz {sm_max} "
+                       "(MEASURED_PEAKS.json clock); ALU issue, no HBM/tensor term (operands in shared memory)",
+        "packed_issue": {
+            "achieved_gtest_s": tests_s / 1e9, "peak_gtest_s": ipeak / 1e9,
+            "frac": tests_s / ipeak if ipeak else None,
+            "model": ("d<=16: 2 IMAD (fma pipe) + 1 LOP3 + 1/2 VIMNMX3 (alu pipe) per test, fma/alu pipes 2 cyc "
+                      "per warp instruction -> 32 tests/clk/SM" if d <= 16 else
+                      f"d>16: {d} FP32 compares per test -> 64/{d} tests/clk/SM"),
+        },
         "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / statistics.mean(dev_ms),
         "tests_per_step": dom_tests,
     }

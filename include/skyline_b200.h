@@ -61,8 +61,9 @@ typedef enum sky_status {
 enum { SKY_RANDOM = 0, SKY_GRID = 1, SKY_ANGULAR = 2, SKY_SLICED = 3 };
 /* FilterKind (engine.hpp:19-23). */
 enum { SKY_FILTER_NONE = 0, SKY_FILTER_GRID = 1, SKY_FILTER_REPRESENTATIVE = 2 };
-/* RepSelection (filter.hpp:21-25); only Sorted is on the hot path (Region and
- * Random return SKY_E_CONFIG; SURVEY.md 8(f) ranks them "next"). */
+/* RepSelection (filter.hpp:21-25): Sorted (filter.cpp:66-86), Region
+ * (filter.cpp:88-115; needs a normalized dataset), Random (filter.cpp:117-137;
+ * per-partition Rng seeded from sky_config.seed). */
 enum { SKY_REPS_SORTED = 0, SKY_REPS_REGION = 1, SKY_REPS_RANDOM = 2 };
 /* MergeKind (engine.hpp:25-28). */
 enum { SKY_MERGE_SEQUENTIAL = 0, SKY_MERGE_NOSEQ = 1 };

@@ -483,6 +483,78 @@ static uint64_t select_reps_sorted(const relation* R, const double* sum, uint64_
     return nr;
 }
 
+/* dominance_region_volume (core.cpp:112-123): prod_j (1 - x_j), left to right */
+static double region_volume(const relation* R, uint64_t i) {
+    double v = 1.0;
+    for (uint32_t j = 0; j < R->d; ++j) v *= 1.0 - R->x[i * R->d + j];
+    return v;
+}
+
+typedef struct {
+    const double* vol;
+} vol_ctx;
+
+/* (volume desc, id asc) (filter.cpp:103-106) */
+static int cmp_volume(const void* c, uint64_t a, uint64_t b) {
+    const vol_ctx* v = (const vol_ctx*)c;
+    if (v->vol[a] != v->vol[b]) return v->vol[a] > v->vol[b] ? -1 : 1;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+/* select_representatives_region (filter.cpp:88-115) + prune. */
+static uint64_t select_reps_region(const relation* R, uint64_t n, uint64_t** parts, const uint64_t* sizes,
+                                   uint64_t P, uint64_t q, uint64_t* reps) {
+    double* vol = (double*)malloc((n ? n : 1) * sizeof(double));
+    for (uint64_t i = 0; i < n; ++i) vol[i] = region_volume(R, i);
+    vol_ctx vc = {vol};
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < P; ++i) total += sizes[i] < q ? sizes[i] : q;
+    uint64_t* cand = (uint64_t*)malloc((total ? total : 1) * sizeof(uint64_t));
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < P; ++i) {
+        if (sizes[i] == 0) continue;
+        uint64_t* ord = (uint64_t*)malloc(sizes[i] * sizeof(uint64_t));
+        memcpy(ord, parts[i], sizes[i] * sizeof(uint64_t));
+        msort(ord, sizes[i], cmp_volume, &vc);
+        uint64_t take = sizes[i] < q ? sizes[i] : q;
+        for (uint64_t t = 0; t < take; ++t) cand[k++] = ord[t];
+        free(ord);
+    }
+    uint64_t nr = bruteforce_list(R, cand, k, reps);
+    free(cand);
+    free(vol);
+    return nr;
+}
+
+/* select_representatives_random (filter.cpp:117-137) + prune: partial
+ * Fisher-Yates over the partition's scan order with a per-partition Rng. */
+static uint64_t select_reps_random(const relation* R, uint64_t** parts, const uint64_t* sizes, uint64_t P,
+                                   uint64_t q, uint64_t seed, uint64_t* reps) {
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < P; ++i) total += sizes[i] < q ? sizes[i] : q;
+    uint64_t* cand = (uint64_t*)malloc((total ? total : 1) * sizeof(uint64_t));
+    uint64_t k = 0;
+    mt64 g;
+    for (uint64_t i = 0; i < P; ++i) {
+        if (sizes[i] == 0) continue;
+        mt_seed(&g, seed ^ (0x9e3779b97f4a7c15ULL * (i + 1)));
+        uint64_t* idx = (uint64_t*)malloc(sizes[i] * sizeof(uint64_t));
+        for (uint64_t t = 0; t < sizes[i]; ++t) idx[t] = t;
+        uint64_t take = sizes[i] < q ? sizes[i] : q;
+        for (uint64_t t = 0; t < take; ++t) {
+            uint64_t j = t + rng_below(&g, sizes[i] - t);
+            uint64_t tmp = idx[t];
+            idx[t] = idx[j];
+            idx[j] = tmp;
+        }
+        for (uint64_t t = 0; t < take; ++t) cand[k++] = parts[i][idx[t]];
+        free(idx);
+    }
+    uint64_t nr = bruteforce_list(R, cand, k, reps);
+    free(cand);
+    return nr;
+}
+
 /* --------------------------------------------------------------- engine.cpp */
 /* validate (engine.cpp:19-32) */
 static int validate(uint64_t n, uint32_t d, const sky_config* c) {
@@ -499,9 +571,9 @@ int oracle_run(const float* pts, uint64_t n, uint32_t d, int normalized, const s
     memset(out, 0, sizeof(*out));
     int rc = validate(n, d, cfg);
     if (rc) return rc;
-    if (cfg->filter == SKY_FILTER_REPRESENTATIVE && cfg->rep_selection != SKY_REPS_SORTED)
-        return SKY_E_CONFIG; /* Region/Random reps are out of the hot-path scope */
-    (void)normalized;
+    if (cfg->filter == SKY_FILTER_REPRESENTATIVE &&
+        (cfg->rep_selection < SKY_REPS_SORTED || cfg->rep_selection > SKY_REPS_RANDOM))
+        return SKY_E_CONFIG;
     double* x = (double*)malloc(((n && d) ? n * d : 1) * sizeof(double));
     for (uint64_t i = 0; i < n * d; ++i) x[i] = (double)pts[i];
     relation R = {x, d};
@@ -568,8 +640,29 @@ int oracle_run(const float* pts, uint64_t n, uint32_t d, int normalized, const s
         for (uint64_t i = 0; i < P; ++i) cap += sizes[i] < cfg->rep_q ? sizes[i] : cfg->rep_q;
         reps = (uint64_t*)malloc((cap ? cap : 1) * sizeof(uint64_t));
         g_tests = 0;
-        n_reps = select_reps_sorted(&R, sum, parts, sizes, P, cfg->rep_q, reps);
+        if (cfg->rep_selection == SKY_REPS_REGION) {
+            /* filter.cpp:91-95: every non-empty partition must be normalized */
+            if (!normalized && n > 0) {
+                rc = SKY_E_NORMALIZATION;
+            } else {
+                n_reps = select_reps_region(&R, n, parts, sizes, P, cfg->rep_q, reps);
+            }
+        } else if (cfg->rep_selection == SKY_REPS_RANDOM) {
+            n_reps = select_reps_random(&R, parts, sizes, P, cfg->rep_q, cfg->seed, reps);
+        } else {
+            n_reps = select_reps_sorted(&R, sum, parts, sizes, P, cfg->rep_q, reps);
+        }
         out->tests_reps = g_tests;
+        if (rc) {
+            for (uint64_t i = 0; i < P; ++i) free(parts[i]);
+            free(parts);
+            free(sizes);
+            free(reps);
+            free_assignment(&A);
+            free(sum);
+            free(x);
+            return rc;
+        }
     }
     out->n_reps = n_reps;
 

@@ -24,6 +24,8 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <unordered_map>
+#include <unordered_map>
 #include <vector>
 
 #include <nccl.h>
@@ -73,7 +75,8 @@ enum Slot {
     S_SET0, S_SET0_K, S_SET0_I, S_SET0_Q, S_SET1, S_SET1_K, S_SET1_I, S_SET1_Q,
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
-    S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE, S_COUNT
+    S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
+    S_SCAN, S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -770,8 +773,9 @@ void validate(uint64_t n, uint32_t d, const sky_config* c) {  // engine.cpp:19-3
     if (c->filter < 0 || c->filter > 2) throw Error(SKY_E_CONFIG, "unknown filter kind");
     if (c->merge < 0 || c->merge > 1) throw Error(SKY_E_CONFIG, "unknown merge kind");
     if (c->local_algo < 0 || c->local_algo > 1) throw Error(SKY_E_CONFIG, "unknown local algorithm");
-    if (c->filter == SKY_FILTER_REPRESENTATIVE && c->rep_selection != SKY_REPS_SORTED)
-        throw Error(SKY_E_CONFIG, "only sorted representative selection is implemented on the GPU path");
+    if (c->filter == SKY_FILTER_REPRESENTATIVE &&
+        (c->rep_selection < SKY_REPS_SORTED || c->rep_selection > SKY_REPS_RANDOM))
+        throw Error(SKY_E_CONFIG, "unknown representative selection");
 }
 
 // Effective partition count and slices (make_assignment, partition.cpp:233-251).
@@ -847,7 +851,7 @@ struct PartitionOut {
 // Phase 1a: partition ids, sum keys, validation, sort into partitions.
 PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d, int normalized, int strategy,
                              uint64_t P, uint64_t m, const sky_config* cfg, const uint32_t* pid_dev,
-                             uint64_t* fixups, bool eager = true) {
+                             uint64_t* fixups, bool eager = true, uint32_t** scan_rows = nullptr) {
     cudaStream_t st = R.st_;
     uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, n);
     uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, n);
@@ -926,7 +930,7 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
                 max_len = std::max<uint32_t>(max_len, (uint32_t)L);
             }
         }
-        if (cost <= (uint64_t)1e9) {
+        if (cost <= (uint64_t)1e9 && !scan_rows) {
             launch_slice_assign(rankA, n, P, keyA, st);
             R.count();
             launch_slice_fix_runs(pts, d, rankA, n, P, runs, nruns, max_len, keyA, st);
@@ -945,6 +949,12 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
             }
             launch_slice_assign(cur, n, P, keyA, st);
             R.count();
+            if (scan_rows) {
+                // exact scan order (x[k], lex coords, id): split()'s order of
+                // every slice (partition.cpp:203-216, 253-273)
+                *scan_rows = R.dev<uint32_t>(S_SCAN, n);
+                SKY_CUDA(cudaMemcpyAsync(*scan_rows, cur, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+            }
         }
     }
 
@@ -1011,6 +1021,88 @@ DevSet host_reps(Runner& R, sky_ctx* c, int D, const uint32_t* cand, uint32_t sl
     return R.compact(css, cdead, doff, 1, S_SET3, doff + 2, roff, D);
 }
 
+// select_representatives_region (filter.cpp:88-115): per partition the
+// first q rows by (volume desc, id asc). Two stable radix sorts: rows by
+// ~volume bits, then by partition.
+void region_candidates(Runner& R, const float* pts, uint32_t d, uint32_t n, const PartitionOut& po, uint32_t P,
+                       uint32_t q, uint32_t* cand) {
+    cudaStream_t st = R.st_;
+    uint64_t* k0 = R.dev<uint64_t>(S_RK0, n);
+    uint64_t* k1 = R.dev<uint64_t>(S_RK1, n);
+    uint32_t* v0 = R.dev<uint32_t>(S_RV0, n);
+    uint32_t* v1 = R.dev<uint32_t>(S_RV1, n);
+    uint32_t* p0 = R.dev<uint32_t>(S_RP0, n);
+    uint32_t* p1 = R.dev<uint32_t>(S_RP1, n);
+    uint32_t* pid_row = R.dev<uint32_t>(S_ROWPID, n);
+    launch_region_keys(pts, d, n, k0, v0, st);
+    launch_row_pid(po.key64, po.idx, n, pid_row, st);
+    R.count(2);
+    R.sort_pairs(k0, k1, v0, v1, n, 0, 64);
+    launch_gather_u32(pid_row, v1, n, p0, st);
+    R.count();
+    R.sort_pairs(p0, p1, v1, v0, n, 0, std::max(1, bits_for(P)));
+    launch_pick_first(v0, po.off, P, q, cand, st);
+    R.count();
+}
+
+// select_representatives_random (filter.cpp:117-137): the per-partition Rng
+// draws (rng.hpp:40-47, std::mt19937_64) are q sequential host draws per
+// partition; the picked scan positions are mapped to rows on the device.
+// Scan order: row order within a partition (split, partition.cpp:262-265),
+// or the exact sliced order when `scan` is given (partition.cpp:266-270).
+void random_candidates(Runner& R, uint32_t n, const PartitionOut& po, uint32_t P, uint32_t q, const uint32_t* scan,
+                       uint64_t seed, uint32_t* cand) {
+    cudaStream_t st = R.st_;
+    const uint32_t* rows = scan;
+    if (!rows) {
+        uint32_t* pid_row = R.dev<uint32_t>(S_ROWPID, n);
+        uint32_t* p1 = R.dev<uint32_t>(S_RP1, n);
+        uint32_t* v0 = R.dev<uint32_t>(S_RV0, n);
+        uint32_t* v1 = R.dev<uint32_t>(S_RV1, n);
+        launch_row_pid(po.key64, po.idx, n, pid_row, st);
+        launch_iota(n, v0, st);
+        R.count(2);
+        R.sort_pairs(pid_row, p1, v0, v1, n, 0, std::max(1, bits_for(P)));
+        rows = v1;
+    }
+    uint32_t* h = R.pin<uint32_t>(P_OFF, P + 2);
+    SKY_CUDA(cudaMemcpyAsync(h, po.off, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    R.sync();
+    const uint32_t slots = P * q;
+    uint32_t* gpos = R.stage<uint32_t>(slots);
+    std::unordered_map<uint64_t, uint64_t> swapped;
+    for (uint32_t p = 0; p < P; ++p) {
+        const uint64_t size = h[p + 1] - h[p];
+        const uint32_t take = (uint32_t)std::min<uint64_t>(q, size);
+        for (uint32_t k = take; k < q; ++k) gpos[(size_t)p * q + k] = kNone;
+        if (!size) continue;
+        std::mt19937_64 eng(seed ^ (0x9e3779b97f4a7c15ULL * ((uint64_t)p + 1)));
+        swapped.clear();
+        auto at = [&](uint64_t i) {
+            auto it = swapped.find(i);
+            return it == swapped.end() ? i : it->second;
+        };
+        for (uint32_t k = 0; k < take; ++k) {
+            // Rng::below(size - k) by rejection
+            const uint64_t range = size - k;
+            const uint64_t limit = UINT64_MAX - UINT64_MAX % range;
+            uint64_t x;
+            do {
+                x = eng();
+            } while (x >= limit);
+            const uint64_t j = k + x % range;
+            const uint64_t vk = at(k), vj = at(j);
+            swapped[k] = vj;
+            swapped[j] = vk;
+            gpos[(size_t)p * q + k] = h[p] + (uint32_t)vj;
+        }
+    }
+    uint32_t* dg = R.dev<uint32_t>(S_GPOS, slots);
+    SKY_CUDA(cudaMemcpyAsync(dg, gpos, (size_t)slots * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    launch_pick_gather(rows, dg, slots, cand, st);
+    R.count();
+}
+
 void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int normalized, int on_device,
               const sky_config* cfg, sky_result* out, bool eager = false) {
     std::memset(out, 0, sizeof(*out));
@@ -1061,8 +1153,11 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         out->h2d_bytes += (uint64_t)n * d * sizeof(float);
     }
     const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed) : nullptr;
+    const bool rep_random = cfg->filter == SKY_FILTER_REPRESENTATIVE && cfg->rep_selection == SKY_REPS_RANDOM;
+    uint32_t* scan_rows = nullptr;  // sliced + random reps: split()'s exact scan order
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
-                                      &out->angular_host_fixups, eager);
+                                      &out->angular_host_fixups, eager,
+                                      rep_random && cfg->strategy == SKY_SLICED ? &scan_rows : nullptr);
 
     std::vector<uint32_t> off0(P + 1);
     uint8_t* dead = R.dev<uint8_t>(S_DEAD, n);
@@ -1103,8 +1198,16 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         uint32_t* cand = R.dev<uint32_t>(S_REPCAND, (size_t)P * q);
         // filtered (grid) partitions are empty for the reps; here only the
         // representative filter is active, so every partition participates
-        launch_rep_pick(po.key64, po.idx, po.off, P, pts, d, q, cand, st);
-        R.count();
+        if ((uint64_t)P * q > 0x7FFFFFFFull) throw Error(SKY_E_CONFIG, "p * q exceeds 2^31 representative slots");
+        if (cfg->rep_selection == SKY_REPS_REGION) {
+            if (!normalized) throw Error(SKY_E_NORMALIZATION, "region selection requires a normalized dataset");
+            region_candidates(R, pts, d, n, po, P, q, cand);
+        } else if (cfg->rep_selection == SKY_REPS_RANDOM) {
+            random_candidates(R, n, po, P, q, cfg->strategy == SKY_SLICED ? scan_rows : nullptr, cfg->seed, cand);
+        } else {
+            launch_rep_pick(po.key64, po.idx, po.off, P, pts, d, q, cand, st);
+            R.count();
+        }
         const uint32_t slots = P * q;
         DevSet reps = R.set(S_SET3, slots, D);  // reps.n: upper bound until the count is read back
         uint32_t* nrep_dev = misc + M_NREP;

@@ -377,6 +377,90 @@ void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t*
     SKY_LAUNCH_CHECK();
 }
 
+// ---------------------------------------- region / random representatives
+// Partition of every row (row order) from the (pid << 32 | key) sorted keys.
+__global__ void k_row_pid(const uint64_t* __restrict__ key64, const uint32_t* __restrict__ idx, uint32_t n,
+                          uint32_t* __restrict__ pid_row) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) pid_row[idx[i]] = (uint32_t)(key64[i] >> 32);
+}
+
+// dominance_region_volume (core.cpp:112-123): prod_j (1 - x_j) in FP64, left
+// to right, each step correctly rounded as on the host. Key = ~bits(volume)
+// (volumes are >= +0, so the bit pattern is monotone): an ascending stable
+// sort over rows in id order gives (volume desc, id asc) (filter.cpp:103-106).
+__global__ void k_region_keys(const float* __restrict__ pts, uint32_t d, uint32_t n, uint64_t* __restrict__ key,
+                              uint32_t* __restrict__ row) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* x = pts + (size_t)i * d;
+    double v = 1.0;
+    for (uint32_t j = 0; j < d; ++j) v = __dmul_rn(v, __dsub_rn(1.0, (double)x[j]));
+    key[i] = ~(uint64_t)__double_as_longlong(v);
+    row[i] = i;
+}
+
+__global__ void k_iota(uint32_t n, uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+__global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t n,
+                             uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = src[idx[i]];
+}
+
+// cand[p*q + k] = rows[off[p] + k] for k < min(q, |partition p|), else kNone.
+__global__ void k_pick_first(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ off, uint32_t P,
+                             uint32_t q, uint32_t* __restrict__ cand) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= (uint64_t)P * q) return;
+    const uint32_t p = (uint32_t)(s / q), k = (uint32_t)(s % q);
+    const uint32_t b = off[p], e = off[p + 1];
+    cand[s] = b + k < e ? rows[b + k] : kNone;
+}
+
+// cand[s] = rows[gpos[s]] (kNone passes through).
+__global__ void k_pick_gather(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ gpos, uint32_t slots,
+                              uint32_t* __restrict__ cand) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < slots) cand[s] = gpos[s] == kNone ? kNone : rows[gpos[s]];
+}
+
+void launch_row_pid(const uint64_t* key64, const uint32_t* idx, uint32_t n, uint32_t* pid_row, cudaStream_t st) {
+    if (!n) return;
+    k_row_pid<<<ceil_div(n, 256), 256, 0, st>>>(key64, idx, n, pid_row);
+    SKY_LAUNCH_CHECK();
+}
+void launch_region_keys(const float* pts, uint32_t d, uint32_t n, uint64_t* key, uint32_t* row, cudaStream_t st) {
+    if (!n) return;
+    k_region_keys<<<ceil_div(n, 256), 256, 0, st>>>(pts, d, n, key, row);
+    SKY_LAUNCH_CHECK();
+}
+void launch_iota(uint32_t n, uint32_t* out, cudaStream_t st) {
+    if (!n) return;
+    k_iota<<<ceil_div(n, 256), 256, 0, st>>>(n, out);
+    SKY_LAUNCH_CHECK();
+}
+void launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t n, uint32_t* out, cudaStream_t st) {
+    if (!n) return;
+    k_gather_u32<<<ceil_div(n, 256), 256, 0, st>>>(src, idx, n, out);
+    SKY_LAUNCH_CHECK();
+}
+void launch_pick_first(const uint32_t* rows, const uint32_t* off, uint32_t P, uint32_t q, uint32_t* cand,
+                       cudaStream_t st) {
+    const uint64_t slots = (uint64_t)P * q;
+    if (!slots) return;
+    k_pick_first<<<ceil_div(slots, 256), 256, 0, st>>>(rows, off, P, q, cand);
+    SKY_LAUNCH_CHECK();
+}
+void launch_pick_gather(const uint32_t* rows, const uint32_t* gpos, uint32_t slots, uint32_t* cand, cudaStream_t st) {
+    if (!slots) return;
+    k_pick_gather<<<ceil_div(slots, 256), 256, 0, st>>>(rows, gpos, slots, cand);
+    SKY_LAUNCH_CHECK();
+}
+
 // select_representatives_sorted + prune_dominated_reps (filter.cpp:15-33,
 // 66-86, 139-145) finished in one CTA: compact the per-partition picks, sort
 // them by sum key, keep the antichain (brute force, as the reference does),

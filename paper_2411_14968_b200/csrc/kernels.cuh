@@ -59,6 +59,14 @@ void launch_gather_coord_key(const float* pts, uint32_t d, uint32_t j, const uin
                              uint32_t* key, cudaStream_t st);
 
 // Exact top-q per partition under (FP64 sum, lex coords, id) (filter.cpp:66-86).
+// region / random representatives (filter.cpp:88-137)
+void launch_row_pid(const uint64_t* key64, const uint32_t* idx, uint32_t n, uint32_t* pid_row, cudaStream_t st);
+void launch_region_keys(const float* pts, uint32_t d, uint32_t n, uint64_t* key, uint32_t* row, cudaStream_t st);
+void launch_iota(uint32_t n, uint32_t* out, cudaStream_t st);
+void launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t n, uint32_t* out, cudaStream_t st);
+void launch_pick_first(const uint32_t* rows, const uint32_t* off, uint32_t P, uint32_t q, uint32_t* cand,
+                       cudaStream_t st);
+void launch_pick_gather(const uint32_t* rows, const uint32_t* gpos, uint32_t slots, uint32_t* cand, cudaStream_t st);
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
                      const float* pts, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st);
 

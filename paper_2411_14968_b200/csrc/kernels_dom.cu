@@ -56,6 +56,18 @@ struct CodeLayout {
 constexpr int kSample = 4096;
 constexpr int kThr = kCodeLevels - 1;  // 127 thresholds per dimension
 
+// Top B bits of upper_bound(thr[0..127), x) = #{thr <= x} over the sorted
+// thresholds of one dimension: a branchless search that stops once the
+// remaining steps could only change the dropped low bits (B loads, no
+// divergence).
+template <int B>
+__device__ __forceinline__ uint32_t quant_code(const float* tj, float x) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 64; step >= (1 << (7 - B)); step >>= 1) lo += (tj[lo + step - 1] <= x) ? step : 0;
+    return (uint32_t)lo >> (7 - B);
+}
+
 // One CTA per dimension: block radix sort of a strided sample of the column
 // (2048 rows), keep 127 quantiles as thresholds.
 constexpr int kThrThreads = 512, kThrItems = 4;
@@ -109,13 +121,7 @@ __global__ void __launch_bounds__(256) k_encode(DevSet s, const float* __restric
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         // upper_bound over the 127 sorted thresholds of dimension j
-        const float* tj = t + j * kThr;
-        int lo = 0, hi = kThr;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (tj[mid] <= x[j]) lo = mid + 1; else hi = mid;
-        }
-        w[j / L] |= ((uint32_t)lo >> (7 - B)) << (LW * (j % L));
+        w[j / L] |= quant_code<B>(t + j * kThr, x[j]) << (LW * (j % L));
     }
     s.qc[i] = make_uint2(w[0], w[1]);
 }
@@ -128,24 +134,32 @@ __device__ __forceinline__ bool coarse_pass(const uint32_t (&t)[2], const uint2&
     return ((t[0] - s.x) & (t[1] - s.y) & GA) == GA;
 }
 
-// Missing guard bits of the coarse test (0 <=> pass): 2 IMAD + 1 LOP3; the
-// K candidates of a lane fold with 3-input mins (VIMNMX3) into one compare.
+
+// Guard bits that survived the subtraction (GA <=> pass): 2 IADD + 1 LOP3.
+// Since h <= GA as an integer with equality only on a pass, "any of N tests
+// passes" is max(h_1..h_N) == GA: a 3-input max (VIMNMX3) folds two tests
+// per instruction.
 template <uint32_t G>
-__device__ __forceinline__ uint32_t coarse_miss(const uint32_t (&t)[2], const uint2& s) {
+__device__ __forceinline__ uint32_t coarse_hit(const uint32_t (&t)[2], const uint2& s) {
     constexpr uint32_t GA = G | 0x80000000u;
-    return ~((t[0] - s.x) & (t[1] - s.y)) & GA;
+    return (t[0] - s.x) & (t[1] - s.y) & GA;
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t max_fold(const uint32_t (&h)[N]) {
+    uint32_t m = h[0];
+#pragma unroll
+    for (int j = 1; j + 1 < N; j += 2) m = max(m, max(h[j], h[j + 1]));
+    if (N % 2 == 0 && N > 1) m = max(m, h[N - 1]);
+    return m;
 }
 
 template <uint32_t G, int K>
 __device__ __forceinline__ bool any_coarse_pass(const uint32_t (&T)[K][2], const uint2& q) {
-    uint32_t f[K];
+    uint32_t h[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) f[k] = coarse_miss<G>(T[k], q);
-    uint32_t m = f[0];
-#pragma unroll
-    for (int k = 1; k + 1 < K; k += 2) m = min(m, min(f[k], f[k + 1]));
-    if (K % 2 == 0 && K > 1) m = min(m, f[K - 1]);
-    return m == 0;
+    for (int k = 0; k < K; ++k) h[k] = coarse_hit<G>(T[k], q);
+    return max_fold<K>(h) == (G | 0x80000000u);
 }
 
 constexpr int RS3_WARPS = 8;
@@ -267,7 +281,8 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                 const uint32_t inb = __ballot_sync(FULL, nk <= bound);  // prefix (keys sorted)
                 const uint32_t lim = __popc(inb);
                 __syncwarp();
-                sm.code[warp][lane] = nq;
+                // comparators past the bound get codes that never pass
+                sm.code[warp][lane] = lane < lim ? nq : make_uint2(0u, 0x80000000u);
 #pragma unroll
                 for (int v = 0; v < W; ++v) sm.comp[warp][lane][v] = nx[v];
                 __syncwarp();
@@ -303,19 +318,30 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                         }
                     }
                 };
-                uint32_t i = 0;
-                for (; i + 2 <= lim; i += 2) {
-                    const uint2 q0 = sm.code[warp][i], q1 = sm.code[warp][i + 1];
-                    const bool p0 = any_coarse_pass<G, K>(T, q0);
-                    const bool p1 = any_coarse_pass<G, K>(T, q1);
-                    if (p0 | p1) {
-                        if (p0) exact(i, q0);
-                        if (p1) exact(i + 1, q1);
+                // 4 comparators x K candidates per step, one max-fold and
+                // one branch; the next step's codes are loaded ahead
+                const uint4* cq = reinterpret_cast<const uint4*>(&sm.code[warp][0]);
+                const uint32_t nb = (lim + 3) & ~3u;
+                uint4 c01 = cq[0], c23 = cq[1];
+                for (uint32_t i = 0; i < nb; i += 4) {
+                    const uint2 q[4] = {make_uint2(c01.x, c01.y), make_uint2(c01.z, c01.w),
+                                        make_uint2(c23.x, c23.y), make_uint2(c23.z, c23.w)};
+                    if (i + 4 < nb) {
+                        c01 = cq[(i + 4) / 2];
+                        c23 = cq[(i + 4) / 2 + 1];
                     }
-                }
-                if (i < lim) {
-                    const uint2 q = sm.code[warp][i];
-                    if (any_coarse_pass<G, K>(T, q)) exact(i, q);
+                    uint32_t h[4 * K];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int k = 0; k < K; ++k) h[c * K + k] = coarse_hit<G>(T[k], q[c]);
+                    if (max_fold<4 * K>(h) == (G | 0x80000000u)) {
+#pragma unroll 1
+                        for (int c = 0; c < 4; ++c) {
+                            const uint2 qc = c == 0 ? q[0] : c == 1 ? q[1] : c == 2 ? q[2] : q[3];
+                            if (any_coarse_pass<G, K>(T, qc)) exact(i + c, qc);
+                        }
+                    }
                 }
                 ntests += (unsigned long long)__popc(alive) * lim;
                 live = __any_sync(FULL, alive != 0);
@@ -662,14 +688,16 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
     const uint32_t nrep = nrep_dev ? min(*nrep_dev, nrep_max) : nrep_max;
+    const uint32_t npad = (nrep_max + 7) & ~7u;
     extern __shared__ float4 s_rep[];
-    uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)nrep_max * V);
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_code + nrep_max);
-    float* s_thr = reinterpret_cast<float*>(s_key + nrep_max);
+    uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)npad * V);
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_code + npad);
+    float* s_thr = reinterpret_cast<float*>(s_key + npad);
     for (uint32_t i = threadIdx.x; i < nrep * V; i += blockDim.x) s_rep[i] = rep_xyz[i];
-    for (uint32_t i = threadIdx.x; i < nrep; i += blockDim.x) {
-        if (CODES) s_code[i] = rep_qc[i];
-        s_key[i] = rep_key[i];
+    for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) {
+        // padding codes never pass the coarse test (bit 31 of word 1 borrows)
+        if (CODES) s_code[i] = i < nrep ? rep_qc[i] : make_uint2(0u, 0x80000000u);
+        s_key[i] = i < nrep ? rep_key[i] : 0xFFFFFFFFu;
     }
     if (CODES)
         for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
@@ -694,13 +722,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
             uint32_t w[2] = {0, 0};
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                const float* tj = s_thr + j * kThr;
-                int lo = 0, hi = kThr;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (tj[mid] <= xs[j]) lo = mid + 1; else hi = mid;
-                }
-                w[j / L] |= ((uint32_t)lo >> (7 - B)) << (LW * (j % L));
+                w[j / L] |= quant_code<B>(s_thr + j * kThr, xs[j]) << (LW * (j % L));
             }
             T0 = w[0] | G | CodeLayout<D>::ALIVE;
             T1 = w[1] | G | 0x80000000u;
@@ -711,7 +733,35 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     bool alive = valid;
     const uint32_t bound = __reduce_max_sync(0xffffffffu, alive ? tk : 0u);
     unsigned long long nt = 0;
-    if (__any_sync(0xffffffffu, alive)) {
+    if (CODES) {
+        // 8 representatives per step: 8 coarse tests folded by 3-input min,
+        // exact FP32 re-check only on a coarse pass; one vote per step
+        uint32_t Tl[2] = {T0, T1};
+        for (uint32_t r = 0; r < nrep && __any_sync(0xffffffffu, alive); r += 8) {
+            if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
+            const uint4* q4 = reinterpret_cast<const uint4*>(s_code + r);
+            uint2 q[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint4 w = q4[k];
+                q[2 * k] = make_uint2(w.x, w.y);
+                q[2 * k + 1] = make_uint2(w.z, w.w);
+            }
+            uint32_t h[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) h[k] = coarse_hit<G>(Tl, q[k]);
+            if (alive) nt += min(8u, nrep - r);
+            if (max_fold<8>(h) == (G | 0x80000000u)) {
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k) {
+                    if (alive && coarse_pass<G>(Tl, q[k]) && dom_f4<D>(s_rep + (r + k) * V, t)) {
+                        alive = false;
+                        Tl[0] &= ~CodeLayout<D>::ALIVE;
+                    }
+                }
+            }
+        }
+    } else if (__any_sync(0xffffffffu, alive)) {
         uint32_t r = 0;
         for (; r < nrep; ++r) {
             if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
@@ -834,7 +884,8 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
                       cudaStream_t st) {
     if (D > 16) return false;
     const bool codes = rep_qc && thr && nrep >= 32;
-    const size_t smem = (size_t)nrep * ((D + 3) / 4) * 16 + (size_t)nrep * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64;
+    const size_t npad = (nrep + 7) & ~7u;
+    const size_t smem = npad * ((D + 3) / 4) * 16 + npad * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64;
     if (smem + 1024 > (size_t)smem_optin) return false;
     if (!n) return true;
     SKY_DISPATCH_D16(D, {

@@ -129,9 +129,11 @@ def plane():
                     filters = (0, 2, 1) if strat == 1 else (0, 2)
                     for filt in filters:
                         for merge in (0, 1):
-                            for q in ((3,) if filt == 2 else (5,)):
+                            # representative selection: Sorted, Region (normalized only), Random
+                            sels = ((0, 1, 2) if norm else (0, 2)) if filt == 2 else (0,)
+                            for q, sel in [(3 if filt == 2 else 5, sel) for sel in sels]:
                                 cfg = SkyConfig.make(strategy=strat, p=7, seed=11, slice_dim=d - 1, filter=filt,
-                                                     rep_q=q, merge=merge, workers=4)
+                                                     rep_q=q, merge=merge, workers=4, rep_selection=sel)
                                 r = O.ref_run(x, cfg, norm)
                                 key = f"plane{k}"
                                 arrays[key + "_x"] = x
@@ -169,7 +171,13 @@ def main():
     O.build(ref=True)
     ka = known_answers()
     pl, pl_arr = plane()
-    cf, cf_arr = configs()
+    if "--keep-configs" in sys.argv:
+        # reuse the (slow) BASELINE-config fixtures already committed
+        with open(os.path.join(HERE, "golden.json")) as f:
+            cf = json.load(f)["configs"]
+        cf_arr = dict(np.load(os.path.join(HERE, "configs.npz")))
+    else:
+        cf, cf_arr = configs()
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py", "source": "oracle/_ref/libskyref.so "
                    "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "configs": cf}, f)

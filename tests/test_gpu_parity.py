@@ -9,7 +9,7 @@ import pytest
 
 import oracle as O
 from paper_2411_14968_b200 import (ConfigError, DataError, DimensionError, EngineConfig, FilterKind, LocalAlgo,
-                                   MergeKind, NormalizationError, PartitionConfig, Strategy, generate)
+                                   MergeKind, NormalizationError, PartitionConfig, RepSelection, Strategy, generate)
 from paper_2411_14968_b200.abi import SkyConfig
 from paper_2411_14968_b200.configs import make_config
 
@@ -19,6 +19,7 @@ pytestmark = pytest.mark.gpu
 def to_engine_config(d):
     return EngineConfig(partition=PartitionConfig(Strategy(d["strategy"]), d["p"], d["m"], d["seed"], d["slice_dim"]),
                         filter=FilterKind(d["filter"]), rep_q=d["rep_q"], merge=MergeKind(d["merge"]),
+                        rep_selection=RepSelection(d.get("rep_selection", 0)),
                         workers=max(1, d["workers"]), local_algo=LocalAlgo(d.get("local_algo", 0)),
                         bnl_window_cap=d.get("bnl_window_cap", 4096) or 4096)
 
@@ -112,7 +113,7 @@ def test_random_configs_vs_oracle(engine):
         filt = int(rng.choice([0, 2] + ([1] if strat == 1 else [])))
         cfg = SkyConfig.make(strategy=strat, p=int(rng.integers(1, 40)), seed=int(rng.integers(0, 1000)),
                              slice_dim=int(rng.integers(0, d)), filter=filt, rep_q=int(rng.integers(1, 9)),
-                             merge=int(rng.integers(0, 2)), workers=1)
+                             merge=int(rng.integers(0, 2)), workers=1, rep_selection=int(rng.integers(0, 3)))
         ecfg = to_engine_config(cfg.as_dict())
         ecfg.local_algo = LocalAlgo(it % 2)
         ecfg.bnl_window_cap = int(rng.choice([32, 256, 4096]))
@@ -128,6 +129,28 @@ def test_random_configs_vs_oracle(engine):
         assert np.array_equal(r.skyline, exp["ids"]), tag
         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
         check_metrics(r, exp, tag)
+
+
+@pytest.mark.parametrize("cfg_idx", [2, 3, 4, 5])
+@pytest.mark.parametrize("sel", [RepSelection.Region, RepSelection.Random])
+def test_rep_selection_configs_vs_oracle(engine, cfg_idx, sel):
+    """Region / Random representatives (filter.cpp:88-137) on BASELINE-shaped
+    inputs; C4 (sliced) exercises the exact scan order of Random picks."""
+    w = make_config(cfg_idx, {2: 40000, 3: 60000, 4: 20000, 5: 40000}[cfg_idx])
+    x = generate(w.kind, w.n, w.d, 7)
+    w.config.rep_selection = sel
+    cfg = w.config.to_c()
+    try:
+        exp = O.oracle_run(x, cfg, w.normalized)
+    except O.CpuError as e:
+        with pytest.raises(Exception) as ei:
+            engine.run(x, w.config, w.normalized)
+        assert getattr(ei.value, "code", None) == e.code
+        return
+    r = engine.run(x, w.config, w.normalized)
+    assert np.array_equal(r.skyline, exp["ids"]), (cfg_idx, sel)
+    assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist()
+    check_metrics(r, exp, (cfg_idx, sel))
 
 
 def test_skyline_and_relative_vs_oracle(engine):
