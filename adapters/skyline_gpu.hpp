@@ -8,9 +8,9 @@
 // PhaseMetrics fields (engine.hpp:40-57). Errors come back as the reference's
 // exception classes (core.hpp:13-34).
 //
-// Requirements: coordinates exactly representable in float32 (the GPU engine
-// compares float32; the BASELINE inputs are float32), d <= 32, and one
-// sky_ctx per thread.
+// Any finite double coordinates: rows that are all float32 values go through
+// sky_run, others through sky_run_f64 (FP64 decisions, identical results).
+// d <= 32 and one sky_ctx per thread.
 #pragma once
 
 #include <cmath>
@@ -58,6 +58,7 @@ inline sky_config to_sky(const EngineConfig& e) {
     c.rep_selection = static_cast<int32_t>(e.rep_selection);
     c.rep_q = e.rep_q;
     c.merge = static_cast<int32_t>(e.merge);
+    c.rep_seed = e.seed;
     c.workers = e.workers;
     return c;
 }
@@ -68,20 +69,29 @@ inline sky_config to_sky(const EngineConfig& e) {
 inline RunResult run(Context& g, const Dataset& r, const EngineConfig& config) {
     const size_t n = r.size(), d = r.d;
     std::vector<float> rows(n * d);
+    std::vector<double> rows64;
+    bool exact32 = true;
     for (size_t i = 0; i < n; ++i) {
         const Point& t = r.points[i];
         if (t.dim() != d) throw DimensionError("ragged dataset");
         for (size_t j = 0; j < d; ++j) {
             const float f = static_cast<float>(t.coords[j]);
-            if (static_cast<double>(f) != t.coords[j] && std::isfinite(t.coords[j]))
-                throw DataError("coordinate not representable in float32");
+            if (static_cast<double>(f) != t.coords[j] && !std::isnan(t.coords[j])) exact32 = false;
             rows[i * d + j] = f;
         }
     }
+    if (!exact32) {
+        rows64.resize(n * d);
+        for (size_t i = 0; i < n; ++i)
+            for (size_t j = 0; j < d; ++j) rows64[i * d + j] = r.points[i].coords[j];
+    }
     const sky_config c = to_sky(config);
     sky_result res;
-    throw_status(sky_run(g.ctx, rows.data(), n, static_cast<uint32_t>(d), r.normalized ? 1 : 0, 0, &c, &res),
-                 sky_last_error(g.ctx));
+    const int rc = exact32 ? sky_run(g.ctx, rows.data(), n, static_cast<uint32_t>(d), r.normalized ? 1 : 0, 0, &c,
+                                     &res)
+                           : sky_run_f64(g.ctx, rows64.data(), n, static_cast<uint32_t>(d), r.normalized ? 1 : 0,
+                                         0, &c, &res);
+    throw_status(rc, sky_last_error(g.ctx));
     RunResult out;
     out.config = config;
     out.effective_p = res.effective_p;

@@ -87,6 +87,10 @@ typedef struct sky_config {
     int32_t local_algo;       /* SKY_LOCAL_SFS | SKY_LOCAL_BNL */
     uint32_t bnl_window_cap;  /* BNL window capacity in points (0 -> 4096) */
     int32_t count_tests;      /* nonzero: kernels count dominance tests */
+    /* EngineConfig::seed (engine.hpp:37): Random representative selection
+     * (filter.cpp:117-137); PartitionConfig::seed above drives the random
+     * partitioner. The reference CLI sets both from --seed (cli.cpp:177-184). */
+    uint64_t rep_seed;
 } sky_config;
 
 /* RunResult + PhaseMetrics (engine.hpp:40-57). Owned by the library until
@@ -138,6 +142,14 @@ SKY_API void sky_config_default(sky_config* cfg);
  * points_on_device == 0 (copied H2D inside the call) or a device pointer on
  * the context's device otherwise. */
 SKY_API int sky_run(sky_ctx* ctx, const float* points, uint64_t n, uint32_t d,
+            int normalized, int points_on_device, const sky_config* cfg,
+            sky_result* out);
+/* skyline::run on FP64 rows (the reference's Dataset coordinates, any
+ * finite double): identical results to the reference for every input.
+ * Keys, codes and coarse tests run on the rows' float32 image; every
+ * dominance decision, partition id, sum and sort order that decides the
+ * result is taken on the doubles (core.hpp:89-107, partition.cpp). */
+SKY_API int sky_run_f64(sky_ctx* ctx, const double* points, uint64_t n, uint32_t d,
             int normalized, int points_on_device, const sky_config* cfg,
             sky_result* out);
 SKY_API void sky_result_free(sky_result* r);

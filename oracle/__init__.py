@@ -72,11 +72,24 @@ _u8p = C.POINTER(C.c_uint8)
 _u64p = C.POINTER(C.c_uint64)
 _i64p = C.POINTER(C.c_int64)
 _f32p = C.POINTER(C.c_float)
+_f64p = C.POINTER(C.c_double)
 
 
 def _f32(a):
     a = np.ascontiguousarray(a, dtype=np.float32)
     return a, a.ctypes.data_as(_f32p)
+
+
+def _rows(a):
+    """(array, pointer, is_f64): float64 arrays stay FP64 (the reference's
+    own coordinate type), anything else becomes float32."""
+    if np.asarray(a).dtype == np.float64:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.ndim == 1:
+            a = a.reshape(-1, 1) if a.size else a.reshape(0, 0)
+        return a, a.ctypes.data_as(_f64p), True
+    a, p = _f32(a)
+    return a, p, False
 
 
 def oracle_lib():
@@ -86,6 +99,8 @@ def oracle_lib():
             build(ref=False)
         lib = C.CDLL(ORACLE_SO)
         lib.oracle_run.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), C.POINTER(_OracleResult)]
+        lib.oracle_run_f64.argtypes = [_f64p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig),
+                                       C.POINTER(_OracleResult)]
         lib.oracle_result_free.argtypes = [C.POINTER(_OracleResult)]
         lib.oracle_assign.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), _u64p, _u64p]
         lib.oracle_bruteforce.argtypes = [_f32p, C.c_uint64, C.c_uint32, _i64p]
@@ -115,6 +130,9 @@ def ref_lib():
             raise RuntimeError(f"{REF_SO} missing: run `make -C oracle ref` where /root/reference exists")
         lib = C.CDLL(REF_SO)
         lib.skyref_run.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), C.POINTER(_RefResult)]
+        lib.skyref_run_f64.argtypes = [_f64p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig),
+                                       C.POINTER(_RefResult)]
+        lib.skyref_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _f64p]
         lib.skyref_result_free.argtypes = [C.POINTER(_RefResult)]
         lib.skyref_assign.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), _u64p, _u64p]
         lib.skyref_bruteforce.argtypes = [_f32p, C.c_uint64, C.c_uint32, _i64p]
@@ -161,10 +179,10 @@ class CpuError(RuntimeError):
 
 def oracle_run(points, cfg: SkyConfig, normalized: bool = True) -> CpuRun:
     lib = oracle_lib()
-    a, p = _f32(points)
+    a, p, f64 = _rows(points)
     n, d = a.shape
     res = _OracleResult()
-    rc = lib.oracle_run(p, n, d, int(normalized), C.byref(cfg), C.byref(res))
+    rc = (lib.oracle_run_f64 if f64 else lib.oracle_run)(p, n, d, int(normalized), C.byref(cfg), C.byref(res))
     if rc:
         raise CpuError(rc)
     try:
@@ -177,10 +195,10 @@ def oracle_run(points, cfg: SkyConfig, normalized: bool = True) -> CpuRun:
 
 def ref_run(points, cfg: SkyConfig, normalized: bool = True) -> CpuRun:
     lib = ref_lib()
-    a, p = _f32(points)
+    a, p, f64 = _rows(points)
     n, d = a.shape
     res = _RefResult()
-    rc = lib.skyref_run(p, n, d, int(normalized), C.byref(cfg), C.byref(res))
+    rc = (lib.skyref_run_f64 if f64 else lib.skyref_run)(p, n, d, int(normalized), C.byref(cfg), C.byref(res))
     if rc:
         raise CpuError(rc)
     try:
@@ -239,3 +257,13 @@ def random_permutation(n, seed):
     out = np.zeros(max(n, 1), np.uint64)
     oracle_lib().oracle_random_permutation(n, seed, out.ctypes.data_as(_u64p))
     return out[:n]
+
+
+def ref_generate(dist: int, n: int, d: int, seed: int) -> np.ndarray:
+    """skyline::generate (datagen.cpp:127-151) of the reference itself:
+    dist 0 uniform, 1 correlated, 2 anticorrelated; FP64 rows."""
+    out = np.zeros((n, d), np.float64)
+    rc = ref_lib().skyref_generate(dist, n, d, seed, out.ctypes.data_as(_f64p))
+    if rc:
+        raise CpuError(rc)
+    return out

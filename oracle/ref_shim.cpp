@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "skyline/core.hpp"
+#include "skyline/datagen.hpp"
 #include "skyline/engine.hpp"
 #include "skyline/filter.hpp"
 #include "skyline/partition.hpp"
@@ -23,7 +24,8 @@ using namespace skyline;
 
 namespace {
 
-Dataset to_dataset(const float* pts, uint64_t n, uint32_t d, int normalized) {
+template <class T>
+Dataset to_dataset(const T* pts, uint64_t n, uint32_t d, int normalized) {
     Dataset r;
     r.d = d;
     r.normalized = normalized != 0;
@@ -47,7 +49,7 @@ EngineConfig to_engine(const sky_config* c) {
     e.rep_q = c->rep_q;
     e.merge = static_cast<MergeKind>(c->merge);
     e.workers = c->workers;
-    e.seed = c->seed;
+    e.seed = c->rep_seed;
     return e;
 }
 
@@ -91,8 +93,9 @@ int skyref_hardware_concurrency(void) {
 
 // skyline::run on float32 rows upcast to double. run_ms is the steady_clock
 // time of run() alone (engine.cpp:144-194 phase timers summed by the caller).
-int skyref_run(const float* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
-               skyref_result* out) {
+extern "C++" {
+template <class T>
+int run_any(const T* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg, skyref_result* out) {
     std::memset(out, 0, sizeof(*out));
     return guarded([&] {
         const Dataset r = to_dataset(pts, n, d, normalized);
@@ -115,6 +118,33 @@ int skyref_run(const float* pts, uint64_t n, uint32_t d, int normalized, const s
         out->partition_ms = res.metrics.partition_ms;
         out->local_ms = res.metrics.local_ms;
         out->merge_ms = res.metrics.merge_ms;
+    });
+}
+}  // extern "C++"
+
+int skyref_run(const float* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+               skyref_result* out) {
+    return run_any(pts, n, d, normalized, cfg, out);
+}
+
+// skyline::run on FP64 rows (the reference's own coordinate type).
+int skyref_run_f64(const double* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+                   skyref_result* out) {
+    return run_any(pts, n, d, normalized, cfg, out);
+}
+
+// skyline::generate (datagen.cpp:127-151): dist 0 uniform, 1 correlated,
+// 2 anticorrelated; rows into out[n*d].
+int skyref_generate(int dist, uint64_t n, uint64_t d, uint64_t seed, double* out) {
+    return guarded([&] {
+        GenSpec g;
+        g.distribution = static_cast<Distribution>(dist);
+        g.n = n;
+        g.d = d;
+        g.seed = seed;
+        const Dataset r = generate(g);
+        for (uint64_t i = 0; i < n; ++i)
+            for (uint64_t j = 0; j < d; ++j) out[i * d + j] = r.points[i].coords[j];
     });
 }
 

@@ -566,16 +566,37 @@ static int validate(uint64_t n, uint32_t d, const sky_config* c) {
     return SKY_OK;
 }
 
+static int oracle_run_x(double* x, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+                        oracle_result* out);
+
 int oracle_run(const float* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
                oracle_result* out) {
-    memset(out, 0, sizeof(*out));
-    int rc = validate(n, d, cfg);
-    if (rc) return rc;
-    if (cfg->filter == SKY_FILTER_REPRESENTATIVE &&
-        (cfg->rep_selection < SKY_REPS_SORTED || cfg->rep_selection > SKY_REPS_RANDOM))
-        return SKY_E_CONFIG;
     double* x = (double*)malloc(((n && d) ? n * d : 1) * sizeof(double));
     for (uint64_t i = 0; i < n * d; ++i) x[i] = (double)pts[i];
+    return oracle_run_x(x, n, d, normalized, cfg, out);
+}
+
+int oracle_run_f64(const double* pts, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+                   oracle_result* out) {
+    double* x = (double*)malloc(((n && d) ? n * d : 1) * sizeof(double));
+    if (n && d) memcpy(x, pts, n * d * sizeof(double));
+    return oracle_run_x(x, n, d, normalized, cfg, out);
+}
+
+/* takes ownership of x */
+static int oracle_run_x(double* x, uint64_t n, uint32_t d, int normalized, const sky_config* cfg,
+                        oracle_result* out) {
+    memset(out, 0, sizeof(*out));
+    int rc = validate(n, d, cfg);
+    if (rc) {
+        free(x);
+        return rc;
+    }
+    if (cfg->filter == SKY_FILTER_REPRESENTATIVE &&
+        (cfg->rep_selection < SKY_REPS_SORTED || cfg->rep_selection > SKY_REPS_RANDOM)) {
+        free(x);
+        return SKY_E_CONFIG;
+    }
     relation R = {x, d};
     double* sum = (double*)malloc((n ? n : 1) * sizeof(double));
     for (uint64_t i = 0; i < n; ++i) sum[i] = coord_sum(&R, i);
@@ -648,7 +669,7 @@ int oracle_run(const float* pts, uint64_t n, uint32_t d, int normalized, const s
                 n_reps = select_reps_region(&R, n, parts, sizes, P, cfg->rep_q, reps);
             }
         } else if (cfg->rep_selection == SKY_REPS_RANDOM) {
-            n_reps = select_reps_random(&R, parts, sizes, P, cfg->rep_q, cfg->seed, reps);
+            n_reps = select_reps_random(&R, parts, sizes, P, cfg->rep_q, cfg->rep_seed, reps);
         } else {
             n_reps = select_reps_sorted(&R, sum, parts, sizes, P, cfg->rep_q, reps);
         }

@@ -35,6 +35,9 @@ typedef struct oracle_result {
  * Returns a sky_status code. */
 int oracle_run(const float* pts, uint64_t n, uint32_t d, int normalized,
                const sky_config* cfg, oracle_result* out);
+/* the same on FP64 rows (the reference's own coordinate type) */
+int oracle_run_f64(const double* pts, uint64_t n, uint32_t d, int normalized,
+                   const sky_config* cfg, oracle_result* out);
 void oracle_result_free(oracle_result* r);
 
 /* make_assignment (partition.cpp:233-251): partition_of[n], *count. */

@@ -37,13 +37,15 @@ class SkyConfig(C.Structure):
         ("local_algo", C.c_int32),
         ("bnl_window_cap", C.c_uint32),
         ("count_tests", C.c_int32),
+        ("rep_seed", C.c_uint64),
     ]
 
     @classmethod
     def make(cls, strategy=0, p=1, m=0, seed=0, slice_dim=0, filter=0, rep_selection=0,
-             rep_q=5, merge=0, workers=1, local_algo=0, bnl_window_cap=4096, count_tests=1):
+             rep_q=5, merge=0, workers=1, local_algo=0, bnl_window_cap=4096, count_tests=1, rep_seed=None):
+        # rep_seed defaults to the partition seed, as the reference CLI sets both
         return cls(strategy, p, m, seed, slice_dim, filter, rep_selection, rep_q, merge,
-                   workers, local_algo, bnl_window_cap, count_tests)
+                   workers, local_algo, bnl_window_cap, count_tests, seed if rep_seed is None else rep_seed)
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -85,7 +87,7 @@ class SkyResult(C.Structure):
 EXPORTED = [
     "sky_ctx_create", "sky_ctx_destroy", "sky_nccl_unique_id", "sky_ctx_create_dist",
     "sky_last_error", "sky_ctx_set_stream",
-    "sky_config_default", "sky_run", "sky_result_free", "sky_assign",
+    "sky_config_default", "sky_run", "sky_run_f64", "sky_result_free", "sky_assign",
     "sky_snap_slices", "sky_relative_skyline", "sky_skyline",
     "sky_representatives", "sky_free", "sky_generate", "sky_plan_lpt",
     "sky_plan_split", "sky_plan_local_shards", "sky_plan_merge_shards", "sky_abi_version",
@@ -118,6 +120,8 @@ def load():
     lib.sky_ctx_set_stream.argtypes = [vp, vp]
     lib.sky_config_default.argtypes = [C.POINTER(SkyConfig)]
     lib.sky_run.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
+                            C.POINTER(SkyConfig), C.POINTER(SkyResult)]
+    lib.sky_run_f64.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
                             C.POINTER(SkyConfig), C.POINTER(SkyResult)]
     lib.sky_result_free.argtypes = [C.POINTER(SkyResult)]
     lib.sky_assign.argtypes = [vp, _f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), _u64p, _u64p]

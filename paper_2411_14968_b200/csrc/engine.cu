@@ -76,7 +76,7 @@ enum Slot {
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
-    S_SCAN, S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
+    S_SCAN, S_PTS64, S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -130,7 +130,7 @@ void random_partition_of(uint64_t n, uint64_t p, uint64_t seed, uint32_t* pid) {
 
 // hyperspherical_angles + angular_index (partition.cpp:118-148) on the host's
 // libm for boundary points.
-uint64_t angular_index_host(const float* x, uint32_t d, uint64_t m) {
+uint64_t angular_index_host(const double* x, uint32_t d, uint64_t m) {
     std::vector<double> ang(d - 1);
     double tail_sq = (double)x[d - 1] * (double)x[d - 1];
     for (uint32_t i = d - 1; i-- > 0;) {
@@ -430,6 +430,9 @@ class Runner {
         SKY_CUDA(cudaMemcpyAsync(di, hi, plan.items.size() * sizeof(Item), cudaMemcpyHostToDevice, st_));
         SKY_CUDA(cudaMemcpyAsync(dr, hr, plan.ranges.size() * sizeof(uint2), cudaMemcpyHostToDevice, st_));
         RelskyArgs a = base;
+        a.x64 = x64_;
+        if (x64_.x && (!a.sid || (!a.indirect && !a.cid)))
+            throw Error(SKY_E_INTERNAL, "FP64 confirmation needs the row ids of both sets");
         a.items = di;
         a.ranges = dr;
         a.n_items = (uint32_t)plan.items.size();
@@ -440,6 +443,7 @@ class Runner {
             Relsky2Args b{};
             b.cidx = dense;
             b.cxyz = a.cxyz; b.cskey = a.cskey; b.cqc = cq;
+            b.x64 = a.x64; b.cid = a.cid; b.sid = a.sid;
             b.sxyz = a.sxyz; b.sskey = a.sskey; b.sqc = sq;
             b.items = di; b.n_items = a.n_items; b.ranges = dr; b.bounded = a.bounded; b.dead = a.dead;
             b.tests = a.tests; b.counter = misc + M_WORK;
@@ -690,6 +694,7 @@ class Runner {
         RelskyArgs a{};
         a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
         a.sxyz = s0.xyz; a.sskey = s0.skey; a.bounded = true; a.dead = dead;
+        a.cid = s0.id; a.sid = s0.id;
         a.tests = count_tests ? tests(1) : nullptr;
         relsky(D, blocks, a, s0.qc, s0.qc);
         std::vector<uint32_t> off1;
@@ -700,6 +705,7 @@ class Runner {
         launch_fill_u8(dead1, 0, s1.n, st_);
         RelskyArgs b2 = a;
         b2.cxyz = s1.xyz; b2.cskey = s1.skey; b2.sxyz = s1.xyz; b2.sskey = s1.skey; b2.dead = dead1;
+        b2.cid = s1.id; b2.sid = s1.id;
         if (D <= 16 && s1.qc) {
             uint64_t pairs = 0;
             for (uint32_t p = 0; p < P; ++p) pairs += (uint64_t)(off1[p + 1] - off1[p]) * (off1[p + 1] - off1[p]) / 2;
@@ -744,6 +750,8 @@ class Runner {
         b.overflow = ovf;
         b.tests = count_tests ? tests(1) : nullptr;
         b.hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + 1;
+        b.x64 = x64_;
+        b.id = s0.id;
         if (s0.n) {
             dom_begin();
             if (packed)
@@ -758,6 +766,7 @@ class Runner {
 
    public:
     sky_ctx* c_;
+    X64 x64_;  // FP64 input of the current run (null for float input)
     cudaStream_t st_;
 };
 
@@ -864,7 +873,7 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     uint32_t* amb = R.dev<uint32_t>(S_AMB, amb_cap);
     uint32_t* skA = nullptr;
     if (strategy == SKY_SLICED) skA = R.dev<uint32_t>(S_SK_A, n);
-    PrepArgs pa{pts, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA, idxA, skA,
+    PrepArgs pa{pts, R.x64_.x, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA, idxA, skA,
                 misc + M_ERR, misc + M_AMB, amb, amb_cap};
     launch_prep(pa, st);
     R.count();
@@ -890,9 +899,16 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
         uint32_t* hp = ha + na;
         float* hrows = reinterpret_cast<float*>(ha + 2 * (size_t)na);
         (void)hrows;
+        std::vector<double> row64(d);
         for (uint32_t k = 0; k < na; ++k) {
-            SKY_CUDA(cudaMemcpy(row.data(), pts + (size_t)ha[k] * d, d * sizeof(float), cudaMemcpyDeviceToHost));
-            hp[k] = (uint32_t)angular_index_host(row.data(), d, m);
+            if (R.x64_.x) {
+                SKY_CUDA(cudaMemcpy(row64.data(), R.x64_.x + (size_t)ha[k] * d, d * sizeof(double),
+                                    cudaMemcpyDeviceToHost));
+            } else {
+                SKY_CUDA(cudaMemcpy(row.data(), pts + (size_t)ha[k] * d, d * sizeof(float), cudaMemcpyDeviceToHost));
+                for (uint32_t j = 0; j < d; ++j) row64[j] = row[j];
+            }
+            hp[k] = (uint32_t)angular_index_host(row64.data(), d, m);
         }
         uint32_t* dp = amb + na;  // reuse tail of the amb buffer for pids (cap >= 2*na checked below)
         if (2 * (size_t)na > amb_cap) dp = R.dev<uint32_t>(S_RUNS, na);
@@ -930,7 +946,7 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
                 max_len = std::max<uint32_t>(max_len, (uint32_t)L);
             }
         }
-        if (cost <= (uint64_t)1e9 && !scan_rows) {
+        if (cost <= (uint64_t)1e9 && !scan_rows && !R.x64_.x) {
             launch_slice_assign(rankA, n, P, keyA, st);
             R.count();
             launch_slice_fix_runs(pts, d, rankA, n, P, runs, nruns, max_len, keyA, st);
@@ -940,11 +956,20 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
             uint32_t* cur = rankB;
             uint32_t* other = rankA;
             SKY_CUDA(cudaMemcpyAsync(cur, idxA, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+            uint64_t* k64a = R.x64_.x ? R.dev<uint64_t>(S_RK0, n) : nullptr;
+            uint64_t* k64b = R.x64_.x ? R.dev<uint64_t>(S_RK1, n) : nullptr;
             for (int j = (int)d - 1; j >= -1; --j) {
                 const uint32_t col = j < 0 ? (uint32_t)cfg->slice_dim : (uint32_t)j;
-                launch_gather_coord_key(pts, d, col, cur, n, skA, st);
-                R.count();
-                R.sort_pairs(skA, skB, cur, other, n, 0, 32);
+                if (R.x64_.x) {
+                    // FP64 input: canonical double bits, 64-bit LSD passes
+                    launch_gather_coord_key64(R.x64_.x, d, col, cur, n, k64a, st);
+                    R.count();
+                    R.sort_pairs(k64a, k64b, cur, other, n, 0, 64);
+                } else {
+                    launch_gather_coord_key(pts, d, col, cur, n, skA, st);
+                    R.count();
+                    R.sort_pairs(skA, skB, cur, other, n, 0, 32);
+                }
                 std::swap(cur, other);
             }
             launch_slice_assign(cur, n, P, keyA, st);
@@ -986,7 +1011,7 @@ DevSet host_reps(Runner& R, sky_ctx* c, int D, const uint32_t* cand, uint32_t sl
     std::memcpy(hc, rows.data(), nc * sizeof(uint32_t));
     SKY_CUDA(cudaMemcpyAsync(drows, hc, nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     DevSet cs = R.set(S_SET3, nc, D);
-    launch_gather_rows(D, pts, d, drows, nc, cs, nullptr, st);
+    launch_gather_rows(D, pts, R.x64_.x, d, drows, nc, cs, st);
     R.count();
     DevSet css = R.set(S_SET1, nc, D);
     {
@@ -1002,13 +1027,15 @@ DevSet host_reps(Runner& R, sky_ctx* c, int D, const uint32_t* cand, uint32_t sl
     }
     uint8_t* cdead = R.dev<uint8_t>(S_CELLDEAD, nc);
     launch_fill_u8(cdead, 0, nc, st);
-    if (launch_small_skyline(D, css.xyz, nc, cdead, count_tests ? R.tests(0) : nullptr, c->smem_optin, st)) {
+    if (launch_small_skyline(D, css.xyz, css.id, nc, cdead, count_tests ? R.tests(0) : nullptr, R.x64_,
+                             c->smem_optin, st)) {
         R.count();
     } else {
         Plan pp;
         for (uint32_t b = 0; b < nc; b += kTile) pp.add(b, std::min(nc, b + (uint32_t)kTile), {make_uint2(0, nc)});
         RelskyArgs ra{};
         ra.cxyz = css.xyz; ra.cskey = css.skey; ra.sxyz = css.xyz; ra.sskey = css.skey;
+        ra.cid = css.id; ra.sid = css.id;
         ra.bounded = true; ra.dead = cdead; ra.tests = count_tests ? R.tests(0) : nullptr;
         R.relsky(D, pp, ra);
     }
@@ -1034,7 +1061,7 @@ void region_candidates(Runner& R, const float* pts, uint32_t d, uint32_t n, cons
     uint32_t* p0 = R.dev<uint32_t>(S_RP0, n);
     uint32_t* p1 = R.dev<uint32_t>(S_RP1, n);
     uint32_t* pid_row = R.dev<uint32_t>(S_ROWPID, n);
-    launch_region_keys(pts, d, n, k0, v0, st);
+    launch_region_keys(pts, R.x64_.x, d, n, k0, v0, st);
     launch_row_pid(po.key64, po.idx, n, pid_row, st);
     R.count(2);
     R.sort_pairs(k0, k1, v0, v1, n, 0, 64);
@@ -1103,8 +1130,8 @@ void random_candidates(Runner& R, uint32_t n, const PartitionOut& po, uint32_t P
     R.count();
 }
 
-void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int normalized, int on_device,
-              const sky_config* cfg, sky_result* out, bool eager = false) {
+void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int normalized, int on_device,
+              const sky_config* cfg, sky_result* out, bool eager = false, bool f64 = false) {
     std::memset(out, 0, sizeof(*out));
     validate(n64, d, cfg);
     uint64_t P64 = 0, m = 0;
@@ -1145,8 +1172,23 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     SKY_CUDA(cudaEventRecord(c->ev[0], st));
     uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
     SKY_CUDA(cudaMemsetAsync(misc, 0, 64 * sizeof(uint32_t), st));
-    const float* pts = points;
-    if (!on_device) {
+    const float* pts = static_cast<const float*>(points);
+    if (f64) {
+        // FP64 rows: keep the doubles for exact decisions, run the layout,
+        // keys, codes and coarse tests on their float32 image
+        const double* p64 = static_cast<const double*>(points);
+        if (!on_device) {
+            double* dp64 = R.dev<double>(S_PTS64, (size_t)n * d);
+            SKY_CUDA(cudaMemcpyAsync(dp64, points, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, st));
+            p64 = dp64;
+            out->h2d_bytes += (uint64_t)n * d * sizeof(double);
+        }
+        float* dp = R.dev<float>(S_PTS, (size_t)n * d);
+        launch_round_rows(p64, (size_t)n * d, dp, st);
+        R.count();
+        pts = dp;
+        R.x64_ = X64{p64, d};
+    } else if (!on_device) {
         float* dp = R.dev<float>(S_PTS, (size_t)n * d);
         SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, st));
         pts = dp;
@@ -1203,15 +1245,16 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
             if (!normalized) throw Error(SKY_E_NORMALIZATION, "region selection requires a normalized dataset");
             region_candidates(R, pts, d, n, po, P, q, cand);
         } else if (cfg->rep_selection == SKY_REPS_RANDOM) {
-            random_candidates(R, n, po, P, q, cfg->strategy == SKY_SLICED ? scan_rows : nullptr, cfg->seed, cand);
+            random_candidates(R, n, po, P, q, cfg->strategy == SKY_SLICED ? scan_rows : nullptr, cfg->rep_seed,
+                              cand);
         } else {
-            launch_rep_pick(po.key64, po.idx, po.off, P, pts, d, q, cand, st);
+            launch_rep_pick(po.key64, po.idx, po.off, P, pts, R.x64_.x, d, q, cand, st);
             R.count();
         }
         const uint32_t slots = P * q;
         DevSet reps = R.set(S_SET3, slots, D);  // reps.n: upper bound until the count is read back
         uint32_t* nrep_dev = misc + M_NREP;
-        if (launch_rep_finalize(D, cand, slots, pts, d, reps, nrep_dev, count_tests ? R.tests(0) : nullptr,
+        if (launch_rep_finalize(D, cand, slots, pts, d, reps, nrep_dev, count_tests ? R.tests(0) : nullptr, R.x64_,
                                 c->smem_optin, st)) {
             // compact + sort + prune in one CTA; the count stays on the device
             R.count();
@@ -1231,9 +1274,9 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
             R.count(2);
         }
         uint8_t* dead_row = R.dev<uint8_t>(S_DEADROW, n);
-        if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.n,
-                                           nrep_dev, pthr, dead_row, dead, count_tests ? R.tests(1) : nullptr,
-                                           c->smem_optin, st)) {
+        if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,
+                                           reps.id, reps.n, nrep_dev, pthr, dead_row, dead,
+                                           count_tests ? R.tests(1) : nullptr, R.x64_, c->smem_optin, st)) {
             R.count();
             any_dead = true;
         } else if (reps.n > 0) {
@@ -1246,6 +1289,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
             for (uint32_t b = 0; b < n; b += kTile) pf.add(b, std::min(n, b + (uint32_t)kTile), {make_uint2(0, reps.n)});
             RelskyArgs fa{};
             fa.cxyz = pts; fa.cskey = reinterpret_cast<const uint32_t*>(po.key64); fa.cidx = po.idx; fa.cd = d;
+            fa.sid = reps.id;
             fa.indirect = true; fa.sxyz = reps.xyz; fa.sskey = reps.skey; fa.bounded = true; fa.dead = dead;
             fa.tests = count_tests ? R.tests(1) : nullptr;
             R.relsky(D, pf, fa);
@@ -1337,6 +1381,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
     launch_fill_u8(fdead, 0, U.n, st);
     RelskyArgs ma{};
     ma.cxyz = U.xyz; ma.cskey = U.skey; ma.bounded = true; ma.dead = fdead;
+    ma.cid = U.id; ma.sid = U.id;
     ma.tests = count_tests ? R.tests(2) : nullptr;
     Plan mp;
     const bool all_mode = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
@@ -1381,7 +1426,7 @@ void run_impl(sky_ctx* c, const float* points, uint64_t n64, uint32_t d, int nor
         R.sort_pairs(U.skey, sk2, iota, perm, U.n, 0, 32);
         launch_gather_set(D, U, perm, US, st);
         R.count();
-        ma.sxyz = US.xyz; ma.sskey = US.skey;
+        ma.sxyz = US.xyz; ma.sskey = US.skey; ma.sid = US.id;
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
     }
@@ -1510,6 +1555,7 @@ void sky_config_default(sky_config* cfg) {
     cfg->local_algo = SKY_LOCAL_SFS;
     cfg->bnl_window_cap = 4096;
     cfg->count_tests = 1;
+    cfg->rep_seed = 0;
 }
 
 int sky_ctx_create(int device, sky_ctx** out) {
@@ -1586,21 +1632,31 @@ int sky_ctx_set_stream(sky_ctx* c, void* stream) {
     return SKY_OK;
 }
 
-int sky_run(sky_ctx* c, const float* points, uint64_t n, uint32_t d, int normalized, int on_device,
-            const sky_config* cfg, sky_result* out) {
+static int run_guarded(sky_ctx* c, const void* points, uint64_t n, uint32_t d, int normalized, int on_device,
+                       const sky_config* cfg, sky_result* out, bool f64) {
     return guarded(c, [&] {
         try {
             try {
-                run_impl(c, points, n, d, normalized, on_device, cfg, out);
+                run_impl(c, points, n, d, normalized, on_device, cfg, out, false, f64);
             } catch (const RedoEager&) {
                 sky_result_free(out);
-                run_impl(c, points, n, d, normalized, on_device, cfg, out, true);
+                run_impl(c, points, n, d, normalized, on_device, cfg, out, true, f64);
             }
         } catch (...) {
             sky_result_free(out);
             throw;
         }
     });
+}
+
+int sky_run(sky_ctx* c, const float* points, uint64_t n, uint32_t d, int normalized, int on_device,
+            const sky_config* cfg, sky_result* out) {
+    return run_guarded(c, points, n, d, normalized, on_device, cfg, out, false);
+}
+
+int sky_run_f64(sky_ctx* c, const double* points, uint64_t n, uint32_t d, int normalized, int on_device,
+                const sky_config* cfg, sky_result* out) {
+    return run_guarded(c, points, n, d, normalized, on_device, cfg, out, true);
 }
 
 void sky_result_free(sky_result* r) {
@@ -1659,7 +1715,7 @@ int sky_relative_skyline(sky_ctx* c, const float* r, uint64_t nr64, const float*
         SKY_CUDA(cudaMemsetAsync(misc, 0, 64 * sizeof(uint32_t), st));
         uint64_t* key = R.dev<uint64_t>(S_KEY_A, nr + nc);
         uint32_t* idx = R.dev<uint32_t>(S_IDX_A, nr + nc);
-        PrepArgs pa{dp, nr + nc, d, SKY_SLICED + 100, 0, 0, nullptr, 0, key, idx, nullptr, misc + M_ERR,
+        PrepArgs pa{dp, nullptr, nr + nc, d, SKY_SLICED + 100, 0, 0, nullptr, 0, key, idx, nullptr, misc + M_ERR,
                     misc + M_AMB, nullptr, 0};
         launch_prep(pa, st);
         // comparators sorted by sum key
@@ -1679,6 +1735,7 @@ int sky_relative_skyline(sky_ctx* c, const float* r, uint64_t nr64, const float*
         pl.order();
         RelskyArgs a{};
         a.cxyz = T.xyz; a.cskey = T.skey; a.sxyz = S.xyz; a.sskey = S.skey; a.dead = dead;
+        a.cid = T.id; a.sid = S.id;
         a.tests = R.tests(0);
         // candidates are in input order, so the key bound is per warp (still
         // sound on any order: a dominator never has a larger key)
@@ -1747,7 +1804,7 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
         PartitionOut po = partition_phase(R, dp, n, d, 0, SKY_RANDOM, p, 0, &cfg, pd, &fix);
         const uint32_t qq = (uint32_t)std::min<uint64_t>(q, n);
         uint32_t* cand = R.dev<uint32_t>(S_REPCAND, (size_t)p * qq);
-        launch_rep_pick(po.key64, po.idx, po.off, (uint32_t)p, dp, d, qq, cand, st);
+        launch_rep_pick(po.key64, po.idx, po.off, (uint32_t)p, dp, nullptr, d, qq, cand, st);
         std::vector<uint32_t> hc((size_t)p * qq);
         SKY_CUDA(cudaMemcpyAsync(hc.data(), cand, hc.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         R.sync();

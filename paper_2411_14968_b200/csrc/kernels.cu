@@ -59,38 +59,41 @@ __device__ __forceinline__ uint32_t canon_bits(float v) {
 __global__ void k_prep(PrepArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
-    const float* x = a.pts + (size_t)i * a.d;
+    const float* xf = a.pts + (size_t)i * a.d;
+    const double* xd = a.pts64 ? a.pts64 + (size_t)i * a.d : nullptr;
+    // every value as the reference sees it (float input upcasts exactly)
+    auto X = [&](uint32_t j) -> double { return xd ? xd[j] : (double)xf[j]; };
     double sum = 0.0;
     uint32_t err = 0;
     uint64_t pid = 0;
     if (a.strategy == SKY_GRID) {
         uint64_t stride = 1;
         for (uint32_t j = 0; j < a.d; ++j) {
-            const float v = x[j];
-            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
-            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
-            if (!(v >= 0.0f && v <= 1.0f)) err |= kErrGridRange;
-            sum = __dadd_rn(sum, (double)v);
-            uint64_t cell = (uint64_t)__dmul_rn((double)v, (double)a.m);
+            const double v = X(j);
+            if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0) err |= kErrAboveOne;
+            if (!(v >= 0.0 && v <= 1.0)) err |= kErrGridRange;
+            sum = __dadd_rn(sum, v);
+            uint64_t cell = (uint64_t)__dmul_rn(v, (double)a.m);
             if (cell >= a.m) cell = a.m - 1;
             pid += cell * stride;
             stride *= a.m;
         }
     } else if (a.strategy == SKY_ANGULAR) {
         for (uint32_t j = 0; j < a.d; ++j) {
-            const float v = x[j];
-            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
-            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
-            sum = __dadd_rn(sum, (double)v);
+            const double v = X(j);
+            if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0) err |= kErrAboveOne;
+            sum = __dadd_rn(sum, v);
         }
         // hyperspherical_angles: tail sums of squares back to front.
         const double PI = 3.14159265358979323846;
-        double tail = __dmul_rn((double)x[a.d - 1], (double)x[a.d - 1]);
+        double tail = __dmul_rn(X(a.d - 1), X(a.d - 1));
         uint64_t stride_i = 1;
         for (uint32_t k = 0; k + 1 < a.d; ++k) stride_i *= a.m;  // m^(d-2) for i = d-2
         bool ambiguous = false;
         for (uint32_t ii = a.d - 1; ii-- > 0;) {
-            const double xi = (double)x[ii];
+            const double xi = X(ii);
             const double phi = atan2(sqrt(tail), xi);
             tail = __dadd_rn(tail, __dmul_rn(xi, xi));
             const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
@@ -110,13 +113,13 @@ __global__ void k_prep(PrepArgs a) {
         }
     } else {
         for (uint32_t j = 0; j < a.d; ++j) {
-            const float v = x[j];
-            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
-            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
-            sum = __dadd_rn(sum, (double)v);
+            const double v = X(j);
+            if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0) err |= kErrAboveOne;
+            sum = __dadd_rn(sum, v);
         }
         if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
-        if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(x[a.slice_dim]);
+        if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(xf[a.slice_dim]);
     }
     if (err) {
         atomicOr(a.err, err);
@@ -238,11 +241,12 @@ void launch_slice_assign(const uint32_t* rank_idx, uint32_t n, uint64_t p, uint6
 
 // coords_then_id_less (core.cpp:10-17) on float rows (exact: float order ==
 // double order of the upcast values).
-__device__ __forceinline__ bool lex_less(const float* pts, uint32_t d, uint32_t a, uint32_t b) {
-    const float* pa = pts + (size_t)a * d;
-    const float* pb = pts + (size_t)b * d;
+template <class T>
+__device__ __forceinline__ bool lex_less(const T* pts, uint32_t d, uint32_t a, uint32_t b) {
+    const T* pa = pts + (size_t)a * d;
+    const T* pb = pts + (size_t)b * d;
     for (uint32_t j = 0; j < d; ++j) {
-        const float x = pa[j], y = pb[j];
+        const T x = pa[j], y = pb[j];
         if (x < y) return true;
         if (x > y) return false;
     }
@@ -285,16 +289,45 @@ void launch_gather_coord_key(const float* pts, uint32_t d, uint32_t j, const uin
     SKY_LAUNCH_CHECK();
 }
 
+// canonical FP64 bits: monotone for values >= 0 (-0.0 folded into +0.0)
+__global__ void k_gather_coord_key64(const double* __restrict__ pts, uint32_t d, uint32_t j,
+                                     const uint32_t* __restrict__ idx, uint32_t n, uint64_t* key) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = pts[(size_t)idx[i] * d + j];
+    key[i] = v == 0.0 ? 0ull : (uint64_t)__double_as_longlong(v);
+}
+
+void launch_gather_coord_key64(const double* pts, uint32_t d, uint32_t j, const uint32_t* idx, uint32_t n,
+                               uint64_t* key, cudaStream_t st) {
+    if (!n) return;
+    k_gather_coord_key64<<<ceil_div(n, 256), 256, 0, st>>>(pts, d, j, idx, n, key);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_round_rows(const double* __restrict__ in, size_t count, float* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = __double2float_rn(in[i]);
+}
+
+void launch_round_rows(const double* in, size_t count, float* out, cudaStream_t st) {
+    if (!count) return;
+    k_round_rows<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(in, count, out);
+    SKY_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------- representatives
-__device__ double row_sum(const float* pts, uint32_t d, uint32_t r) {
-    const float* x = pts + (size_t)r * d;
+template <class T>
+__device__ double row_sum(const T* pts, uint32_t d, uint32_t r) {
+    const T* x = pts + (size_t)r * d;
     double s = 0.0;
     for (uint32_t j = 0; j < d; ++j) s = __dadd_rn(s, (double)x[j]);
     return s;
 }
 
 // (coord_sum, coords_then_id_less) total order of filter.cpp:74-79.
-__device__ bool rep_less(const float* pts, uint32_t d, uint32_t a, uint32_t b) {
+template <class T>
+__device__ bool rep_less(const T* pts, uint32_t d, uint32_t a, uint32_t b) {
     const double sa = row_sum(pts, d, a), sb = row_sum(pts, d, b);
     if (sa != sb) return sa < sb;
     return lex_less(pts, d, a, b);
@@ -303,8 +336,9 @@ __device__ bool rep_less(const float* pts, uint32_t d, uint32_t a, uint32_t b) {
 // One CTA per partition. Rows are sorted by (pid, skey, row); skey ties can
 // hide (sum, lex, id) order, so the tie run that straddles position q-1 is
 // resolved exactly by repeated block-wide argmin.
+template <class T>
 __global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* __restrict__ idx,
-                           const uint32_t* __restrict__ off, const float* __restrict__ pts, uint32_t d,
+                           const uint32_t* __restrict__ off, const T* __restrict__ pts, uint32_t d,
                            uint32_t q, uint32_t* cand) {
     const uint32_t p = blockIdx.x;
     const uint32_t a = off[p], b = off[p + 1];
@@ -371,9 +405,12 @@ __global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* _
 }
 
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
-                     const float* pts, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st) {
+                     const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st) {
     if (!P) return;
-    k_rep_pick<<<P, 128, 0, st>>>(key64, idx, off, pts, d, q, cand);
+    if (pts64)
+        k_rep_pick<double><<<P, 128, 0, st>>>(key64, idx, off, pts64, d, q, cand);
+    else
+        k_rep_pick<float><<<P, 128, 0, st>>>(key64, idx, off, pts, d, q, cand);
     SKY_LAUNCH_CHECK();
 }
 
@@ -389,11 +426,12 @@ __global__ void k_row_pid(const uint64_t* __restrict__ key64, const uint32_t* __
 // to right, each step correctly rounded as on the host. Key = ~bits(volume)
 // (volumes are >= +0, so the bit pattern is monotone): an ascending stable
 // sort over rows in id order gives (volume desc, id asc) (filter.cpp:103-106).
-__global__ void k_region_keys(const float* __restrict__ pts, uint32_t d, uint32_t n, uint64_t* __restrict__ key,
+template <class T>
+__global__ void k_region_keys(const T* __restrict__ pts, uint32_t d, uint32_t n, uint64_t* __restrict__ key,
                               uint32_t* __restrict__ row) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float* x = pts + (size_t)i * d;
+    const T* x = pts + (size_t)i * d;
     double v = 1.0;
     for (uint32_t j = 0; j < d; ++j) v = __dmul_rn(v, __dsub_rn(1.0, (double)x[j]));
     key[i] = ~(uint64_t)__double_as_longlong(v);
@@ -433,9 +471,13 @@ void launch_row_pid(const uint64_t* key64, const uint32_t* idx, uint32_t n, uint
     k_row_pid<<<ceil_div(n, 256), 256, 0, st>>>(key64, idx, n, pid_row);
     SKY_LAUNCH_CHECK();
 }
-void launch_region_keys(const float* pts, uint32_t d, uint32_t n, uint64_t* key, uint32_t* row, cudaStream_t st) {
+void launch_region_keys(const float* pts, const double* pts64, uint32_t d, uint32_t n, uint64_t* key, uint32_t* row,
+                        cudaStream_t st) {
     if (!n) return;
-    k_region_keys<<<ceil_div(n, 256), 256, 0, st>>>(pts, d, n, key, row);
+    if (pts64)
+        k_region_keys<double><<<ceil_div(n, 256), 256, 0, st>>>(pts64, d, n, key, row);
+    else
+        k_region_keys<float><<<ceil_div(n, 256), 256, 0, st>>>(pts, d, n, key, row);
     SKY_LAUNCH_CHECK();
 }
 void launch_iota(uint32_t n, uint32_t* out, cudaStream_t st) {
@@ -470,7 +512,8 @@ constexpr int REPF_THREADS = 1024, REPF_ITEMS = 2, REPF_MAX = REPF_THREADS * REP
 template <int D>
 __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* __restrict__ cand, uint32_t slots,
                                                                const float* __restrict__ pts, uint32_t d, DevSet out,
-                                                               uint32_t* out_count, unsigned long long* tests) {
+                                                               uint32_t* out_count, unsigned long long* tests,
+                                                               X64 x64) {
     constexpr int V = Dims<D>::V;
     using Scan = cub::BlockScan<uint32_t, REPF_THREADS>;
     using Sort = cub::BlockRadixSort<uint32_t, REPF_THREADS, REPF_ITEMS, uint32_t>;
@@ -505,7 +548,6 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
     for (uint32_t i = t; i < n; i += REPF_THREADS) {
         const float* x = pts + (size_t)s_row[i] * d;
         float4* dst = s_xyz + (size_t)i * V;
-        double sum = 0.0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             float c[4];
@@ -513,10 +555,10 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
             for (int q = 0; q < 4; ++q) {
                 const uint32_t j = 4 * v + q;
                 c[q] = j < d ? x[j] : 0.0f;
-                if (j < d) sum = __dadd_rn(sum, (double)c[q]);
             }
             dst[v] = make_float4(c[0], c[1], c[2], c[3]);
         }
+        const double sum = x64.x ? row_sum(x64.x, d, s_row[i]) : row_sum(pts, d, s_row[i]);
         s_key[i] = __float_as_uint(__double2float_rn(sum));
     }
     __syncthreads();
@@ -549,7 +591,7 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
                 gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
                 lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
             }
-            dom = !gt && lt;
+            dom = !gt && (x64.x ? dom64(x64, s_row[j], s_row[i]) : lt);
         }
         s_dead[i] = dom;
     }
@@ -580,13 +622,13 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
 }
 
 bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
-                         uint32_t* out_count, unsigned long long* tests, int smem_optin, cudaStream_t st) {
+                         uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {
     if (slots > (uint32_t)REPF_MAX) return false;
     const size_t smem = (size_t)REPF_MAX * ((D + 3) / 4) * 16 + (size_t)REPF_MAX * 13 + 64;
     if (smem + 48 * 1024 > (size_t)smem_optin) return false;
     SKY_DISPATCH_D(D, {
         SKY_CUDA(cudaFuncSetAttribute(k_rep_finalize<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_rep_finalize<DT><<<1, REPF_THREADS, smem, st>>>(cand, slots, pts, d, out, out_count, tests);
+        k_rep_finalize<DT><<<1, REPF_THREADS, smem, st>>>(cand, slots, pts, d, out, out_count, tests, x64);
     });
     SKY_LAUNCH_CHECK();
     return true;
@@ -645,30 +687,25 @@ void launch_scatter_indirect(int D, const float* pts, uint32_t d, const uint32_t
 // Rows of the input -> DevSet (reps, small sets). skey recomputed when
 // skey_src is null.
 template <int D>
-__global__ void k_gather_rows(const float* __restrict__ pts, uint32_t d, const uint32_t* __restrict__ rows,
-                              uint32_t n, DevSet out) {
+__global__ void k_gather_rows(const float* __restrict__ pts, const double* __restrict__ pts64, uint32_t d,
+                              const uint32_t* __restrict__ rows, uint32_t n, DevSet out) {
     constexpr int D4 = Dims<D>::D4;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t row = rows[i];
     const float* x = pts + (size_t)row * d;
     float* dst = out.xyz + (size_t)i * D4;
-    double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < D4; ++j) {
-        const float v = (uint32_t)j < d ? x[j] : 0.0f;
-        dst[j] = v;
-        if ((uint32_t)j < d) s = __dadd_rn(s, (double)v);
-    }
+    for (int j = 0; j < D4; ++j) dst[j] = (uint32_t)j < d ? x[j] : 0.0f;
+    const double s = pts64 ? row_sum(pts64, d, row) : row_sum(pts, d, row);  // same key as k_prep
     out.skey[i] = __float_as_uint(__double2float_rn(s));
     out.id[i] = row;
 }
 
-void launch_gather_rows(int D, const float* pts, uint32_t d, const uint32_t* rows, uint32_t n, DevSet out,
-                        const uint32_t* skey_src, cudaStream_t st) {
-    (void)skey_src;
+void launch_gather_rows(int D, const float* pts, const double* pts64, uint32_t d, const uint32_t* rows, uint32_t n,
+                        DevSet out, cudaStream_t st) {
     if (!n) return;
-    SKY_DISPATCH_D(D, (k_gather_rows<DT><<<ceil_div(n, 256), 256, 0, st>>>(pts, d, rows, n, out)));
+    SKY_DISPATCH_D(D, (k_gather_rows<DT><<<ceil_div(n, 256), 256, 0, st>>>(pts, pts64, d, rows, n, out)));
     SKY_LAUNCH_CHECK();
 }
 
@@ -782,6 +819,15 @@ __device__ __forceinline__ bool dominates_f(const float (&s)[D], const float (&t
     return lt;
 }
 
+// s <= t everywhere on the float image (necessary for FP64 dominance).
+template <int D>
+__device__ __forceinline__ bool le_all_f(const float (&s)[D], const float (&t)[D]) {
+    bool gt = false;
+#pragma unroll
+    for (int j = 0; j < D; ++j) gt |= s[j] > t[j];
+    return !gt;
+}
+
 template <int D, bool INDIRECT>
 __global__ void __launch_bounds__(RS_THREADS) k_relsky(RelskyArgs a) {
     constexpr int V = Dims<D>::V;
@@ -881,7 +927,12 @@ __global__ void __launch_bounds__(RS_THREADS) k_relsky(RelskyArgs a) {
                     }
 #pragma unroll
                     for (int k = 0; k < RS_K; ++k) {
-                        if (alive[k] && dominates_f<D>(s, t[k])) {
+                        const bool dom =
+                            a.x64.x ? le_all_f<D>(s, t[k]) &&
+                                          dom64(a.x64, a.sid[base + i],
+                                                INDIRECT ? a.cidx[pos0 + k] : a.cid[pos0 + k])
+                                    : dominates_f<D>(s, t[k]);
+                        if (alive[k] && dom) {
                             alive[k] = false;
                             ntests += i + 1;
                         }
@@ -1023,8 +1074,16 @@ __global__ void __launch_bounds__(BNL_B) k_bnl(BnlArgs a, uint32_t cap, uint32_t
                                 lt |= s[j] < t[j];
                             }
                             ntests += 2;  // both directions
-                            if (!gt && lt) alive = false;              // window dominates t
-                            else if (gt && !lt) w_kill[w] = 1;          // t dominates window tuple
+                            if (a.x64.x) {
+                                // float image equal or one-sided: confirm on the doubles
+                                const uint32_t rw = a.id[win_pos[w]], rt = a.id[mypos];
+                                if (!gt && dom64(a.x64, rw, rt)) alive = false;
+                                else if (!lt && dom64(a.x64, rt, rw)) w_kill[w] = 1;
+                            } else if (!gt && lt) {
+                                alive = false;                          // window dominates t
+                            } else if (gt && !lt) {
+                                w_kill[w] = 1;                          // t dominates window tuple
+                            }
                         }
                     }
                 }
@@ -1042,7 +1101,13 @@ __global__ void __launch_bounds__(BNL_B) k_bnl(BnlArgs a, uint32_t cap, uint32_t
                         if (4 * v + 3 < D) s[4 * v + 3] = q.w;
                     }
                     ++ntests;
-                    if (dominates_f<D>(s, t)) alive = false;
+                    if (a.x64.x) {
+                        if (le_all_f<D>(s, t) &&
+                            dom64(a.x64, a.id[first ? seg_b + k0 + b : ovf[k0 + b]], a.id[mypos]))
+                            alive = false;
+                    } else if (dominates_f<D>(s, t)) {
+                        alive = false;
+                    }
                 }
                 __syncthreads();
                 // remove killed (1) and confirmed (2) window tuples; compact

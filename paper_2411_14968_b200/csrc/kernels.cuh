@@ -20,8 +20,32 @@ struct DevSet {
     uint32_t n = 0;
 };
 
+// FP64 input (sky_run_f64): the engine keeps a float32 image of the rows for
+// its layout, keys, codes and coarse tests (round-to-nearest is monotone, so
+// s <= t implies rn(s) <= rn(t)), and confirms every dominance that survives
+// the float test on the original doubles of the two rows.
+struct X64 {
+    const double* x = nullptr;  // row-major n x d input, or null (float input)
+    uint32_t d = 0;
+};
+#ifdef __CUDACC__
+// dominates_raw (core.hpp:89-96) on the original FP64 rows rs, rt.
+__device__ __forceinline__ bool dom64(const X64& e, uint32_t rs, uint32_t rt) {
+    const double* s = e.x + (size_t)rs * e.d;
+    const double* t = e.x + (size_t)rt * e.d;
+    bool lt = false;
+    for (uint32_t j = 0; j < e.d; ++j) {
+        const double a = s[j], b = t[j];
+        if (a > b) return false;
+        lt |= a < b;
+    }
+    return lt;
+}
+#endif
+
 struct PrepArgs {
     const float* pts;
+    const double* pts64;     // FP64 input (validation, sums and partition ids from the doubles)
     uint32_t n, d;
     int strategy;
     uint64_t m;
@@ -57,31 +81,36 @@ void launch_slice_fix_runs(const float* pts, uint32_t d, const uint32_t* rank_id
                            cudaStream_t st);
 void launch_gather_coord_key(const float* pts, uint32_t d, uint32_t j, const uint32_t* idx, uint32_t n,
                              uint32_t* key, cudaStream_t st);
+void launch_gather_coord_key64(const double* pts, uint32_t d, uint32_t j, const uint32_t* idx, uint32_t n,
+                               uint64_t* key, cudaStream_t st);
+// float32 image (round to nearest) of FP64 rows
+void launch_round_rows(const double* in, size_t count, float* out, cudaStream_t st);
 
 // Exact top-q per partition under (FP64 sum, lex coords, id) (filter.cpp:66-86).
 // region / random representatives (filter.cpp:88-137)
 void launch_row_pid(const uint64_t* key64, const uint32_t* idx, uint32_t n, uint32_t* pid_row, cudaStream_t st);
-void launch_region_keys(const float* pts, uint32_t d, uint32_t n, uint64_t* key, uint32_t* row, cudaStream_t st);
+void launch_region_keys(const float* pts, const double* pts64, uint32_t d, uint32_t n, uint64_t* key, uint32_t* row,
+                        cudaStream_t st);
 void launch_iota(uint32_t n, uint32_t* out, cudaStream_t st);
 void launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t n, uint32_t* out, cudaStream_t st);
 void launch_pick_first(const uint32_t* rows, const uint32_t* off, uint32_t P, uint32_t q, uint32_t* cand,
                        cudaStream_t st);
 void launch_pick_gather(const uint32_t* rows, const uint32_t* gpos, uint32_t slots, uint32_t* cand, cudaStream_t st);
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
-                     const float* pts, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st);
+                     const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st);
 
 // Representative finish on the device (<= 2048 picks): key-sorted antichain
 // into `out`, count in *out_count. false: too many picks (host path).
 bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
-                         uint32_t* out_count, unsigned long long* tests, int smem_optin, cudaStream_t st);
+                         uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st);
 
 // Compaction plumbing.
 void launch_scatter_direct(int D, const DevSet& in, const uint8_t* dead, const uint32_t* pos, DevSet out,
                            cudaStream_t st);
 void launch_scatter_indirect(int D, const float* pts, uint32_t d, const uint32_t* idx, const uint64_t* key64,
                              uint32_t n, const uint8_t* dead, const uint32_t* pos, DevSet out, cudaStream_t st);
-void launch_gather_rows(int D, const float* pts, uint32_t d, const uint32_t* rows, uint32_t n, DevSet out,
-                        const uint32_t* skey_src, cudaStream_t st);
+void launch_gather_rows(int D, const float* pts, const double* pts64, uint32_t d, const uint32_t* rows, uint32_t n,
+                        DevSet out, cudaStream_t st);
 void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st);
 void launch_remap_offsets(const uint32_t* off_old, uint32_t P, const uint32_t* pos, const uint8_t* dead,
                           uint32_t n, uint32_t* off_new, cudaStream_t st);
@@ -113,6 +142,9 @@ struct RelskyArgs {
     bool bounded;
     uint8_t* dead;
     unsigned long long* tests;
+    X64 x64;                 // FP64 confirmation (rows: cid / cidx, sid)
+    const uint32_t* cid;     // direct candidates: row id of each position
+    const uint32_t* sid;     // row id of each comparator position
 };
 void launch_relsky(int D, const RelskyArgs& a, cudaStream_t st);
 
@@ -142,6 +174,9 @@ struct Relsky2Args {
     uint32_t* counter;   // zeroed work counter (persistent warps fetch items)
     const uint32_t* wcount;  // window lengths for dynamic ranges (y has bit 31 set)
     unsigned long long* coarse_hits;  // optional: exact checks performed
+    X64 x64;                  // FP64 confirmation
+    const uint32_t* cid;      // row id of each candidate position
+    const uint32_t* sid;      // row id of each comparator position
 };
 // tile = candidates per item (<= 32 * 8, one warp); picks K from it.
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);
@@ -157,6 +192,8 @@ struct BnlArgs {
     uint32_t* overflow;       // scratch: n entries
     unsigned long long* tests;
     unsigned long long* hits;  // optional: exact checks performed
+    X64 x64;                   // FP64 confirmation
+    const uint32_t* id;        // row id of each set position
 };
 // Largest window <= want whose shared-memory footprint fits smem_optin.
 uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin);
@@ -173,14 +210,14 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey,
 // positions (dead_pos[i] |= dead_row[idx[i]]).
 // nrep: host upper bound (shared-memory sizing); nrep_dev: optional device count.
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
-                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const uint32_t* nrep_dev,
-                      const float* thr, uint8_t* dead_row, uint8_t* dead_pos, unsigned long long* tests, int smem_optin,
-                      cudaStream_t st);
+                      const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,
+                      const uint32_t* nrep_dev, const float* thr, uint8_t* dead_row, uint8_t* dead_pos,
+                      unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st);
 // Quantization thresholds from a strided sample of row-major input rows.
 void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st);
 // Skyline of one small set in one CTA (false: too big, use k_relsky).
-bool launch_small_skyline(int D, const float* xyz, uint32_t n, uint8_t* dead, unsigned long long* tests,
-                          int smem_optin, cudaStream_t st);
+bool launch_small_skyline(int D, const float* xyz, const uint32_t* id, uint32_t n, uint8_t* dead,
+                          unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st);
 
 // Random partitioner (kernels_rand.cu): bit-exact assign_random on the GPU.
 size_t random_scratch_bytes(uint32_t n);

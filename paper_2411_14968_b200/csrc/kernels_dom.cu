@@ -309,7 +309,13 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                                 gt |= (sa.x > tb.x) | (sa.y > tb.y) | (sa.z > tb.z) | (sa.w > tb.w);
                                 lt |= (sa.x < tb.x) | (sa.y < tb.y) | (sa.z < tb.z) | (sa.w < tb.w);
                             }
-                            if (!gt && lt) {
+                            bool dom = !gt && lt;
+                            if (a.x64.x && !gt) {
+                                // FP64 input: confirm on the original rows
+                                const uint32_t slot = it.cb + k * 32 + lane;
+                                dom = dom64(a.x64, a.sid[base + i], a.cid[a.cidx ? a.cidx[slot] : slot]);
+                            }
+                            if (dom) {
                                 alive &= ~(1u << k);
                                 T[k][0] &= ~CodeLayout<D>::ALIVE;
                                 atomicOr(&sm.deadmask[lane], 1u << k);
@@ -403,6 +409,22 @@ __device__ __forceinline__ bool dom_f4(const float4* __restrict__ s, const float
         lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
     }
     return !gt && lt;
+}
+
+// dom_f4, or for FP64 input: s <= t on the float image (necessary), then
+// dominates_raw on the original doubles of rows rs, rt.
+template <int D>
+__device__ __forceinline__ bool dom_f4x(const float4* __restrict__ s, const float4* __restrict__ t, const X64& e,
+                                        uint32_t rs, uint32_t rt) {
+    if (!e.x) return dom_f4<D>(s, t);
+    constexpr int V = Dims2<D>::V;
+    bool gt = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const float4 a = s[v], b = t[v];
+        gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
+    }
+    return !gt && dom64(e, rs, rt);
 }
 
 template <int D>
@@ -553,11 +575,12 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                     float4 wv[V];
 #pragma unroll
                     for (int v = 0; v < V; ++v) wv[v] = wx[v];
-                    if (d1 && dom_f4<D>(wv, t)) {
+                    const uint32_t rw = a.x64.x ? a.id[w_pos[w]] : 0, rt = a.x64.x ? a.id[mypos] : 0;
+                    if (d1 && dom_f4x<D>(wv, t, a.x64, rw, rt)) {
                         alive = false;
                         T0 &= ~ALIVE;
                     }
-                    if (d2 && dom_f4<D>(t, wv)) {
+                    if (d2 && dom_f4x<D>(t, wv, a.x64, rt, rw)) {
                         w_kill[w] = 1;
                         killed_any = true;
                     }
@@ -589,7 +612,9 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                     if (b_key[u] > tkey) continue;  // sorted batches: a dominator has key <= tkey
                     const uint2 uq = b_code[u];
                     if (u != (uint32_t)tid && ((T0 - uq.x) & (T1 - uq.y) & GA) == GA) {
-                        if (dom_f4<D>(b_xyz + u * V, t)) {
+                        if (dom_f4x<D>(b_xyz + u * V, t, a.x64,
+                                       a.x64.x ? a.id[first ? seg_b + k0 + u : ovf[k0 + u]] : 0,
+                                       a.x64.x ? a.id[mypos] : 0)) {
                             alive = false;
                             T0 &= ~ALIVE;
                         }
@@ -681,9 +706,11 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
                                                    const uint32_t* __restrict__ idx,
                                                    const float4* __restrict__ rep_xyz,
                                                    const uint32_t* __restrict__ rep_key, const uint2* __restrict__ rep_qc,
+                                                   const uint32_t* __restrict__ rep_id,
                                                    uint32_t nrep_max, const uint32_t* nrep_dev,
                                                    const float* __restrict__ thr,
-                                                   uint8_t* __restrict__ dead_row, unsigned long long* tests) {
+                                                   uint8_t* __restrict__ dead_row, unsigned long long* tests,
+                                                   X64 x64) {
     constexpr int V = Dims2<D>::V;
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
@@ -716,6 +743,11 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         for (int j = 0; j < 4 * V; ++j) {
             xs[j] = (valid && j < D && (uint32_t)j < d) ? x[j] : 0.0f;
             if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)xs[j]);  // same key as k_prep
+        }
+        if (x64.x && valid) {
+            const double* xd = x64.x + (size_t)row * d;
+            sum = 0.0;
+            for (uint32_t j = 0; j < d; ++j) sum = __dadd_rn(sum, xd[j]);
         }
         tk = __float_as_uint(__double2float_rn(sum));
         if (CODES && valid) {
@@ -754,7 +786,8 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
             if (max_fold<8>(h) == (G | 0x80000000u)) {
 #pragma unroll 1
                 for (int k = 0; k < 8; ++k) {
-                    if (alive && coarse_pass<G>(Tl, q[k]) && dom_f4<D>(s_rep + (r + k) * V, t)) {
+                    if (alive && coarse_pass<G>(Tl, q[k]) &&
+                        dom_f4x<D>(s_rep + (r + k) * V, t, x64, x64.x ? rep_id[r + k] : 0, row)) {
                         alive = false;
                         Tl[0] &= ~CodeLayout<D>::ALIVE;
                     }
@@ -771,7 +804,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
                 constexpr uint32_t GA = G | 0x80000000u;
                 maybe = ((T0 - q.x) & (T1 - q.y) & GA) == GA;
             }
-            if (maybe && s_key[r] <= tk && dom_f4<D>(s_rep + r * V, t)) {
+            if (maybe && s_key[r] <= tk && dom_f4x<D>(s_rep + r * V, t, x64, x64.x ? rep_id[r] : 0, row)) {
                 alive = false;
                 nt += r + 1;
                 T0 &= ~CodeLayout<D>::ALIVE;
@@ -804,8 +837,9 @@ __global__ void k_gather_dead(const uint32_t* __restrict__ idx, const uint8_t* _
 // filter.cpp:139-145): the set in shared memory, every thread tests its
 // points against all others.
 template <int D>
-__global__ void __launch_bounds__(1024) k_small_skyline(const float4* __restrict__ xyz, uint32_t n,
-                                                        uint8_t* __restrict__ dead, unsigned long long* tests) {
+__global__ void __launch_bounds__(1024) k_small_skyline(const float4* __restrict__ xyz, const uint32_t* __restrict__ id,
+                                                        uint32_t n, uint8_t* __restrict__ dead,
+                                                        unsigned long long* tests, X64 x64) {
     constexpr int V = Dims2<D>::V;
     extern __shared__ float4 s_pts[];
     for (uint32_t i = threadIdx.x; i < n * V; i += blockDim.x) s_pts[i] = xyz[i];
@@ -815,7 +849,8 @@ __global__ void __launch_bounds__(1024) k_small_skyline(const float4* __restrict
         bool dom = false;
         for (uint32_t j = 0; j < n && !dom; ++j) {
             ++nt;
-            if (j != i && dom_f4<D>(s_pts + j * V, s_pts + i * V)) dom = true;
+            if (j != i && dom_f4x<D>(s_pts + j * V, s_pts + i * V, x64, x64.x ? id[j] : 0, x64.x ? id[i] : 0))
+                dom = true;
         }
         dead[i] = dom ? 1 : 0;
     }
@@ -879,9 +914,9 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey,
 }
 
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
-                      const uint32_t* rep_key, const uint2* rep_qc, uint32_t nrep, const uint32_t* nrep_dev,
-                      const float* thr, uint8_t* dead_row, uint8_t* dead_pos, unsigned long long* tests, int smem_optin,
-                      cudaStream_t st) {
+                      const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,
+                      const uint32_t* nrep_dev, const float* thr, uint8_t* dead_row, uint8_t* dead_pos,
+                      unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {
     if (D > 16) return false;
     const bool codes = rep_qc && thr && nrep >= 32;
     const size_t npad = (nrep + 7) & ~7u;
@@ -894,14 +929,14 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
             SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
             k_prefilter<DT, true, true><<<ceil_div(n, 256), 256, smem, st>>>(
-                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, nrep, nrep_dev, thr, dead_pos,
-                tests);
+                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
+                dead_pos, tests, x64);
         } else {
             SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
             k_prefilter<DT, false, false><<<ceil_div(n, 256), 256, smem, st>>>(
-                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, nullptr, nrep, nrep_dev, nullptr,
-                dead_row, tests);
+                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, nullptr, rep_id, nrep, nrep_dev,
+                nullptr, dead_row, tests, x64);
         }
     });
     SKY_LAUNCH_CHECK();
@@ -911,15 +946,15 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
     return true;
 }
 
-bool launch_small_skyline(int D, const float* xyz, uint32_t n, uint8_t* dead, unsigned long long* tests,
-                          int smem_optin, cudaStream_t st) {
+bool launch_small_skyline(int D, const float* xyz, const uint32_t* id, uint32_t n, uint8_t* dead,
+                          unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {
     if (D > 16 || n > 4096) return false;
     const size_t smem = (size_t)n * ((D + 3) / 4) * 16 + 16;
     if (smem + 1024 > (size_t)smem_optin) return false;
     if (!n) return true;
     SKY_DISPATCH_D16(D, {
         SKY_CUDA(cudaFuncSetAttribute(k_small_skyline<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_small_skyline<DT><<<1, 1024, smem, st>>>(reinterpret_cast<const float4*>(xyz), n, dead, tests);
+        k_small_skyline<DT><<<1, 1024, smem, st>>>(reinterpret_cast<const float4*>(xyz), id, n, dead, tests, x64);
     });
     SKY_LAUNCH_CHECK();
     return true;

@@ -135,7 +135,8 @@ class EngineConfig:
             strategy=int(p.strategy), p=int(p.p), m=int(p.m), seed=int(p.seed), slice_dim=int(p.slice_dim),
             filter=int(self.filter), rep_selection=int(self.rep_selection), rep_q=int(self.rep_q),
             merge=int(self.merge), workers=int(self.workers), local_algo=int(self.local_algo),
-            bnl_window_cap=int(self.bnl_window_cap), count_tests=int(bool(self.count_tests)))
+            bnl_window_cap=int(self.bnl_window_cap), count_tests=int(bool(self.count_tests)),
+            rep_seed=int(self.seed))
 
 
 @dataclass
@@ -181,6 +182,16 @@ def snap_slices(target_p: int, k: int) -> int:
     out = C.c_uint64(0)
     _raise(abi.load().sky_snap_slices(target_p, k, C.byref(out)))
     return int(out.value)
+
+
+def _as_rows(points) -> np.ndarray:
+    """float32 rows, or float64 rows when some value is not a float32."""
+    a = np.asarray(points)
+    if a.dtype == np.float64:
+        a64 = np.ascontiguousarray(a)
+        if a64.ndim == 2 and not np.array_equal(a64.astype(np.float32).astype(np.float64), a64, equal_nan=True):
+            return a64
+    return _as_points(a)
 
 
 def _as_points(points) -> np.ndarray:
@@ -246,19 +257,22 @@ class Engine:
 
     # skyline::run (engine.hpp:88)
     def run(self, points, config: EngineConfig, normalized: bool = True, *, device_ptr: Optional[int] = None,
-            n: Optional[int] = None, d: Optional[int] = None) -> RunResult:
-        """Run the engine. `points` is an (n, d) float32 host array, or pass
-        device_ptr/n/d for rows already resident on the GPU."""
+            n: Optional[int] = None, d: Optional[int] = None, dtype=np.float32) -> RunResult:
+        """Run the engine (skyline::run). `points` is an (n, d) host array, or
+        pass device_ptr/n/d (and dtype) for rows already resident on the GPU.
+        float64 rows take the exact FP64 path (sky_run_f64) unless every value
+        is a float32, in which case both paths give the same result and the
+        float32 one is used."""
         cfg = config.to_c()
         res = abi.SkyResult()
         if device_ptr is not None:
-            rc = self._lib.sky_run(self._h, C.c_void_p(device_ptr), n, d, int(normalized), 1, C.byref(cfg),
-                                   C.byref(res))
+            fn = self._lib.sky_run_f64 if np.dtype(dtype) == np.float64 else self._lib.sky_run
+            rc = fn(self._h, C.c_void_p(device_ptr), n, d, int(normalized), 1, C.byref(cfg), C.byref(res))
         else:
-            a = _as_points(points)
+            a = _as_rows(points)
             n, d = a.shape
-            rc = self._lib.sky_run(self._h, a.ctypes.data_as(C.c_void_p), n, d, int(normalized), 0,
-                                   C.byref(cfg), C.byref(res))
+            fn = self._lib.sky_run_f64 if a.dtype == np.float64 else self._lib.sky_run
+            rc = fn(self._h, a.ctypes.data_as(C.c_void_p), n, d, int(normalized), 0, C.byref(cfg), C.byref(res))
         self._err(rc)
         try:
             ids = np.ctypeslib.as_array(res.ids, shape=(res.n_ids,)).copy() if res.n_ids else np.zeros(0, np.int64)

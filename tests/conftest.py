@@ -28,5 +28,6 @@ def golden():
     with open(os.path.join(here, "golden.json")) as f:
         g = json.load(f)
     g["plane_arrays"] = np.load(os.path.join(here, "plane.npz"))
+    g["plane64_arrays"] = np.load(os.path.join(here, "plane64.npz"))
     g["config_arrays"] = np.load(os.path.join(here, "configs.npz"))
     return g

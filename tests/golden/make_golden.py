@@ -147,6 +147,39 @@ def plane():
     return out, arrays
 
 
+def plane64():
+    """FP64 inputs (the reference's own coordinate type): the reference's
+    generators (datagen.cpp:16-57) and a k/7 lattice (ties, not float32)."""
+    out = []
+    arrays = {}
+    k = 0
+    for dist in ("uniform", "correlated", "anticorrelated", "lattice7"):
+        for d in (2, 4, 7):
+            n = 500
+            if dist == "lattice7":
+                x = np.random.default_rng(77 + d).integers(0, 8, (n, d)) / 7.0
+            else:
+                x = O.ref_generate({"uniform": 0, "correlated": 1, "anticorrelated": 2}[dist], n, d, 40 + d)
+            xkey = f"p64_{dist}_{d}_x"
+            arrays[xkey] = x
+            for strat in (0, 1, 2, 3):
+                for filt in ((0, 2, 1) if strat == 1 else (0, 2)):
+                    for sel in ((0, 1, 2) if filt == 2 else (0,)):
+                        for merge in (0, 1):
+                            cfg = SkyConfig.make(strategy=strat, p=7, seed=13, slice_dim=d - 1, filter=filt,
+                                                 rep_q=3, merge=merge, workers=4, rep_selection=sel)
+                            r = O.ref_run(x, cfg, True)
+                            key = f"p64c{k}"
+                            arrays[key + "_ids"] = r["ids"]
+                            arrays[key + "_lss"] = r["local_skyline_sizes"].astype(np.int64)
+                            out.append({"key": key, "x": xkey, "dist": dist, "n": n, "d": d, "normalized": True,
+                                        "cfg": cfg.as_dict(), "effective_p": r["effective_p"],
+                                        "union_size": r["union_size"], "filtered_count": r["filtered_count"],
+                                        "final_size": r["final_size"]})
+                            k += 1
+    return out, arrays
+
+
 def configs():
     out = []
     arrays = {}
@@ -171,6 +204,7 @@ def main():
     O.build(ref=True)
     ka = known_answers()
     pl, pl_arr = plane()
+    p64, p64_arr = plane64()
     if "--keep-configs" in sys.argv:
         # reuse the (slow) BASELINE-config fixtures already committed
         with open(os.path.join(HERE, "golden.json")) as f:
@@ -180,7 +214,8 @@ def main():
         cf, cf_arr = configs()
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py", "source": "oracle/_ref/libskyref.so "
-                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "configs": cf}, f)
+                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "plane64": p64, "configs": cf}, f)
+    np.savez_compressed(os.path.join(HERE, "plane64.npz"), **p64_arr)
     np.savez_compressed(os.path.join(HERE, "plane.npz"), **pl_arr)
     np.savez_compressed(os.path.join(HERE, "configs.npz"), **cf_arr)
     print(len(ka), "known answers;", len(pl), "plane cases;", len(cf), "configs")

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 def to_engine_config(d):
     return EngineConfig(partition=PartitionConfig(Strategy(d["strategy"]), d["p"], d["m"], d["seed"], d["slice_dim"]),
                         filter=FilterKind(d["filter"]), rep_q=d["rep_q"], merge=MergeKind(d["merge"]),
-                        rep_selection=RepSelection(d.get("rep_selection", 0)),
+                        rep_selection=RepSelection(d.get("rep_selection", 0)), seed=d.get("rep_seed", d["seed"]),
                         workers=max(1, d["workers"]), local_algo=LocalAlgo(d.get("local_algo", 0)),
                         bnl_window_cap=d.get("bnl_window_cap", 4096) or 4096)
 
@@ -77,6 +77,43 @@ def test_plane_matches_reference(engine, golden, local_algo):
         assert np.array_equal(r.skyline, arr[key + "_ids"]), key
         assert r.metrics.local_skyline_sizes == arr[key + "_lss"].tolist(), key
         check_metrics(r, case, key)
+
+
+@pytest.mark.parametrize("local_algo", [LocalAlgo.SFS, LocalAlgo.BNL])
+def test_plane64_matches_reference(engine, golden, local_algo):
+    """FP64 rows through sky_run_f64: the reference's generators and a k/7
+    lattice whose values are not float32 (rounding creates ties the doubles
+    do not have)."""
+    arr = golden["plane64_arrays"]
+    for case in golden["plane64"]:
+        key = case["key"]
+        x = arr[case["x"]]
+        cfg = to_engine_config(case["cfg"])
+        cfg.local_algo = local_algo
+        cfg.bnl_window_cap = 64
+        r = engine.run(x, cfg, case["normalized"])
+        assert np.array_equal(r.skyline, arr[key + "_ids"]), key
+        assert r.metrics.local_skyline_sizes == arr[key + "_lss"].tolist(), key
+        check_metrics(r, case, key)
+
+
+def test_f64_large_vs_oracle(engine):
+    """FP64 rows at BASELINE-like sizes: near-ties below float32 resolution."""
+    rng = np.random.default_rng(3)
+    for it, (strat, filt, sel) in enumerate([(2, 2, 0), (3, 2, 0), (0, 0, 0), (1, 2, 1), (3, 2, 2), (1, 1, 0)]):
+        n, d = 30000, 4 + it % 3
+        base = (rng.integers(0, 1 << 20, (n, d)) / float(1 << 20))
+        x = np.clip(base + rng.integers(-2, 3, (n, d)) * 2.0 ** -40, 0.0, 1.0)  # differences below float32 ulp
+        cfg = SkyConfig.make(strategy=strat, p=16, seed=it, slice_dim=0, filter=filt, rep_q=4, merge=1,
+                             rep_selection=sel)
+        exp = O.oracle_run(x, cfg, True)
+        for algo in (LocalAlgo.SFS, LocalAlgo.BNL):
+            ecfg = to_engine_config(cfg.as_dict())
+            ecfg.local_algo = algo
+            r = engine.run(x, ecfg, True)
+            assert np.array_equal(r.skyline, exp["ids"]), (it, algo)
+            assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), (it, algo)
+            check_metrics(r, exp, (it, algo))
 
 
 @pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4, 5])

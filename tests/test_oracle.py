@@ -54,6 +54,21 @@ def test_plane_matches_reference_goldens(golden):
             assert r[m] == case[m], (key, m)
 
 
+def test_plane64_matches_reference_goldens(golden):
+    """FP64 rows (the reference's coordinate type): the restatement keeps
+    every decision in double precision."""
+    arr = golden["plane64_arrays"]
+    for case in golden["plane64"]:
+        key = case["key"]
+        x = arr[case["x"]]
+        assert x.dtype == np.float64
+        r = O.oracle_run(x, _cfg(case["cfg"]), case["normalized"])
+        assert np.array_equal(r["ids"], arr[key + "_ids"]), key
+        assert np.array_equal(r["local_skyline_sizes"].astype(np.int64), arr[key + "_lss"]), key
+        for m in ("effective_p", "union_size", "filtered_count", "final_size"):
+            assert r[m] == case[m], (key, m)
+
+
 def test_configs_match_reference_goldens(golden):
     from paper_2411_14968_b200.skyline import generate
     import hashlib
