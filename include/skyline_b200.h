@@ -189,6 +189,29 @@ SKY_API void sky_free(void* ptr);
  * Deterministic for (kind, n, d, seed) regardless of thread count. */
 SKY_API int sky_generate(int kind, uint64_t n, uint32_t d, uint64_t seed, float* out);
 
+/* ---- Data in and out (datagen.hpp / io.hpp of the reference) ------------ */
+/* Distribution (datagen.hpp:12-16). */
+enum { SKY_DIST_UNIFORM = 0, SKY_DIST_CORRELATED = 1, SKY_DIST_ANTICORRELATED = 2 };
+/* skyline::generate (datagen.cpp:127-151): n rows of d doubles, normalized,
+ * bit-identical to the reference for (dist, n, d, seed). out[n*d]. */
+SKY_API int sky_generate_family(int dist, uint64_t n, uint32_t d, uint64_t seed, double* out);
+/* skyline::normalize (datagen.cpp:153-168): column min-max to [0,1] in place. */
+SKY_API int sky_normalize(double* rows, uint64_t n, uint32_t d);
+/* skyline::ingest_csv (datagen.cpp:170-218): header row, selected columns in
+ * the given order (all when n_columns == 0), maximize[j] != 0 negates column
+ * j (Direction::Max), rows with a missing or non-numeric value dropped, then
+ * column min-max normalisation. *rows is malloc'ed (free with sky_free).
+ * Errors: SKY_E_IO (cannot open), SKY_E_DATA (empty / no usable rows),
+ * SKY_E_CONFIG (unknown column, direction count); text in sky_host_error(). */
+SKY_API int sky_ingest_csv(const char* path, const char* const* columns, uint32_t n_columns,
+                   const uint8_t* maximize, uint32_t n_maximize, double** rows,
+                   uint64_t* n, uint32_t* d);
+/* skyline::write_csv (datagen.cpp:220-238): header d0..d{d-1}, shortest
+ * round-trip doubles. */
+SKY_API int sky_write_csv(const char* path, const double* rows, uint64_t n, uint32_t d);
+/* Message of the last failed host-only call on this thread. */
+SKY_API const char* sky_host_error(void);
+
 /* Multi-rank planning helpers (host-only, pure functions; used by the
  * NCCL path and by the gloo tests). Longest-processing-time assignment of
  * `count` weighted units to `ranks` owners; owner[count]. */

@@ -133,6 +133,10 @@ def ref_lib():
         lib.skyref_run_f64.argtypes = [_f64p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig),
                                        C.POINTER(_RefResult)]
         lib.skyref_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _f64p]
+        lib.skyref_ingest_csv.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), C.c_uint32, _u8p, C.c_uint32,
+                                          C.POINTER(_f64p), _u64p, C.POINTER(C.c_uint32)]
+        lib.skyref_write_csv.argtypes = [C.c_char_p, _f64p, C.c_uint64, C.c_uint32]
+        lib.skyref_free.argtypes = [C.c_void_p]
         lib.skyref_result_free.argtypes = [C.POINTER(_RefResult)]
         lib.skyref_assign.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), _u64p, _u64p]
         lib.skyref_bruteforce.argtypes = [_f32p, C.c_uint64, C.c_uint32, _i64p]
@@ -267,3 +271,30 @@ def ref_generate(dist: int, n: int, d: int, seed: int) -> np.ndarray:
     if rc:
         raise CpuError(rc)
     return out
+
+
+def ref_ingest_csv(path: str, columns=None, maximize=None) -> np.ndarray:
+    """skyline::ingest_csv of the reference itself (raises CpuError)."""
+    lib = ref_lib()
+    cols = list(columns or [])
+    arr = (C.c_char_p * max(1, len(cols)))(*[c.encode() for c in cols])
+    mx = list(maximize or [])
+    flags = np.array([1 if c in mx else 0 for c in cols], np.uint8) if mx else np.zeros(1, np.uint8)
+    rows = _f64p()
+    n = C.c_uint64(0)
+    d = C.c_uint32(0)
+    rc = lib.skyref_ingest_csv(path.encode(), arr, len(cols), flags.ctypes.data_as(_u8p), len(cols) if mx else 0,
+                               C.byref(rows), C.byref(n), C.byref(d))
+    if rc:
+        raise CpuError(rc)
+    try:
+        return np.ctypeslib.as_array(rows, shape=(n.value, d.value)).copy()
+    finally:
+        lib.skyref_free(rows)
+
+
+def ref_write_csv(path: str, rows) -> None:
+    a = np.ascontiguousarray(rows, dtype=np.float64)
+    rc = ref_lib().skyref_write_csv(path.encode(), a.ctypes.data_as(_f64p), a.shape[0], a.shape[1])
+    if rc:
+        raise CpuError(rc)

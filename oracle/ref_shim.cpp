@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -147,6 +148,41 @@ int skyref_generate(int dist, uint64_t n, uint64_t d, uint64_t seed, double* out
             for (uint64_t j = 0; j < d; ++j) out[i * d + j] = r.points[i].coords[j];
     });
 }
+
+// skyline::ingest_csv (datagen.cpp:170-218); *rows malloc'ed.
+int skyref_ingest_csv(const char* path, const char* const* cols, uint32_t ncols, const uint8_t* maxflags,
+                      uint32_t nmax, double** rows, uint64_t* n, uint32_t* d) {
+    *rows = nullptr;
+    *n = 0;
+    *d = 0;
+    return guarded([&] {
+        std::vector<std::string> columns(cols, cols + ncols);
+        std::vector<Direction> dirs;
+        for (uint32_t j = 0; j < nmax; ++j) dirs.push_back(maxflags[j] ? Direction::Max : Direction::Min);
+        const Dataset r = ingest_csv(path, columns, dirs);
+        *n = r.size();
+        *d = static_cast<uint32_t>(r.d);
+        *rows = static_cast<double*>(std::malloc((r.size() * r.d ? r.size() * r.d : 1) * sizeof(double)));
+        for (uint64_t i = 0; i < r.size(); ++i)
+            for (uint64_t j = 0; j < r.d; ++j) (*rows)[i * r.d + j] = r.points[i].coords[j];
+    });
+}
+
+// skyline::write_csv (datagen.cpp:220-238).
+int skyref_write_csv(const char* path, const double* rows, uint64_t n, uint32_t d) {
+    return guarded([&] {
+        Dataset r;
+        r.d = d;
+        r.points.resize(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            r.points[i].coords.assign(rows + i * d, rows + (i + 1) * d);
+            r.points[i].id = static_cast<PointId>(i);
+        }
+        write_csv(r, path);
+    });
+}
+
+void skyref_free(void* p) { std::free(p); }
 
 void skyref_result_free(skyref_result* r) {
     std::free(r->ids);

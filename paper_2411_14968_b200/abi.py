@@ -13,6 +13,7 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "libskyline_b200.so")
 
 SKY_OK = 0
+SKY_E_CONFIG, SKY_E_DIMENSION, SKY_E_NORMALIZATION, SKY_E_DATA, SKY_E_IO = 1, 2, 3, 4, 5
 STATUS_NAMES = {
     0: "OK", 1: "ConfigError", 2: "DimensionError", 3: "NormalizationError",
     4: "DataError", 5: "IoError", 10: "CudaError", 11: "NcclError", 12: "InternalError",
@@ -91,6 +92,7 @@ EXPORTED = [
     "sky_snap_slices", "sky_relative_skyline", "sky_skyline",
     "sky_representatives", "sky_free", "sky_generate", "sky_plan_lpt",
     "sky_plan_split", "sky_plan_local_shards", "sky_plan_merge_shards", "sky_abi_version",
+    "sky_generate_family", "sky_normalize", "sky_ingest_csv", "sky_write_csv", "sky_host_error",
 ]
 
 _lib = None
@@ -123,6 +125,12 @@ def load():
                             C.POINTER(SkyConfig), C.POINTER(SkyResult)]
     lib.sky_run_f64.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
                             C.POINTER(SkyConfig), C.POINTER(SkyResult)]
+    lib.sky_generate_family.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.c_double)]
+    lib.sky_normalize.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_uint32]
+    lib.sky_ingest_csv.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), C.c_uint32, _u8p, C.c_uint32,
+                                   C.POINTER(C.POINTER(C.c_double)), _u64p, C.POINTER(C.c_uint32)]
+    lib.sky_write_csv.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.c_uint64, C.c_uint32]
+    lib.sky_host_error.restype = C.c_char_p
     lib.sky_result_free.argtypes = [C.POINTER(SkyResult)]
     lib.sky_assign.argtypes = [vp, _f32p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(SkyConfig), _u64p, _u64p]
     lib.sky_snap_slices.argtypes = [C.c_uint64, C.c_uint64, _u64p]

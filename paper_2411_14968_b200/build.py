@@ -19,6 +19,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "csrc")
 OUT = os.path.join(PKG, "libskyline_b200.so")
+CLI = os.path.join(PKG, "skyline-cli")
+CLI_SRC = os.path.join(ROOT, "tools", "skyline_cli.cpp")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -26,7 +28,7 @@ COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibilit
           "-I", os.path.join(ROOT, "include")]
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcudafe", "--diag_suppress=177", "-diag-suppress", "1444"]
-SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "host.cpp"]
+SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "host.cpp", "dataio.cpp"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 
 
@@ -63,7 +65,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
+    build_cli(force)
     return OUT
+
+
+def build_cli(force: bool = False) -> str:
+    """tools/skyline_cli.cpp -> paper_2411_14968_b200/skyline-cli (the GPU
+    skyline-cli; host C++ linked against libskyline_b200.so via $ORIGIN)."""
+    hdr = os.path.join(ROOT, "include", "skyline_b200.h")
+    if force or _newer([CLI_SRC, hdr, OUT], CLI):
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI,
+               "-L", PKG, "-lskyline_b200", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("skyline-cli build failed")
+    return CLI
 
 
 def main():

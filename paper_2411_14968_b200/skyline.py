@@ -378,6 +378,63 @@ def generate(kind: int, n: int, d: int, seed: int) -> np.ndarray:
     return out
 
 
+class Distribution(enum.IntEnum):
+    """datagen.hpp:12-16"""
+    Uniform = 0
+    Correlated = 1
+    Anticorrelated = 2
+
+
+def _host_raise(rc: int):
+    if rc != abi.SKY_OK:
+        _raise(rc, abi.load().sky_host_error().decode(errors="replace"))
+
+
+def generate_family(distribution, n: int, d: int, seed: int) -> np.ndarray:
+    """skyline::generate (datagen.cpp:127-151): FP64 rows identical to the
+    reference's for (distribution, n, d, seed)."""
+    out = np.empty((n, d), np.float64)
+    _host_raise(abi.load().sky_generate_family(int(distribution), n, d, seed,
+                                               out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def normalize(rows) -> np.ndarray:
+    """skyline::normalize (datagen.cpp:153-168): column min-max to [0,1]."""
+    a = np.array(rows, dtype=np.float64, order="C", copy=True)
+    n, d = a.shape
+    _host_raise(abi.load().sky_normalize(a.ctypes.data_as(C.POINTER(C.c_double)), n, d))
+    return a
+
+
+def ingest_csv(path: str, columns=None, maximize=None) -> np.ndarray:
+    """skyline::ingest_csv (datagen.cpp:170-218): selected columns (all when
+    None), `maximize` = column names where larger raw values are better."""
+    lib = abi.load()
+    cols = list(columns or [])
+    arr = (C.c_char_p * max(1, len(cols)))(*[c.encode() for c in cols])
+    mx = list(maximize or [])
+    if mx and not cols:
+        raise ConfigError("maximize needs explicit columns")
+    flags = np.array([1 if c in mx else 0 for c in cols], np.uint8) if mx else np.zeros(1, np.uint8)
+    rows = C.POINTER(C.c_double)()
+    n = C.c_uint64(0)
+    d = C.c_uint32(0)
+    _host_raise(lib.sky_ingest_csv(path.encode(), arr, len(cols), flags.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                   len(cols) if mx else 0, C.byref(rows), C.byref(n), C.byref(d)))
+    try:
+        return np.ctypeslib.as_array(rows, shape=(n.value, d.value)).copy()
+    finally:
+        lib.sky_free(rows)
+
+
+def write_csv(path: str, rows) -> None:
+    """skyline::write_csv (datagen.cpp:220-238)."""
+    a = np.ascontiguousarray(rows, dtype=np.float64)
+    n, d = a.shape
+    _host_raise(abi.load().sky_write_csv(path.encode(), a.ctypes.data_as(C.POINTER(C.c_double)), n, d))
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _raise(abi.load().sky_nccl_unique_id(buf, 128))

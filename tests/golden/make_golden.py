@@ -180,6 +180,75 @@ def plane64():
     return out, arrays
 
 
+INGEST_CASES = [
+    # (name, csv text, columns, maximize)
+    ("plain", "a,b,c\n1,2,3\n4,5,6\n7,8,9\n", None, None),
+    ("trim_cr_blank", " a , b \r\n1.5, 2\r\n\r\n  \n3 ,4.25\r\n-1,0\r\n", None, None),
+    ("bad_rows", "x,y\n1,2\nfoo,3\n4,\n5\n6,7,8\n1e3,nan\ninf,1\n9,10\n", None, None),
+    ("select_max", "p,q,r\n1,10,100\n2,30,50\n3,20,75\n", ["r", "p"], ["r"]),
+    ("constant_col", "u,v\n5,1\n5,2\n5,3\n", None, None),
+    ("precision", "a,b\n0.1,0.7\n0.2,0.30000000000000004\n1e-300,2.5e10\n", None, None),
+    ("unknown_col", "a,b\n1,2\n", ["zz"], None),
+    ("empty", "", None, None),
+    ("no_rows", "a,b\nq,r\n", None, None),
+]
+
+
+def dataio():
+    """The steps either side of the path: the reference's
+    generators, CSV ingest and CSV output."""
+    import tempfile
+    gens = []
+    for dist in (0, 1, 2):
+        for n, d, seed in ((1000, 1, 0), (2000, 3, 7), (500, 8, 123456789), (3000, 5, 2 ** 63 + 5)):
+            x = O.ref_generate(dist, n, d, seed)
+            gens.append({"dist": dist, "n": n, "d": d, "seed": seed,
+                         "sha256": hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest(),
+                         "head": x[:3].tolist()})
+    ingest = []
+    with tempfile.TemporaryDirectory() as td:
+        for name, text, cols, mx in INGEST_CASES:
+            path = os.path.join(td, name + ".csv")
+            with open(path, "w", newline="") as f:
+                f.write(text)
+            case = {"name": name, "text": text, "columns": cols, "maximize": mx}
+            try:
+                r = O.ref_ingest_csv(path, cols, mx)
+                case["rows_hex"] = [[v.hex() for v in row] for row in r.tolist()]
+                case["shape"] = list(r.shape)
+            except O.CpuError as e:
+                case["error"] = e.code
+            ingest.append(case)
+        rows = O.ref_generate(2, 50, 4, 99)
+        rows[0, 0] = 1e-7
+        rows[1, 1] = 123456.0
+        rows[2, 2] = 0.0
+        path = os.path.join(td, "w.csv")
+        O.ref_write_csv(path, rows)
+        wcsv = {"rows_hex": [[v.hex() for v in r] for r in rows.tolist()], "text": open(path).read()}
+        # skyline-cli generate: the reference's generate() + write_csv() bytes
+        gen_csv = []
+        for dist, n, d, seed in ((2, 200, 3, 5), (0, 100, 6, 0), (1, 150, 2, 77)):
+            path = os.path.join(td, f"g{dist}.csv")
+            O.ref_write_csv(path, O.ref_generate(dist, n, d, seed))
+            gen_csv.append({"dist": dist, "n": n, "d": d, "seed": seed,
+                            "sha256": hashlib.sha256(open(path, "rb").read()).hexdigest()})
+    # skyline-cli run: the reference's run() on its own generated data
+    cli = []
+    for gen, flags in ((("anticorrelated", 20000, 4, 3), dict(strategy=2, filter=2, merge=1, p=16)),
+                       (("uniform", 5000, 3, 9), dict(strategy=0, filter=0, merge=0, p=8)),
+                       (("correlated", 8000, 5, 1), dict(strategy=3, filter=2, merge=1, p=12, rep_selection=2)),
+                       (("anticorrelated", 6000, 2, 4), dict(strategy=1, filter=1, merge=1, p=9))):
+        dist = {"uniform": 0, "correlated": 1, "anticorrelated": 2}[gen[0]]
+        x = O.ref_generate(dist, gen[1], gen[2], gen[3])
+        cfg = SkyConfig.make(seed=gen[3], rep_q=5, workers=1, **flags)
+        r = O.ref_run(x, cfg, True)
+        cli.append({"gen": list(gen), "cfg": cfg.as_dict(), "ids": r["ids"].tolist(),
+                    "effective_p": r["effective_p"], "union_size": r["union_size"],
+                    "filtered_count": r["filtered_count"], "final_size": r["final_size"]})
+    return {"generate": gens, "ingest": ingest, "write_csv": wcsv, "generate_csv": gen_csv, "cli_run": cli}
+
+
 def configs():
     out = []
     arrays = {}
@@ -205,6 +274,7 @@ def main():
     ka = known_answers()
     pl, pl_arr = plane()
     p64, p64_arr = plane64()
+    dio = dataio()
     if "--keep-configs" in sys.argv:
         # reuse the (slow) BASELINE-config fixtures already committed
         with open(os.path.join(HERE, "golden.json")) as f:
@@ -214,7 +284,7 @@ def main():
         cf, cf_arr = configs()
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py", "source": "oracle/_ref/libskyref.so "
-                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "plane64": p64, "configs": cf}, f)
+                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "plane64": p64, "dataio": dio, "configs": cf}, f)
     np.savez_compressed(os.path.join(HERE, "plane64.npz"), **p64_arr)
     np.savez_compressed(os.path.join(HERE, "plane.npz"), **pl_arr)
     np.savez_compressed(os.path.join(HERE, "configs.npz"), **cf_arr)
