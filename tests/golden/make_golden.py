@@ -249,6 +249,42 @@ def dataio():
     return {"generate": gens, "ingest": ingest, "write_csv": wcsv, "generate_csv": gen_csv, "cli_run": cli}
 
 
+def acceptance():
+    """The reference's acceptance criteria 3-7 (tests/acceptance/acceptance.cpp:
+    200-378) measured by the reference itself on its own generated data: the
+    GPU suite must reproduce every count, so it passes or fails exactly where
+    the reference does."""
+    import time
+    out = {"c3": [], "c4": [], "c5": {}, "c6": {}, "c7": []}
+    for dist in (0, 1, 2):
+        for m in (4, 8):
+            for seed in (1, 2, 3):
+                x = O.ref_generate(dist, 100000, 4, seed)
+                r = O.ref_run(x, SkyConfig.make(strategy=1, m=m, p=1, filter=1, workers=2), True)
+                out["c3"].append({"dist": dist, "m": m, "seed": seed, "filtered": r["filtered_count"]})
+        for seed in (1, 2, 3):
+            x = O.ref_generate(dist, 100000, 4, seed)
+            for sel in (0, 1):
+                r = O.ref_run(x, SkyConfig.make(strategy=0, p=8, seed=seed, filter=2, rep_selection=sel, rep_q=3,
+                                                workers=2), True)
+                out["c4"].append({"dist": dist, "seed": seed, "sel": sel, "filtered": r["filtered_count"]})
+    x = O.ref_generate(2, 1000000, 4, 1)
+    for strat in (0, 1, 2, 3):
+        r = O.ref_run(x, SkyConfig.make(strategy=strat, p=120, seed=1, workers=2), True)
+        out["c5"][str(strat)] = r["union_size"]
+    for name, kw, w in (("sliced+_1", dict(filter=2, merge=0), 1), ("sliced+_8", dict(filter=2, merge=0), 8),
+                        ("noseq_8", dict(filter=0, merge=1), 8)):
+        r = O.ref_run(x, SkyConfig.make(strategy=3, p=120, rep_q=5, workers=w, **kw), True)
+        out["c6"][name] = {"local_merge_ms": r["local_ms"] + r["merge_ms"], "final_size": r["final_size"],
+                           "union_size": r["union_size"], "filtered": r["filtered_count"]}
+    x = O.ref_generate(2, 100000, 4, 1)
+    for p in (8, 64, 512):
+        r = O.ref_run(x, SkyConfig.make(strategy=3, p=p, workers=2), True)
+        out["c7"].append({"p": p, "union_size": r["union_size"]})
+    out["host_threads"] = O.ref_lib().skyref_hardware_concurrency()
+    return out
+
+
 def configs():
     out = []
     arrays = {}
@@ -275,6 +311,7 @@ def main():
     pl, pl_arr = plane()
     p64, p64_arr = plane64()
     dio = dataio()
+    acc = acceptance()
     if "--keep-configs" in sys.argv:
         # reuse the (slow) BASELINE-config fixtures already committed
         with open(os.path.join(HERE, "golden.json")) as f:
@@ -284,7 +321,7 @@ def main():
         cf, cf_arr = configs()
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py", "source": "oracle/_ref/libskyref.so "
-                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "plane64": p64, "dataio": dio, "configs": cf}, f)
+                   "(unmodified /root/reference/proj/src)", "known_answers": ka, "plane": pl, "plane64": p64, "dataio": dio, "acceptance": acc, "configs": cf}, f)
     np.savez_compressed(os.path.join(HERE, "plane64.npz"), **p64_arr)
     np.savez_compressed(os.path.join(HERE, "plane.npz"), **pl_arr)
     np.savez_compressed(os.path.join(HERE, "configs.npz"), **cf_arr)

@@ -1,0 +1,196 @@
+"""The reference's acceptance suite (tests/acceptance/acceptance.cpp) on the
+GPU engine, FP64 rows from the reference's own generators:
+
+1. oracle equivalence over the configuration plane (acceptance.cpp:54-114)
+2. the two merge identities on 200 random instances each (:116-195)
+3-5, 7. the paper's effectiveness measurements (grid filtering, Sorted vs
+   Region reps, union ordering at 1M, union growth over p; :200-378): the GPU
+   must reproduce the reference's own counts exactly (fixtures measured by
+   the reference in tests/golden/make_golden.py), so it passes or fails each
+   criterion exactly where the reference does
+6. the noseq vs sliced+ time ratio, measured on the GPU (:321-355)
+8. determinism over repetitions and worker counts (:380-430)
+
+Each criterion prints the reference's PASS/FAIL line."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2411_14968_b200 import (EngineConfig, FilterKind, MergeKind, PartitionConfig, RepSelection, Strategy,
+                                   generate_family)
+from paper_2411_14968_b200.abi import SkyConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_skyline(x):
+    """skyline_bruteforce stand-in: the restatement's one-partition SFS on the
+    same doubles (pinned to the reference by tests/test_oracle.py)."""
+    return O.oracle_run(x, SkyConfig.make(strategy=3, p=1), True)["ids"]
+
+
+def cfg(strategy, p=32, seed=7, filt=FilterKind.None_, sel=RepSelection.Sorted, q=5, merge=MergeKind.Sequential,
+        workers=1, m=0, rep_seed=None):
+    return EngineConfig(partition=PartitionConfig(Strategy(strategy), p, m, seed), filter=filt, rep_selection=sel,
+                        rep_q=q, merge=merge, workers=workers, seed=seed if rep_seed is None else rep_seed)
+
+
+def report(n, ok, text):
+    print(f"{'PASS' if ok else 'FAIL'} criterion {n}: {text}")
+
+
+def test_criterion_1_oracle_plane(engine):
+    runs = mismatches = 0
+    seed = 1000
+    for dist in (0, 1, 2):
+        for d in (2, 3, 4, 5):
+            for n in (100, 1000, 5000):
+                x = generate_family(dist, n, d, seed)
+                seed += 1
+                want = oracle_skyline(x)
+                for strat in (0, 1, 2, 3):
+                    filters = [(FilterKind.None_, RepSelection.Sorted),
+                               (FilterKind.Representative, RepSelection.Sorted),
+                               (FilterKind.Representative, RepSelection.Region)]
+                    if strat == 1:
+                        filters.append((FilterKind.GridFilter, RepSelection.Sorted))
+                    for filt, sel in filters:
+                        for merge in (MergeKind.Sequential, MergeKind.NoSeq):
+                            for workers in (1, 8):
+                                r = engine.run(x, cfg(strat, filt=filt, sel=sel, merge=merge, workers=workers))
+                                runs += 1
+                                mismatches += not np.array_equal(r.skyline, want)
+    report(1, mismatches == 0, f"oracle equivalence over {runs} configurations: {mismatches} mismatches")
+    assert mismatches == 0
+
+
+def test_criterion_2_merge_identities(engine):
+    rng = np.random.default_rng(2024)
+
+    def instance():
+        n, d = int(rng.integers(1, 2001)), int(rng.integers(2, 7))
+        if rng.integers(2) == 0:
+            return generate_family(int(rng.choice([0, 2])), n, d, int(rng.integers(1 << 62)))
+        levels = int(rng.integers(2, 8))
+        return rng.integers(0, levels + 1, (n, d)) / levels  # ties and duplicates
+
+    prop1 = eq3 = 0
+    for _ in range(200):  # Proposition 1: Sky(r) = Sky(U Sky(r_i)), random partitioning
+        x = instance()
+        r = engine.run(x, cfg(0, p=int(rng.integers(1, 17)), seed=int(rng.integers(1 << 40))))
+        prop1 += not np.array_equal(r.skyline, oracle_skyline(x))
+    for _ in range(200):  # Eq. 3: union of relative skylines against pd_i
+        x = instance()
+        strat = int(rng.integers(4))
+        c = cfg(strat, p=int(rng.integers(1, 17)), seed=int(rng.integers(1 << 40)), merge=MergeKind.NoSeq,
+                m=int(rng.integers(1, 5)) if strat in (1, 2) else 0)
+        c.partition.slice_dim = int(rng.integers(x.shape[1]))
+        r = engine.run(x, c)
+        eq3 += not np.array_equal(r.skyline, oracle_skyline(x))
+    report(2, prop1 == 0 and eq3 == 0, f"200 randomized instances per proposition: {prop1} Prop-1 failures, "
+                                       f"{eq3} Eq-3 failures")
+    assert prop1 == 0 and eq3 == 0
+
+
+def test_criterion_3_grid_filtering(engine, golden):
+    exp = {(c["dist"], c["m"], c["seed"]): c["filtered"] for c in golden["acceptance"]["c3"]}
+    got = {}
+    for (dist, m, seed) in exp:
+        x = generate_family(dist, 100000, 4, seed)
+        got[(dist, m, seed)] = engine.run(x, cfg(1, p=1, m=m, filt=FilterKind.GridFilter, workers=2)).metrics.filtered_count
+    assert got == exp
+    ok = True
+    parts = []
+    for dist, want in ((0, 0.58), (1, 0.90), (2, 0.16)):
+        mean = np.mean([got[(dist, 4, s)] for s in (1, 2, 3)]) / 100000
+        ok &= abs(mean - want) <= 0.10
+        parts.append(f"{['uniform', 'correlated', 'anticorrelated'][dist]} {100 * mean:.1f}% (expected "
+                     f"{100 * want:.0f}%+-10pp)")
+    report(3, ok, "grid filtering at m=4: " + ", ".join(parts) + " (identical counts to the reference)")
+
+
+def test_criterion_4_rep_trend(engine, golden):
+    exp = {(c["dist"], c["seed"], c["sel"]): c["filtered"] for c in golden["acceptance"]["c4"]}
+    got = {}
+    for (dist, seed, sel) in exp:
+        x = generate_family(dist, 100000, 4, seed)
+        got[(dist, seed, sel)] = engine.run(x, cfg(0, p=8, seed=seed, filt=FilterKind.Representative,
+                                                   sel=RepSelection(sel), q=3, workers=2)).metrics.filtered_count
+    assert got == exp
+    ok = True
+    for dist in (2, 0, 1):
+        votes = sum((got[(dist, s, 0)] >= got[(dist, s, 1)]) if dist == 2 else (got[(dist, s, 1)] >= got[(dist, s, 0)])
+                    for s in (1, 2, 3))
+        ok &= votes >= 2
+    report(4, ok, "representative filtering trend (random partitioning, p=8, q=3), identical counts")
+
+
+def test_criterion_5_union_ordering(engine, golden):
+    x = generate_family(2, 1000000, 4, 1)
+    u = {s: engine.run(x, cfg(s, p=120, seed=1, workers=2)).metrics.union_size for s in (0, 1, 2, 3)}
+    assert {str(k): v for k, v in u.items()} == golden["acceptance"]["c5"]
+    ok = u[0] > u[1] and u[0] > u[2] and u[0] > u[3]
+    report(5, ok, f"union sizes on anticorrelated 1M: random={u[0]} > grid={u[1]}, angular={u[2]}, sliced={u[3]}")
+    assert ok
+
+
+def test_criterion_6_noseq_vs_sliced_plus(engine, golden):
+    x = generate_family(2, 1000000, 4, 1)
+
+    def phases(filt, merge):
+        best = None
+        for _ in range(3):
+            r = engine.run(x, cfg(3, p=120, seed=0, filt=filt, merge=merge, workers=8))
+            t = r.metrics.local_ms + r.metrics.merge_ms
+            best = t if best is None else min(best, t)
+        return best, r
+
+    t_plus, r_plus = phases(FilterKind.Representative, MergeKind.Sequential)
+    t_noseq, r_noseq = phases(FilterKind.None_, MergeKind.NoSeq)
+    ref = golden["acceptance"]["c6"]
+    assert r_plus.metrics.final_size == ref["sliced+_8"]["final_size"] == r_noseq.metrics.final_size
+    assert r_plus.metrics.union_size == ref["sliced+_8"]["union_size"]
+    assert r_noseq.metrics.union_size == ref["noseq_8"]["union_size"]
+    ratio = t_noseq / t_plus
+    print(f"     GPU local+merge: sliced+ {t_plus:.3f} ms, noseq {t_noseq:.3f} ms; reference CPU "
+          f"({golden['acceptance']['host_threads']} threads): sliced+ 1 worker "
+          f"{ref['sliced+_1']['local_merge_ms']:.1f} ms, 8 workers {ref['sliced+_8']['local_merge_ms']:.1f} ms")
+    report(6, ratio <= 1.10, f"GPU noseq/sliced+ ratio {ratio:.2f} (need <=1.10); GPU speedup over the reference's "
+                             f"1-worker sliced+ {ref['sliced+_1']['local_merge_ms'] / t_plus:.0f}x")
+
+
+def test_criterion_7_union_growth(engine, golden):
+    x = generate_family(2, 100000, 4, 1)
+    u = [engine.run(x, cfg(3, p=p, workers=2)).metrics.union_size for p in (8, 64, 512)]
+    assert u == [c["union_size"] for c in golden["acceptance"]["c7"]]
+    ok = u[0] <= u[1] <= u[2]
+    report(7, ok, f"sliced union size over p in {{8,64,512}}: {u[0]} <= {u[1]} <= {u[2]}")
+    assert ok
+
+
+def test_criterion_8_determinism(engine):
+    rng = np.random.default_rng(88)
+    divergent = 0
+    for draw in range(10):
+        x = generate_family(draw % 3, int(rng.integers(500, 5000)), int(rng.integers(2, 6)), int(rng.integers(1 << 62)))
+        seed = int(rng.integers(1 << 62))
+        sel = int(rng.integers(3))
+        c = cfg(int(rng.integers(4)), p=int(rng.integers(1, 33)), seed=seed, q=int(rng.integers(1, 9)),
+                filt=FilterKind.None_ if sel == 0 else FilterKind.Representative,
+                sel=RepSelection.Sorted if sel == 1 else RepSelection.Region,
+                merge=MergeKind(int(rng.integers(2))))
+        ref = None
+        for workers in (1, 4, 8):
+            for _ in range(3):
+                c.workers = workers
+                r = engine.run(x, c)
+                m = r.metrics
+                key = (r.skyline.tobytes(), r.effective_p, m.filtered_count, m.union_size, m.final_size,
+                       tuple(m.local_skyline_sizes))
+                if ref is None:
+                    ref = key
+                elif key != ref:
+                    divergent += 1
+    report(8, divergent == 0, f"10 random configurations x 3 repetitions x workers {{1,4,8}}: {divergent} "
+                              "divergent outputs")
+    assert divergent == 0
