@@ -76,7 +76,7 @@ enum Slot {
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
-    S_SCAN, S_PTS64, S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
+    S_SCAN, S_PTS64, S_GROUPS, S_GB, S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -84,9 +84,12 @@ enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PC
 constexpr int kTile = 512;          // candidates per relsky item (RS_THREADS * RS_K)
 constexpr uint32_t kChunk = 8192;   // comparators per relsky item before bounding
 constexpr uint32_t kBlock = 512;    // local block-skyline size
+// candidate x comparator pairs (before bounding) below which the remaining
+// comparators of a multi-wave relsky run as one last wave
+constexpr uint64_t kWaveSplitPairs = 8ull << 30;
 
 // misc device words
-enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_TESTS = 8 /* 4 x u64 */,
+enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_NITEMS = 7, M_TESTS = 8 /* 4 x u64 */,
        M_HITS = 16 /* 4 x u64, per phase */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
@@ -458,80 +461,149 @@ class Runner {
         count();
     }
 
-    // Two-wave relative skyline of the candidates of partitions [qb, qe)
-    // (positions offc[p]..offc[p+1] of `C`) against their comparator ranges
-    // (comps_of(p), most likely dominators first). Wave A: every candidate vs
-    // the first `head` comparators of its list. The surviving candidates are
-    // then compacted into dense per-partition lists, so wave B (the rest of
-    // the list) runs full tiles of live candidates instead of tiles whose
-    // dominated slots still burn test issue.
+    // Multi-wave relative skyline of the candidates of partitions [qb, qe)
+    // (positions offc[p]..offc[p+1] of `C`) against their comparator lists
+    // (comps_of(p), most likely dominators first). Wave 0 tests every
+    // candidate against the first `head` comparators of its list; wave w >= 1
+    // takes the next head*3*4^(w-1) comparators. Between waves the live
+    // candidates are compacted into dense per-partition lists and the next
+    // wave's items are built on the device (k_plan_items), so tiles stay full
+    // of live candidates without a host round trip.
     template <class CompsOf>
     void relsky_waves(int D, const std::vector<uint32_t>& offc, uint32_t qb, uint32_t qe, CompsOf comps_of,
                       const RelskyArgs& base, const uint2* cq, const uint2* sq, uint32_t tile, uint32_t chunk,
                       uint32_t head) {
         if (qb >= qe) return;
-        std::vector<std::vector<uint2>> rest(qe - qb);
-        std::vector<uint2> comps, first;
+        const uint32_t np = qe - qb;
+        std::vector<std::vector<uint2>> lists(np);
+        uint64_t maxlen = 0;
+        for (uint32_t p = qb; p < qe; ++p) {
+            if (offc[p + 1] == offc[p]) continue;
+            comps_of(p, lists[p - qb]);
+            uint64_t len = 0;
+            for (const uint2& r : lists[p - qb]) len += r.y - r.x;
+            maxlen = std::max(maxlen, len);
+        }
+        // the sub-list [lo, hi) (in comparator counts) of a list
+        auto slice = [](const std::vector<uint2>& l, uint64_t lo, uint64_t hi, std::vector<uint2>& out) {
+            out.clear();
+            uint64_t at = 0;
+            for (const uint2& r : l) {
+                const uint64_t len = r.y - r.x, b = std::max(lo, at), e = std::min(hi, at + len);
+                if (b < e) out.push_back(make_uint2(r.x + (uint32_t)(b - at), r.x + (uint32_t)(e - at)));
+                at += len;
+                if (at >= hi) break;
+            }
+        };
+        std::vector<uint2> sub;
         Plan A;
         A.tile = tile;
         A.chunk = chunk;
-        uint64_t rest_total = 0;
         for (uint32_t p = qb; p < qe; ++p) {
-            if (offc[p + 1] == offc[p]) continue;
-            comps_of(p, comps);
-            first.clear();
-            uint32_t budget = head;
-            size_t r = 0;
-            for (; r < comps.size() && budget; ++r) {
-                const uint32_t len = comps[r].y - comps[r].x;
-                if (len <= budget) {
-                    first.push_back(comps[r]);
-                    budget -= len;
-                } else {
-                    first.push_back(make_uint2(comps[r].x, comps[r].x + budget));
-                    rest[p - qb].push_back(make_uint2(comps[r].x + budget, comps[r].y));
-                    budget = 0;
-                }
-            }
-            for (; r < comps.size(); ++r) rest[p - qb].push_back(comps[r]);
-            for (const uint2& x : rest[p - qb]) rest_total += x.y - x.x;
-            if (first.empty()) continue;
-            for (uint32_t b = offc[p]; b < offc[p + 1]; b += tile) A.add(b, std::min(offc[p + 1], b + tile), first);
+            slice(lists[p - qb], 0, head, sub);
+            if (sub.empty()) continue;
+            for (uint32_t b = offc[p]; b < offc[p + 1]; b += tile) A.add(b, std::min(offc[p + 1], b + tile), sub);
         }
         A.order();
         relsky(D, A, base, cq, sq);
-        if (!rest_total) return;
-        // dense lists of the live candidates, per partition
+        if (maxlen <= head) return;
+
         const uint32_t cb = offc[qb], cn = offc[qe] - cb;
         uint32_t* pos = dev<uint32_t>(S_POS, cn);
-        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
-        scan_live(base.dead + cb, pos, cn);
-        launch_count_total(pos, base.dead + cb, cn, misc + M_TOTAL, st_);
-        const uint32_t np = qe - qb;
         uint32_t* hrel = stage<uint32_t>(np + 2);
         for (uint32_t p = qb; p <= qe; ++p) hrel[p - qb] = offc[p] - cb;
         uint32_t* drel = dev<uint32_t>(S_OFF_C, np + 1);
         uint32_t* dnew = dev<uint32_t>(S_SIZES, np + 1);
-        SKY_CUDA(cudaMemcpyAsync(drel, hrel, (np + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
-        launch_remap_offsets(drel, np, pos, base.dead + cb, cn, dnew, st_);
         uint32_t* dense = dev<uint32_t>(S_DENSE, cn);
-        launch_compact_pos(base.dead + cb, pos, cn, cb, dense, st_);
-        count(4);
-        uint32_t* hnew = pin<uint32_t>(P_RUNS, np + 1);
-        SKY_CUDA(cudaMemcpyAsync(hnew, dnew, (np + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
-        sync();
-        std::vector<uint32_t> doff(hnew, hnew + np + 1);
-        Plan B;
-        B.tile = tile;
-        B.chunk = chunk;
-        for (uint32_t p = qb; p < qe; ++p) {
-            const auto& rr = rest[p - qb];
-            if (rr.empty()) continue;
-            const uint32_t b0 = doff[p - qb], e0 = doff[p - qb + 1];
-            for (uint32_t b = b0; b < e0; b += tile) B.add(b, std::min(e0, b + tile), rr);
+        uint32_t* nitems = dev<uint32_t>(S_MISC, 64) + M_NITEMS;
+        SKY_CUDA(cudaMemcpyAsync(drel, hrel, (np + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        std::vector<uint64_t> lens(np, 0);
+        for (uint32_t k = 0; k < np; ++k)
+            for (const uint2& r : lists[k]) lens[k] += r.y - r.x;
+        for (uint64_t lo = head, len = 3ull * head; lo < maxlen; lo += len, len *= 4) {
+            // split further only while the rest is worth a compaction pass
+            uint64_t rest = 0;
+            for (uint32_t k = 0; k < np; ++k)
+                if (lens[k] > lo) rest += (uint64_t)(offc[qb + k + 1] - offc[qb + k]) * (lens[k] - lo);
+            if (rest < kWaveSplitPairs) len = maxlen - lo;
+            const uint64_t hi = lo + len;
+            // this wave's comparator groups per partition (host: the lists are static)
+            std::vector<uint2> ranges, groups;
+            std::vector<uint32_t> gb(np + 1, 0);
+            uint32_t max_groups = 0;
+            uint64_t cap = 0;
+            for (uint32_t p = qb; p < qe; ++p) {
+                slice(lists[p - qb], lo, hi, sub);
+                uint32_t ng = 0, acc = 0, lb = (uint32_t)ranges.size();
+                for (const uint2& r : sub) {
+                    for (uint32_t b = r.x; b < r.y;) {
+                        const uint32_t take = std::min(r.y - b, chunk - acc);
+                        ranges.push_back(make_uint2(b, b + take));
+                        b += take;
+                        acc += take;
+                        if (acc >= chunk) {
+                            groups.push_back(make_uint2(lb, (uint32_t)ranges.size()));
+                            lb = (uint32_t)ranges.size();
+                            acc = 0;
+                            ++ng;
+                        }
+                    }
+                }
+                if ((uint32_t)ranges.size() > lb) {
+                    groups.push_back(make_uint2(lb, (uint32_t)ranges.size()));
+                    ++ng;
+                }
+                gb[p - qb + 1] = gb[p - qb] + ng;
+                max_groups = std::max(max_groups, ng);
+                cap += (uint64_t)ng * ((offc[p + 1] - offc[p] + tile - 1) / tile);
+            }
+            if (!cap) continue;
+            // dense lists of the candidates still alive
+            scan_live(base.dead + cb, pos, cn);
+            launch_remap_offsets(drel, np, pos, base.dead + cb, cn, dnew, st_);
+            launch_compact_pos(base.dead + cb, pos, cn, cb, dense, st_);
+            count(4);
+            uint2* hr = stage<uint2>(ranges.size());
+            std::memcpy(hr, ranges.data(), ranges.size() * sizeof(uint2));
+            uint2* hg = stage<uint2>(groups.size());
+            std::memcpy(hg, groups.data(), groups.size() * sizeof(uint2));
+            uint32_t* hgb = stage<uint32_t>(np + 1);
+            std::memcpy(hgb, gb.data(), (np + 1) * sizeof(uint32_t));
+            uint2* dr = dev<uint2>(S_RANGES, ranges.size());
+            uint2* dg = dev<uint2>(S_GROUPS, groups.size());
+            uint32_t* dgb = dev<uint32_t>(S_GB, np + 1);
+            Item* di = dev<Item>(S_ITEMS, cap);
+            SKY_CUDA(cudaMemcpyAsync(dr, hr, ranges.size() * sizeof(uint2), cudaMemcpyHostToDevice, st_));
+            SKY_CUDA(cudaMemcpyAsync(dg, hg, groups.size() * sizeof(uint2), cudaMemcpyHostToDevice, st_));
+            SKY_CUDA(cudaMemcpyAsync(dgb, hgb, (np + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+            launch_plan_items(dnew, np, dgb, dg, max_groups, tile, di, nitems, st_);
+            count();
+            relsky_dev(D, tile, base, cq, sq, dense, di, (uint32_t)cap, nitems, dr);
         }
-        B.order();
-        relsky(D, B, base, cq, sq, dense);
+    }
+
+    // One relsky launch over device-built items (count in device memory).
+    void relsky_dev(int D, uint32_t tile, const RelskyArgs& base, const uint2* cq, const uint2* sq,
+                    const uint32_t* dense, const Item* items, uint32_t cap, const uint32_t* n_items_dev,
+                    const uint2* ranges) {
+        if (x64_.x && (!base.sid || !base.cid))
+            throw Error(SKY_E_INTERNAL, "FP64 confirmation needs the row ids of both sets");
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        SKY_CUDA(cudaMemsetAsync(misc + M_WORK, 0, sizeof(uint32_t), st_));
+        Relsky2Args b{};
+        b.cidx = dense;
+        b.cxyz = base.cxyz; b.cskey = base.cskey; b.cqc = cq;
+        b.x64 = x64_; b.cid = base.cid; b.sid = base.sid;
+        b.sxyz = base.sxyz; b.sskey = base.sskey; b.sqc = sq;
+        b.items = items; b.n_items = cap; b.n_items_dev = n_items_dev; b.ranges = ranges;
+        b.bounded = base.bounded; b.dead = base.dead;
+        b.tests = base.tests; b.counter = misc + M_WORK;
+        const int phase = base.tests ? (int)(base.tests - tests(0)) : 3;
+        b.coarse_hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + phase;
+        dom_begin();
+        launch_relsky2(D, (int)tile, b, c_->sm_count, st_);
+        dom_end();
+        count();
     }
 
     // CUDA events around each dominance launch; summed once the run drained

@@ -177,9 +177,17 @@ struct Relsky2Args {
     X64 x64;                  // FP64 confirmation
     const uint32_t* cid;      // row id of each candidate position
     const uint32_t* sid;      // row id of each comparator position
+    const uint32_t* n_items_dev;  // optional: item count in device memory (n_items = capacity)
 };
 // tile = candidates per item (<= 32 * 8, one warp); picks K from it.
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);
+// Items of a relsky wave built on the device from the dense candidate
+// offsets of np partitions (dnew[np+1], relative to the dense list) and each
+// partition's comparator groups (groups[gb[p]..gb[p+1]) = (lb, le) into the
+// wave's range array): tiles of `tile` candidates x groups, group-major.
+// *count = items written (<= cap).
+void launch_plan_items(const uint32_t* dnew, uint32_t np, const uint32_t* gb, const uint2* groups, uint32_t max_groups,
+                       uint32_t tile, Item* items, uint32_t* count, cudaStream_t st);
 
 // BNL local skylines: one CTA per partition segment, window capped at
 // `window` points in shared memory; partition input in scan order.

@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
         if (threadIdx.x < 32) sm.deadmask[threadIdx.x] = 0;
         __syncthreads();
         const uint32_t item = sm.item;
-        if (item >= a.n_items) break;
+        if (item >= (a.n_items_dev ? *a.n_items_dev : a.n_items)) break;
         const Item it = a.items[item];
 
         uint32_t T[K][2];
@@ -325,17 +325,13 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                     }
                 };
                 // 4 comparators x K candidates per step, one max-fold and
-                // one branch; the next step's codes are loaded ahead
+                // one branch. Two register buffers alternate, each loaded one
+                // step ahead, so no codes are copied between steps.
                 const uint4* cq = reinterpret_cast<const uint4*>(&sm.code[warp][0]);
                 const uint32_t nb = (lim + 3) & ~3u;
-                uint4 c01 = cq[0], c23 = cq[1];
-                for (uint32_t i = 0; i < nb; i += 4) {
+                auto step = [&](uint32_t i, const uint4 c01, const uint4 c23) {
                     const uint2 q[4] = {make_uint2(c01.x, c01.y), make_uint2(c01.z, c01.w),
                                         make_uint2(c23.x, c23.y), make_uint2(c23.z, c23.w)};
-                    if (i + 4 < nb) {
-                        c01 = cq[(i + 4) / 2];
-                        c23 = cq[(i + 4) / 2 + 1];
-                    }
                     uint32_t h[4 * K];
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
@@ -348,6 +344,19 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
                             if (any_coarse_pass<G, K>(T, qc)) exact(i + c, qc);
                         }
                     }
+                };
+                // comparators past lim carry never-pass codes, so the loop
+                // runs whole pairs of steps (32 is a multiple of 8)
+                const uint32_t nb8 = (nb + 7) & ~7u;
+                uint4 a01 = cq[0], a23 = cq[1];
+                for (uint32_t i = 0; i < nb8; i += 8) {
+                    const uint4 b01 = cq[(i + 4) / 2], b23 = cq[(i + 4) / 2 + 1];
+                    step(i, a01, a23);
+                    if (i + 8 < nb8) {
+                        a01 = cq[(i + 8) / 2];
+                        a23 = cq[(i + 8) / 2 + 1];
+                    }
+                    step(i + 4, b01, b23);
                 }
                 ntests += (unsigned long long)__popc(alive) * lim;
                 live = __any_sync(FULL, alive != 0);
@@ -975,6 +984,43 @@ void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, flo
 void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st, const uint32_t* n_dev) {
     if (!s.n) return;
     SKY_DISPATCH_D16(D, (k_encode<DT><<<ceil_div(s.n, 256), 256, 0, st>>>(s, thr, n_dev)));
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void __launch_bounds__(1024) k_plan_items(const uint32_t* __restrict__ dnew, uint32_t np,
+                                                     const uint32_t* __restrict__ gb, const uint2* __restrict__ groups,
+                                                     uint32_t max_groups, uint32_t tile, Item* __restrict__ items,
+                                                     uint32_t* count) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    uint32_t base = 0;
+    for (uint32_t j = 0; j < max_groups; ++j) {
+        for (uint32_t p0 = 0; p0 < np; p0 += 1024) {
+            const uint32_t p = p0 + threadIdx.x;
+            uint32_t nt = 0, b = 0, e = 0;
+            uint2 g = make_uint2(0, 0);
+            if (p < np && j < gb[p + 1] - gb[p]) {
+                b = dnew[p];
+                e = dnew[p + 1];
+                nt = (e - b + tile - 1) / tile;
+                g = groups[gb[p] + j];
+            }
+            uint32_t off, total;
+            Scan(tmp).ExclusiveSum(nt, off, total);
+            for (uint32_t t = 0; t < nt; ++t) {
+                const uint32_t cb = b + t * tile;
+                items[base + off + t] = Item{cb, min(cb + tile, e), g.x, g.y};
+            }
+            base += total;
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) *count = base;
+}
+
+void launch_plan_items(const uint32_t* dnew, uint32_t np, const uint32_t* gb, const uint2* groups, uint32_t max_groups,
+                       uint32_t tile, Item* items, uint32_t* count, cudaStream_t st) {
+    k_plan_items<<<1, 1024, 0, st>>>(dnew, np, gb, groups, max_groups, tile, items, count);
     SKY_LAUNCH_CHECK();
 }
 
