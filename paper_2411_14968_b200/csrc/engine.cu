@@ -362,12 +362,12 @@ class Runner {
         count(4);
     }
     template <class K>
-    void sort_keys(const K* kin, K* kout, uint32_t n) {
+    void sort_keys(const K* kin, K* kout, uint32_t n, int end_bit = 8 * sizeof(K)) {
         if (!n) return;
         size_t bytes = 0;
-        SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kin, kout, (int)n, 0, (int)(8 * sizeof(K)), st_));
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kin, kout, (int)n, 0, end_bit, st_));
         void* tmp = c_->dev.get(S_CUB, bytes);
-        SKY_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, kin, kout, (int)n, 0, (int)(8 * sizeof(K)), st_));
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, kin, kout, (int)n, 0, end_bit, st_));
         count(4);
     }
     struct NotDead {
@@ -715,7 +715,7 @@ class Runner {
                                    c_->comm, st_));
         }
         SKY_NCCL(ncclGroupEnd());
-        sort_keys(all, out, total);
+        sort_keys(all, out, total, 32);
         return total;
     }
 
@@ -1552,7 +1552,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     uint32_t nf = nmine;
     uint32_t* final_ids = idsB;
     if (W == 1) {
-        R.sort_keys(idsA, idsB, nf);
+        R.sort_keys(idsA, idsB, nf, std::max(1, bits_for(n)));  // ids < n
     } else {
         nf = R.gather_ids(idsA, nmine, idsB);  // all ranks' survivors, then sorted
         final_ids = idsB;

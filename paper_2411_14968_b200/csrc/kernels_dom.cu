@@ -226,15 +226,25 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 
         uint32_t T[K][2];
         uint32_t alive = 0, my_max = 0;
+        // three rounds of independent loads (positions, dead flags, codes +
+        // keys) instead of K dependent chains
+        uint32_t cpos[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const uint32_t slot = it.cb + k * 32 + lane;
+            cpos[k] = slot < it.ce ? (a.cidx ? a.cidx[slot] : slot) : kNone;  // dense candidate lists
+        }
+        bool slot_live[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) slot_live[k] = cpos[k] != kNone && !a.dead[cpos[k]];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
             // empty / dead slot: lane guards set (no borrow can reach bit 31),
             // alive guard clear -> never passes
             T[k][0] = G;
             T[k][1] = G | 0x80000000u;
-            const uint32_t c = (slot < it.ce && a.cidx) ? a.cidx[slot] : slot;  // dense candidate lists
-            if (slot < it.ce && !a.dead[c]) {
+            if (slot_live[k]) {
+                const uint32_t c = cpos[k];
                 alive |= 1u << k;
                 const uint2 q = a.cqc[c];
                 T[k][0] = q.x | G | CodeLayout<D>::ALIVE;
@@ -792,11 +802,16 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
 #pragma unroll
             for (int k = 0; k < 8; ++k) h[k] = coarse_hit<G>(Tl, q[k]);
             if (alive) nt += min(8u, nrep - r);
-            if (max_fold<8>(h) == (G | 0x80000000u)) {
-#pragma unroll 1
-                for (int k = 0; k < 8; ++k) {
-                    if (alive && coarse_pass<G>(Tl, q[k]) &&
-                        dom_f4x<D>(s_rep + (r + k) * V, t, x64, x64.x ? rep_id[r + k] : 0, row)) {
+            constexpr uint32_t GA = G | 0x80000000u;
+            if (max_fold<8>(h) == GA) {
+                // exact checks for the representatives whose codes passed
+                uint32_t m = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) m |= (h[k] == GA ? 1u : 0u) << k;
+                while (m && alive) {
+                    const int k = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (dom_f4x<D>(s_rep + (r + k) * V, t, x64, x64.x ? rep_id[r + k] : 0, row)) {
                         alive = false;
                         Tl[0] &= ~CodeLayout<D>::ALIVE;
                     }
@@ -991,27 +1006,49 @@ __global__ void __launch_bounds__(1024) k_plan_items(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ gb, const uint2* __restrict__ groups,
                                                      uint32_t max_groups, uint32_t tile, Item* __restrict__ items,
                                                      uint32_t* count) {
+    // One CTA, one thread per partition (chunks of 1024). Per group level j:
+    // a block scan of the tile counts of the partitions that have a j-th
+    // group, then every thread writes items, each located by binary search
+    // over the scanned offsets in shared memory.
     using Scan = cub::BlockScan<uint32_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_off[1024], s_b[1024], s_e[1024], s_g[1024];
+    __shared__ uint32_t s_total;
+    constexpr uint32_t kGroupsSmem = 2048;
+    __shared__ uint2 s_groups[kGroupsSmem];  // all groups when they fit (the usual case)
+    const uint32_t ngroups = gb[np];
+    const bool cached = ngroups <= kGroupsSmem;
+    if (cached)
+        for (uint32_t i = threadIdx.x; i < ngroups; i += 1024) s_groups[i] = groups[i];
     uint32_t base = 0;
-    for (uint32_t j = 0; j < max_groups; ++j) {
-        for (uint32_t p0 = 0; p0 < np; p0 += 1024) {
-            const uint32_t p = p0 + threadIdx.x;
-            uint32_t nt = 0, b = 0, e = 0;
-            uint2 g = make_uint2(0, 0);
-            if (p < np && j < gb[p + 1] - gb[p]) {
-                b = dnew[p];
-                e = dnew[p + 1];
-                nt = (e - b + tile - 1) / tile;
-                g = groups[gb[p] + j];
-            }
+    for (uint32_t p0 = 0; p0 < np; p0 += 1024) {
+        const uint32_t p = p0 + threadIdx.x, np_here = min(1024u, np - p0);
+        uint32_t tiles = 0, ng = 0;
+        if (p < np) {
+            s_b[threadIdx.x] = dnew[p];
+            s_e[threadIdx.x] = dnew[p + 1];
+            s_g[threadIdx.x] = gb[p];
+            ng = gb[p + 1] - gb[p];
+            tiles = (s_e[threadIdx.x] - s_b[threadIdx.x] + tile - 1) / tile;
+        }
+        for (uint32_t j = 0; j < max_groups; ++j) {
             uint32_t off, total;
-            Scan(tmp).ExclusiveSum(nt, off, total);
-            for (uint32_t t = 0; t < nt; ++t) {
-                const uint32_t cb = b + t * tile;
-                items[base + off + t] = Item{cb, min(cb + tile, e), g.x, g.y};
+            Scan(tmp).ExclusiveSum(j < ng ? tiles : 0u, off, total);
+            s_off[threadIdx.x] = off;
+            if (threadIdx.x == 0) s_total = total;
+            __syncthreads();
+            for (uint32_t x = threadIdx.x; x < s_total; x += 1024) {
+                uint32_t lo = 0, hi = np_here;  // last q with s_off[q] <= x
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (s_off[mid] <= x) lo = mid; else hi = mid;
+                }
+                const uint32_t t = x - s_off[lo];
+                const uint2 g = cached ? s_groups[s_g[lo] + j] : groups[s_g[lo] + j];
+                const uint32_t cb = s_b[lo] + t * tile;
+                items[base + x] = Item{cb, min(cb + tile, s_e[lo]), g.x, g.y};
             }
-            base += total;
+            base += s_total;
             __syncthreads();
         }
     }
