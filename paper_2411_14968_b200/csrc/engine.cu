@@ -76,7 +76,8 @@ enum Slot {
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
-    S_SCAN, S_PTS64, S_GROUPS, S_GB, S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
+    S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JCNT2, S_JPRE2, S_JOBS, S_DEAD1, S_OFF_D, S_DNEW,
+    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -87,10 +88,14 @@ constexpr uint32_t kBlock = 512;    // local block-skyline size
 // candidate x comparator pairs (before bounding) below which the remaining
 // comparators of a multi-wave relsky run as one last wave
 constexpr uint64_t kWaveSplitPairs = 8ull << 30;
+// above this many input rows the single-GPU path reads the filtered count
+// back before sizing the downstream sets by it
+constexpr uint32_t kExactCapRows = 0;
 
 // misc device words
 enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_NITEMS = 7, M_TESTS = 8 /* 4 x u64 */,
-       M_HITS = 16 /* 4 x u64, per phase */ };
+       M_HITS = 16 /* 4 x u64, per phase */,
+       M_S0 = 24, M_S1 = 25, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;
@@ -352,6 +357,15 @@ class Runner {
         }
     }
 
+    // the same with the set's row count in device memory (s.n = capacity)
+    void encode_dev(int D, DevSet& s, const uint32_t* n_dev) {
+        if (D > 16 || !s.n) return;
+        float* thr = dev<float>(S_THR, (size_t)D * (kCodeLevels - 1));
+        launch_thresholds(D, s, thr, st_, n_dev);
+        launch_encode(D, s, thr, st_, n_dev);
+        count(2);
+    }
+
     template <class K, class V>
     void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint32_t n, int bb, int eb) {
         if (!n) return;
@@ -405,6 +419,137 @@ class Runner {
         launch_scatter_direct(D, in, dead, pos, out, st_);
         count();
         return out;
+    }
+
+    // Compaction with the count kept on the device: `in` has in.n slots (a
+    // capacity; slots at or past the live count must be flagged dead). The
+    // result has n = in.n slots, offsets off_out and *total live rows.
+    DevSet compact_dev(const DevSet& in, const uint8_t* dead, const uint32_t* off_in, uint32_t P, int out_base,
+                       uint32_t* off_out, uint32_t* total, int D) {
+        uint32_t* pos = dev<uint32_t>(S_POS, in.n);
+        scan_live(dead, pos, in.n);
+        launch_count_total(pos, dead, in.n, total, st_);
+        launch_remap_offsets(off_in, P, pos, dead, in.n, off_out, st_);
+        DevSet out = set(out_base, in.n, D);
+        launch_scatter_direct(D, in, dead, pos, out, st_);
+        count(3);
+        return out;
+    }
+
+    // exclusive scan of n_plus1 words (the last output = the total)
+    void scan_u32(const uint32_t* in, uint32_t* out, uint32_t n_plus1) {
+        size_t bytes = 0;
+        SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n_plus1, st_));
+        void* tmp = c_->dev.get(S_CUB, bytes);
+        SKY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)n_plus1, st_));
+        count(2);
+    }
+
+    // Direct items of device-built jobs; *n_items points at the device count.
+    Item* expand_jobs(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, uint32_t tile, uint32_t chunk,
+                      uint32_t max_chunks, uint64_t item_cap, const uint32_t** n_items) {
+        uint32_t* cnt = dev<uint32_t>(S_JCNT, cap + 1);
+        uint32_t* pre = dev<uint32_t>(S_JPRE, cap + 1);
+        launch_job_counts(jobs, n_jobs, cap, tile, chunk, max_chunks, cnt, st_);
+        scan_u32(cnt, pre, cap + 1);
+        Item* items = dev<Item>(S_ITEMS, item_cap);
+        launch_job_items(jobs, n_jobs, cap, pre, tile, chunk, max_chunks, items, st_);
+        count(2);
+        *n_items = pre + cap;
+        return items;
+    }
+
+    // One relsky launch over device-built direct items.
+    void relsky_direct(int D, uint32_t tile, const RelskyArgs& base, const uint2* cq, const uint2* sq,
+                       const uint32_t* dense, const Item* items, uint64_t cap, const uint32_t* n_items_dev) {
+        if (x64_.x && (!base.sid || !base.cid))
+            throw Error(SKY_E_INTERNAL, "FP64 confirmation needs the row ids of both sets");
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        SKY_CUDA(cudaMemsetAsync(misc + M_WORK, 0, sizeof(uint32_t), st_));
+        Relsky2Args b{};
+        b.cidx = dense;
+        b.cxyz = base.cxyz; b.cskey = base.cskey; b.cqc = cq;
+        b.x64 = x64_; b.cid = base.cid; b.sid = base.sid;
+        b.sxyz = base.sxyz; b.sskey = base.sskey; b.sqc = sq;
+        b.items = items; b.n_items = (uint32_t)std::min<uint64_t>(cap, 0xFFFFFFFFu); b.n_items_dev = n_items_dev;
+        b.direct = true;
+        b.bounded = base.bounded; b.dead = base.dead;
+        b.tests = base.tests; b.counter = misc + M_WORK;
+        const int phase = base.tests ? (int)(base.tests - tests(0)) : 3;
+        b.coarse_hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + phase;
+        dom_begin();
+        launch_relsky2(D, (int)tile, b, c_->sm_count, st_);
+        dom_end();
+        count();
+    }
+
+    // Local SFS with every count on the device (single GPU): the block stage
+    // and both waves are planned by kernels from device offsets, so no host
+    // round trip until the union's offsets are read by the caller.
+    //   s0: n = capacity, *n0 live rows, partitions off0_dev[P+1].
+    DevSet local_sfs_dev(int D, const DevSet& s0, const uint32_t* n0, const uint32_t* off0_dev, uint32_t P,
+                         uint32_t* off_u_dev, uint32_t* n_u, bool count_tests) {
+        const uint32_t cap = s0.n;
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        uint8_t* dead = dev<uint8_t>(S_DEAD, cap);
+        launch_fill_u8(dead, 0, cap, st_);
+        launch_fill_tail_u8(dead, 1, n0, cap, st_);
+        count();
+        RelskyArgs a{};
+        a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
+        a.sxyz = s0.xyz; a.sskey = s0.skey; a.bounded = true; a.dead = dead;
+        a.cid = s0.id; a.sid = s0.id;
+        a.tests = count_tests ? tests(1) : nullptr;
+        // block stage: 512-row blocks of every partition against themselves
+        const uint32_t bt = 256;
+        const uint32_t jcap = (cap + kBlock - 1) / kBlock + P;
+        uint32_t* bc = dev<uint32_t>(S_JCNT2, P + 1);
+        uint32_t* bp = dev<uint32_t>(S_JPRE2, P + 1);
+        launch_block_counts(off0_dev, P, kBlock, bc, st_);
+        scan_u32(bc, bp, P + 1);
+        Job* jobs = dev<Job>(S_JOBS, std::max<uint32_t>(jcap, P));
+        launch_block_jobs(off0_dev, P, kBlock, bp, jobs, st_);
+        count(2);
+        const uint32_t* n_items = nullptr;
+        Item* items = expand_jobs(jobs, bp + P, jcap, bt, kBlock, 1, (uint64_t)jcap * (kBlock / bt), &n_items);
+        relsky_direct(D, bt, a, s0.qc, s0.qc, nullptr, items, (uint64_t)jcap * (kBlock / bt), n_items);
+
+        uint32_t* off1 = dev<uint32_t>(S_OFF_D, P + 1);
+        uint32_t* n1 = misc + M_S1;
+        DevSet s1 = compact_dev(s0, dead, off0_dev, P, S_SET1, off1, n1, D);
+        uint8_t* dead1 = dev<uint8_t>(S_DEAD1, cap);
+        launch_fill_u8(dead1, 0, cap, st_);
+        launch_fill_tail_u8(dead1, 1, n1, cap, st_);
+        count();
+        RelskyArgs b2 = a;
+        b2.cxyz = s1.xyz; b2.cskey = s1.skey; b2.sxyz = s1.xyz; b2.sskey = s1.skey; b2.dead = dead1;
+        b2.cid = s1.id; b2.sid = s1.id;
+        // grain from the capacity: ~ rows per partition
+        const uint64_t per = (uint64_t)cap / std::max<uint32_t>(1, P);
+        const uint32_t tile = per >= 2048 ? 256 : (per >= 512 ? 128 : 64);
+        const uint32_t chunk = 2048, max_chunks = 64, head = 2048;
+        const uint64_t icap = ((uint64_t)cap / tile + P) * max_chunks;
+        uint32_t* np_dev = misc + M_NP;
+        uint32_t* hp = stage<uint32_t>(1);
+        *hp = P;
+        SKY_CUDA(cudaMemcpyAsync(np_dev, hp, sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        // wave 0: every row of a partition against the partition's first `head` rows
+        launch_partition_jobs(off1, off1, nullptr, P, 0, head, jobs, st_);
+        count();
+        items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+        relsky_direct(D, tile, b2, s1.qc, s1.qc, nullptr, items, icap, n_items);
+        // wave 1: the live rows (dense lists) against the rest of their partition
+        uint32_t* pos = dev<uint32_t>(S_POS, cap);
+        uint32_t* dnew = dev<uint32_t>(S_DNEW, P + 1);
+        uint32_t* dense = dev<uint32_t>(S_DENSE, cap);
+        scan_live(dead1, pos, cap);
+        launch_remap_offsets(off1, P, pos, dead1, cap, dnew, st_);
+        launch_compact_pos(dead1, pos, cap, 0, dense, st_);
+        launch_partition_jobs(dnew, off1, nullptr, P, head, ~0ull, jobs, st_);
+        count(3);
+        items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+        relsky_direct(D, tile, b2, s1.qc, s1.qc, dense, items, icap, n_items);
+        return compact_dev(s1, dead1, off1, P, S_SET2, off_u_dev, n_u, D);
     }
 
     void relsky(int D, const Plan& plan, const RelskyArgs& base, const uint2* cq = nullptr,
@@ -800,7 +945,8 @@ class Runner {
 
     // BNL local skylines (k_bnl), window capped at cfg.bnl_window_cap.
     DevSet local_bnl(int D, const DevSet& s0, uint32_t* off0_dev, uint32_t P, uint32_t window, uint32_t* off_u_dev,
-                     std::vector<uint32_t>& off_u, bool count_tests, uint32_t* used_window) {
+                     std::vector<uint32_t>& off_u, bool count_tests, uint32_t* used_window,
+                     uint32_t* n_u = nullptr) {
         uint8_t* dead = dev<uint8_t>(S_DEAD, s0.n);
         launch_fill_u8(dead, 1, s0.n, st_);
         const bool packed = D <= 16 && s0.qc;
@@ -833,6 +979,9 @@ class Runner {
             dom_end();
             count();
         }
+        // rows past the live count stay dead (the fill above), so a capacity-
+        // sized set compacts with the count on the device
+        if (n_u) return compact_dev(s0, dead, off0_dev, P, S_SET2, off_u_dev, n_u, D);
         return compact(s0, dead, off0_dev, P, S_SET2, off_u_dev, off_u, D);
     }
 
@@ -1370,10 +1519,55 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     }
 
     // materialize the surviving rows in (pid, sum key) order
+    const int W = c->world, rank = c->rank;
     std::vector<uint32_t> off1;
     uint32_t* off1_dev = R.dev<uint32_t>(S_OFF_B, P + 1);
     DevSet s0;
-    {
+    std::vector<uint32_t> offu;
+    uint32_t* offu_dev = R.dev<uint32_t>(S_OFF_A, P + 1);
+    DevSet U;
+    std::vector<uint32_t> pr(2, 0);
+    pr[1] = P;
+    if (W == 1) {
+        // Single GPU: every count stays on the device until the union of the
+        // local skylines is known (one host round trip for this phase).
+        uint32_t* pos = R.dev<uint32_t>(S_POS, n);
+        R.scan_live(dead, pos, n);
+        launch_count_total(pos, dead, n, misc + M_S0, st);
+        launch_remap_offsets(po.off, P, pos, dead, n, off1_dev, st);
+        R.count(2);
+        // capacity of the filtered set: n, or for large inputs the exact
+        // count (one early round trip), so later passes are not sized by n
+        uint32_t cap0 = n;
+        if (n > kExactCapRows) {
+            uint32_t* hc = R.pin<uint32_t>(P_MISC, 8);
+            SKY_CUDA(cudaMemcpyAsync(hc, misc + M_S0, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            R.sync();
+            cap0 = hc[0];
+        }
+        s0 = R.set(S_SET0, cap0, D);
+        launch_scatter_indirect(D, pts, d, po.idx, po.key64, n, dead, pos, s0, st);
+        R.count();
+        R.encode_dev(D, s0, misc + M_S0);
+        if (cfg->local_algo == SKY_LOCAL_BNL) {
+            uint32_t used = 0;
+            std::vector<uint32_t> unused;
+            U = R.local_bnl(D, s0, off1_dev, P, cfg->bnl_window_cap, offu_dev, unused, count_tests, &used,
+                            misc + M_U);
+        } else {
+            U = R.local_sfs_dev(D, s0, misc + M_S0, off1_dev, P, offu_dev, misc + M_U, count_tests);
+        }
+        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32);
+        SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        const uint32_t* hmisc = h + P + 1;
+        check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
+        if (cfg->filter == SKY_FILTER_REPRESENTATIVE) out->n_reps = hmisc[M_NREP];
+        rep_filtered = (uint64_t)n - hmisc[M_S0] - grid_filtered;
+        offu.assign(h, h + P + 1);
+        U.n = hmisc[M_U];
+    } else {
         uint32_t* pos = R.dev<uint32_t>(S_POS, n);
         R.scan_live(dead, pos, n);
         launch_count_total(pos, dead, n, misc + M_TOTAL, st);
@@ -1394,40 +1588,30 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         R.count();
         rep_filtered = (uint64_t)n - total - grid_filtered;
         R.encode(D, s0);
-    }
-    out->filtered_count = grid_filtered + rep_filtered;
 
-    // ----------------------------------------------------- local skylines
-    // Multi-GPU: every rank holds the same s0 (phase 1a above is replicated);
-    // the local phase is sharded by contiguous, cost-balanced partition
-    // ranges, and the local skylines are all-gathered over NCCL.
-    const int W = c->world, rank = c->rank;
-    std::vector<uint32_t> pr = plan_local_shards(off1, P, W);
-    const uint32_t pb = pr[rank], pe = pr[rank + 1];
-    std::vector<uint32_t> offu;
-    uint32_t* offu_dev = R.dev<uint32_t>(S_OFF_A, P + 1);
-    DevSet U;
-    {
+        // ----------------------------------------------------- local skylines
+        // Multi-GPU: every rank holds the same s0 (phase 1a above is
+        // replicated); the local phase is sharded by contiguous, cost-balanced
+        // partition ranges, and the local skylines are all-gathered over NCCL.
+        pr = plan_local_shards(off1, P, W);
+        const uint32_t pb = pr[rank], pe = pr[rank + 1];
         // view of this rank's partitions
         const uint32_t base = off1[pb], cnt = off1[pe] - base;
         const int D4 = (D + 3) / 4 * 4;
         DevSet mine = s0;
-        if (W > 1) {
-            mine.xyz = s0.xyz + (size_t)base * D4;
-            mine.skey = s0.skey + base;
-            mine.id = s0.id + base;
-            mine.qc = s0.qc ? s0.qc + base : nullptr;
-            mine.n = cnt;
-        }
+        mine.xyz = s0.xyz + (size_t)base * D4;
+        mine.skey = s0.skey + base;
+        mine.id = s0.id + base;
+        mine.qc = s0.qc ? s0.qc + base : nullptr;
+        mine.n = cnt;
         const uint32_t Pm = pe - pb;
         std::vector<uint32_t> offm(Pm + 1);
         for (uint32_t k = 0; k <= Pm; ++k) offm[k] = off1[pb + k] - base;
-        uint32_t* offm_dev = off1_dev;
-        if (W > 1) {
-            offm_dev = R.dev<uint32_t>(S_OFF_C, Pm + 1);
-            uint32_t* h = R.stage<uint32_t>(Pm + 1);
-            std::memcpy(h, offm.data(), (Pm + 1) * sizeof(uint32_t));
-            SKY_CUDA(cudaMemcpyAsync(offm_dev, h, (Pm + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        uint32_t* offm_dev = R.dev<uint32_t>(S_OFF_C, Pm + 1);
+        {
+            uint32_t* hs = R.stage<uint32_t>(Pm + 1);
+            std::memcpy(hs, offm.data(), (Pm + 1) * sizeof(uint32_t));
+            SKY_CUDA(cudaMemcpyAsync(offm_dev, hs, (Pm + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
         }
         std::vector<uint32_t> offum;
         DevSet Um;
@@ -1437,13 +1621,9 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         } else {
             Um = R.local_sfs(D, mine, offm, offm_dev, Pm, offu_dev, offum, count_tests);
         }
-        if (W == 1) {
-            U = Um;
-            offu = offum;
-        } else {
-            U = R.gather_union(D, Um, offum, pr, P, offu, offu_dev);
-        }
+        U = R.gather_union(D, Um, offum, pr, P, offu, offu_dev);
     }
+    out->filtered_count = grid_filtered + rep_filtered;
     SKY_CUDA(cudaEventRecord(c->ev[2], st));
     for (uint32_t p = 0; p < P; ++p) out->local_skyline_sizes[p] = offu[p + 1] - offu[p];
     out->union_size = U.n;

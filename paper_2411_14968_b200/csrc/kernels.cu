@@ -88,11 +88,38 @@ __global__ void k_prep(PrepArgs a) {
         }
         // hyperspherical_angles: tail sums of squares back to front.
         const double PI = 3.14159265358979323846;
-        double tail = __dmul_rn(X(a.d - 1), X(a.d - 1));
         uint64_t stride_i = 1;
         for (uint32_t k = 0; k + 1 < a.d; ++k) stride_i *= a.m;  // m^(d-2) for i = d-2
+        // FP32 pass first: its slice value is within ~1e-6 relative of the
+        // FP64 one, so a value clear of every interior boundary gives the
+        // same floor; rows that come near one redo the FP64 computation.
+        bool exact64 = false;
+        {
+            const float fm = (float)a.m, tol = 1e-4f * fmaxf(1.0f, fm / 16.0f);
+            float tail32 = xf[a.d - 1] * xf[a.d - 1];
+            uint64_t pid32 = 0, st = stride_i;
+            // squares must stay normal floats for that error bound
+            for (uint32_t j = 0; j < a.d; ++j) {
+                const float xj = xf[j];
+                if (xj != 0.0f && !(xj > 1e-15f && xj < 1e15f)) exact64 = true;
+            }
+            for (uint32_t ii = a.d - 1; ii-- > 0;) {
+                const float xi = xf[ii];
+                const float v = 2.0f * atan2f(sqrtf(tail32), xi) / 3.14159265f * fm;
+                tail32 += xi * xi;
+                const float r = rintf(v);
+                if (r >= 1.0f && r <= fm - 1.0f && fabsf(v - r) <= tol) exact64 = true;
+                uint64_t slice = (uint64_t)fmaxf(v, 0.0f);
+                if (slice >= a.m) slice = a.m - 1;
+                st /= a.m;
+                pid32 += slice * (st ? st : 1);
+            }
+            pid = pid32;
+        }
+        double tail = __dmul_rn(X(a.d - 1), X(a.d - 1));
         bool ambiguous = false;
-        for (uint32_t ii = a.d - 1; ii-- > 0;) {
+        if (exact64) pid = 0;
+        for (uint32_t ii = a.d - 1; exact64 && ii-- > 0;) {
             const double xi = X(ii);
             const double phi = atan2(sqrt(tail), xi);
             tail = __dadd_rn(tail, __dmul_rn(xi, xi));
@@ -507,25 +534,21 @@ void launch_pick_gather(const uint32_t* rows, const uint32_t* gpos, uint32_t slo
 // 66-86, 139-145) finished in one CTA: compact the per-partition picks, sort
 // them by sum key, keep the antichain (brute force, as the reference does),
 // emit them key-sorted with their count in device memory.
-constexpr int REPF_THREADS = 1024, REPF_ITEMS = 2, REPF_MAX = REPF_THREADS * REPF_ITEMS;
+constexpr int REPF_ITEMS = 2, REPF_MAX = 1024 * REPF_ITEMS;
 
-template <int D>
-__global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* __restrict__ cand, uint32_t slots,
-                                                               const float* __restrict__ pts, uint32_t d, DevSet out,
-                                                               uint32_t* out_count, unsigned long long* tests,
-                                                               X64 x64) {
+template <int D, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_rep_finalize(const uint32_t* __restrict__ cand, uint32_t slots,
+                                                          const float* __restrict__ pts, uint32_t d, DevSet out,
+                                                          uint32_t* out_count, unsigned long long* tests, X64 x64) {
     constexpr int V = Dims<D>::V;
-    using Scan = cub::BlockScan<uint32_t, REPF_THREADS>;
-    using Sort = cub::BlockRadixSort<uint32_t, REPF_THREADS, REPF_ITEMS, uint32_t>;
-    __shared__ union {
-        typename Scan::TempStorage scan;
-        typename Sort::TempStorage sort;
-    } tmp;
-    extern __shared__ float4 s_xyz[];  // [REPF_MAX][V], then rows, keys, order, dead flags
-    uint32_t* s_row = reinterpret_cast<uint32_t*>(s_xyz + (size_t)REPF_MAX * V);
-    uint32_t* s_key = s_row + REPF_MAX;
-    uint32_t* s_ord = s_key + REPF_MAX;
-    uint8_t* s_dead = reinterpret_cast<uint8_t*>(s_ord + REPF_MAX);
+    constexpr int MAXN = THREADS * REPF_ITEMS;
+    using Scan = cub::BlockScan<uint32_t, THREADS>;
+    __shared__ typename Scan::TempStorage tmp;
+    extern __shared__ float4 s_xyz[];  // [MAXN][V], then rows, keys, order, dead flags
+    uint32_t* s_row = reinterpret_cast<uint32_t*>(s_xyz + (size_t)MAXN * V);
+    uint32_t* s_key = s_row + MAXN;
+    uint32_t* s_ord = s_key + MAXN;
+    uint8_t* s_dead = reinterpret_cast<uint8_t*>(s_ord + MAXN);
     __shared__ uint32_t s_n;
     const int t = threadIdx.x;
     // 1. compact the picks (slot order = partition order)
@@ -537,7 +560,7 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
         flags[k] = rows[k] != kNone;
     }
     uint32_t offs[REPF_ITEMS], total;
-    Scan(tmp.scan).ExclusiveSum(flags, offs, total);
+    Scan(tmp).ExclusiveSum(flags, offs, total);
 #pragma unroll
     for (int k = 0; k < REPF_ITEMS; ++k)
         if (flags[k]) s_row[offs[k]] = rows[k];
@@ -545,8 +568,9 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
     __syncthreads();
     const uint32_t n = s_n;
     // 2. coordinates and FP64-sum keys
-    for (uint32_t i = t; i < n; i += REPF_THREADS) {
-        const float* x = pts + (size_t)s_row[i] * d;
+    for (uint32_t i = t; i < n; i += THREADS) {
+        const uint32_t r = s_row[i];
+        const float* x = pts + (size_t)r * d;
         float4* dst = s_xyz + (size_t)i * V;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -558,30 +582,22 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
             }
             dst[v] = make_float4(c[0], c[1], c[2], c[3]);
         }
-        const double sum = x64.x ? row_sum(x64.x, d, s_row[i]) : row_sum(pts, d, s_row[i]);
+        const double sum = x64.x ? row_sum(x64.x, d, r) : row_sum(pts, d, r);
         s_key[i] = __float_as_uint(__double2float_rn(sum));
     }
     __syncthreads();
-    // 3. key order
-    uint32_t keys[REPF_ITEMS], vals[REPF_ITEMS];
-#pragma unroll
-    for (int k = 0; k < REPF_ITEMS; ++k) {
-        const uint32_t i = t * REPF_ITEMS + k;
-        keys[k] = i < n ? s_key[i] : 0xFFFFFFFFu;
-        vals[k] = i;
-    }
-    __syncthreads();
-    Sort(tmp.sort).Sort(keys, vals);
-#pragma unroll
-    for (int k = 0; k < REPF_ITEMS; ++k) s_ord[t * REPF_ITEMS + k] = vals[k];
-    __syncthreads();
-    // 4. antichain: brute force over all candidates
+    // 3. key order by ranks (stable: ties keep slot order); the antichain
+    //    test of step 4 runs in the same pass
     unsigned long long nt = 0;
-    for (uint32_t i = t; i < n; i += REPF_THREADS) {
+    for (uint32_t i = t; i < n; i += THREADS) {
+        const uint32_t ki = s_key[i];
         const float4* ti = s_xyz + (size_t)i * V;
+        uint32_t rank = 0;
         bool dom = false;
-        for (uint32_t j = 0; j < n && !dom; ++j) {
-            if (j == i) continue;
+        for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t kj = s_key[j];
+            rank += (kj < ki) | ((kj == ki) & (j < i));
+            if (dom || j == i || kj > ki) continue;  // a dominator has a key <= ki
             ++nt;
             const float4* sj = s_xyz + (size_t)j * V;
             bool gt = false, lt = false;
@@ -593,6 +609,7 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
             }
             dom = !gt && (x64.x ? dom64(x64, s_row[j], s_row[i]) : lt);
         }
+        s_ord[rank] = i;
         s_dead[i] = dom;
     }
     __syncthreads();
@@ -603,7 +620,7 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
         const uint32_t p = t * REPF_ITEMS + k;
         keep[k] = p < n && !s_dead[s_ord[p]];
     }
-    Scan(tmp.scan).ExclusiveSum(keep, kpos, ktot);
+    Scan(tmp).ExclusiveSum(keep, kpos, ktot);
 #pragma unroll
     for (int k = 0; k < REPF_ITEMS; ++k) {
         if (!keep[k]) continue;
@@ -621,14 +638,25 @@ __global__ void __launch_bounds__(REPF_THREADS) k_rep_finalize(const uint32_t* _
     }
 }
 
+template <int D, int THREADS>
+void rep_finalize_launch(const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
+                         uint32_t* out_count, unsigned long long* tests, X64 x64, size_t smem, cudaStream_t st) {
+    SKY_CUDA(cudaFuncSetAttribute(k_rep_finalize<D, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_rep_finalize<D, THREADS><<<1, THREADS, smem, st>>>(cand, slots, pts, d, out, out_count, tests, x64);
+}
+
 bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
                          uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {
     if (slots > (uint32_t)REPF_MAX) return false;
-    const size_t smem = (size_t)REPF_MAX * ((D + 3) / 4) * 16 + (size_t)REPF_MAX * 13 + 64;
-    if (smem + 48 * 1024 > (size_t)smem_optin) return false;
+    const bool small = slots <= 256u * REPF_ITEMS;
+    const size_t maxn = small ? 256u * REPF_ITEMS : (size_t)REPF_MAX;
+    const size_t smem = maxn * ((D + 3) / 4) * 16 + maxn * 13 + 64;
+    if (smem + 16 * 1024 > (size_t)smem_optin) return false;
     SKY_DISPATCH_D(D, {
-        SKY_CUDA(cudaFuncSetAttribute(k_rep_finalize<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_rep_finalize<DT><<<1, REPF_THREADS, smem, st>>>(cand, slots, pts, d, out, out_count, tests, x64);
+        if (small)
+            rep_finalize_launch<DT, 256>(cand, slots, pts, d, out, out_count, tests, x64, smem, st);
+        else
+            rep_finalize_launch<DT, 1024>(cand, slots, pts, d, out, out_count, tests, x64, smem, st);
     });
     SKY_LAUNCH_CHECK();
     return true;
@@ -783,6 +811,17 @@ void launch_compact_pos(const uint8_t* dead, const uint32_t* pos, uint32_t n, ui
 
 void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st) {
     if (n) SKY_CUDA(cudaMemsetAsync(p, v, n, st));
+}
+
+__global__ void k_fill_tail_u8(uint8_t* __restrict__ p, uint8_t v, const uint32_t* __restrict__ count, uint32_t cap) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cap && i >= *count) p[i] = v;
+}
+
+void launch_fill_tail_u8(uint8_t* p, uint8_t v, const uint32_t* count, uint32_t cap, cudaStream_t st) {
+    if (!cap) return;
+    k_fill_tail_u8<<<ceil_div(cap, 256), 256, 0, st>>>(p, v, count, cap);
+    SKY_LAUNCH_CHECK();
 }
 
 __global__ void k_mark_cells_dead(const uint64_t* __restrict__ key64, uint32_t n, const uint8_t* __restrict__ cell_dead,

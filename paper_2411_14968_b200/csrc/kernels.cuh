@@ -118,6 +118,8 @@ void launch_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, ui
 void launch_compact_ids(const uint32_t* id, const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t* out,
                         cudaStream_t st);
 void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st);
+// p[i] = v for *count <= i < cap (the unused tail of a set sized by capacity)
+void launch_fill_tail_u8(uint8_t* p, uint8_t v, const uint32_t* count, uint32_t cap, cudaStream_t st);
 // out[pos[i]] = base + i for live i (dense list of live positions)
 void launch_compact_pos(const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t base, uint32_t* out,
                         cudaStream_t st);
@@ -154,7 +156,8 @@ void launch_relsky(int D, const RelskyArgs& a, cudaStream_t st);
 // words rules out most non-dominating pairs; pairs that pass are confirmed
 // with the exact float test.
 constexpr int kCodeLevels = 128;
-void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st);   // thr[D][127]
+// thr[D][127]; n_dev: optional device row count (s.n is then an upper bound)
+void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st, const uint32_t* n_dev = nullptr);
 // fills s.qc; n_dev: optional device-side row count (s.n is then an upper bound)
 void launch_encode(int D, const DevSet& s, const float* thr, cudaStream_t st, const uint32_t* n_dev = nullptr);
 struct Relsky2Args {
@@ -178,9 +181,35 @@ struct Relsky2Args {
     const uint32_t* cid;      // row id of each candidate position
     const uint32_t* sid;      // row id of each comparator position
     const uint32_t* n_items_dev;  // optional: item count in device memory (n_items = capacity)
+    bool direct;                  // items hold their comparator range itself in (lb, le)
 };
 // tile = candidates per item (<= 32 * 8, one warp); picks K from it.
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);
+// Device-side planning. A job = candidates [cb, ce) of a candidate list x one
+// comparator range [lo, hi) (sorted by key). Jobs come from device offsets;
+// they expand into direct items: tiles of `tile` candidates x chunks of the
+// range (at most max_chunks per job: the chunk grows for longer ranges),
+// chunk-major inside a job. Item / job counts are exclusive scans of
+// per-job counts (Runner::scan_u32), so every count stays on the device.
+struct Job {
+    uint32_t cb, ce, lo, hi;
+};
+// blocks of `block` rows inside each partition of a set (off[P+1]), each
+// block against itself: counts[p] = blocks of p; then jobs at prefix[p].
+void launch_block_counts(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* counts, cudaStream_t st);
+void launch_block_jobs(const uint32_t* off, uint32_t P, uint32_t block, const uint32_t* prefix, Job* jobs,
+                       cudaStream_t st);
+// one job per partition: candidates [coff[p], coff[p+1]) vs the comparator
+// sub-range [soff[p] + lo, soff[p] + hi) clipped to [soff[p], soff[p+1]) when
+// soff is given ("self" lists), else [lo, hi) clipped to [0, *n_comp).
+void launch_partition_jobs(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
+                           uint64_t lo, uint64_t hi, Job* jobs, cudaStream_t st);
+// counts[j] = items of job j (0 for j >= *n_jobs), j < cap
+void launch_job_counts(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, uint32_t tile, uint32_t chunk,
+                       uint32_t max_chunks, uint32_t* counts, cudaStream_t st);
+void launch_job_items(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, const uint32_t* prefix, uint32_t tile,
+                      uint32_t chunk, uint32_t max_chunks, Item* items, cudaStream_t st);
+
 // Items of a relsky wave built on the device from the dense candidate
 // offsets of np partitions (dnew[np+1], relative to the dense list) and each
 // partition's comparator groups (groups[gb[p]..gb[p+1]) = (lb, le) into the

@@ -73,12 +73,13 @@ __device__ __forceinline__ uint32_t quant_code(const float* tj, float x) {
 constexpr int kThrThreads = 512, kThrItems = 4;
 template <int D>
 __global__ void __launch_bounds__(kThrThreads) k_thresholds(const float* __restrict__ src, uint32_t stride, uint32_t ncols,
-                                                           uint32_t n, float* thr) {
+                                                           uint32_t n_host, float* thr, const uint32_t* n_dev) {
     constexpr int SMP = kThrThreads * kThrItems;
     using Sort = cub::BlockRadixSort<float, kThrThreads, kThrItems>;
     __shared__ typename Sort::TempStorage tmp;
     __shared__ float v[SMP];
     const int j = blockIdx.x;
+    const uint32_t n = n_dev ? min(*n_dev, n_host) : n_host;
     const uint32_t S = n < (uint32_t)SMP ? n : (uint32_t)SMP;
     float keys[kThrItems];
 #pragma unroll
@@ -262,8 +263,10 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
         __syncthreads();  // candidate coordinates staged
         bool live = __any_sync(FULL, alive != 0);
 
-        for (uint32_t r = it.lb; live && r < it.le; ++r) {
-            const uint2 rg = a.ranges[r];
+        // direct items carry their one comparator range in (lb, le)
+        const uint32_t r_end = a.direct ? it.lb + 1 : it.le;
+        for (uint32_t r = it.lb; live && r < r_end; ++r) {
+            const uint2 rg = a.direct ? make_uint2(it.lb, it.le) : a.ranges[r];
             const uint32_t sb = rg.x, se = range_end(a, rg);
             uint32_t base = sb + warp * 32;
             if (base >= se) continue;
@@ -984,15 +987,15 @@ bool launch_small_skyline(int D, const float* xyz, const uint32_t* id, uint32_t 
     return true;
 }
 
-void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st) {
+void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st, const uint32_t* n_dev) {
     if (!s.n) return;
-    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(s.xyz, (DT + 3) / 4 * 4, DT, s.n, thr)));
+    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(s.xyz, (DT + 3) / 4 * 4, DT, s.n, thr, n_dev)));
     SKY_LAUNCH_CHECK();
 }
 
 void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st) {
     if (!n) return;
-    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(pts, d, d, n, thr)));
+    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(pts, d, d, n, thr, nullptr)));
     SKY_LAUNCH_CHECK();
 }
 
@@ -1058,6 +1061,113 @@ __global__ void __launch_bounds__(1024) k_plan_items(const uint32_t* __restrict_
 void launch_plan_items(const uint32_t* dnew, uint32_t np, const uint32_t* gb, const uint2* groups, uint32_t max_groups,
                        uint32_t tile, Item* items, uint32_t* count, cudaStream_t st) {
     k_plan_items<<<1, 1024, 0, st>>>(dnew, np, gb, groups, max_groups, tile, items, count);
+    SKY_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------ device planning
+__global__ void k_block_counts(const uint32_t* __restrict__ off, uint32_t P, uint32_t block,
+                               uint32_t* __restrict__ counts) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P) counts[p] = (off[p + 1] - off[p] + block - 1) / block;
+    if (p == P) counts[P] = 0;
+}
+
+__global__ void k_block_jobs(const uint32_t* __restrict__ off, uint32_t P, uint32_t block,
+                             const uint32_t* __restrict__ prefix, Job* __restrict__ jobs) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const uint32_t b = off[p], e = off[p + 1];
+    uint32_t j = prefix[p];
+    for (uint32_t x = b; x < e; x += block, ++j) {
+        const uint32_t y = min(x + block, e);
+        jobs[j] = Job{x, y, x, y};
+    }
+}
+
+__global__ void k_partition_jobs(const uint32_t* __restrict__ coff, const uint32_t* __restrict__ soff,
+                                 const uint32_t* __restrict__ n_comp, uint32_t P, uint64_t lo, uint64_t hi,
+                                 Job* __restrict__ jobs) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    uint64_t rb, re;
+    if (soff) {
+        rb = soff[p];
+        re = soff[p + 1];
+    } else {
+        rb = 0;
+        re = *n_comp;
+    }
+    const uint64_t len = re - rb;
+    const uint64_t l = rb + min(lo, len), h = rb + min(hi, len);
+    jobs[p] = Job{coff[p], coff[p + 1], (uint32_t)l, (uint32_t)h};
+}
+
+__device__ __forceinline__ void job_shape(const Job& jb, uint32_t tile, uint32_t chunk, uint32_t max_chunks,
+                                          uint32_t* ntile, uint32_t* nch, uint32_t* ch) {
+    const uint32_t len = jb.hi > jb.lo ? jb.hi - jb.lo : 0;
+    *ntile = (jb.ce - jb.cb + tile - 1) / tile;
+    uint32_t c = chunk;
+    if ((len + c - 1) / c > max_chunks) c = (len + max_chunks - 1) / max_chunks;
+    *ch = c;
+    *nch = len ? (len + c - 1) / c : 0;
+}
+
+__global__ void k_job_counts(const Job* __restrict__ jobs, const uint32_t* __restrict__ n_jobs, uint32_t cap,
+                             uint32_t tile, uint32_t chunk, uint32_t max_chunks, uint32_t* __restrict__ counts) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > cap) return;
+    uint32_t c = 0;
+    if (j < cap && j < *n_jobs) {
+        uint32_t nt, nc, ch;
+        job_shape(jobs[j], tile, chunk, max_chunks, &nt, &nc, &ch);
+        c = nt * nc;
+    }
+    counts[j] = c;
+}
+
+// one CTA per job; chunk-major inside the job (every tile meets chunk g
+// before any tile meets chunk g+1)
+__global__ void k_job_items(const Job* __restrict__ jobs, const uint32_t* __restrict__ n_jobs,
+                            const uint32_t* __restrict__ prefix, uint32_t tile, uint32_t chunk, uint32_t max_chunks,
+                            Item* __restrict__ items) {
+    const uint32_t j = blockIdx.x;
+    if (j >= *n_jobs) return;
+    const Job jb = jobs[j];
+    uint32_t nt, nc, ch;
+    job_shape(jb, tile, chunk, max_chunks, &nt, &nc, &ch);
+    const uint32_t base = prefix[j], n = nt * nc;
+    for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+        const uint32_t g = x / nt, t = x - g * nt;
+        const uint32_t cb = jb.cb + t * tile, lo = jb.lo + g * ch;
+        items[base + x] = Item{cb, min(cb + tile, jb.ce), lo, min(lo + ch, jb.hi)};
+    }
+}
+
+void launch_block_counts(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* counts, cudaStream_t st) {
+    k_block_counts<<<ceil_div(P + 1, 256), 256, 0, st>>>(off, P, block, counts);
+    SKY_LAUNCH_CHECK();
+}
+void launch_block_jobs(const uint32_t* off, uint32_t P, uint32_t block, const uint32_t* prefix, Job* jobs,
+                       cudaStream_t st) {
+    if (!P) return;
+    k_block_jobs<<<ceil_div(P, 256), 256, 0, st>>>(off, P, block, prefix, jobs);
+    SKY_LAUNCH_CHECK();
+}
+void launch_partition_jobs(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
+                           uint64_t lo, uint64_t hi, Job* jobs, cudaStream_t st) {
+    if (!P) return;
+    k_partition_jobs<<<ceil_div(P, 256), 256, 0, st>>>(coff, soff, n_comp, P, lo, hi, jobs);
+    SKY_LAUNCH_CHECK();
+}
+void launch_job_counts(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, uint32_t tile, uint32_t chunk,
+                       uint32_t max_chunks, uint32_t* counts, cudaStream_t st) {
+    k_job_counts<<<ceil_div(cap + 1, 256), 256, 0, st>>>(jobs, n_jobs, cap, tile, chunk, max_chunks, counts);
+    SKY_LAUNCH_CHECK();
+}
+void launch_job_items(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, const uint32_t* prefix, uint32_t tile,
+                      uint32_t chunk, uint32_t max_chunks, Item* items, cudaStream_t st) {
+    if (!cap) return;
+    k_job_items<<<cap, 128, 0, st>>>(jobs, n_jobs, prefix, tile, chunk, max_chunks, items);
     SKY_LAUNCH_CHECK();
 }
 
