@@ -1682,7 +1682,15 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
     }
-    if (P > 1) {
+    // single GPU, all-pairs merge: the candidates are the union itself in
+    // global key order, so a tile's key bound is as tight as it can be
+    const bool global_cands = W == 1 && all_mode && P > 1 && D <= 16 && U.qc;
+    if (global_cands) {
+        ma.cxyz = US.xyz; ma.cskey = US.skey; ma.cid = US.id;
+        const std::vector<uint32_t> offg = {0, U.n};
+        R.relsky_waves(D, offg, 0, 1, [&](uint32_t, std::vector<uint2>& c) { c.assign(1, make_uint2(0, U.n)); },
+                       ma, US.qc, US.qc, mp.tile, mp.chunk, 4096);
+    } else if (P > 1) {
         const uint2* sq = all_mode ? US.qc : U.qc;
         auto comps_of = [&](uint32_t i, std::vector<uint2>& c) {
             if (all_mode)
@@ -1716,37 +1724,48 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     }
 
     // surviving ids of this rank's candidates, ascending (engine.cpp:128-133)
-    const uint32_t cb = offu[qb], cn = offu[qe] - cb;
+    const uint32_t cb = global_cands ? 0 : offu[qb], cn = global_cands ? U.n : offu[qe] - cb;
+    const uint32_t* cand_ids = global_cands ? US.id : U.id;
     uint32_t* pos = R.dev<uint32_t>(S_POS, cn);
     R.scan_live(fdead + cb, pos, cn);
     launch_count_total(pos, fdead + cb, cn, misc + M_TOTAL, st);
     R.count();
     uint32_t* hm = R.pin<uint32_t>(P_MISC, 32);
-    SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    R.sync();
-    const uint32_t nmine = cn ? hm[0] : 0;
-    uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, std::max<uint32_t>(nmine, U.n));
-    uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, std::max<uint32_t>(nmine, U.n));
-    launch_compact_ids(U.id + cb, fdead + cb, pos, cn, idsA, st);
-    R.count();
-    uint32_t nf = nmine;
+    uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, std::max<uint32_t>(cn, 1));
+    uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, std::max<uint32_t>(cn, 1));
+    uint32_t nf = 0, n_copy = 0;
     uint32_t* final_ids = idsB;
     if (W == 1) {
-        R.sort_keys(idsA, idsB, nf, std::max(1, bits_for(n)));  // ids < n
+        // no round trip: the ids fill a cn-slot buffer (unused slots all ones,
+        // sorted last) and the count travels back with them
+        SKY_CUDA(cudaMemsetAsync(idsA, 0xFF, (size_t)cn * sizeof(uint32_t), st));
+        launch_compact_ids(cand_ids + cb, fdead + cb, pos, cn, idsA, st);
+        R.count();
+        R.sort_keys(idsA, idsB, cn, std::max(1, bits_for(n)));  // ids < n
+        n_copy = cn;
     } else {
-        nf = R.gather_ids(idsA, nmine, idsB);  // all ranks' survivors, then sorted
-        final_ids = idsB;
+        SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        const uint32_t nmine = cn ? hm[0] : 0;
+        launch_compact_ids(cand_ids + cb, fdead + cb, pos, cn, idsA, st);
+        R.count();
+        uint32_t* all = R.dev<uint32_t>(S_IDS_B, std::max<uint32_t>(U.n, 1));
+        nf = R.gather_ids(idsA, nmine, all);  // all ranks' survivors, then sorted
+        final_ids = all;
+        n_copy = nf;
         R.reduce_counters();
     }
     SKY_CUDA(cudaEventRecord(c->ev[3], st));
-    uint32_t* hid = R.pin<uint32_t>(P_IDS, nf);
-    SKY_CUDA(cudaMemcpyAsync(hid, final_ids, (size_t)nf * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    uint32_t* hid = R.pin<uint32_t>(P_IDS, n_copy);
+    SKY_CUDA(cudaMemcpyAsync(hid, final_ids, (size_t)n_copy * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     unsigned long long* ht = reinterpret_cast<unsigned long long*>(hm + 4);
     SKY_CUDA(cudaMemcpyAsync(ht, R.tests(0), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SKY_CUDA(cudaMemcpyAsync(ht + 3, misc + M_HITS, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SKY_CUDA(cudaEventRecord(c->ev[4], st));
     R.sync();
-    out->d2h_bytes += (uint64_t)nf * sizeof(uint32_t);
+    if (W == 1) nf = cn ? hm[0] : 0;
+    out->d2h_bytes += (uint64_t)n_copy * sizeof(uint32_t);
     out->ids = static_cast<int64_t*>(std::malloc((nf ? nf : 1) * sizeof(int64_t)));
     for (uint32_t i = 0; i < nf; ++i) out->ids[i] = hid[i];
     out->n_ids = out->final_size = nf;
