@@ -76,7 +76,7 @@ enum Slot {
     S_SET2, S_SET2_K, S_SET2_I, S_SET2_Q, S_SET3, S_SET3_K, S_SET3_I, S_SET3_Q,
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
-    S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JCNT2, S_JPRE2, S_JOBS, S_DEAD1, S_OFF_D, S_DNEW,
+    S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
     S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
 };
 // pinned slots
@@ -95,7 +95,7 @@ constexpr uint32_t kExactCapRows = 0;
 // misc device words
 enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_NITEMS = 7, M_TESTS = 8 /* 4 x u64 */,
        M_HITS = 16 /* 4 x u64, per phase */,
-       M_S0 = 24, M_S1 = 25, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */ };
+       M_S0 = 24, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;
@@ -500,30 +500,11 @@ class Runner {
         a.sxyz = s0.xyz; a.sskey = s0.skey; a.bounded = true; a.dead = dead;
         a.cid = s0.id; a.sid = s0.id;
         a.tests = count_tests ? tests(1) : nullptr;
-        // block stage: 512-row blocks of every partition against themselves
-        const uint32_t bt = 256;
-        const uint32_t jcap = (cap + kBlock - 1) / kBlock + P;
-        uint32_t* bc = dev<uint32_t>(S_JCNT2, P + 1);
-        uint32_t* bp = dev<uint32_t>(S_JPRE2, P + 1);
-        launch_block_counts(off0_dev, P, kBlock, bc, st_);
-        scan_u32(bc, bp, P + 1);
-        Job* jobs = dev<Job>(S_JOBS, std::max<uint32_t>(jcap, P));
-        launch_block_jobs(off0_dev, P, kBlock, bp, jobs, st_);
-        count(2);
+        // No block stage: the first wave (every row against the strongest
+        // `head` rows of its partition) already removes most dominated rows,
+        // and the second runs over dense lists of the survivors.
+        Job* jobs = dev<Job>(S_JOBS, P);
         const uint32_t* n_items = nullptr;
-        Item* items = expand_jobs(jobs, bp + P, jcap, bt, kBlock, 1, (uint64_t)jcap * (kBlock / bt), &n_items);
-        relsky_direct(D, bt, a, s0.qc, s0.qc, nullptr, items, (uint64_t)jcap * (kBlock / bt), n_items);
-
-        uint32_t* off1 = dev<uint32_t>(S_OFF_D, P + 1);
-        uint32_t* n1 = misc + M_S1;
-        DevSet s1 = compact_dev(s0, dead, off0_dev, P, S_SET1, off1, n1, D);
-        uint8_t* dead1 = dev<uint8_t>(S_DEAD1, cap);
-        launch_fill_u8(dead1, 0, cap, st_);
-        launch_fill_tail_u8(dead1, 1, n1, cap, st_);
-        count();
-        RelskyArgs b2 = a;
-        b2.cxyz = s1.xyz; b2.cskey = s1.skey; b2.sxyz = s1.xyz; b2.sskey = s1.skey; b2.dead = dead1;
-        b2.cid = s1.id; b2.sid = s1.id;
         // grain from the capacity: ~ rows per partition
         const uint64_t per = (uint64_t)cap / std::max<uint32_t>(1, P);
         const uint32_t tile = per >= 2048 ? 256 : (per >= 512 ? 128 : 64);
@@ -534,22 +515,22 @@ class Runner {
         *hp = P;
         SKY_CUDA(cudaMemcpyAsync(np_dev, hp, sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
         // wave 0: every row of a partition against the partition's first `head` rows
-        launch_partition_jobs(off1, off1, nullptr, P, 0, head, jobs, st_);
+        launch_partition_jobs(off0_dev, off0_dev, nullptr, P, 0, head, jobs, st_);
         count();
-        items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
-        relsky_direct(D, tile, b2, s1.qc, s1.qc, nullptr, items, icap, n_items);
+        Item* items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+        relsky_direct(D, tile, a, s0.qc, s0.qc, nullptr, items, icap, n_items);
         // wave 1: the live rows (dense lists) against the rest of their partition
         uint32_t* pos = dev<uint32_t>(S_POS, cap);
         uint32_t* dnew = dev<uint32_t>(S_DNEW, P + 1);
         uint32_t* dense = dev<uint32_t>(S_DENSE, cap);
-        scan_live(dead1, pos, cap);
-        launch_remap_offsets(off1, P, pos, dead1, cap, dnew, st_);
-        launch_compact_pos(dead1, pos, cap, 0, dense, st_);
-        launch_partition_jobs(dnew, off1, nullptr, P, head, ~0ull, jobs, st_);
+        scan_live(dead, pos, cap);
+        launch_remap_offsets(off0_dev, P, pos, dead, cap, dnew, st_);
+        launch_compact_pos(dead, pos, cap, 0, dense, st_);
+        launch_partition_jobs(dnew, off0_dev, nullptr, P, head, ~0ull, jobs, st_);
         count(3);
         items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
-        relsky_direct(D, tile, b2, s1.qc, s1.qc, dense, items, icap, n_items);
-        return compact_dev(s1, dead1, off1, P, S_SET2, off_u_dev, n_u, D);
+        relsky_direct(D, tile, a, s0.qc, s0.qc, dense, items, icap, n_items);
+        return compact_dev(s0, dead, off0_dev, P, S_SET2, off_u_dev, n_u, D);
     }
 
     void relsky(int D, const Plan& plan, const RelskyArgs& base, const uint2* cq = nullptr,

@@ -194,11 +194,6 @@ void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStr
 struct Job {
     uint32_t cb, ce, lo, hi;
 };
-// blocks of `block` rows inside each partition of a set (off[P+1]), each
-// block against itself: counts[p] = blocks of p; then jobs at prefix[p].
-void launch_block_counts(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* counts, cudaStream_t st);
-void launch_block_jobs(const uint32_t* off, uint32_t P, uint32_t block, const uint32_t* prefix, Job* jobs,
-                       cudaStream_t st);
 // one job per partition: candidates [coff[p], coff[p+1]) vs the comparator
 // sub-range [soff[p] + lo, soff[p] + hi) clipped to [soff[p], soff[p+1]) when
 // soff is given ("self" lists), else [lo, hi) clipped to [0, *n_comp).

@@ -1065,25 +1065,6 @@ void launch_plan_items(const uint32_t* dnew, uint32_t np, const uint32_t* gb, co
 }
 
 // ------------------------------------------------------ device planning
-__global__ void k_block_counts(const uint32_t* __restrict__ off, uint32_t P, uint32_t block,
-                               uint32_t* __restrict__ counts) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < P) counts[p] = (off[p + 1] - off[p] + block - 1) / block;
-    if (p == P) counts[P] = 0;
-}
-
-__global__ void k_block_jobs(const uint32_t* __restrict__ off, uint32_t P, uint32_t block,
-                             const uint32_t* __restrict__ prefix, Job* __restrict__ jobs) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    const uint32_t b = off[p], e = off[p + 1];
-    uint32_t j = prefix[p];
-    for (uint32_t x = b; x < e; x += block, ++j) {
-        const uint32_t y = min(x + block, e);
-        jobs[j] = Job{x, y, x, y};
-    }
-}
-
 __global__ void k_partition_jobs(const uint32_t* __restrict__ coff, const uint32_t* __restrict__ soff,
                                  const uint32_t* __restrict__ n_comp, uint32_t P, uint64_t lo, uint64_t hi,
                                  Job* __restrict__ jobs) {
@@ -1143,16 +1124,6 @@ __global__ void k_job_items(const Job* __restrict__ jobs, const uint32_t* __rest
     }
 }
 
-void launch_block_counts(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* counts, cudaStream_t st) {
-    k_block_counts<<<ceil_div(P + 1, 256), 256, 0, st>>>(off, P, block, counts);
-    SKY_LAUNCH_CHECK();
-}
-void launch_block_jobs(const uint32_t* off, uint32_t P, uint32_t block, const uint32_t* prefix, Job* jobs,
-                       cudaStream_t st) {
-    if (!P) return;
-    k_block_jobs<<<ceil_div(P, 256), 256, 0, st>>>(off, P, block, prefix, jobs);
-    SKY_LAUNCH_CHECK();
-}
 void launch_partition_jobs(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
                            uint64_t lo, uint64_t hi, Job* jobs, cudaStream_t st) {
     if (!P) return;
