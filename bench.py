@@ -56,6 +56,22 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(tag):
+    """DRAM bytes (read + write) per launch of the dominance kernel, mean over
+    the launches of one `ncu --set full` capture committed under profiles/."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                launches = json.load(f).get(tag) or []
+        except (OSError, ValueError):
+            continue
+        v = [e["dram_traffic_bytes"] for e in launches if "relsky3" in e.get("kernel", "")]
+        if v:
+            return statistics.mean(v), os.path.relpath(path, ROOT) + f" [{tag}, {len(v)} k_relsky3 launches]"
+    return None, None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -65,19 +81,60 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed
+    region: NVML every 10 ms (plus one sample at start and stop), or
+    `nvidia-smi -lms 100` when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    NVML_REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, power_w, reasons set)
         self.proc = None
         self.thread = None
+        self.stop_evt = threading.Event()
+        self.nvml = None
+        self.handle = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(device).uuid)
+                self.handle = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(device)
+        except Exception:
+            self.nvml = None
+
+    def _sample_nvml(self):
+        n, h = self.nvml, self.handle
+        try:
+            sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+            mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+            pw = n.nvmlDeviceGetPowerUsage(h) / 1000.0
+            bits = n.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.rows.append((float(sm), float(mx), pw, {k for k, b in self.NVML_REASONS.items() if bits & b}))
+        except Exception:
+            pass
 
     def start(self):
+        if self.nvml is not None:
+            self._sample_nvml()
+
+            def loop():
+                while not self.stop_evt.wait(0.01):
+                    self._sample_nvml()
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
@@ -89,37 +146,43 @@ class ClockSampler:
         self.thread.start()
 
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+            if len(parts) < 8:
+                continue
+            try:
+                self.rows.append((float(parts[0]), float(parts[1]), float(parts[2]),
+                                  {nm for nm, v in zip(names, parts[4:8]) if v.lower().startswith("active")}))
+            except ValueError:
+                pass
 
     def stop(self):
+        self.stop_evt.set()
+        if self.nvml is not None:
+            if self.thread:
+                self.thread.join(timeout=2)
+            self._sample_nvml()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-        if self.thread:
-            self.thread.join(timeout=2)
+            if self.thread:
+                self.thread.join(timeout=2)
         return self.summary()
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
         reasons = set()
         for r in self.rows:
-            for nm, v in zip(names, r[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+            reasons |= r[3]
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": sorted(reasons), "samples": len(self.rows),
-                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
-                                   default=None)}
+                "power_w_max": max(r[2] for r in self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def dist_env():
@@ -283,9 +346,11 @@ def run_ours(args):
     peak = n_sm * FP32_COMPARES_PER_CLK_PER_SM * sm_max * 1e6 / 1e9
     per_clk = PACKED_TESTS_PER_CLK_PER_SM if d <= 16 else FP32_COMPARES_PER_CLK_PER_SM / d
     ipeak = n_sm * per_clk * sm_max * 1e6
+    traffic, traffic_src = ncu_traffic(f"c{args.config}")
     roofline = {
         "bound": "alu", "kernel": "k_relsky3 + k_bnl2 (dominance tests)", "achieved": achieved, "peak": peak,
-        "unit": "Gcompare/s", "frac": achieved / peak if peak else None, "traffic": None,
+        "unit": "Gcompare/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+        "traffic_source": traffic_src,
         "algorithmic_unit": f"1 dominance (pair) test = d = {d} FP32 compares (SURVEY 8(d))",
         "peak_source": f"{n_sm} SM x {FP32_COMPARES_PER_CLK_PER_SM} FP32 compare/clk x sm_max_mhz {sm_max} "
                        "(MEASURED_PEAKS.json clock); ALU issue, no HBM/tensor term (operands in shared memory)",
