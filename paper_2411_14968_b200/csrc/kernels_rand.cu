@@ -45,56 +45,61 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
 // Untempered mt19937_64(seed) state sequence -> out[0..count): the state
 // words form one sequence x[m] = x[m-156] ^ tw(x[m-312], x[m-311])
 // (x[0..311] = seeded state; output k = temper(x[312+k]), applied by the
-// parallel consumer). Terms m0+t and m0+156+t (t < 156) depend only on
-// earlier groups, except that m0+311 needs x[m0], which thread 155
-// recomputes; so a 624-term ring needs one barrier per 312 outputs.
+// parallel consumer). Thread t < 156 keeps A = x[m0-312+t] and
+// B = x[m0-156+t] in registers and produces x[m0+t] = B ^ tw(A, A') and
+// x[m0+156+t] = x[m0+t] ^ tw(B, B'), the primed values being thread t+1's
+// (warp shuffles; shared memory across warp boundaries). Thread 155's
+// B' = x[m0] is recomputed from thread 0 and 1's registers. One barrier
+// per 312 outputs; the boundary slots are double-buffered by parity.
+// (A single-warp variant without barriers measured slower: it is issue
+// bound at ~130 instructions per 312 outputs.)
 __global__ void __launch_bounds__(160) k_mt64(uint64_t seed, uint32_t count, uint64_t* __restrict__ out) {
-    constexpr uint32_t R = 2 * MT_N;
-    __shared__ uint64_t x[R];
-    const uint32_t t = threadIdx.x;
+    __shared__ uint64_t init[MT_N];
+    __shared__ uint64_t sA[2][8], sB[2][8], sA1[2];  // per parity: each warp's lane-0 A/B; thread 1's A
+    const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) {
-        x[0] = seed;
-        for (int i = 1; i < MT_N; ++i) x[i] = 6364136223846793005ull * (x[i - 1] ^ (x[i - 1] >> 62)) + (uint64_t)i;
+        init[0] = seed;
+        for (int i = 1; i < MT_N; ++i)
+            init[i] = 6364136223846793005ull * (init[i - 1] ^ (init[i - 1] >> 62)) + (uint64_t)i;
     }
     __syncthreads();
-    uint32_t r0 = MT_N;  // ring position of m0
-    for (uint32_t k0 = 0; k0 < count; k0 += MT_N) {
-        uint64_t v0 = 0, v1 = 0;
-        uint32_t p0 = 0, p1 = 0;
-        if (t < MT_M) {
-            auto at = [&](uint32_t back) {  // x[m0 + t - back]
-                uint32_t q = r0 + t + R - back;
-                while (q >= R) q -= R;
-                return x[q];
-            };
-            const uint64_t a = at(MT_M), b = at(MT_N), c = at(MT_N - 1);
-            v0 = a ^ mt_tw(b, c);                              // x[m0 + t]
-            uint64_t c2;                                       // x[m0 + t - 155]
-            if (t + 1 < MT_M) {
-                c2 = at(MT_M - 1);
-            } else {                                           // x[m0], recomputed
-                uint32_t q0 = r0 + R - MT_M, q1 = r0 + R - MT_N, q2 = r0 + R - MT_N + 1;
-                while (q0 >= R) q0 -= R;
-                while (q1 >= R) q1 -= R;
-                while (q2 >= R) q2 -= R;
-                c2 = x[q0] ^ mt_tw(x[q1], x[q2]);
-            }
-            v1 = v0 ^ mt_tw(a, c2);                            // x[m0 + 156 + t]
-            p0 = r0 + t;
-            if (p0 >= R) p0 -= R;
-            p1 = p0 + MT_M;
-            if (p1 >= R) p1 -= R;
+    uint64_t A = 0, B = 0;
+    if (t < MT_M) {
+        A = init[t];
+        B = init[MT_M + t];
+    }
+    uint32_t par = 0;
+    for (uint32_t k0 = 0; k0 < count; k0 += MT_N, par ^= 1) {
+        if (t < MT_M && lane == 0) {
+            sA[par][w] = A;
+            sB[par][w] = B;
         }
-        __syncthreads();  // every read of the previous groups is done
+        if (t == 1) sA1[par] = A;
+        __syncthreads();
+        // neighbour (t+1) values: shuffle inside the warp, shared memory at
+        // the warp's last lane
+        const uint64_t An = __shfl_down_sync(0xffffffffu, A, 1);
+        const uint64_t Bn = __shfl_down_sync(0xffffffffu, B, 1);
         if (t < MT_M) {
-            x[p0] = v0;
-            x[p1] = v1;
+            uint64_t A1, B1;
+            if (t + 1 == MT_M) {
+                // t = 155: A' = x[m0-156] = thread 0's B; B' = x[m0] recomputed
+                A1 = sB[par][0];
+                B1 = sB[par][0] ^ mt_tw(sA[par][0], sA1[par]);
+            } else if (lane == 31) {
+                A1 = sA[par][w + 1];
+                B1 = sB[par][w + 1];
+            } else {
+                A1 = An;
+                B1 = Bn;
+            }
+            const uint64_t v0 = B ^ mt_tw(A, A1);   // x[m0 + t]
+            const uint64_t v1 = v0 ^ mt_tw(B, B1);  // x[m0 + 156 + t]
             if (k0 + t < count) out[k0 + t] = v0;
             if (k0 + MT_M + t < count) out[k0 + MT_M + t] = v1;
+            A = v0;
+            B = v1;
         }
-        r0 += MT_N;
-        if (r0 >= R) r0 -= R;
-        __syncthreads();
     }
 }
 
