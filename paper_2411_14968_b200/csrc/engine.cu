@@ -65,6 +65,9 @@ struct sky_ctx {
     // multi-GPU: one rank per process, NCCL over NVLink/NVSwitch
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    // device copy of the mt19937_64 jump polynomials (random partitioner)
+    uint32_t* mt_jump = nullptr;
+    uint32_t mt_jump_rows = 0;
 };
 
 namespace {
@@ -859,7 +862,21 @@ class Runner {
         void* scratch = c_->dev.get(S_RAND, random_scratch_bytes(n));
         const size_t cb = random_cub_bytes(n);
         void* ct = c_->dev.get(S_CUB, cb);
-        if (!random_partition_gpu(n, P, seed, pid, scratch, ct, cb, c_->sm_count, st_, &c_->launches)) {
+        const uint32_t* jt = nullptr;
+        const uint32_t rows = mt_jump_chunks(n) ? mt_jump_chunks(n) - 1 : 0;
+        if (n - 1 > (1u << 18) && rows) {
+            if (c_->mt_jump_rows < rows) {
+                const uint32_t* h = mt_jump_table(kJumpLog2, rows);  // host, built once per process
+                if (c_->mt_jump) SKY_CUDA(cudaFree(c_->mt_jump));
+                c_->mt_jump = nullptr;
+                const size_t bytes = (size_t)rows * mt_jump_words() * sizeof(uint32_t);
+                SKY_CUDA(cudaMalloc(&c_->mt_jump, bytes));
+                SKY_CUDA(cudaMemcpy(c_->mt_jump, h, bytes, cudaMemcpyHostToDevice));
+                c_->mt_jump_rows = rows;
+            }
+            jt = c_->mt_jump;
+        }
+        if (!random_partition_gpu(n, P, seed, pid, scratch, ct, cb, c_->sm_count, st_, &c_->launches, jt)) {
             uint32_t* h = pin<uint32_t>(P_PID, n);
             random_partition_of(n, P, seed, h);
             SKY_CUDA(cudaMemcpyAsync(pid, h, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
@@ -1872,6 +1889,7 @@ void sky_ctx_destroy(sky_ctx* c) {
     for (auto& e : c->dom_ev)
         if (e) cudaEventDestroy(e);
     for (auto& b : c->stage) cudaFreeHost(b.first);
+    if (c->mt_jump) cudaFree(c->mt_jump);
     c->dev.release();
     if (c->own) cudaStreamDestroy(c->own);
     delete c;

@@ -254,7 +254,15 @@ bool launch_small_skyline(int D, const float* xyz, const uint32_t* id, uint32_t 
 // Random partitioner (kernels_rand.cu): bit-exact assign_random on the GPU.
 size_t random_scratch_bytes(uint32_t n);
 size_t random_cub_bytes(uint32_t n);
+// jump_table: device copy of mt_jump_table(kJumpLog2, chunks-1) (mtjump.cpp)
+// or null for the single-CTA stream.
+constexpr uint32_t kJumpLog2 = 14;
+inline uint32_t mt_jump_chunks(uint32_t n) { return n < 2 ? 0u : ((n - 1) + (1u << kJumpLog2) - 1) >> kJumpLog2; }
 bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, void* scratch, void* cub_tmp,
-                          size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches);
+                          size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches,
+                          const uint32_t* jump_table = nullptr);
+// host: jump polynomials t^(k 2^log2_stride) mod phi, k = 1..chunks (mtjump.cpp)
+const uint32_t* mt_jump_table(uint32_t log2_stride, uint32_t chunks);
+int mt_jump_words();
 
 }  // namespace sky

@@ -42,32 +42,18 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
     return x;
 }
 
-// Untempered mt19937_64(seed) state sequence -> out[0..count): the state
-// words form one sequence x[m] = x[m-156] ^ tw(x[m-312], x[m-311])
-// (x[0..311] = seeded state; output k = temper(x[312+k]), applied by the
-// parallel consumer). Thread t < 156 keeps A = x[m0-312+t] and
+// Untempered mt19937_64 state sequence: x[m] = x[m-156] ^ tw(x[m-312], x[m-311]).
+// Thread t < 156 of a 160+-thread CTA keeps A = x[m0-312+t] and
 // B = x[m0-156+t] in registers and produces x[m0+t] = B ^ tw(A, A') and
 // x[m0+156+t] = x[m0+t] ^ tw(B, B'), the primed values being thread t+1's
 // (warp shuffles; shared memory across warp boundaries). Thread 155's
 // B' = x[m0] is recomputed from thread 0 and 1's registers. One barrier
-// per 312 outputs; the boundary slots are double-buffered by parity.
-// (A single-warp variant without barriers measured slower: it is issue
-// bound at ~130 instructions per 312 outputs.)
-__global__ void __launch_bounds__(160) k_mt64(uint64_t seed, uint32_t count, uint64_t* __restrict__ out) {
-    __shared__ uint64_t init[MT_N];
+// per 312 outputs; the boundary slots are double-buffered by parity. Every
+// thread of the CTA must call it. (A single-warp variant without barriers
+// measured slower: issue bound at ~130 instructions per 312 outputs.)
+__device__ void mt_generate(uint64_t A, uint64_t B, uint32_t count, uint64_t* __restrict__ out) {
     __shared__ uint64_t sA[2][8], sB[2][8], sA1[2];  // per parity: each warp's lane-0 A/B; thread 1's A
     const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
-    if (t == 0) {
-        init[0] = seed;
-        for (int i = 1; i < MT_N; ++i)
-            init[i] = 6364136223846793005ull * (init[i - 1] ^ (init[i - 1] >> 62)) + (uint64_t)i;
-    }
-    __syncthreads();
-    uint64_t A = 0, B = 0;
-    if (t < MT_M) {
-        A = init[t];
-        B = init[MT_M + t];
-    }
     uint32_t par = 0;
     for (uint32_t k0 = 0; k0 < count; k0 += MT_N, par ^= 1) {
         if (t < MT_M && lane == 0) {
@@ -76,8 +62,6 @@ __global__ void __launch_bounds__(160) k_mt64(uint64_t seed, uint32_t count, uin
         }
         if (t == 1) sA1[par] = A;
         __syncthreads();
-        // neighbour (t+1) values: shuffle inside the warp, shared memory at
-        // the warp's last lane
         const uint64_t An = __shfl_down_sync(0xffffffffu, A, 1);
         const uint64_t Bn = __shfl_down_sync(0xffffffffu, B, 1);
         if (t < MT_M) {
@@ -101,6 +85,83 @@ __global__ void __launch_bounds__(160) k_mt64(uint64_t seed, uint32_t count, uin
             B = v1;
         }
     }
+}
+
+// Sequential stream: x[0..311] = seeded state (optionally to state_out);
+// out[k] = x[312 + k] for k < count (untempered; the consumer tempers).
+__global__ void __launch_bounds__(160) k_mt64(uint64_t seed, uint32_t count, uint64_t* __restrict__ out,
+                                              uint64_t* __restrict__ state_out) {
+    __shared__ uint64_t init[MT_N];
+    const uint32_t t = threadIdx.x;
+    if (t == 0) {
+        init[0] = seed;
+        for (int i = 1; i < MT_N; ++i)
+            init[i] = 6364136223846793005ull * (init[i - 1] ^ (init[i - 1] >> 62)) + (uint64_t)i;
+    }
+    __syncthreads();
+    if (state_out)
+        for (uint32_t i = t; i < MT_N; i += blockDim.x) state_out[i] = init[i];
+    uint64_t A = 0, B = 0;
+    if (t < MT_M) {
+        A = init[t];
+        B = init[MT_M + t];
+    }
+    mt_generate(A, B, count, out);
+}
+
+// Jump-ahead stream: chunk k = blockIdx.x writes out[kJ .. min(m, (k+1)J)).
+// Its start window W_kJ = sum_i g_k[i] W_i (g_k = t^(kJ) mod phi, table row
+// k-1; mtjump.cpp) is a correlation of g_k's coefficient bits with the first
+// 19937 + 312 stream words xs[] (seeded state + 19937 outputs), evaluated in
+// shared memory over the set bits only; then the chunk runs mt_generate.
+constexpr uint32_t MT_DEG = 19937, MT_XS = MT_DEG + MT_N, MT_GW = 624;
+
+__global__ void __launch_bounds__(1024) k_mt_jump(const uint64_t* __restrict__ xs, const uint32_t* __restrict__ gtab,
+                                                  uint32_t J, uint32_t m, uint64_t* __restrict__ out) {
+    extern __shared__ uint64_t sm_x[];               // [MT_XS]
+    uint32_t* sm_g = reinterpret_cast<uint32_t*>(sm_x + MT_XS);  // [MT_GW]
+    __shared__ unsigned long long win[MT_N];
+    const uint32_t k = blockIdx.x, t = threadIdx.x;
+    if (k == 0) {
+        for (uint32_t i = t; i < MT_N; i += blockDim.x) win[i] = xs[i];
+    } else {
+        for (uint32_t i = t; i < MT_XS; i += blockDim.x) sm_x[i] = xs[i];
+        const uint32_t* g = gtab + (size_t)(k - 1) * MT_GW;
+        for (uint32_t i = t; i < MT_GW; i += blockDim.x) sm_g[i] = g[i];
+        for (uint32_t i = t; i < MT_N; i += blockDim.x) win[i] = 0;
+        __syncthreads();
+        // warp w takes coefficient words w, w+32, ...; lane l accumulates
+        // window words l + 32r (10 independent accumulators)
+        constexpr int RW = (MT_N + 31) / 32;
+        const uint32_t lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+        uint64_t acc[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) acc[r] = 0;
+        for (uint32_t wi = w; wi < MT_GW; wi += nw) {
+            uint32_t gw = sm_g[wi];
+            while (gw) {
+                const uint32_t i = wi * 32 + (uint32_t)(__ffs(gw) - 1);  // i < 19937
+                gw &= gw - 1;
+                const uint64_t* xi = sm_x + i + lane;
+#pragma unroll
+                for (int r = 0; r < RW; ++r)
+                    if (lane + 32 * r < MT_N) acc[r] ^= xi[32 * r];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+            if (lane + 32 * r < MT_N) atomicXor(&win[lane + 32 * r], (unsigned long long)acc[r]);
+    }
+    __syncthreads();
+    uint64_t A = 0, B = 0;
+    if (t < MT_M) {
+        A = win[t];
+        B = win[MT_M + t];
+    }
+    const uint64_t base = (uint64_t)k * J;
+    const uint64_t left = base >= m ? 0ull : (uint64_t)m - base;
+    const uint32_t cnt = (uint32_t)(left < J ? left : J);
+    mt_generate(A, B, cnt, out + base);
 }
 
 // step i = n - k: j_i = x_k mod i, key (j_i << 32 | i); flag a rejected draw
@@ -211,7 +272,8 @@ size_t random_scratch_bytes(uint32_t n) {
 // (nothing written) when a draw would have been rejected; the caller then
 // reproduces the shuffle on the host. Synchronizes once to read the flag.
 bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, void* scratch, void* cub_tmp,
-                          size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches) {
+                          size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches,
+                          const uint32_t* jump_table) {
     if (n == 0) return true;
     if (n == 1) {
         SKY_CUDA(cudaMemsetAsync(pid, 0, sizeof(uint32_t), st));
@@ -230,7 +292,18 @@ bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, 
     const uint32_t m = n - 1;
     SKY_CUDA(cudaMemsetAsync(misc, 0, 4 * sizeof(uint32_t), st));
     SKY_CUDA(cudaMemsetAsync(head, 0xFF, (size_t)n * sizeof(uint32_t), st));
-    k_mt64<<<1, 160, 0, st>>>(seed, m, x);
+    if (jump_table && m > (1u << 18)) {
+        // many CTAs: each chunk of 2^kJumpLog2 outputs from its jumped window
+        uint64_t* xs = key;  // 20249 words of scratch, consumed before k_fy_draws writes key
+        k_mt64<<<1, 160, 0, st>>>(seed, MT_DEG, xs + MT_N, xs);
+        const uint32_t J = 1u << kJumpLog2, chunks = (m + J - 1) / J;
+        const size_t smem = (size_t)MT_XS * 8 + MT_GW * 4;
+        SKY_CUDA(cudaFuncSetAttribute(k_mt_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_mt_jump<<<chunks, 1024, smem, st>>>(xs, jump_table, J, m, x);
+        if (launches) *launches += 1;
+    } else {
+        k_mt64<<<1, 160, 0, st>>>(seed, m, x, nullptr);
+    }
     k_fy_draws<<<ceil_div(m, 256), 256, 0, st>>>(x, n, key, jv, misc);
     int end_bit = 32;
     while (end_bit < 64 && (uint64_t{1} << (end_bit - 32)) < n) ++end_bit;
