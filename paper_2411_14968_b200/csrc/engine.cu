@@ -98,7 +98,8 @@ constexpr uint32_t kExactCapRows = 0;
 // misc device words
 enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_NITEMS = 7, M_TESTS = 8 /* 4 x u64 */,
        M_HITS = 16 /* 4 x u64, per phase */,
-       M_S0 = 24, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */ };
+       M_S0 = 24, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */,
+       M_RFLAG = 28 /* random partitioner: a draw the reference would reject */ };
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;
@@ -857,7 +858,9 @@ class Runner {
 
     // partition_of of assign_random (partition.cpp:36-54) on the device; the
     // host reproduces it only if a draw would have been rejected.
-    uint32_t* random_pids(uint32_t n, uint64_t P, uint64_t seed) {
+    // deferred: a rejected draw sets misc[M_RFLAG] instead of a host round
+    // trip; the caller redoes the run eagerly (host shuffle) when it is set
+    uint32_t* random_pids(uint32_t n, uint64_t P, uint64_t seed, bool deferred = false) {
         uint32_t* pid = dev<uint32_t>(S_PID, n);
         void* scratch = c_->dev.get(S_RAND, random_scratch_bytes(n));
         const size_t cb = random_cub_bytes(n);
@@ -876,7 +879,8 @@ class Runner {
             }
             jt = c_->mt_jump;
         }
-        if (!random_partition_gpu(n, P, seed, pid, scratch, ct, cb, c_->sm_count, st_, &c_->launches, jt)) {
+        uint32_t* flag = deferred ? dev<uint32_t>(S_MISC, 64) + M_RFLAG : nullptr;
+        if (!random_partition_gpu(n, P, seed, pid, scratch, ct, cb, c_->sm_count, st_, &c_->launches, jt, flag)) {
             uint32_t* h = pin<uint32_t>(P_PID, n);
             random_partition_of(n, P, seed, h);
             SKY_CUDA(cudaMemcpyAsync(pid, h, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
@@ -1413,7 +1417,8 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         pts = dp;
         out->h2d_bytes += (uint64_t)n * d * sizeof(float);
     }
-    const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed) : nullptr;
+    const bool defer_rand = !eager && c->world == 1;
+    const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed, defer_rand) : nullptr;
     const bool rep_random = cfg->filter == SKY_FILTER_REPRESENTATIVE && cfg->rep_selection == SKY_REPS_RANDOM;
     uint32_t* scan_rows = nullptr;  // sliced + random reps: split()'s exact scan order
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
@@ -1561,6 +1566,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         R.sync();
         const uint32_t* hmisc = h + P + 1;
         check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
+        if (defer_rand && hmisc[M_RFLAG]) throw RedoEager{};  // redo with the host shuffle
         if (cfg->filter == SKY_FILTER_REPRESENTATIVE) out->n_reps = hmisc[M_NREP];
         rep_filtered = (uint64_t)n - hmisc[M_S0] - grid_filtered;
         offu.assign(h, h + P + 1);

@@ -258,9 +258,12 @@ size_t random_cub_bytes(uint32_t n);
 // or null for the single-CTA stream.
 constexpr uint32_t kJumpLog2 = 14;
 inline uint32_t mt_jump_chunks(uint32_t n) { return n < 2 ? 0u : ((n - 1) + (1u << kJumpLog2) - 1) >> kJumpLog2; }
+// flag_dev: when given, a rejected draw only sets *flag_dev (no sync; the
+// caller checks it later and redoes the run); otherwise the function syncs,
+// and returns false on a rejection (nothing written).
 bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, void* scratch, void* cub_tmp,
                           size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches,
-                          const uint32_t* jump_table = nullptr);
+                          const uint32_t* jump_table = nullptr, uint32_t* flag_dev = nullptr);
 // host: jump polynomials t^(k 2^log2_stride) mod phi, k = 1..chunks (mtjump.cpp)
 const uint32_t* mt_jump_table(uint32_t log2_stride, uint32_t chunks);
 int mt_jump_words();

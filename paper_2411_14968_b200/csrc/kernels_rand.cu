@@ -164,9 +164,11 @@ __global__ void __launch_bounds__(1024) k_mt_jump(const uint64_t* __restrict__ x
     mt_generate(A, B, cnt, out + base);
 }
 
-// step i = n - k: j_i = x_k mod i, key (j_i << 32 | i); flag a rejected draw
-__global__ void k_fy_draws(const uint64_t* __restrict__ x, uint32_t n, uint64_t* __restrict__ key,
-                           uint32_t* __restrict__ jv, uint32_t* flag) {
+// step i = n - k: j_i = x_k mod i; flag a rejected draw. The (j, i) pairs
+// are stored in ascending-i order (slot m-1-k), so a stable sort by j alone
+// leaves every S_p in ascending step order.
+__global__ void k_fy_draws(const uint64_t* __restrict__ x, uint32_t n, uint32_t* __restrict__ jkey,
+                           uint32_t* __restrict__ ival, uint32_t* __restrict__ jv, uint32_t* flag) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k + 1 >= n) return;  // n-1 steps
     const uint64_t i = (uint64_t)n - k;
@@ -175,33 +177,36 @@ __global__ void k_fy_draws(const uint64_t* __restrict__ x, uint32_t n, uint64_t*
     if (v >= limit) atomicOr(flag, 1u);
     const uint32_t j = (uint32_t)(v % i);
     jv[k] = j;
-    key[k] = ((uint64_t)j << 32) | (uint32_t)i;
+    const uint32_t slot = n - 2 - k;  // m - 1 - k
+    jkey[slot] = j;
+    ival[slot] = (uint32_t)i;
 }
 
-__global__ void k_fy_heads(const uint64_t* __restrict__ key, uint32_t m, uint32_t* __restrict__ head) {
+__global__ void k_fy_heads(const uint32_t* __restrict__ sj, uint32_t m, uint32_t* __restrict__ head) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= m) return;
-    const uint32_t p = (uint32_t)(key[q] >> 32);
-    if (q == 0 || (uint32_t)(key[q - 1] >> 32) != p) head[p] = q;
+    const uint32_t p = sj[q];
+    if (q == 0 || sj[q - 1] != p) head[p] = q;
 }
 
 // gnext[i]: next larger step in S_{j_i}; f pointers for every step i.
-__global__ void k_fy_ptrs(const uint64_t* __restrict__ key, uint32_t m, const uint32_t* __restrict__ head, uint32_t n,
-                          uint32_t* __restrict__ gnext, uint32_t* __restrict__ fptr, uint32_t* __restrict__ fval) {
+__global__ void k_fy_ptrs(const uint32_t* __restrict__ sj, const uint32_t* __restrict__ si, uint32_t m,
+                          const uint32_t* __restrict__ head, uint32_t n, uint32_t* __restrict__ gnext,
+                          uint32_t* __restrict__ fptr, uint32_t* __restrict__ fval) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q < m) {
-        const uint32_t p = (uint32_t)(key[q] >> 32), i = (uint32_t)key[q];
-        gnext[i] = (q + 1 < m && (uint32_t)(key[q + 1] >> 32) == p) ? (uint32_t)key[q + 1] : kNone;
+        const uint32_t p = sj[q], i = si[q];
+        gnext[i] = (q + 1 < m && sj[q + 1] == p) ? si[q + 1] : kNone;
     }
     const uint32_t i = q + 2;  // steps 2..n
     if (i <= n) {
         const uint32_t h = head[i - 1];
         uint32_t v = kNone;
         if (h != kNone) {
-            v = (uint32_t)key[h];
+            v = si[h];
             if (v == i) {
                 const uint32_t h2 = h + 1;
-                v = (h2 < m && (uint32_t)(key[h2] >> 32) == i - 1) ? (uint32_t)key[h2] : kNone;
+                v = (h2 < m && sj[h2] == i - 1) ? si[h2] : kNone;
             }
         }
         if (v == kNone) {
@@ -246,13 +251,13 @@ __global__ void k_fy_jump(uint32_t n, uint32_t* __restrict__ fptr, uint32_t* __r
 // perm[k] (k >= 1) = g(k+1); perm[0] = value at 0 after its last touch.
 __global__ void k_fy_final(uint32_t n, uint64_t p, const uint32_t* __restrict__ jv, const uint32_t* __restrict__ gnext,
                            const uint32_t* __restrict__ fval, const uint32_t* __restrict__ head,
-                           const uint64_t* __restrict__ key, uint32_t* __restrict__ pid) {
+                           const uint32_t* __restrict__ si, uint32_t* __restrict__ pid) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     uint32_t v;
     if (k == 0) {
         const uint32_t h = head[0];
-        v = h == kNone ? 0u : fval[(uint32_t)key[h]];
+        v = h == kNone ? 0u : fval[si[h]];
     } else {
         const uint32_t i = k + 1;
         const uint32_t gn = gnext[i];
@@ -273,7 +278,7 @@ size_t random_scratch_bytes(uint32_t n) {
 // reproduces the shuffle on the host. Synchronizes once to read the flag.
 bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, void* scratch, void* cub_tmp,
                           size_t cub_bytes, int sm_count, cudaStream_t st, uint32_t* launches,
-                          const uint32_t* jump_table) {
+                          const uint32_t* jump_table, uint32_t* flag_dev) {
     if (n == 0) return true;
     if (n == 1) {
         SKY_CUDA(cudaMemsetAsync(pid, 0, sizeof(uint32_t), st));
@@ -281,8 +286,12 @@ bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, 
     }
     char* s = static_cast<char*>(scratch);
     uint64_t* x = reinterpret_cast<uint64_t*>(s);
-    uint64_t* key = x + n;
-    uint64_t* key2 = key + n;
+    uint64_t* key = x + n;   // jkey | ival (and the jump prefix before them)
+    uint64_t* key2 = key + n;  // sj | si
+    uint32_t* jkey = reinterpret_cast<uint32_t*>(key);
+    uint32_t* ival = jkey + n;
+    uint32_t* sj = reinterpret_cast<uint32_t*>(key2);
+    uint32_t* si = sj + n;
     uint32_t* jv = reinterpret_cast<uint32_t*>(key2 + n);
     uint32_t* head = jv + n;
     uint32_t* gnext = head + n;
@@ -304,15 +313,15 @@ bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, 
     } else {
         k_mt64<<<1, 160, 0, st>>>(seed, m, x, nullptr);
     }
-    k_fy_draws<<<ceil_div(m, 256), 256, 0, st>>>(x, n, key, jv, misc);
-    int end_bit = 32;
-    while (end_bit < 64 && (uint64_t{1} << (end_bit - 32)) < n) ++end_bit;
+    k_fy_draws<<<ceil_div(m, 256), 256, 0, st>>>(x, n, jkey, ival, jv, flag_dev ? flag_dev : misc);
+    int end_bit = 1;
+    while (end_bit < 32 && (uint64_t{1} << end_bit) < n) ++end_bit;  // j < n
     size_t need = 0;
-    SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, key, key2, (int)m, 0, end_bit, st));
+    SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, jkey, sj, ival, si, (int)m, 0, end_bit, st));
     if (need > cub_bytes) throw Error(SKY_E_INTERNAL, "cub scratch too small for the random partitioner");
-    SKY_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, need, key, key2, (int)m, 0, end_bit, st));
-    k_fy_heads<<<ceil_div(m, 256), 256, 0, st>>>(key2, m, head);
-    k_fy_ptrs<<<ceil_div(n, 256), 256, 0, st>>>(key2, m, head, n, gnext, fptr, fval);
+    SKY_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, need, jkey, sj, ival, si, (int)m, 0, end_bit, st));
+    k_fy_heads<<<ceil_div(m, 256), 256, 0, st>>>(sj, m, head);
+    k_fy_ptrs<<<ceil_div(n, 256), 256, 0, st>>>(sj, si, m, head, n, gnext, fptr, fval);
     {
         int per_sm = 0;
         SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fy_jump, 256, 0));
@@ -322,9 +331,10 @@ bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, 
         void* args[] = {&nn, &fptr, &fval, &pending};
         SKY_CUDA(cudaLaunchCooperativeKernel((void*)k_fy_jump, grid, 256, args, 0, st));
     }
-    k_fy_final<<<ceil_div(n, 256), 256, 0, st>>>(n, p, jv, gnext, fval, head, key2, pid);
+    k_fy_final<<<ceil_div(n, 256), 256, 0, st>>>(n, p, jv, gnext, fval, head, si, pid);
     SKY_LAUNCH_CHECK();
     if (launches) *launches += 7 + 4;
+    if (flag_dev) return true;  // the caller checks the rejection flag at its next round trip
     uint32_t flag = 0;
     SKY_CUDA(cudaMemcpyAsync(&flag, misc, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     SKY_CUDA(cudaStreamSynchronize(st));
@@ -334,8 +344,8 @@ bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, 
 size_t random_cub_bytes(uint32_t n) {
     if (n < 2) return 16;
     size_t need = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, need, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)(n - 1), 0, 64,
-                                   (cudaStream_t)0);
+    cub::DeviceRadixSort::SortPairs(nullptr, need, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n - 1), 0, 32, (cudaStream_t)0);
     return need;
 }
 
