@@ -1096,8 +1096,12 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     uint32_t* amb = R.dev<uint32_t>(S_AMB, amb_cap);
     uint32_t* skA = nullptr;
     if (strategy == SKY_SLICED) skA = R.dev<uint32_t>(S_SK_A, n);
+    // sort key (pid << 32 | skey): with skey's low pb bits cleared the sort
+    // needs 32 key bits (4 radix passes) for P <= 2^12 partitions
+    const int pb = std::max(1, bits_for(P));
+    const uint32_t key_shift = pb <= 12 ? (uint32_t)pb : 0u;
     PrepArgs pa{pts, R.x64_.x, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA, idxA, skA,
-                misc + M_ERR, misc + M_AMB, amb, amb_cap};
+                misc + M_ERR, misc + M_AMB, amb, amb_cap, key_shift};
     launch_prep(pa, st);
     R.count();
 
@@ -1207,8 +1211,8 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     }
 
     // one radix sort by (pid, sum key); stable, so ties keep row order
-    const int end_bit = 32 + std::max(1, bits_for(P));
-    R.sort_pairs(keyA, keyB, idxA, idxB, n, 0, std::min(64, end_bit));
+    const int end_bit = 32 + pb;
+    R.sort_pairs(keyA, keyB, idxA, idxB, n, (int)key_shift, std::min(64, end_bit));
     uint32_t* off = R.dev<uint32_t>(S_OFF_A, P + 1);
     launch_seg_offsets(keyB, n, (uint32_t)P, off, st);
     R.count();
@@ -1500,7 +1504,8 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         uint8_t* dead_row = R.dev<uint8_t>(S_DEADROW, n);
         if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,
                                            reps.id, reps.n, nrep_dev, pthr, dead_row, dead,
-                                           count_tests ? R.tests(1) : nullptr, R.x64_, c->smem_optin, st)) {
+                                           count_tests ? R.tests(1) : nullptr, R.x64_, c->smem_optin, st,
+                                           (uint64_t)n * d * sizeof(float) <= (48ull << 20))) {
             R.count();
             any_dead = true;
         } else if (reps.n > 0) {
@@ -1514,7 +1519,9 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             RelskyArgs fa{};
             fa.cxyz = pts; fa.cskey = reinterpret_cast<const uint32_t*>(po.key64); fa.cidx = po.idx; fa.cd = d;
             fa.sid = reps.id;
-            fa.indirect = true; fa.sxyz = reps.xyz; fa.sskey = reps.skey; fa.bounded = true; fa.dead = dead;
+            // candidate keys are truncated (key_shift), the reps' are not:
+            // no key bound across the two
+            fa.indirect = true; fa.sxyz = reps.xyz; fa.sskey = reps.skey; fa.bounded = false; fa.dead = dead;
             fa.tests = count_tests ? R.tests(1) : nullptr;
             R.relsky(D, pf, fa);
             any_dead = true;
@@ -1992,7 +1999,7 @@ int sky_relative_skyline(sky_ctx* c, const float* r, uint64_t nr64, const float*
         uint64_t* key = R.dev<uint64_t>(S_KEY_A, nr + nc);
         uint32_t* idx = R.dev<uint32_t>(S_IDX_A, nr + nc);
         PrepArgs pa{dp, nullptr, nr + nc, d, SKY_SLICED + 100, 0, 0, nullptr, 0, key, idx, nullptr, misc + M_ERR,
-                    misc + M_AMB, nullptr, 0};
+                    misc + M_AMB, nullptr, 0, 0};
         launch_prep(pa, st);
         // comparators sorted by sum key
         uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, nc);

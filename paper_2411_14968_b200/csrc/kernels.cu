@@ -152,7 +152,9 @@ __global__ void k_prep(PrepArgs a) {
         atomicOr(a.err, err);
         pid = 0;  // the run fails at its next host check; keep every index in bounds
     }
-    const uint32_t skey = __float_as_uint(__double2float_rn(sum));  // monotone in sum
+    // monotone in sum; truncation keeps it monotone (and the partition sort
+    // one radix pass shorter)
+    const uint32_t skey = __float_as_uint(__double2float_rn(sum)) & ~((1u << a.key_shift) - 1u);
     a.key64[i] = (pid << 32) | skey;
     a.idx[i] = i;
 }
@@ -401,6 +403,48 @@ __global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* _
     }
     // select `need` smallest of the run under the exact order
     __shared__ uint32_t s_best[32];
+    constexpr uint32_t RUN_SMEM = 1024;
+    if (rb - ra <= RUN_SMEM) {
+        // the run's FP64 sums once, into shared memory; then `need` rounds of
+        // block argmin over (sum, lex coords, id) with lex only on equal sums
+        __shared__ double s_sum[RUN_SMEM];
+        __shared__ uint32_t s_rowr[RUN_SMEM];
+        __shared__ uint8_t s_taken[RUN_SMEM];
+        const uint32_t L = rb - ra;
+        for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+            const uint32_t row = idx[ra + e];
+            s_rowr[e] = row;
+            s_sum[e] = row_sum(pts, d, row);
+            s_taken[e] = 0;
+        }
+        __syncthreads();
+        auto less = [&](uint32_t x, uint32_t y) {  // run slots
+            if (s_sum[x] != s_sum[y]) return s_sum[x] < s_sum[y];
+            return lex_less(pts, d, s_rowr[x], s_rowr[y]);
+        };
+        for (uint32_t r = 0; r < need; ++r) {
+            uint32_t best = kNone;
+            for (uint32_t e = threadIdx.x; e < L; e += blockDim.x)
+                if (!s_taken[e] && (best == kNone || less(e, best))) best = e;
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint32_t other = __shfl_down_sync(0xffffffffu, best, o);
+                if (other != kNone && (best == kNone || less(other, best))) best = other;
+            }
+            if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t bb = kNone;
+                for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+                    const uint32_t o = s_best[w];
+                    if (o != kNone && (bb == kNone || less(o, bb))) bb = o;
+                }
+                s_taken[bb] = 1;
+                out[ra - a + r] = s_rowr[bb];
+            }
+            __syncthreads();
+        }
+        return;
+    }
     uint32_t last = kNone;
     for (uint32_t r = 0; r < need; ++r) {
         uint32_t best = kNone;
@@ -586,18 +630,30 @@ __global__ void __launch_bounds__(THREADS) k_rep_finalize(const uint32_t* __rest
         s_key[i] = __float_as_uint(__double2float_rn(sum));
     }
     __syncthreads();
-    // 3. key order by ranks (stable: ties keep slot order); the antichain
-    //    test of step 4 runs in the same pass
-    unsigned long long nt = 0;
+    // 3. key order by ranks (stable: ties keep slot order)
     for (uint32_t i = t; i < n; i += THREADS) {
         const uint32_t ki = s_key[i];
-        const float4* ti = s_xyz + (size_t)i * V;
         uint32_t rank = 0;
-        bool dom = false;
         for (uint32_t j = 0; j < n; ++j) {
             const uint32_t kj = s_key[j];
             rank += (kj < ki) | ((kj == ki) & (j < i));
-            if (dom || j == i || kj > ki) continue;  // a dominator has a key <= ki
+        }
+        s_ord[rank] = i;
+    }
+    __syncthreads();
+    // 4. antichain: a candidate meets the candidates in key order up to its
+    //    own key (a dominator's key is <= its own) and stops at the first
+    //    dominator; the strongest candidates come first, so most stop early
+    unsigned long long nt = 0;
+    for (uint32_t pi = t; pi < n; pi += THREADS) {
+        const uint32_t i = s_ord[pi];
+        const uint32_t ki = s_key[i];
+        const float4* ti = s_xyz + (size_t)i * V;
+        bool dom = false;
+        for (uint32_t pj = 0; pj < n && !dom; ++pj) {
+            const uint32_t j = s_ord[pj];
+            if (s_key[j] > ki) break;
+            if (j == i) continue;
             ++nt;
             const float4* sj = s_xyz + (size_t)j * V;
             bool gt = false, lt = false;
@@ -609,7 +665,6 @@ __global__ void __launch_bounds__(THREADS) k_rep_finalize(const uint32_t* __rest
             }
             dom = !gt && (x64.x ? dom64(x64, s_row[j], s_row[i]) : lt);
         }
-        s_ord[rank] = i;
         s_dead[i] = dom;
     }
     __syncthreads();

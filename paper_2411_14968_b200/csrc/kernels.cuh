@@ -59,6 +59,7 @@ struct PrepArgs {
     uint32_t* amb_count;     // out (angular): boundary points
     uint32_t* amb_list;
     uint32_t amb_cap;
+    uint32_t key_shift;      // low bits of skey cleared (the partition sort skips them)
 };
 void launch_prep(const PrepArgs& a, cudaStream_t st);
 
@@ -244,7 +245,7 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey,
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
                       const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,
                       const uint32_t* nrep_dev, const float* thr, uint8_t* dead_row, uint8_t* dead_pos,
-                      unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st);
+                      unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st, bool posorder = true);
 // Quantization thresholds from a strided sample of row-major input rows.
 void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st);
 // Skyline of one small set in one CTA (false: too big, use k_relsky).

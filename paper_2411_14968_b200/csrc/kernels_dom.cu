@@ -943,7 +943,7 @@ void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey,
 bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, uint32_t n, const float* rep_xyz,
                       const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,
                       const uint32_t* nrep_dev, const float* thr, uint8_t* dead_row, uint8_t* dead_pos,
-                      unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {
+                      unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st, bool posorder) {
     if (D > 16) return false;
     const bool codes = rep_qc && thr && nrep >= 32;
     const size_t npad = (nrep + 7) & ~7u;
@@ -951,13 +951,22 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
     if (smem + 1024 > (size_t)smem_optin) return false;
     if (!n) return true;
     SKY_DISPATCH_D16(D, {
-        if (codes) {
-            // many representatives: sorted positions, flags written in place
+        if (codes && posorder) {
+            // many representatives, input in L2: sorted positions (a warp's
+            // rows have close keys, so its key bound cuts early), flags in place
             SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
             k_prefilter<DT, true, true><<<ceil_div(n, 256), 256, smem, st>>>(
                 pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
                 dead_pos, tests, x64);
+        } else if (codes) {
+            // large input: rows streamed in row order (coalesced), flags
+            // gathered into position order afterwards
+            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            k_prefilter<DT, true, false><<<ceil_div(n, 256), 256, smem, st>>>(
+                pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
+                dead_row, tests, x64);
         } else {
             SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
@@ -967,7 +976,7 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
         }
     });
     SKY_LAUNCH_CHECK();
-    if (codes) return true;
+    if (codes && posorder) return true;
     k_gather_dead<<<ceil_div(n, 256), 256, 0, st>>>(idx, dead_row, n, dead_pos);
     SKY_LAUNCH_CHECK();
     return true;
