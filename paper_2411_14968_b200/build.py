@@ -42,7 +42,7 @@ def _newer(src_list, target):
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "skyline_b200.h")]
-    objs = []
+    objs, jobs = [], []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
@@ -52,13 +52,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if s.endswith(".cpp"):
                 flags = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                          "-I", os.path.join(ROOT, "include")]
-            cmd = [NVCC, *flags, "-c", src, "-o", obj]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {s}")
-            if verbose:
-                sys.stderr.write(r.stderr)
+            jobs.append((s, [NVCC, *flags, "-c", src, "-o", obj]))
+    # the translation units compile independently: run them side by side
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: (j[0], subprocess.run(j[1], capture_output=True, text=True)), jobs))
+    for s, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {s}")
+        if verbose:
+            sys.stderr.write(r.stderr)
     if force or _newer(objs, OUT):
         cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-lnccl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
