@@ -21,6 +21,7 @@
 
 #include "skyline/core.hpp"
 #include "skyline/engine.hpp"
+#include "skyline/sequential.hpp"
 #include "skyline_b200.h"
 
 namespace skyline::gpu {
@@ -109,6 +110,25 @@ inline RunResult run(Context& g, const Dataset& r, const EngineConfig& config) {
     m.final_size = res.final_size;
     sky_result_free(&res);
     return out;
+}
+
+// skyline::sfs (sequential.hpp:29) on the GPU: the skyline of one relation,
+// id-sorted. The scoring function only orders the reference's scan, so every
+// monotone score gives the same set; VolumeComplement is monotone on [0,1]
+// coordinates only (sequential.hpp:14-16) and is accepted there.
+inline SkylineSet sfs(Context& g, const Dataset& r, Scoring f = Scoring::Sum) {
+    if (f == Scoring::VolumeComplement)
+        for (const Point& t : r.points)
+            for (double v : t.coords)
+                if (!(v >= 0.0 && v <= 1.0))
+                    throw NormalizationError("VolumeComplement scoring needs coordinates in [0,1]");
+    Dataset copy = r;
+    copy.normalized = false;  // any finite non-negative data (sky_skyline semantics)
+    EngineConfig one;         // one sliced partition, no filter: Sky(r) itself
+    one.partition.strategy = Strategy::Sliced;
+    one.partition.p = 1;
+    RunResult res = run(g, copy, one);
+    return std::move(res.skyline);
 }
 
 }  // namespace skyline::gpu

@@ -85,7 +85,31 @@ def build_cli(force: bool = False) -> str:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("skyline-cli build failed")
+    build_adapter_check(force)
     return CLI
+
+
+def build_adapter_check(force: bool = False):
+    """tools/adapter_check.cpp -> paper_2411_14968_b200/adapter-check: the
+    drop-in adapter against the reference engine (oracle/_ref, the checker),
+    built where the reference headers exist; the binary travels to the GPU."""
+    ref_inc = "/root/reference/proj/include"
+    ref_so = os.path.join(ROOT, "oracle", "_ref", "libskyref.so")
+    src = os.path.join(ROOT, "tools", "adapter_check.cpp")
+    out = os.path.join(PKG, "adapter-check")
+    if not (os.path.isdir(ref_inc) and os.path.exists(ref_so)):
+        return None
+    deps = [src, ref_so, OUT, os.path.join(ROOT, "adapters", "skyline_gpu.hpp")]
+    if force or _newer(deps, out):
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-O2", "-std=c++20", "-I", ref_inc, "-I", os.path.join(ROOT, "include"), "-I",
+               os.path.join(ROOT, "adapters"), src, "-o", out, "-L", PKG, "-lskyline_b200", "-L",
+               os.path.dirname(ref_so), "-lskyref", "-Wl,-rpath,$ORIGIN:$ORIGIN/../oracle/_ref"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("adapter-check build failed")
+    return out
 
 
 def main():

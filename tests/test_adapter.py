@@ -37,3 +37,17 @@ int main(int argc, char**) {
                         "-I", os.path.join(ROOT, "adapters"), p, "-L", libdir, "-lskyline_b200",
                         f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
         assert subprocess.run([exe]).returncode == 0
+
+
+@pytest.mark.gpu
+def test_adapter_matches_reference_on_gpu():
+    """The prebuilt adapter-check binary (tools/adapter_check.cpp, built where
+    the reference headers exist) runs skyline::run (the reference, as the
+    checker) and skyline::gpu::run on the same Datasets of the reference's
+    generator and compares skylines and metrics."""
+    exe = os.path.join(ROOT, "paper_2411_14968_b200", "adapter-check")
+    if not os.path.exists(exe):
+        pytest.skip("adapter-check not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "0 mismatches" in r.stdout
