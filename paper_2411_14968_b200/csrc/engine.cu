@@ -68,6 +68,9 @@ struct sky_ctx {
     // device copy of the mt19937_64 jump polynomials (random partitioner)
     uint32_t* mt_jump = nullptr;
     uint32_t mt_jump_rows = 0;
+    // SKY_PROFILE_TIMELINE: an event after every counted launch (host issue
+    // time + device completion time), printed when the run drains
+    std::vector<cudaEvent_t> tl_ev;
 };
 
 namespace {
@@ -80,7 +83,7 @@ enum Slot {
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
     S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
-    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_COUNT
+    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -324,7 +327,8 @@ class Runner {
     T* dev(int slot, size_t n) { return c_->dev.as<T>(slot, n ? n : 1); }
     template <class T>
     T* pin(int slot, size_t n) { return c_->pin.as<T>(slot, n ? n : 1); }
-    void sync() {
+    void sync(int line = __builtin_LINE()) {
+        if (tl_) mark(-line);
         SKY_CUDA(cudaStreamSynchronize(st_));
         if (prof_) {
             const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start_).count();
@@ -334,7 +338,36 @@ class Runner {
     bool prof_ = std::getenv("SKY_PROFILE_HOST") != nullptr;
     int n_sync_ = 0;
     std::chrono::steady_clock::time_point t_start_ = std::chrono::steady_clock::now();
-    void count(int k = 1) { c_->launches += k; }
+    void count(int k = 1, int line = __builtin_LINE()) {
+        c_->launches += k;
+        if (tl_) mark(line);
+    }
+    bool tl_ = std::getenv("SKY_PROFILE_TIMELINE") != nullptr;
+    std::vector<std::pair<int, double>> tl_marks_;
+    void mark(int line) {
+        auto& e = c_->tl_ev;
+        if (e.size() <= tl_marks_.size()) {
+            cudaEvent_t ev;
+            SKY_CUDA(cudaEventCreate(&ev));
+            e.push_back(ev);
+        }
+        SKY_CUDA(cudaEventRecord(e[tl_marks_.size()], st_));
+        tl_marks_.emplace_back(
+            line, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start_).count());
+    }
+    // after the stream drained: line, host issue ms, device ms (from the first mark)
+    void timeline_dump() {
+        if (!tl_ || tl_marks_.empty()) return;
+        float prev = 0.f;
+        for (size_t k = 0; k < tl_marks_.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c_->tl_ev[0], c_->tl_ev[k]);
+            std::fprintf(stderr, "TL %3zu line %5d host %8.3f dev %8.3f (+%7.3f)\n", k, tl_marks_[k].first,
+                         tl_marks_[k].second, ms, ms - prev);
+            prev = ms;
+        }
+        tl_marks_.clear();
+    }
 
     DevSet set(int base, uint32_t n, int D) {
         DevSet s;
@@ -1395,6 +1428,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
 
     Runner R(c);
     cudaStream_t st = c->stream;
+    if (R.tl_) R.mark(__LINE__);
 
     SKY_CUDA(cudaEventRecord(c->ev[0], st));
     uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
@@ -1676,18 +1710,9 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         // angular pd_i is every other local (engine.cpp:98-103) and u_i is an
         // antichain, so testing against all of U is the same relation;
         // merge_sequential (engine.cpp:65-72) is Sky(U) by definition.
+        // U's partitions are runs sorted by key: one stable P-way merge
         US = R.set(S_SET3, U.n, D);
-        uint32_t* iota = R.dev<uint32_t>(S_PERM_A, U.n);
-        uint32_t* perm = R.dev<uint32_t>(S_PERM_B, U.n);
-        uint32_t* sk2 = R.dev<uint32_t>(S_SKTMP, U.n);
-        {
-            // iota on device: exclusive scan of all-live flags
-            uint8_t* z = R.dev<uint8_t>(S_DEAD, U.n);
-            launch_fill_u8(z, 0, U.n, st);
-            R.scan_live(z, iota, U.n);
-        }
-        R.sort_pairs(U.skey, sk2, iota, perm, U.n, 0, 32);
-        launch_gather_set(D, U, perm, US, st);
+        launch_merge_runs(D, U, offu_dev, P, US, st);
         R.count();
         ma.sxyz = US.xyz; ma.sskey = US.skey; ma.sid = US.id;
     } else if (P > 1) {
@@ -1737,24 +1762,24 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     // surviving ids of this rank's candidates, ascending (engine.cpp:128-133)
     const uint32_t cb = global_cands ? 0 : offu[qb], cn = global_cands ? U.n : offu[qe] - cb;
     const uint32_t* cand_ids = global_cands ? US.id : U.id;
-    uint32_t* pos = R.dev<uint32_t>(S_POS, cn);
-    R.scan_live(fdead + cb, pos, cn);
-    launch_count_total(pos, fdead + cb, cn, misc + M_TOTAL, st);
-    R.count();
     uint32_t* hm = R.pin<uint32_t>(P_MISC, 32);
     uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, std::max<uint32_t>(cn, 1));
     uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, std::max<uint32_t>(cn, 1));
     uint32_t nf = 0, n_copy = 0;
     uint32_t* final_ids = idsB;
     if (W == 1) {
-        // no round trip: the ids fill a cn-slot buffer (unused slots all ones,
-        // sorted last) and the count travels back with them
-        SKY_CUDA(cudaMemsetAsync(idsA, 0xFF, (size_t)cn * sizeof(uint32_t), st));
-        launch_compact_ids(cand_ids + cb, fdead + cb, pos, cn, idsA, st);
-        R.count();
-        R.sort_keys(idsA, idsB, cn, std::max(1, bits_for(n)));  // ids < n
+        // no round trip: ascending ids through a bitmap over the row ids,
+        // written into a cn-slot buffer; the count travels back with them
+        uint32_t* bm = R.dev<uint32_t>(S_BM, (size_t)n / 32 + 1);
+        uint32_t* bt = R.dev<uint32_t>(S_BMT, bm_blocks(n));
+        launch_ids_bitmap(cand_ids + cb, fdead + cb, cn, n, bm, bt, idsB, misc + M_TOTAL, st);
+        R.count(cn ? 3 : 2);
         n_copy = cn;
     } else {
+        uint32_t* pos = R.dev<uint32_t>(S_POS, cn);
+        R.scan_live(fdead + cb, pos, cn);
+        launch_count_total(pos, fdead + cb, cn, misc + M_TOTAL, st);
+        R.count();
         SKY_CUDA(cudaMemcpyAsync(hm, misc + M_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         R.sync();
         const uint32_t nmine = cn ? hm[0] : 0;
@@ -1795,6 +1820,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     out->kernel_launches = c->launches;
     out->dom_launches = c->dom_launches;
     R.dom_collect();
+    R.timeline_dump();
     out->dom_kernel_ms = c->dom_ms;
     out->dom_tests = ht[0] + ht[1] + ht[2];
     out->dom_exact_checks = ht[3] + ht[4] + ht[5] + ht[6];

@@ -813,6 +813,168 @@ void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out
     SKY_LAUNCH_CHECK();
 }
 
+// Stable P-way merge of key-sorted runs (run p = positions off[p]..off[p+1]
+// of `in`) into `out` in global key order: the same permutation as a stable
+// radix sort of the concatenation. One warp per element: lanes binary-search
+// the other runs (runs before p count keys <= k, runs after p keys < k, so
+// equal keys keep run order), the warp sums the ranks and copies the row.
+template <int D>
+__global__ void __launch_bounds__(256) k_merge_runs(DevSet in, const uint32_t* __restrict__ off, uint32_t P,
+                                                    uint32_t n, DevSet out) {
+    constexpr int V = Dims<D>::V;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    // run of element i: the last p with off[p] <= i
+    uint32_t lo = 0, hi = P;  // off[lo] <= i < off[hi]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= i) lo = mid; else hi = mid;
+    }
+    const uint32_t p = lo;
+    const uint32_t k = __ldg(in.skey + i);
+    uint32_t rank = lane == 0 ? i - __ldg(off + p) : 0u;
+    for (uint32_t q = lane; q < P; q += 32) {
+        if (q == p) continue;
+        uint32_t a = __ldg(off + q), b = __ldg(off + q + 1);
+        const uint32_t base = a;
+        if (q < p) {
+            while (a < b) {  // first key > k
+                const uint32_t m = (a + b) >> 1;
+                if (__ldg(in.skey + m) <= k) a = m + 1; else b = m;
+            }
+        } else {
+            while (a < b) {  // first key >= k
+                const uint32_t m = (a + b) >> 1;
+                if (__ldg(in.skey + m) < k) a = m + 1; else b = m;
+            }
+        }
+        rank += a - base;
+    }
+    rank = __reduce_add_sync(0xffffffffu, rank);
+    if (lane < (uint32_t)V)
+        reinterpret_cast<float4*>(out.xyz)[(size_t)rank * V + lane] =
+            reinterpret_cast<const float4*>(in.xyz)[(size_t)i * V + lane];
+    if (lane == 31) {
+        out.skey[rank] = k;
+        out.id[rank] = in.id[i];
+        if (in.qc && out.qc) out.qc[rank] = in.qc[i];
+    }
+}
+
+void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st) {
+    if (!in.n) return;
+    SKY_DISPATCH_D(D, (k_merge_runs<DT><<<ceil_div((uint64_t)in.n * 32, 256), 256, 0, st>>>(in, off, P, in.n, out)));
+    SKY_LAUNCH_CHECK();
+}
+
+// Ascending ids of the live candidates without a sort: a bitmap over the row
+// ids (bit per input row), per-block popcounts, then each block emits its
+// ids at the prefix of the blocks before it. kBmWords words per block.
+constexpr uint32_t kBmWords = 2048;
+
+__global__ void k_bm_set(const uint32_t* __restrict__ id, const uint8_t* __restrict__ dead, uint32_t n,
+                         uint32_t* __restrict__ bm) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || dead[i]) return;
+    const uint32_t v = id[i];
+    atomicOr(bm + (v >> 5), 1u << (v & 31));
+}
+
+__global__ void __launch_bounds__(256) k_bm_count(const uint32_t* __restrict__ bm, uint32_t words,
+                                                  uint32_t* __restrict__ block_tot) {
+    const uint32_t b0 = blockIdx.x * kBmWords;
+    uint32_t c = 0;
+    for (uint32_t w = b0 + threadIdx.x; w < min(words, b0 + kBmWords); w += blockDim.x) c += __popc(bm[w]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ uint32_t s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s[k];
+        block_tot[blockIdx.x] = t;
+    }
+}
+
+// 256 threads x 8 consecutive words per step; `total` (if set) gets the count
+__global__ void __launch_bounds__(256) k_bm_emit(const uint32_t* __restrict__ bm, uint32_t words,
+                                                 const uint32_t* __restrict__ block_tot, uint32_t* __restrict__ out,
+                                                 uint32_t* total) {
+    __shared__ uint32_t s[8];
+    __shared__ uint32_t s_base;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // prefix of the blocks before this one
+    uint32_t pre = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += block_tot[b];
+    pre = __reduce_add_sync(0xffffffffu, pre);
+    if (lane == 0) s[wid] = pre;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s[k];
+        s_base = t;
+        if (total && blockIdx.x == gridDim.x - 1) *total = t + block_tot[blockIdx.x];
+    }
+    __syncthreads();
+    uint32_t base = s_base;
+    const uint32_t b0 = blockIdx.x * kBmWords, b1 = min(words, b0 + kBmWords);
+    for (uint32_t w0 = b0; w0 < b1; w0 += 256 * 8) {
+        uint32_t v[8];
+        uint32_t c = 0;
+        const uint32_t wb = w0 + threadIdx.x * 8;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = wb + k < b1 ? bm[wb + k] : 0u;
+            c += __popc(v[k]);
+        }
+        // block exclusive scan of c
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        __syncthreads();
+        if (lane == 31) s[wid] = x;
+        __syncthreads();
+        uint32_t wpre = 0, all = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            wpre += (uint32_t)k < wid ? s[k] : 0u;
+            all += s[k];
+        }
+        uint32_t o = base + wpre + x - c;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t m = v[k];
+            while (m) {
+                const uint32_t bit = __ffs(m) - 1;
+                m &= m - 1;
+                out[o++] = ((wb + k) << 5) | bit;
+            }
+        }
+        base += all;
+    }
+}
+
+uint32_t bm_blocks(uint32_t n_ids) { return ceil_div(ceil_div(std::max<uint32_t>(n_ids, 1), 32), kBmWords); }
+
+void launch_ids_bitmap(const uint32_t* id, const uint8_t* dead, uint32_t n, uint32_t n_ids, uint32_t* bm,
+                       uint32_t* block_tot, uint32_t* out, uint32_t* total, cudaStream_t st) {
+    const uint32_t words = ceil_div(std::max<uint32_t>(n_ids, 1), 32);
+    SKY_CUDA(cudaMemsetAsync(bm, 0, (size_t)words * sizeof(uint32_t), st));
+    if (n) {
+        k_bm_set<<<ceil_div(n, 256), 256, 0, st>>>(id, dead, n, bm);
+        SKY_LAUNCH_CHECK();
+    }
+    const uint32_t blocks = bm_blocks(n_ids);
+    k_bm_count<<<blocks, 256, 0, st>>>(bm, words, block_tot);
+    SKY_LAUNCH_CHECK();
+    k_bm_emit<<<blocks, 256, 0, st>>>(bm, words, block_tot, out, total);
+    SKY_LAUNCH_CHECK();
+}
+
 __global__ void k_remap_offsets(const uint32_t* __restrict__ off_old, uint32_t P, const uint32_t* __restrict__ pos,
                                 const uint8_t* __restrict__ dead, uint32_t n, uint32_t* off_new) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;

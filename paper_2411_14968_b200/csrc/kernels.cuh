@@ -113,6 +113,12 @@ void launch_scatter_indirect(int D, const float* pts, uint32_t d, const uint32_t
 void launch_gather_rows(int D, const float* pts, const double* pts64, uint32_t d, const uint32_t* rows, uint32_t n,
                         DevSet out, cudaStream_t st);
 void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st);
+// stable merge of the key-sorted runs off[P+1] of `in` into `out` (key order)
+void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st);
+// ascending ids (< n_ids) of the live entries of id[n] via a bitmap; count in *total
+uint32_t bm_blocks(uint32_t n_ids);
+void launch_ids_bitmap(const uint32_t* id, const uint8_t* dead, uint32_t n, uint32_t n_ids, uint32_t* bm,
+                       uint32_t* block_tot, uint32_t* out, uint32_t* total, cudaStream_t st);
 void launch_remap_offsets(const uint32_t* off_old, uint32_t P, const uint32_t* pos, const uint8_t* dead,
                           uint32_t n, uint32_t* off_new, cudaStream_t st);
 void launch_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, uint32_t* total, cudaStream_t st);
