@@ -71,6 +71,9 @@ struct sky_ctx {
     // SKY_PROFILE_TIMELINE: an event after every counted launch (host issue
     // time + device completion time), printed when the run drains
     std::vector<cudaEvent_t> tl_ev;
+    // host round trips: spin on an event instead of a blocking stream sync
+    // (the wake-up of cudaStreamSynchronize costs ~15-20 us per round trip)
+    cudaEvent_t sync_ev = nullptr;
 };
 
 namespace {
@@ -83,7 +86,7 @@ enum Slot {
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
     S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
-    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_COUNT
+    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -102,7 +105,10 @@ constexpr uint32_t kExactCapRows = 0;
 enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_NITEMS = 7, M_TESTS = 8 /* 4 x u64 */,
        M_HITS = 16 /* 4 x u64, per phase */,
        M_S0 = 24, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */,
-       M_RFLAG = 28 /* random partitioner: a draw the reference would reject */ };
+       M_RFLAG = 28 /* random partitioner: a draw the reference would reject */,
+       M_OVF = 29 /* stream path: a representative candidate bucket overflowed */ };
+// stream path (representative filter over large inputs): candidate bucket size
+constexpr uint32_t kRepBucket = 1024;
 
 uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;
@@ -329,7 +335,13 @@ class Runner {
     T* pin(int slot, size_t n) { return c_->pin.as<T>(slot, n ? n : 1); }
     void sync(int line = __builtin_LINE()) {
         if (tl_) mark(-line);
-        SKY_CUDA(cudaStreamSynchronize(st_));
+        if (!c_->sync_ev) SKY_CUDA(cudaEventCreateWithFlags(&c_->sync_ev, cudaEventDisableTiming));
+        SKY_CUDA(cudaEventRecord(c_->sync_ev, st_));
+        while (true) {
+            const cudaError_t e = cudaEventQuery(c_->sync_ev);
+            if (e == cudaSuccess) break;
+            if (e != cudaErrorNotReady) SKY_CUDA(e);
+        }
         if (prof_) {
             const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start_).count();
             std::fprintf(stderr, "  sync #%d at %.3f ms\n", ++n_sync_, t);
@@ -1116,7 +1128,8 @@ struct PartitionOut {
 // Phase 1a: partition ids, sum keys, validation, sort into partitions.
 PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d, int normalized, int strategy,
                              uint64_t P, uint64_t m, const sky_config* cfg, const uint32_t* pid_dev,
-                             uint64_t* fixups, bool eager = true, uint32_t** scan_rows = nullptr) {
+                             uint64_t* fixups, bool eager = true, uint32_t** scan_rows = nullptr,
+                             bool sort_rows = true, uint32_t* gmin = nullptr) {
     cudaStream_t st = R.st_;
     uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, n);
     uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, n);
@@ -1133,9 +1146,13 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     // needs 32 key bits (4 radix passes) for P <= 2^12 partitions
     const int pb = std::max(1, bits_for(P));
     const uint32_t key_shift = pb <= 12 ? (uint32_t)pb : 0u;
-    PrepArgs pa{pts, R.x64_.x, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA, idxA, skA,
-                misc + M_ERR, misc + M_AMB, amb, amb_cap, key_shift};
-    launch_prep(pa, st);
+    PrepArgs pa{pts, R.x64_.x, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA,
+                sort_rows ? idxA : nullptr, skA, misc + M_ERR, misc + M_AMB, amb, amb_cap, key_shift};
+    if (gmin) {
+        pa.gmin = gmin;
+        pa.P = (uint32_t)P;
+    }
+    launch_prep(pa, st, R.c_->sm_count);
     R.count();
 
     // errors + angular boundary points (one host round trip). Deferred mode
@@ -1243,6 +1260,9 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
         }
     }
 
+    // stream path: the keys stay in row order (only the survivors of the
+    // representative filter are sorted, run_impl)
+    if (!sort_rows) return PartitionOut{keyA, nullptr, nullptr};
     // one radix sort by (pid, sum key); stable, so ties keep row order
     const int end_bit = 32 + pb;
     R.sort_pairs(keyA, keyB, idxA, idxB, n, (int)key_shift, std::min(64, end_bit));
@@ -1459,9 +1479,30 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed, defer_rand) : nullptr;
     const bool rep_random = cfg->filter == SKY_FILTER_REPRESENTATIVE && cfg->rep_selection == SKY_REPS_RANDOM;
     uint32_t* scan_rows = nullptr;  // sliced + random reps: split()'s exact scan order
+    // Stream path (single GPU, sorted representatives, large input): no sort
+    // of every row. Representatives come from per-partition candidate
+    // buckets, the prefilter streams the rows in row order and appends the
+    // survivors' (partition, key, row) sort keys, and only the survivors are
+    // sorted into partitions. The same s0 as the sorted path (stable order).
+    bool stream = false;
+    {
+        const int pb = std::max(1, bits_for(P));
+        const char* env = std::getenv("SKY_STREAM");
+        const bool want = env ? env[0] == '1' : (uint64_t)n * d * sizeof(float) > (48ull << 20);
+        stream = want && !eager && c->world == 1 && !f64 && cfg->filter == SKY_FILTER_REPRESENTATIVE &&
+                 cfg->rep_selection == SKY_REPS_SORTED && cfg->strategy != SKY_SLICED && pb <= 12 &&
+                 (uint64_t)P * std::min<uint64_t>(cfg->rep_q, n) <= 2048 && cfg->rep_q <= 64 && D <= 16 &&
+                 ((uintptr_t)pts & 15) == 0 && (uint64_t)P * kRepBucket <= (1ull << 31) &&
+                 32 + bits_for(n) <= 64;
+    }
+    // stream path: the prep pass also leaves each CTA's minimum key per
+    // partition (the representative candidate bound)
+    const uint32_t prep_grid = prep_stream_grid(n, c->sm_count);
+    uint32_t* gmin = stream ? R.dev<uint32_t>(S_GMIN, (size_t)prep_grid * P) : nullptr;
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
                                       &out->angular_host_fixups, eager,
-                                      rep_random && cfg->strategy == SKY_SLICED ? &scan_rows : nullptr);
+                                      rep_random && cfg->strategy == SKY_SLICED ? &scan_rows : nullptr, !stream,
+                                      gmin);
 
     std::vector<uint32_t> off0(P + 1);
     uint8_t* dead = R.dev<uint8_t>(S_DEAD, n);
@@ -1490,7 +1531,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         R.count();
         any_dead = grid_filtered > 0;
         R.sync();
-    } else {
+    } else if (!stream) {
         launch_fill_u8(dead, 0, n, st);
     }
     SKY_CUDA(cudaEventRecord(c->ev[1], st));
@@ -1509,6 +1550,16 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         } else if (cfg->rep_selection == SKY_REPS_RANDOM) {
             random_candidates(R, n, po, P, q, cfg->strategy == SKY_SLICED ? scan_rows : nullptr, cfg->rep_seed,
                               cand);
+        } else if (stream) {
+            // candidate buckets (rows under the per-partition key bound),
+            // each sorted by (key, row), then the same exact pick
+            uint32_t* thr = R.dev<uint32_t>(S_PTHR2, P);
+            uint32_t* bcnt = R.dev<uint32_t>(S_BCNT, P);
+            uint64_t* bkey = R.dev<uint64_t>(S_BKEY, (size_t)P * kRepBucket);
+            uint32_t* brow = R.dev<uint32_t>(S_BROW, (size_t)P * kRepBucket);
+                        launch_rep_candidates(po.key64, n, P, q, prep_grid, gmin, thr, kRepBucket, bcnt, bkey, brow, pts, d,
+                                  cand, misc + M_OVF, st);
+            R.count(3);
         } else {
             launch_rep_pick(po.key64, po.idx, po.off, P, pts, R.x64_.x, d, q, cand, st);
             R.count();
@@ -1535,8 +1586,19 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             launch_encode(D, reps, pthr, st, nrep_dev);
             R.count(2);
         }
-        uint8_t* dead_row = R.dev<uint8_t>(S_DEADROW, n);
-        if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,
+        uint8_t* dead_row = stream ? nullptr : R.dev<uint8_t>(S_DEADROW, n);
+        if (stream) {
+            PrefilterAppend app;
+            app.key64 = po.key64;
+            app.out = R.dev<uint64_t>(S_SURV, n);
+            app.count = misc + M_S0;
+            app.key_shift = (uint32_t)std::max(1, bits_for(P));
+            app.row_bits = (uint32_t)std::max(1, bits_for(n));
+            if (!launch_prefilter_append(D, pts, d, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.id, reps.n,
+                                         nrep_dev, pthr, app, count_tests ? R.tests(1) : nullptr, c->smem_optin, st))
+                throw Error(SKY_E_INTERNAL, "stream prefilter not applicable");
+            R.count();
+        } else if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,
                                            reps.id, reps.n, nrep_dev, pthr, dead_row, dead,
                                            count_tests ? R.tests(1) : nullptr, R.x64_, c->smem_optin, st,
                                            (uint64_t)n * d * sizeof(float) <= (48ull << 20))) {
@@ -1572,7 +1634,47 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     DevSet U;
     std::vector<uint32_t> pr(2, 0);
     pr[1] = P;
-    if (W == 1) {
+    if (W == 1 && stream) {
+        // survivors of the stream prefilter: count (round trip), sort by
+        // (partition, key, row), unpack into partition order
+        uint32_t* hc = R.pin<uint32_t>(P_MISC, 32);
+        SKY_CUDA(cudaMemcpyAsync(hc, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        check_prep(hc[M_ERR], hc[M_AMB], cfg->strategy, eager);
+        if (hc[M_OVF]) throw RedoEager{};  // a candidate bucket filled up: sorted path
+        const uint32_t ns = hc[M_S0];
+        const uint32_t rb = (uint32_t)std::max(1, bits_for(n));
+        uint64_t* surv = R.dev<uint64_t>(S_SURV, n);
+        uint64_t* surv2 = R.dev<uint64_t>(S_SURV2, std::max<uint32_t>(ns, 1));
+        R.sort_keys(surv, surv2, ns, 32 + (int)rb);
+        uint64_t* k64 = R.dev<uint64_t>(S_KEY_B, std::max<uint32_t>(ns, 1));
+        uint32_t* rows = R.dev<uint32_t>(S_IDX_B, std::max<uint32_t>(ns, 1));
+        launch_unpack_survivors(surv2, ns, rb, (uint32_t)std::max(1, bits_for(P)), P, k64, rows, off1_dev, st);
+        R.count();
+        s0 = R.set(S_SET0, ns, D);
+        launch_scatter_indirect(D, pts, d, rows, k64, ns, nullptr, nullptr, s0, st);
+        R.count();
+        R.encode_dev(D, s0, misc + M_S0);
+        if (cfg->local_algo == SKY_LOCAL_BNL) {
+            uint32_t used = 0;
+            std::vector<uint32_t> unused;
+            U = R.local_bnl(D, s0, off1_dev, P, cfg->bnl_window_cap, offu_dev, unused, count_tests, &used,
+                            misc + M_U);
+        } else {
+            U = R.local_sfs_dev(D, s0, misc + M_S0, off1_dev, P, offu_dev, misc + M_U, count_tests);
+        }
+        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32);
+        SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        const uint32_t* hmisc = h + P + 1;
+        check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
+        if (defer_rand && hmisc[M_RFLAG]) throw RedoEager{};
+        out->n_reps = hmisc[M_NREP];
+        rep_filtered = (uint64_t)n - ns;
+        offu.assign(h, h + P + 1);
+        U.n = hmisc[M_U];
+    } else if (W == 1) {
         // Single GPU: every count stays on the device until the union of the
         // local skylines is known (one host round trip for this phase).
         uint32_t* pos = R.dev<uint32_t>(S_POS, n);
@@ -1927,6 +2029,9 @@ void sky_ctx_destroy(sky_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& e : c->dom_ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->tl_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->sync_ev) cudaEventDestroy(c->sync_ev);
     for (auto& b : c->stage) cudaFreeHost(b.first);
     if (c->mt_jump) cudaFree(c->mt_jump);
     c->dev.release();

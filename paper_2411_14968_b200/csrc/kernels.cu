@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
+#include "stream.cuh"
 
 namespace sky {
 
@@ -56,32 +57,58 @@ __device__ __forceinline__ uint32_t canon_bits(float v) {
 // no FMA), input validation (core.cpp:21-46, partition.cpp:26-29), partition
 // id for grid (partition.cpp:66-75) and angular (partition.cpp:118-148), and
 // the slicing key for sliced.
-__global__ void k_prep(PrepArgs a) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
-    const float* xf = a.pts + (size_t)i * a.d;
-    const double* xd = a.pts64 ? a.pts64 + (size_t)i * a.d : nullptr;
+// Row accessors of the prep pass: a row in memory (float or FP64 rows,
+// loops not unrolled) or a float row held in registers (loops fully
+// unrolled so every index is static).
+struct MemRow {
+    static constexpr int kUnroll = 1;
+    const float* xf;
+    const double* xd;
+    __device__ __forceinline__ float f(uint32_t j) const { return xf[j]; }
     // every value as the reference sees it (float input upcasts exactly)
-    auto X = [&](uint32_t j) -> double { return xd ? xd[j] : (double)xf[j]; };
+    __device__ __forceinline__ double X(uint32_t j) const { return xd ? xd[j] : (double)xf[j]; }
+};
+template <int DP>
+struct RegRow {
+    static constexpr int kUnroll = DP;
+    float v[DP];
+    __device__ __forceinline__ float f(uint32_t j) const { return v[j]; }
+    __device__ __forceinline__ double X(uint32_t j) const { return (double)v[j]; }
+};
+
+// One row of the prep pass: validation, FP64 sum, partition id, sort key
+// (j < DMAX covers every coordinate: DMAX >= d). Returns the sort key.
+template <int DMAX, class Row>
+__device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, const Row& R) {
+    constexpr int U = Row::kUnroll;
+    const int d = (int)a.d;
     double sum = 0.0;
     uint32_t err = 0;
     uint64_t pid = 0;
     if (a.strategy == SKY_GRID) {
-        uint64_t stride = 1;
-        for (uint32_t j = 0; j < a.d; ++j) {
-            const double v = X(j);
+        // m^d <= kMaxPartitions (2^22): 32-bit cell arithmetic
+        uint32_t stride = 1, pid32 = 0;
+        const uint32_t m32 = (uint32_t)a.m;
+        const double md = (double)a.m;
+#pragma unroll U
+        for (int j = 0; j < DMAX; ++j) {
+            if (j >= d) break;
+            const double v = R.X(j);
             if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
             if (a.normalized && v > 1.0) err |= kErrAboveOne;
             if (!(v >= 0.0 && v <= 1.0)) err |= kErrGridRange;
             sum = __dadd_rn(sum, v);
-            uint64_t cell = (uint64_t)__dmul_rn(v, (double)a.m);
-            if (cell >= a.m) cell = a.m - 1;
-            pid += cell * stride;
-            stride *= a.m;
+            uint32_t cell = __double2uint_rz(__dmul_rn(v, md));  // exact product, floor
+            if (cell >= m32) cell = m32 - 1;
+            pid32 += cell * stride;
+            stride *= m32;
         }
+        pid = pid32;
     } else if (a.strategy == SKY_ANGULAR) {
-        for (uint32_t j = 0; j < a.d; ++j) {
-            const double v = X(j);
+#pragma unroll U
+        for (int j = 0; j < DMAX; ++j) {
+            if (j >= d) break;
+            const double v = R.X(j);
             if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
             if (a.normalized && v > 1.0) err |= kErrAboveOne;
             sum = __dadd_rn(sum, v);
@@ -89,22 +116,30 @@ __global__ void k_prep(PrepArgs a) {
         // hyperspherical_angles: tail sums of squares back to front.
         const double PI = 3.14159265358979323846;
         uint64_t stride_i = 1;
-        for (uint32_t k = 0; k + 1 < a.d; ++k) stride_i *= a.m;  // m^(d-2) for i = d-2
+        for (int k = 0; k + 1 < d; ++k) stride_i *= a.m;  // divided before each use: m^i for slice i
         // FP32 pass first: its slice value is within ~1e-6 relative of the
         // FP64 one, so a value clear of every interior boundary gives the
         // same floor; rows that come near one redo the FP64 computation.
         bool exact64 = false;
         {
             const float fm = (float)a.m, tol = 1e-4f * fmaxf(1.0f, fm / 16.0f);
-            float tail32 = xf[a.d - 1] * xf[a.d - 1];
+            float tail32 = 0.0f;
             uint64_t pid32 = 0, st = stride_i;
             // squares must stay normal floats for that error bound
-            for (uint32_t j = 0; j < a.d; ++j) {
-                const float xj = xf[j];
+#pragma unroll U
+            for (int j = 0; j < DMAX; ++j) {
+                if (j >= d) break;
+                const float xj = R.f(j);
                 if (xj != 0.0f && !(xj > 1e-15f && xj < 1e15f)) exact64 = true;
             }
-            for (uint32_t ii = a.d - 1; ii-- > 0;) {
-                const float xi = xf[ii];
+#pragma unroll U
+            for (int ii = DMAX - 1; ii >= 0; --ii) {
+                if (ii > d - 1) continue;
+                const float xi = R.f(ii);
+                if (ii == d - 1) {
+                    tail32 = xi * xi;
+                    continue;
+                }
                 const float v = 2.0f * atan2f(sqrtf(tail32), xi) / 3.14159265f * fm;
                 tail32 += xi * xi;
                 const float r = rintf(v);
@@ -116,37 +151,49 @@ __global__ void k_prep(PrepArgs a) {
             }
             pid = pid32;
         }
-        double tail = __dmul_rn(X(a.d - 1), X(a.d - 1));
         bool ambiguous = false;
-        if (exact64) pid = 0;
-        for (uint32_t ii = a.d - 1; exact64 && ii-- > 0;) {
-            const double xi = X(ii);
-            const double phi = atan2(sqrt(tail), xi);
-            tail = __dadd_rn(tail, __dmul_rn(xi, xi));
-            const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
-            uint64_t slice = (uint64_t)v;
-            if (slice >= a.m) slice = a.m - 1;
-            // CUDA's atan2 may differ from the host libm by an ulp or two; a
-            // value this close to an interior slice boundary is resolved on
-            // the host with the reference's own formula.
-            const double r = rint(v);
-            if (r >= 1.0 && r <= (double)(a.m - 1) && fabs(v - r) <= 1e-9 * fmax(1.0, v)) ambiguous = true;
-            stride_i /= a.m;
-            pid += slice * (stride_i ? stride_i : 1);
+        if (exact64) {
+            pid = 0;
+            double tail = 0.0;
+#pragma unroll U
+            for (int ii = DMAX - 1; ii >= 0; --ii) {
+                if (ii > d - 1) continue;
+                const double xi = R.X(ii);
+                if (ii == d - 1) {
+                    tail = __dmul_rn(xi, xi);
+                    continue;
+                }
+                const double phi = atan2(sqrt(tail), xi);
+                tail = __dadd_rn(tail, __dmul_rn(xi, xi));
+                const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
+                uint64_t slice = (uint64_t)v;
+                if (slice >= a.m) slice = a.m - 1;
+                // CUDA's atan2 may differ from the host libm by an ulp or two; a
+                // value this close to an interior slice boundary is resolved on
+                // the host with the reference's own formula.
+                const double r = rint(v);
+                if (r >= 1.0 && r <= (double)(a.m - 1) && fabs(v - r) <= 1e-9 * fmax(1.0, v)) ambiguous = true;
+                stride_i /= a.m;
+                pid += slice * (stride_i ? stride_i : 1);
+            }
         }
         if (ambiguous) {
             const uint32_t k = atomicAdd(a.amb_count, 1u);
             if (k < a.amb_cap) a.amb_list[k] = i;
         }
     } else {
-        for (uint32_t j = 0; j < a.d; ++j) {
-            const double v = X(j);
+        float sv = 0.0f;
+#pragma unroll U
+        for (int j = 0; j < DMAX; ++j) {
+            if (j >= d) break;
+            const double v = R.X(j);
             if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
             if (a.normalized && v > 1.0) err |= kErrAboveOne;
             sum = __dadd_rn(sum, v);
+            if ((uint32_t)j == a.slice_dim) sv = R.f(j);
         }
         if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
-        if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(xf[a.slice_dim]);
+        if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(sv);
     }
     if (err) {
         atomicOr(a.err, err);
@@ -155,15 +202,93 @@ __global__ void k_prep(PrepArgs a) {
     // monotone in sum; truncation keeps it monotone (and the partition sort
     // one radix pass shorter)
     const uint32_t skey = __float_as_uint(__double2float_rn(sum)) & ~((1u << a.key_shift) - 1u);
-    a.key64[i] = (pid << 32) | skey;
-    a.idx[i] = i;
+    const uint64_t key = (pid << 32) | skey;
+    a.key64[i] = key;
+    if (a.idx) a.idx[i] = i;
+    return key;
 }
 
-void launch_prep(const PrepArgs& a, cudaStream_t st) {
+__global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.n)
+        prep_row<32>(a, i, MemRow{a.pts + (size_t)i * a.d, a.pts64 ? a.pts64 + (size_t)i * a.d : nullptr});
+}
+
+// Persistent prep over row tiles streamed by the bulk-copy engine; each row
+// moves from the staged tile into registers with the widest shared load its
+// stride allows. With a.gmin set, also the per-CTA minimum key of every
+// partition (gmin[blockIdx.x * P + p]; the stream path's representative bound).
+template <int DP>
+__global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
+    extern __shared__ __align__(16) char s_prep[];
+    char* smem = s_prep;
+    uint32_t* s_min = reinterpret_cast<uint32_t*>(smem + stream_smem_bytes(a.d));
+    if (a.gmin) {
+        for (uint32_t p = threadIdx.x; p < a.P; p += blockDim.x) s_min[p] = 0xFFFFFFFFu;
+    }
+    const uint32_t d = a.d;
+    stream_row_tiles(a.pts, a.n, d, smem, [&](const float* tile, uint32_t r0, uint32_t nr) {
+        if (threadIdx.x < nr) {
+            const uint32_t i = r0 + threadIdx.x;
+            const float* x = tile + (size_t)threadIdx.x * d;
+            RegRow<DP> R;
+            if ((d & 3) == 0) {
+#pragma unroll
+                for (int v = 0; v < (DP + 3) / 4; ++v) {
+                    const float4 q = 4 * v < (int)d ? reinterpret_cast<const float4*>(x)[v]
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (4 * v < DP) R.v[4 * v] = q.x;
+                    if (4 * v + 1 < DP) R.v[4 * v + 1] = q.y;
+                    if (4 * v + 2 < DP) R.v[4 * v + 2] = q.z;
+                    if (4 * v + 3 < DP) R.v[4 * v + 3] = q.w;
+                }
+            } else if ((d & 1) == 0) {
+#pragma unroll
+                for (int v = 0; v < (DP + 1) / 2; ++v) {
+                    const float2 q = 2 * v < (int)d ? reinterpret_cast<const float2*>(x)[v] : make_float2(0.f, 0.f);
+                    if (2 * v < DP) R.v[2 * v] = q.x;
+                    if (2 * v + 1 < DP) R.v[2 * v + 1] = q.y;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < DP; ++j) R.v[j] = j < (int)d ? x[j] : 0.0f;
+            }
+            const uint64_t key = prep_row<DP>(a, i, R);
+            if (a.gmin) {
+                // read first: after the first rows most keys are above the minimum
+                const uint32_t p = (uint32_t)(key >> 32), k = (uint32_t)key;
+                if (k < s_min[p]) atomicMin(s_min + p, k);
+            }
+        }
+    });
+    if (a.gmin) {
+        __syncthreads();
+        for (uint32_t p = threadIdx.x; p < a.P; p += blockDim.x) a.gmin[(size_t)blockIdx.x * a.P + p] = s_min[p];
+    }
+}
+
+uint32_t prep_stream_grid(uint32_t n, int sm_count) {
+    return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows), 4u * (uint32_t)sm_count));
+}
+
+void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
     if (a.n == 0) return;
-    k_prep<<<ceil_div(a.n, 256), 256, 0, st>>>(a);
+    if (!a.pts64 && a.d <= 32 && ((uintptr_t)a.pts & 15) == 0 && sm_count > 0) {
+        // float rows, 16-byte aligned: persistent CTAs, bulk-copied row tiles
+        const size_t smem = stream_smem_bytes(a.d) + (a.gmin ? (size_t)a.P * sizeof(uint32_t) : 0);
+        SKY_DISPATCH_D(padded_dim(a.d), {
+            if (smem > 48 * 1024)
+                SKY_CUDA(cudaFuncSetAttribute(k_prep_stream<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+            k_prep_stream<DT><<<prep_stream_grid(a.n, sm_count), kStreamRows, smem, st>>>(a);
+        });
+    } else {
+        if (a.gmin) throw Error(SKY_E_INTERNAL, "partition minima need the streamed prep");
+        k_prep<<<ceil_div(a.n, 256), 256, 0, st>>>(a);
+    }
     SKY_LAUNCH_CHECK();
 }
+
 
 // The angular stride loop above walks i = d-2 .. 0 with stride m^i.
 // (stride_i starts at m^(d-1) and is divided before use.)
@@ -176,6 +301,34 @@ __global__ void k_seg_offsets(const uint64_t* __restrict__ key64, uint32_t n, ui
     for (int64_t q = prev + 1; q <= (int64_t)p; ++q) off[q] = i;
     if (i == n - 1)
         for (uint32_t q = p + 1; q <= P; ++q) off[q] = n;
+}
+
+// sorted survivor keys ((key64 >> key_shift) << row_bits | row) -> key64,
+// row and the partition offsets off[P+1]
+__global__ void k_unpack_survivors(const uint64_t* __restrict__ comp, uint32_t n, uint32_t row_bits,
+                                   uint32_t key_shift, uint32_t P, uint64_t* __restrict__ key64,
+                                   uint32_t* __restrict__ idx, uint32_t* __restrict__ off) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t c = comp[i];
+    const uint64_t k = (c >> row_bits) << key_shift;
+    key64[i] = k;
+    idx[i] = (uint32_t)(c & ((1ull << row_bits) - 1));
+    const uint32_t p = (uint32_t)(k >> 32);
+    const int64_t prev = i ? (int64_t)((comp[i - 1] >> row_bits) << key_shift >> 32) : -1;
+    for (int64_t q = prev + 1; q <= (int64_t)p; ++q) off[q] = i;
+    if (i == n - 1)
+        for (uint32_t q = p + 1; q <= P; ++q) off[q] = n;
+}
+
+void launch_unpack_survivors(const uint64_t* comp, uint32_t n, uint32_t row_bits, uint32_t key_shift, uint32_t P,
+                             uint64_t* key64, uint32_t* idx, uint32_t* off, cudaStream_t st) {
+    if (n == 0) {
+        SKY_CUDA(cudaMemsetAsync(off, 0, (P + 1) * sizeof(uint32_t), st));
+        return;
+    }
+    k_unpack_survivors<<<ceil_div(n, 256), 256, 0, st>>>(comp, n, row_bits, key_shift, P, key64, idx, off);
+    SKY_LAUNCH_CHECK();
 }
 
 void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t* off, cudaStream_t st) {
@@ -367,10 +520,10 @@ __device__ bool rep_less(const T* pts, uint32_t d, uint32_t a, uint32_t b) {
 // resolved exactly by repeated block-wide argmin.
 template <class T>
 __global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* __restrict__ idx,
-                           const uint32_t* __restrict__ off, const T* __restrict__ pts, uint32_t d,
-                           uint32_t q, uint32_t* cand) {
+                           const uint32_t* __restrict__ off, const uint32_t* __restrict__ off_end,
+                           const T* __restrict__ pts, uint32_t d, uint32_t q, uint32_t* cand) {
     const uint32_t p = blockIdx.x;
-    const uint32_t a = off[p], b = off[p + 1];
+    const uint32_t a = off[p], b = off_end ? off_end[p] : off[p + 1];
     uint32_t* out = cand + (size_t)p * q;
     const uint32_t size = b - a;
     const uint32_t take = size < q ? size : q;
@@ -475,13 +628,199 @@ __global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* _
     }
 }
 
+// ------------------------------------ representative candidates (stream path)
+// select_representatives_sorted (filter.cpp:66-86) without sorting every row:
+// the q-th smallest key of a partition is at most the q-th smallest of its
+// per-chunk minima (q chunks each hold a row at or below their minimum), so
+// the rows with key <= that bound contain the first q rows of the sorted
+// partition and the whole tie run at position q. Only they are sorted.
+//
+// thr[p] = q-th smallest of gmin[., p] (0xFFFFFFFF when fewer than q chunks
+// hold rows of p: then every row of p is a candidate). A warp per partition.
+__global__ void k_part_thresh(const uint32_t* __restrict__ gmin, uint32_t G, uint32_t P, uint32_t q,
+                              uint32_t* __restrict__ thr) {
+    const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (p >= P) return;
+    uint64_t last = 0;
+    for (uint32_t r = 0; r < q; ++r) {
+        uint64_t best = ~0ull;
+        for (uint32_t c = lane; c < G; c += 32) {
+            const uint64_t v = ((uint64_t)gmin[(size_t)c * P + p] << 32) | c;
+            if ((r == 0 || v > last) && v < best) best = v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+            best = y < best ? y : best;
+        }
+        last = best;
+        if (best == ~0ull) break;
+    }
+    if (lane == 0) thr[p] = (uint32_t)(last >> 32);
+}
+
+// rows with key <= thr[pid] into per-partition buckets of B slots
+__global__ void k_cand_bucket(const uint64_t* __restrict__ key64, uint32_t n, const uint32_t* __restrict__ thr,
+                              uint32_t B, uint32_t* __restrict__ cnt, uint64_t* __restrict__ bkey,
+                              uint32_t* __restrict__ brow, uint32_t* overflow) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = __ldcs(key64 + i);
+    const uint32_t p = (uint32_t)(k >> 32);
+    if ((uint32_t)k > __ldg(thr + p)) return;
+    const uint32_t s = atomicAdd(cnt + p, 1u);
+    if (s < B) {
+        bkey[(size_t)p * B + s] = k;
+        brow[(size_t)p * B + s] = i;
+    } else {
+        atomicOr(overflow, 1u);
+    }
+}
+
+// Ascending bitonic sort of s[0, n2) (n2 a power of two) by the block.
+__device__ __forceinline__ void block_bitonic_sort(uint64_t* s, uint32_t n2) {
+    for (uint32_t k = 2; k <= n2; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+                // i-th compare-exchange pair of this pass
+                const uint32_t lo = 2 * i - (i & (j - 1)), hi = lo + j;
+                const bool up = (lo & k) == 0;
+                const uint64_t x = s[lo], y = s[hi];
+                if ((x > y) == up) {
+                    s[lo] = y;
+                    s[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// One CTA per partition: its bucket sorted by (key, row), then the first q by
+// the reference order (filter.cpp:74-79): rows below the q-th key as they
+// are, the tie run at position q resolved by (FP64 sum, lex coords, id) in
+// `need` rounds of block argmin (k_rep_pick's rule).
+__global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict__ bkey,
+                                                     const uint32_t* __restrict__ brow,
+                                                     const uint32_t* __restrict__ cnt, uint32_t B,
+                                                     const float* __restrict__ pts, uint32_t d, uint32_t q,
+                                                     uint32_t* __restrict__ cand, uint32_t run_floats) {
+    constexpr uint32_t MAXB = 1024;
+    __shared__ uint64_t s_c[MAXB];  // (key << 32 | row)
+    __shared__ double s_sum[MAXB];
+    __shared__ uint8_t s_taken[MAXB];
+    __shared__ uint32_t s_ra, s_rb, s_best[8];
+    const uint32_t p = blockIdx.x;
+    const uint32_t c = min(cnt[p], min(B, MAXB));
+    uint32_t* out = cand + (size_t)p * q;
+    for (uint32_t k = threadIdx.x; k < q; k += blockDim.x) out[k] = kNone;
+    if (c == 0) return;
+    uint32_t n2 = 1;
+    while (n2 < c) n2 <<= 1;
+    const size_t base = (size_t)p * B;
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x)
+        s_c[i] = i < c ? ((uint64_t)(uint32_t)bkey[base + i] << 32) | brow[base + i] : ~0ull;
+    if (threadIdx.x == 0) {
+        s_ra = 0;
+        s_rb = c;
+    }
+    __syncthreads();
+    block_bitonic_sort(s_c, n2);
+    const uint32_t take = min(c, q);
+    const uint32_t v = (uint32_t)(s_c[take - 1] >> 32);
+    // tie run [ra, rb) of key v
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
+        const uint32_t ki = (uint32_t)(s_c[i] >> 32);
+        if (ki == v && i > 0 && (uint32_t)(s_c[i - 1] >> 32) != v) s_ra = i;
+        if (ki > v && (uint32_t)(s_c[i - 1] >> 32) == v) s_rb = i;
+    }
+    __syncthreads();
+    const uint32_t ra = s_ra, rb = s_rb;
+    for (uint32_t k = threadIdx.x; k < ra; k += blockDim.x) out[k] = (uint32_t)s_c[k];
+    const uint32_t need = take - ra, L = rb - ra;
+    if (need == L) {
+        for (uint32_t k = threadIdx.x; k < need; k += blockDim.x) out[ra + k] = (uint32_t)s_c[ra + k];
+        return;
+    }
+    // the run's rows (coordinates, FP64 sums) in shared memory: a run of
+    // duplicates compares every coordinate of every pair
+    extern __shared__ float s_run[];  // [L][d] when run_smem
+    const bool in_smem = (size_t)L * d <= run_floats;
+    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+        const uint32_t row = (uint32_t)s_c[ra + e];
+        const float* x = pts + (size_t)row * d;
+        double sum = 0.0;
+        for (uint32_t j = 0; j < d; ++j) {
+            const float v = x[j];
+            sum = __dadd_rn(sum, (double)v);
+            if (in_smem) s_run[(size_t)e * d + j] = v;
+        }
+        s_sum[e] = sum;
+        s_taken[e] = 0;
+    }
+    __syncthreads();
+    auto less = [&](uint32_t x, uint32_t y) {  // run slots: (sum, lex coords, id)
+        if (s_sum[x] != s_sum[y]) return s_sum[x] < s_sum[y];
+        if (!in_smem) return lex_less(pts, d, (uint32_t)s_c[ra + x], (uint32_t)s_c[ra + y]);
+        const float* a = s_run + (size_t)x * d;
+        const float* b = s_run + (size_t)y * d;
+        for (uint32_t j = 0; j < d; ++j) {
+            if (a[j] < b[j]) return true;
+            if (a[j] > b[j]) return false;
+        }
+        return (uint32_t)s_c[ra + x] < (uint32_t)s_c[ra + y];
+    };
+    for (uint32_t r = 0; r < need; ++r) {
+        uint32_t best = kNone;
+        for (uint32_t e = threadIdx.x; e < L; e += blockDim.x)
+            if (!s_taken[e] && (best == kNone || less(e, best))) best = e;
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint32_t other = __shfl_down_sync(0xffffffffu, best, o);
+            if (other != kNone && (best == kNone || less(other, best))) best = other;
+        }
+        if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t bb = kNone;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+                const uint32_t o = s_best[w];
+                if (o != kNone && (bb == kNone || less(o, bb))) bb = o;
+            }
+            s_taken[bb] = 1;
+            out[ra + r] = (uint32_t)s_c[ra + bb];
+        }
+        __syncthreads();
+    }
+}
+
+void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t q, uint32_t G,
+                           const uint32_t* gmin, uint32_t* thr, uint32_t B, uint32_t* cnt, uint64_t* bkey,
+                           uint32_t* brow, const float* pts, uint32_t d, uint32_t* cand, uint32_t* overflow,
+                           cudaStream_t st) {
+    if (B > 1024) throw Error(SKY_E_INTERNAL, "candidate buckets hold at most 1024 rows");
+    k_part_thresh<<<ceil_div((uint64_t)P * 32, 256), 256, 0, st>>>(gmin, G, P, q, thr);
+    SKY_LAUNCH_CHECK();
+    SKY_CUDA(cudaMemsetAsync(cnt, 0, P * sizeof(uint32_t), st));
+    k_cand_bucket<<<ceil_div(n, 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
+    SKY_LAUNCH_CHECK();
+    const uint32_t run_floats = std::min<uint32_t>(B * d, 16u * 1024);  // <= 64 KB of run coordinates
+    static bool attr = false;
+    if (!attr) {
+        SKY_CUDA(cudaFuncSetAttribute(k_bucket_pick, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr = true;
+    }
+    k_bucket_pick<<<P, 256, run_floats * sizeof(float), st>>>(bkey, brow, cnt, B, pts, d, q, cand, run_floats);
+    SKY_LAUNCH_CHECK();
+}
+
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
-                     const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st) {
+                     const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st,
+                     const uint32_t* off_end) {
     if (!P) return;
     if (pts64)
-        k_rep_pick<double><<<P, 128, 0, st>>>(key64, idx, off, pts64, d, q, cand);
+        k_rep_pick<double><<<P, 128, 0, st>>>(key64, idx, off, off_end, pts64, d, q, cand);
     else
-        k_rep_pick<float><<<P, 128, 0, st>>>(key64, idx, off, pts, d, q, cand);
+        k_rep_pick<float><<<P, 128, 0, st>>>(key64, idx, off, off_end, pts, d, q, cand);
     SKY_LAUNCH_CHECK();
 }
 
@@ -592,7 +931,8 @@ __global__ void __launch_bounds__(THREADS) k_rep_finalize(const uint32_t* __rest
     uint32_t* s_row = reinterpret_cast<uint32_t*>(s_xyz + (size_t)MAXN * V);
     uint32_t* s_key = s_row + MAXN;
     uint32_t* s_ord = s_key + MAXN;
-    uint8_t* s_dead = reinterpret_cast<uint8_t*>(s_ord + MAXN);
+    uint64_t* s_sort = reinterpret_cast<uint64_t*>(s_ord + MAXN);
+    uint8_t* s_dead = reinterpret_cast<uint8_t*>(s_sort + MAXN);
     __shared__ uint32_t s_n;
     const int t = threadIdx.x;
     // 1. compact the picks (slot order = partition order)
@@ -630,42 +970,52 @@ __global__ void __launch_bounds__(THREADS) k_rep_finalize(const uint32_t* __rest
         s_key[i] = __float_as_uint(__double2float_rn(sum));
     }
     __syncthreads();
-    // 3. key order by ranks (stable: ties keep slot order)
-    for (uint32_t i = t; i < n; i += THREADS) {
-        const uint32_t ki = s_key[i];
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < n; ++j) {
-            const uint32_t kj = s_key[j];
-            rank += (kj < ki) | ((kj == ki) & (j < i));
-        }
-        s_ord[rank] = i;
+    // 3. key order (stable: ties keep slot order): bitonic sort of
+    //    (key << 32 | slot)
+    constexpr int NW = THREADS / 32;
+    const uint32_t lane = t & 31, wid = t >> 5;
+    {
+        uint32_t n2 = 1;
+        while (n2 < n) n2 <<= 1;
+        for (uint32_t i = t; i < n2; i += THREADS) s_sort[i] = i < n ? ((uint64_t)s_key[i] << 32) | i : ~0ull;
+        __syncthreads();
+        block_bitonic_sort(s_sort, n2);
+        for (uint32_t i = t; i < n; i += THREADS) s_ord[i] = (uint32_t)s_sort[i];
     }
     __syncthreads();
     // 4. antichain: a candidate meets the candidates in key order up to its
-    //    own key (a dominator's key is <= its own) and stops at the first
-    //    dominator; the strongest candidates come first, so most stop early
+    //    own key (a dominator's key is <= its own); a warp per candidate,
+    //    lanes split the comparators, the warp stops at the first dominator
     unsigned long long nt = 0;
-    for (uint32_t pi = t; pi < n; pi += THREADS) {
+    for (uint32_t pi = wid; pi < n; pi += NW) {
         const uint32_t i = s_ord[pi];
         const uint32_t ki = s_key[i];
         const float4* ti = s_xyz + (size_t)i * V;
         bool dom = false;
-        for (uint32_t pj = 0; pj < n && !dom; ++pj) {
-            const uint32_t j = s_ord[pj];
-            if (s_key[j] > ki) break;
-            if (j == i) continue;
-            ++nt;
-            const float4* sj = s_xyz + (size_t)j * V;
-            bool gt = false, lt = false;
+        for (uint32_t b = 0; b < n; b += 32) {
+            const uint32_t pj = b + lane;
+            bool hit = false;
+            const uint32_t j = pj < n ? s_ord[pj] : 0u;
+            const bool in = pj < n && s_key[j] <= ki;
+            if (in && j != i) {
+                ++nt;
+                const float4* sj = s_xyz + (size_t)j * V;
+                bool gt = false, lt = false;
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const float4 a = sj[v], b = ti[v];
-                gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
-                lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
+                for (int v = 0; v < V; ++v) {
+                    const float4 a = sj[v], c = ti[v];
+                    gt |= (a.x > c.x) | (a.y > c.y) | (a.z > c.z) | (a.w > c.w);
+                    lt |= (a.x < c.x) | (a.y < c.y) | (a.z < c.z) | (a.w < c.w);
+                }
+                hit = !gt && (x64.x ? dom64(x64, s_row[j], s_row[i]) : lt);
             }
-            dom = !gt && (x64.x ? dom64(x64, s_row[j], s_row[i]) : lt);
+            if (__any_sync(0xffffffffu, hit)) {
+                dom = true;
+                break;
+            }
+            if (!__all_sync(0xffffffffu, in)) break;  // keys sorted: the rest are larger
         }
-        s_dead[i] = dom;
+        if (lane == 0) s_dead[i] = dom;
     }
     __syncthreads();
     // 5. survivors in key order
@@ -703,13 +1053,13 @@ void rep_finalize_launch(const uint32_t* cand, uint32_t slots, const float* pts,
 bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
                          uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {
     if (slots > (uint32_t)REPF_MAX) return false;
-    const bool small = slots <= 256u * REPF_ITEMS;
-    const size_t maxn = small ? 256u * REPF_ITEMS : (size_t)REPF_MAX;
-    const size_t smem = maxn * ((D + 3) / 4) * 16 + maxn * 13 + 64;
+    const bool small = slots <= 512u * REPF_ITEMS;
+    const size_t maxn = small ? 512u * REPF_ITEMS : (size_t)REPF_MAX;
+    const size_t smem = maxn * ((D + 3) / 4) * 16 + maxn * 21 + 64;
     if (smem + 16 * 1024 > (size_t)smem_optin) return false;
     SKY_DISPATCH_D(D, {
         if (small)
-            rep_finalize_launch<DT, 256>(cand, slots, pts, d, out, out_count, tests, x64, smem, st);
+            rep_finalize_launch<DT, 512>(cand, slots, pts, d, out, out_count, tests, x64, smem, st);
         else
             rep_finalize_launch<DT, 1024>(cand, slots, pts, d, out, out_count, tests, x64, smem, st);
     });

@@ -60,11 +60,19 @@ struct PrepArgs {
     uint32_t* amb_list;
     uint32_t amb_cap;
     uint32_t key_shift;      // low bits of skey cleared (the partition sort skips them)
+    uint32_t* gmin = nullptr;  // out (optional, streamed prep): per-CTA minimum key of each partition
+    uint32_t P = 0;
 };
-void launch_prep(const PrepArgs& a, cudaStream_t st);
+// sm_count > 0: persistent streamed prep when the rows allow it (float,
+// aligned); required when a.gmin is set (grid = prep_stream_grid chunks)
+void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count = 0);
+uint32_t prep_stream_grid(uint32_t n, int sm_count);
 
 // Partition boundaries of a (pid << 32 | skey)-sorted key array: off[P+1].
 void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t* off, cudaStream_t st);
+// sorted survivor keys of launch_prefilter_append -> key64, rows, offsets[P+1]
+void launch_unpack_survivors(const uint64_t* comp, uint32_t n, uint32_t row_bits, uint32_t key_shift, uint32_t P,
+                             uint64_t* key64, uint32_t* idx, uint32_t* off, cudaStream_t st);
 
 // Patch pid bits of key64 for rows listed in (rows, pids).
 void launch_patch_pid(uint64_t* key64, const uint32_t* rows, const uint32_t* pids, uint32_t count,
@@ -97,8 +105,19 @@ void launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t n, uin
 void launch_pick_first(const uint32_t* rows, const uint32_t* off, uint32_t P, uint32_t q, uint32_t* cand,
                        cudaStream_t st);
 void launch_pick_gather(const uint32_t* rows, const uint32_t* gpos, uint32_t slots, uint32_t* cand, cudaStream_t st);
+// off_end (optional): partition p spans [off[p], off_end[p]) instead of [off[p], off[p+1])
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
-                     const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st);
+                     const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st,
+                     const uint32_t* off_end = nullptr);
+// Stream path of the sorted representatives (select_representatives_sorted,
+// filter.cpp:66-86): per-partition key bound = q-th smallest of the prep
+// CTAs' minima gmin[G][P] -> rows under the bound in B-slot buckets (overflow
+// flag set if one fills) -> each bucket sorted, first q picked exactly into
+// cand[p * q + k] (kNone when the partition has fewer rows).
+void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t q, uint32_t G,
+                           const uint32_t* gmin, uint32_t* thr, uint32_t B, uint32_t* cnt, uint64_t* bkey,
+                           uint32_t* brow, const float* pts, uint32_t d, uint32_t* cand, uint32_t* overflow,
+                           cudaStream_t st);
 
 // Representative finish on the device (<= 2048 picks): key-sorted antichain
 // into `out`, count in *out_count. false: too many picks (host path).
@@ -243,6 +262,20 @@ void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint3
 uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey, uint32_t cap, uint32_t grid,
                  uint32_t* counter, cudaStream_t st);
+
+// Row-order prefilter that appends the survivors' sort keys
+// ((key64[row] >> key_shift) << row_bits | row) to out, count in *count.
+struct PrefilterAppend {
+    const uint64_t* key64 = nullptr;  // row order (pid << 32 | truncated skey)
+    uint64_t* out = nullptr;
+    uint32_t* count = nullptr;
+    uint32_t key_shift = 0, row_bits = 0;
+};
+// false: not applicable (d > 16, unaligned rows, shared memory)
+bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, const float* rep_xyz,
+                             const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,
+                             const uint32_t* nrep_dev, const float* thr, const PrefilterAppend& app,
+                             unsigned long long* tests, int smem_optin, cudaStream_t st);
 
 // Streaming representative prefilter (false: not applicable, use k_relsky).
 // Rows are tested in input order (dead_row), then folded into the sorted

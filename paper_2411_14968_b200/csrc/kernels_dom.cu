@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "stream.cuh"
 
 namespace sky {
 
@@ -723,7 +724,11 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
 // share a partition and have neighbouring keys, so they finish together) and
 // writes dead_pos[i]; otherwise thread i takes row i (coalesced stream) and
 // writes dead_row[i].
-template <int D, bool CODES, bool POSORDER>
+// APPEND (row order): instead of flags, the surviving rows are appended to
+// app.out as ((key64 >> key_shift) << row_bits | row), count in *app.count —
+// the survivors' (partition, key, row) sort key; the CTA's rows are staged
+// through shared memory with coalesced float4 loads.
+template <int D, bool CODES, bool POSORDER, bool APPEND = false>
 __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts, uint32_t d, uint32_t n,
                                                    const uint32_t* __restrict__ idx,
                                                    const float4* __restrict__ rep_xyz,
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
                                                    uint32_t nrep_max, const uint32_t* nrep_dev,
                                                    const float* __restrict__ thr,
                                                    uint8_t* __restrict__ dead_row, unsigned long long* tests,
-                                                   X64 x64) {
+                                                   X64 x64, PrefilterAppend app = {}) {
     constexpr int V = Dims2<D>::V;
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
@@ -750,22 +755,34 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     }
     if (CODES)
         for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
+    // APPEND: the row tiles stream through shared memory after the tables
+    char* s_stage = reinterpret_cast<char*>(
+        (reinterpret_cast<uintptr_t>(s_thr + (CODES ? D * kThr : 0)) + 15) & ~uintptr_t{15});
     __syncthreads();
-    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = slot < n && (!POSORDER || !dead_row[slot]);
-    const uint32_t row = (POSORDER && slot < n) ? idx[slot] : slot;
+    unsigned long long nt = 0;
+    auto process = [&](const float* x, const uint32_t slot, const bool valid, const uint32_t row) {
     float4 t[V];
     uint32_t tk = 0;
     uint32_t T0 = G, T1 = G | 0x80000000u;  // never passes unless set below
     {
         float xs[4 * V];
-        const float* x = pts + (size_t)row * d;
         double sum = 0.0;
+        if (APPEND && (d & 3) == 0) {
+            // staged rows with d % 4 == 0: 16-byte shared loads (a quarter of
+            // the bank wavefronts of scalar loads at an even row stride)
 #pragma unroll
-        for (int j = 0; j < 4 * V; ++j) {
-            xs[j] = (valid && j < D && (uint32_t)j < d) ? x[j] : 0.0f;
-            if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)xs[j]);  // same key as k_prep
+            for (int v = 0; v < V; ++v) {
+                const float4 q = (valid && 4 * v < (int)d) ? reinterpret_cast<const float4*>(x)[v]
+                                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                xs[4 * v] = q.x; xs[4 * v + 1] = q.y; xs[4 * v + 2] = q.z; xs[4 * v + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4 * V; ++j) xs[j] = (valid && j < D && (uint32_t)j < d) ? x[j] : 0.0f;
         }
+#pragma unroll
+        for (int j = 0; j < 4 * V; ++j)
+            if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)xs[j]);  // same key as k_prep
         if (x64.x && valid) {
             const double* xd = x64.x + (size_t)row * d;
             sum = 0.0;
@@ -786,7 +803,6 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     }
     bool alive = valid;
     const uint32_t bound = __reduce_max_sync(0xffffffffu, alive ? tk : 0u);
-    unsigned long long nt = 0;
     if (CODES) {
         // 8 representatives per step: 8 coarse tests folded by 3-input min,
         // exact FP32 re-check only on a coarse pass; one vote per step
@@ -843,10 +859,32 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         }
         if (alive) nt += r;
     }
-    if (POSORDER) {
+    if (APPEND) {
+        const bool keep = valid && alive;
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(app.count, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep)
+            app.out[base + __popc(bal & ((1u << lane) - 1u))] =
+                ((__ldcs(app.key64 + row) >> app.key_shift) << app.row_bits) | row;
+    } else if (POSORDER) {
         if (valid && !alive) dead_row[slot] = 1;
     } else if (valid) {
         dead_row[row] = alive ? 0 : 1;
+    }
+    };
+    if (APPEND) {
+        stream_row_tiles(pts, n, d, s_stage, [&](const float* tile, uint32_t r0, uint32_t nr) {
+            const uint32_t r = r0 + threadIdx.x;
+            process(tile + (size_t)threadIdx.x * d, r, threadIdx.x < nr, r);
+        });
+    } else {
+        const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+        const bool valid = slot < n && (!POSORDER || !dead_row[slot]);
+        const uint32_t row = (POSORDER && slot < n) ? idx[slot] : slot;
+        process(pts + (size_t)row * d, slot, valid, row);
     }
     if (tests) {
         nt = warp_sum(nt);
@@ -978,6 +1016,40 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
     SKY_LAUNCH_CHECK();
     if (codes && posorder) return true;
     k_gather_dead<<<ceil_div(n, 256), 256, 0, st>>>(idx, dead_row, n, dead_pos);
+    SKY_LAUNCH_CHECK();
+    return true;
+}
+
+bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, const float* rep_xyz,
+                             const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,
+                             const uint32_t* nrep_dev, const float* thr, const PrefilterAppend& app,
+                             unsigned long long* tests, int smem_optin, cudaStream_t st) {
+    if (D > 16 || ((uintptr_t)pts & 15)) return false;
+    const bool codes = rep_qc && thr && nrep >= 32;
+    const size_t npad = (nrep + 7) & ~7u;
+    const size_t smem = npad * ((D + 3) / 4) * 16 + npad * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64 +
+                        stream_smem_bytes(d) + 16;
+    if (smem + 1024 > (size_t)smem_optin) return false;
+    if (!n) return true;
+    // persistent CTAs: as many as fit, capped by the tile count
+    auto go = [&](auto kern, const uint2* qc, const float* th) {
+        SKY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)kStreamRows, smem));
+        int dev = 0, sms = 148;
+        SKY_CUDA(cudaGetDevice(&dev));
+        SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows),
+                                                                       (uint32_t)std::max(1, per_sm) * sms));
+        kern<<<grid, kStreamRows, smem, st>>>(pts, d, n, nullptr, reinterpret_cast<const float4*>(rep_xyz), rep_key,
+                                              qc, rep_id, nrep, nrep_dev, th, nullptr, tests, X64{}, app);
+    };
+    SKY_DISPATCH_D16(D, {
+        if (codes)
+            go(k_prefilter<DT, true, false, true>, rep_qc, thr);
+        else
+            go(k_prefilter<DT, false, false, true>, nullptr, nullptr);
+    });
     SKY_LAUNCH_CHECK();
     return true;
 }

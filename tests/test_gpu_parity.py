@@ -306,3 +306,39 @@ def test_distributed_context_single_rank():
             assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist()
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_stream_path_forced(engine, golden, monkeypatch, stream):
+    """The stream path (sorted representatives from per-partition candidate
+    buckets, row-order prefilter that appends survivor keys, survivors-only
+    sort; engine.cu `stream`) and the sorted path, each forced at sizes the
+    oracle finishes quickly: the golden plane, the reduced BASELINE configs
+    and random configurations."""
+    monkeypatch.setenv("SKY_STREAM", stream)
+    test_plane_matches_reference(engine, golden, LocalAlgo.SFS)
+    for idx in (2, 3, 5):
+        test_baseline_configs_reduced(engine, golden, idx)
+    test_random_configs_vs_oracle(engine)
+
+
+def test_stream_path_bucket_overflow(engine, monkeypatch):
+    """Candidate buckets that fill up (duplicate-heavy rows, rows sorted by
+    partition) fall back to the sorted path with identical results."""
+    monkeypatch.setenv("SKY_STREAM", "1")
+    rng = np.random.default_rng(3)
+    cases = [
+        np.zeros((6000, 3), np.float32),                                   # every row identical
+        np.repeat(rng.random((3, 4), dtype=np.float32), 3000, axis=0),     # three values, 3000 copies
+        np.sort(rng.random((20000, 4), dtype=np.float32), axis=0),         # partitions concentrated by row
+        rng.integers(0, 3, (20000, 5)).astype(np.float32) / 2,             # lattice ties
+    ]
+    for k, x in enumerate(cases):
+        for strat, p in ((1, 2), (0, 16), (2, 16)):
+            cfg = SkyConfig.make(strategy=strat, p=p, m=p if strat == 1 else 0, seed=k, filter=2, rep_q=5, merge=1,
+                                 workers=1)
+            exp = O.oracle_run(x, cfg, True)
+            r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+            assert np.array_equal(r.skyline, exp["ids"]), (k, strat)
+            check_metrics(r, exp, (k, strat))
+            assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), (k, strat)
