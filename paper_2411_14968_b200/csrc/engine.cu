@@ -86,7 +86,7 @@ enum Slot {
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
     S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
-    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_COUNT
+    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -1488,7 +1488,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     {
         const int pb = std::max(1, bits_for(P));
         const char* env = std::getenv("SKY_STREAM");
-        const bool want = env ? env[0] == '1' : (uint64_t)n * d * sizeof(float) > (48ull << 20);
+        const bool want = env ? env[0] == '1' : (uint64_t)n * d * sizeof(float) > (32ull << 20);
         stream = want && !eager && c->world == 1 && !f64 && cfg->filter == SKY_FILTER_REPRESENTATIVE &&
                  cfg->rep_selection == SKY_REPS_SORTED && cfg->strategy != SKY_SLICED && pb <= 12 &&
                  (uint64_t)P * std::min<uint64_t>(cfg->rep_q, n) <= 2048 && cfg->rep_q <= 64 && D <= 16 &&
@@ -1567,8 +1567,14 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         const uint32_t slots = P * q;
         DevSet reps = R.set(S_SET3, slots, D);  // reps.n: upper bound until the count is read back
         uint32_t* nrep_dev = misc + M_NREP;
-        if (launch_rep_finalize(D, cand, slots, pts, d, reps, nrep_dev, count_tests ? R.tests(0) : nullptr, R.x64_,
-                                c->smem_optin, st)) {
+        if (launch_rep_finalize_par(D, cand, slots, pts, d, reps, nrep_dev, count_tests ? R.tests(0) : nullptr,
+                                    R.x64_, c->smem_optin, c->sm_count,
+                                    R.dev<char>(S_REPF, rep_finalize_scratch_bytes(D)), st)) {
+            // keys, rank + antichain (a warp per pick), placement by rank;
+            // the count stays on the device
+            R.count(3);
+        } else if (launch_rep_finalize(D, cand, slots, pts, d, reps, nrep_dev, count_tests ? R.tests(0) : nullptr,
+                                       R.x64_, c->smem_optin, st)) {
             // compact + sort + prune in one CTA; the count stays on the device
             R.count();
         } else {

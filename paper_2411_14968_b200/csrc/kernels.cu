@@ -62,6 +62,7 @@ __device__ __forceinline__ uint32_t canon_bits(float v) {
 // unrolled so every index is static).
 struct MemRow {
     static constexpr int kUnroll = 1;
+    static constexpr bool kF32 = false;  // decisions on X() (float or FP64 rows)
     const float* xf;
     const double* xd;
     __device__ __forceinline__ float f(uint32_t j) const { return xf[j]; }
@@ -71,6 +72,7 @@ struct MemRow {
 template <int DP>
 struct RegRow {
     static constexpr int kUnroll = DP;
+    static constexpr bool kF32 = true;  // float rows: validation and cells in FP32 (exact, see prep_row)
     float v[DP];
     __device__ __forceinline__ float f(uint32_t j) const { return v[j]; }
     __device__ __forceinline__ double X(uint32_t j) const { return (double)v[j]; }
@@ -85,7 +87,29 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
     double sum = 0.0;
     uint32_t err = 0;
     uint64_t pid = 0;
-    if (a.strategy == SKY_GRID) {
+    if (a.strategy == SKY_GRID && Row::kF32) {
+        // float rows: the comparisons give the same answers in FP32 as on the
+        // exact upcast; cell = floor(x * m) from the product rounded toward
+        // zero (floor(x*m) < m <= 2^22 is representable, so rz(x*m) lies in
+        // [floor(x*m), x*m] and has the same floor)
+        uint32_t stride = 1, pid32 = 0;
+        const uint32_t m32 = (uint32_t)a.m;
+        const float mf = (float)a.m;
+#pragma unroll U
+        for (int j = 0; j < DMAX; ++j) {
+            if (j >= d) break;
+            const float v = R.f(j);
+            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
+            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+            if (!(v >= 0.0f && v <= 1.0f)) err |= kErrGridRange;
+            sum = __dadd_rn(sum, (double)v);
+            uint32_t cell = __float2uint_rz(__fmul_rz(v, mf));
+            if (cell >= m32) cell = m32 - 1;
+            pid32 += cell * stride;
+            stride *= m32;
+        }
+        pid = pid32;
+    } else if (a.strategy == SKY_GRID) {
         // m^d <= kMaxPartitions (2^22): 32-bit cell arithmetic
         uint32_t stride = 1, pid32 = 0;
         const uint32_t m32 = (uint32_t)a.m;
@@ -217,7 +241,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 // Persistent prep over row tiles streamed by the bulk-copy engine; each row
 // moves from the staged tile into registers with the widest shared load its
 // stride allows. With a.gmin set, also the per-CTA minimum key of every
-// partition (gmin[blockIdx.x * P + p]; the stream path's representative bound).
+// partition (gmin[p * gridDim.x + blockIdx.x]; the stream path's representative bound).
 template <int DP>
 __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
     extern __shared__ __align__(16) char s_prep[];
@@ -227,7 +251,7 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
         for (uint32_t p = threadIdx.x; p < a.P; p += blockDim.x) s_min[p] = 0xFFFFFFFFu;
     }
     const uint32_t d = a.d;
-    stream_row_tiles(a.pts, a.n, d, smem, [&](const float* tile, uint32_t r0, uint32_t nr) {
+    stream_row_tiles(a.pts, a.n, d, smem, [&](const float* tile, uint32_t r0, uint32_t nr, const uint64_t*) {
         if (threadIdx.x < nr) {
             const uint32_t i = r0 + threadIdx.x;
             const float* x = tile + (size_t)threadIdx.x * d;
@@ -263,7 +287,7 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
     });
     if (a.gmin) {
         __syncthreads();
-        for (uint32_t p = threadIdx.x; p < a.P; p += blockDim.x) a.gmin[(size_t)blockIdx.x * a.P + p] = s_min[p];
+        for (uint32_t p = threadIdx.x; p < a.P; p += blockDim.x) a.gmin[(size_t)p * gridDim.x + blockIdx.x] = s_min[p];
     }
 }
 
@@ -645,7 +669,7 @@ __global__ void k_part_thresh(const uint32_t* __restrict__ gmin, uint32_t G, uin
     for (uint32_t r = 0; r < q; ++r) {
         uint64_t best = ~0ull;
         for (uint32_t c = lane; c < G; c += 32) {
-            const uint64_t v = ((uint64_t)gmin[(size_t)c * P + p] << 32) | c;
+            const uint64_t v = ((uint64_t)gmin[(size_t)p * G + c] << 32) | c;
             if ((r == 0 || v > last) && v < best) best = v;
         }
 #pragma unroll
@@ -744,29 +768,55 @@ __global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict_
     }
     // the run's rows (coordinates, FP64 sums) in shared memory: a run of
     // duplicates compares every coordinate of every pair
-    extern __shared__ float s_run[];  // [L][d] when run_smem
-    const bool in_smem = (size_t)L * d <= run_floats;
-    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
-        const uint32_t row = (uint32_t)s_c[ra + e];
-        const float* x = pts + (size_t)row * d;
-        double sum = 0.0;
-        for (uint32_t j = 0; j < d; ++j) {
-            const float v = x[j];
-            sum = __dadd_rn(sum, (double)v);
-            if (in_smem) s_run[(size_t)e * d + j] = v;
+    extern __shared__ float4 s_run4[];  // [L][d4] when in_smem (rows padded to float4s)
+    float* s_run = reinterpret_cast<float*>(s_run4);
+    const uint32_t d4 = (d + 3) & ~3u;
+    const bool in_smem = (size_t)L * d4 <= run_floats;
+    if (in_smem) {
+        // every coordinate of the run by its own thread (independent loads),
+        // then the sums from shared memory
+        // 8 loads in flight per thread (the rows are scattered: each load is a miss)
+        const uint32_t total = L * d4;
+        for (uint32_t k0 = threadIdx.x; k0 < total; k0 += 8 * blockDim.x) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t k = k0 + u * blockDim.x;
+                const uint32_t e = k / d4, j = k - e * d4;
+                v[u] = (k < total && j < d) ? pts[(size_t)(uint32_t)s_c[ra + e] * d + j] : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t k = k0 + u * blockDim.x;
+                if (k < total) s_run[k] = v[u];
+            }
         }
-        s_sum[e] = sum;
-        s_taken[e] = 0;
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+            double sum = 0.0;
+            for (uint32_t j = 0; j < d; ++j) sum = __dadd_rn(sum, (double)s_run[(size_t)e * d4 + j]);
+            s_sum[e] = sum;
+            s_taken[e] = 0;
+        }
+    } else {
+        for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+            s_sum[e] = row_sum(pts, d, (uint32_t)s_c[ra + e]);
+            s_taken[e] = 0;
+        }
     }
     __syncthreads();
     auto less = [&](uint32_t x, uint32_t y) {  // run slots: (sum, lex coords, id)
         if (s_sum[x] != s_sum[y]) return s_sum[x] < s_sum[y];
         if (!in_smem) return lex_less(pts, d, (uint32_t)s_c[ra + x], (uint32_t)s_c[ra + y]);
-        const float* a = s_run + (size_t)x * d;
-        const float* b = s_run + (size_t)y * d;
-        for (uint32_t j = 0; j < d; ++j) {
-            if (a[j] < b[j]) return true;
-            if (a[j] > b[j]) return false;
+        // padding lanes are 0 in both rows: they never decide
+        const float4* a = s_run4 + (size_t)x * (d4 / 4);
+        const float4* b = s_run4 + (size_t)y * (d4 / 4);
+        for (uint32_t v = 0; v < d4 / 4; ++v) {
+            const float4 p = a[v], q = b[v];
+            if (p.x != q.x) return p.x < q.x;
+            if (p.y != q.y) return p.y < q.y;
+            if (p.z != q.z) return p.z < q.z;
+            if (p.w != q.w) return p.w < q.w;
         }
         return (uint32_t)s_c[ra + x] < (uint32_t)s_c[ra + y];
     };
@@ -780,14 +830,17 @@ __global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict_
         }
         if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t bb = kNone;
-            for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
-                const uint32_t o = s_best[w];
-                if (o != kNone && (bb == kNone || less(o, bb))) bb = o;
+        if (threadIdx.x < 32) {
+            // the 8 warp winners by a 3-step tree in warp 0
+            uint32_t bb = threadIdx.x < 8 ? s_best[threadIdx.x] : kNone;
+            for (int o = 4; o > 0; o >>= 1) {
+                const uint32_t other = __shfl_down_sync(0xffffffffu, bb, o);
+                if (other != kNone && (bb == kNone || less(other, bb))) bb = other;
             }
-            s_taken[bb] = 1;
-            out[ra + r] = (uint32_t)s_c[ra + bb];
+            if (threadIdx.x == 0) {
+                s_taken[bb] = 1;
+                out[ra + r] = (uint32_t)s_c[ra + bb];
+            }
         }
         __syncthreads();
     }
@@ -952,21 +1005,35 @@ __global__ void __launch_bounds__(THREADS) k_rep_finalize(const uint32_t* __rest
     __syncthreads();
     const uint32_t n = s_n;
     // 2. coordinates and FP64-sum keys
-    for (uint32_t i = t; i < n; i += THREADS) {
-        const uint32_t r = s_row[i];
-        const float* x = pts + (size_t)r * d;
-        float4* dst = s_xyz + (size_t)i * V;
+    // every coordinate by its own thread (independent loads), then the
+    // FP64 sums from shared memory (FP64 rows: from the doubles)
+    {
+        float* sx = reinterpret_cast<float*>(s_xyz);
+        const uint32_t total = n * 4 * V;
+        for (uint32_t k0 = t; k0 < total; k0 += 4 * THREADS) {
+            float v[4];  // 4 loads in flight per thread
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            float c[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t j = 4 * v + q;
-                c[q] = j < d ? x[j] : 0.0f;
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t k = k0 + u * THREADS;
+                const uint32_t i = k / (4 * V), j = k - i * (4 * V);
+                v[u] = (k < total && j < d) ? pts[(size_t)s_row[i] * d + j] : 0.0f;
             }
-            dst[v] = make_float4(c[0], c[1], c[2], c[3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t k = k0 + u * THREADS;
+                if (k < total) sx[k] = v[u];
+            }
         }
-        const double sum = x64.x ? row_sum(x64.x, d, r) : row_sum(pts, d, r);
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < n; i += THREADS) {
+        double sum = 0.0;
+        if (x64.x) {
+            sum = row_sum(x64.x, d, s_row[i]);
+        } else {
+            const float* sx = reinterpret_cast<const float*>(s_xyz + (size_t)i * V);
+            for (uint32_t j = 0; j < d; ++j) sum = __dadd_rn(sum, (double)sx[j]);
+        }
         s_key[i] = __float_as_uint(__double2float_rn(sum));
     }
     __syncthreads();
@@ -1049,6 +1116,142 @@ void rep_finalize_launch(const uint32_t* cand, uint32_t slots, const float* pts,
     SKY_CUDA(cudaFuncSetAttribute(k_rep_finalize<D, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_rep_finalize<D, THREADS><<<1, THREADS, smem, st>>>(cand, slots, pts, d, out, out_count, tests, x64);
 }
+
+// The same finish spread over the GPU (three launches): per-slot coordinates
+// and keys; a warp per slot for its key rank and whether any other pick
+// dominates it (all picks in shared memory); one CTA places the survivors by
+// rank. The single-CTA kernel above runs ~130k warp instructions on one SM
+// for 1280 picks.
+template <int D>
+__global__ void __launch_bounds__(256) k_repf_load(const uint32_t* __restrict__ cand, uint32_t slots,
+                                                   const float* __restrict__ pts, uint32_t d, X64 x64,
+                                                   float4* __restrict__ cx, uint32_t* __restrict__ ckey) {
+    constexpr int V = Dims<D>::V;
+    const uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sl >= slots) return;
+    const uint32_t r = cand[sl];
+    float c[4 * V];
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4 * V; ++j) c[j] = (r != kNone && (uint32_t)j < d) ? pts[(size_t)r * d + j] : 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4 * V; ++j)
+        if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)c[j]);
+    if (x64.x && r != kNone) sum = row_sum(x64.x, d, r);
+#pragma unroll
+    for (int v = 0; v < V; ++v) cx[(size_t)sl * V + v] = make_float4(c[4 * v], c[4 * v + 1], c[4 * v + 2], c[4 * v + 3]);
+    // sums are finite and >= 0: 0xFFFFFFFF (a NaN pattern) marks an empty slot
+    ckey[sl] = r == kNone ? 0xFFFFFFFFu : __float_as_uint(__double2float_rn(sum));
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_repf_dom(const float4* __restrict__ cx, const uint32_t* __restrict__ ckey,
+                                                  const uint32_t* __restrict__ cand, uint32_t slots, X64 x64,
+                                                  uint32_t* __restrict__ rank, uint8_t* __restrict__ dead,
+                                                  unsigned long long* tests) {
+    constexpr int V = Dims<D>::V;
+    extern __shared__ float4 s_x[];  // [slots][V], then keys
+    uint32_t* s_k = reinterpret_cast<uint32_t*>(s_x + (size_t)slots * V);
+    for (uint32_t i = threadIdx.x; i < slots * V; i += blockDim.x) s_x[i] = cx[i];
+    for (uint32_t i = threadIdx.x; i < slots; i += blockDim.x) s_k[i] = ckey[i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    unsigned long long nt = 0;
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < slots; i += warps) {
+        const uint32_t ki = s_k[i];
+        if (ki == 0xFFFFFFFFu) continue;  // empty slot (warp-uniform)
+        float4 t[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) t[v] = s_x[(size_t)i * V + v];
+        uint32_t rk = 0;
+        bool hit = false;
+        for (uint32_t j = lane; j < slots; j += 32) {
+            const uint32_t kj = s_k[j];
+            rk += (kj < ki) | ((kj == ki) & (j < i));
+            if (!hit && kj <= ki && j != i) {
+                ++nt;
+                bool gt = false, lt = false;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const float4 a = s_x[(size_t)j * V + v], b = t[v];
+                    gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
+                    lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
+                }
+                hit = !gt && (x64.x ? dom64(x64, cand[j], cand[i]) : lt);
+            }
+        }
+        rk = __reduce_add_sync(0xffffffffu, rk);
+        const bool dom = __any_sync(0xffffffffu, hit);
+        if (lane == 0) {
+            rank[i] = rk;
+            dead[i] = dom;
+        }
+    }
+    if (tests) {
+        nt = warp_sum_u64(nt);
+        if (lane == 0 && nt) atomicAdd(tests, nt);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(1024) k_repf_emit(const float4* __restrict__ cx, const uint32_t* __restrict__ ckey,
+                                                    const uint32_t* __restrict__ cand, uint32_t slots,
+                                                    const uint32_t* __restrict__ rank, const uint8_t* __restrict__ dead,
+                                                    DevSet out, uint32_t* out_count) {
+    constexpr int V = Dims<D>::V;
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_at[REPF_MAX];  // slot at each rank, kNone if dominated / unused
+    for (uint32_t i = threadIdx.x; i < REPF_MAX; i += blockDim.x) s_at[i] = kNone;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < slots; i += blockDim.x)
+        if (ckey[i] != 0xFFFFFFFFu && !dead[i]) s_at[rank[i]] = i;
+    __syncthreads();
+    uint32_t keep[REPF_ITEMS], pos[REPF_ITEMS], total;
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) keep[k] = s_at[threadIdx.x * REPF_ITEMS + k] != kNone;
+    Scan(tmp).ExclusiveSum(keep, pos, total);
+#pragma unroll
+    for (int k = 0; k < REPF_ITEMS; ++k) {
+        if (!keep[k]) continue;
+        const uint32_t i = s_at[threadIdx.x * REPF_ITEMS + k], o = pos[k];
+#pragma unroll
+        for (int v = 0; v < V; ++v) reinterpret_cast<float4*>(out.xyz)[(size_t)o * V + v] = cx[(size_t)i * V + v];
+        out.skey[o] = ckey[i];
+        out.id[o] = cand[i];
+    }
+    if (threadIdx.x == 0) *out_count = total;
+}
+
+bool launch_rep_finalize_par(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
+                             uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, int sm_count,
+                             void* scratch, cudaStream_t st) {
+    if (slots > (uint32_t)REPF_MAX || slots == 0) return false;
+    const int V = (D + 3) / 4;
+    const size_t smem = (size_t)slots * (V * 16 + 4) + 16;
+    if (smem + 1024 > (size_t)smem_optin) return false;
+    char* sc = static_cast<char*>(scratch);
+    float4* cx = reinterpret_cast<float4*>(sc);
+    uint32_t* ckey = reinterpret_cast<uint32_t*>(sc + (size_t)REPF_MAX * V * 16);
+    uint32_t* rank = ckey + REPF_MAX;
+    uint8_t* dead = reinterpret_cast<uint8_t*>(rank + REPF_MAX);
+    // one warp per slot, as many CTAs as fit one wave
+    const uint32_t dom_grid = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(slots, 8), (uint32_t)sm_count));
+    SKY_DISPATCH_D(D, {
+        k_repf_load<DT><<<ceil_div(slots, 256), 256, 0, st>>>(cand, slots, pts, d, x64, cx, ckey);
+        SKY_LAUNCH_CHECK();
+        if (smem > 48 * 1024)
+            SKY_CUDA(cudaFuncSetAttribute(k_repf_dom<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_repf_dom<DT><<<dom_grid, 256, smem, st>>>(cx, ckey, cand, slots, x64, rank, dead, tests);
+        SKY_LAUNCH_CHECK();
+        k_repf_emit<DT><<<1, 1024, 0, st>>>(cx, ckey, cand, slots, rank, dead, out, out_count);
+        SKY_LAUNCH_CHECK();
+    });
+    return true;
+}
+
+size_t rep_finalize_scratch_bytes(int D) { return (size_t)REPF_MAX * (((D + 3) / 4) * 16 + 9) + 64; }
 
 bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
                          uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st) {

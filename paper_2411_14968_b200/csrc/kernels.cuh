@@ -111,7 +111,7 @@ void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t*
                      const uint32_t* off_end = nullptr);
 // Stream path of the sorted representatives (select_representatives_sorted,
 // filter.cpp:66-86): per-partition key bound = q-th smallest of the prep
-// CTAs' minima gmin[G][P] -> rows under the bound in B-slot buckets (overflow
+// CTAs' minima gmin[P][G] -> rows under the bound in B-slot buckets (overflow
 // flag set if one fills) -> each bucket sorted, first q picked exactly into
 // cand[p * q + k] (kNone when the partition has fewer rows).
 void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t q, uint32_t G,
@@ -123,6 +123,13 @@ void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32
 // into `out`, count in *out_count. false: too many picks (host path).
 bool launch_rep_finalize(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
                          uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st);
+
+// The same finish in three launches spread over the GPU (scratch:
+// rep_finalize_scratch_bytes(D)). false: not applicable (use the above).
+bool launch_rep_finalize_par(int D, const uint32_t* cand, uint32_t slots, const float* pts, uint32_t d, DevSet out,
+                             uint32_t* out_count, unsigned long long* tests, X64 x64, int smem_optin, int sm_count,
+                             void* scratch, cudaStream_t st);
+size_t rep_finalize_scratch_bytes(int D);
 
 // Compaction plumbing.
 void launch_scatter_direct(int D, const DevSet& in, const uint8_t* dead, const uint32_t* pos, DevSet out,

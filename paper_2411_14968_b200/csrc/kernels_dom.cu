@@ -742,6 +742,9 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
     const uint32_t nrep = nrep_dev ? min(*nrep_dev, nrep_max) : nrep_max;
+    // packed codes pay off from 32 representatives on (the count may only be
+    // known on the device)
+    const bool use_codes = CODES && nrep >= 32;
     const uint32_t npad = (nrep_max + 7) & ~7u;
     extern __shared__ float4 s_rep[];
     uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)npad * V);
@@ -751,7 +754,8 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) {
         // padding codes never pass the coarse test (bit 31 of word 1 borrows)
         if (CODES) s_code[i] = i < nrep ? rep_qc[i] : make_uint2(0u, 0x80000000u);
-        s_key[i] = i < nrep ? rep_key[i] : 0xFFFFFFFFu;
+        // APPEND compares truncated keys (the rows' keys come from key64)
+        s_key[i] = i < nrep ? (APPEND ? rep_key[i] & ~((1u << app.key_shift) - 1u) : rep_key[i]) : 0xFFFFFFFFu;
     }
     if (CODES)
         for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
@@ -760,7 +764,8 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         (reinterpret_cast<uintptr_t>(s_thr + (CODES ? D * kThr : 0)) + 15) & ~uintptr_t{15});
     __syncthreads();
     unsigned long long nt = 0;
-    auto process = [&](const float* x, const uint32_t slot, const bool valid, const uint32_t row) {
+    auto process = [&](const float* x, const uint32_t slot, const bool valid, const uint32_t row,
+                       const uint64_t* key_in) {
     float4 t[V];
     uint32_t tk = 0;
     uint32_t T0 = G, T1 = G | 0x80000000u;  // never passes unless set below
@@ -780,16 +785,22 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
 #pragma unroll
             for (int j = 0; j < 4 * V; ++j) xs[j] = (valid && j < D && (uint32_t)j < d) ? x[j] : 0.0f;
         }
+        if (APPEND) {
+            // the prep pass's (truncated) key, staged with the row: no FP64
+            // sum per row; with few representatives no key gating at all
+            tk = !use_codes ? 0xFFFFFFFFu : (valid ? (uint32_t)*key_in : 0u);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4 * V; ++j)
-            if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)xs[j]);  // same key as k_prep
-        if (x64.x && valid) {
-            const double* xd = x64.x + (size_t)row * d;
-            sum = 0.0;
-            for (uint32_t j = 0; j < d; ++j) sum = __dadd_rn(sum, xd[j]);
+            for (int j = 0; j < 4 * V; ++j)
+                if ((uint32_t)j < d) sum = __dadd_rn(sum, (double)xs[j]);  // same key as k_prep
+            if (x64.x && valid) {
+                const double* xd = x64.x + (size_t)row * d;
+                sum = 0.0;
+                for (uint32_t j = 0; j < d; ++j) sum = __dadd_rn(sum, xd[j]);
+            }
+            tk = __float_as_uint(__double2float_rn(sum));
         }
-        tk = __float_as_uint(__double2float_rn(sum));
-        if (CODES && valid) {
+        if (use_codes && valid) {
             uint32_t w[2] = {0, 0};
 #pragma unroll
             for (int j = 0; j < D; ++j) {
@@ -803,7 +814,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     }
     bool alive = valid;
     const uint32_t bound = __reduce_max_sync(0xffffffffu, alive ? tk : 0u);
-    if (CODES) {
+    if (use_codes) {
         // 8 representatives per step: 8 coarse tests folded by 3-input min,
         // exact FP32 re-check only on a coarse pass; one vote per step
         uint32_t Tl[2] = {T0, T1};
@@ -842,7 +853,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         for (; r < nrep; ++r) {
             if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
             bool maybe = alive;
-            if (CODES) {
+            if (use_codes) {
                 const uint2 q = s_code[r];
                 constexpr uint32_t GA = G | 0x80000000u;
                 maybe = ((T0 - q.x) & (T1 - q.y) & GA) == GA;
@@ -868,7 +879,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep)
             app.out[base + __popc(bal & ((1u << lane) - 1u))] =
-                ((__ldcs(app.key64 + row) >> app.key_shift) << app.row_bits) | row;
+                ((app.key64[row] >> app.key_shift) << app.row_bits) | row;
     } else if (POSORDER) {
         if (valid && !alive) dead_row[slot] = 1;
     } else if (valid) {
@@ -876,15 +887,18 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     }
     };
     if (APPEND) {
-        stream_row_tiles(pts, n, d, s_stage, [&](const float* tile, uint32_t r0, uint32_t nr) {
-            const uint32_t r = r0 + threadIdx.x;
-            process(tile + (size_t)threadIdx.x * d, r, threadIdx.x < nr, r);
-        });
+        stream_row_tiles(
+            pts, n, d, s_stage,
+            [&](const float* tile, uint32_t r0, uint32_t nr, const uint64_t* keys) {
+                const uint32_t r = r0 + threadIdx.x;
+                process(tile + (size_t)threadIdx.x * d, r, threadIdx.x < nr, r, keys + threadIdx.x);
+            },
+            app.key64);
     } else {
         const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
         const bool valid = slot < n && (!POSORDER || !dead_row[slot]);
         const uint32_t row = (POSORDER && slot < n) ? idx[slot] : slot;
-        process(pts + (size_t)row * d, slot, valid, row);
+        process(pts + (size_t)row * d, slot, valid, row, nullptr);
     }
     if (tests) {
         nt = warp_sum(nt);
@@ -1028,7 +1042,7 @@ bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, co
     const bool codes = rep_qc && thr && nrep >= 32;
     const size_t npad = (nrep + 7) & ~7u;
     const size_t smem = npad * ((D + 3) / 4) * 16 + npad * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64 +
-                        stream_smem_bytes(d) + 16;
+                        stream_smem_bytes(d, true) + 16;
     if (smem + 1024 > (size_t)smem_optin) return false;
     if (!n) return true;
     // persistent CTAs: as many as fit, capped by the tile count

@@ -49,22 +49,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-// Shared memory of the ring: kStreamStages tiles of kStreamRows * d floats,
-// then the barriers.
-__host__ __device__ inline size_t stream_smem_bytes(uint32_t d) {
-    return (size_t)kStreamStages * kStreamRows * d * sizeof(float) + kStreamStages * sizeof(uint64_t) + 16;
+// Shared memory of the ring: kStreamStages stages of (kStreamRows * d
+// floats [+ kStreamRows u64 of the optional per-row aux array]), then the
+// barriers.
+__host__ __device__ inline size_t stream_stage_bytes(uint32_t d, bool aux) {
+    return (size_t)kStreamRows * d * sizeof(float) + (aux ? kStreamRows * sizeof(uint64_t) : 0);
+}
+__host__ __device__ inline size_t stream_smem_bytes(uint32_t d, bool aux = false) {
+    return (size_t)kStreamStages * stream_stage_bytes(d, aux) + kStreamStages * sizeof(uint64_t) + 16;
 }
 
-// Walk this CTA's tiles. `body(tile, row0, nrows)` runs on every thread with
-// the tile's rows in shared memory (row r of the tile at tile + r * d); it
-// must not call __syncthreads. `smem` is 16-byte aligned, stream_smem_bytes(d)
-// long. pts must be 16-byte aligned.
+// Walk this CTA's tiles. `body(tile, row0, nrows, aux_tile)` runs on every
+// thread with the tile's rows in shared memory (row r of the tile at
+// tile + r * d) and, if `aux` is given, aux[row0 .. row0 + nrows) at
+// aux_tile; it must not call __syncthreads. `smem` is 16-byte aligned,
+// stream_smem_bytes(d, aux != nullptr) long; pts and aux 16-byte aligned.
 template <class Body>
 __device__ __forceinline__ void stream_row_tiles(const float* __restrict__ pts, uint32_t n, uint32_t d, char* smem,
-                                                 Body&& body) {
-    const uint32_t tile_floats = kStreamRows * d;
-    float* stage = reinterpret_cast<float*>(smem);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kStreamStages * tile_floats * sizeof(float));
+                                                 Body&& body, const uint64_t* __restrict__ aux = nullptr) {
+    const size_t stage_bytes = stream_stage_bytes(d, aux != nullptr);
+    const size_t row_bytes = (size_t)kStreamRows * d * sizeof(float);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStreamStages * stage_bytes);
     const uint32_t tiles = (n + kStreamRows - 1) / kStreamRows;
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
@@ -72,14 +77,17 @@ __device__ __forceinline__ void stream_row_tiles(const float* __restrict__ pts, 
         mbar_fence_init();
     }
     __syncthreads();
-    // the bulk copy takes the 16-byte multiple of a tile; the few floats of
-    // an odd-sized last tile past it are loaded by the threads
+    // the bulk copies take the 16-byte multiples of a tile; the few words of
+    // an odd-sized last tile past them are loaded by the threads
     auto issue = [&](uint32_t t, uint32_t s) {
         const uint32_t r0 = t * kStreamRows;
         const uint32_t nr = min(kStreamRows, n - r0);
         const uint32_t bytes = (nr * d * (uint32_t)sizeof(float)) & ~15u;
-        mbar_arrive_expect_tx(bars + s, bytes);
-        if (bytes) bulk_g2s(stage + (size_t)s * tile_floats, pts + (size_t)r0 * d, bytes, bars + s);
+        const uint32_t abytes = aux ? (nr * (uint32_t)sizeof(uint64_t)) & ~15u : 0u;
+        char* st = smem + s * stage_bytes;
+        mbar_arrive_expect_tx(bars + s, bytes + abytes);
+        if (bytes) bulk_g2s(st, pts + (size_t)r0 * d, bytes, bars + s);
+        if (abytes) bulk_g2s(st + row_bytes, aux + r0, abytes, bars + s);
     };
     if (tid == 0)
         for (uint32_t s = 0; s < kStreamStages; ++s) {
@@ -91,15 +99,20 @@ __device__ __forceinline__ void stream_row_tiles(const float* __restrict__ pts, 
         if (t >= tiles) break;
         const uint32_t s = it % kStreamStages;
         mbar_wait(bars + s, (it / kStreamStages) & 1u);
-        float* tile = stage + (size_t)s * tile_floats;
+        char* st = smem + s * stage_bytes;
+        float* tile = reinterpret_cast<float*>(st);
+        uint64_t* atile = aux ? reinterpret_cast<uint64_t*>(st + row_bytes) : nullptr;
         const uint32_t r0 = t * kStreamRows;
         const uint32_t nr = min(kStreamRows, n - r0);
         const uint32_t nf = nr * d, done = (nf * (uint32_t)sizeof(float) & ~15u) / (uint32_t)sizeof(float);
-        if (done != nf) {  // last tile only (uniform branch)
+        const uint32_t adone = (nr * (uint32_t)sizeof(uint64_t) & ~15u) / (uint32_t)sizeof(uint64_t);
+        if (done != nf || (aux && adone != nr)) {  // last tile only (uniform branch)
             for (uint32_t k = done + tid; k < nf; k += blockDim.x) tile[k] = pts[(size_t)r0 * d + k];
+            if (aux)
+                for (uint32_t k = adone + tid; k < nr; k += blockDim.x) atile[k] = aux[r0 + k];
             __syncthreads();
         }
-        body(tile, r0, nr);
+        body(tile, r0, nr, atile);
         __syncthreads();  // stage s is free again
         const uint32_t tn = t + kStreamStages * gridDim.x;
         if (tid == 0 && tn < tiles) issue(tn, s);
