@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SKY_ABI_VERSION 1
+#define SKY_ABI_VERSION 2
 
 /* Return codes mirror the reference's exception classes (core.hpp:13-34). */
 typedef enum sky_status {
@@ -116,6 +116,10 @@ typedef struct sky_result {
     uint64_t dom_tests;         /* dominance tests they executed */
     uint64_t dom_exact_checks;  /* pairs the packed codes could not rule out */
     uint64_t exact_checks_merge;
+    /* HBM streaming passes (prep, representative prefilter, candidate pass) */
+    uint32_t stream_launches;
+    double stream_kernel_ms;    /* summed CUDA-event time of those launches */
+    uint64_t stream_bytes;      /* algorithmic bytes they move (reads + writes) */
 } sky_result;
 
 typedef struct sky_ctx sky_ctx;

@@ -80,6 +80,9 @@ class SkyResult(C.Structure):
         ("dom_tests", C.c_uint64),
         ("dom_exact_checks", C.c_uint64),
         ("exact_checks_merge", C.c_uint64),
+        ("stream_launches", C.c_uint32),
+        ("stream_kernel_ms", C.c_double),
+        ("stream_bytes", C.c_uint64),
     ]
 
 

@@ -55,6 +55,9 @@ struct sky_ctx {
     cudaEvent_t ev[6] = {};
     std::vector<cudaEvent_t> dom_ev;  // (start, end) pairs, one per dominance launch of a run
     uint32_t dom_used = 0;
+    std::vector<cudaEvent_t> hbm_ev;  // (start, end) pairs of the HBM streaming passes of a run
+    uint32_t hbm_used = 0;
+    uint64_t hbm_bytes = 0;
     // pinned staging for async H2D copies: bump-allocated per run, never
     // reused within a run, so no launch has to wait for its copy to drain
     std::vector<std::pair<char*, size_t>> stage;
@@ -304,6 +307,8 @@ class Runner {
     Runner(sky_ctx* c) : c_(c), st_(c->stream) {
         c->stage_cur = c->stage_off = 0;
         c->dom_used = 0;
+        c->hbm_used = 0;
+        c->hbm_bytes = 0;
     }
 
     // Pinned bytes that stay untouched until the stream drains.
@@ -796,6 +801,30 @@ class Runner {
         ++c_->dom_used;
         c_->dom_launches += 1;
     }
+    // the same for the HBM streaming passes, with their algorithmic bytes
+    void hbm_begin() {
+        auto& e = c_->hbm_ev;
+        while (e.size() < 2 * (size_t)(c_->hbm_used + 1)) {
+            cudaEvent_t ev;
+            SKY_CUDA(cudaEventCreate(&ev));
+            e.push_back(ev);
+        }
+        SKY_CUDA(cudaEventRecord(e[2 * c_->hbm_used], st_));
+    }
+    void hbm_end(uint64_t bytes) {
+        SKY_CUDA(cudaEventRecord(c_->hbm_ev[2 * c_->hbm_used + 1], st_));
+        ++c_->hbm_used;
+        c_->hbm_bytes += bytes;
+    }
+    double hbm_collect() {
+        double t = 0.0;
+        for (uint32_t k = 0; k < c_->hbm_used; ++k) {
+            float ms = 0.f;
+            SKY_CUDA(cudaEventElapsedTime(&ms, c_->hbm_ev[2 * k], c_->hbm_ev[2 * k + 1]));
+            t += ms;
+        }
+        return t;
+    }
     void dom_collect() {
         for (uint32_t k = 0; k < c_->dom_used; ++k) {
             float ms = 0.f;
@@ -1119,6 +1148,17 @@ void check_prep(uint32_t err, uint32_t amb, int strategy, bool eager) {
     if (!eager && strategy == SKY_ANGULAR && amb) throw RedoEager{};
 }
 
+// Low bits cleared from the sum key in the (pid << 32 | skey) sort key, so
+// the partition sort needs 32 - shift + pb bits: 24 (3 radix passes) up to
+// 32 partitions (the key keeps >= 19 bits: 10 mantissa bits), else 32 (4
+// passes) up to 2^12 partitions, else none. A coarser key only adds ties;
+// every bounded test scans equal keys, so results do not depend on it.
+uint32_t key_shift_for(uint64_t P) {
+    const int pb = std::max(1, bits_for(P));
+    if (pb <= 5) return (uint32_t)pb + 8;
+    return pb <= 12 ? (uint32_t)pb : 0u;
+}
+
 struct PartitionOut {
     uint64_t* key64;   // sorted (pid << 32 | skey)
     uint32_t* idx;     // row of each sorted position
@@ -1145,14 +1185,18 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     // sort key (pid << 32 | skey): with skey's low pb bits cleared the sort
     // needs 32 key bits (4 radix passes) for P <= 2^12 partitions
     const int pb = std::max(1, bits_for(P));
-    const uint32_t key_shift = pb <= 12 ? (uint32_t)pb : 0u;
+    const uint32_t key_shift = key_shift_for(P);
     PrepArgs pa{pts, R.x64_.x, n, d, strategy, m, normalized, pid_in, (uint32_t)cfg->slice_dim, keyA,
                 sort_rows ? idxA : nullptr, skA, misc + M_ERR, misc + M_AMB, amb, amb_cap, key_shift};
     if (gmin) {
         pa.gmin = gmin;
         pa.P = (uint32_t)P;
     }
+    R.hbm_begin();
     launch_prep(pa, st, R.c_->sm_count);
+    // rows read once; key (8 B) written, row index (4 B) when sorting follows
+    R.hbm_end((uint64_t)n * d * (R.x64_.x ? 8 : 4) + (uint64_t)n * (sort_rows ? 12 : 8) +
+              (strategy == SKY_SLICED ? 4ull * n : 0ull));
     R.count();
 
     // errors + angular boundary points (one host round trip). Deferred mode
@@ -1557,8 +1601,10 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             uint32_t* bcnt = R.dev<uint32_t>(S_BCNT, P);
             uint64_t* bkey = R.dev<uint64_t>(S_BKEY, (size_t)P * kRepBucket);
             uint32_t* brow = R.dev<uint32_t>(S_BROW, (size_t)P * kRepBucket);
-                        launch_rep_candidates(po.key64, n, P, q, prep_grid, gmin, thr, kRepBucket, bcnt, bkey, brow, pts, d,
+                        R.hbm_begin();
+            launch_rep_candidates(po.key64, n, P, q, prep_grid, gmin, thr, kRepBucket, bcnt, bkey, brow, pts, d,
                                   cand, misc + M_OVF, st);
+            R.hbm_end((uint64_t)n * 8);  // the key pass (thresholds and picks are small)
             R.count(3);
         } else {
             launch_rep_pick(po.key64, po.idx, po.off, P, pts, R.x64_.x, d, q, cand, st);
@@ -1598,16 +1644,20 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             app.key64 = po.key64;
             app.out = R.dev<uint64_t>(S_SURV, n);
             app.count = misc + M_S0;
-            app.key_shift = (uint32_t)std::max(1, bits_for(P));
+            app.key_shift = key_shift_for(P);
             app.row_bits = (uint32_t)std::max(1, bits_for(n));
+            R.hbm_begin();
             if (!launch_prefilter_append(D, pts, d, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.id, reps.n,
                                          nrep_dev, pthr, app, count_tests ? R.tests(1) : nullptr, c->smem_optin, st))
                 throw Error(SKY_E_INTERNAL, "stream prefilter not applicable");
+            R.hbm_end((uint64_t)n * (4ull * d + 8));  // rows + keys (survivor writes are few)
             R.count();
-        } else if (reps.n > 0 && launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,
-                                           reps.id, reps.n, nrep_dev, pthr, dead_row, dead,
-                                           count_tests ? R.tests(1) : nullptr, R.x64_, c->smem_optin, st,
-                                           (uint64_t)n * d * sizeof(float) <= (48ull << 20))) {
+        } else if (reps.n > 0 && (R.hbm_begin(),  // an unmatched begin is overwritten by the next
+                                  launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,
+                                                   reps.id, reps.n, nrep_dev, pthr, dead_row, dead,
+                                                   count_tests ? R.tests(1) : nullptr, R.x64_, c->smem_optin, st,
+                                                   (uint64_t)n * d * sizeof(float) <= (48ull << 20)))) {
+            R.hbm_end((uint64_t)n * (4ull * d + 5));  // rows through the index, dead flags
             R.count();
             any_dead = true;
         } else if (reps.n > 0) {
@@ -1652,10 +1702,10 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         const uint32_t rb = (uint32_t)std::max(1, bits_for(n));
         uint64_t* surv = R.dev<uint64_t>(S_SURV, n);
         uint64_t* surv2 = R.dev<uint64_t>(S_SURV2, std::max<uint32_t>(ns, 1));
-        R.sort_keys(surv, surv2, ns, 32 + (int)rb);
+        R.sort_keys(surv, surv2, ns, 32 + std::max(1, bits_for(P)) - (int)key_shift_for(P) + (int)rb);
         uint64_t* k64 = R.dev<uint64_t>(S_KEY_B, std::max<uint32_t>(ns, 1));
         uint32_t* rows = R.dev<uint32_t>(S_IDX_B, std::max<uint32_t>(ns, 1));
-        launch_unpack_survivors(surv2, ns, rb, (uint32_t)std::max(1, bits_for(P)), P, k64, rows, off1_dev, st);
+        launch_unpack_survivors(surv2, ns, rb, key_shift_for(P), P, k64, rows, off1_dev, st);
         R.count();
         s0 = R.set(S_SET0, ns, D);
         launch_scatter_indirect(D, pts, d, rows, k64, ns, nullptr, nullptr, s0, st);
@@ -1928,6 +1978,9 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     out->kernel_launches = c->launches;
     out->dom_launches = c->dom_launches;
     R.dom_collect();
+    out->stream_kernel_ms = R.hbm_collect();
+    out->stream_bytes = c->hbm_bytes;
+    out->stream_launches = c->hbm_used;
     R.timeline_dump();
     out->dom_kernel_ms = c->dom_ms;
     out->dom_tests = ht[0] + ht[1] + ht[2];
@@ -2036,6 +2089,8 @@ void sky_ctx_destroy(sky_ctx* c) {
     for (auto& e : c->dom_ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->tl_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->hbm_ev)
         if (e) cudaEventDestroy(e);
     if (c->sync_ev) cudaEventDestroy(c->sync_ev);
     for (auto& b : c->stage) cudaFreeHost(b.first);

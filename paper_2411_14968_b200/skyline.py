@@ -161,6 +161,9 @@ class PhaseMetrics:
     dom_launches: int = 0
     dom_kernel_ms: float = 0.0
     dom_tests: int = 0
+    stream_launches: int = 0
+    stream_kernel_ms: float = 0.0
+    stream_bytes: int = 0
     dom_exact_checks: int = 0
 
     @property
@@ -288,7 +291,9 @@ class Engine:
                 angular_host_fixups=int(res.angular_host_fixups), kernel_launches=int(res.kernel_launches),
                 h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
                 dom_launches=int(res.dom_launches), dom_kernel_ms=float(res.dom_kernel_ms),
-                dom_tests=int(res.dom_tests), dom_exact_checks=int(res.dom_exact_checks))
+                dom_tests=int(res.dom_tests), dom_exact_checks=int(res.dom_exact_checks),
+                stream_launches=int(res.stream_launches), stream_kernel_ms=float(res.stream_kernel_ms),
+                stream_bytes=int(res.stream_bytes))
             return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
         finally:
             self._lib.sky_result_free(C.byref(res))

@@ -62,10 +62,15 @@ def summarize_launches(path):
     hdr = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hdr]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     for r in rows[hdr + 1:]:
         if len(r) <= vi:
+            continue
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
+        if r[ki].startswith("void at::"):  # bench.py's L2 flush (torch), not an engine kernel
             continue
         v = float(r[vi].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki].split("(")[0]
@@ -87,8 +92,13 @@ def main():
     os.makedirs(outdir, exist_ok=True)
     summary = {}
     for spec in a.reports:
-        path, tag = spec.split(":")
-        summary[tag] = summarize_report(path)
+        # path:tag (dominance kernels) or path:tag:stream (HBM streaming passes)
+        parts = spec.split(":")
+        path, tag = parts[0], parts[1]
+        if len(parts) > 2 and parts[2] == "stream":
+            summary.setdefault("stream", {})[tag] = summarize_report(path)
+        else:
+            summary[tag] = summarize_report(path)
     for spec in a.launches:
         path, tag = spec.split(":")
         summary[f"{tag}_launch_list"] = summarize_launches(path)
