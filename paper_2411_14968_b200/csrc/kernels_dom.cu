@@ -630,11 +630,13 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                 }
                 for (; w < wn; ++w) slow(w);
                 if (valid) ntests += 2ull * wn;
-                // batch x batch: is t dominated by an earlier-or-equal-key batch tuple?
-                for (uint32_t u = 0; u < bn; ++u) {
-                    if (b_key[u] > tkey) continue;  // sorted batches: a dominator has key <= tkey
+                // batch x batch: is t dominated by an earlier-or-equal-key batch
+                // tuple? Batch keys are nondecreasing (the partition and the
+                // overflow list keep key order), so the scan stops at the first
+                // larger key; 4 tuples per step, coarse misses max-folded.
+                auto slow_b = [&](uint32_t u) {
                     const uint2 uq = b_code[u];
-                    if (u != (uint32_t)tid && ((T0 - uq.x) & (T1 - uq.y) & GA) == GA) {
+                    if (u != (uint32_t)tid && b_key[u] <= tkey && ((T0 - uq.x) & (T1 - uq.y) & GA) == GA) {
                         if (dom_f4x<D>(b_xyz + u * V, t, a.x64,
                                        a.x64.x ? a.id[first ? seg_b + k0 + u : ovf[k0 + u]] : 0,
                                        a.x64.x ? a.id[mypos] : 0)) {
@@ -642,8 +644,28 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                             T0 &= ~ALIVE;
                         }
                     }
+                };
+                uint32_t u = 0;
+                if (valid && alive) {
+                    for (; u + 4 <= bn; u += 4) {
+                        const uint4 kk = *reinterpret_cast<const uint4*>(b_key + u);
+                        if (kk.x > tkey) break;
+                        const uint4 qa = *reinterpret_cast<const uint4*>(b_code + u);
+                        const uint4 qb = *reinterpret_cast<const uint4*>(b_code + u + 2);
+                        const uint32_t f0 = ~((T0 - qa.x) & (T1 - qa.y)) & GA;
+                        const uint32_t f1 = ~((T0 - qa.z) & (T1 - qa.w)) & GA;
+                        const uint32_t f2 = ~((T0 - qb.x) & (T1 - qb.y)) & GA;
+                        const uint32_t f3 = ~((T0 - qb.z) & (T1 - qb.w)) & GA;
+                        if (min(min(f0, f1), min(f2, f3)) == 0) {
+                            slow_b(u);
+                            slow_b(u + 1);
+                            slow_b(u + 2);
+                            slow_b(u + 3);
+                        }
+                    }
+                    for (; u < bn && b_key[u] <= tkey; ++u) slow_b(u);
+                    ntests += u;
                 }
-                if (valid) ntests += bn - 1;
                 if (__syncthreads_or(killed_any)) compact_window();
                 // survivors enter the window in batch order, or spill
                 {
