@@ -46,6 +46,10 @@ extern "C" int sky_plan_split(const uint64_t* cost_prefix, uint64_t count, int r
 struct sky_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
+    // side stream for the input copy when it can overlap data-independent
+    // work (the random partitioner), with its fork/join events
+    cudaStream_t copy = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaStream_t stream = nullptr;
     std::string err;
     Arena dev;
@@ -1513,14 +1517,26 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         R.count();
         pts = dp;
         R.x64_ = X64{p64, d};
-    } else if (!on_device) {
+    }
+    // random partitioning does not read the rows: their copy runs on the
+    // side stream, overlapped with the partitioner, and joins before prep
+    const bool overlap_copy = !f64 && !on_device && cfg->strategy == SKY_RANDOM && c->copy;
+    if (!f64 && !on_device) {
         float* dp = R.dev<float>(S_PTS, (size_t)n * d);
-        SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, st));
+        if (overlap_copy) {
+            SKY_CUDA(cudaEventRecord(c->fork_ev, st));
+            SKY_CUDA(cudaStreamWaitEvent(c->copy, c->fork_ev, 0));
+            SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, c->copy));
+            SKY_CUDA(cudaEventRecord(c->join_ev, c->copy));
+        } else {
+            SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, st));
+        }
         pts = dp;
         out->h2d_bytes += (uint64_t)n * d * sizeof(float);
     }
     const bool defer_rand = !eager && c->world == 1;
     const uint32_t* pid_dev = cfg->strategy == SKY_RANDOM ? R.random_pids(n, P, cfg->seed, defer_rand) : nullptr;
+    if (overlap_copy) SKY_CUDA(cudaStreamWaitEvent(st, c->join_ev, 0));
     const bool rep_random = cfg->filter == SKY_FILTER_REPRESENTATIVE && cfg->rep_selection == SKY_REPS_RANDOM;
     uint32_t* scan_rows = nullptr;  // sliced + random reps: split()'s exact scan order
     // Stream path (single GPU, sorted representatives, large input): no sort
@@ -2034,6 +2050,9 @@ int sky_ctx_create(int device, sky_ctx** out) {
     int rc = guarded(c, [&] {
         SKY_CUDA(cudaSetDevice(device));
         SKY_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        SKY_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        SKY_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+        SKY_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
         c->stream = c->own;
         SKY_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         SKY_CUDA(cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -2097,6 +2116,9 @@ void sky_ctx_destroy(sky_ctx* c) {
     if (c->mt_jump) cudaFree(c->mt_jump);
     c->dev.release();
     if (c->own) cudaStreamDestroy(c->own);
+    if (c->copy) cudaStreamDestroy(c->copy);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
     delete c;
 }
 
