@@ -93,7 +93,7 @@ enum Slot {
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
     S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
-    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_COUNT
+    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_DCBT, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -572,21 +572,37 @@ class Runner {
         uint32_t* hp = stage<uint32_t>(1);
         *hp = P;
         SKY_CUDA(cudaMemcpyAsync(np_dev, hp, sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        // jobs -> items: one fused planning launch for up to 1024 partitions
+        auto plan = [&](const uint32_t* coff, uint64_t lo, uint64_t hi) -> Item* {
+            Item* it = dev<Item>(S_ITEMS, icap);
+            uint32_t* ni = misc + M_NITEMS;
+            if (launch_plan_partition_items(coff, off0_dev, nullptr, P, lo, hi, tile, chunk, max_chunks,
+                                            (uint32_t)std::min<uint64_t>(icap, 0xFFFFFFFFu), it, ni, st_)) {
+                count();
+                n_items = ni;
+                return it;
+            }
+            launch_partition_jobs(coff, off0_dev, nullptr, P, lo, hi, jobs, st_);
+            count();
+            return expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+        };
         // wave 0: every row of a partition against the partition's first `head` rows
-        launch_partition_jobs(off0_dev, off0_dev, nullptr, P, 0, head, jobs, st_);
-        count();
-        Item* items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+        Item* items = plan(off0_dev, 0, head);
         relsky_direct(D, tile, a, s0.qc, s0.qc, nullptr, items, icap, n_items);
         // wave 1: the live rows (dense lists) against the rest of their partition
-        uint32_t* pos = dev<uint32_t>(S_POS, cap);
         uint32_t* dnew = dev<uint32_t>(S_DNEW, P + 1);
         uint32_t* dense = dev<uint32_t>(S_DENSE, cap);
-        scan_live(dead, pos, cap);
-        launch_remap_offsets(off0_dev, P, pos, dead, cap, dnew, st_);
-        launch_compact_pos(dead, pos, cap, 0, dense, st_);
-        launch_partition_jobs(dnew, off0_dev, nullptr, P, head, ~0ull, jobs, st_);
-        count(3);
-        items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+        if (launch_dense_compact(dead, cap, off0_dev, P, 0, dense, dnew, nullptr,
+                                 dev<uint32_t>(S_DCBT, dense_compact_scratch(cap) / 4), st_)) {
+            count(2);
+        } else {
+            uint32_t* pos = dev<uint32_t>(S_POS, cap);
+            scan_live(dead, pos, cap);
+            launch_remap_offsets(off0_dev, P, pos, dead, cap, dnew, st_);
+            launch_compact_pos(dead, pos, cap, 0, dense, st_);
+            count(2);
+        }
+        items = plan(dnew, head, ~0ull);
         relsky_direct(D, tile, a, s0.qc, s0.qc, dense, items, icap, n_items);
         return compact_dev(s0, dead, off0_dev, P, S_SET2, off_u_dev, n_u, D);
     }
@@ -743,10 +759,15 @@ class Runner {
             }
             if (!cap) continue;
             // dense lists of the candidates still alive
-            scan_live(base.dead + cb, pos, cn);
-            launch_remap_offsets(drel, np, pos, base.dead + cb, cn, dnew, st_);
-            launch_compact_pos(base.dead + cb, pos, cn, cb, dense, st_);
-            count(4);
+            if (launch_dense_compact(base.dead + cb, cn, drel, np, cb, dense, dnew, nullptr,
+                                     dev<uint32_t>(S_DCBT, dense_compact_scratch(cn) / 4), st_)) {
+                count(2);
+            } else {
+                scan_live(base.dead + cb, pos, cn);
+                launch_remap_offsets(drel, np, pos, base.dead + cb, cn, dnew, st_);
+                launch_compact_pos(base.dead + cb, pos, cn, cb, dense, st_);
+                count(4);
+            }
             uint2* hr = stage<uint2>(ranges.size());
             std::memcpy(hr, ranges.data(), ranges.size() * sizeof(uint2));
             uint2* hg = stage<uint2>(groups.size());

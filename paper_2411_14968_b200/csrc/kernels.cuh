@@ -238,6 +238,18 @@ void launch_job_counts(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, ui
 void launch_job_items(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, const uint32_t* prefix, uint32_t tile,
                       uint32_t chunk, uint32_t max_chunks, Item* items, cudaStream_t st);
 
+// jobs + counts + scan + items in one CTA (P <= 1024; false otherwise);
+// *n_items = min(items, cap)
+bool launch_plan_partition_items(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
+                                 uint64_t lo, uint64_t hi, uint32_t tile, uint32_t chunk, uint32_t max_chunks,
+                                 uint32_t cap, Item* items, uint32_t* n_items, cudaStream_t st);
+// dense list of live entries + remapped segment offsets (off[P+1] sorted)
+// in two launches; block_tot: dense_compact_scratch(n) bytes. false: n == 0
+bool launch_dense_compact(const uint8_t* dead, uint32_t n, const uint32_t* off, uint32_t P, uint32_t base,
+                          uint32_t* dense, uint32_t* off_new, uint32_t* total, uint32_t* block_tot,
+                          cudaStream_t st);
+size_t dense_compact_scratch(uint32_t n);
+
 // Items of a relsky wave built on the device from the dense candidate
 // offsets of np partitions (dnew[np+1], relative to the dense list) and each
 // partition's comparator groups (groups[gb[p]..gb[p+1]) = (lb, le) into the

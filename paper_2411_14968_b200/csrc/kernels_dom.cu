@@ -1259,6 +1259,158 @@ void launch_job_items(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, con
     SKY_LAUNCH_CHECK();
 }
 
+// The three planning steps above (jobs, counts + scan, items) in one CTA
+// for up to 1024 partitions: thread p builds job p and counts its items, a
+// block scan places them, then the CTA writes every item (binary search of
+// the item's job in the shared prefix).
+__global__ void __launch_bounds__(1024) k_plan_partition_items(const uint32_t* __restrict__ coff,
+                                                               const uint32_t* __restrict__ soff,
+                                                               const uint32_t* __restrict__ n_comp, uint32_t P,
+                                                               uint64_t lo, uint64_t hi, uint32_t tile,
+                                                               uint32_t chunk, uint32_t max_chunks, uint32_t cap,
+                                                               Item* __restrict__ items, uint32_t* n_items) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ Job s_job[1024];
+    __shared__ uint32_t s_pre[1025], s_nt[1024], s_ch[1024];
+    const uint32_t p = threadIdx.x;
+    uint32_t cnt = 0;
+    if (p < P) {
+        uint64_t rb, re;
+        if (soff) {
+            rb = soff[p];
+            re = soff[p + 1];
+        } else {
+            rb = 0;
+            re = *n_comp;
+        }
+        const uint64_t len = re - rb;
+        const Job jb{coff[p], coff[p + 1], (uint32_t)(rb + min(lo, len)), (uint32_t)(rb + min(hi, len))};
+        uint32_t nt, nc, ch;
+        job_shape(jb, tile, chunk, max_chunks, &nt, &nc, &ch);
+        s_job[p] = jb;
+        s_nt[p] = nt;
+        s_ch[p] = ch;
+        cnt = nt * nc;
+    }
+    uint32_t pre, total;
+    Scan(tmp).ExclusiveSum(cnt, pre, total);
+    s_pre[p] = pre;
+    if (p == 0) s_pre[1024] = total;
+    __syncthreads();
+    const uint32_t nout = min(total, cap);
+    for (uint32_t x = threadIdx.x; x < nout; x += blockDim.x) {
+        // job of item x: last j with s_pre[j] <= x (jobs with no items share a prefix)
+        uint32_t a = 0, b = min(P, 1024u);
+        while (b - a > 1) {
+            const uint32_t m = (a + b) >> 1;
+            if (s_pre[m] <= x) a = m; else b = m;
+        }
+        const Job jb = s_job[a];
+        const uint32_t nt = s_nt[a], ch = s_ch[a], r = x - s_pre[a];
+        const uint32_t g = r / nt, t = r - g * nt;
+        const uint32_t cb = jb.cb + t * tile, l = jb.lo + g * ch;
+        items[x] = Item{cb, min(cb + tile, jb.ce), l, min(l + ch, jb.hi)};
+    }
+    if (threadIdx.x == 0) *n_items = nout;
+}
+
+bool launch_plan_partition_items(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
+                                 uint64_t lo, uint64_t hi, uint32_t tile, uint32_t chunk, uint32_t max_chunks,
+                                 uint32_t cap, Item* items, uint32_t* n_items, cudaStream_t st) {
+    if (P == 0 || P > 1024) return false;
+    k_plan_partition_items<<<1, 1024, 0, st>>>(coff, soff, n_comp, P, lo, hi, tile, chunk, max_chunks, cap, items,
+                                               n_items);
+    SKY_LAUNCH_CHECK();
+    return true;
+}
+
+// Dense list of the live entries of dead[0, n) (base + i, ascending) and the
+// segment offsets mapped onto it (off_new[p] = live entries before off[p]),
+// in two launches (instead of scan init + scan + remap + compaction): per-
+// block live counts, then each block takes the prefix of the blocks before
+// it, scans its 8-entry-per-thread spans and writes positions and the
+// offsets that fall in its range.
+constexpr uint32_t kDcPer = 8, kDcThreads = 256, kDcTile = kDcPer * kDcThreads;
+
+__global__ void __launch_bounds__(kDcThreads) k_dc_count(const uint8_t* __restrict__ dead, uint32_t n,
+                                                         uint32_t* __restrict__ block_tot) {
+    const uint32_t i0 = blockIdx.x * kDcTile + threadIdx.x * kDcPer;
+    uint32_t c = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kDcPer; ++u) c += (i0 + u < n && !dead[i0 + u]) ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ uint32_t s[kDcThreads / 32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t k = 0; k < kDcThreads / 32; ++k) t += s[k];
+        block_tot[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kDcThreads) k_dc_emit(const uint8_t* __restrict__ dead, uint32_t n,
+                                                        const uint32_t* __restrict__ block_tot,
+                                                        const uint32_t* __restrict__ off, uint32_t P, uint32_t base,
+                                                        uint32_t* __restrict__ dense, uint32_t* __restrict__ off_new,
+                                                        uint32_t* total_out) {
+    using Scan = cub::BlockScan<uint32_t, kDcThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_w[kDcThreads / 32];
+    // prefix of the blocks before this one (and the grand total for the last)
+    uint32_t pb = 0;
+    for (uint32_t k = threadIdx.x; k < blockIdx.x; k += kDcThreads) pb += block_tot[k];
+    pb = __reduce_add_sync(0xffffffffu, pb);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = pb;
+    __syncthreads();
+    uint32_t bpre = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kDcThreads / 32; ++k) bpre += s_w[k];
+    const uint32_t i0 = blockIdx.x * kDcTile + threadIdx.x * kDcPer;
+    uint32_t live = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kDcPer; ++u)
+        if (i0 + u < n && !dead[i0 + u]) live |= 1u << u;
+    uint32_t pre;
+    Scan(tmp).ExclusiveSum((uint32_t)__popc(live), pre);
+    pre += bpre;
+    uint32_t o = pre;
+#pragma unroll
+    for (uint32_t u = 0; u < kDcPer; ++u)
+        if ((live >> u) & 1u) dense[o++] = base + i0 + u;
+    // offsets inside this thread's span [i0, i0 + kDcPer); off[] is sorted.
+    // The last thread of the grid also takes every offset at or past n.
+    const bool last = blockIdx.x == gridDim.x - 1 && threadIdx.x == kDcThreads - 1;
+    const uint32_t lo_i = last ? min(i0, n) : i0, hi_i = last ? 0xFFFFFFFFu : i0 + kDcPer;
+    if (lo_i < n || last) {
+        uint32_t a = 0, c = P + 1;  // first p with off[p] >= lo_i
+        while (a < c) {
+            const uint32_t m = (a + c) >> 1;
+            if (off[m] < lo_i) a = m + 1; else c = m;
+        }
+        for (uint32_t p = a; p <= P && off[p] < hi_i; ++p) {
+            const uint32_t at = off[p];
+            off_new[p] = at >= n ? pre + __popc(live) : pre + __popc(live & ((1u << (at - i0)) - 1u));
+        }
+    }
+    if (last && total_out) *total_out = pre + __popc(live);
+}
+
+bool launch_dense_compact(const uint8_t* dead, uint32_t n, const uint32_t* off, uint32_t P, uint32_t base,
+                          uint32_t* dense, uint32_t* off_new, uint32_t* total, uint32_t* block_tot,
+                          cudaStream_t st) {
+    if (n == 0 || n > (64u << 20)) return false;
+    const uint32_t blocks = ceil_div(n, kDcTile);
+    k_dc_count<<<blocks, kDcThreads, 0, st>>>(dead, n, block_tot);
+    SKY_LAUNCH_CHECK();
+    k_dc_emit<<<blocks, kDcThreads, 0, st>>>(dead, n, block_tot, off, P, base, dense, off_new, total);
+    SKY_LAUNCH_CHECK();
+    return true;
+}
+
+size_t dense_compact_scratch(uint32_t n) { return (size_t)ceil_div(n, kDcTile) * sizeof(uint32_t) + 16; }
+
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st) {
     if (!a.n_items) return;
     if (tile <= 1 * 32) {
