@@ -98,6 +98,12 @@ enum Slot {
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
 
+// tuning knob from the environment (experiments), else the default
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? (uint32_t)std::strtoul(v, nullptr, 10) : dflt;
+}
+
 constexpr int kTile = 512;          // candidates per relsky item (RS_THREADS * RS_K)
 constexpr uint32_t kChunk = 8192;   // comparators per relsky item before bounding
 constexpr uint32_t kBlock = 512;    // local block-skyline size
@@ -566,7 +572,7 @@ class Runner {
         // grain from the capacity: ~ rows per partition
         const uint64_t per = (uint64_t)cap / std::max<uint32_t>(1, P);
         const uint32_t tile = per >= 2048 ? 256 : (per >= 512 ? 128 : 64);
-        const uint32_t chunk = 2048, max_chunks = 64, head = 2048;
+        const uint32_t chunk = env_u32("SKY_SFS_CHUNK", 2048), max_chunks = 64, head = env_u32("SKY_SFS_HEAD", 2048);
         const uint64_t icap = ((uint64_t)cap / tile + P) * max_chunks;
         uint32_t* np_dev = misc + M_NP;
         uint32_t* hp = stage<uint32_t>(1);
@@ -1920,7 +1926,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         ma.cxyz = US.xyz; ma.cskey = US.skey; ma.cid = US.id;
         const std::vector<uint32_t> offg = {0, U.n};
         R.relsky_waves(D, offg, 0, 1, [&](uint32_t, std::vector<uint2>& c) { c.assign(1, make_uint2(0, U.n)); },
-                       ma, US.qc, US.qc, mp.tile, mp.chunk, 4096);
+                       ma, US.qc, US.qc, mp.tile, mp.chunk, env_u32("SKY_MERGE_HEAD", 4096));
     } else if (P > 1) {
         const uint2* sq = all_mode ? US.qc : U.qc;
         auto comps_of = [&](uint32_t i, std::vector<uint2>& c) {
@@ -1933,7 +1939,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             // wave A: the nearest slice / cell (or the strongest keys of the
             // union), wave B: the rest over dense tiles of survivors
             std::vector<uint2> c0;
-            uint32_t head = 4096;
+            uint32_t head = env_u32("SKY_MERGE_HEAD", 4096);
             if (!all_mode)
                 for (uint32_t i = qb; i < qe; ++i) {
                     comps_of(i, c0);
