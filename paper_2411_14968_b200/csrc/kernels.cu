@@ -137,10 +137,11 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
             if (a.normalized && v > 1.0) err |= kErrAboveOne;
             sum = __dadd_rn(sum, v);
         }
-        // hyperspherical_angles: tail sums of squares back to front.
+        // hyperspherical_angles: tail sums of squares back to front; the
+        // partition index sum_i slice_i * m^i (angular_index) by Horner's rule
+        // over i = d-2 .. 0 (m^(d-1) <= 2^22: 32-bit arithmetic, no division)
         const double PI = 3.14159265358979323846;
-        uint64_t stride_i = 1;
-        for (int k = 0; k + 1 < d; ++k) stride_i *= a.m;  // divided before each use: m^i for slice i
+        const uint32_t m32 = (uint32_t)a.m;
         // FP32 pass first: its slice value is within ~1e-6 relative of the
         // FP64 one, so a value clear of every interior boundary gives the
         // same floor; rows that come near one redo the FP64 computation.
@@ -148,7 +149,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         {
             const float fm = (float)a.m, tol = 1e-4f * fmaxf(1.0f, fm / 16.0f);
             float tail32 = 0.0f;
-            uint64_t pid32 = 0, st = stride_i;
+            uint32_t pid32 = 0;
             // squares must stay normal floats for that error bound
 #pragma unroll U
             for (int j = 0; j < DMAX; ++j) {
@@ -168,16 +169,15 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                 tail32 += xi * xi;
                 const float r = rintf(v);
                 if (r >= 1.0f && r <= fm - 1.0f && fabsf(v - r) <= tol) exact64 = true;
-                uint64_t slice = (uint64_t)fmaxf(v, 0.0f);
-                if (slice >= a.m) slice = a.m - 1;
-                st /= a.m;
-                pid32 += slice * (st ? st : 1);
+                uint32_t slice = (uint32_t)fmaxf(v, 0.0f);
+                if (slice >= m32) slice = m32 - 1;
+                pid32 = pid32 * m32 + slice;
             }
             pid = pid32;
         }
         bool ambiguous = false;
         if (exact64) {
-            pid = 0;
+            uint32_t pid64 = 0;
             double tail = 0.0;
 #pragma unroll U
             for (int ii = DMAX - 1; ii >= 0; --ii) {
@@ -190,16 +190,16 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                 const double phi = atan2(sqrt(tail), xi);
                 tail = __dadd_rn(tail, __dmul_rn(xi, xi));
                 const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
-                uint64_t slice = (uint64_t)v;
-                if (slice >= a.m) slice = a.m - 1;
+                uint32_t slice = (uint32_t)v;
+                if (slice >= m32) slice = m32 - 1;
                 // CUDA's atan2 may differ from the host libm by an ulp or two; a
                 // value this close to an interior slice boundary is resolved on
                 // the host with the reference's own formula.
                 const double r = rint(v);
                 if (r >= 1.0 && r <= (double)(a.m - 1) && fabs(v - r) <= 1e-9 * fmax(1.0, v)) ambiguous = true;
-                stride_i /= a.m;
-                pid += slice * (stride_i ? stride_i : 1);
+                pid64 = pid64 * m32 + slice;
             }
+            pid = pid64;
         }
         if (ambiguous) {
             const uint32_t k = atomicAdd(a.amb_count, 1u);
@@ -314,8 +314,6 @@ void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
 }
 
 
-// The angular stride loop above walks i = d-2 .. 0 with stride m^i.
-// (stride_i starts at m^(d-1) and is divided before use.)
 
 __global__ void k_seg_offsets(const uint64_t* __restrict__ key64, uint32_t n, uint32_t P, uint32_t* off) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
