@@ -132,10 +132,18 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) break;
-            const double v = R.X(j);
-            if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
-            if (a.normalized && v > 1.0) err |= kErrAboveOne;
-            sum = __dadd_rn(sum, v);
+            if (Row::kF32) {
+                // float rows: the same answers as on the exact upcast
+                const float v = R.f(j);
+                if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
+                if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+                sum = __dadd_rn(sum, (double)v);
+            } else {
+                const double v = R.X(j);
+                if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
+                if (a.normalized && v > 1.0) err |= kErrAboveOne;
+                sum = __dadd_rn(sum, v);
+            }
         }
         // hyperspherical_angles: tail sums of squares back to front; the
         // partition index sum_i slice_i * m^i (angular_index) by Horner's rule
@@ -148,6 +156,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         bool exact64 = false;
         {
             const float fm = (float)a.m, tol = 1e-4f * fmaxf(1.0f, fm / 16.0f);
+            const float scale = 2.0f / 3.14159265f * fm;  // a filter value: exactness comes from the FP64 redo
             float tail32 = 0.0f;
             uint32_t pid32 = 0;
             // squares must stay normal floats for that error bound
@@ -165,7 +174,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                     tail32 = xi * xi;
                     continue;
                 }
-                const float v = 2.0f * atan2f(sqrtf(tail32), xi) / 3.14159265f * fm;
+                const float v = atan2f(sqrtf(tail32), xi) * scale;
                 tail32 += xi * xi;
                 const float r = rintf(v);
                 if (r >= 1.0f && r <= fm - 1.0f && fabsf(v - r) <= tol) exact64 = true;
@@ -210,10 +219,17 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) break;
-            const double v = R.X(j);
-            if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
-            if (a.normalized && v > 1.0) err |= kErrAboveOne;
-            sum = __dadd_rn(sum, v);
+            if (Row::kF32) {
+                const float v = R.f(j);
+                if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
+                if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+                sum = __dadd_rn(sum, (double)v);
+            } else {
+                const double v = R.X(j);
+                if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
+                if (a.normalized && v > 1.0) err |= kErrAboveOne;
+                sum = __dadd_rn(sum, v);
+            }
             if ((uint32_t)j == a.slice_dim) sv = R.f(j);
         }
         if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
