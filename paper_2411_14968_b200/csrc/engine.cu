@@ -1223,6 +1223,14 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
         pa.gmin = gmin;
         pa.P = (uint32_t)P;
     }
+    if (strategy == SKY_ANGULAR && m >= 2 && m <= 8) {
+        // slice boundaries k*pi/(2m) as tan^2 (k = 1..m-1) for the FP32 filter
+        const double PI = 3.14159265358979323846;
+        for (uint64_t k = 1; k < m; ++k) {
+            const double t = std::tan((double)k * PI / (2.0 * (double)m));
+            pa.tan2[k - 1] = (float)(t * t);
+        }
+    }
     R.hbm_begin();
     launch_prep(pa, st, R.c_->sm_count);
     // rows read once; key (8 B) written, row index (4 B) when sorting follows

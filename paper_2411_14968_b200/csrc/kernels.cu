@@ -174,12 +174,30 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                     tail32 = xi * xi;
                     continue;
                 }
-                const float v = atan2f(sqrtf(tail32), xi) * scale;
-                tail32 += xi * xi;
-                const float r = rintf(v);
-                if (r >= 1.0f && r <= fm - 1.0f && fabsf(v - r) <= tol) exact64 = true;
-                uint32_t slice = (uint32_t)fmaxf(v, 0.0f);
-                if (slice >= m32) slice = m32 - 1;
+                uint32_t slice;
+                if (m32 <= 8 && a.tan2[0] != 0.0f) {
+                    // phi_i = atan2(sqrt(tail), x_i) passes the boundary k*pi/(2m)
+                    // iff tail >= x_i^2 tan^2(k*pi/(2m)) (x_i >= 0, tan^2 increasing
+                    // on [0, pi/2)): no atan2 or sqrt. A row within 1e-3 (relative)
+                    // of a boundary redoes FP64 below; rounding here is ~1e-6.
+                    const float x2 = xi * xi;
+                    slice = 0;
+                    if (!(tail32 == 0.0f && !signbit(xi))) {  // atan2(+0, +0) = atan2(0, x > 0) = 0
+                        for (uint32_t k = 1; k < m32; ++k) {
+                            const float b = x2 * a.tan2[k - 1];
+                            slice += tail32 >= b ? 1u : 0u;
+                            if (fabsf(tail32 - b) <= 1e-3f * b) exact64 = true;
+                        }
+                    }
+                    tail32 += x2;
+                } else {
+                    const float v = atan2f(sqrtf(tail32), xi) * scale;
+                    tail32 += xi * xi;
+                    const float r = rintf(v);
+                    if (r >= 1.0f && r <= fm - 1.0f && fabsf(v - r) <= tol) exact64 = true;
+                    slice = (uint32_t)fmaxf(v, 0.0f);
+                    if (slice >= m32) slice = m32 - 1;
+                }
                 pid32 = pid32 * m32 + slice;
             }
             pid = pid32;

@@ -62,6 +62,9 @@ struct PrepArgs {
     uint32_t key_shift;      // low bits of skey cleared (the partition sort skips them)
     uint32_t* gmin = nullptr;  // out (optional, streamed prep): per-CTA minimum key of each partition
     uint32_t P = 0;
+    // angular, m <= 8: tan^2(k*pi/(2m)) for k = 1..m-1 (slice boundaries as
+    // tangent ratios); tan2[0] == 0 means "not set" (atan2 filter instead)
+    float tan2[8] = {};
 };
 // sm_count > 0: persistent streamed prep when the rows allow it (float,
 // aligned); required when a.gmin is set (grid = prep_stream_grid chunks)

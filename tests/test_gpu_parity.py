@@ -342,3 +342,24 @@ def test_stream_path_bucket_overflow(engine, monkeypatch):
             assert np.array_equal(r.skyline, exp["ids"]), (k, strat)
             check_metrics(r, exp, (k, strat))
             assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), (k, strat)
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 8])
+def test_angular_boundaries_vs_oracle(engine, m):
+    """Angular partition ids on lattice rows that sit exactly on slice
+    boundaries (x_i^2 == tail sums, zeros, -0.0): the tangent-ratio filter
+    (k_prep_stream) must defer every such row to the exact FP64 path."""
+    rng = np.random.default_rng(100 + m)
+    for d in (2, 3, 4, 6):
+        x = (rng.integers(0, 5, (3000, d)) / 4).astype(np.float32)
+        x[:50] = 0.0
+        x[50:100, 0] = -0.0
+        x[100:110] = 0.5
+        cfg = SkyConfig.make(strategy=2, p=m ** (d - 1), m=m, seed=1, filter=0, merge=1, workers=1)
+        exp = O.oracle_run(x, cfg, True)
+        r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+        assert np.array_equal(r.skyline, exp["ids"]), (m, d)
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), (m, d)
+        po, _ = engine.make_assignment(x, PartitionConfig(Strategy.Angular, p=m ** (d - 1), m=m))
+        epo, _ = O.oracle_assign(x, cfg, True)
+        assert np.array_equal(np.asarray(po), np.asarray(epo)), (m, d)
