@@ -1592,7 +1592,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     }
     // stream path: the prep pass also leaves each CTA's minimum key per
     // partition (the representative candidate bound)
-    const uint32_t prep_grid = prep_stream_grid(n, c->sm_count);
+    const uint32_t prep_grid = stream ? prep_stream_grid(n, d, P, c->sm_count) : 0;
     uint32_t* gmin = stream ? R.dev<uint32_t>(S_GMIN, (size_t)prep_grid * P) : nullptr;
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
                                       &out->angular_host_fixups, eager,

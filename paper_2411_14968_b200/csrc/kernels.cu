@@ -325,21 +325,29 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
     }
 }
 
-uint32_t prep_stream_grid(uint32_t n, int sm_count) {
-    return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows), 4u * (uint32_t)sm_count));
+// Persistent grid of the streamed prep: as many CTAs as fit on the SMs (the
+// per-tile work is a dependent chain; resident warps hide it), at most one
+// per tile. Deterministic for (n, d, P) on a device, so callers can size
+// per-CTA outputs (gmin) with it.
+uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count) {
+    const size_t smem = stream_smem_bytes(d) + (size_t)P * sizeof(uint32_t);
+    int per_sm = 4;
+    SKY_DISPATCH_D(padded_dim(d), {
+        if (smem > 48 * 1024)
+            SKY_CUDA(cudaFuncSetAttribute(k_prep_stream<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prep_stream<DT>, (int)kStreamRows, smem));
+    });
+    per_sm = std::max(1, std::min(per_sm, 8));
+    return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows), (uint32_t)per_sm * (uint32_t)sm_count));
 }
 
 void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
     if (a.n == 0) return;
     if (!a.pts64 && a.d <= 32 && ((uintptr_t)a.pts & 15) == 0 && sm_count > 0) {
         // float rows, 16-byte aligned: persistent CTAs, bulk-copied row tiles
-        const size_t smem = stream_smem_bytes(a.d) + (a.gmin ? (size_t)a.P * sizeof(uint32_t) : 0);
-        SKY_DISPATCH_D(padded_dim(a.d), {
-            if (smem > 48 * 1024)
-                SKY_CUDA(cudaFuncSetAttribute(k_prep_stream<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem));
-            k_prep_stream<DT><<<prep_stream_grid(a.n, sm_count), kStreamRows, smem, st>>>(a);
-        });
+        const size_t smem = stream_smem_bytes(a.d) + (size_t)a.P * sizeof(uint32_t);
+        const uint32_t grid = prep_stream_grid(a.n, a.d, a.P, sm_count);  // sets the smem attribute
+        SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT><<<grid, kStreamRows, smem, st>>>(a)));
     } else {
         if (a.gmin) throw Error(SKY_E_INTERNAL, "partition minima need the streamed prep");
         k_prep<<<ceil_div(a.n, 256), 256, 0, st>>>(a);
