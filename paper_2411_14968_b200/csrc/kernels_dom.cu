@@ -1372,29 +1372,32 @@ __global__ void __launch_bounds__(kDcThreads) k_dc_emit(const uint8_t* __restric
 #pragma unroll
     for (uint32_t u = 0; u < kDcPer; ++u)
         if (i0 + u < n && !dead[i0 + u]) live |= 1u << u;
-    uint32_t pre;
-    Scan(tmp).ExclusiveSum((uint32_t)__popc(live), pre);
+    uint32_t pre, agg;
+    Scan(tmp).ExclusiveSum((uint32_t)__popc(live), pre, agg);
     pre += bpre;
     uint32_t o = pre;
 #pragma unroll
     for (uint32_t u = 0; u < kDcPer; ++u)
         if ((live >> u) & 1u) dense[o++] = base + i0 + u;
-    // offsets inside this thread's span [i0, i0 + kDcPer); off[] is sorted.
-    // The last thread of the grid also takes every offset at or past n.
-    const bool last = blockIdx.x == gridDim.x - 1 && threadIdx.x == kDcThreads - 1;
-    const uint32_t lo_i = last ? min(i0, n) : i0, hi_i = last ? 0xFFFFFFFFu : i0 + kDcPer;
-    if (lo_i < n || last) {
-        uint32_t a = 0, c = P + 1;  // first p with off[p] >= lo_i
+    // offsets inside this thread's span [i0, min(i0 + kDcPer, n)); off[] is
+    // sorted. Offsets at or past n (empty tail segments) get the total from
+    // the last block, one per thread.
+    if (i0 < n) {
+        const uint32_t hi_i = min(i0 + kDcPer, n);
+        uint32_t a = 0, c = P + 1;  // first p with off[p] >= i0
         while (a < c) {
             const uint32_t m = (a + c) >> 1;
-            if (off[m] < lo_i) a = m + 1; else c = m;
+            if (off[m] < i0) a = m + 1; else c = m;
         }
-        for (uint32_t p = a; p <= P && off[p] < hi_i; ++p) {
-            const uint32_t at = off[p];
-            off_new[p] = at >= n ? pre + __popc(live) : pre + __popc(live & ((1u << (at - i0)) - 1u));
-        }
+        for (uint32_t p = a; p <= P && off[p] < hi_i; ++p)
+            off_new[p] = pre + __popc(live & ((1u << (off[p] - i0)) - 1u));
     }
-    if (last && total_out) *total_out = pre + __popc(live);
+    if (blockIdx.x == gridDim.x - 1) {
+        const uint32_t total = bpre + agg;
+        for (uint32_t p = threadIdx.x; p <= P; p += kDcThreads)
+            if (off[p] >= n) off_new[p] = total;
+        if (threadIdx.x == 0 && total_out) *total_out = total;
+    }
 }
 
 bool launch_dense_compact(const uint8_t* dead, uint32_t n, const uint32_t* off, uint32_t P, uint32_t base,
