@@ -746,6 +746,8 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
 // share a partition and have neighbouring keys, so they finish together) and
 // writes dead_pos[i]; otherwise thread i takes row i (coalesced stream) and
 // writes dead_row[i].
+constexpr uint32_t kAppendSmemReps = 256;
+
 // APPEND (row order): instead of flags, the surviving rows are appended to
 // app.out as ((key64 >> key_shift) << row_bits | row), count in *app.count —
 // the survivors' (partition, key, row) sort key; the CTA's rows are staged
@@ -767,18 +769,36 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     // packed codes pay off from 32 representatives on (the count may only be
     // known on the device)
     const bool use_codes = CODES && nrep >= 32;
-    const uint32_t npad = (nrep_max + 7) & ~7u;
-    extern __shared__ float4 s_rep[];
-    uint2* s_code = reinterpret_cast<uint2*>(s_rep + (size_t)npad * V);
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_code + npad);
-    float* s_thr = reinterpret_cast<float*>(s_key + npad);
-    for (uint32_t i = threadIdx.x; i < nrep * V; i += blockDim.x) s_rep[i] = rep_xyz[i];
-    for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) {
-        // padding codes never pass the coarse test (bit 31 of word 1 borrows)
-        if (CODES) s_code[i] = i < nrep ? rep_qc[i] : make_uint2(0u, 0x80000000u);
-        // APPEND compares truncated keys (the rows' keys come from key64)
-        s_key[i] = i < nrep ? (APPEND ? rep_key[i] & ~((1u << app.key_shift) - 1u) : rep_key[i]) : 0xFFFFFFFFu;
+    // APPEND reserves shared memory for kAppendSmemReps representatives only
+    // (the count is known on the device alone; a smaller reservation keeps
+    // more CTAs resident for the row stream); more than that are read from
+    // global memory (L1-cached broadcasts), guarded by their count.
+    const uint32_t ncap = APPEND ? min(nrep_max, kAppendSmemReps) : nrep_max;
+    const uint32_t npad = (ncap + 7) & ~7u;
+    const bool greps = APPEND && nrep > ncap;
+    extern __shared__ float4 s_rep_smem[];
+    uint2* s_code_smem = reinterpret_cast<uint2*>(s_rep_smem + (size_t)npad * V);
+    uint32_t* s_key_smem = reinterpret_cast<uint32_t*>(s_code_smem + npad);
+    float* s_thr = reinterpret_cast<float*>(s_key_smem + npad);
+    const float4* s_rep = greps ? rep_xyz : s_rep_smem;
+    const uint32_t kmask = APPEND ? ~((1u << app.key_shift) - 1u) : 0xFFFFFFFFu;
+    if (!greps) {
+        for (uint32_t i = threadIdx.x; i < nrep * V; i += blockDim.x) s_rep_smem[i] = rep_xyz[i];
+        for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) {
+            // padding codes never pass the coarse test (bit 31 of word 1 borrows)
+            if (CODES) s_code_smem[i] = i < nrep ? rep_qc[i] : make_uint2(0u, 0x80000000u);
+            // APPEND compares truncated keys (the rows' keys come from key64)
+            s_key_smem[i] = i < nrep ? rep_key[i] & kmask : 0xFFFFFFFFu;
+        }
     }
+    auto key_at = [&](uint32_t r) -> uint32_t {
+        if (!greps) return s_key_smem[r];
+        return r < nrep ? __ldg(rep_key + r) & kmask : 0xFFFFFFFFu;
+    };
+    auto code_at = [&](uint32_t r) -> uint2 {
+        if (!greps) return s_code_smem[r];
+        return r < nrep ? __ldg(rep_qc + r) : make_uint2(0u, 0x80000000u);
+    };
     if (CODES)
         for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
     // APPEND: the row tiles stream through shared memory after the tables
@@ -841,14 +861,19 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         // exact FP32 re-check only on a coarse pass; one vote per step
         uint32_t Tl[2] = {T0, T1};
         for (uint32_t r = 0; r < nrep && __any_sync(0xffffffffu, alive); r += 8) {
-            if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
-            const uint4* q4 = reinterpret_cast<const uint4*>(s_code + r);
+            if (key_at(r) > bound) break;  // warp-uniform: reps sorted by key
             uint2 q[8];
+            if (!greps) {
+                const uint4* q4 = reinterpret_cast<const uint4*>(s_code_smem + r);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint4 w = q4[k];
-                q[2 * k] = make_uint2(w.x, w.y);
-                q[2 * k + 1] = make_uint2(w.z, w.w);
+                for (int k = 0; k < 4; ++k) {
+                    const uint4 w = q4[k];
+                    q[2 * k] = make_uint2(w.x, w.y);
+                    q[2 * k + 1] = make_uint2(w.z, w.w);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) q[k] = code_at(r + k);
             }
             uint32_t h[8];
 #pragma unroll
@@ -873,14 +898,15 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     } else if (__any_sync(0xffffffffu, alive)) {
         uint32_t r = 0;
         for (; r < nrep; ++r) {
-            if (s_key[r] > bound) break;  // warp-uniform: reps sorted by key
+            const uint32_t kr = key_at(r);
+            if (kr > bound) break;  // warp-uniform: reps sorted by key
             bool maybe = alive;
             if (use_codes) {
-                const uint2 q = s_code[r];
+                const uint2 q = code_at(r);
                 constexpr uint32_t GA = G | 0x80000000u;
                 maybe = ((T0 - q.x) & (T1 - q.y) & GA) == GA;
             }
-            if (maybe && s_key[r] <= tk && dom_f4x<D>(s_rep + r * V, t, x64, x64.x ? rep_id[r] : 0, row)) {
+            if (maybe && kr <= tk && dom_f4x<D>(s_rep + r * V, t, x64, x64.x ? rep_id[r] : 0, row)) {
                 alive = false;
                 nt += r + 1;
                 T0 &= ~CodeLayout<D>::ALIVE;
@@ -1062,7 +1088,7 @@ bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, co
                              unsigned long long* tests, int smem_optin, cudaStream_t st) {
     if (D > 16 || ((uintptr_t)pts & 15)) return false;
     const bool codes = rep_qc && thr && nrep >= 32;
-    const size_t npad = (nrep + 7) & ~7u;
+    const size_t npad = (std::min(nrep, kAppendSmemReps) + 7) & ~7u;
     const size_t smem = npad * ((D + 3) / 4) * 16 + npad * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64 +
                         stream_smem_bytes(d, true) + 16;
     if (smem + 1024 > (size_t)smem_optin) return false;
