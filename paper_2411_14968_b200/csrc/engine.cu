@@ -1685,7 +1685,9 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         if (reps.n >= 32 && D <= 16 && reps.qc) {
             // one quantization for rows and representatives: quantiles of the input
             pthr = R.dev<float>(S_PTHR, (size_t)D * (kCodeLevels - 1));
-            launch_thresholds_rows(D, pts, d, n, pthr, st);
+            // codes pay off from 32 representatives on: the prefilter decides
+            // on the device count, so the thresholds are skipped below it
+            launch_thresholds_rows(D, pts, d, n, pthr, st, nrep_dev, 32);
             launch_encode(D, reps, pthr, st, nrep_dev);
             R.count(2);
         }

@@ -183,7 +183,9 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                     const float x2 = xi * xi;
                     slice = 0;
                     if (!(tail32 == 0.0f && !signbit(xi))) {  // atan2(+0, +0) = atan2(0, x > 0) = 0
-                        for (uint32_t k = 1; k < m32; ++k) {
+#pragma unroll
+                        for (uint32_t k = 1; k < 8; ++k) {  // static indices: no local copy of the args
+                            if (k >= m32) break;
                             const float b = x2 * a.tan2[k - 1];
                             slice += tail32 >= b ? 1u : 0u;
                             if (fabsf(tail32 - b) <= 1e-3f * b) exact64 = true;

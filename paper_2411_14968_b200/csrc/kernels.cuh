@@ -308,7 +308,9 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
                       const uint32_t* nrep_dev, const float* thr, uint8_t* dead_row, uint8_t* dead_pos,
                       unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st, bool posorder = true);
 // Quantization thresholds from a strided sample of row-major input rows.
-void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st);
+// gate (optional): the kernel returns at once when *gate < gate_min
+void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st,
+                            const uint32_t* gate = nullptr, uint32_t gate_min = 0);
 // Skyline of one small set in one CTA (false: too big, use k_relsky).
 bool launch_small_skyline(int D, const float* xyz, const uint32_t* id, uint32_t n, uint8_t* dead,
                           unsigned long long* tests, X64 x64, int smem_optin, cudaStream_t st);

@@ -74,7 +74,10 @@ __device__ __forceinline__ uint32_t quant_code(const float* tj, float x) {
 constexpr int kThrThreads = 512, kThrItems = 4;
 template <int D>
 __global__ void __launch_bounds__(kThrThreads) k_thresholds(const float* __restrict__ src, uint32_t stride, uint32_t ncols,
-                                                           uint32_t n_host, float* thr, const uint32_t* n_dev) {
+                                                           uint32_t n_host, float* thr, const uint32_t* n_dev,
+                                                           const uint32_t* gate = nullptr, uint32_t gate_min = 0) {
+    // gate: skip when a device count says the thresholds will not be used
+    if (gate && *gate < gate_min) return;
     constexpr int SMP = kThrThreads * kThrItems;
     using Sort = cub::BlockRadixSort<float, kThrThreads, kThrItems>;
     __shared__ typename Sort::TempStorage tmp;
@@ -1136,9 +1139,10 @@ void launch_thresholds(int D, const DevSet& s, float* thr, cudaStream_t st, cons
     SKY_LAUNCH_CHECK();
 }
 
-void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st) {
+void launch_thresholds_rows(int D, const float* pts, uint32_t d, uint32_t n, float* thr, cudaStream_t st,
+                            const uint32_t* gate, uint32_t gate_min) {
     if (!n) return;
-    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(pts, d, d, n, thr, nullptr)));
+    SKY_DISPATCH_D16(D, (k_thresholds<DT><<<DT, kThrThreads, 0, st>>>(pts, d, d, n, thr, nullptr, gate, gate_min)));
     SKY_LAUNCH_CHECK();
 }
 

@@ -363,3 +363,18 @@ def test_angular_boundaries_vs_oracle(engine, m):
         po, _ = engine.make_assignment(x, PartitionConfig(Strategy.Angular, p=m ** (d - 1), m=m))
         epo, _ = O.oracle_assign(x, cfg, True)
         assert np.array_equal(np.asarray(po), np.asarray(epo)), (m, d)
+
+
+def test_stream_path_many_representatives(engine, monkeypatch):
+    """Stream path with more representatives than its shared-memory
+    reservation (256): the prefilter reads the rest from global memory."""
+    monkeypatch.setenv("SKY_STREAM", "1")
+    for d, m, q in ((7, 2, 8), (5, 3, 6)):
+        x = generate(2, 60000, d, 5)
+        cfg = SkyConfig.make(strategy=2, p=m ** (d - 1), m=m, seed=3, filter=2, rep_q=q, merge=1, workers=1)
+        exp = O.oracle_run(x, cfg, True)
+        r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+        assert r.metrics.n_reps > 256, r.metrics.n_reps
+        assert np.array_equal(r.skyline, exp["ids"]), (d, m)
+        check_metrics(r, exp, (d, m))
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), (d, m)
