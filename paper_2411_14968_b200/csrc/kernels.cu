@@ -87,6 +87,22 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
     double sum = 0.0;
     uint32_t err = 0;
     uint64_t pid = 0;
+    // float rows: one range test per coordinate (NaN fails it); the error
+    // bits are worked out only for a row that fails (make_dataset,
+    // core.cpp:32-41; cell_of, partition.cpp:26-29)
+    auto f32_errors = [&](bool grid) {
+        uint32_t e = 0;
+#pragma unroll U
+        for (int j = 0; j < DMAX; ++j) {
+            if (j >= d) break;
+            const float v = R.f(j);
+            if (!(isfinite(v) && v >= 0.0f)) e |= kErrNonFinite;
+            if (a.normalized && v > 1.0f) e |= kErrAboveOne;
+            if (grid && !(v >= 0.0f && v <= 1.0f)) e |= kErrGridRange;
+        }
+        return e;
+    };
+    const float upper = a.normalized || a.strategy == SKY_GRID ? 1.0f : 3.402823466e38f;
     if (a.strategy == SKY_GRID && Row::kF32) {
         // float rows: the comparisons give the same answers in FP32 as on the
         // exact upcast; cell = floor(x * m) from the product rounded toward
@@ -95,19 +111,18 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         uint32_t stride = 1, pid32 = 0;
         const uint32_t m32 = (uint32_t)a.m;
         const float mf = (float)a.m;
+        bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) break;
             const float v = R.f(j);
-            if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
-            if (a.normalized && v > 1.0f) err |= kErrAboveOne;
-            if (!(v >= 0.0f && v <= 1.0f)) err |= kErrGridRange;
+            ok &= (v >= 0.0f) & (v <= 1.0f);
             sum = __dadd_rn(sum, (double)v);
-            uint32_t cell = __float2uint_rz(__fmul_rz(v, mf));
-            if (cell >= m32) cell = m32 - 1;
+            const uint32_t cell = min(__float2uint_rz(__fmul_rz(v, mf)), m32 - 1);
             pid32 += cell * stride;
             stride *= m32;
         }
+        if (!ok) err = f32_errors(true);
         pid = pid32;
     } else if (a.strategy == SKY_GRID) {
         // m^d <= kMaxPartitions (2^22): 32-bit cell arithmetic
@@ -129,14 +144,14 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
         pid = pid32;
     } else if (a.strategy == SKY_ANGULAR) {
+        bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) break;
             if (Row::kF32) {
                 // float rows: the same answers as on the exact upcast
                 const float v = R.f(j);
-                if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
-                if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+                ok &= (v >= 0.0f) & (v <= upper);
                 sum = __dadd_rn(sum, (double)v);
             } else {
                 const double v = R.X(j);
@@ -145,6 +160,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                 sum = __dadd_rn(sum, v);
             }
         }
+        if (Row::kF32 && !ok) err = f32_errors(false);
         // hyperspherical_angles: tail sums of squares back to front; the
         // partition index sum_i slice_i * m^i (angular_index) by Horner's rule
         // over i = d-2 .. 0 (m^(d-1) <= 2^22: 32-bit arithmetic, no division)
@@ -236,13 +252,13 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
     } else {
         float sv = 0.0f;
+        bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) break;
             if (Row::kF32) {
                 const float v = R.f(j);
-                if (!(isfinite(v) && v >= 0.0f)) err |= kErrNonFinite;
-                if (a.normalized && v > 1.0f) err |= kErrAboveOne;
+                ok &= (v >= 0.0f) & (v <= upper);
                 sum = __dadd_rn(sum, (double)v);
             } else {
                 const double v = R.X(j);
@@ -252,6 +268,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
             }
             if ((uint32_t)j == a.slice_dim) sv = R.f(j);
         }
+        if (Row::kF32 && !ok) err = f32_errors(false);
         if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
         if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(sv);
     }
