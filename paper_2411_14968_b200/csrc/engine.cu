@@ -571,7 +571,8 @@ class Runner {
         const uint32_t* n_items = nullptr;
         // grain from the capacity: ~ rows per partition
         const uint64_t per = (uint64_t)cap / std::max<uint32_t>(1, P);
-        const uint32_t tile = per >= 2048 ? 256 : (per >= 512 ? 128 : 64);
+        uint32_t tile = per >= 2048 ? 256 : (per >= 512 ? 128 : 64);
+        tile = env_u32("SKY_SFS_TILE", tile);
         const uint32_t chunk = env_u32("SKY_SFS_CHUNK", 2048), max_chunks = 64, head = env_u32("SKY_SFS_HEAD", 2048);
         const uint64_t icap = ((uint64_t)cap / tile + P) * max_chunks;
         uint32_t* np_dev = misc + M_NP;
@@ -879,7 +880,7 @@ class Runner {
         // ~4 items per resident CTA (8 warps share an item's comparators);
         // shrink the comparator chunk first (keeps 256-candidate tiles), the
         // candidate tile only when candidates are few
-        const uint64_t target = (uint64_t)c_->sm_count * 2 * 4;
+        const uint64_t target = (uint64_t)c_->sm_count * 2 * env_u32("SKY_GRAIN_ITEMS", 4);
         uint32_t t = 256, ch = 16384;
         while (ch > 2048 && n_cands && pairs / ((uint64_t)t * ch) < target) ch /= 2;
         while (t > 32 && n_cands && n_cands / t < (uint64_t)c_->sm_count * 2) t /= 2;
