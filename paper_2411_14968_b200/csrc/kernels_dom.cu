@@ -416,6 +416,12 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 // the next pass has consumed that many overflow tuples.
 constexpr int BNL2_B = 1024;
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
 template <int D>
 size_t bnl2_smem(uint32_t cap) {
     constexpr int V = Dims2<D>::V;
@@ -612,12 +618,16 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
                     }
                 };
                 uint32_t w = 0;
+                // shared-window addresses as 32-bit registers (the compiler
+                // otherwise re-derives the window base every step)
+                uint32_t a_code = smem_u32(w_code), a_key = smem_u32(w_key);
+                asm volatile("" : "+r"(a_code), "+r"(a_key));
                 for (; w + 4 <= wn; w += 4) {
                     // four entries per step: forward coarse misses fold with
                     // 3-input mins, the reverse test is gated by the keys
-                    const uint4 qa = *reinterpret_cast<const uint4*>(w_code + w);
-                    const uint4 qb = *reinterpret_cast<const uint4*>(w_code + w + 2);
-                    const uint4 kk = *reinterpret_cast<const uint4*>(w_key + w);
+                    const uint4 qa = lds128(a_code + w * 8);
+                    const uint4 qb = lds128(a_code + w * 8 + 16);
+                    const uint4 kk = lds128(a_key + w * 4);
                     const uint32_t f0 = ~((T0 - qa.x) & (T1 - qa.y)) & GA;
                     const uint32_t f1 = ~((T0 - qa.z) & (T1 - qa.w)) & GA;
                     const uint32_t f2 = ~((T0 - qb.x) & (T1 - qb.y)) & GA;
