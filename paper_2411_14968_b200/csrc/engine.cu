@@ -93,7 +93,7 @@ enum Slot {
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
     S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
-    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_DCBT, S_COUNT
+    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_DCBT, S_OFFG, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -612,6 +612,57 @@ class Runner {
         items = plan(dnew, head, ~0ull);
         relsky_direct(D, tile, a, s0.qc, s0.qc, dense, items, icap, n_items);
         return compact_dev(s0, dead, off0_dev, P, S_SET2, off_u_dev, n_u, D);
+    }
+
+    // Sky(U) on one GPU without a host round trip (random / angular NoSeq,
+    // sequential merge: u_i are antichains, so the merge is the skyline of
+    // the union). U (n = capacity, live count *n_u, key-sorted partition runs
+    // off_u[P+1]) is merged into key order (US, slot S_SET3), then two waves
+    // as in local_sfs_dev with all of US as one partition: every row against
+    // the strongest `head` rows, then the survivors against the rest. Items
+    // and the comparator chunk are planned on the device from *n_u. Dead
+    // flags of US (tail past *n_u set) go to *dead_out.
+    DevSet merge_all_dev(int D, const DevSet& U, const uint32_t* off_u, uint32_t P, const uint32_t* n_u,
+                         bool count_tests, uint8_t** dead_out) {
+        const uint32_t cap = U.n;
+        DevSet US = set(S_SET3, cap, D);
+        launch_merge_runs(D, U, off_u, P, US, st_, n_u);
+        uint8_t* dead = dev<uint8_t>(S_CELLDEAD, cap);
+        launch_fill_u8(dead, 0, cap, st_);
+        launch_fill_tail_u8(dead, 1, n_u, cap, st_);
+        count(3);
+        *dead_out = dead;
+        if (!cap) return US;
+        uint32_t* misc = dev<uint32_t>(S_MISC, 64);
+        uint32_t* offg = dev<uint32_t>(S_OFFG, 2);  // {0, *n_u}: the one "partition"
+        SKY_CUDA(cudaMemsetAsync(offg, 0, sizeof(uint32_t), st_));
+        SKY_CUDA(cudaMemcpyAsync(offg + 1, n_u, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st_));
+        RelskyArgs a{};
+        a.cxyz = US.xyz; a.cskey = US.skey; a.cid = US.id;
+        a.sxyz = US.xyz; a.sskey = US.skey; a.sid = US.id;
+        a.indirect = false; a.bounded = true; a.dead = dead;
+        a.tests = count_tests ? tests(2) : nullptr;
+        const uint32_t tile = env_u32("SKY_MERGE_TILE", cap <= 300000 ? 128u : 256u);
+        const uint32_t max_chunks = 64, head = env_u32("SKY_MERGE_HEAD", 4096);
+        const uint32_t target = (uint32_t)c_->sm_count * 2 * env_u32("SKY_GRAIN_ITEMS", 4);
+        const uint64_t icap = ((uint64_t)cap / tile + 2) * max_chunks;
+        const uint32_t icap32 = (uint32_t)std::min<uint64_t>(icap, 0xFFFFFFFFu);
+        Item* items = dev<Item>(S_ITEMS, icap);
+        uint32_t* ni = misc + M_NITEMS;
+        launch_plan_partition_items(offg, nullptr, n_u, 1, 0, head, tile, 0, max_chunks, icap32, items, ni, st_,
+                                    target);
+        count();
+        relsky_direct(D, tile, a, US.qc, US.qc, nullptr, items, icap, ni);
+        uint32_t* dnew = dev<uint32_t>(S_DNEW, 2);
+        uint32_t* dense = dev<uint32_t>(S_DENSE, cap);
+        launch_dense_compact(dead, cap, offg, 1, 0, dense, dnew, nullptr,
+                             dev<uint32_t>(S_DCBT, dense_compact_scratch(cap) / 4), st_);
+        count(2);
+        launch_plan_partition_items(dnew, nullptr, n_u, 1, head, ~0ull, tile, 0, max_chunks, icap32, items, ni, st_,
+                                    target);
+        count();
+        relsky_direct(D, tile, a, US.qc, US.qc, dense, items, icap, ni);
+        return US;
     }
 
     void relsky(int D, const Plan& plan, const RelskyArgs& base, const uint2* cq = nullptr,
@@ -1744,6 +1795,89 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     DevSet U;
     std::vector<uint32_t> pr(2, 0);
     pr[1] = P;
+    // all-pairs merge on one GPU (random / angular NoSeq, sequential merge):
+    // the stable merge of the union's runs into key order needs no host
+    // count, so it is queued before the union's round trip and runs while
+    // the host waits and plans (count and offsets stay on the device)
+    const bool all_mode_merge = cfg->merge == SKY_MERGE_SEQUENTIAL || cfg->strategy == SKY_RANDOM ||
+                                cfg->strategy == SKY_ANGULAR;
+    bool us_early = false;
+    // one GPU, all-pairs merge: the whole merge and the ids are queued before
+    // the only host round trip of the step (finish_dev_merge)
+    // Its kernels are sized by the union's capacity (the filtered set), so it
+    // is used where that is close to the union: representative filtering
+    // (without it the capacity is every row, e.g. config 1's 100k for a
+    // 1.4k union) and a filtered set large enough for the round trip to count
+    const bool dev_merge_cfg = W == 1 && all_mode_merge && P > 1 && D <= 16 &&
+                               cfg->filter == SKY_FILTER_REPRESENTATIVE &&
+                               std::getenv("SKY_HOST_MERGE") == nullptr;
+    auto dev_merge_ok = [&](uint32_t capacity) { return dev_merge_cfg && capacity >= 8192; };
+    auto finish_dev_merge = [&](const DevSet& Ucap, uint32_t ns_host) {
+        SKY_CUDA(cudaEventRecord(c->ev[2], st));
+        uint8_t* fdead = nullptr;
+        DevSet US = R.merge_all_dev(D, Ucap, offu_dev, P, misc + M_U, count_tests, &fdead);
+        SKY_CUDA(cudaEventRecord(c->ev[3], st));
+        // ascending ids written by the emit kernel straight into pinned host
+        // memory (mapped under UVA): no copy of a capacity-sized buffer
+        const uint32_t cap = Ucap.n;
+        uint32_t* hid = R.pin<uint32_t>(P_IDS, std::max<uint32_t>(cap, 1));
+        uint32_t* bm = R.dev<uint32_t>(S_BM, (size_t)n / 32 + 1);
+        uint32_t* bt = R.dev<uint32_t>(S_BMT, bm_blocks(n));
+        launch_ids_bitmap(US.id, fdead, cap, n, bm, bt, hid, misc + M_TOTAL, st);
+        R.count(cap ? 3 : 2);
+        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32 + 16);
+        uint32_t* hmisc = h + P + 1;
+        unsigned long long* ht = reinterpret_cast<unsigned long long*>(hmisc + 32);
+        SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(hmisc, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(ht, R.tests(0), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaMemcpyAsync(ht + 3, misc + M_HITS, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        SKY_CUDA(cudaEventRecord(c->ev[4], st));
+        R.sync();
+        check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
+        if (defer_rand && hmisc[M_RFLAG]) throw RedoEager{};
+        if (hmisc[M_OVF]) throw RedoEager{};
+        if (cfg->filter == SKY_FILTER_REPRESENTATIVE) out->n_reps = hmisc[M_NREP];
+        const uint32_t ns = stream ? ns_host : hmisc[M_S0];
+        out->filtered_count = (uint64_t)n - ns;
+        for (uint32_t p = 0; p < P; ++p) out->local_skyline_sizes[p] = h[p + 1] - h[p];
+        out->union_size = hmisc[M_U];
+        const uint32_t nf = hmisc[M_TOTAL];
+        out->d2h_bytes += (uint64_t)nf * sizeof(uint32_t);
+        out->ids = static_cast<int64_t*>(std::malloc((nf ? nf : 1) * sizeof(int64_t)));
+        for (uint32_t i = 0; i < nf; ++i) out->ids[i] = hid[i];
+        out->n_ids = out->final_size = nf;
+        out->tests_reps = ht[0];
+        out->tests_local = ht[1];
+        out->tests_merge = ht[2];
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+        out->partition_ms = ms;
+        cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+        out->local_ms = ms;
+        cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+        out->merge_ms = ms;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
+        out->total_ms = ms;
+        out->kernel_launches = c->launches;
+        out->dom_launches = c->dom_launches;
+        R.dom_collect();
+        out->stream_kernel_ms = R.hbm_collect();
+        out->stream_bytes = c->hbm_bytes;
+        out->stream_launches = c->hbm_used;
+        R.timeline_dump();
+        out->dom_kernel_ms = c->dom_ms;
+        out->dom_tests = ht[0] + ht[1] + ht[2];
+        out->dom_exact_checks = ht[3] + ht[4] + ht[5] + ht[6];
+        out->exact_checks_merge = ht[5];
+    };
+    auto early_merge = [&](const DevSet& Ucap) {
+        if (!(all_mode_merge && P > 1)) return;
+        DevSet USc = R.set(S_SET3, Ucap.n, D);  // capacity; the live count is misc[M_U]
+        launch_merge_runs(D, Ucap, offu_dev, P, USc, st, misc + M_U);
+        R.count();
+        us_early = true;
+    };
     if (W == 1 && stream) {
         // survivors of the stream prefilter: count (round trip), sort by
         // (partition, key, row), unpack into partition order
@@ -1773,6 +1907,11 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         } else {
             U = R.local_sfs_dev(D, s0, misc + M_S0, off1_dev, P, offu_dev, misc + M_U, count_tests);
         }
+        if (dev_merge_ok(U.n)) {
+            finish_dev_merge(U, ns);
+            return;
+        }
+        early_merge(U);
         uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32);
         SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -1813,6 +1952,11 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         } else {
             U = R.local_sfs_dev(D, s0, misc + M_S0, off1_dev, P, offu_dev, misc + M_U, count_tests);
         }
+        if (dev_merge_ok(U.n) && grid_filtered == 0) {
+            finish_dev_merge(U, 0);
+            return;
+        }
+        early_merge(U);
         uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32);
         SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         SKY_CUDA(cudaMemcpyAsync(h + P + 1, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -1923,9 +2067,11 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         // antichain, so testing against all of U is the same relation;
         // merge_sequential (engine.cpp:65-72) is Sky(U) by definition.
         // U's partitions are runs sorted by key: one stable P-way merge
-        US = R.set(S_SET3, U.n, D);
-        launch_merge_runs(D, U, offu_dev, P, US, st);
-        R.count();
+        US = R.set(S_SET3, U.n, D);  // the same buffers as the early merge's (grow-only arena)
+        if (!us_early) {
+            launch_merge_runs(D, U, offu_dev, P, US, st);
+            R.count();
+        }
         ma.sxyz = US.xyz; ma.sskey = US.skey; ma.sid = US.id;
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;

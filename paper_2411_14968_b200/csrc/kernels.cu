@@ -1432,11 +1432,11 @@ void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out
 // equal keys keep run order), the warp sums the ranks and copies the row.
 template <int D>
 __global__ void __launch_bounds__(256) k_merge_runs(DevSet in, const uint32_t* __restrict__ off, uint32_t P,
-                                                    uint32_t n, DevSet out) {
+                                                    uint32_t n, DevSet out, const uint32_t* n_dev) {
     constexpr int V = Dims<D>::V;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (i >= n) return;
+    if (i >= (n_dev ? min(*n_dev, n) : n)) return;
     // run of element i: the last p with off[p] <= i
     uint32_t lo = 0, hi = P;  // off[lo] <= i < off[hi]
     while (hi - lo > 1) {
@@ -1474,9 +1474,11 @@ __global__ void __launch_bounds__(256) k_merge_runs(DevSet in, const uint32_t* _
     }
 }
 
-void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st) {
+void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st,
+                       const uint32_t* n_dev) {
     if (!in.n) return;
-    SKY_DISPATCH_D(D, (k_merge_runs<DT><<<ceil_div((uint64_t)in.n * 32, 256), 256, 0, st>>>(in, off, P, in.n, out)));
+    SKY_DISPATCH_D(D, (k_merge_runs<DT><<<ceil_div((uint64_t)in.n * 32, 256), 256, 0, st>>>(in, off, P, in.n, out,
+                                                                                            n_dev)));
     SKY_LAUNCH_CHECK();
 }
 

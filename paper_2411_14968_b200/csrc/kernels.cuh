@@ -143,7 +143,9 @@ void launch_gather_rows(int D, const float* pts, const double* pts64, uint32_t d
                         DevSet out, cudaStream_t st);
 void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st);
 // stable merge of the key-sorted runs off[P+1] of `in` into `out` (key order)
-void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st);
+// (n_dev: live count on the device, in.n the capacity)
+void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st,
+                       const uint32_t* n_dev = nullptr);
 // ascending ids (< n_ids) of the live entries of id[n] via a bitmap; count in *total
 uint32_t bm_blocks(uint32_t n_ids);
 void launch_ids_bitmap(const uint32_t* id, const uint8_t* dead, uint32_t n, uint32_t n_ids, uint32_t* bm,
@@ -243,9 +245,11 @@ void launch_job_items(const Job* jobs, const uint32_t* n_jobs, uint32_t cap, con
 
 // jobs + counts + scan + items in one CTA (P <= 1024; false otherwise);
 // *n_items = min(items, cap)
+// chunk == 0: the chunk is derived on the device from the counts (>= grain_target items)
 bool launch_plan_partition_items(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
                                  uint64_t lo, uint64_t hi, uint32_t tile, uint32_t chunk, uint32_t max_chunks,
-                                 uint32_t cap, Item* items, uint32_t* n_items, cudaStream_t st);
+                                 uint32_t cap, Item* items, uint32_t* n_items, cudaStream_t st,
+                                 uint32_t grain_target = 0);
 // dense list of live entries + remapped segment offsets (off[P+1] sorted)
 // in two launches; block_tot: dense_compact_scratch(n) bytes. false: n == 0
 bool launch_dense_compact(const uint8_t* dead, uint32_t n, const uint32_t* off, uint32_t P, uint32_t base,

@@ -1308,12 +1308,28 @@ __global__ void __launch_bounds__(1024) k_plan_partition_items(const uint32_t* _
                                                                const uint32_t* __restrict__ n_comp, uint32_t P,
                                                                uint64_t lo, uint64_t hi, uint32_t tile,
                                                                uint32_t chunk, uint32_t max_chunks, uint32_t cap,
-                                                               Item* __restrict__ items, uint32_t* n_items) {
+                                                               Item* __restrict__ items, uint32_t* n_items,
+                                                               uint32_t grain_target) {
     using Scan = cub::BlockScan<uint32_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ Job s_job[1024];
     __shared__ uint32_t s_pre[1025], s_nt[1024], s_ch[1024];
+    __shared__ uint32_t s_chunk;
     const uint32_t p = threadIdx.x;
+    if (chunk == 0) {
+        // chunk from the device counts (Runner::pick_grain's rule): halve
+        // from 16384 while the launch would have fewer than grain_target items
+        if (p == 0) {
+            const uint64_t nc = coff[P] - coff[0];
+            const uint64_t ns = n_comp ? *n_comp : (uint64_t)(soff[P] - soff[0]);
+            const uint64_t pairs = nc * ns / 2;
+            uint32_t ch = 16384;
+            while (ch > 2048 && pairs / ((uint64_t)tile * ch) < grain_target) ch /= 2;
+            s_chunk = ch;
+        }
+        __syncthreads();
+        chunk = s_chunk;
+    }
     uint32_t cnt = 0;
     if (p < P) {
         uint64_t rb, re;
@@ -1357,10 +1373,10 @@ __global__ void __launch_bounds__(1024) k_plan_partition_items(const uint32_t* _
 
 bool launch_plan_partition_items(const uint32_t* coff, const uint32_t* soff, const uint32_t* n_comp, uint32_t P,
                                  uint64_t lo, uint64_t hi, uint32_t tile, uint32_t chunk, uint32_t max_chunks,
-                                 uint32_t cap, Item* items, uint32_t* n_items, cudaStream_t st) {
+                                 uint32_t cap, Item* items, uint32_t* n_items, cudaStream_t st, uint32_t grain_target) {
     if (P == 0 || P > 1024) return false;
     k_plan_partition_items<<<1, 1024, 0, st>>>(coff, soff, n_comp, P, lo, hi, tile, chunk, max_chunks, cap, items,
-                                               n_items);
+                                               n_items, grain_target);
     SKY_LAUNCH_CHECK();
     return true;
 }

@@ -378,3 +378,23 @@ def test_stream_path_many_representatives(engine, monkeypatch):
         assert np.array_equal(r.skyline, exp["ids"]), (d, m)
         check_metrics(r, exp, (d, m))
         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), (d, m)
+
+
+@pytest.mark.parametrize("host_merge", ["0", "1"])
+def test_device_merge_vs_oracle(engine, monkeypatch, host_merge):
+    """The all-pairs merge planned on the device with the ids written to
+    mapped host memory (one round trip per step) and the host-planned merge,
+    on inputs whose filtered set is large enough to take the device path."""
+    if host_merge == "1":
+        monkeypatch.setenv("SKY_HOST_MERGE", "1")
+    else:
+        monkeypatch.delenv("SKY_HOST_MERGE", raising=False)
+    for strat, p, merge, seed in ((2, 64, 1, 1), (0, 16, 1, 2), (0, 8, 0, 3)):
+        x = generate(2, 150000, 6, seed)
+        cfg = SkyConfig.make(strategy=strat, p=p, seed=seed, filter=2, rep_q=8, merge=merge, workers=1)
+        exp = O.oracle_run(x, cfg, True)
+        r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+        tag = (strat, p, merge, host_merge)
+        assert np.array_equal(r.skyline, exp["ids"]), tag
+        check_metrics(r, exp, tag)
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
