@@ -1531,7 +1531,14 @@ __global__ void __launch_bounds__(256) k_bm_emit(const uint32_t* __restrict__ bm
         if (total && blockIdx.x == gridDim.x - 1) *total = t + block_tot[blockIdx.x];
     }
     __syncthreads();
-    uint32_t base = s_base;
+    // a block's ids are staged in shared memory and written out coalesced
+    // when they fit (the output may be mapped host memory: full-line writes)
+    constexpr uint32_t kStage = 4096;
+    __shared__ uint32_t s_out[kStage];
+    const bool staged = block_tot[blockIdx.x] <= kStage;
+    const uint32_t gbase = s_base;
+    uint32_t base = staged ? 0u : gbase;
+    uint32_t* dst = staged ? s_out : out;
     const uint32_t b0 = blockIdx.x * kBmWords, b1 = min(words, b0 + kBmWords);
     for (uint32_t w0 = b0; w0 < b1; w0 += 256 * 8) {
         uint32_t v[8];
@@ -1565,10 +1572,14 @@ __global__ void __launch_bounds__(256) k_bm_emit(const uint32_t* __restrict__ bm
             while (m) {
                 const uint32_t bit = __ffs(m) - 1;
                 m &= m - 1;
-                out[o++] = ((wb + k) << 5) | bit;
+                dst[o++] = ((wb + k) << 5) | bit;
             }
         }
         base += all;
+    }
+    if (staged) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < base; i += blockDim.x) out[gbase + i] = s_out[i];
     }
 }
 
