@@ -869,44 +869,106 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     }
     bool alive = valid;
     const uint32_t bound = __reduce_max_sync(0xffffffffu, alive ? tk : 0u);
+    bool flags_done = false;
     if (use_codes) {
         // 8 representatives per step: 8 coarse tests folded by 3-input min,
         // exact FP32 re-check only on a coarse pass; one vote per step
-        uint32_t Tl[2] = {T0, T1};
-        for (uint32_t r = 0; r < nrep && __any_sync(0xffffffffu, alive); r += 8) {
-            if (key_at(r) > bound) break;  // warp-uniform: reps sorted by key
-            uint2 q[8];
-            if (!greps) {
-                const uint4* q4 = reinterpret_cast<const uint4*>(s_code_smem + r);
+        auto scan = [&](uint32_t r0, uint32_t r1, uint32_t bnd, uint32_t (&Tl)[2], const float4 (&tx)[V],
+                        uint32_t rowx, bool& al) {
+            for (uint32_t r = r0; r < r1 && __any_sync(0xffffffffu, al); r += 8) {
+                if (key_at(r) > bnd) break;  // warp-uniform: reps sorted by key
+                uint2 q[8];
+                if (!greps) {
+                    const uint4* q4 = reinterpret_cast<const uint4*>(s_code_smem + r);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint4 w = q4[k];
-                    q[2 * k] = make_uint2(w.x, w.y);
-                    q[2 * k + 1] = make_uint2(w.z, w.w);
+                    for (int k = 0; k < 4; ++k) {
+                        const uint4 w = q4[k];
+                        q[2 * k] = make_uint2(w.x, w.y);
+                        q[2 * k + 1] = make_uint2(w.z, w.w);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) q[k] = code_at(r + k);
                 }
-            } else {
+                uint32_t h[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) q[k] = code_at(r + k);
-            }
-            uint32_t h[8];
+                for (int k = 0; k < 8; ++k) h[k] = coarse_hit<G>(Tl, q[k]);
+                if (al) nt += min(8u, nrep - r);
+                constexpr uint32_t GA = G | 0x80000000u;
+                if (max_fold<8>(h) == GA) {
+                    // exact checks for the representatives whose codes passed
+                    uint32_t m = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) h[k] = coarse_hit<G>(Tl, q[k]);
-            if (alive) nt += min(8u, nrep - r);
-            constexpr uint32_t GA = G | 0x80000000u;
-            if (max_fold<8>(h) == GA) {
-                // exact checks for the representatives whose codes passed
-                uint32_t m = 0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) m |= (h[k] == GA ? 1u : 0u) << k;
-                while (m && alive) {
-                    const int k = __ffs(m) - 1;
-                    m &= m - 1;
-                    if (dom_f4x<D>(s_rep + (r + k) * V, t, x64, x64.x ? rep_id[r + k] : 0, row)) {
-                        alive = false;
-                        Tl[0] &= ~CodeLayout<D>::ALIVE;
+                    for (int k = 0; k < 8; ++k) m |= (h[k] == GA ? 1u : 0u) << k;
+                    while (m && al) {
+                        const int k = __ffs(m) - 1;
+                        m &= m - 1;
+                        if (dom_f4x<D>(s_rep + (r + k) * V, tx, x64, x64.x ? rep_id[r + k] : 0, rowx)) {
+                            al = false;
+                            Tl[0] &= ~CodeLayout<D>::ALIVE;
+                        }
                     }
                 }
             }
+        };
+        uint32_t Tl[2] = {T0, T1};
+        constexpr uint32_t K1 = 64;
+        if constexpr (POSORDER && !APPEND) {
+            if (nrep > K1) {
+                // The strongest K1 representatives kill most rows; the rows
+                // still alive are regrouped into dense warps for the rest, so
+                // a warp no longer runs the whole list for one survivor.
+                __shared__ float4 s_ct[256][V];
+                __shared__ uint32_t s_cm[256][5];
+                __shared__ uint32_t s_wc[8], s_nalive;
+                scan(0, K1, bound, Tl, t, row, alive);
+                if (valid && !alive) dead_row[slot] = 1;
+                const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                const uint32_t bal = __ballot_sync(0xffffffffu, alive);
+                if (lane == 0) s_wc[wid] = __popc(bal);
+                __syncthreads();
+                uint32_t pos = __popc(bal & ((1u << lane) - 1u)), tot = 0;
+                for (uint32_t w2 = 0; w2 < blockDim.x / 32; ++w2) {
+                    pos += w2 < wid ? s_wc[w2] : 0u;
+                    tot += s_wc[w2];
+                }
+                if (alive) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) s_ct[pos][v] = t[v];
+                    s_cm[pos][0] = Tl[0];
+                    s_cm[pos][1] = Tl[1];
+                    s_cm[pos][2] = tk;
+                    s_cm[pos][3] = slot;
+                    s_cm[pos][4] = row;
+                }
+                if (threadIdx.x == 0) s_nalive = tot;
+                __syncthreads();
+                const uint32_t na = s_nalive;
+                bool al2 = threadIdx.x < na;
+                uint32_t T2[2] = {G, G | 0x80000000u}, tk2 = 0, slot2 = 0, row2 = 0;
+                float4 t2[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) t2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (al2) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) t2[v] = s_ct[threadIdx.x][v];
+                    T2[0] = s_cm[threadIdx.x][0];
+                    T2[1] = s_cm[threadIdx.x][1];
+                    tk2 = s_cm[threadIdx.x][2];
+                    slot2 = s_cm[threadIdx.x][3];
+                    row2 = s_cm[threadIdx.x][4];
+                }
+                if (__any_sync(0xffffffffu, al2)) {
+                    const uint32_t bound2 = __reduce_max_sync(0xffffffffu, al2 ? tk2 : 0u);
+                    scan(K1, nrep, bound2, T2, t2, row2, al2);
+                }
+                if (threadIdx.x < na && !al2) dead_row[slot2] = 1;
+                flags_done = true;
+            } else {
+                scan(0, nrep, bound, Tl, t, row, alive);
+            }
+        } else {
+            scan(0, nrep, bound, Tl, t, row, alive);
         }
     } else if (__any_sync(0xffffffffu, alive)) {
         uint32_t r = 0;
@@ -942,7 +1004,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
             app.out[base + __popc(bal & ((1u << lane) - 1u))] =
                 ((app.key64[row] >> app.key_shift) << app.row_bits) | row;
     } else if (POSORDER) {
-        if (valid && !alive) dead_row[slot] = 1;
+        if (valid && !alive && !flags_done) dead_row[slot] = 1;
     } else if (valid) {
         dead_row[row] = alive ? 0 : 1;
     }
