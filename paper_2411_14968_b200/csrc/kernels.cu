@@ -8,10 +8,40 @@
 // all their candidates are dominated.
 #include <cub/cub.cuh>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "kernels.cuh"
 #include "stream.cuh"
 
 namespace sky {
+
+// Host-side caches for launch configuration queries (the dynamic shared
+// memory attribute and the occupancy of a kernel), so a run does not pay
+// for them on every launch.
+void ensure_smem_attr(const void* func, size_t smem) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> done;
+    if (smem <= 48 * 1024) return;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = done[func];
+    if (cur >= smem) return;
+    SKY_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+}
+int occupancy_cached(const void* func, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(func, threads, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int per_sm = 0;
+    SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem));
+    cache[key] = per_sm;
+    return per_sm;
+}
 
 int padded_dim(uint32_t d) {
     static const int widths[] = {2, 3, 4, 5, 6, 8, 10, 12, 16, 24, 32};
@@ -352,9 +382,8 @@ uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count) {
     const size_t smem = stream_smem_bytes(d) + (size_t)P * sizeof(uint32_t);
     int per_sm = 4;
     SKY_DISPATCH_D(padded_dim(d), {
-        if (smem > 48 * 1024)
-            SKY_CUDA(cudaFuncSetAttribute(k_prep_stream<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prep_stream<DT>, (int)kStreamRows, smem));
+        ensure_smem_attr((const void*)k_prep_stream<DT>, smem);
+        per_sm = occupancy_cached((const void*)k_prep_stream<DT>, (int)kStreamRows, smem);
     });
     per_sm = std::max(1, std::min(per_sm, 8));
     return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows), (uint32_t)per_sm * (uint32_t)sm_count));

@@ -7,7 +7,10 @@ namespace sky {
 
 // Internal dimensionality: d is padded with zero coordinates up to one of
 // the instantiated widths (zeros never change a dominance outcome).
-int padded_dim(uint32_t d);  // 0 if unsupported (d > 32)
+int padded_dim(uint32_t d);
+// cached cudaFuncSetAttribute(MaxDynamicSharedMemorySize) / occupancy query
+void ensure_smem_attr(const void* func, size_t smem);
+int occupancy_cached(const void* func, int threads, size_t smem);  // 0 if unsupported (d > 32)
 
 // Point set on the device in dominance-friendly layout: AoS coords with
 // stride round4(D) floats (16-byte aligned rows), plus the 32-bit sort key

@@ -1170,12 +1170,14 @@ bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, co
     if (!n) return true;
     // persistent CTAs: as many as fit, capped by the tile count
     auto go = [&](auto kern, const uint2* qc, const float* th) {
-        SKY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)kStreamRows, smem));
-        int dev = 0, sms = 148;
-        SKY_CUDA(cudaGetDevice(&dev));
-        SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        ensure_smem_attr((const void*)kern, smem);
+        const int per_sm = occupancy_cached((const void*)kern, (int)kStreamRows, smem);
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            SKY_CUDA(cudaGetDevice(&dev));
+            SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        }
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows),
                                                                        (uint32_t)std::max(1, per_sm) * sms));
         kern<<<grid, kStreamRows, smem, st>>>(pts, d, n, nullptr, reinterpret_cast<const float4*>(rep_xyz), rep_key,
