@@ -1095,7 +1095,7 @@ void launch_bnl2_impl(const BnlArgs& a, const uint2* qc, const uint32_t* skey, u
                       uint32_t* counter, cudaStream_t st) {
     cap &= ~3u;  // 4-entry loads of codes / keys
     const size_t smem = bnl2_smem<D>(cap);
-    SKY_CUDA(cudaFuncSetAttribute(k_bnl2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem_attr((const void*)k_bnl2<D>, smem);
     k_bnl2<D><<<grid, BNL2_B, smem, st>>>(a, qc, skey, cap, counter);
     SKY_LAUNCH_CHECK();
 }
@@ -1129,22 +1129,19 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
         if (codes && posorder) {
             // many representatives, input in L2: sorted positions (a warp's
             // rows have close keys, so its key bound cuts early), flags in place
-            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+            ensure_smem_attr((const void*)k_prefilter<DT, true, true>, smem);
             k_prefilter<DT, true, true><<<ceil_div(n, 256), 256, smem, st>>>(
                 pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
                 dead_pos, tests, x64);
         } else if (codes) {
             // large input: rows streamed in row order (coalesced), flags
             // gathered into position order afterwards
-            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+            ensure_smem_attr((const void*)k_prefilter<DT, true, false>, smem);
             k_prefilter<DT, true, false><<<ceil_div(n, 256), 256, smem, st>>>(
                 pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
                 dead_row, tests, x64);
         } else {
-            SKY_CUDA(cudaFuncSetAttribute(k_prefilter<DT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+            ensure_smem_attr((const void*)k_prefilter<DT, false, false>, smem);
             k_prefilter<DT, false, false><<<ceil_div(n, 256), 256, smem, st>>>(
                 pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, nullptr, rep_id, nrep, nrep_dev,
                 nullptr, dead_row, tests, x64);
