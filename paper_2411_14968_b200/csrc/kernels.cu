@@ -23,7 +23,7 @@ namespace sky {
 void ensure_smem_attr(const void* func, size_t smem) {
     static std::mutex mu;
     static std::map<const void*, size_t> done;
-    if (smem <= 48 * 1024) return;
+    // set even below 48 KB: static + dynamic shared memory past 48 KB needs it
     std::lock_guard<std::mutex> lk(mu);
     size_t& cur = done[func];
     if (cur >= smem) return;
