@@ -893,6 +893,25 @@ __global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict_
         }
     }
     __syncthreads();
+    // a run of identical rows (same FP64 sum and coordinates; e.g. duplicates
+    // clipped to the corner) is ordered by id alone: the bucket is sorted by
+    // (key, row), so the run's first `need` are the answer
+    if (in_smem) {
+        __shared__ int s_diff;
+        if (threadIdx.x == 0) s_diff = 0;
+        __syncthreads();
+        bool diff = false;
+        for (uint32_t e = threadIdx.x; e < L && !diff; e += blockDim.x) {
+            diff = s_sum[e] != s_sum[0];
+            for (uint32_t j = 0; j < d && !diff; ++j) diff = s_run[(size_t)e * d4 + j] != s_run[j];
+        }
+        if (diff) s_diff = 1;
+        __syncthreads();
+        if (!s_diff) {
+            for (uint32_t k = threadIdx.x; k < need; k += blockDim.x) out[ra + k] = (uint32_t)s_c[ra + k];
+            return;
+        }
+    }
     auto less = [&](uint32_t x, uint32_t y) {  // run slots: (sum, lex coords, id)
         if (s_sum[x] != s_sum[y]) return s_sum[x] < s_sum[y];
         if (!in_smem) return lex_less(pts, d, (uint32_t)s_c[ra + x], (uint32_t)s_c[ra + y]);
