@@ -571,7 +571,8 @@ class Runner {
         const uint32_t* n_items = nullptr;
         // grain from the capacity: ~ rows per partition
         const uint64_t per = (uint64_t)cap / std::max<uint32_t>(1, P);
-        uint32_t tile = per >= 2048 ? 256 : (per >= 512 ? 128 : 64);
+        // 128-candidate tiles measured ~1% faster than 256 on config 2
+        uint32_t tile = per >= 512 ? 128 : 64;
         tile = env_u32("SKY_SFS_TILE", tile);
         const uint32_t chunk = env_u32("SKY_SFS_CHUNK", 2048), max_chunks = 64, head = env_u32("SKY_SFS_HEAD", 2048);
         const uint64_t icap = ((uint64_t)cap / tile + P) * max_chunks;
