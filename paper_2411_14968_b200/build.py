@@ -29,7 +29,7 @@ COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibilit
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcudafe", "--diag_suppress=177", "-diag-suppress", "1444"]
 SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "host.cpp", "dataio.cpp", "mtjump.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh"]
+HEADERS = ["common.cuh", "kernels.cuh", "stream.cuh"]
 
 
 def _newer(src_list, target):
