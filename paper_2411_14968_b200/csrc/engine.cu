@@ -50,6 +50,7 @@ struct sky_ctx {
     // work (the random partitioner), with its fork/join events
     cudaStream_t copy = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaEvent_t chunk_ev[4] = {};  // chunked input copy (prep overlaps the copy)
     cudaStream_t stream = nullptr;
     std::string err;
     Arena dev;
@@ -1243,6 +1244,12 @@ uint32_t key_shift_for(uint64_t P) {
     return pb <= 12 ? (uint32_t)pb : 0u;
 }
 
+// a range of input rows whose host->device copy completes at `ready`
+struct InputChunk {
+    uint32_t r0, r1;
+    cudaEvent_t ready;
+};
+
 struct PartitionOut {
     uint64_t* key64;   // sorted (pid << 32 | skey)
     uint32_t* idx;     // row of each sorted position
@@ -1253,7 +1260,8 @@ struct PartitionOut {
 PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d, int normalized, int strategy,
                              uint64_t P, uint64_t m, const sky_config* cfg, const uint32_t* pid_dev,
                              uint64_t* fixups, bool eager = true, uint32_t** scan_rows = nullptr,
-                             bool sort_rows = true, uint32_t* gmin = nullptr) {
+                             bool sort_rows = true, uint32_t* gmin = nullptr,
+                             const std::vector<InputChunk>* in_chunks = nullptr) {
     cudaStream_t st = R.st_;
     uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, n);
     uint64_t* keyB = R.dev<uint64_t>(S_KEY_B, n);
@@ -1285,7 +1293,22 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
         }
     }
     R.hbm_begin();
-    launch_prep(pa, st, R.c_->sm_count);
+    if (in_chunks && !in_chunks->empty() && !gmin && !R.x64_.x) {
+        // the rows arrive in chunks on the copy stream: each chunk's prep
+        // starts as soon as its copy lands (overlapping the later copies)
+        for (const InputChunk& ch : *in_chunks) {
+            SKY_CUDA(cudaStreamWaitEvent(st, ch.ready, 0));
+            PrepArgs pc = pa;
+            pc.pts = pts + (size_t)ch.r0 * d;
+            pc.n = ch.r1 - ch.r0;
+            pc.row_base = ch.r0;
+            launch_prep(pc, st, R.c_->sm_count);
+        }
+    } else {
+        if (in_chunks)
+            for (const InputChunk& ch : *in_chunks) SKY_CUDA(cudaStreamWaitEvent(st, ch.ready, 0));
+        launch_prep(pa, st, R.c_->sm_count);
+    }
     // rows read once; key (8 B) written, row index (4 B) when sorting follows
     R.hbm_end((uint64_t)n * d * (R.x64_.x ? 8 : 4) + (uint64_t)n * (sort_rows ? 12 : 8) +
               (strategy == SKY_SLICED ? 4ull * n : 0ull));
@@ -1609,9 +1632,25 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     // random partitioning does not read the rows: their copy runs on the
     // side stream, overlapped with the partitioner, and joins before prep
     const bool overlap_copy = !f64 && !on_device && cfg->strategy == SKY_RANDOM && c->copy;
+    std::vector<InputChunk> in_chunks;
     if (!f64 && !on_device) {
         float* dp = R.dev<float>(S_PTS, (size_t)n * d);
-        if (overlap_copy) {
+        // copies of 4+ MB in four chunks on the side stream: the prep of a
+        // chunk runs while the next one is copied (partition_phase)
+        const bool chunked = !overlap_copy && c->copy && c->chunk_ev[0] && (uint64_t)n * d * 4 >= (4ull << 20);
+        if (chunked) {
+            SKY_CUDA(cudaEventRecord(c->fork_ev, st));
+            SKY_CUDA(cudaStreamWaitEvent(c->copy, c->fork_ev, 0));
+            const uint32_t per = (ceil_div(n, 4) + 255) & ~255u;
+            for (uint32_t k = 0; k < 4; ++k) {
+                const uint32_t r0 = std::min(n, k * per), r1 = std::min(n, r0 + per);
+                if (r0 >= r1) break;
+                SKY_CUDA(cudaMemcpyAsync(dp + (size_t)r0 * d, static_cast<const float*>(points) + (size_t)r0 * d,
+                                         (size_t)(r1 - r0) * d * sizeof(float), cudaMemcpyHostToDevice, c->copy));
+                SKY_CUDA(cudaEventRecord(c->chunk_ev[k], c->copy));
+                in_chunks.push_back(InputChunk{r0, r1, c->chunk_ev[k]});
+            }
+        } else if (overlap_copy) {
             SKY_CUDA(cudaEventRecord(c->fork_ev, st));
             SKY_CUDA(cudaStreamWaitEvent(c->copy, c->fork_ev, 0));
             SKY_CUDA(cudaMemcpyAsync(dp, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, c->copy));
@@ -1650,7 +1689,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
                                       &out->angular_host_fixups, eager,
                                       rep_random && cfg->strategy == SKY_SLICED ? &scan_rows : nullptr, !stream,
-                                      gmin);
+                                      gmin, &in_chunks);
 
     std::vector<uint32_t> off0(P + 1);
     uint8_t* dead = R.dev<uint8_t>(S_DEAD, n);
@@ -2238,6 +2277,7 @@ int sky_ctx_create(int device, sky_ctx** out) {
         SKY_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
         SKY_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
         SKY_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+        for (auto& e : c->chunk_ev) SKY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->stream = c->own;
         SKY_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         SKY_CUDA(cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -2304,6 +2344,8 @@ void sky_ctx_destroy(sky_ctx* c) {
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
+    for (auto& e : c->chunk_ev)
+        if (e) cudaEventDestroy(e);
     delete c;
 }
 

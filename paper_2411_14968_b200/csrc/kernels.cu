@@ -318,7 +318,8 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < a.n)
-        prep_row<32>(a, i, MemRow{a.pts + (size_t)i * a.d, a.pts64 ? a.pts64 + (size_t)i * a.d : nullptr});
+        prep_row<32>(a, a.row_base + i,
+                     MemRow{a.pts + (size_t)i * a.d, a.pts64 ? a.pts64 + (size_t)i * a.d : nullptr});
 }
 
 // Persistent prep over row tiles streamed by the bulk-copy engine; each row
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
     const uint32_t d = a.d;
     stream_row_tiles(a.pts, a.n, d, smem, [&](const float* tile, uint32_t r0, uint32_t nr, const uint64_t*) {
         if (threadIdx.x < nr) {
-            const uint32_t i = r0 + threadIdx.x;
+            const uint32_t i = a.row_base + r0 + threadIdx.x;
             const float* x = tile + (size_t)threadIdx.x * d;
             RegRow<DP> R;
             if ((d & 3) == 0) {

@@ -68,6 +68,9 @@ struct PrepArgs {
     // angular, m <= 8: tan^2(k*pi/(2m)) for k = 1..m-1 (slice boundaries as
     // tangent ratios); tan2[0] == 0 means "not set" (atan2 filter instead)
     float tan2[8] = {};
+    // rows [0, n) of this launch are rows row_base + [0, n) of the input
+    // (pts already points at row row_base): outputs are indexed globally
+    uint32_t row_base = 0;
 };
 // sm_count > 0: persistent streamed prep when the rows allow it (float,
 // aligned); required when a.gmin is set (grid = prep_stream_grid chunks)
