@@ -398,3 +398,17 @@ def test_device_merge_vs_oracle(engine, monkeypatch, host_merge):
         assert np.array_equal(r.skyline, exp["ids"]), tag
         check_metrics(r, exp, tag)
         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+
+
+def test_chunked_input_copy_vs_oracle(engine):
+    """Host inputs of 4 MB and more are copied in four chunks whose prep
+    starts as each lands: the same result as the oracle (angular, sliced)."""
+    x = generate(2, 200000, 6, 9)
+    assert x.nbytes >= 4 << 20
+    for strat, p in ((2, 64), (3, 16)):
+        cfg = SkyConfig.make(strategy=strat, p=p, seed=4, filter=2, rep_q=8, merge=1, workers=1)
+        exp = O.oracle_run(x, cfg, True)
+        r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+        assert np.array_equal(r.skyline, exp["ids"]), strat
+        check_metrics(r, exp, strat)
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), strat
