@@ -412,3 +412,24 @@ def test_chunked_input_copy_vs_oracle(engine):
         assert np.array_equal(r.skyline, exp["ids"]), strat
         check_metrics(r, exp, strat)
         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), strat
+
+
+def test_repeated_runs_reuse_buffers(engine):
+    """Repeated runs of one shape (arena buffers, pinned result memory and
+    launch-shape caches reused), then another input: every run exact."""
+    x = generate(2, 150000, 6, 21)
+    cfg = SkyConfig.make(strategy=2, p=64, seed=2, filter=2, rep_q=8, merge=1, workers=1)
+    exp = O.oracle_run(x, cfg, True)
+    ecfg = to_engine_config(cfg.as_dict())
+    for it in range(5):
+        r = engine.run(x, ecfg, True)
+        assert np.array_equal(r.skyline, exp["ids"]), it
+        check_metrics(r, exp, it)
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), it
+    # a different input afterwards (other key or the same one): still exact
+    y = generate(2, 150000, 6, 22)
+    exp2 = O.oracle_run(y, cfg, True)
+    for it in range(3):
+        r = engine.run(y, ecfg, True)
+        assert np.array_equal(r.skyline, exp2["ids"]), ("y", it)
+        check_metrics(r, exp2, ("y", it))
