@@ -31,8 +31,9 @@ def test_config_struct_layout_matches_header():
 #include <stddef.h>
 #include "skyline_b200.h"
 int main(void){
- printf("%zu %zu %zu %zu %zu\n", sizeof(sky_config), offsetof(sky_config, rep_q), offsetof(sky_config, count_tests),
-        sizeof(sky_result), offsetof(sky_result, kernel_launches));
+ printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(sky_config), offsetof(sky_config, rep_q),
+        offsetof(sky_config, count_tests), sizeof(sky_result), offsetof(sky_result, kernel_launches),
+        offsetof(sky_result, stream_kernel_ms), offsetof(sky_result, stream_bytes));
  return 0;}
 '''
     with tempfile.TemporaryDirectory() as td:
@@ -42,7 +43,8 @@ int main(void){
         subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), p, "-o", exe], check=True)
         vals = list(map(int, subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()))
     assert vals == [C.sizeof(abi.SkyConfig), abi.SkyConfig.rep_q.offset, abi.SkyConfig.count_tests.offset,
-                    C.sizeof(abi.SkyResult), abi.SkyResult.kernel_launches.offset]
+                    C.sizeof(abi.SkyResult), abi.SkyResult.kernel_launches.offset,
+                    abi.SkyResult.stream_kernel_ms.offset, abi.SkyResult.stream_bytes.offset]
 
 
 def test_snap_slices_known_answers():
