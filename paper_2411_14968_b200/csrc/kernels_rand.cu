@@ -238,13 +238,13 @@ __global__ void k_fy_jump(uint32_t n, uint32_t* __restrict__ fptr, uint32_t* __r
             }
         }
         local = __reduce_add_sync(0xffffffffu, local);
-        if ((threadIdx.x & 31) == 0 && local) atomicAdd(pending + (round & 1), local);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(pending + (round & 3), local);
+        // one grid barrier per round: four rotating counters; the one reset
+        // here was last read right after round-2's barrier, which every
+        // thread passed before round-1's
+        if (blockIdx.x == 0 && threadIdx.x == 0) pending[(round + 2) & 3] = 0;
         grid.sync();
-        const uint32_t left = pending[round & 1];
-        grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x == 0) pending[(round + 1) & 1] = 0;
-        if (left == 0) break;
-        grid.sync();
+        if (pending[round & 3] == 0) break;
     }
 }
 
@@ -297,9 +297,9 @@ bool random_partition_gpu(uint32_t n, uint64_t p, uint64_t seed, uint32_t* pid, 
     uint32_t* gnext = head + n;
     uint32_t* fptr = gnext + (n + 1);
     uint32_t* fval = fptr + (n + 1);
-    uint32_t* misc = fval + (n + 1);  // flag, pending[2]
+    uint32_t* misc = fval + (n + 1);  // flag, pending[4]
     const uint32_t m = n - 1;
-    SKY_CUDA(cudaMemsetAsync(misc, 0, 4 * sizeof(uint32_t), st));
+    SKY_CUDA(cudaMemsetAsync(misc, 0, 8 * sizeof(uint32_t), st));
     SKY_CUDA(cudaMemsetAsync(head, 0xFF, (size_t)n * sizeof(uint32_t), st));
     if (jump_table && m > (1u << 18)) {
         // many CTAs: each chunk of 2^kJumpLog2 outputs from its jumped window
