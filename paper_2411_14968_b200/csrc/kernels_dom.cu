@@ -755,16 +755,21 @@ __global__ void __launch_bounds__(BNL2_B) k_bnl2(BnlArgs a, const uint2* __restr
 // representative with key <= the warp's bound, the exact test only where the
 // codes pass. A row stops at its first dominator, a warp when all its rows
 // are dominated.
+// Codes are used from 32 representatives on (the count may be known on the
+// device only).
 // POSORDER: thread i takes sorted position i (row idx[i]; a warp's rows then
 // share a partition and have neighbouring keys, so they finish together) and
-// writes dead_pos[i]; otherwise thread i takes row i (coalesced stream) and
-// writes dead_row[i].
+// writes dead_pos[i]; after the strongest 64 representatives the CTA's rows
+// still alive are regrouped into dense warps for the rest of the list.
+// Otherwise thread i takes row i (coalesced stream) and writes dead_row[i].
 constexpr uint32_t kAppendSmemReps = 256;
 
-// APPEND (row order): instead of flags, the surviving rows are appended to
-// app.out as ((key64 >> key_shift) << row_bits | row), count in *app.count —
-// the survivors' (partition, key, row) sort key; the CTA's rows are staged
-// through shared memory with coalesced float4 loads.
+// APPEND (row order, the stream path): persistent CTAs walk bulk-copied row
+// tiles with the rows' keys staged alongside (stream_row_tiles); instead of
+// flags, the surviving rows are appended to app.out as
+// ((key64 >> key_shift) << row_bits | row), count in *app.count — the
+// survivors' (partition, key, row) sort key. Shared memory holds at most
+// kAppendSmemReps representatives; a longer list is read from global memory.
 template <int D, bool CODES, bool POSORDER, bool APPEND = false>
 __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts, uint32_t d, uint32_t n,
                                                    const uint32_t* __restrict__ idx,
