@@ -302,6 +302,7 @@ struct PrefilterAppend {
     uint64_t* out = nullptr;
     uint32_t* count = nullptr;
     uint32_t key_shift = 0, row_bits = 0;
+    uint32_t regroup = 64;  // POSORDER: representatives before the CTA regroups its live rows
 };
 // false: not applicable (d > 16, unaligned rows, shared memory)
 bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, const float* rep_xyz,

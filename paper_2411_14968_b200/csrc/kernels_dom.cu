@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "stream.cuh"
@@ -917,7 +918,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
             }
         };
         uint32_t Tl[2] = {T0, T1};
-        constexpr uint32_t K1 = 64;
+        const uint32_t K1 = app.regroup & ~7u;
         if constexpr (POSORDER && !APPEND) {
             if (nrep > K1) {
                 // The strongest K1 representatives kill most rows; the rows
@@ -1135,9 +1136,11 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
             // many representatives, input in L2: sorted positions (a warp's
             // rows have close keys, so its key bound cuts early), flags in place
             ensure_smem_attr((const void*)k_prefilter<DT, true, true>, smem);
+            PrefilterAppend rg;
+            if (const char* e = std::getenv("SKY_PF_REGROUP")) rg.regroup = (uint32_t)std::strtoul(e, nullptr, 10);
             k_prefilter<DT, true, true><<<ceil_div(n, 256), 256, smem, st>>>(
                 pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
-                dead_pos, tests, x64);
+                dead_pos, tests, x64, rg);
         } else if (codes) {
             // large input: rows streamed in row order (coalesced), flags
             // gathered into position order afterwards
