@@ -1484,8 +1484,11 @@ __global__ void __launch_bounds__(256) k_merge_runs(DevSet in, const uint32_t* _
                                                     uint32_t n, DevSet out, const uint32_t* n_dev) {
     constexpr int V = Dims<D>::V;
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (i >= (n_dev ? min(*n_dev, n) : n)) return;
+    const uint32_t limit = n_dev ? min(*n_dev, n) : n;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    // persistent warps over the live count (the grid is sized for residency,
+    // not for the capacity)
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < limit; i += nwarps) {
     // run of element i: the last p with off[p] <= i
     uint32_t lo = 0, hi = P;  // off[lo] <= i < off[hi]
     while (hi - lo > 1) {
@@ -1521,13 +1524,20 @@ __global__ void __launch_bounds__(256) k_merge_runs(DevSet in, const uint32_t* _
         out.id[rank] = in.id[i];
         if (in.qc && out.qc) out.qc[rank] = in.qc[i];
     }
+    }
 }
 
 void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st,
                        const uint32_t* n_dev) {
     if (!in.n) return;
-    SKY_DISPATCH_D(D, (k_merge_runs<DT><<<ceil_div((uint64_t)in.n * 32, 256), 256, 0, st>>>(in, off, P, in.n, out,
-                                                                                            n_dev)));
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        SKY_CUDA(cudaGetDevice(&dev));
+        SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const uint32_t grid = std::min<uint32_t>(ceil_div((uint64_t)in.n * 32, 256), (uint32_t)sms * 8);
+    SKY_DISPATCH_D(D, (k_merge_runs<DT><<<grid, 256, 0, st>>>(in, off, P, in.n, out, n_dev)));
     SKY_LAUNCH_CHECK();
 }
 
