@@ -1974,7 +1974,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         // capacity of the filtered set: n, or for large inputs the exact
         // count (one early round trip), so later passes are not sized by n
         uint32_t cap0 = n;
-        if (n > kExactCapRows) {
+        if (n > kExactCapRows && !env_u32("SKY_NO_CAP_SYNC", 0)) {
             uint32_t* hc = R.pin<uint32_t>(P_MISC, 8);
             SKY_CUDA(cudaMemcpyAsync(hc, misc + M_S0, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
             R.sync();
