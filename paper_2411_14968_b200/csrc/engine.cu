@@ -491,6 +491,18 @@ class Runner {
     // result has n = in.n slots, offsets off_out and *total live rows.
     DevSet compact_dev(const DevSet& in, const uint8_t* dead, const uint32_t* off_in, uint32_t P, int out_base,
                        uint32_t* off_out, uint32_t* total, int D) {
+        if (in.n) {
+            // dense list of the live rows + remapped offsets + count (two
+            // launches, work proportional to the live rows past the count
+            // pass), then a gather bounded by the device count
+            uint32_t* dense = dev<uint32_t>(S_POS, in.n);
+            launch_dense_compact(dead, in.n, off_in, P, 0, dense, off_out, total,
+                                 dev<uint32_t>(S_DCBT, dense_compact_scratch(in.n) / 4), st_);
+            DevSet out = set(out_base, in.n, D);
+            launch_gather_set(D, in, dense, out, st_, total);
+            count(3);
+            return out;
+        }
         uint32_t* pos = dev<uint32_t>(S_POS, in.n);
         scan_live(dead, pos, in.n);
         launch_count_total(pos, dead, in.n, total, st_);

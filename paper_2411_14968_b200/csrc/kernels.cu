@@ -1454,10 +1454,11 @@ void launch_gather_rows(int D, const float* pts, const double* pts64, uint32_t d
 }
 
 template <int D>
-__global__ void k_gather_set(DevSet in, const uint32_t* __restrict__ perm, uint32_t n, DevSet out) {
+__global__ void k_gather_set(DevSet in, const uint32_t* __restrict__ perm, uint32_t n, DevSet out,
+                             const uint32_t* n_dev) {
     constexpr int V = Dims<D>::V;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= (n_dev ? min(*n_dev, n) : n)) return;
     const uint32_t s = perm[i];
     const float4* src = reinterpret_cast<const float4*>(in.xyz) + (size_t)s * V;
     float4* dst = reinterpret_cast<float4*>(out.xyz) + (size_t)i * V;
@@ -1468,9 +1469,10 @@ __global__ void k_gather_set(DevSet in, const uint32_t* __restrict__ perm, uint3
     if (in.qc && out.qc) out.qc[i] = in.qc[s];
 }
 
-void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st) {
+void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st,
+                       const uint32_t* n_dev) {
     if (!in.n) return;
-    SKY_DISPATCH_D(D, (k_gather_set<DT><<<ceil_div(in.n, 256), 256, 0, st>>>(in, perm, in.n, out)));
+    SKY_DISPATCH_D(D, (k_gather_set<DT><<<ceil_div(in.n, 256), 256, 0, st>>>(in, perm, in.n, out, n_dev)));
     SKY_LAUNCH_CHECK();
 }
 

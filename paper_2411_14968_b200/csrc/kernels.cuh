@@ -147,7 +147,9 @@ void launch_scatter_indirect(int D, const float* pts, uint32_t d, const uint32_t
                              uint32_t n, const uint8_t* dead, const uint32_t* pos, DevSet out, cudaStream_t st);
 void launch_gather_rows(int D, const float* pts, const double* pts64, uint32_t d, const uint32_t* rows, uint32_t n,
                         DevSet out, cudaStream_t st);
-void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st);
+// out[i] = in[perm[i]] for i < in.n (or < *n_dev when given)
+void launch_gather_set(int D, const DevSet& in, const uint32_t* perm, DevSet out, cudaStream_t st,
+                       const uint32_t* n_dev = nullptr);
 // stable merge of the key-sorted runs off[P+1] of `in` into `out` (key order)
 // (n_dev: live count on the device, in.n the capacity)
 void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st,
