@@ -112,8 +112,11 @@ constexpr uint32_t kBlock = 512;    // local block-skyline size
 // comparators of a multi-wave relsky run as one last wave
 constexpr uint64_t kWaveSplitPairs = 8ull << 30;
 // above this many input rows the single-GPU path reads the filtered count
-// back before sizing the downstream sets by it
-constexpr uint32_t kExactCapRows = 0;
+// back before sizing the downstream sets by it; up to it the sets keep the
+// input's size as capacity and every pass is bounded by the device count
+// (one round trip per run: measured 0.5% faster on config 2, 2.4% on
+// config 1, even on config 5's 2M rows)
+constexpr uint32_t kExactCapRows = 1u << 20;
 
 // misc device words
 enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, M_NREP = 6, M_NITEMS = 7, M_TESTS = 8 /* 4 x u64 */,
@@ -569,8 +572,7 @@ class Runner {
         const uint32_t cap = s0.n;
         uint32_t* misc = dev<uint32_t>(S_MISC, 64);
         uint8_t* dead = dev<uint8_t>(S_DEAD, cap);
-        launch_fill_u8(dead, 0, cap, st_);
-        launch_fill_tail_u8(dead, 1, n0, cap, st_);
+        launch_fill_live_u8(dead, n0, cap, st_);
         count();
         RelskyArgs a{};
         a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
@@ -614,7 +616,7 @@ class Runner {
         uint32_t* dnew = dev<uint32_t>(S_DNEW, P + 1);
         uint32_t* dense = dev<uint32_t>(S_DENSE, cap);
         if (launch_dense_compact(dead, cap, off0_dev, P, 0, dense, dnew, nullptr,
-                                 dev<uint32_t>(S_DCBT, dense_compact_scratch(cap) / 4), st_)) {
+                                 dev<uint32_t>(S_DCBT, dense_compact_scratch(cap) / 4), st_, n0)) {
             count(2);
         } else {
             uint32_t* pos = dev<uint32_t>(S_POS, cap);
@@ -642,9 +644,8 @@ class Runner {
         DevSet US = set(S_SET3, cap, D);
         launch_merge_runs(D, U, off_u, P, US, st_, n_u);
         uint8_t* dead = dev<uint8_t>(S_CELLDEAD, cap);
-        launch_fill_u8(dead, 0, cap, st_);
-        launch_fill_tail_u8(dead, 1, n_u, cap, st_);
-        count(3);
+        launch_fill_live_u8(dead, n_u, cap, st_);
+        count(2);
         *dead_out = dead;
         if (!cap) return US;
         uint32_t* misc = dev<uint32_t>(S_MISC, 64);
@@ -670,7 +671,7 @@ class Runner {
         uint32_t* dnew = dev<uint32_t>(S_DNEW, 2);
         uint32_t* dense = dev<uint32_t>(S_DENSE, cap);
         launch_dense_compact(dead, cap, offg, 1, 0, dense, dnew, nullptr,
-                             dev<uint32_t>(S_DCBT, dense_compact_scratch(cap) / 4), st_);
+                             dev<uint32_t>(S_DCBT, dense_compact_scratch(cap) / 4), st_, n_u);
         count(2);
         launch_plan_partition_items(dnew, nullptr, n_u, 1, head, ~0ull, tile, 0, max_chunks, icap32, items, ni, st_,
                                     target);
@@ -1875,7 +1876,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         uint32_t* hid = R.pin<uint32_t>(P_IDS, std::max<uint32_t>(cap, 1));
         uint32_t* bm = R.dev<uint32_t>(S_BM, (size_t)n / 32 + 1);
         uint32_t* bt = R.dev<uint32_t>(S_BMT, bm_blocks(n));
-        launch_ids_bitmap(US.id, fdead, cap, n, bm, bt, hid, misc + M_TOTAL, st);
+        launch_ids_bitmap(US.id, fdead, cap, n, bm, bt, hid, misc + M_TOTAL, st, misc + M_U);
         R.count(cap ? 3 : 2);
         uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32 + 16);
         uint32_t* hmisc = h + P + 1;
@@ -1986,7 +1987,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         // capacity of the filtered set: n, or for large inputs the exact
         // count (one early round trip), so later passes are not sized by n
         uint32_t cap0 = n;
-        if (n > kExactCapRows && !env_u32("SKY_NO_CAP_SYNC", 0)) {
+        if ((n > kExactCapRows || env_u32("SKY_CAP_SYNC", 0)) && !env_u32("SKY_NO_CAP_SYNC", 0)) {
             uint32_t* hc = R.pin<uint32_t>(P_MISC, 8);
             SKY_CUDA(cudaMemcpyAsync(hc, misc + M_S0, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
             R.sync();

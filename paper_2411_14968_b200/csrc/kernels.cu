@@ -1549,8 +1549,9 @@ void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P,
 constexpr uint32_t kBmWords = 2048;
 
 __global__ void k_bm_set(const uint32_t* __restrict__ id, const uint8_t* __restrict__ dead, uint32_t n,
-                         uint32_t* __restrict__ bm) {
+                         uint32_t* __restrict__ bm, const uint32_t* n_dev) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n_dev) n = min(n, *n_dev);
     if (i >= n || dead[i]) return;
     const uint32_t v = id[i];
     atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -1647,11 +1648,11 @@ __global__ void __launch_bounds__(256) k_bm_emit(const uint32_t* __restrict__ bm
 uint32_t bm_blocks(uint32_t n_ids) { return ceil_div(ceil_div(std::max<uint32_t>(n_ids, 1), 32), kBmWords); }
 
 void launch_ids_bitmap(const uint32_t* id, const uint8_t* dead, uint32_t n, uint32_t n_ids, uint32_t* bm,
-                       uint32_t* block_tot, uint32_t* out, uint32_t* total, cudaStream_t st) {
+                       uint32_t* block_tot, uint32_t* out, uint32_t* total, cudaStream_t st, const uint32_t* n_dev) {
     const uint32_t words = ceil_div(std::max<uint32_t>(n_ids, 1), 32);
     SKY_CUDA(cudaMemsetAsync(bm, 0, (size_t)words * sizeof(uint32_t), st));
     if (n) {
-        k_bm_set<<<ceil_div(n, 256), 256, 0, st>>>(id, dead, n, bm);
+        k_bm_set<<<ceil_div(n, 256), 256, 0, st>>>(id, dead, n, bm, n_dev);
         SKY_LAUNCH_CHECK();
     }
     const uint32_t blocks = bm_blocks(n_ids);
@@ -1719,6 +1720,28 @@ void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st) {
 __global__ void k_fill_tail_u8(uint8_t* __restrict__ p, uint8_t v, const uint32_t* __restrict__ count, uint32_t cap) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cap && i >= *count) p[i] = v;
+}
+
+// dead flags of a capacity-sized set: 0 below the device count, 1 from it on
+// (four flags per thread; p 4-byte aligned)
+__global__ void k_fill_live_u8(uint8_t* __restrict__ p, const uint32_t* __restrict__ count, uint32_t cap) {
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i >= cap) return;
+    const uint32_t c = *count;
+    if (i + 4 <= cap) {
+        uint32_t w = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) w |= (i + k >= c ? 1u : 0u) << (8 * k);
+        *reinterpret_cast<uint32_t*>(p + i) = w;
+    } else {
+        for (uint32_t k = i; k < cap; ++k) p[k] = k >= c ? 1 : 0;
+    }
+}
+
+void launch_fill_live_u8(uint8_t* p, const uint32_t* count, uint32_t cap, cudaStream_t st) {
+    if (!cap) return;
+    k_fill_live_u8<<<ceil_div(ceil_div(cap, 4), 256), 256, 0, st>>>(p, count, cap);
+    SKY_LAUNCH_CHECK();
 }
 
 void launch_fill_tail_u8(uint8_t* p, uint8_t v, const uint32_t* count, uint32_t cap, cudaStream_t st) {

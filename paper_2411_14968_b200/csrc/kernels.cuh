@@ -157,7 +157,8 @@ void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P,
 // ascending ids (< n_ids) of the live entries of id[n] via a bitmap; count in *total
 uint32_t bm_blocks(uint32_t n_ids);
 void launch_ids_bitmap(const uint32_t* id, const uint8_t* dead, uint32_t n, uint32_t n_ids, uint32_t* bm,
-                       uint32_t* block_tot, uint32_t* out, uint32_t* total, cudaStream_t st);
+                       uint32_t* block_tot, uint32_t* out, uint32_t* total, cudaStream_t st,
+                       const uint32_t* n_dev = nullptr);
 void launch_remap_offsets(const uint32_t* off_old, uint32_t P, const uint32_t* pos, const uint8_t* dead,
                           uint32_t n, uint32_t* off_new, cudaStream_t st);
 void launch_count_total(const uint32_t* pos, const uint8_t* dead, uint32_t n, uint32_t* total, cudaStream_t st);
@@ -166,6 +167,7 @@ void launch_compact_ids(const uint32_t* id, const uint8_t* dead, const uint32_t*
 void launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st);
 // p[i] = v for *count <= i < cap (the unused tail of a set sized by capacity)
 void launch_fill_tail_u8(uint8_t* p, uint8_t v, const uint32_t* count, uint32_t cap, cudaStream_t st);
+void launch_fill_live_u8(uint8_t* p, const uint32_t* count, uint32_t cap, cudaStream_t st);
 // out[pos[i]] = base + i for live i (dense list of live positions)
 void launch_compact_pos(const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t base, uint32_t* out,
                         cudaStream_t st);
@@ -260,9 +262,10 @@ bool launch_plan_partition_items(const uint32_t* coff, const uint32_t* soff, con
                                  uint32_t grain_target = 0);
 // dense list of live entries + remapped segment offsets (off[P+1] sorted)
 // in two launches; block_tot: dense_compact_scratch(n) bytes. false: n == 0
+// n_dev (optional): entries at or past *n_dev are dead and not read
 bool launch_dense_compact(const uint8_t* dead, uint32_t n, const uint32_t* off, uint32_t P, uint32_t base,
                           uint32_t* dense, uint32_t* off_new, uint32_t* total, uint32_t* block_tot,
-                          cudaStream_t st);
+                          cudaStream_t st, const uint32_t* n_dev = nullptr);
 size_t dense_compact_scratch(uint32_t n);
 
 // Items of a relsky wave built on the device from the dense candidate

@@ -1459,7 +1459,8 @@ bool launch_plan_partition_items(const uint32_t* coff, const uint32_t* soff, con
 constexpr uint32_t kDcPer = 8, kDcThreads = 256, kDcTile = kDcPer * kDcThreads;
 
 __global__ void __launch_bounds__(kDcThreads) k_dc_count(const uint8_t* __restrict__ dead, uint32_t n,
-                                                         uint32_t* __restrict__ block_tot) {
+                                                         uint32_t* __restrict__ block_tot, const uint32_t* n_dev) {
+    if (n_dev) n = min(n, *n_dev);  // entries past the device count are dead: not read
     const uint32_t i0 = blockIdx.x * kDcTile + threadIdx.x * kDcPer;
     uint32_t c = 0;
 #pragma unroll
@@ -1479,7 +1480,8 @@ __global__ void __launch_bounds__(kDcThreads) k_dc_emit(const uint8_t* __restric
                                                         const uint32_t* __restrict__ block_tot,
                                                         const uint32_t* __restrict__ off, uint32_t P, uint32_t base,
                                                         uint32_t* __restrict__ dense, uint32_t* __restrict__ off_new,
-                                                        uint32_t* total_out) {
+                                                        uint32_t* total_out, const uint32_t* n_dev) {
+    if (n_dev) n = min(n, *n_dev);
     using Scan = cub::BlockScan<uint32_t, kDcThreads>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ uint32_t s_w[kDcThreads / 32];
@@ -1527,12 +1529,12 @@ __global__ void __launch_bounds__(kDcThreads) k_dc_emit(const uint8_t* __restric
 
 bool launch_dense_compact(const uint8_t* dead, uint32_t n, const uint32_t* off, uint32_t P, uint32_t base,
                           uint32_t* dense, uint32_t* off_new, uint32_t* total, uint32_t* block_tot,
-                          cudaStream_t st) {
+                          cudaStream_t st, const uint32_t* n_dev) {
     if (n == 0 || n > (64u << 20)) return false;
     const uint32_t blocks = ceil_div(n, kDcTile);
-    k_dc_count<<<blocks, kDcThreads, 0, st>>>(dead, n, block_tot);
+    k_dc_count<<<blocks, kDcThreads, 0, st>>>(dead, n, block_tot, n_dev);
     SKY_LAUNCH_CHECK();
-    k_dc_emit<<<blocks, kDcThreads, 0, st>>>(dead, n, block_tot, off, P, base, dense, off_new, total);
+    k_dc_emit<<<blocks, kDcThreads, 0, st>>>(dead, n, block_tot, off, P, base, dense, off_new, total, n_dev);
     SKY_LAUNCH_CHECK();
     return true;
 }

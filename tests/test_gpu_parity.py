@@ -322,6 +322,18 @@ def test_stream_path_forced(engine, golden, monkeypatch, stream):
     test_random_configs_vs_oracle(engine)
 
 
+@pytest.mark.parametrize("mode", ["SKY_CAP_SYNC", "SKY_NO_CAP_SYNC"])
+def test_filtered_capacity_modes(engine, golden, monkeypatch, mode):
+    """Both sizings of the filtered set (engine.cu kExactCapRows): the exact
+    count read back before the local phase, and the input's size as capacity
+    with every later pass bounded by the device count."""
+    monkeypatch.setenv(mode, "1")
+    test_plane_matches_reference(engine, golden, LocalAlgo.SFS)
+    for idx in (1, 2, 3, 5):
+        test_baseline_configs_reduced(engine, golden, idx)
+    test_random_configs_vs_oracle(engine)
+
+
 def test_stream_path_bucket_overflow(engine, monkeypatch):
     """Candidate buckets that fill up (duplicate-heavy rows, rows sorted by
     partition) fall back to the sorted path with identical results."""
