@@ -153,6 +153,7 @@ def ref_lib():
         lib.skyref_representatives.argtypes = [_f32p, C.c_uint64, C.c_uint32, _u64p, C.c_uint64, C.c_uint64, _i64p]
         lib.skyref_representatives.restype = C.c_uint64
         lib.skyref_hardware_concurrency.restype = C.c_int
+        lib.skyref_generate_baseline.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, _f32p]
         _ref = lib
     return _ref
 
@@ -261,6 +262,17 @@ def random_permutation(n, seed):
     out = np.zeros(max(n, 1), np.uint64)
     oracle_lib().oracle_random_permutation(n, seed, out.ctypes.data_as(_u64p))
     return out[:n]
+
+
+def ref_generate_baseline(kind: int, n: int, d: int, seed: int = 42) -> np.ndarray:
+    """BASELINE.json input `kind` (1..5) as float32 n x d, built inside
+    oracle/_ref/libskyref.so from include/skyline_baseline_gen.h — the same
+    bytes as the product's sky_generate, without loading the product."""
+    out = np.empty((n, d), np.float32)
+    rc = ref_lib().skyref_generate_baseline(kind, n, d, seed, out.ctypes.data_as(_f32p))
+    if rc:
+        raise CpuError(rc)
+    return out
 
 
 def ref_generate(dist: int, n: int, d: int, seed: int) -> np.ndarray:

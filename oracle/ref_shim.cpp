@@ -20,6 +20,7 @@
 #include "skyline/partition.hpp"
 #include "skyline/sequential.hpp"
 #include "../include/skyline_b200.h"
+#include "../include/skyline_baseline_gen.h"
 
 using namespace skyline;
 
@@ -136,6 +137,13 @@ int skyref_run_f64(const double* pts, uint64_t n, uint32_t d, int normalized, co
 
 // skyline::generate (datagen.cpp:127-151): dist 0 uniform, 1 correlated,
 // 2 anticorrelated; rows into out[n*d].
+// BASELINE.json's synthetic inputs (include/skyline_baseline_gen.h): the
+// same bytes the product's sky_generate writes, so the reference arm and the
+// golden script never load the product library to build their input.
+int skyref_generate_baseline(int kind, uint64_t n, uint32_t d, uint64_t seed, float* out) {
+    return sky_baseline_gen::generate(kind, n, d, seed, out) ? SKY_OK : SKY_E_CONFIG;
+}
+
 int skyref_generate(int dist, uint64_t n, uint64_t d, uint64_t seed, double* out) {
     return guarded([&] {
         GenSpec g;

@@ -28,7 +28,7 @@ COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibilit
           "-I", os.path.join(ROOT, "include")]
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcudafe", "--diag_suppress=177", "-diag-suppress", "1444"]
-SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "host.cpp", "dataio.cpp", "mtjump.cpp"]
+SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "host.cpp", "dataio.cpp", "mtjump.cpp", "angular.cpp"]
 HEADERS = ["common.cuh", "kernels.cuh", "stream.cuh"]
 
 
@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
     if force or _newer(objs, OUT):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-lnccl", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-lnccl", "-lpthread", "-lquadmath"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

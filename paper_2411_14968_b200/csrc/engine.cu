@@ -82,6 +82,11 @@ struct sky_ctx {
     // host round trips: spin on an event instead of a blocking stream sync
     // (the wake-up of cudaStreamSynchronize costs ~15-20 us per round trip)
     cudaEvent_t sync_ev = nullptr;
+    // exact angular slice thresholds (angular_thresholds) for slices ang_m,
+    // and the device copy last uploaded
+    std::vector<double4> ang_host;
+    uint64_t ang_m = 0, ang_dev_m = 0;
+    const void* ang_dev_ptr = nullptr;
 };
 
 namespace {
@@ -94,7 +99,7 @@ enum Slot {
     S_PERM_A, S_PERM_B, S_IDS_A, S_IDS_B, S_CELLDEAD, S_BNL_POS, S_BNL_META,
     S_OVF, S_SKTMP, S_THR, S_RAND, S_OFF_C, S_SIZES, S_GCOUNT, S_PTHR, S_DEADROW, S_DENSE,
     S_SCAN, S_PTS64, S_GROUPS, S_GB, S_JCNT, S_JPRE, S_JOBS, S_DNEW,
-    S_ROWPID, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_DCBT, S_OFFG, S_COUNT
+    S_ROWPID, S_AMBROWS, S_ANGT, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_DCBT, S_OFFG, S_COUNT
 };
 // pinned slots
 enum PSlot { P_PID, P_MISC, P_OFF, P_ITEMS, P_RANGES, P_IDS, P_AMB, P_RUNS, P_PCOUNT };
@@ -1061,6 +1066,24 @@ class Runner {
         return pid;
     }
 
+    // exact angular slice thresholds for m (host table cached per context)
+    const double4* angular_table(uint64_t m) {
+        if (m > kAngularExactMaxM) return nullptr;
+        if (c_->ang_m != m) {
+            c_->ang_host.resize(m - 1);
+            angular_thresholds(m, c_->ang_host.data());
+            c_->ang_m = m;
+            c_->ang_dev_m = 0;
+        }
+        double4* t = dev<double4>(S_ANGT, m - 1);
+        if (c_->ang_dev_m != m || c_->ang_dev_ptr != t) {
+            SKY_CUDA(cudaMemcpy(t, c_->ang_host.data(), (m - 1) * sizeof(double4), cudaMemcpyHostToDevice));
+            c_->ang_dev_m = m;
+            c_->ang_dev_ptr = t;
+        }
+        return t;
+    }
+
     unsigned long long* tests(int k) {
         return reinterpret_cast<unsigned long long*>(dev<uint32_t>(S_MISC, 64) + M_TESTS) + k;
     }
@@ -1283,7 +1306,9 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
     const uint32_t* pid_in = strategy == SKY_RANDOM ? pid_dev : nullptr;
     if (strategy == SKY_RANDOM && !pid_in && n) throw Error(SKY_E_INTERNAL, "random strategy without partition ids");
-    const uint32_t amb_cap = 1u << 16;
+    // angular rows the device cannot decide (see angular_thresholds): the
+    // list holds every row if need be
+    const uint32_t amb_cap = strategy == SKY_ANGULAR ? std::max<uint32_t>(n, 1) : 1u;
     uint32_t* amb = R.dev<uint32_t>(S_AMB, amb_cap);
     uint32_t* skA = nullptr;
     if (strategy == SKY_SLICED) skA = R.dev<uint32_t>(S_SK_A, n);
@@ -1296,6 +1321,11 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
     if (gmin) {
         pa.gmin = gmin;
         pa.P = (uint32_t)P;
+    }
+    if (strategy == SKY_ANGULAR && m >= 2) {
+        pa.ang_thr = R.angular_table(m);
+        volatile double one = 1.0;
+        pa.ang_c45 = std::atan2(one, one);  // the host libm's atan2(x, x) (partition.cpp:128)
     }
     if (strategy == SKY_ANGULAR && m >= 2 && m <= 8) {
         // slice boundaries k*pi/(2m) as tan^2 (k = 1..m-1) for the FP32 filter
@@ -1338,32 +1368,23 @@ PartitionOut partition_phase(Runner& R, const float* pts, uint32_t n, uint32_t d
         check_prep(hm[M_ERR], 0, strategy, true);
     }
     if (eager && strategy == SKY_ANGULAR && hm[M_AMB]) {
-        const uint32_t na = hm[M_AMB];
-        if (na > amb_cap) throw Error(SKY_E_INTERNAL, "too many angular boundary points");
-        uint32_t* ha = R.pin<uint32_t>(P_AMB, 3 * (size_t)na + 1);
-        SKY_CUDA(cudaMemcpyAsync(ha, amb, na * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        // rows whose slice the device left open (the exact angle within the
+        // host libm's 1-ulp latitude of a boundary, or m > kAngularExactMaxM):
+        // one gather, one copy each way, the reference's formula on the host
+        const uint32_t na = std::min(hm[M_AMB], amb_cap);
+        double* drows = R.dev<double>(S_AMBROWS, (size_t)na * d);
+        launch_gather_rows_f64(pts, R.x64_.x, d, amb, na, 0, drows, st);
+        R.count();
+        double* hrows = R.pin<double>(P_AMB, (size_t)na * d + na);
+        SKY_CUDA(cudaMemcpyAsync(hrows, drows, (size_t)na * d * sizeof(double), cudaMemcpyDeviceToHost, st));
         R.sync();
-        // fetch the rows and recompute with the host libm
-        std::vector<float> row(d);
-        uint32_t* hp = ha + na;
-        float* hrows = reinterpret_cast<float*>(ha + 2 * (size_t)na);
-        (void)hrows;
-        std::vector<double> row64(d);
-        for (uint32_t k = 0; k < na; ++k) {
-            if (R.x64_.x) {
-                SKY_CUDA(cudaMemcpy(row64.data(), R.x64_.x + (size_t)ha[k] * d, d * sizeof(double),
-                                    cudaMemcpyDeviceToHost));
-            } else {
-                SKY_CUDA(cudaMemcpy(row.data(), pts + (size_t)ha[k] * d, d * sizeof(float), cudaMemcpyDeviceToHost));
-                for (uint32_t j = 0; j < d; ++j) row64[j] = row[j];
-            }
-            hp[k] = (uint32_t)angular_index_host(row64.data(), d, m);
-        }
-        uint32_t* dp = amb + na;  // reuse tail of the amb buffer for pids (cap >= 2*na checked below)
-        if (2 * (size_t)na > amb_cap) dp = R.dev<uint32_t>(S_RUNS, na);
+        uint32_t* hp = reinterpret_cast<uint32_t*>(hrows + (size_t)na * d);
+        for (uint32_t k = 0; k < na; ++k) hp[k] = (uint32_t)angular_index_host(hrows + (size_t)k * d, d, m);
+        uint32_t* dp = R.dev<uint32_t>(S_RUNS, na);
         SKY_CUDA(cudaMemcpyAsync(dp, hp, na * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
         launch_patch_pid(keyA, amb, dp, na, st);
         R.count();
+        R.sync();  // the pinned pids above are reused by later phases
         *fixups = na;
     }
 

@@ -108,6 +108,54 @@ struct RegRow {
     __device__ __forceinline__ double X(uint32_t j) const { return (double)v[j]; }
 };
 
+// sign of y - x * (th + tl) for doubles x, y >= 0 in [2^-600, 2^600]:
+// +1 / -1, or 0 when the difference is within the error bound (|.| <=
+// 2^-98 of the operands; the threshold itself is accurate to ~2^-105)
+__device__ __forceinline__ int cmp_tan(double y, double x, double th, double tl) {
+    const double p = __dmul_rn(x, th);
+    const double e = fma(x, th, -p);  // x*th = p + e exactly
+    const double r = __dsub_rn(y, p);  // exact when p is within a factor 2 of y
+    const double s = __dsub_rn(__dsub_rn(r, e), __dmul_rn(x, tl));
+    const double tol = 0x1p-98 * fmax(y, p);
+    return s > tol ? 1 : (s < -tol ? -1 : 0);
+}
+
+// slice of one hyperspherical angle phi = atan2(y, x) (partition.cpp:128-143)
+// as the reference computes it on the host libm; *amb when the exact angle
+// lies within the libm's 1-ulp latitude of a slice boundary.
+__device__ __forceinline__ uint32_t angular_slice_exact(double y, double x, const double4* __restrict__ thr,
+                                                        uint32_t m, double c45, bool* amb) {
+    if (y == 0.0) return 0;  // atan2(+0, x >= 0) = +0
+    double phi = -1.0;
+    if (x == 0.0) {
+        phi = 0x1.921fb54442d18p+0;  // atan2(y > 0, +0) = rn(pi/2)
+    } else if (y == x) {
+        phi = c45;  // the host libm's atan2(x, x)
+    } else {
+        // scale to a common exponent (the comparison is scale invariant)
+        const int ex = max(ilogb(y), ilogb(x));
+        const double ys = scalbn(y, -ex), xs = scalbn(x, -ex);
+        if (xs < 0x1p-600) return m - 1;  // angle within 2^-600 of pi/2: above every boundary
+        if (ys < 0x1p-600) return 0;      // angle within 2^-600 of 0: below every boundary
+        // s = #{k : phi >= phi*_k} (the angle is above tan(phi*_k))
+        uint32_t lo = 0, hi = m - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            const double4 t = thr[mid - 1];
+            if (cmp_tan(ys, xs, t.z, t.w) > 0) lo = mid; else hi = mid - 1;
+        }
+        // the next boundary must be cleared from below: angle <= pred(phi*)
+        if (lo + 1 <= m - 1) {
+            const double4 t = thr[lo];
+            if (cmp_tan(ys, xs, t.x, t.y) >= 0) *amb = true;
+        }
+        return lo;
+    }
+    const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), 3.14159265358979323846), (double)m);
+    const uint32_t slice = (uint32_t)v;
+    return slice >= m ? m - 1 : slice;
+}
+
 // One row of the prep pass: validation, FP64 sum, partition id, sort key
 // (j < DMAX covers every coordinate: DMAX >= d). Returns the sort key.
 template <int DMAX, class Row>
@@ -262,16 +310,22 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                     tail = __dmul_rn(xi, xi);
                     continue;
                 }
-                const double phi = atan2(sqrt(tail), xi);
+                uint32_t slice;
+                if (a.ang_thr) {
+                    bool amb = false;
+                    slice = angular_slice_exact(__dsqrt_rn(tail), xi, a.ang_thr, m32, a.ang_c45, &amb);
+                    ambiguous |= amb;
+                } else {
+                    // m > kAngularExactMaxM: CUDA's atan2 (within 2 ulp) and a
+                    // band around each boundary resolved on the host libm
+                    const double phi = atan2(sqrt(tail), xi);
+                    const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
+                    slice = (uint32_t)v;
+                    if (slice >= m32) slice = m32 - 1;
+                    const double r = rint(v);
+                    if (r >= 1.0 && r <= (double)(a.m - 1) && fabs(v - r) <= 1e-9 * fmax(1.0, v)) ambiguous = true;
+                }
                 tail = __dadd_rn(tail, __dmul_rn(xi, xi));
-                const double v = __dmul_rn(__ddiv_rn(__dmul_rn(2.0, phi), PI), (double)a.m);
-                uint32_t slice = (uint32_t)v;
-                if (slice >= m32) slice = m32 - 1;
-                // CUDA's atan2 may differ from the host libm by an ulp or two; a
-                // value this close to an interior slice boundary is resolved on
-                // the host with the reference's own formula.
-                const double r = rint(v);
-                if (r >= 1.0 && r <= (double)(a.m - 1) && fabs(v - r) <= 1e-9 * fmax(1.0, v)) ambiguous = true;
                 pid64 = pid64 * m32 + slice;
             }
             pid = pid64;
@@ -450,6 +504,23 @@ void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t*
         return;
     }
     k_seg_offsets<<<ceil_div(n, 256), 256, 0, st>>>(key64, n, P, off);
+    SKY_LAUNCH_CHECK();
+}
+
+__global__ void k_gather_rows_f64(const float* pts, const double* pts64, uint32_t d, const uint32_t* rows,
+                                  uint32_t count, uint32_t row_base, double* out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (uint64_t)count * d) return;
+    const uint32_t k = (uint32_t)(t / d), j = (uint32_t)(t % d);
+    const size_t r = (size_t)(rows[k] - row_base) * d + j;
+    out[t] = pts64 ? pts64[r] : (double)pts[r];
+}
+
+void launch_gather_rows_f64(const float* pts, const double* pts64, uint32_t d, const uint32_t* rows,
+                            uint32_t count, uint32_t row_base, double* out, cudaStream_t st) {
+    if (!count) return;
+    const uint64_t total = (uint64_t)count * d;
+    k_gather_rows_f64<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(pts, pts64, d, rows, count, row_base, out);
     SKY_LAUNCH_CHECK();
 }
 

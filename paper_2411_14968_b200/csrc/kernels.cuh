@@ -59,7 +59,7 @@ struct PrepArgs {
     uint32_t* idx;           // out: identity
     uint32_t* slice_key;     // out (sliced): canonical bits of x[slice_dim]
     uint32_t* err;           // out: error bits
-    uint32_t* amb_count;     // out (angular): boundary points
+    uint32_t* amb_count;     // out (angular): rows whose slice the device cannot decide
     uint32_t* amb_list;
     uint32_t amb_cap;
     uint32_t key_shift;      // low bits of skey cleared (the partition sort skips them)
@@ -71,6 +71,11 @@ struct PrepArgs {
     // rows [0, n) of this launch are rows row_base + [0, n) of the input
     // (pts already points at row row_base): outputs are indexed globally
     uint32_t row_base = 0;
+    // angular: exact slice thresholds (angular_thresholds), one double4
+    // (tan(pred(phi*_k)) hi/lo, tan(phi*_k) hi/lo) per interior boundary
+    // k = 1..m-1; null -> FP64 atan2 with an ambiguity band (host libm)
+    const double4* ang_thr = nullptr;
+    double ang_c45 = 0.0;    // the host libm's atan2(x, x) (the y == x tie)
 };
 // sm_count > 0: persistent streamed prep when the rows allow it (float,
 // aligned); required when a.gmin is set (grid = prep_stream_grid chunks)
@@ -82,6 +87,22 @@ void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t*
 // sorted survivor keys of launch_prefilter_append -> key64, rows, offsets[P+1]
 void launch_unpack_survivors(const uint64_t* comp, uint32_t n, uint32_t row_bits, uint32_t key_shift, uint32_t P,
                              uint64_t* key64, uint32_t* idx, uint32_t* off, cudaStream_t st);
+
+// Exact angular slicing (partition.cpp:118-148). For an interior boundary
+// k = 1..m-1 let phi*_k be the smallest double phi with
+// (size_t)(2.0 * phi / pi * m) >= k (the reference's own arithmetic). The
+// host libm's atan2 is faithful (error < 1 ulp), so the reference's slice is
+// decided by the exact angle alone unless it lies strictly between
+// pred(phi*_k) and phi*_k. Per boundary the table holds tan(pred(phi*_k)) and
+// tan(phi*_k) as double-doubles (from quad precision); the device compares
+// y = sqrt(tail) against x * tan(.) with an exact product. Returns the
+// number of entries written (m - 1); m <= kAngularExactMaxM.
+constexpr uint64_t kAngularExactMaxM = 65536;
+uint64_t angular_thresholds(uint64_t m, double4* out);
+
+// Rows (global index list) gathered as doubles for a host fix-up.
+void launch_gather_rows_f64(const float* pts, const double* pts64, uint32_t d, const uint32_t* rows,
+                            uint32_t count, uint32_t row_base, double* out, cudaStream_t st);
 
 // Patch pid bits of key64 for rows listed in (rows, pids).
 void launch_patch_pid(uint64_t* key64, const uint32_t* rows, const uint32_t* pids, uint32_t count,

@@ -377,6 +377,45 @@ def test_angular_boundaries_vs_oracle(engine, m):
         assert np.array_equal(np.asarray(po), np.asarray(epo)), (m, d)
 
 
+@pytest.mark.parametrize("m", [2, 4])
+def test_angular_many_boundary_rows(engine, m):
+    """Integer rows put hundreds of thousands of angles exactly on a slice
+    boundary (x_i == x_j gives atan2 = pi/4): all of them are decided on the
+    device (no host fix-up, no cap). Partition ids vs the
+    reference itself, and a full run vs the reference."""
+    x = generate(5, 2_000_000, 5, 42)
+    cfg = SkyConfig.make(strategy=2, p=m ** 4, m=m, seed=1, filter=2, rep_q=5, merge=1, workers=8)
+    po, _ = engine.make_assignment(x, PartitionConfig(Strategy.Angular, p=m ** 4, m=m), False)
+    if O.ref_available():
+        epo, _ = O.oracle_assign(x, cfg, False, ref=True)
+        assert np.array_equal(np.asarray(po), np.asarray(epo))
+        exp = O.ref_run(x, cfg, False)
+    else:
+        exp = O.oracle_run(x, cfg, False)
+    r = engine.run(x, to_engine_config(cfg.as_dict()), False)
+    assert r.metrics.angular_host_fixups == 0
+    assert np.array_equal(r.skyline, exp["ids"])
+    check_metrics(r, exp, m)
+    assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist()
+
+
+def test_angular_libm_latitude_rows_vs_oracle(engine):
+    """k/7 lattice rows whose angle sits within one ulp of pi/4 (y = sqrt(x^2)
+    rounded, not equal to x): the reference's slice depends on the host
+    libm's rounding there, so those rows take the batched host fix-up."""
+    rng = np.random.default_rng(7)
+    x = (rng.integers(0, 8, (200_000, 3)) / 7).astype(np.float64)
+    for m in (2, 4):
+        cfg = SkyConfig.make(strategy=2, p=m ** 2, m=m, seed=1, filter=0, merge=1, workers=1)
+        epo, _ = O.oracle_assign(x.astype(np.float32), cfg, True)
+        po, _ = engine.make_assignment(x.astype(np.float32), PartitionConfig(Strategy.Angular, p=m ** 2, m=m))
+        assert np.array_equal(np.asarray(po), np.asarray(epo)), m
+        exp = O.oracle_run(x, cfg, True)
+        r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+        assert np.array_equal(r.skyline, exp["ids"]), m
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), m
+
+
 def test_stream_path_many_representatives(engine, monkeypatch):
     """Stream path with more representatives than its shared-memory
     reservation (256): the prefilter reads the rest from global memory."""
