@@ -125,7 +125,9 @@ __device__ __forceinline__ int cmp_tan(double y, double x, double th, double tl)
 // lies within the libm's 1-ulp latitude of a slice boundary.
 __device__ __forceinline__ uint32_t angular_slice_exact(double y, double x, const double4* __restrict__ thr,
                                                         uint32_t m, double c45, bool* amb) {
-    if (y == 0.0) return 0;  // atan2(+0, x >= 0) = +0
+    // y = sqrt(sum of squares) is +0 or positive; x >= 0 may be -0.0:
+    // atan2(+0, +0) = +0 (slice 0), atan2(+0, -0) = pi (2m, clamped to m - 1)
+    if (y == 0.0) return signbit(x) ? m - 1 : 0;
     double phi = -1.0;
     if (x == 0.0) {
         phi = 0x1.921fb54442d18p+0;  // atan2(y > 0, +0) = rn(pi/2)
