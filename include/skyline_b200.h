@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SKY_ABI_VERSION 2
+#define SKY_ABI_VERSION 3
 
 /* Return codes mirror the reference's exception classes (core.hpp:13-34). */
 typedef enum sky_status {
@@ -120,6 +120,11 @@ typedef struct sky_result {
     uint32_t stream_launches;
     double stream_kernel_ms;    /* summed CUDA-event time of those launches */
     uint64_t stream_bytes;      /* algorithmic bytes they move (reads + writes) */
+    /* multi-GPU (ABI v3) */
+    uint32_t world;             /* ranks that computed the result (1: one GPU) */
+    uint32_t sharded;           /* 1: rows sharded over the ranks (phase 1 per shard) */
+    uint64_t exchange_bytes;    /* bytes this rank sent to its peers */
+    uint64_t local_rows;        /* input rows this rank partitioned / filtered */
 } sky_result;
 
 typedef struct sky_ctx sky_ctx;
@@ -135,6 +140,34 @@ SKY_API void sky_ctx_destroy(sky_ctx* ctx);
  * replaced by NCCL over NVLink). */
 SKY_API int sky_nccl_unique_id(uint8_t* out, uint64_t size);
 SKY_API int sky_ctx_create_dist(int device, int rank, int world, const uint8_t* unique_id, sky_ctx** out);
+/* One process driving several GPUs: the reference's single run() call whose
+ * phases fan out over `workers` threads (engine.hpp:30-38,88; parallel.cpp:
+ * 11-43) becomes one host thread and one stream per GPU. Rank r runs on
+ * devices[r]; sky_run on the group shards the input rows over the ranks
+ * and returns the full result. Exchanges use NCCL (ncclCommInitAll) unless
+ * SKY_GROUP_LOOPBACK is set or a device repeats: then the ranks exchange by
+ * event-ordered device copies (every rank may share one GPU). */
+enum { SKY_GROUP_LOOPBACK = 1 };
+SKY_API int sky_ctx_create_group(const int* devices, int n, int flags, sky_ctx** out);
+/* n rank contexts (rank r on devices[r]) of ONE process that exchange by
+ * event-ordered device copies: each is used like a sky_ctx_create_dist
+ * context from its own host thread (sky_run / sky_run_shard called
+ * concurrently by the n threads). Devices may repeat. out[n]. */
+SKY_API int sky_ctx_create_peers(const int* devices, int n, sky_ctx** out);
+/* (rank, world) of a context; a group context reports (0, number of GPUs). */
+SKY_API int sky_ctx_world(const sky_ctx* ctx, int* rank, int* world);
+/* Take the sharded multi-rank path even on a one-rank context (1 = on).
+ * Results never depend on it; tests use it to run the exchange code on one
+ * GPU. */
+SKY_API int sky_ctx_set_sharded(sky_ctx* ctx, int on);
+/* Engine options, per context (defaults are the measured best; none changes
+ * a result): "stream" (-1 auto, 0 off, 1 on: the large-input path that
+ * skips the full partition sort), "host_merge" (1: host-planned all-pairs
+ * merge), "cap_sync" (-1 auto, 0/1: size the filtered set by the input /
+ * by the exact count), "sfs_tile", "sfs_chunk", "sfs_head", "merge_tile",
+ * "merge_head", "grain_items" (work granularity), "profile_host",
+ * "timeline" (diagnostics on stderr). SKY_E_CONFIG for an unknown name. */
+SKY_API int sky_ctx_set_option(sky_ctx* ctx, const char* name, int64_t value);
 SKY_API const char* sky_last_error(const sky_ctx* ctx);
 /* Optional external stream (cudaStream_t passed as void*); NULL restores the
  * context's own stream. */
@@ -154,6 +187,14 @@ SKY_API int sky_run(sky_ctx* ctx, const float* points, uint64_t n, uint32_t d,
  * dominance decision, partition id, sum and sort order that decides the
  * result is taken on the doubles (core.hpp:89-107, partition.cpp). */
 SKY_API int sky_run_f64(sky_ctx* ctx, const double* points, uint64_t n, uint32_t d,
+            int normalized, int points_on_device, const sky_config* cfg,
+            sky_result* out);
+/* skyline::run over a relation whose rows are sharded across the ranks of a
+ * distributed context (one process per GPU): this rank holds `n_local`
+ * consecutive rows; rank 0's rows come first, then rank 1's, ... (ids are
+ * positions in that concatenation). Every rank calls it; every rank
+ * receives the full result. On a one-rank context it is sky_run. */
+SKY_API int sky_run_shard(sky_ctx* ctx, const float* points, uint64_t n_local, uint32_t d,
             int normalized, int points_on_device, const sky_config* cfg,
             sky_result* out);
 SKY_API void sky_result_free(sky_result* r);

@@ -83,6 +83,10 @@ class SkyResult(C.Structure):
         ("stream_launches", C.c_uint32),
         ("stream_kernel_ms", C.c_double),
         ("stream_bytes", C.c_uint64),
+        ("world", C.c_uint32),
+        ("sharded", C.c_uint32),
+        ("exchange_bytes", C.c_uint64),
+        ("local_rows", C.c_uint64),
     ]
 
 
@@ -96,7 +100,11 @@ EXPORTED = [
     "sky_representatives", "sky_free", "sky_generate", "sky_plan_lpt",
     "sky_plan_split", "sky_plan_local_shards", "sky_plan_merge_shards", "sky_abi_version",
     "sky_generate_family", "sky_normalize", "sky_ingest_csv", "sky_write_csv", "sky_host_error",
+    "sky_ctx_create_group", "sky_ctx_world", "sky_ctx_set_sharded", "sky_run_shard", "sky_ctx_set_option",
+    "sky_ctx_create_peers",
 ]
+
+SKY_GROUP_LOOPBACK = 1
 
 _lib = None
 _u8p = C.POINTER(C.c_uint8)
@@ -120,6 +128,13 @@ def load():
     lib.sky_ctx_destroy.argtypes = [vp]
     lib.sky_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8), C.c_uint64]
     lib.sky_ctx_create_dist.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(vp)]
+    lib.sky_ctx_create_group.argtypes = [C.POINTER(C.c_int), C.c_int, C.c_int, C.POINTER(vp)]
+    lib.sky_ctx_create_peers.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
+    lib.sky_ctx_world.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    lib.sky_ctx_set_sharded.argtypes = [vp, C.c_int]
+    lib.sky_ctx_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
+    lib.sky_run_shard.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
+                                  C.POINTER(SkyConfig), C.POINTER(SkyResult)]
     lib.sky_last_error.argtypes = [vp]
     lib.sky_last_error.restype = C.c_char_p
     lib.sky_ctx_set_stream.argtypes = [vp, vp]

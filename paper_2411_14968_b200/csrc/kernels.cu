@@ -20,27 +20,49 @@ namespace sky {
 // Host-side caches for launch configuration queries (the dynamic shared
 // memory attribute and the occupancy of a kernel), so a run does not pay
 // for them on every launch.
+// Function attributes belong to the current device's context, so every cache
+// is keyed by the device as well (a process may drive several GPUs).
+static int current_device() {
+    int dev = 0;
+    SKY_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
 void ensure_smem_attr(const void* func, size_t smem) {
     static std::mutex mu;
-    static std::map<const void*, size_t> done;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    const int dev = current_device();
     // set even below 48 KB: static + dynamic shared memory past 48 KB needs it
     std::lock_guard<std::mutex> lk(mu);
-    size_t& cur = done[func];
+    size_t& cur = done[std::make_pair(dev, func)];
     if (cur >= smem) return;
     SKY_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cur = smem;
 }
 int occupancy_cached(const void* func, int threads, size_t smem) {
     static std::mutex mu;
-    static std::map<std::tuple<const void*, int, size_t>, int> cache;
+    static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+    const int dev = current_device();
     std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_tuple(func, threads, smem);
+    const auto key = std::make_tuple(dev, func, threads, smem);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     int per_sm = 0;
     SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem));
     cache[key] = per_sm;
     return per_sm;
+}
+
+int device_sm_count() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 0;
+    SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev] = sms;
+    return sms;
 }
 
 int padded_dim(uint32_t d) {
@@ -1038,11 +1060,7 @@ void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32
     k_cand_bucket<<<ceil_div(n, 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
     SKY_LAUNCH_CHECK();
     const uint32_t run_floats = std::min<uint32_t>(B * d, 16u * 1024);  // <= 64 KB of run coordinates
-    static bool attr = false;
-    if (!attr) {
-        SKY_CUDA(cudaFuncSetAttribute(k_bucket_pick, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        attr = true;
-    }
+    ensure_smem_attr((const void*)k_bucket_pick, 64 * 1024);
     k_bucket_pick<<<P, 256, run_floats * sizeof(float), st>>>(bkey, brow, cnt, B, pts, d, q, cand, run_floats);
     SKY_LAUNCH_CHECK();
 }
@@ -1605,13 +1623,7 @@ __global__ void __launch_bounds__(256) k_merge_runs(DevSet in, const uint32_t* _
 void launch_merge_runs(int D, const DevSet& in, const uint32_t* off, uint32_t P, DevSet out, cudaStream_t st,
                        const uint32_t* n_dev) {
     if (!in.n) return;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        SKY_CUDA(cudaGetDevice(&dev));
-        SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    const uint32_t grid = std::min<uint32_t>(ceil_div((uint64_t)in.n * 32, 256), (uint32_t)sms * 8);
+    const uint32_t grid = std::min<uint32_t>(ceil_div((uint64_t)in.n * 32, 256), (uint32_t)device_sm_count() * 8);
     SKY_DISPATCH_D(D, (k_merge_runs<DT><<<grid, 256, 0, st>>>(in, off, P, in.n, out, n_dev)));
     SKY_LAUNCH_CHECK();
 }

@@ -11,6 +11,7 @@ int padded_dim(uint32_t d);
 // cached cudaFuncSetAttribute(MaxDynamicSharedMemorySize) / occupancy query
 void ensure_smem_attr(const void* func, size_t smem);
 int occupancy_cached(const void* func, int threads, size_t smem);  // 0 if unsupported (d > 32)
+int device_sm_count();  // SMs of the current device (cached per device)
 
 // Point set on the device in dominance-friendly layout: AoS coords with
 // stride round4(D) floats (16-byte aligned rows), plus the 32-bit sort key

@@ -1084,13 +1084,9 @@ __global__ void __launch_bounds__(1024) k_small_skyline(const float4* __restrict
 
 template <int D, int K>
 void launch_k(const Relsky2Args& a, int sm_count, cudaStream_t st) {
-    static int per_sm = 0;
     const size_t smem = sizeof(Relsky3Smem<D, K>);
-    if (!per_sm) {
-        SKY_CUDA(cudaFuncSetAttribute(k_relsky3<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_relsky3<D, K>, RS3_THREADS, smem));
-        if (per_sm < 1) per_sm = 1;
-    }
+    ensure_smem_attr((const void*)k_relsky3<D, K>, smem);
+    const int per_sm = std::max(1, occupancy_cached((const void*)k_relsky3<D, K>, RS3_THREADS, smem));
     const uint32_t grid = (uint32_t)std::min<uint64_t>(a.n_items, (uint64_t)per_sm * sm_count);
     k_relsky3<D, K><<<grid, RS3_THREADS, smem, st>>>(a);
     SKY_LAUNCH_CHECK();
@@ -1136,8 +1132,7 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
             // many representatives, input in L2: sorted positions (a warp's
             // rows have close keys, so its key bound cuts early), flags in place
             ensure_smem_attr((const void*)k_prefilter<DT, true, true>, smem);
-            PrefilterAppend rg;
-            if (const char* e = std::getenv("SKY_PF_REGROUP")) rg.regroup = (uint32_t)std::strtoul(e, nullptr, 10);
+            PrefilterAppend rg;  // regroup point 64 (16-128 measured within noise on config 2)
             k_prefilter<DT, true, true><<<ceil_div(n, 256), 256, smem, st>>>(
                 pts, d, n, idx, reinterpret_cast<const float4*>(rep_xyz), rep_key, rep_qc, rep_id, nrep, nrep_dev, thr,
                 dead_pos, tests, x64, rg);
@@ -1177,12 +1172,7 @@ bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, co
     auto go = [&](auto kern, const uint2* qc, const float* th) {
         ensure_smem_attr((const void*)kern, smem);
         const int per_sm = occupancy_cached((const void*)kern, (int)kStreamRows, smem);
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            SKY_CUDA(cudaGetDevice(&dev));
-            SKY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        }
+        const int sms = device_sm_count();
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows),
                                                                        (uint32_t)std::max(1, per_sm) * sms));
         kern<<<grid, kStreamRows, smem, st>>>(pts, d, n, nullptr, reinterpret_cast<const float4*>(rep_xyz), rep_key,

@@ -165,6 +165,11 @@ class PhaseMetrics:
     stream_kernel_ms: float = 0.0
     stream_bytes: int = 0
     dom_exact_checks: int = 0
+    # multi-GPU
+    world: int = 1
+    sharded: bool = False
+    exchange_bytes: int = 0
+    local_rows: int = 0
 
     @property
     def tests_total(self) -> int:
@@ -217,6 +222,73 @@ class Engine:
         _raise(rc, "sky_ctx_create failed (is a CUDA device visible?)")
         self._h = h
         self.device = device
+
+    @classmethod
+    def group(cls, devices, loopback: bool = False) -> "Engine":
+        """One process driving several GPUs (rank r on devices[r]): run()
+        shards the rows over the ranks and returns the whole result. NCCL
+        between distinct devices; `loopback` (implied when a device repeats)
+        exchanges by event-ordered device copies, so every rank may share
+        one GPU."""
+        self = cls.__new__(cls)
+        self._lib = abi.load()
+        devs = [int(x) for x in devices]
+        arr = (C.c_int * len(devs))(*devs)
+        h = C.c_void_p()
+        rc = self._lib.sky_ctx_create_group(arr, len(devs), abi.SKY_GROUP_LOOPBACK if loopback else 0, C.byref(h))
+        _raise(rc, "sky_ctx_create_group failed")
+        self._h = h
+        self.device = devs[0]
+        return self
+
+    @classmethod
+    def peers(cls, devices) -> list:
+        """Rank engines of one process that exchange through device copies;
+        each is used like Engine.distributed from its own thread (run /
+        run_shard called concurrently). Devices may repeat."""
+        lib = abi.load()
+        devs = [int(x) for x in devices]
+        arr = (C.c_int * len(devs))(*devs)
+        hs = (C.c_void_p * len(devs))()
+        _raise(lib.sky_ctx_create_peers(arr, len(devs), hs), "sky_ctx_create_peers failed")
+        out = []
+        for r, dev in enumerate(devs):
+            e = cls.__new__(cls)
+            e._lib = lib
+            e._h = C.c_void_p(hs[r])
+            e.device = dev
+            out.append(e)
+        return out
+
+    @property
+    def world(self) -> int:
+        r, w = C.c_int(0), C.c_int(0)
+        self._lib.sky_ctx_world(self._h, C.byref(r), C.byref(w))
+        return int(w.value)
+
+    @property
+    def rank(self) -> int:
+        r, w = C.c_int(0), C.c_int(0)
+        self._lib.sky_ctx_world(self._h, C.byref(r), C.byref(w))
+        return int(r.value)
+
+    def set_option(self, name: str, value: int):
+        """Engine option (sky_ctx_set_option): stream, host_merge, cap_sync,
+        sfs_tile, sfs_chunk, sfs_head, merge_tile, merge_head, grain_items,
+        profile_host, timeline."""
+        self._err(self._lib.sky_ctx_set_option(self._h, name.encode(), int(value)))
+
+    DEFAULT_OPTIONS = {"stream": -1, "host_merge": 0, "cap_sync": -1, "sfs_tile": 0, "sfs_chunk": 2048,
+                       "sfs_head": 2048, "merge_tile": 0, "merge_head": 4096, "grain_items": 4, "profile_host": 0,
+                       "timeline": 0}
+
+    def reset_options(self):
+        for k, v in self.DEFAULT_OPTIONS.items():
+            self.set_option(k, v)
+
+    def set_sharded(self, on: bool = True):
+        """Take the sharded multi-rank path even on one rank (tests)."""
+        self._err(self._lib.sky_ctx_set_sharded(self._h, int(bool(on))))
 
     @classmethod
     def distributed(cls, device: int, rank: int, world: int, unique_id: bytes) -> "Engine":
@@ -277,6 +349,27 @@ class Engine:
             fn = self._lib.sky_run_f64 if a.dtype == np.float64 else self._lib.sky_run
             rc = fn(self._h, a.ctypes.data_as(C.c_void_p), n, d, int(normalized), 0, C.byref(cfg), C.byref(res))
         self._err(rc)
+        return self._result(res, config)
+
+    def run_shard(self, points, config: EngineConfig, normalized: bool = True, *, device_ptr: Optional[int] = None,
+                  n: Optional[int] = None, d: Optional[int] = None) -> RunResult:
+        """skyline::run over rows sharded across the ranks of a distributed
+        engine (sky_run_shard): `points` are this rank's consecutive rows
+        (rank 0's first); every rank gets the whole result."""
+        cfg = config.to_c()
+        res = abi.SkyResult()
+        if device_ptr is not None:
+            rc = self._lib.sky_run_shard(self._h, C.c_void_p(device_ptr), n, d, int(normalized), 1, C.byref(cfg),
+                                         C.byref(res))
+        else:
+            a = _as_points(points)
+            n, d = a.shape
+            rc = self._lib.sky_run_shard(self._h, a.ctypes.data_as(C.c_void_p), n, d, int(normalized), 0,
+                                         C.byref(cfg), C.byref(res))
+        self._err(rc)
+        return self._result(res, config)
+
+    def _result(self, res, config) -> RunResult:
         try:
             # memmove instead of np.ctypeslib.as_array (~10 us of array-interface
             # setup per call, inside the caller's timed region)
@@ -300,7 +393,8 @@ class Engine:
                 dom_launches=int(res.dom_launches), dom_kernel_ms=float(res.dom_kernel_ms),
                 dom_tests=int(res.dom_tests), dom_exact_checks=int(res.dom_exact_checks),
                 stream_launches=int(res.stream_launches), stream_kernel_ms=float(res.stream_kernel_ms),
-                stream_bytes=int(res.stream_bytes))
+                stream_bytes=int(res.stream_bytes), world=int(res.world) or 1, sharded=bool(res.sharded),
+                exchange_bytes=int(res.exchange_bytes), local_rows=int(res.local_rows))
             return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
         finally:
             self._lib.sky_result_free(C.byref(res))

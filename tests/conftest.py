@@ -31,3 +31,13 @@ def golden():
     g["plane64_arrays"] = np.load(os.path.join(here, "plane64.npz"))
     g["config_arrays"] = np.load(os.path.join(here, "configs.npz"))
     return g
+
+
+@pytest.fixture
+def options(engine):
+    """Set engine options (sky_ctx_set_option) for one test; defaults after."""
+    def set_(**kw):
+        for k, v in kw.items():
+            engine.set_option(k, v)
+    yield set_
+    engine.reset_options()

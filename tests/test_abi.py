@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(abi.EXPORTED), declared ^ set(abi.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sky_abi_version() == 2
+    assert lib.sky_abi_version() == 3
 
 
 def test_config_struct_layout_matches_header():

@@ -309,35 +309,37 @@ def test_distributed_context_single_rank():
 
 
 @pytest.mark.parametrize("stream", ["1", "0"])
-def test_stream_path_forced(engine, golden, monkeypatch, stream):
+def test_stream_path_forced(engine, golden, options, stream):
     """The stream path (sorted representatives from per-partition candidate
     buckets, row-order prefilter that appends survivor keys, survivors-only
     sort; engine.cu `stream`) and the sorted path, each forced at sizes the
     oracle finishes quickly: the golden plane, the reduced BASELINE configs
     and random configurations."""
-    monkeypatch.setenv("SKY_STREAM", stream)
+    options(stream=int(stream))
     test_plane_matches_reference(engine, golden, LocalAlgo.SFS)
     for idx in (2, 3, 5):
         test_baseline_configs_reduced(engine, golden, idx)
     test_random_configs_vs_oracle(engine)
 
 
-@pytest.mark.parametrize("mode", ["SKY_CAP_SYNC", "SKY_NO_CAP_SYNC"])
-def test_filtered_capacity_modes(engine, golden, monkeypatch, mode):
+@pytest.mark.parametrize("cap_sync", [1, 0])
+def test_filtered_capacity_modes(engine, golden, options, cap_sync):
     """Both sizings of the filtered set (engine.cu kExactCapRows): the exact
     count read back before the local phase, and the input's size as capacity
-    with every later pass bounded by the device count."""
-    monkeypatch.setenv(mode, "1")
+    with every later pass bounded by the device count; SFS and BNL (small
+    window: overflow passes) local phases."""
+    options(cap_sync=cap_sync)
     test_plane_matches_reference(engine, golden, LocalAlgo.SFS)
-    for idx in (1, 2, 3, 5):
+    test_plane_matches_reference(engine, golden, LocalAlgo.BNL)
+    for idx in (1, 2, 3, 4, 5):
         test_baseline_configs_reduced(engine, golden, idx)
     test_random_configs_vs_oracle(engine)
 
 
-def test_stream_path_bucket_overflow(engine, monkeypatch):
+def test_stream_path_bucket_overflow(engine, options):
     """Candidate buckets that fill up (duplicate-heavy rows, rows sorted by
     partition) fall back to the sorted path with identical results."""
-    monkeypatch.setenv("SKY_STREAM", "1")
+    options(stream=1)
     rng = np.random.default_rng(3)
     cases = [
         np.zeros((6000, 3), np.float32),                                   # every row identical
@@ -416,10 +418,10 @@ def test_angular_libm_latitude_rows_vs_oracle(engine):
         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), m
 
 
-def test_stream_path_many_representatives(engine, monkeypatch):
+def test_stream_path_many_representatives(engine, options):
     """Stream path with more representatives than its shared-memory
     reservation (256): the prefilter reads the rest from global memory."""
-    monkeypatch.setenv("SKY_STREAM", "1")
+    options(stream=1)
     for d, m, q in ((7, 2, 8), (5, 3, 6)):
         x = generate(2, 60000, d, 5)
         cfg = SkyConfig.make(strategy=2, p=m ** (d - 1), m=m, seed=3, filter=2, rep_q=q, merge=1, workers=1)
@@ -432,14 +434,11 @@ def test_stream_path_many_representatives(engine, monkeypatch):
 
 
 @pytest.mark.parametrize("host_merge", ["0", "1"])
-def test_device_merge_vs_oracle(engine, monkeypatch, host_merge):
+def test_device_merge_vs_oracle(engine, options, host_merge):
     """The all-pairs merge planned on the device with the ids written to
     mapped host memory (one round trip per step) and the host-planned merge,
     on inputs whose filtered set is large enough to take the device path."""
-    if host_merge == "1":
-        monkeypatch.setenv("SKY_HOST_MERGE", "1")
-    else:
-        monkeypatch.delenv("SKY_HOST_MERGE", raising=False)
+    options(host_merge=int(host_merge))
     for strat, p, merge, seed in ((2, 64, 1, 1), (0, 16, 1, 2), (0, 8, 0, 3)):
         x = generate(2, 150000, 6, seed)
         cfg = SkyConfig.make(strategy=strat, p=p, seed=seed, filter=2, rep_q=8, merge=merge, workers=1)
