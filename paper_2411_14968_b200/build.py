@@ -24,8 +24,30 @@ CLI_SRC = os.path.join(ROOT, "tools", "skyline_cli.cpp")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    """The NCCL that torch loads (the nvidia-nccl wheel), so the process holds
+    one libnccl.so.2 whichever of torch and this library loads first; the
+    system NCCL otherwise."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for p in (spec.submodule_search_locations or []) if spec else []:
+            if os.path.exists(os.path.join(p, "lib", "libnccl.so.2")) and os.path.exists(
+                    os.path.join(p, "include", "nccl.h")):
+                return p
+    except (ImportError, ValueError):
+        pass
+    return None
+
+
+NCCL_DIR = _nccl_dir()
+NCCL_INC = ["-I", os.path.join(NCCL_DIR, "include")] if NCCL_DIR else []
+NCCL_LINK = (["-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker",
+              "-rpath=" + os.path.join(NCCL_DIR, "lib")] if NCCL_DIR else ["-lnccl"])
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-          "-I", os.path.join(ROOT, "include")]
+          "-I", os.path.join(ROOT, "include")] + NCCL_INC
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcudafe", "--diag_suppress=177", "-diag-suppress", "1444"]
 SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "shard.cu", "comm.cpp", "host.cpp", "dataio.cpp", "mtjump.cpp", "angular.cpp"]
@@ -51,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             flags = CU_FLAGS if s.endswith(".cu") else ARCH + COMMON + ["-x", "cu"]
             if s.endswith(".cpp"):
                 flags = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-                         "-I", os.path.join(ROOT, "include")]
+                         "-I", os.path.join(ROOT, "include")] + NCCL_INC
             jobs.append((s, [NVCC, *flags, "-c", src, "-o", obj]))
     # the translation units compile independently: run them side by side
     from concurrent.futures import ThreadPoolExecutor
@@ -64,7 +86,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
     if force or _newer(objs, OUT):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-lnccl", "-lpthread", "-lquadmath"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", *NCCL_LINK, "-lpthread", "-lquadmath"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -333,6 +333,8 @@ class Runner {
     // Every API call ends with the stream drained (its results are read on
     // the host), so a new Runner may recycle the staging and event pools.
     Runner(sky_ctx* c) : c_(c), st_(c->stream) {
+        prof_ = c->opt.profile_host != 0;
+        tl_ = c->opt.timeline != 0;
         c->stage_cur = c->stage_off = 0;
         c->dom_used = 0;
         c->hbm_used = 0;
@@ -380,14 +382,14 @@ class Runner {
             std::fprintf(stderr, "  sync #%d at %.3f ms\n", ++n_sync_, t);
         }
     }
-    bool prof_ = c_->opt.profile_host != 0;
+    bool prof_ = false;  // sky_options::profile_host (set in the constructor)
     int n_sync_ = 0;
     std::chrono::steady_clock::time_point t_start_ = std::chrono::steady_clock::now();
     void count(int k = 1, int line = __builtin_LINE()) {
         c_->launches += k;
         if (tl_) mark(line);
     }
-    bool tl_ = c_->opt.timeline != 0;
+    bool tl_ = false;  // sky_options::timeline (set in the constructor)
     std::vector<std::pair<int, double>> tl_marks_;
     void mark(int line) {
         auto& e = c_->tl_ev;
