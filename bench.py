@@ -307,7 +307,11 @@ def run_ours(args):
 
     w = make_config(args.config, args.n)
     x = generate(w.kind, w.n, w.d, 42)
-    x_pin = torch.from_numpy(x).pin_memory()
+    # multi-GPU: rank r holds rows [N*r/W, N*(r+1)/W) (its shard, in HBM for
+    # `value`, in pinned host memory for `e2e`) and calls sky_run_shard
+    r0, r1 = w.n * rank // world, w.n * (rank + 1) // world
+    x_mine = x[r0:r1] if world > 1 else x
+    x_pin = torch.from_numpy(np.ascontiguousarray(x_mine)).pin_memory()
     x_host = x_pin.numpy()  # pinned view
     x_dev = x_pin.to(f"cuda:{local}")
     if world > 1:
@@ -322,11 +326,16 @@ def run_ours(args):
     eng.set_stream(stream.cuda_stream)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     n, d = x.shape
+    n_mine = x_mine.shape[0]
 
     def step_dev():
+        if world > 1:
+            return eng.run_shard(None, w.config, w.normalized, device_ptr=x_dev.data_ptr(), n=n_mine, d=d)
         return eng.run(None, w.config, w.normalized, device_ptr=x_dev.data_ptr(), n=n, d=d)
 
     def step_e2e():
+        if world > 1:
+            return eng.run_shard(x_host, w.config, w.normalized)
         return eng.run(x_host, w.config, w.normalized)
 
     def barrier():
@@ -382,6 +391,10 @@ def run_ours(args):
     dom_ms = statistics.mean(rr.metrics.dom_kernel_ms for rr in dev_res)
     dom_tests = statistics.mean(rr.metrics.dom_tests for rr in dev_res)
     launches = sum(rr.metrics.kernel_launches for rr in dev_res)
+    if world > 1:
+        t = torch.tensor([launches], dtype=torch.int64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        launches = int(t[0])
 
     peaks = measured_peaks()
     props = torch.cuda.get_device_properties(local)
@@ -395,7 +408,11 @@ def run_ours(args):
     achieved = tests_s * d / 1e9  # Gcompare/s
     peak = n_sm * FP32_COMPARES_PER_CLK_PER_SM * sm_max * 1e6 / 1e9
     per_clk = PACKED_TESTS_PER_CLK_PER_SM if d <= 16 else FP32_COMPARES_PER_CLK_PER_SM / d
-    ipeak = n_sm * per_clk * sm_max * 1e6
+    ipeak_model = n_sm * per_clk * sm_max * 1e6
+    # measured: the dominance core's packed-code test loop alone on every SM
+    # (sky_issue_peak, k_issue_peak), outside the timed region
+    ipeak_meas = eng.issue_peak(d) if d <= 16 else None
+    ipeak = ipeak_meas or ipeak_model
     traffic, traffic_src = ncu_traffic(f"c{args.config}")
     roofline = {
         "bound": "alu", "kernel": "k_relsky3 + k_bnl2 (dominance tests)", "achieved": achieved, "peak": peak,
@@ -407,6 +424,9 @@ def run_ours(args):
         "packed_issue": {
             "achieved_gtest_s": tests_s / 1e9, "peak_gtest_s": ipeak / 1e9,
             "frac": tests_s / ipeak if ipeak else None,
+            "peak_source": ("measured: k_issue_peak (the packed-code test loop of k_relsky3 alone, every SM, "
+                            "best of K in {4,8} x 2..8 CTAs/SM; sky_issue_peak)" if ipeak_meas else "model"),
+            "model_peak_gtest_s": ipeak_model / 1e9,
             "model": ("d<=16: 2 IMAD (fma pipe) + 1 LOP3 + 1/2 VIMNMX3 (alu pipe) per test, fma/alu pipes 2 cyc "
                       "per warp instruction -> 32 tests/clk/SM" if d <= 16 else
                       f"d>16: {d} FP32 compares per test -> 64/{d} tests/clk/SM"),
@@ -448,9 +468,9 @@ def run_ours(args):
         "data": "synthetic (sky_generate, seed 42)",
         "config": bench_config(w),
         "effective_p": r.effective_p,
-        "parallelism": (f"{world} ranks: replicated partition/filter, partition-sharded local phase, "
-                        "candidate-sharded merge, NCCL all-gather of locals and survivors")
-        if world > 1 else "single-gpu",
+        "parallelism": (f"{world} ranks: rows sharded (partition + representative prefilter per shard), "
+                        "survivors routed to partition owners (NCCL all-to-all), local skylines all-gathered, "
+                        "candidate-sharded merge") if world > 1 else "single-gpu",
         "tests_per_s": tests_per_step * args.steps * jobs / (total_dev / 1e3),
         "skyline_size": int(r.skyline.size), "union_size": m.union_size, "filtered_count": m.filtered_count,
         "phase_ms": {"partition": m.partition_ms, "local": m.local_ms, "merge": m.merge_ms},
@@ -463,8 +483,13 @@ def run_ours(args):
     if total_e2e is not None:
         e0 = e2e_res[-1]
         assert np.array_equal(e0.skyline, r.skyline)
+        h2d, d2h = int(e0.metrics.h2d_bytes), int(e0.metrics.d2h_bytes)
+        if world > 1:  # every rank copies its own shard in and the ids out
+            t = torch.tensor([h2d, d2h], dtype=torch.int64, device=f"cuda:{local}")
+            dist.all_reduce(t)
+            h2d, d2h = int(t[0]), int(t[1])
         line["e2e"] = {"value": w.n * args.steps * jobs / (total_e2e / 1e3), "unit": UNIT,
-                       "h2d_bytes_per_step": int(e0.metrics.h2d_bytes), "d2h_bytes_per_step": int(e0.metrics.d2h_bytes),
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "ms_per_step": total_e2e / args.steps}
     if rank == 0 and not args.no_cpu_baseline:
         import oracle

@@ -272,6 +272,16 @@ SKY_API int sky_plan_local_shards(const uint32_t* off, uint64_t P, int world, ui
 SKY_API int sky_plan_merge_shards(const uint32_t* offu, uint64_t P, int world, const sky_config* cfg,
                                   uint32_t d, uint64_t m, uint32_t* bounds);
 
+/* Measured issue peak of the dominance core: the packed-code test loop of
+ * the merge/SFS kernel alone (codes in registers and shared memory, 4
+ * comparators x K candidates per step, no exit) on every SM of the
+ * context's device: K candidates per thread (1, 2, 4, 8), ctas_per_sm CTAs
+ * of 256 threads per SM, `iters` passes over 32 comparators per thread.
+ * k == 0: the best over K in {4, 8} and 2..8 CTAs per SM. *tests_per_s:
+ * pair tests per second (the dominance roofline denominator); d <= 16. */
+SKY_API int sky_issue_peak(sky_ctx* ctx, uint32_t d, int k, int ctas_per_sm, uint32_t iters,
+                           double* tests_per_s);
+
 SKY_API int sky_abi_version(void);
 
 #ifdef __cplusplus

@@ -1238,6 +1238,27 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
 
 void sky_free(void* p) { std::free(p); }
 
+int sky_issue_peak(sky_ctx* c, uint32_t d, int k, int ctas_per_sm, uint32_t iters, double* tests_per_s) {
+    c = single_gpu(c);
+    return guarded(c, [&] {
+        const int D = padded_dim(d);
+        if (!D || D > 16) throw Error(SKY_E_DIMENSION, "the packed-code core covers d <= 16");
+        unsigned long long* sink = static_cast<unsigned long long*>(c->dev.get(S_MISC, 64 * sizeof(uint32_t)));
+        if (k > 0) {
+            if (ctas_per_sm < 1 || ctas_per_sm > 8 || iters < 1) throw Error(SKY_E_CONFIG, "bad microbenchmark shape");
+            *tests_per_s = measure_issue_peak(D, k, ctas_per_sm, iters, c->sm_count, c->stream, sink);
+            return;
+        }
+        double best = 0.0;
+        for (int K : {4, 8})
+            for (int bps : {2, 4, 8}) {
+                const uint32_t iters = (uint32_t)(40000 / (K / 4) / (bps / 2));
+                best = std::max(best, measure_issue_peak(D, K, bps, iters, c->sm_count, c->stream, sink));
+            }
+        *tests_per_s = best;
+    });
+}
+
 int sky_plan_local_shards(const uint32_t* off, uint64_t P, int world, uint32_t* bounds) {
     return guarded(nullptr, [&] {
         if (world < 1) throw Error(SKY_E_CONFIG, "world must be >= 1");

@@ -255,6 +255,9 @@ struct Relsky2Args {
 };
 // tile = candidates per item (<= 32 * 8, one warp); picks K from it.
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);
+// tests/s of the packed-code test loop alone (k_issue_peak) on a full grid
+double measure_issue_peak(int D, int K, int blocks_per_sm, uint32_t iters, int sm_count, cudaStream_t st,
+                          unsigned long long* sink);
 // Device-side planning. A job = candidates [cb, ce) of a candidate list x one
 // comparator range [lo, hi) (sorted by key). Jobs come from device offsets;
 // they expand into direct items: tiles of `tile` candidates x chunks of the

@@ -1546,4 +1546,88 @@ void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStr
     }
 }
 
+// ------------------------------------------------- issue-rate microbenchmark
+// The packed-code test loop of k_relsky3 alone: K candidates' codes in
+// registers, a warp's 32 comparator codes in shared memory read as uint4
+// pairs (ld.shared.v4, as the kernel's double buffer does), 4 comparators x K
+// candidates per step folded by VIMNMX3 into one branch that never fires.
+// Its tests/s with every SM busy is the measured issue peak of the dominance
+// core's instruction mix (the roofline denominator in bench.py).
+__device__ __forceinline__ uint4 lds128v(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+template <int D, int K>
+__global__ void __launch_bounds__(256) k_issue_peak(uint32_t iters, uint32_t seed, unsigned long long* sink) {
+    constexpr uint32_t G = CodeLayout<D>::G;
+    constexpr uint32_t GA = G | 0x80000000u;
+    __shared__ __align__(16) uint2 code[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // never-pass comparators (word 1 borrows out of bit 31), unknown to the compiler
+    code[warp][lane] = make_uint2(seed * (uint32_t)(lane + 1), 0x80000000u | (seed & 1u));
+    __syncwarp();
+    uint32_t T[K][2];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        T[k][0] = (seed ^ (threadIdx.x * 977u + k)) | G | CodeLayout<D>::ALIVE;
+        T[k][1] = (seed * 31u + threadIdx.x + k) | G | 0x80000000u;
+    }
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(&code[warp][0]);
+    uint32_t hits = 0;
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (uint32_t i = 0; i < 32; i += 4) {
+            // volatile loads: ptxas may not keep one iteration's codes for the next
+            const uint4 c01 = lds128v(base + i * 8), c23 = lds128v(base + i * 8 + 16);
+            const uint2 q[4] = {make_uint2(c01.x, c01.y), make_uint2(c01.z, c01.w), make_uint2(c23.x, c23.y),
+                                make_uint2(c23.z, c23.w)};
+            uint32_t h[4 * K];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int k = 0; k < K; ++k) h[c * K + k] = coarse_hit<G>(T[k], q[c]);
+            if (max_fold<4 * K>(h) == GA) ++hits;
+        }
+    }
+    if (hits) atomicAdd(sink, (unsigned long long)hits);
+}
+
+template <int D, int K>
+double issue_peak_impl(int sm_count, uint32_t iters, int blocks_per_sm, cudaStream_t st, unsigned long long* sink) {
+    const uint32_t grid = (uint32_t)(sm_count * blocks_per_sm);
+    k_issue_peak<D, K><<<grid, 256, 0, st>>>(16, 12345u, sink);  // warm-up
+    SKY_LAUNCH_CHECK();
+    cudaEvent_t e0, e1;
+    SKY_CUDA(cudaEventCreate(&e0));
+    SKY_CUDA(cudaEventCreate(&e1));
+    SKY_CUDA(cudaEventRecord(e0, st));
+    k_issue_peak<D, K><<<grid, 256, 0, st>>>(iters, 12345u, sink);
+    SKY_LAUNCH_CHECK();
+    SKY_CUDA(cudaEventRecord(e1, st));
+    SKY_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double tests = (double)grid * 256.0 * iters * 32.0 * K;
+    return tests / (ms / 1e3);
+}
+
+double measure_issue_peak(int D, int K, int blocks_per_sm, uint32_t iters, int sm_count, cudaStream_t st,
+                          unsigned long long* sink) {
+    double r = 0.0;
+#define SKY_IP(KK) SKY_DISPATCH_D16(D, (r = issue_peak_impl<DT, KK>(sm_count, iters, blocks_per_sm, st, sink)))
+    if (K <= 1) { SKY_IP(1); }
+    else if (K <= 2) { SKY_IP(2); }
+    else if (K <= 4) { SKY_IP(4); }
+    else { SKY_IP(8); }
+#undef SKY_IP
+    return r;
+}
+
 }  // namespace sky

@@ -331,12 +331,21 @@ void run_sharded(sky_ctx* c, const float* src, uint32_t nl, uint32_t row0, const
             uint32_t* h = R.pin<uint32_t>(P_SH_RUNS, 2 * (size_t)nruns);
             SKY_CUDA(cudaMemcpyAsync(h, runs, 2 * (size_t)nruns * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
             R.sync();
+            // the kernel lists the runs in atomic order: sort them, so every
+            // rank lays out the run table (assembled by an all-reduce) alike
+            std::vector<uint2> rl(nruns);
+            for (uint32_t k = 0; k < nruns; ++k) rl[k] = make_uint2(h[2 * k], h[2 * k + 1]);
+            std::sort(rl.begin(), rl.end(), [](const uint2& a, const uint2& b) { return a.x < b.x; });
+            uint32_t* hs = R.stage<uint32_t>(2 * (size_t)nruns);
             for (uint32_t k = 0; k < nruns; ++k) {
-                const uint32_t L = h[2 * k + 1] - h[2 * k];
+                hs[2 * k] = rl[k].x;
+                hs[2 * k + 1] = rl[k].y;
+                const uint32_t L = rl[k].y - rl[k].x;
                 runb[k + 1] = runb[k] + L;
                 cost += (uint64_t)L * L;
                 max_len = std::max(max_len, L);
             }
+            SKY_CUDA(cudaMemcpyAsync(runs, hs, 2 * (size_t)nruns * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
         }
         // every rank sees the same runs: the same decision everywhere
         if (cost > (uint64_t)1e9) throw ReplicatePhase1{};

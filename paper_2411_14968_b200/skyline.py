@@ -286,6 +286,14 @@ class Engine:
         for k, v in self.DEFAULT_OPTIONS.items():
             self.set_option(k, v)
 
+    def issue_peak(self, d: int, k: int = 0, ctas_per_sm: int = 2, iters: int = 20000) -> float:
+        """Measured pair tests/s of the dominance core's packed-code loop on
+        every SM (sky_issue_peak): the dominance roofline denominator (k = 0:
+        the best over the kernel's shapes)."""
+        v = C.c_double(0.0)
+        self._err(self._lib.sky_issue_peak(self._h, int(d), int(k), int(ctas_per_sm), int(iters), C.byref(v)))
+        return float(v.value)
+
     def set_sharded(self, on: bool = True):
         """Take the sharded multi-rank path even on one rank (tests)."""
         self._err(self._lib.sky_ctx_set_sharded(self._h, int(bool(on))))

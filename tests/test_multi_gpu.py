@@ -229,3 +229,37 @@ def test_single_rank_forced_sharded(engine):
             same(e.run(x, cfg, True), O.oracle_run(x, cfg.to_c(), True), cfg.partition.strategy.name)
     finally:
         e.close()
+
+
+@pytest.mark.parametrize("i", [1, 2, 3, 4, 5])
+def test_full_size_group_matches_reference(i):
+    """Full BASELINE sizes through two sharded loopback ranks on the one GPU:
+    the reference's own result (tests/golden/full, from oracle/_ref)."""
+    import hashlib
+
+    from test_full_size import _check, load
+    g, ids = load(i)
+    w = make_config(i)
+    x = generate(w.kind, w.n, w.d, 42)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == g["input_sha256"]
+    e = Engine.group([0, 0], loopback=True)
+    try:
+        r = e.run(x, w.config, w.normalized)
+        assert r.metrics.sharded and r.metrics.world == 2
+        _check(r, g, ids, f"c{i} W=2")
+    finally:
+        e.close()
+
+
+def test_group_sliced_many_tie_runs(group):
+    """Sliced partitions whose boundaries fall inside many tie runs of the
+    slice attribute (the run table is laid out identically on every rank,
+    whatever order the device lists the runs in)."""
+    rng = np.random.default_rng(21)
+    for it in range(3):
+        x = rng.random((20000, 4), dtype=np.float32)
+        x[:, 0] = (rng.integers(0, 40, 20000) / 39).astype(np.float32)
+        for p, filt in ((64, FilterKind.Representative), (127, FilterKind.None_)):
+            cfg = EngineConfig(partition=PartitionConfig(Strategy.Sliced, p=p), filter=filt, rep_q=3,
+                               merge=MergeKind.NoSeq)
+            same(group.run(x, cfg, True), O.oracle_run(x, cfg.to_c(), True), (it, p))
