@@ -11,6 +11,14 @@
 // Any finite double coordinates: rows that are all float32 values go through
 // sky_run, others through sky_run_f64 (FP64 decisions, identical results).
 // d <= 32 and one sky_ctx per thread.
+//
+// Several GPUs from one reference thread: Context::devices({0, 1, ...}) (or
+// Context::first(n)) makes a group context; run(ctx, dataset, config) then
+// shards the rows over the GPUs (one host thread and stream per GPU inside
+// the library, NCCL between them) and returns the same RunResult. The
+// reference's EngineConfig::workers fans out threads (engine.hpp:30-38);
+// Context::for_workers(config.workers) maps it onto min(workers, visible
+// GPUs) devices.
 #pragma once
 
 #include <cmath>
@@ -42,9 +50,37 @@ inline void throw_status(int rc, const char* msg) {
 struct Context {
     sky_ctx* ctx = nullptr;
     explicit Context(int device = 0) { throw_status(sky_ctx_create(device, &ctx), "sky_ctx_create failed"); }
+    // one process, several GPUs (rank r on devices[r]); flags: SKY_GROUP_LOOPBACK
+    static std::unique_ptr<Context> devices(const std::vector<int>& devs, int flags = 0) {
+        std::unique_ptr<Context> c(new Context(nullptr));
+        throw_status(sky_ctx_create_group(devs.data(), static_cast<int>(devs.size()), flags, &c->ctx),
+                     "sky_ctx_create_group failed");
+        return c;
+    }
+    // devices 0..n-1
+    static std::unique_ptr<Context> first(int n) {
+        std::vector<int> devs(n > 0 ? n : 1);
+        for (size_t i = 0; i < devs.size(); ++i) devs[i] = static_cast<int>(i);
+        return devs.size() == 1 ? std::unique_ptr<Context>(new Context(0)) : devices(devs);
+    }
+    // EngineConfig::workers -> min(workers, visible GPUs) devices
+    static std::unique_ptr<Context> for_workers(size_t workers) {
+        int visible = sky_device_count();
+        if (visible < 1) visible = 1;
+        const size_t n = workers < 1 ? 1 : (workers < static_cast<size_t>(visible) ? workers : visible);
+        return first(static_cast<int>(n));
+    }
+    int world() const {
+        int r = 0, w = 1;
+        sky_ctx_world(ctx, &r, &w);
+        return w;
+    }
     ~Context() { sky_ctx_destroy(ctx); }
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
+
+   private:
+    explicit Context(std::nullptr_t) {}
 };
 
 inline sky_config to_sky(const EngineConfig& e) {

@@ -154,6 +154,8 @@ SKY_API int sky_ctx_create_group(const int* devices, int n, int flags, sky_ctx**
  * context from its own host thread (sky_run / sky_run_shard called
  * concurrently by the n threads). Devices may repeat. out[n]. */
 SKY_API int sky_ctx_create_peers(const int* devices, int n, sky_ctx** out);
+/* CUDA devices visible to this process (0 when none). */
+SKY_API int sky_device_count(void);
 /* (rank, world) of a context; a group context reports (0, number of GPUs). */
 SKY_API int sky_ctx_world(const sky_ctx* ctx, int* rank, int* world);
 /* Take the sharded multi-rank path even on a one-rank context (1 = on).

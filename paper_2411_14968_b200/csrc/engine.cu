@@ -928,6 +928,15 @@ int sky_ctx_create_peers(const int* devices, int n, sky_ctx** out) {
     return rc;
 }
 
+int sky_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 int sky_ctx_world(const sky_ctx* c, int* rank, int* world) {
     if (!c) return SKY_E_CONFIG;
     if (rank) *rank = c->group ? 0 : c->rank;

@@ -23,7 +23,9 @@ int main(int argc, char**) {
         skyline::Dataset r;
         skyline::EngineConfig c;
         auto res = skyline::gpu::run(g, r, c);
-        return (int)res.skyline.size();
+        auto many = skyline::gpu::Context::for_workers(c.workers);  // one process, several GPUs
+        auto res2 = skyline::gpu::run(*many, r, c);
+        return (int)(res.skyline.size() + res2.skyline.size());
     }
     return 0;
 }

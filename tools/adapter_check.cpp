@@ -31,8 +31,13 @@ static bool same(const RunResult& a, const RunResult& b, std::string& why) {
 }
 
 int main() {
-    gpu::Context g(0);
+    gpu::Context g1(0);
+    // the same calls through a two-rank group context (rows sharded over
+    // the ranks; both ranks on device 0, exchanging through device copies)
+    auto g2 = gpu::Context::devices({0, 0}, SKY_GROUP_LOOPBACK);
     int bad = 0, runs = 0;
+  for (gpu::Context* gp : {&g1, g2.get()}) {
+    gpu::Context& g = *gp;
     const Distribution dists[] = {Distribution::Uniform, Distribution::Correlated, Distribution::Anticorrelated};
     for (Distribution dist : dists) {
         for (size_t d : {2, 4, 6}) {
@@ -56,8 +61,8 @@ int main() {
                         ++runs;
                         if (!same(want, got, why)) {
                             ++bad;
-                            std::printf("MISMATCH (%s): dist %d d=%zu strategy %d filter %d merge %d\n", why.c_str(),
-                                        (int)dist, d, (int)s, f, (int)m);
+                            std::printf("MISMATCH (%s): gpus %d dist %d d=%zu strategy %d filter %d merge %d\n",
+                                        why.c_str(), g.world(), (int)dist, d, (int)s, f, (int)m);
                         }
                     }
                 }
@@ -76,6 +81,7 @@ int main() {
             }
         }
     }
+  }
     std::printf("adapter_check: %d runs, %d mismatches\n", runs, bad);
     return bad;
 }

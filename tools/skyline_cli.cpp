@@ -269,8 +269,17 @@ struct Result {
 
 struct Gpu {
     sky_ctx* ctx = nullptr;
-    explicit Gpu(int device) {
-        if (sky_ctx_create(device, &ctx) != SKY_OK) throw RuntimeError("cannot create a GPU context");
+    // one GPU (`device`), or `gpus` > 1 devices device..device+gpus-1 driven
+    // from this process (a group context: rows sharded over the GPUs)
+    Gpu(int device, int gpus) {
+        if (gpus <= 1) {
+            if (sky_ctx_create(device, &ctx) != SKY_OK) throw RuntimeError("cannot create a GPU context");
+            return;
+        }
+        std::vector<int> devs;
+        for (int k = 0; k < gpus; ++k) devs.push_back(device + k);
+        if (sky_ctx_create_group(devs.data(), gpus, 0, &ctx) != SKY_OK)
+            throw RuntimeError("cannot create a " + std::to_string(gpus) + "-GPU context");
     }
     ~Gpu() { sky_ctx_destroy(ctx); }
     // status codes mirror the reference's exception classes (core.hpp:13-34)
@@ -371,7 +380,7 @@ int do_run(int argc, char** argv) {
     Args a = parse_args(argc, argv, 2,
                         {"--input", "--gen", "--seed", "--columns", "--max-columns", "--preset", "--strategy",
                          "--filter", "--merge", "--partitions", "--slices", "--slice-dim", "--reps-q", "--workers",
-                         "--out", "--format", "--device", "--local-algo", "--bnl-window"},
+                         "--out", "--format", "--device", "--gpus", "--local-algo", "--bnl-window"},
                         {"--oracle", "--no-timings"});
     const uint64_t seed = a.u64("--seed", 0);
     // load_input (cli.cpp:157-196)
@@ -431,7 +440,7 @@ int do_run(int argc, char** argv) {
     }
     apply_gpu_extras(a, c);
 
-    Gpu gpu((int)a.u64("--device", 0));
+    Gpu gpu((int)a.u64("--device", 0), (int)a.u64("--gpus", 1));
     Result res;
     gpu.run(data, c, res);
     std::optional<bool> oracle_match;
@@ -490,7 +499,7 @@ int do_run(int argc, char** argv) {
 int do_bench(int argc, char** argv) {
     Args a = parse_args(argc, argv, 2,
                         {"--dist", "--n", "--d", "--strategy", "--filter", "--merge", "--partitions", "--workers",
-                         "--repetitions", "--reps-q", "--seed", "--out", "--device", "--local-algo", "--bnl-window"},
+                         "--repetitions", "--reps-q", "--seed", "--out", "--device", "--gpus", "--local-algo", "--bnl-window"},
                         {});
     const auto dists = a.list("--dist", {"anticorrelated"});
     const auto ns = a.list("--n", {"100000"});
@@ -503,7 +512,7 @@ int do_bench(int argc, char** argv) {
     const uint64_t reps = a.u64("--repetitions", 1), q = a.u64("--reps-q", 5), seed = a.u64("--seed", 0);
     sky_config extras = base_config();
     apply_gpu_extras(a, extras);
-    Gpu gpu((int)a.u64("--device", 0));
+    Gpu gpu((int)a.u64("--device", 0), (int)a.u64("--gpus", 1));
     std::ostringstream table;
     table << kCsvHeader << '\n';
     Data data;
@@ -576,7 +585,8 @@ void usage(std::ostream& os) {
           "      [--workers W] [--oracle] [--no-timings] [--out PATH] [--format json|csv]\n"
           "  bench [--dist a,b] [--n N,..] [--d D,..] [--strategy ..] [--filter ..] [--merge ..]\n"
           "        [--partitions ..] [--workers ..] [--repetitions R] [--reps-q Q] [--seed S] [--out PATH]\n"
-          "  GPU options (run, bench): --device I, --local-algo sfs|bnl, --bnl-window W\n";
+          "  GPU options (run, bench): --device I, --gpus N (devices I..I+N-1), --local-algo sfs|bnl,\n"
+          "    --bnl-window W\n";
 }
 
 }  // namespace
