@@ -167,7 +167,8 @@ SKY_API int sky_ctx_set_sharded(sky_ctx* ctx, int on);
  * skips the full partition sort), "host_merge" (1: host-planned all-pairs
  * merge), "cap_sync" (-1 auto, 0/1: size the filtered set by the input /
  * by the exact count), "sfs_tile", "sfs_chunk", "sfs_head", "merge_tile",
- * "merge_head", "grain_items" (work granularity), "profile_host",
+ * "merge_head", "grain_items" (work granularity), "bnl_block" (rows per
+ * BNL block, one CTA each; 0 = one CTA per partition), "profile_host",
  * "timeline" (diagnostics on stderr). SKY_E_CONFIG for an unknown name. */
 SKY_API int sky_ctx_set_option(sky_ctx* ctx, const char* name, int64_t value);
 SKY_API const char* sky_last_error(const sky_ctx* ctx);

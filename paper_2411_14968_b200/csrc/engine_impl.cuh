@@ -37,6 +37,7 @@ struct sky_options {
     uint32_t merge_tile = 0;    // candidates per merge item (0: from the union size)
     uint32_t merge_head = 4096; // merge wave 0 length
     uint32_t grain_items = 4;   // work items per resident CTA
+    uint32_t bnl_block = 2048;  // BNL: rows per block (one CTA each), 0 = one CTA per partition
     int32_t profile_host = 0;   // print host-side planning / wait times
     int32_t timeline = 0;       // an event after every launch, dumped per run
 };
@@ -110,7 +111,7 @@ enum Slot {
     S_ROWPID, S_AMBROWS, S_ANGT, S_RK0, S_RK1, S_RV0, S_RV1, S_RP0, S_RP1, S_GPOS, S_BM, S_BMT, S_GMIN, S_PTHR2, S_BCNT, S_BKEY, S_BROW, S_OBE, S_SURV, S_SURV2, S_REPF, S_DCBT, S_OFFG,
     // sharded multi-GPU run (shard.cu)
     S_SH_SKG, S_SH_IOTA, S_SH_RUNB, S_SH_TAB, S_SH_IDS, S_SH_TABALL, S_SH_IDSALL, S_SH_CANDG, S_SH_CNT,
-    S_SH_K64R, S_SH_K64S, S_SH_PERM, S_SH_OFFM, S_SH_FULL,
+    S_SH_K64R, S_SH_K64S, S_SH_PERM, S_SH_OFFM, S_SH_FULL, S_BNL_SEG,
     S_SETS, S_SETS_K, S_SETS_I, S_SETS_Q,  // rows sent to their partition owners
     S_SETR, S_SETR_K, S_SETR_I, S_SETR_Q,  // rows received from the other ranks
     S_COUNT
@@ -1175,7 +1176,15 @@ class Runner {
         return compact(s1, dead1, off1_dev, P, S_SET2, off_u_dev, off_u, D);
     }
 
-    // BNL local skylines (k_bnl), window capped at cfg.bnl_window_cap.
+    // BNL local skylines (k_bnl2), window capped at cfg.bnl_window_cap.
+    // With opt.bnl_block > 0 (default) each partition (rows in key order) is
+    // cut into blocks of at most that many rows and one CTA runs BNL per
+    // block, so the grid covers every SM however few partitions there are;
+    // then every block survivor is tested against the rows of its partition
+    // with key <= its own (Prop. 2 of the paper applied inside a partition:
+    // the partition's skyline is the union of the block skylines minus what
+    // a row of another block dominates; a dominator never has a larger key,
+    // so the earlier blocks and its own hold every possible one).
     DevSet local_bnl(int D, const DevSet& s0, uint32_t* off0_dev, uint32_t P, uint32_t window, uint32_t* off_u_dev,
                      std::vector<uint32_t>& off_u, bool count_tests, uint32_t* used_window,
                      uint32_t* n_u = nullptr) {
@@ -1185,7 +1194,22 @@ class Runner {
         const uint32_t want = window ? window : 4096;
         const uint32_t cap = packed ? bnl2_window_fit(D, want, c_->smem_optin) : bnl_window_fit(D, want, c_->smem_optin);
         *used_window = cap;
-        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(P, (uint32_t)c_->sm_count));
+        uint32_t block = c_->opt.bnl_block;
+        if (block > cap) block = cap;  // a block always fits the window: one pass, no overflow
+        const bool blocks = packed && block >= 64 && P <= 4096;
+        // a block's survivors never outgrow the block: the window shrinks to
+        // it (less shared memory, two CTAs per SM)
+        const uint32_t wcap = blocks ? std::min(cap, (block + 3) & ~3u) : cap;
+        // BNL segments: the partitions, or their blocks (count bounded by the capacity)
+        const uint32_t segs = blocks ? P + ceil_div(s0.n, block) : P;
+        uint32_t* seg_off = off0_dev;
+        if (blocks) {
+            seg_off = dev<uint32_t>(S_BNL_SEG, (size_t)segs + 1);
+            launch_split_segments(off0_dev, P, block, seg_off, segs, st_);
+            count();
+        }
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(segs, (uint32_t)c_->sm_count *
+                                                                                 (blocks ? 2u : 1u)));
         uint32_t* wpos = dev<uint32_t>(S_BNL_POS, (size_t)grid * cap);
         uint32_t* wmeta = dev<uint32_t>(S_BNL_META, (size_t)grid * cap);
         uint32_t* ovf = dev<uint32_t>(S_OVF, s0.n);
@@ -1193,9 +1217,9 @@ class Runner {
         SKY_CUDA(cudaMemsetAsync(misc + M_BNLCTR, 0, sizeof(uint32_t), st_));
         BnlArgs b{};
         b.xyz = s0.xyz;
-        b.seg_off = off0_dev;
-        b.P = P;
-        b.window = cap;
+        b.seg_off = seg_off;
+        b.P = segs;
+        b.window = wcap;
         b.dead = dead;
         b.overflow = ovf;
         b.tests = count_tests ? tests(1) : nullptr;
@@ -1205,11 +1229,47 @@ class Runner {
         if (s0.n) {
             dom_begin();
             if (packed)
-                launch_bnl2(D, b, s0.qc, s0.skey, cap & ~3u, grid, misc + M_BNLCTR, st_);
+                launch_bnl2(D, b, s0.qc, s0.skey, wcap & ~3u, grid, misc + M_BNLCTR, st_);
             else
                 launch_bnl_full(D, b, cap, grid, wpos, wmeta, misc + M_BNLCTR, st_);
             dom_end();
             count();
+        }
+        if (blocks && s0.n) {
+            // block survivors (dense, per partition) against their partition
+            RelskyArgs a{};
+            a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
+            a.sxyz = s0.xyz; a.sskey = s0.skey; a.bounded = true; a.dead = dead;
+            a.cid = s0.id; a.sid = s0.id;
+            a.tests = count_tests ? tests(1) : nullptr;
+            const uint32_t ncap = s0.n;
+            uint32_t* dnew = dev<uint32_t>(S_DNEW, P + 1);
+            uint32_t* dense = dev<uint32_t>(S_DENSE, ncap);
+            launch_dense_compact(dead, ncap, off0_dev, P, 0, dense, dnew, nullptr,
+                                 dev<uint32_t>(S_DCBT, dense_compact_scratch(ncap) / 4), st_);
+            count(2);
+            const uint64_t per = (uint64_t)ncap / std::max<uint32_t>(1, P);
+            const uint32_t tile = per >= 512 ? 128 : 64, chunk = c_->opt.sfs_chunk, max_chunks = 64;
+            const uint64_t icap = ((uint64_t)ncap / tile + P) * max_chunks;
+            Item* items = dev<Item>(S_ITEMS, icap);
+            uint32_t* ni = misc + M_NITEMS;
+            const uint32_t icap32 = (uint32_t)std::min<uint64_t>(icap, 0xFFFFFFFFu);
+            if (!launch_plan_partition_items(dnew, off0_dev, nullptr, P, 0, ~0ull, tile, chunk, max_chunks, icap32,
+                                             items, ni, st_)) {
+                Job* jobs = dev<Job>(S_JOBS, P);
+                uint32_t* np_dev = misc + M_NP;
+                uint32_t* hp = stage<uint32_t>(1);
+                *hp = P;
+                SKY_CUDA(cudaMemcpyAsync(np_dev, hp, sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+                launch_partition_jobs(dnew, off0_dev, nullptr, P, 0, ~0ull, jobs, st_);
+                count();
+                const uint32_t* n_items = nullptr;
+                items = expand_jobs(jobs, np_dev, P, tile, chunk, max_chunks, icap, &n_items);
+                relsky_direct(D, tile, a, s0.qc, s0.qc, dense, items, icap, n_items);
+            } else {
+                count();
+                relsky_direct(D, tile, a, s0.qc, s0.qc, dense, items, icap, ni);
+            }
         }
         // rows past the live count stay dead (the fill above), so a capacity-
         // sized set compacts with the count on the device

@@ -320,6 +320,11 @@ uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint32_t* win_pos, uint32_t* win_meta,
                      uint32_t* counter, cudaStream_t st);
 
+// Partitions off[P+1] cut into blocks of <= `block` rows: sub[cap+1] block
+// offsets (empty blocks pad the tail up to cap).
+void launch_split_segments(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* sub, uint32_t cap,
+                           cudaStream_t st);
+
 // Packed-code BNL (D <= 16): window codes + metadata in shared memory.
 uint32_t bnl2_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl2(int D, const BnlArgs& a, const uint2* qc, const uint32_t* skey, uint32_t cap, uint32_t grid,

@@ -1546,6 +1546,40 @@ void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStr
     }
 }
 
+// ------------------------------------------------------- BNL sub-blocks
+// Cut each partition [off[p], off[p+1]) into consecutive blocks of at most
+// `block` rows: sub[0..*n_sub] block offsets, padded with empty blocks up to
+// sub[cap] (one CTA; each thread takes a contiguous run of partitions).
+__global__ void __launch_bounds__(1024) k_split_segments(const uint32_t* __restrict__ off, uint32_t P, uint32_t block,
+                                                         uint32_t* __restrict__ sub, uint32_t cap) {
+    __shared__ uint32_t s_tot[1024];
+    const uint32_t t = threadIdx.x, per = (P + 1023) / 1024;
+    const uint32_t p0 = min(P, t * per), p1 = min(P, p0 + per);
+    uint32_t mine = 0;
+    for (uint32_t p = p0; p < p1; ++p) mine += (off[p + 1] - off[p] + block - 1) / block;
+    s_tot[t] = mine;
+    __syncthreads();
+    // exclusive scan of the per-thread totals (Hillis-Steele over 1024 words)
+    for (uint32_t s = 1; s < 1024; s <<= 1) {
+        const uint32_t v = t >= s ? s_tot[t - s] : 0u;
+        __syncthreads();
+        s_tot[t] += v;
+        __syncthreads();
+    }
+    uint32_t at = s_tot[t] - mine;
+    for (uint32_t p = p0; p < p1; ++p)
+        for (uint32_t b = off[p]; b < off[p + 1]; b += block) sub[at++] = b;
+    const uint32_t total = s_tot[1023];
+    const uint32_t end = off[P];
+    for (uint32_t j = total + t; j <= cap; j += 1024) sub[j] = end;
+}
+
+void launch_split_segments(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* sub, uint32_t cap,
+                           cudaStream_t st) {
+    k_split_segments<<<1, 1024, 0, st>>>(off, P, block, sub, cap);
+    SKY_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------- issue-rate microbenchmark
 // The packed-code test loop of k_relsky3 alone: K candidates' codes in
 // registers, a warp's 32 comparator codes in shared memory read as uint4
