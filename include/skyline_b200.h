@@ -168,7 +168,9 @@ SKY_API int sky_ctx_set_sharded(sky_ctx* ctx, int on);
  * merge), "cap_sync" (-1 auto, 0/1: size the filtered set by the input /
  * by the exact count), "sfs_tile", "sfs_chunk", "sfs_head", "merge_tile",
  * "merge_head", "grain_items" (work granularity), "bnl_block" (rows per
- * BNL block, one CTA each; 0 = one CTA per partition), "profile_host",
+ * BNL block, one CTA each; 0 = one CTA per partition), "merge_index" (1:
+ * merge through a cell index of the union), "merge_cell_rows" (its target
+ * rows per cell), "profile_host",
  * "timeline" (diagnostics on stderr). SKY_E_CONFIG for an unknown name. */
 SKY_API int sky_ctx_set_option(sky_ctx* ctx, const char* name, int64_t value);
 SKY_API const char* sky_last_error(const sky_ctx* ctx);

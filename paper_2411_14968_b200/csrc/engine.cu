@@ -983,6 +983,8 @@ int sky_ctx_set_option(sky_ctx* c, const char* name, int64_t v) {
     else if (k == "merge_head" && u) o.merge_head = u;
     else if (k == "grain_items" && u) o.grain_items = u;
     else if (k == "bnl_block") o.bnl_block = u;
+    else if (k == "merge_index") o.merge_index = s > 0;
+    else if (k == "merge_cell_rows" && u) o.merge_cell_rows = u;
     else if (k == "profile_host") o.profile_host = s > 0;
     else if (k == "timeline") o.timeline = s > 0;
     else {

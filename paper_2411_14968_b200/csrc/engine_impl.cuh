@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <string>
 #include <thread>
@@ -38,6 +39,8 @@ struct sky_options {
     uint32_t merge_head = 4096; // merge wave 0 length
     uint32_t grain_items = 4;   // work items per resident CTA
     uint32_t bnl_block = 2048;  // BNL: rows per block (one CTA each), 0 = one CTA per partition
+    int32_t merge_index = 1;    // merge through the cell index of the union (host-planned merges)
+    uint32_t merge_cell_rows = 1024;  // target rows per cell of that index
     int32_t profile_host = 0;   // print host-side planning / wait times
     int32_t timeline = 0;       // an event after every launch, dumped per run
 };
@@ -1705,6 +1708,60 @@ inline void random_candidates(Runner& R, uint32_t n, const PartitionOut& po, uin
 }
 
 
+// For each cell of a 4^k grid, the cells that weakly dominate it (every
+// digit <=), nearest first (L1 distance over the digits, then cell id).
+// Built once per k and kept for the process.
+inline const std::vector<std::vector<uint32_t>>& dominating_cells(uint32_t k) {
+    static std::mutex mu;
+    static std::vector<std::vector<uint32_t>> tables[9];
+    std::lock_guard<std::mutex> lk(mu);
+    std::vector<std::vector<uint32_t>>& t = tables[k];
+    if (!t.empty()) return t;
+    const uint32_t n = 1u << (2 * k);
+    t.resize(n);
+    std::vector<std::pair<uint32_t, uint32_t>> near;
+    for (uint32_t cell = 0; cell < n; ++cell) {
+        uint32_t dc[8];
+        uint32_t lim = 1;
+        for (uint32_t j = 0, x = cell; j < k; ++j, x >>= 2) {
+            dc[j] = x & 3u;
+            lim *= dc[j] + 1;
+        }
+        near.clear();
+        for (uint32_t r = 0; r < lim; ++r) {
+            uint32_t x = r, id = 0, mul = 1, dist = 0;
+            for (uint32_t j = 0; j < k; ++j) {
+                const uint32_t dd = x % (dc[j] + 1);
+                x /= dc[j] + 1;
+                id += dd * mul;
+                mul *= 4;
+                dist += dc[j] - dd;
+            }
+            near.push_back({dist, id});
+        }
+        std::sort(near.begin(), near.end());
+        for (const auto& p : near) t[cell].push_back(p.second);
+    }
+    return t;
+}
+
+// Cell index of the union for the merge: k = floor(log4(|U| / cell_rows))
+// dimensions (at most 6 and d), the slice dimension first for sliced
+// partitioning; k = 0 (no index) below 16k rows.
+inline CellSpec cell_spec(uint32_t nU, uint32_t d, int D, const sky_config* cfg, uint32_t cell_rows) {
+    CellSpec cs;
+    if (D > 16 || nU < 16384 || !cell_rows) return cs;
+    uint32_t k = 0;
+    for (uint64_t v = nU / cell_rows; v >= 4 && k < 6; v /= 4) ++k;
+    k = std::min<uint32_t>(k, d);
+    uint32_t first = cfg->strategy == SKY_SLICED && cfg->slice_dim < d ? (uint32_t)cfg->slice_dim : 0;
+    cs.dim[0] = (uint8_t)first;
+    for (uint32_t j = 0, t = 1; t < k; ++j)
+        if (j != first) cs.dim[t++] = (uint8_t)j;
+    cs.k = k;
+    return cs;
+}
+
 // The final phase (merge_sequential / merge_noseq, engine.cpp:190-194) and
 // the result record. U: the union of the local skylines in partition order
 // (offsets offu / offu_dev), identical on every rank; with world > 1 each
@@ -1751,8 +1808,10 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
         }
         R.pick_grain(D, cands, pairs, &mp.tile, &mp.chunk);
     }
+    const CellSpec cells = cell_spec(U.n, d, D, cfg, c->opt.merge_cell_rows);
+    const bool indexed = P > 1 && D <= 16 && U.qc && cells.k > 0 && c->opt.merge_index;
     DevSet US;
-    if (all_mode && P > 1) {
+    if (all_mode && P > 1 && !indexed) {
         // Sky(U) against the whole union sorted by sum key: for random and
         // angular pd_i is every other local (engine.cpp:98-103) and u_i is an
         // antichain, so testing against all of U is the same relation;
@@ -1767,10 +1826,68 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
     } else if (P > 1) {
         ma.sxyz = U.xyz; ma.sskey = U.skey;
     }
+    // Indexed Sky(U). Every merge kind yields Sky(U): the u_i are antichains
+    // and pd_i (engine.cpp:74-114) holds every row of U that can dominate a
+    // row of u_i (random / angular: all of U; grid: the weakly dominating
+    // cells; sliced: the earlier slices, since s < t implies s <lex t), and a
+    // comparison with any other row of U cannot change a test. So U is
+    // ordered by (cell, key), cells = the quartiles of k code dimensions
+    // (4^k cells), and a row is tested only against the cells that weakly
+    // dominate its own (s <= t implies cell(s) <= cell(t) digit by digit),
+    // each range bounded by the tile's key.
+    DevSet UC;
+    std::vector<uint32_t> coff;
+    uint32_t icb = 0, ice = 0;  // this rank's cells
+    if (indexed) {
+        UC = R.set(S_SET3, U.n, D);
+        uint64_t* k0 = R.dev<uint64_t>(S_RK0, U.n);
+        uint64_t* k1 = R.dev<uint64_t>(S_RK1, U.n);
+        uint32_t* v0 = R.dev<uint32_t>(S_RV0, U.n);
+        uint32_t* v1 = R.dev<uint32_t>(S_RV1, U.n);
+        launch_cell_keys(D, U.qc, U.skey, U.n, cells, k0, v0, st);
+        R.count();
+        const uint32_t ncell = 1u << (2 * cells.k);
+        R.sort_pairs(k0, k1, v0, v1, U.n, 0, 32 + 2 * (int)cells.k);
+        launch_gather_set(D, U, v1, UC, st);
+        uint32_t* coff_dev = R.dev<uint32_t>(S_OFF_C, ncell + 1);
+        launch_seg_offsets(k1, U.n, ncell, coff_dev, st);
+        R.count(2);
+        uint32_t* h = R.pin<uint32_t>(P_SH_OFF, ncell + 1);
+        SKY_CUDA(cudaMemcpyAsync(h, coff_dev, (ncell + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        R.sync();
+        coff.assign(h, h + ncell + 1);
+        // per cell: the non-empty weakly dominating cells, nearest first
+        const std::vector<std::vector<uint32_t>>& dom = dominating_cells(cells.k);
+        std::vector<std::vector<uint2>> lists(ncell);
+        std::vector<uint64_t> cmp_rows(ncell, 0);
+        for (uint32_t cell = 0; cell < ncell; ++cell) {
+            if (coff[cell + 1] == coff[cell]) continue;
+            for (uint32_t id : dom[cell])
+                if (coff[id + 1] > coff[id]) {
+                    lists[cell].push_back(make_uint2(coff[id], coff[id + 1]));
+                    cmp_rows[cell] += coff[id + 1] - coff[id];
+                }
+        }
+        auto comps_of = [&](uint32_t cell, std::vector<uint2>& out) { out = lists[cell]; };
+        // cells split over the ranks by test volume (candidates x comparators)
+        const std::vector<uint32_t> cr = plan_ranges(coff, ncell, W, [&](uint32_t cell) -> uint64_t {
+            const uint64_t nc = coff[cell + 1] - coff[cell];
+            return nc ? nc * (cmp_rows[cell] / 2 + 1) : 0;
+        });
+        icb = cr[rank];
+        ice = cr[rank + 1];
+        uint64_t pairs = 0;
+        for (uint32_t cell = icb; cell < ice; ++cell) pairs += (uint64_t)(coff[cell + 1] - coff[cell]) * cmp_rows[cell] / 2;
+        R.pick_grain(D, coff[ice] - coff[icb], pairs, &mp.tile, &mp.chunk);
+        ma.cxyz = UC.xyz; ma.cskey = UC.skey; ma.cid = UC.id;
+        ma.sxyz = UC.xyz; ma.sskey = UC.skey; ma.sid = UC.id;
+        R.relsky_waves(D, coff, icb, ice, comps_of, ma, UC.qc, UC.qc, mp.tile, mp.chunk, c->opt.merge_head);
+    }
     // single GPU, all-pairs merge: the candidates are the union itself in
     // global key order, so a tile's key bound is as tight as it can be
-    const bool global_cands = W == 1 && all_mode && P > 1 && D <= 16 && U.qc;
-    if (global_cands) {
+    const bool global_cands = !indexed && W == 1 && all_mode && P > 1 && D <= 16 && U.qc;
+    if (indexed) {
+    } else if (global_cands) {
         ma.cxyz = US.xyz; ma.cskey = US.skey; ma.cid = US.id;
         const std::vector<uint32_t> offg = {0, U.n};
         R.relsky_waves(D, offg, 0, 1, [&](uint32_t, std::vector<uint2>& c) { c.assign(1, make_uint2(0, U.n)); },
@@ -1809,8 +1926,9 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
     }
 
     // surviving ids of this rank's candidates, ascending (engine.cpp:128-133)
-    const uint32_t cb = global_cands ? 0 : offu[qb], cn = global_cands ? U.n : offu[qe] - cb;
-    const uint32_t* cand_ids = global_cands ? US.id : U.id;
+    const uint32_t cb = indexed ? coff[icb] : global_cands ? 0 : offu[qb];
+    const uint32_t cn = indexed ? coff[ice] - cb : global_cands ? U.n : offu[qe] - cb;
+    const uint32_t* cand_ids = indexed ? UC.id : global_cands ? US.id : U.id;
     uint32_t* hm = R.pin<uint32_t>(P_MISC, 32);
     uint32_t* idsA = R.dev<uint32_t>(S_IDS_A, std::max<uint32_t>(cn, 1));
     uint32_t* idsB = R.dev<uint32_t>(S_IDS_B, std::max<uint32_t>(cn, 1));

@@ -320,6 +320,16 @@ uint32_t bnl_window_fit(int D, uint32_t want, int smem_optin);
 void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint32_t* win_pos, uint32_t* win_meta,
                      uint32_t* counter, cudaStream_t st);
 
+// Cell index of a set with packed codes: k dimensions (dim[0] the least
+// significant digit), 4 buckets each (the quartiles of the codes).
+struct CellSpec {
+    uint32_t k = 0;
+    uint8_t dim[8] = {};
+};
+// key[i] = (cell << 32) | skey[i], idx[i] = i
+void launch_cell_keys(int D, const uint2* qc, const uint32_t* skey, uint32_t n, const CellSpec& cs, uint64_t* key,
+                      uint32_t* idx, cudaStream_t st);
+
 // Partitions off[P+1] cut into blocks of <= `block` rows: sub[cap+1] block
 // offsets (empty blocks pad the tail up to cap).
 void launch_split_segments(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* sub, uint32_t cap,

@@ -1546,6 +1546,36 @@ void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStr
     }
 }
 
+// ----------------------------------------------------------- cell index
+// (cell << 32 | skey) of every row of a set: the cell is the top two bits
+// (quartile) of the packed code of each of the spec's dimensions, in mixed
+// radix 4. Codes are monotone in the coordinate, so s <= t implies
+// cell digit(s) <= cell digit(t) on every dimension.
+template <int D>
+__global__ void k_cell_keys(const uint2* __restrict__ qc, const uint32_t* __restrict__ skey, uint32_t n, CellSpec cs,
+                            uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
+    constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint2 q = qc[i];
+    uint32_t cell = 0;
+    for (int t = (int)cs.k - 1; t >= 0; --t) {
+        const int j = cs.dim[t];
+        const uint32_t w = j / L ? q.y : q.x;
+        const uint32_t code = (w >> (LW * (j % L))) & ((1u << B) - 1u);
+        cell = cell * 4u + (code >> (B - 2));
+    }
+    key[i] = ((uint64_t)cell << 32) | skey[i];
+    idx[i] = i;
+}
+
+void launch_cell_keys(int D, const uint2* qc, const uint32_t* skey, uint32_t n, const CellSpec& cs, uint64_t* key,
+                      uint32_t* idx, cudaStream_t st) {
+    if (!n) return;
+    SKY_DISPATCH_D16(D, (k_cell_keys<DT><<<ceil_div(n, 256), 256, 0, st>>>(qc, skey, n, cs, key, idx)));
+    SKY_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------- BNL sub-blocks
 // Cut each partition [off[p], off[p+1]) into consecutive blocks of at most
 // `block` rows: sub[0..*n_sub] block offsets, padded with empty blocks up to
