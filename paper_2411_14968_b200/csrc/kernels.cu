@@ -182,6 +182,18 @@ __device__ __forceinline__ uint32_t angular_slice_exact(double y, double x, cons
 
 // One row of the prep pass: validation, FP64 sum, partition id, sort key
 // (j < DMAX covers every coordinate: DMAX >= d). Returns the sort key.
+// End of a row's coordinates inside a loop over j < DMAX: a row in memory
+// stops the loop; a row in registers (unrolled, DMAX = its width) skips the
+// remaining iterations instead, so every index stays a compile-time
+// constant and the row never goes to local memory.
+#define SKY_ROW_END            \
+    {                          \
+        if constexpr (U == 1)  \
+            break;             \
+        else                   \
+            continue;          \
+    }
+
 template <int DMAX, class Row>
 __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, const Row& R) {
     constexpr int U = Row::kUnroll;
@@ -196,7 +208,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         uint32_t e = 0;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
-            if (j >= d) break;
+            if (j >= d) SKY_ROW_END;
             const float v = R.f(j);
             if (!(isfinite(v) && v >= 0.0f)) e |= kErrNonFinite;
             if (a.normalized && v > 1.0f) e |= kErrAboveOne;
@@ -216,7 +228,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
-            if (j >= d) break;
+            if (j >= d) SKY_ROW_END;
             const float v = R.f(j);
             ok &= (v >= 0.0f) & (v <= 1.0f);
             sum = __dadd_rn(sum, (double)v);
@@ -233,7 +245,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         const double md = (double)a.m;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
-            if (j >= d) break;
+            if (j >= d) SKY_ROW_END;
             const double v = R.X(j);
             if (!(isfinite(v) && v >= 0.0)) err |= kErrNonFinite;
             if (a.normalized && v > 1.0) err |= kErrAboveOne;
@@ -249,7 +261,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
-            if (j >= d) break;
+            if (j >= d) SKY_ROW_END;
             if (Row::kF32) {
                 // float rows: the same answers as on the exact upcast
                 const float v = R.f(j);
@@ -280,7 +292,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
             // squares must stay normal floats for that error bound
 #pragma unroll U
             for (int j = 0; j < DMAX; ++j) {
-                if (j >= d) break;
+                if (j >= d) SKY_ROW_END;
                 const float xj = R.f(j);
                 if (xj != 0.0f && !(xj > 1e-15f && xj < 1e15f)) exact64 = true;
             }
@@ -363,7 +375,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
-            if (j >= d) break;
+            if (j >= d) SKY_ROW_END;
             if (Row::kF32) {
                 const float v = R.f(j);
                 ok &= (v >= 0.0f) & (v <= upper);
@@ -871,17 +883,30 @@ __global__ void k_part_thresh(const uint32_t* __restrict__ gmin, uint32_t G, uin
 __global__ void k_cand_bucket(const uint64_t* __restrict__ key64, uint32_t n, const uint32_t* __restrict__ thr,
                               uint32_t B, uint32_t* __restrict__ cnt, uint64_t* __restrict__ bkey,
                               uint32_t* __restrict__ brow, uint32_t* overflow) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint64_t k = __ldcs(key64 + i);
-    const uint32_t p = (uint32_t)(k >> 32);
-    if ((uint32_t)k > __ldg(thr + p)) return;
-    const uint32_t s = atomicAdd(cnt + p, 1u);
-    if (s < B) {
-        bkey[(size_t)p * B + s] = k;
-        brow[(size_t)p * B + s] = i;
+    // four consecutive keys per thread (two 16-byte streaming loads in flight)
+    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i0 >= n) return;
+    uint64_t k[4];
+    if (i0 + 4 <= n) {
+        const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(key64 + i0));
+        const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(key64 + i0) + 1);
+        k[0] = a.x; k[1] = a.y; k[2] = b.x; k[3] = b.y;
     } else {
-        atomicOr(overflow, 1u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k[j] = i0 + j < n ? __ldcs(key64 + i0 + j) : ~0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (k[j] == ~0ull) continue;
+        const uint32_t p = (uint32_t)(k[j] >> 32);
+        if ((uint32_t)k[j] > __ldg(thr + p)) continue;
+        const uint32_t s = atomicAdd(cnt + p, 1u);
+        if (s < B) {
+            bkey[(size_t)p * B + s] = k[j];
+            brow[(size_t)p * B + s] = i0 + j;
+        } else {
+            atomicOr(overflow, 1u);
+        }
     }
 }
 
@@ -1057,7 +1082,7 @@ void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32
     k_part_thresh<<<ceil_div((uint64_t)P * 32, 256), 256, 0, st>>>(gmin, G, P, q, thr);
     SKY_LAUNCH_CHECK();
     SKY_CUDA(cudaMemsetAsync(cnt, 0, P * sizeof(uint32_t), st));
-    k_cand_bucket<<<ceil_div(n, 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
+    k_cand_bucket<<<ceil_div(ceil_div(n, 4), 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
     SKY_LAUNCH_CHECK();
     const uint32_t run_floats = std::min<uint32_t>(B * d, 16u * 1024);  // <= 64 KB of run coordinates
     ensure_smem_attr((const void*)k_bucket_pick, 64 * 1024);

@@ -992,7 +992,8 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
                 nt += r + 1;
                 T0 &= ~CodeLayout<D>::ALIVE;
             }
-            if ((r & 15) == 15 && !__any_sync(0xffffffffu, alive)) {
+            // few representatives: the strongest usually kill the whole warp
+            if (((r & 15) == 15 || nrep <= 32) && !__any_sync(0xffffffffu, alive)) {
                 ++r;
                 break;
             }
