@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <random>
@@ -1708,33 +1709,35 @@ inline void random_candidates(Runner& R, uint32_t n, const PartitionOut& po, uin
 }
 
 
-// For each cell of a 4^k grid, the cells that weakly dominate it (every
+// For each cell of a cell index, the cells that weakly dominate it (every
 // digit <=), nearest first (L1 distance over the digits, then cell id).
-// Built once per k and kept for the process.
-inline const std::vector<std::vector<uint32_t>>& dominating_cells(uint32_t k) {
+// Built once per digit layout and kept for the process.
+inline const std::vector<std::vector<uint32_t>>& dominating_cells(const CellSpec& cs) {
     static std::mutex mu;
-    static std::vector<std::vector<uint32_t>> tables[9];
+    static std::map<std::vector<uint8_t>, std::vector<std::vector<uint32_t>>> tables;
+    const std::vector<uint8_t> layout(cs.bits, cs.bits + cs.k);
     std::lock_guard<std::mutex> lk(mu);
-    std::vector<std::vector<uint32_t>>& t = tables[k];
+    std::vector<std::vector<uint32_t>>& t = tables[layout];
     if (!t.empty()) return t;
-    const uint32_t n = 1u << (2 * k);
+    const uint32_t k = cs.k, n = 1u << cs.total_bits();
     t.resize(n);
     std::vector<std::pair<uint32_t, uint32_t>> near;
     for (uint32_t cell = 0; cell < n; ++cell) {
-        uint32_t dc[8];
+        uint32_t dc[16], sh[16];
         uint32_t lim = 1;
-        for (uint32_t j = 0, x = cell; j < k; ++j, x >>= 2) {
-            dc[j] = x & 3u;
+        for (uint32_t j = 0, at = 0; j < k; ++j) {
+            sh[j] = at;
+            dc[j] = (cell >> at) & ((1u << cs.bits[j]) - 1u);
+            at += cs.bits[j];
             lim *= dc[j] + 1;
         }
         near.clear();
         for (uint32_t r = 0; r < lim; ++r) {
-            uint32_t x = r, id = 0, mul = 1, dist = 0;
+            uint32_t x = r, id = 0, dist = 0;
             for (uint32_t j = 0; j < k; ++j) {
                 const uint32_t dd = x % (dc[j] + 1);
                 x /= dc[j] + 1;
-                id += dd * mul;
-                mul *= 4;
+                id |= dd << sh[j];
                 dist += dc[j] - dd;
             }
             near.push_back({dist, id});
@@ -1745,20 +1748,30 @@ inline const std::vector<std::vector<uint32_t>>& dominating_cells(uint32_t k) {
     return t;
 }
 
-// Cell index of the union for the merge: k = floor(log4(|U| / cell_rows))
-// dimensions (at most 6 and d), the slice dimension first for sliced
-// partitioning; k = 0 (no index) below 16k rows.
+// Cell index of the union for the merge: K = log2(|U| / cell_rows) digit
+// bits (at most 12 and d), one per dimension in turn (the slice dimension
+// first for sliced partitioning); no index below 16k rows. Halves on many
+// dimensions prune more pairs than quartiles on few: on C4's union one bit
+// on each of the 10 dimensions leaves half the comparisons of two bits on 5.
 inline CellSpec cell_spec(uint32_t nU, uint32_t d, int D, const sky_config* cfg, uint32_t cell_rows) {
     CellSpec cs;
-    if (D > 16 || nU < 16384 || !cell_rows) return cs;
-    uint32_t k = 0;
-    for (uint64_t v = nU / cell_rows; v >= 4 && k < 6; v /= 4) ++k;
-    k = std::min<uint32_t>(k, d);
-    uint32_t first = cfg->strategy == SKY_SLICED && cfg->slice_dim < d ? (uint32_t)cfg->slice_dim : 0;
-    cs.dim[0] = (uint8_t)first;
-    for (uint32_t j = 0, t = 1; t < k; ++j)
-        if (j != first) cs.dim[t++] = (uint8_t)j;
-    cs.k = k;
+    if (D > 16 || nU < 16384 || !cell_rows || d == 0) return cs;
+    uint32_t K = 0;
+    for (uint64_t v = nU / cell_rows; v >= 2 && K < 12; v /= 2) ++K;
+    K = std::min<uint32_t>(K, 2 * std::min<uint32_t>(d, 16));
+    if (K > d) K = d;  // measured on C4: a second bit on some dimensions adds more ranges than it prunes
+    if (!K) return cs;
+    const uint32_t first = cfg->strategy == SKY_SLICED && cfg->slice_dim < d ? (uint32_t)cfg->slice_dim : 0;
+    const uint32_t nd = std::min<uint32_t>(d, 16);
+    std::vector<uint32_t> order(1, first);
+    for (uint32_t j = 0; j < nd; ++j)
+        if (j != first) order.push_back(j);
+    cs.k = std::min(K, nd);
+    for (uint32_t t = 0; t < cs.k; ++t) {
+        cs.dim[t] = (uint8_t)order[t];
+        cs.bits[t] = 1;
+    }
+    for (uint32_t t = 0, extra = K - cs.k; t < cs.k && extra; ++t, --extra) cs.bits[t] = 2;
     return cs;
 }
 
@@ -1846,8 +1859,8 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
         uint32_t* v1 = R.dev<uint32_t>(S_RV1, U.n);
         launch_cell_keys(D, U.qc, U.skey, U.n, cells, k0, v0, st);
         R.count();
-        const uint32_t ncell = 1u << (2 * cells.k);
-        R.sort_pairs(k0, k1, v0, v1, U.n, 0, 32 + 2 * (int)cells.k);
+        const uint32_t ncell = 1u << cells.total_bits();
+        R.sort_pairs(k0, k1, v0, v1, U.n, 0, 32 + (int)cells.total_bits());
         launch_gather_set(D, U, v1, UC, st);
         uint32_t* coff_dev = R.dev<uint32_t>(S_OFF_C, ncell + 1);
         launch_seg_offsets(k1, U.n, ncell, coff_dev, st);
@@ -1857,7 +1870,7 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
         R.sync();
         coff.assign(h, h + ncell + 1);
         // per cell: the non-empty weakly dominating cells, nearest first
-        const std::vector<std::vector<uint32_t>>& dom = dominating_cells(cells.k);
+        const std::vector<std::vector<uint32_t>>& dom = dominating_cells(cells);
         std::vector<std::vector<uint2>> lists(ncell);
         std::vector<uint64_t> cmp_rows(ncell, 0);
         for (uint32_t cell = 0; cell < ncell; ++cell) {

@@ -321,10 +321,17 @@ void launch_bnl_full(int D, const BnlArgs& a, uint32_t cap, uint32_t grid, uint3
                      uint32_t* counter, cudaStream_t st);
 
 // Cell index of a set with packed codes: k dimensions (dim[0] the least
-// significant digit), 4 buckets each (the quartiles of the codes).
+// significant digit), dimension t split into 2^bits[t] buckets by the top
+// bits of its code (halves or quartiles of the code range).
 struct CellSpec {
     uint32_t k = 0;
-    uint8_t dim[8] = {};
+    uint8_t dim[16] = {};
+    uint8_t bits[16] = {};
+    uint32_t total_bits() const {
+        uint32_t b = 0;
+        for (uint32_t t = 0; t < k; ++t) b += bits[t];
+        return b;
+    }
 };
 // key[i] = (cell << 32) | skey[i], idx[i] = i
 void launch_cell_keys(int D, const uint2* qc, const uint32_t* skey, uint32_t n, const CellSpec& cs, uint64_t* key,

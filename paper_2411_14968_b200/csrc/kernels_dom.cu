@@ -1548,10 +1548,10 @@ void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStr
 }
 
 // ----------------------------------------------------------- cell index
-// (cell << 32 | skey) of every row of a set: the cell is the top two bits
-// (quartile) of the packed code of each of the spec's dimensions, in mixed
-// radix 4. Codes are monotone in the coordinate, so s <= t implies
-// cell digit(s) <= cell digit(t) on every dimension.
+// (cell << 32 | skey) of every row of a set: the cell digit of each of the
+// spec's dimensions is the top bits[t] bits of its packed code, dim[0] the
+// least significant. Codes are monotone in the coordinate, so s <= t
+// implies digit(s) <= digit(t) on every dimension.
 template <int D>
 __global__ void k_cell_keys(const uint2* __restrict__ qc, const uint32_t* __restrict__ skey, uint32_t n, CellSpec cs,
                             uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
@@ -1564,7 +1564,7 @@ __global__ void k_cell_keys(const uint2* __restrict__ qc, const uint32_t* __rest
         const int j = cs.dim[t];
         const uint32_t w = j / L ? q.y : q.x;
         const uint32_t code = (w >> (LW * (j % L))) & ((1u << B) - 1u);
-        cell = cell * 4u + (code >> (B - 2));
+        cell = (cell << cs.bits[t]) | (code >> (B - cs.bits[t]));
     }
     key[i] = ((uint64_t)cell << 32) | skey[i];
     idx[i] = i;
