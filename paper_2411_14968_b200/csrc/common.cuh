@@ -45,7 +45,9 @@ struct Item {
 };
 
 // Grow-only device buffers keyed by slot; reused across runs so the timed
-// loop never allocates.
+// loop never allocates. A slot that grows during a run keeps its old buffer
+// alive until the next run starts (retire()), so a pointer taken earlier in
+// the run stays valid whatever later code asks of the same slot.
 class Arena {
    public:
     ~Arena() { release(); }
@@ -53,7 +55,7 @@ class Arena {
         if (slot >= (int)bufs_.size()) bufs_.resize(slot + 1);
         Buf& b = bufs_[slot];
         if (b.cap < bytes) {
-            if (b.ptr) cudaFree(b.ptr);
+            if (b.ptr) retired_.push_back(b.ptr);
             b.ptr = nullptr;
             size_t cap = bytes + bytes / 4 + 256;
             SKY_CUDA(cudaMalloc(&b.ptr, cap));
@@ -61,11 +63,17 @@ class Arena {
         }
         return b.ptr;
     }
+    // free the buffers replaced during the previous run (its work has drained)
+    void retire() {
+        for (void* p : retired_) cudaFree(p);
+        retired_.clear();
+    }
     template <class T>
     T* as(int slot, size_t n) {
         return static_cast<T*>(get(slot, n * sizeof(T) + 16));
     }
     void release() {
+        retire();
         for (Buf& b : bufs_)
             if (b.ptr) cudaFree(b.ptr);
         bufs_.clear();
@@ -77,6 +85,7 @@ class Arena {
         size_t cap = 0;
     };
     std::vector<Buf> bufs_;
+    std::vector<void*> retired_;
 };
 
 // Pinned host staging buffers keyed by slot.

@@ -78,6 +78,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     if (!D) throw Error(SKY_E_DIMENSION, "the GPU engine supports d <= 32");
 
     Runner R(c);
+    R.s0_dims_ = d;
     cudaStream_t st = c->stream;
     if (R.tl_) R.mark(__LINE__);
 
@@ -519,7 +520,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         const uint32_t Pm = pe - pb;
         std::vector<uint32_t> offm(Pm + 1);
         for (uint32_t k = 0; k <= Pm; ++k) offm[k] = off1[pb + k] - base;
-        uint32_t* offm_dev = R.dev<uint32_t>(S_OFF_C, Pm + 1);
+        uint32_t* offm_dev = R.dev<uint32_t>(S_OFFM, Pm + 1);  // not S_OFF_C: the local waves use it
         {
             uint32_t* hs = R.stage<uint32_t>(Pm + 1);
             std::memcpy(hs, offm.data(), (Pm + 1) * sizeof(uint32_t));

@@ -118,6 +118,7 @@ enum Slot {
     S_SH_K64R, S_SH_K64S, S_SH_PERM, S_SH_OFFM, S_SH_FULL, S_BNL_SEG,
     S_SETS, S_SETS_K, S_SETS_I, S_SETS_Q,  // rows sent to their partition owners
     S_SETR, S_SETR_K, S_SETR_I, S_SETR_Q,  // rows received from the other ranks
+    S_DEAD2, S_SOFF, S_SH_OFFU, S_OFFM,
     S_COUNT
 };
 // pinned slots
@@ -319,6 +320,35 @@ struct Plan {
         flush();
     }
 
+    // Candidates [cb, ce) in tiles of `tile`, each tile against every group
+    // of at most `chunk` comparators of `comps`; the ranges are stored once
+    // and the tiles' items point at the same groups.
+    void add_shared(uint32_t cb, uint32_t ce, const std::vector<uint2>& comps) {
+        std::vector<uint2> groups;  // (lb, le) into `ranges`
+        uint32_t acc = 0, lb = (uint32_t)ranges.size();
+        for (uint2 r : comps) {
+            for (uint32_t b = r.x; b < r.y;) {
+                const uint32_t take = std::min(r.y - b, chunk - acc);
+                ranges.push_back(make_uint2(b, b + take));
+                b += take;
+                acc += take;
+                if (acc >= chunk) {
+                    groups.push_back(make_uint2(lb, (uint32_t)ranges.size()));
+                    lb = (uint32_t)ranges.size();
+                    acc = 0;
+                }
+            }
+        }
+        if ((uint32_t)ranges.size() > lb) groups.push_back(make_uint2(lb, (uint32_t)ranges.size()));
+        for (uint32_t b = cb; b < ce; b += tile) {
+            const uint32_t e = std::min(ce, b + tile);
+            for (uint32_t g = 0; g < (uint32_t)groups.size(); ++g) {
+                items.push_back(Item{b, e, groups[g].x, groups[g].y});
+                group.push_back(g);
+            }
+        }
+    }
+
     // Launch order by wave: a stable counting pass over the group index.
     void order() {
         if (items.empty()) return;
@@ -333,11 +363,51 @@ struct Plan {
     }
 };
 
+// For each cell of a cell index, the cells that weakly dominate it (every
+// digit <=), nearest first (L1 distance over the digits, then cell id).
+// Built once per digit layout and kept for the process.
+inline const std::vector<std::vector<uint32_t>>& dominating_cells(const CellSpec& cs) {
+    static std::mutex mu;
+    static std::map<std::vector<uint8_t>, std::vector<std::vector<uint32_t>>> tables;
+    const std::vector<uint8_t> layout(cs.bits, cs.bits + cs.k);
+    std::lock_guard<std::mutex> lk(mu);
+    std::vector<std::vector<uint32_t>>& t = tables[layout];
+    if (!t.empty()) return t;
+    const uint32_t k = cs.k, n = 1u << cs.total_bits();
+    t.resize(n);
+    std::vector<std::pair<uint32_t, uint32_t>> near;
+    for (uint32_t cell = 0; cell < n; ++cell) {
+        uint32_t dc[16], sh[16];
+        uint32_t lim = 1;
+        for (uint32_t j = 0, at = 0; j < k; ++j) {
+            sh[j] = at;
+            dc[j] = (cell >> at) & ((1u << cs.bits[j]) - 1u);
+            at += cs.bits[j];
+            lim *= dc[j] + 1;
+        }
+        near.clear();
+        for (uint32_t r = 0; r < lim; ++r) {
+            uint32_t x = r, id = 0, dist = 0;
+            for (uint32_t j = 0; j < k; ++j) {
+                const uint32_t dd = x % (dc[j] + 1);
+                x /= dc[j] + 1;
+                id |= dd << sh[j];
+                dist += dc[j] - dd;
+            }
+            near.push_back({dist, id});
+        }
+        std::sort(near.begin(), near.end());
+        for (const auto& p : near) t[cell].push_back(p.second);
+    }
+    return t;
+}
+
 class Runner {
    public:
     // Every API call ends with the stream drained (its results are read on
     // the host), so a new Runner may recycle the staging and event pools.
     Runner(sky_ctx* c) : c_(c), st_(c->stream) {
+        c->dev.retire();  // the previous call drained its stream
         prof_ = c->opt.profile_host != 0;
         tl_ = c->opt.timeline != 0;
         c->stage_cur = c->stage_off = 0;
@@ -796,7 +866,8 @@ class Runner {
         for (uint32_t p = qb; p < qe; ++p) {
             slice(lists[p - qb], 0, head, sub);
             if (sub.empty()) continue;
-            for (uint32_t b = offc[p]; b < offc[p + 1]; b += tile) A.add(b, std::min(offc[p + 1], b + tile), sub);
+            // the partition's comparator groups once, shared by all its tiles
+            A.add_shared(offc[p], offc[p + 1], sub);
         }
         A.order();
         relsky(D, A, base, cq, sq);
@@ -1239,7 +1310,9 @@ class Runner {
             dom_end();
             count();
         }
-        if (blocks && s0.n) {
+        if (blocks && s0.n && indexed_partition_sky(D, s0, dead, off0_dev, P, s0_dims_, count_tests)) {
+            // reconciled through the per-partition cell index
+        } else if (blocks && s0.n) {
             // block survivors (dense, per partition) against their partition
             RelskyArgs a{};
             a.cxyz = s0.xyz; a.cskey = s0.skey; a.indirect = false;
@@ -1281,9 +1354,97 @@ class Runner {
         return compact(s0, dead, off0_dev, P, S_SET2, off_u_dev, off_u, D);
     }
 
+    // Relative skyline of every live row of S against its own partition
+    // through a per-partition cell index (the indexed merge of §4 applied
+    // inside the partitions): the live rows in (partition, cell, key) order,
+    // cells = one code bit on each of K dimensions (K = log2 of the mean
+    // live rows per partition / 1024, at most d), each row tested against
+    // the cells of its partition that weakly dominate its own, nearest
+    // first, bounded by the tile's key. Sets dead[] of the dominated rows.
+    // Two host round trips (the live count, the cell offsets). false: the
+    // partitions are too small for an index; nothing was done.
+    bool indexed_partition_sky(int D, const DevSet& S, uint8_t* dead, const uint32_t* off_dev, uint32_t P,
+                               uint32_t d, bool count_tests) {
+        if (D > 16 || !S.qc || !S.n || !P || P > 4096 || !c_->opt.merge_index) return false;
+        const uint32_t pb = (uint32_t)std::max(1, bits_for(P));
+        uint32_t K = 0;
+        for (uint64_t v = (uint64_t)S.n / P / 1024; v >= 2 && K < d && K < 10; v /= 2) ++K;
+        if (K < 2 || 32 + K + pb > 64) return false;
+        CellSpec cs;
+        cs.k = K;
+        for (uint32_t t = 0; t < K; ++t) {
+            cs.dim[t] = (uint8_t)t;
+            cs.bits[t] = 1;
+        }
+        // live rows, dense per partition, and their count
+        uint32_t* dense = dev<uint32_t>(S_DENSE, S.n);
+        uint32_t* dnew = dev<uint32_t>(S_DNEW, P + 1);
+        launch_dense_compact(dead, S.n, off_dev, P, 0, dense, dnew, nullptr,
+                             dev<uint32_t>(S_DCBT, dense_compact_scratch(S.n) / 4), st_);
+        count(2);
+        uint32_t* h = pin<uint32_t>(P_SH_OFF, 2);
+        SKY_CUDA(cudaMemcpyAsync(h, dnew + P, sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        sync();
+        const uint32_t nl = h[0];
+        if (!nl) return true;
+        uint64_t* k0 = dev<uint64_t>(S_RK0, nl);
+        uint64_t* k1 = dev<uint64_t>(S_RK1, nl);
+        uint32_t* v0 = dev<uint32_t>(S_RV0, nl);
+        uint32_t* v1 = dev<uint32_t>(S_RV1, nl);
+        uint32_t* rows2 = dev<uint32_t>(S_RP0, nl);
+        launch_part_cell_keys(D, S.qc, S.skey, dense, dnew, P, nl, cs, k0, v0, st_);
+        count();
+        sort_pairs(k0, k1, v0, v1, nl, 0, (int)(32 + K + pb));
+        launch_gather_u32(dense, v1, nl, rows2, st_);
+        DevSet S2 = set(S_SET1, nl, D);
+        DevSet Sv = S;
+        Sv.n = nl;  // the gather runs over the nl picked rows (out[i] = S[rows2[i]])
+        launch_gather_set(D, Sv, rows2, S2, st_);
+        const uint32_t NS = P << K;
+        uint32_t* soff = dev<uint32_t>(S_SOFF, NS + 1);
+        launch_seg_offsets(k1, nl, NS, soff, st_);
+        count(3);
+        uint32_t* hs = pin<uint32_t>(P_SH_OFF, NS + 1);
+        SKY_CUDA(cudaMemcpyAsync(hs, soff, (NS + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+        sync();
+        const std::vector<uint32_t> so(hs, hs + NS + 1);
+        const std::vector<std::vector<uint32_t>>& dom = dominating_cells(cs);
+        const uint32_t ncell = 1u << K;
+        uint64_t pairs = 0;
+        std::vector<std::vector<uint2>> lists(NS);
+        for (uint32_t s = 0; s < NS; ++s) {
+            if (so[s + 1] == so[s]) continue;
+            const uint32_t base = s & ~(ncell - 1u), cell = s & (ncell - 1u);
+            uint64_t cmp = 0;
+            for (uint32_t c2 : dom[cell]) {
+                const uint32_t s2 = base | c2;
+                if (so[s2 + 1] > so[s2]) {
+                    lists[s].push_back(make_uint2(so[s2], so[s2 + 1]));
+                    cmp += so[s2 + 1] - so[s2];
+                }
+            }
+            pairs += (uint64_t)(so[s + 1] - so[s]) * cmp / 2;
+        }
+        uint8_t* dead2 = dev<uint8_t>(S_DEAD2, nl);
+        launch_fill_u8(dead2, 0, nl, st_);
+        count();
+        RelskyArgs a{};
+        a.cxyz = S2.xyz; a.cskey = S2.skey; a.cid = S2.id; a.indirect = false;
+        a.sxyz = S2.xyz; a.sskey = S2.skey; a.sid = S2.id; a.bounded = true; a.dead = dead2;
+        a.tests = count_tests ? tests(1) : nullptr;
+        uint32_t tile, chunk;
+        pick_grain(D, nl, pairs, &tile, &chunk);
+        relsky_waves(D, so, 0, NS, [&](uint32_t s, std::vector<uint2>& out) { out = lists[s]; }, a, S2.qc, S2.qc,
+                     tile, chunk, c_->opt.sfs_head);
+        launch_scatter_dead(dead2, rows2, nl, dead, st_);
+        count();
+        return true;
+    }
+
    public:
     sky_ctx* c_;
     X64 x64_;  // FP64 input of the current run (null for float input)
+    uint32_t s0_dims_ = 0;  // coordinates per row of the current run (d)
     cudaStream_t st_;
 };
 
@@ -1708,45 +1869,6 @@ inline void random_candidates(Runner& R, uint32_t n, const PartitionOut& po, uin
     R.count();
 }
 
-
-// For each cell of a cell index, the cells that weakly dominate it (every
-// digit <=), nearest first (L1 distance over the digits, then cell id).
-// Built once per digit layout and kept for the process.
-inline const std::vector<std::vector<uint32_t>>& dominating_cells(const CellSpec& cs) {
-    static std::mutex mu;
-    static std::map<std::vector<uint8_t>, std::vector<std::vector<uint32_t>>> tables;
-    const std::vector<uint8_t> layout(cs.bits, cs.bits + cs.k);
-    std::lock_guard<std::mutex> lk(mu);
-    std::vector<std::vector<uint32_t>>& t = tables[layout];
-    if (!t.empty()) return t;
-    const uint32_t k = cs.k, n = 1u << cs.total_bits();
-    t.resize(n);
-    std::vector<std::pair<uint32_t, uint32_t>> near;
-    for (uint32_t cell = 0; cell < n; ++cell) {
-        uint32_t dc[16], sh[16];
-        uint32_t lim = 1;
-        for (uint32_t j = 0, at = 0; j < k; ++j) {
-            sh[j] = at;
-            dc[j] = (cell >> at) & ((1u << cs.bits[j]) - 1u);
-            at += cs.bits[j];
-            lim *= dc[j] + 1;
-        }
-        near.clear();
-        for (uint32_t r = 0; r < lim; ++r) {
-            uint32_t x = r, id = 0, dist = 0;
-            for (uint32_t j = 0; j < k; ++j) {
-                const uint32_t dd = x % (dc[j] + 1);
-                x /= dc[j] + 1;
-                id |= dd << sh[j];
-                dist += dc[j] - dd;
-            }
-            near.push_back({dist, id});
-        }
-        std::sort(near.begin(), near.end());
-        for (const auto& p : near) t[cell].push_back(p.second);
-    }
-    return t;
-}
 
 // Cell index of the union for the merge: K = log2(|U| / cell_rows) digit
 // bits (at most 12 and d), one per dimension in turn (the slice dimension

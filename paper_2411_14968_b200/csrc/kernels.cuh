@@ -337,6 +337,13 @@ struct CellSpec {
 void launch_cell_keys(int D, const uint2* qc, const uint32_t* skey, uint32_t n, const CellSpec& cs, uint64_t* key,
                       uint32_t* idx, cudaStream_t st);
 
+// Rows dense[j] (partitions doff[P+1] over j): key[j] = (partition << (32 +
+// K) | cell << 32 | skey), idx[j] = j
+void launch_part_cell_keys(int D, const uint2* qc, const uint32_t* skey, const uint32_t* dense, const uint32_t* doff,
+                           uint32_t P, uint32_t n, const CellSpec& cs, uint64_t* key, uint32_t* idx, cudaStream_t st);
+// dead[rows[i]] |= flag[i]
+void launch_scatter_dead(const uint8_t* flag, const uint32_t* rows, uint32_t n, uint8_t* dead, cudaStream_t st);
+
 // Partitions off[P+1] cut into blocks of <= `block` rows: sub[cap+1] block
 // offsets (empty blocks pad the tail up to cap).
 void launch_split_segments(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* sub, uint32_t cap,

@@ -1577,6 +1577,56 @@ void launch_cell_keys(int D, const uint2* qc, const uint32_t* skey, uint32_t n, 
     SKY_LAUNCH_CHECK();
 }
 
+// Rows of a dense list (dense[j], partitions doff[P+1] over j) keyed by
+// (partition << (32 + K) | cell << 32 | skey), idx[j] = j.
+template <int D>
+__global__ void k_part_cell_keys(const uint2* __restrict__ qc, const uint32_t* __restrict__ skey,
+                                 const uint32_t* __restrict__ dense, const uint32_t* __restrict__ doff, uint32_t P,
+                                 uint32_t n, CellSpec cs, uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
+    constexpr int L = CodeLayout<D>::L, LW = CodeLayout<D>::LW, B = CodeLayout<D>::B;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    // partition of dense position j: the last p with doff[p] <= j
+    uint32_t lo = 0, hi = P;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (doff[mid] <= j) lo = mid; else hi = mid;
+    }
+    const uint32_t i = dense[j];
+    const uint2 q = qc[i];
+    uint32_t cell = 0, K = 0;
+    for (int t = (int)cs.k - 1; t >= 0; --t) {
+        const int dj = cs.dim[t];
+        const uint32_t w = dj / L ? q.y : q.x;
+        const uint32_t code = (w >> (LW * (dj % L))) & ((1u << B) - 1u);
+        cell = (cell << cs.bits[t]) | (code >> (B - cs.bits[t]));
+        K += cs.bits[t];
+    }
+    key[j] = ((uint64_t)lo << (32 + K)) | ((uint64_t)cell << 32) | skey[i];
+    idx[j] = j;
+}
+
+void launch_part_cell_keys(int D, const uint2* qc, const uint32_t* skey, const uint32_t* dense, const uint32_t* doff,
+                           uint32_t P, uint32_t n, const CellSpec& cs, uint64_t* key, uint32_t* idx, cudaStream_t st) {
+    if (!n) return;
+    SKY_DISPATCH_D16(D, (k_part_cell_keys<DT><<<ceil_div(n, 256), 256, 0, st>>>(qc, skey, dense, doff, P, n, cs,
+                                                                                 key, idx)));
+    SKY_LAUNCH_CHECK();
+}
+
+// dead[rows[i]] |= flag[i]
+__global__ void k_scatter_dead(const uint8_t* __restrict__ flag, const uint32_t* __restrict__ rows, uint32_t n,
+                               uint8_t* __restrict__ dead) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) dead[rows[i]] = 1;
+}
+
+void launch_scatter_dead(const uint8_t* flag, const uint32_t* rows, uint32_t n, uint8_t* dead, cudaStream_t st) {
+    if (!n) return;
+    k_scatter_dead<<<ceil_div(n, 256), 256, 0, st>>>(flag, rows, n, dead);
+    SKY_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------- BNL sub-blocks
 // Cut each partition [off[p], off[p+1]) into consecutive blocks of at most
 // `block` rows: sub[0..*n_sub] block offsets, padded with empty blocks up to

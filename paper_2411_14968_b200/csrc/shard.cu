@@ -223,6 +223,7 @@ void run_sharded(sky_ctx* c, const float* src, uint32_t nl, uint32_t row0, const
     const bool reps_on = cfg->filter == SKY_FILTER_REPRESENTATIVE;
 
     Runner R(c);
+    R.s0_dims_ = d;
     cudaStream_t st = c->stream;
     SKY_CUDA(cudaEventRecord(c->ev[0], st));
     uint32_t* misc = R.dev<uint32_t>(S_MISC, 64);
@@ -574,7 +575,7 @@ void run_sharded(sky_ctx* c, const float* src, uint32_t nl, uint32_t row0, const
     uint32_t* hn = R.stage<uint32_t>(1);
     *hn = n_recv;
     SKY_CUDA(cudaMemcpyAsync(misc + M_S0, hn, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    uint32_t* offum_dev = R.dev<uint32_t>(S_OFF_C, Pm + 1);
+    uint32_t* offum_dev = R.dev<uint32_t>(S_SH_OFFU, Pm + 1);  // not S_OFF_C: the local phase's waves use it
     DevSet Um;
     std::vector<uint32_t> offum(Pm + 1, 0);
     if (n_recv && Pm) {
