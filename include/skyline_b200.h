@@ -170,7 +170,8 @@ SKY_API int sky_ctx_set_sharded(sky_ctx* ctx, int on);
  * "merge_head", "grain_items" (work granularity), "bnl_block" (rows per
  * BNL block, one CTA each; 0 = one CTA per partition), "merge_index" (1:
  * merge through a cell index of the union), "merge_cell_rows" (its target
- * rows per cell), "profile_host",
+ * rows per cell), "range_par" (ranges per work item from which each warp
+ * takes whole comparator ranges; 0 = never), "profile_host",
  * "timeline" (diagnostics on stderr). SKY_E_CONFIG for an unknown name. */
 SKY_API int sky_ctx_set_option(sky_ctx* ctx, const char* name, int64_t value);
 SKY_API const char* sky_last_error(const sky_ctx* ctx);

@@ -42,6 +42,7 @@ struct sky_options {
     uint32_t bnl_block = 2048;  // BNL: rows per block (one CTA each), 0 = one CTA per partition
     int32_t merge_index = 1;    // merge through the cell index of the union (host-planned merges)
     uint32_t merge_cell_rows = 1024;  // target rows per cell of that index
+    uint32_t range_par = 4;     // ranges per item from which warps take whole ranges (0: never)
     int32_t profile_host = 0;   // print host-side planning / wait times
     int32_t timeline = 0;       // an event after every launch, dumped per run
 };
@@ -814,6 +815,7 @@ class Runner {
             b.sxyz = a.sxyz; b.sskey = a.sskey; b.sqc = sq;
             b.items = di; b.n_items = a.n_items; b.ranges = dr; b.bounded = a.bounded; b.dead = a.dead;
             b.tests = a.tests; b.counter = misc + M_WORK;
+            b.range_par = c_->opt.range_par && plan.ranges.size() >= (size_t)c_->opt.range_par * plan.items.size();
             const int phase = a.tests ? (int)(a.tests - tests(0)) : 3;
             b.coarse_hits = reinterpret_cast<unsigned long long*>(misc + M_HITS) + phase;
             launch_relsky2(D, (int)plan.tile, b, c_->sm_count, st_);
@@ -948,14 +950,15 @@ class Runner {
             SKY_CUDA(cudaMemcpyAsync(dgb, hgb, (np + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
             launch_plan_items(dnew, np, dgb, dg, max_groups, tile, di, nitems, st_);
             count();
-            relsky_dev(D, tile, base, cq, sq, dense, di, (uint32_t)cap, nitems, dr);
+            relsky_dev(D, tile, base, cq, sq, dense, di, (uint32_t)cap, nitems, dr,
+                       c_->opt.range_par && ranges.size() >= (size_t)c_->opt.range_par * groups.size());
         }
     }
 
     // One relsky launch over device-built items (count in device memory).
     void relsky_dev(int D, uint32_t tile, const RelskyArgs& base, const uint2* cq, const uint2* sq,
                     const uint32_t* dense, const Item* items, uint32_t cap, const uint32_t* n_items_dev,
-                    const uint2* ranges) {
+                    const uint2* ranges, bool range_par = false) {
         if (x64_.x && (!base.sid || !base.cid))
             throw Error(SKY_E_INTERNAL, "FP64 confirmation needs the row ids of both sets");
         uint32_t* misc = dev<uint32_t>(S_MISC, 64);
@@ -966,6 +969,7 @@ class Runner {
         b.x64 = x64_; b.cid = base.cid; b.sid = base.sid;
         b.sxyz = base.sxyz; b.sskey = base.sskey; b.sqc = sq;
         b.items = items; b.n_items = cap; b.n_items_dev = n_items_dev; b.ranges = ranges;
+        b.range_par = range_par;
         b.bounded = base.bounded; b.dead = base.dead;
         b.tests = base.tests; b.counter = misc + M_WORK;
         const int phase = base.tests ? (int)(base.tests - tests(0)) : 3;

@@ -252,6 +252,10 @@ struct Relsky2Args {
     const uint32_t* sid;      // row id of each comparator position
     const uint32_t* n_items_dev;  // optional: item count in device memory (n_items = capacity)
     bool direct;                  // items hold their comparator range itself in (lb, le)
+    // many short ranges per item (cell-indexed lists): each warp takes whole
+    // ranges (w, w + 8, ...) instead of every 8th batch of each range, so no
+    // range is a short burst shared by eight warps
+    bool range_par = false;
 };
 // tile = candidates per item (<= 32 * 8, one warp); picks K from it.
 void launch_relsky2(int D, int tile, const Relsky2Args& a, int sm_count, cudaStream_t st);

@@ -270,10 +270,12 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 
         // direct items carry their one comparator range in (lb, le)
         const uint32_t r_end = a.direct ? it.lb + 1 : it.le;
-        for (uint32_t r = it.lb; live && r < r_end; ++r) {
+        const bool rpar = a.range_par && !a.direct;
+        const uint32_t bstep = rpar ? 32u : 32u * RS3_WARPS;
+        for (uint32_t r = it.lb + (rpar ? warp : 0); live && r < r_end; r += rpar ? RS3_WARPS : 1) {
             const uint2 rg = a.direct ? make_uint2(it.lb, it.le) : a.ranges[r];
             const uint32_t sb = rg.x, se = range_end(a, rg);
-            uint32_t base = sb + warp * 32;
+            uint32_t base = sb + (rpar ? 0u : warp * 32u);
             if (base >= se) continue;
             // prefetch this warp's first batch
             uint32_t idx = base + lane;
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 #pragma unroll
                 for (int v = 0; v < W; ++v) nx[v] = x[v];
             }
-            for (; base < se; base += 32 * RS3_WARPS) {
+            for (; base < se; base += bstep) {
                 // fold in kills published by the other warps
                 const uint32_t dm = sm.deadmask[lane];
                 if (dm & alive) {
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
 #pragma unroll
                 for (int v = 0; v < W; ++v) sm.comp[warp][lane][v] = nx[v];
                 __syncwarp();
-                idx = base + 32 * RS3_WARPS + lane;
+                idx = base + bstep + lane;
                 if (lim == 32 && idx < se) {
                     nq = a.sqc[idx];
                     nk = a.sskey[idx];
