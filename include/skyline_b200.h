@@ -239,6 +239,14 @@ SKY_API void sky_free(void* ptr);
  * anticorrelated (s~N(0.5,0.0625) + rejection), 3 correlated, 5 ints [0,16).
  * Deterministic for (kind, n, d, seed) regardless of thread count. */
 SKY_API int sky_generate(int kind, uint64_t n, uint32_t d, uint64_t seed, float* out);
+/* The same rows generated on the context's device (dev_out: n*d floats of
+ * device memory): chunk c's mt19937_64 stream in one CTA, rows consumed in
+ * stream order (the rejection loop of kinds 2/4 by a warp testing 32
+ * attempts per step). Integer-only kinds 1 and 5 equal sky_generate bit for
+ * bit; kinds 2-4 use CUDA's log / cos in the normals and equal it wherever
+ * those round like the host libm (every BASELINE config at full size, see
+ * tests/test_generate_gpu.py). */
+SKY_API int sky_generate_device(sky_ctx* ctx, int kind, uint64_t n, uint32_t d, uint64_t seed, float* dev_out);
 
 /* ---- Data in and out (datagen.hpp / io.hpp of the reference) ------------ */
 /* Distribution (datagen.hpp:12-16). */

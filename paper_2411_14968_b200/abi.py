@@ -101,7 +101,7 @@ EXPORTED = [
     "sky_plan_split", "sky_plan_local_shards", "sky_plan_merge_shards", "sky_abi_version",
     "sky_generate_family", "sky_normalize", "sky_ingest_csv", "sky_write_csv", "sky_host_error",
     "sky_ctx_create_group", "sky_ctx_world", "sky_ctx_set_sharded", "sky_run_shard", "sky_ctx_set_option",
-    "sky_ctx_create_peers", "sky_issue_peak", "sky_device_count",
+    "sky_ctx_create_peers", "sky_issue_peak", "sky_device_count", "sky_generate_device",
 ]
 
 SKY_GROUP_LOOPBACK = 1
@@ -166,6 +166,7 @@ def load():
                                           _u32p]
     lib.sky_issue_peak.argtypes = [vp, C.c_uint32, C.c_int, C.c_int, C.c_uint32, C.POINTER(C.c_double)]
     lib.sky_device_count.restype = C.c_int
+    lib.sky_generate_device.argtypes = [vp, C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, vp]
     lib.sky_abi_version.restype = C.c_int
     _lib = lib
     return lib

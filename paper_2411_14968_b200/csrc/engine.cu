@@ -1252,6 +1252,26 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
 
 void sky_free(void* p) { std::free(p); }
 
+int sky_generate_device(sky_ctx* c, int kind, uint64_t n, uint32_t d, uint64_t seed, float* dev_out) {
+    c = single_gpu(c);
+    return guarded(c, [&] {
+        if (kind < 1 || kind > 5 || d < 1) throw Error(SKY_E_CONFIG, "generator kind 1..5 and d >= 1");
+        if (!n) return;
+        uint32_t* stuck = static_cast<uint32_t*>(c->dev.get(S_GCOUNT, 64));
+        SKY_CUDA(cudaMemsetAsync(stuck, 0, sizeof(uint32_t), c->stream));
+        launch_generate_baseline(kind, n, d, seed, dev_out, stuck, c->stream);
+        uint32_t h = 0;
+        SKY_CUDA(cudaMemcpyAsync(&h, stuck, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        SKY_CUDA(cudaStreamSynchronize(c->stream));
+        if (h) {
+            // a rejection loop outran the device ring: the host generator
+            std::vector<float> rows(n * d);
+            if (sky_generate(kind, n, d, seed, rows.data()) != SKY_OK) throw Error(SKY_E_CONFIG, "generator failed");
+            SKY_CUDA(cudaMemcpy(dev_out, rows.data(), rows.size() * sizeof(float), cudaMemcpyHostToDevice));
+        }
+    });
+}
+
 int sky_issue_peak(sky_ctx* c, uint32_t d, int k, int ctas_per_sm, uint32_t iters, double* tests_per_s) {
     c = single_gpu(c);
     return guarded(c, [&] {

@@ -2018,6 +2018,7 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
         uint64_t pairs = 0;
         for (uint32_t cell = icb; cell < ice; ++cell) pairs += (uint64_t)(coff[cell + 1] - coff[cell]) * cmp_rows[cell] / 2;
         R.pick_grain(D, coff[ice] - coff[icb], pairs, &mp.tile, &mp.chunk);
+        if (c->opt.merge_tile) mp.tile = c->opt.merge_tile;
         ma.cxyz = UC.xyz; ma.cskey = UC.skey; ma.cid = UC.id;
         ma.sxyz = UC.xyz; ma.sskey = UC.skey; ma.sid = UC.id;
         R.relsky_waves(D, coff, icb, ice, comps_of, ma, UC.qc, UC.qc, mp.tile, mp.chunk, c->opt.merge_head);

@@ -348,6 +348,12 @@ void launch_part_cell_keys(int D, const uint2* qc, const uint32_t* skey, const u
 // dead[rows[i]] |= flag[i]
 void launch_scatter_dead(const uint8_t* flag, const uint32_t* rows, uint32_t n, uint8_t* dead, cudaStream_t st);
 
+// The BASELINE synthetic inputs (include/skyline_baseline_gen.h) generated
+// on the device, n x d float32 rows into out (kind 1..5); *stuck set if a
+// rejection loop outran the stream ring (the caller then uses the host).
+void launch_generate_baseline(int kind, uint64_t n, uint32_t d, uint64_t seed, float* out, uint32_t* stuck,
+                              cudaStream_t st);
+
 // Partitions off[P+1] cut into blocks of <= `block` rows: sub[cap+1] block
 // offsets (empty blocks pad the tail up to cap).
 void launch_split_segments(const uint32_t* off, uint32_t P, uint32_t block, uint32_t* sub, uint32_t cap,

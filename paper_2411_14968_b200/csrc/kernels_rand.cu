@@ -266,6 +266,189 @@ __global__ void k_fy_final(uint32_t n, uint64_t p, const uint32_t* __restrict__ 
     pid[v] = (uint32_t)(k % p);
 }
 
+
+// ------------------------------------------------------------ generators
+// The BASELINE inputs (include/skyline_baseline_gen.h) on the device: chunk
+// c of 65,536 rows is one CTA running its own mt19937_64 stream (seed ^
+// 0x9E3779B97F4A7C15 * (c + 1)) block by block into a shared-memory ring
+// (threads 0..155 as in mt_generate) while the rows consume it in stream
+// order. Rows with a fixed number of draws (kinds 1, 3, 5) are converted by
+// all threads in parallel; the anti-correlated rejection loop (kinds 2, 4)
+// is one warp testing 32 consecutive attempts per step (a ballot picks the
+// first accepted). Host arithmetic is restated exactly (no FMA contraction;
+// float uniforms from 24 bits); the normals go through CUDA's log / cos,
+// so kinds 2-4 equal the host generator wherever those round like the host
+// libm (checked at the BASELINE sizes by tests/test_generate_gpu.py).
+constexpr uint32_t GEN_RING = 32;         // blocks of 312 draws in the ring (78 KB)
+constexpr uint32_t GEN_THREADS = 192;
+constexpr uint64_t GEN_CHUNK = 65536;
+
+__device__ __forceinline__ float gen_f32(uint64_t x) { return (float)(mt_temper(x) >> 40) * 0x1.0p-24f; }
+__device__ __forceinline__ double gen_u01(uint64_t x) { return (double)(mt_temper(x) >> 11) * 0x1.0p-53; }
+__device__ __forceinline__ double gen_u01_pos(uint64_t x) { return (double)((mt_temper(x) >> 11) + 1) * 0x1.0p-53; }
+// Rng::normal (rng.hpp:31-37): mean + stddev * r * cos(2 pi u2), evaluated
+// in the host's order without contraction
+__device__ __forceinline__ double gen_normal(uint64_t x1, uint64_t x2, double mean, double stddev) {
+    const double u1 = gen_u01_pos(x1), u2 = gen_u01(x2);
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    const double c = cos(__dmul_rn(6.283185307179586476925286766559, u2));
+    return __dadd_rn(mean, __dmul_rn(__dmul_rn(stddev, r), c));
+}
+__device__ __forceinline__ double gen_clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+__global__ void __launch_bounds__(GEN_THREADS) k_gen_baseline(int kind, uint64_t n, uint32_t d, uint64_t seed,
+                                                               float* __restrict__ out, uint32_t* stuck) {
+    extern __shared__ uint64_t ring[];  // [GEN_RING * MT_N]
+    __shared__ uint64_t init[MT_N];
+    __shared__ uint64_t sA[2][8], sB[2][8], sA1[2];
+    __shared__ unsigned long long s_pos;  // next unconsumed draw (stream index)
+    __shared__ unsigned long long s_q;    // anti-correlated: next attempt of the row at s_pos (0: none yet)
+    __shared__ uint32_t s_row;            // next row of the chunk
+    const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint64_t c = blockIdx.x, r0 = c * GEN_CHUNK;
+    const uint32_t rows = (uint32_t)min(GEN_CHUNK, n - r0);
+    if (t == 0) {
+        init[0] = seed ^ (0x9E3779B97F4A7C15ull * (c + 1));
+        for (int i = 1; i < MT_N; ++i)
+            init[i] = 6364136223846793005ull * (init[i - 1] ^ (init[i - 1] >> 62)) + (uint64_t)i;
+        s_pos = 0;
+        s_q = 0;
+        s_row = 0;
+    }
+    __syncthreads();
+    uint64_t A = 0, B = 0;
+    if (t < MT_M) {
+        A = init[t];
+        B = init[MT_M + t];
+    }
+    const bool fixed = kind == 1 || kind == 3 || kind == 5;
+    const uint32_t per = kind == 3 ? 2 + 2 * d : d;  // draws per row (fixed kinds)
+    uint64_t made = 0;                                  // draws generated so far
+    uint32_t par = 0;
+    while (true) {
+        // produce one block if the ring has room past the unconsumed draws
+        const uint64_t pos = s_pos;
+        const bool room = made + MT_N <= pos - pos % MT_N + (uint64_t)(GEN_RING - 1) * MT_N;
+        if (room) {
+            if (t < MT_M && lane == 0) {
+                sA[par][w] = A;
+                sB[par][w] = B;
+            }
+            if (t == 1) sA1[par] = A;
+        }
+        __syncthreads();
+        if (room) {
+            const uint64_t An = __shfl_down_sync(0xffffffffu, A, 1);
+            const uint64_t Bn = __shfl_down_sync(0xffffffffu, B, 1);
+            if (t < MT_M) {
+                uint64_t A1, B1;
+                if (t + 1 == MT_M) {
+                    A1 = sB[par][0];
+                    B1 = sB[par][0] ^ mt_tw(sA[par][0], sA1[par]);
+                } else if (lane == 31) {
+                    A1 = sA[par][w + 1];
+                    B1 = sB[par][w + 1];
+                } else {
+                    A1 = An;
+                    B1 = Bn;
+                }
+                const uint64_t v0 = B ^ mt_tw(A, A1), v1 = v0 ^ mt_tw(B, B1);
+                const uint32_t slot = (uint32_t)((made / MT_N) % GEN_RING) * MT_N;
+                ring[slot + t] = v0;
+                ring[slot + MT_M + t] = v1;
+                A = v0;
+                B = v1;
+            }
+            made += MT_N;
+            par ^= 1;
+        }
+        __syncthreads();
+        // consume: rows whose draws are all in the ring
+        if (fixed) {
+            const uint32_t row0 = s_row;
+            const uint64_t ready = made / per;
+            const uint32_t avail_rows = ready < rows ? (uint32_t)ready : rows;
+            for (uint32_t r = row0 + t; r < avail_rows; r += GEN_THREADS) {
+                const uint64_t p = (uint64_t)r * per;
+                float* x = out + (r0 + r) * d;
+                auto at = [&](uint64_t q) { return ring[(uint32_t)(q % (GEN_RING * MT_N))]; };
+                if (kind == 1) {
+                    for (uint32_t j = 0; j < d; ++j) x[j] = gen_f32(at(p + j));
+                } else if (kind == 5) {
+                    for (uint32_t j = 0; j < d; ++j) x[j] = (float)(mt_temper(at(p + j)) >> 60);
+                } else {
+                    const double v = gen_clip01(gen_normal(at(p), at(p + 1), 0.5, 0.25));
+                    for (uint32_t j = 0; j < d; ++j)
+                        x[j] = (float)gen_clip01(__dadd_rn(v, gen_normal(at(p + 2 + 2 * j), at(p + 3 + 2 * j), 0.0, 0.05)));
+                }
+            }
+            __syncthreads();
+            if (t == 0) {
+                s_row = avail_rows;
+                s_pos = (uint64_t)avail_rows * per;
+            }
+            __syncthreads();
+            if (avail_rows >= rows) break;
+        } else {
+            // one warp: s (2 draws), then attempts of d uniforms until one
+            // lands within the tolerance; 32 attempts per step
+            if (w == 0) {
+                uint64_t p = s_pos, q0 = s_q;
+                uint32_t r = s_row;
+                const uint64_t lim = made;
+                const double tol = __dmul_rn(0.01, (double)d);
+                while (r < rows) {
+                    // the row's s and a full step of attempts must be in the ring
+                    const uint64_t qs = q0 ? q0 : p + 2;
+                    if (qs + 32ull * d > lim) break;
+                    auto at = [&](uint64_t q) { return ring[(uint32_t)(q % (GEN_RING * MT_N))]; };
+                    const double s = gen_clip01(gen_normal(at(p), at(p + 1), 0.5, 0.0625));
+                    const double target = __dmul_rn((double)d, s);
+                    uint64_t q = qs;
+                    bool done = false;
+                    while (!done) {
+                        if (q + 32ull * d > lim) break;
+                        double sum = 0.0;
+                        for (uint32_t j = 0; j < d; ++j) sum = __dadd_rn(sum, (double)gen_f32(at(q + lane * d + j)));
+                        const bool ok = fabs(__dsub_rn(sum, target)) <= tol;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                        if (bal) {
+                            const uint32_t win = __ffs(bal) - 1;
+                            const uint64_t qa = q + (uint64_t)win * d;
+                            float* x = out + (r0 + r) * d;
+                            for (uint32_t j = lane; j < d; j += 32) x[j] = gen_f32(at(qa + j));
+                            q = qa + d;
+                            done = true;
+                        } else {
+                            q += 32ull * d;
+                        }
+                    }
+                    if (!done) {  // more draws needed: resume this row at attempt q
+                        q0 = q;
+                        break;
+                    }
+                    p = q;
+                    q0 = 0;
+                    ++r;
+                }
+                if (lane == 0) {
+                    s_pos = p;
+                    s_q = q0;
+                    s_row = r;
+                }
+            }
+            __syncthreads();
+            if (s_row >= rows) break;
+            // a row whose attempts outrun the whole ring (probability below
+            // 1e-30 per row): report it, the caller generates on the host
+            if (!room && (s_q ? s_q : s_pos + 2) + 32ull * d > made) {
+                if (t == 0) atomicOr(stuck, 1u);
+                break;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 size_t random_scratch_bytes(uint32_t n) {
@@ -347,6 +530,16 @@ size_t random_cub_bytes(uint32_t n) {
     cub::DeviceRadixSort::SortPairs(nullptr, need, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n - 1), 0, 32, (cudaStream_t)0);
     return need;
+}
+
+void launch_generate_baseline(int kind, uint64_t n, uint32_t d, uint64_t seed, float* out, uint32_t* stuck,
+                              cudaStream_t st) {
+    if (!n) return;
+    const uint64_t chunks = (n + GEN_CHUNK - 1) / GEN_CHUNK;
+    const size_t smem = (size_t)GEN_RING * MT_N * sizeof(uint64_t);
+    ensure_smem_attr((const void*)k_gen_baseline, smem);
+    k_gen_baseline<<<(unsigned)chunks, GEN_THREADS, smem, st>>>(kind == 4 ? 2 : kind, n, d, seed, out, stuck);
+    SKY_LAUNCH_CHECK();
 }
 
 }  // namespace sky

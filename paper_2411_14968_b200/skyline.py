@@ -294,6 +294,12 @@ class Engine:
         self._err(self._lib.sky_issue_peak(self._h, int(d), int(k), int(ctas_per_sm), int(iters), C.byref(v)))
         return float(v.value)
 
+    def generate_device(self, kind: int, n: int, d: int, seed: int, device_ptr: int):
+        """The BASELINE synthetic rows (as `generate`) written by the GPU into
+        n*d float32 of device memory at device_ptr (sky_generate_device)."""
+        self._err(self._lib.sky_generate_device(self._h, int(kind), int(n), int(d), int(seed),
+                                                C.c_void_p(device_ptr)))
+
     def set_sharded(self, on: bool = True):
         """Take the sharded multi-rank path even on one rank (tests)."""
         self._err(self._lib.sky_ctx_set_sharded(self._h, int(bool(on))))

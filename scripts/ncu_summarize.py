@@ -72,6 +72,8 @@ def summarize_launches(path):
             continue
         if r[ki].startswith("void at::"):  # bench.py's L2 flush (torch), not an engine kernel
             continue
+        if "k_issue_peak" in r[ki]:  # bench.py's issue-peak microbenchmark, outside the timed steps
+            continue
         v = float(r[vi].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki].split("(")[0]
         agg[name][0] += 1
