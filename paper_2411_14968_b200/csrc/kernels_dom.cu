@@ -170,6 +170,9 @@ __device__ __forceinline__ bool any_coarse_pass(const uint32_t (&T)[K][2], const
 
 constexpr int RS3_WARPS = 8;
 constexpr int RS3_THREADS = RS3_WARPS * 32;
+#ifndef RS3_MINB
+#define RS3_MINB 2
+#endif
 
 template <int D>
 __device__ __forceinline__ bool dominates_exact(const float4* __restrict__ s, const float4* __restrict__ t) {
@@ -211,7 +214,7 @@ struct Relsky3Smem {
 };
 
 template <int D, int K>
-__global__ void __launch_bounds__(RS3_THREADS, 2) k_relsky3(Relsky2Args a) {
+__global__ void __launch_bounds__(RS3_THREADS, RS3_MINB) k_relsky3(Relsky2Args a) {
     constexpr int W = Dims2<D>::V;
     constexpr uint32_t G = CodeLayout<D>::G;
     constexpr uint32_t FULL = 0xffffffffu;
@@ -1385,8 +1388,10 @@ __global__ void __launch_bounds__(1024) k_plan_partition_items(const uint32_t* _
             const uint64_t nc = coff[P] - coff[0];
             const uint64_t ns = n_comp ? *n_comp : (uint64_t)(soff[P] - soff[0]);
             const uint64_t pairs = nc * ns / 2;
+            // small sets: down to 256 comparators per item, so a few hundred
+            // rows still spread over many SMs
             uint32_t ch = 16384;
-            while (ch > 2048 && pairs / ((uint64_t)tile * ch) < grain_target) ch /= 2;
+            while (ch > 256 && pairs / ((uint64_t)tile * ch) < grain_target) ch /= 2;
             s_chunk = ch;
         }
         __syncthreads();
