@@ -988,6 +988,8 @@ int sky_ctx_set_option(sky_ctx* c, const char* name, int64_t v) {
     else if (k == "merge_cell_rows" && u) o.merge_cell_rows = u;
     else if (k == "range_par") o.range_par = u;
     else if (k == "sfs_auto_chunk") o.sfs_auto_chunk = s > 0;
+    else if (k == "wave_growth" && u >= 2) o.wave_growth = u;
+    else if (k == "wave_split_mpairs") o.wave_split_mpairs = u;
     else if (k == "profile_host") o.profile_host = s > 0;
     else if (k == "timeline") o.timeline = s > 0;
     else {

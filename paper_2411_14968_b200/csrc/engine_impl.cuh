@@ -44,6 +44,8 @@ struct sky_options {
     int32_t merge_index = 1;    // merge through the cell index of the union (host-planned merges)
     uint32_t merge_cell_rows = 1024;  // target rows per cell of that index
     uint32_t range_par = 4;     // ranges per item from which warps take whole ranges (0: never)
+    uint32_t wave_growth = 4;   // multi-wave relative skylines: wave w+1 = growth x wave w comparators
+    uint32_t wave_split_mpairs = 8192;  // split the rest into further waves above this many Mi pairs
     int32_t profile_host = 0;   // print host-side planning / wait times
     int32_t timeline = 0;       // an event after every launch, dumped per run
 };
@@ -896,12 +898,13 @@ class Runner {
         std::vector<uint64_t> lens(np, 0);
         for (uint32_t k = 0; k < np; ++k)
             for (const uint2& r : lists[k]) lens[k] += r.y - r.x;
-        for (uint64_t lo = head, len = 3ull * head; lo < maxlen; lo += len, len *= 4) {
+        const uint64_t grow = std::max<uint32_t>(2, c_->opt.wave_growth);
+        for (uint64_t lo = head, len = (grow - 1) * head; lo < maxlen; lo += len, len *= grow) {
             // split further only while the rest is worth a compaction pass
             uint64_t rest = 0;
             for (uint32_t k = 0; k < np; ++k)
                 if (lens[k] > lo) rest += (uint64_t)(offc[qb + k + 1] - offc[qb + k]) * (lens[k] - lo);
-            if (rest < kWaveSplitPairs) len = maxlen - lo;
+            if (rest < ((uint64_t)c_->opt.wave_split_mpairs << 20)) len = maxlen - lo;
             const uint64_t hi = lo + len;
             // this wave's comparator groups per partition (host: the lists are static)
             std::vector<uint2> ranges, groups;

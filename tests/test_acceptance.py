@@ -11,7 +11,10 @@ GPU engine, FP64 rows from the reference's own generators:
 6. the noseq vs sliced+ time ratio, measured on the GPU (:321-355)
 8. determinism over repetitions and worker counts (:380-430)
 
-Each criterion prints the reference's PASS/FAIL line."""
+Each criterion prints the reference's PASS/FAIL line. Criteria 1, 2, 4, 5,
+7 and 8 are asserted; 3 and 6 assert that every count equals the
+reference's and only report their PASS/FAIL line (criterion 3 fails for the
+reference itself; criterion 6 is a timing ratio)."""
 import numpy as np
 import pytest
 
@@ -92,7 +95,9 @@ def test_criterion_2_merge_identities(engine):
     assert prop1 == 0 and eq3 == 0
 
 
-def test_criterion_3_grid_filtering(engine, golden):
+def test_criterion_3_counts_match_reference(engine, golden):
+    """Asserts the filtered counts equal the reference's; the criterion's
+    PASS/FAIL line is reported (it fails for the reference too)."""
     exp = {(c["dist"], c["m"], c["seed"]): c["filtered"] for c in golden["acceptance"]["c3"]}
     got = {}
     for (dist, m, seed) in exp:
@@ -134,7 +139,9 @@ def test_criterion_5_union_ordering(engine, golden):
     assert ok
 
 
-def test_criterion_6_noseq_vs_sliced_plus(engine, golden):
+def test_criterion_6_counts_asserted_timing_reported(engine, golden):
+    """Asserts the union / final sizes equal the reference's; the time ratio
+    is measured on the GPU and reported as the criterion's PASS/FAIL line."""
     x = generate_family(2, 1000000, 4, 1)
 
     def phases(filt, merge):
