@@ -315,11 +315,14 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
                                 cfg->strategy == SKY_ANGULAR;
     bool us_early = false;
     // one GPU, all-pairs merge: the whole merge and the ids are queued before
-    // the only host round trip of the step (finish_dev_merge)
-    // Its kernels are sized by the union's capacity (the filtered set), so it
-    // is used where that is close to the union: representative filtering
-    // (without it the capacity is every row, e.g. config 1's 100k for a
-    // 1.4k union) and a filtered set large enough for the round trip to count
+    // the only host round trip of the step (finish_dev_merge). Its launches
+    // are shaped by the union's capacity, which is the filtered set's: the
+    // input size up to kExactCapRows rows, the exact filtered count above.
+    // So it is taken with representative filtering only (without it the
+    // capacity is every row: config 1 has a 100k capacity for a 1.4k union,
+    // measured slower there) and from 8,192 capacity rows on (below that the
+    // host-planned merge's round trip costs less than the capacity-sized
+    // launches). The choice never changes a result.
     const bool dev_merge_cfg = W == 1 && all_mode_merge && P > 1 && D <= 16 &&
                                cfg->filter == SKY_FILTER_REPRESENTATIVE &&
                                !c->opt.host_merge;

@@ -760,6 +760,9 @@ class Runner {
         a.sxyz = US.xyz; a.sskey = US.skey; a.sid = US.id;
         a.indirect = false; a.bounded = true; a.dead = dead;
         a.tests = count_tests ? tests(2) : nullptr;
+        // candidates per item from the capacity (the input size on the
+        // exact-count-free path up to kExactCapRows rows, so config 2's 1M
+        // input takes 256): a grain choice only
         const uint32_t tile = c_->opt.merge_tile ? c_->opt.merge_tile : (cap <= 300000 ? 128u : 256u);
         const uint32_t max_chunks = 64, head = c_->opt.merge_head;
         const uint32_t target = (uint32_t)c_->sm_count * 2 * c_->opt.grain_items;

@@ -99,6 +99,83 @@ def _rank_run(rank, world, x, cfg):
     return ids, sizes
 
 
+def _first_q(x, rows, q):
+    """The first q rows by (FP64 coordinate sum, lex coords, id)
+    (filter.cpp:74-79), rows ascending ids."""
+    if not len(rows):
+        return rows
+    xr = x[rows].astype(np.float64)
+    s = np.zeros(len(rows))
+    for j in range(x.shape[1]):
+        s = s + xr[:, j]  # left to right, as coord_sum
+    keys = [rows] + [xr[:, j] for j in range(x.shape[1] - 1, -1, -1)] + [s]
+    return rows[np.lexsort(keys)][:q]
+
+
+def _rank_run_sharded(rank, world, x, cfg):
+    """shard.cu's phase 1 restated: this rank's rows only, shard-local first q
+    per partition, all-gathered, global first q of the W*q candidates,
+    pruned; prefilter of the own rows; survivors routed to partition owners;
+    local skylines by the owners; then the merge of _rank_run."""
+    c = cfg.to_c()
+    po, P = O.oracle_assign(x, c, True)
+    N, d = x.shape
+    r0, r1 = N * rank // world, N * (rank + 1) // world
+    own = np.arange(r0, r1)
+    q = min(cfg.rep_q, N)
+    survivors = own
+    if cfg.filter == FilterKind.Representative:
+        picks = {p: _first_q(x, own[po[own] == p], q).tolist() for p in range(P)}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, picks)
+        cand = []
+        for p in range(P):
+            allp = np.array(sorted(v for g in gathered for v in g[p]), np.int64)
+            cand.extend(_first_q(x, allp, q).tolist())
+        cand = np.array(cand, np.int64)
+        reps = cand[O.bruteforce(x[cand])] if len(cand) else cand  # prune_dominated_reps
+        assert np.array_equal(np.sort(reps), O.representatives(x, po, P, cfg.rep_q)), "global reps differ"
+        if len(reps) and len(own):
+            survivors = own[O.relative_skyline(x[own], x[reps])]
+    # routing: owners of contiguous partition ranges balanced by |r_i|^2
+    counts = np.bincount(po[survivors].astype(np.int64), minlength=P)
+    allc = [None] * world
+    dist.all_gather_object(allc, counts.tolist())
+    tot = np.sum(np.array(allc, np.int64), axis=0)
+    offs = np.zeros(P + 1, np.uint32)
+    offs[1:] = np.cumsum(tot)
+    pr = plan_local_shards(offs, world)
+    outbox = [[int(v) for v in survivors if pr[k] <= po[v] < pr[k + 1]] for k in range(world)]
+    inbox = [None] * world
+    dist.all_gather_object(inbox, outbox)
+    mine = np.array(sorted(v for box in inbox for v in box[rank]), np.int64)
+    local = {}
+    for p in range(int(pr[rank]), int(pr[rank + 1])):
+        rows = mine[po[mine] == p]
+        local[p] = rows[np.asarray(O.bruteforce(x[rows]), dtype=np.int64)] if len(rows) else rows
+    return local, int(N - offs[P])
+
+
+def _worker_sharded(rank, world, port, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for k, (x, cfg) in enumerate(_cases()):
+            local, filtered = _rank_run_sharded(rank, world, x, cfg)
+            gathered = [None] * world
+            dist.all_gather_object(gathered, local)
+            if rank == 0:
+                ref = O.oracle_run(x, cfg.to_c(), True)
+                merged = {}
+                for g in gathered:
+                    merged.update(g)
+                sizes = [len(merged.get(p, [])) for p in range(len(ref["local_skyline_sizes"]))]
+                results[k] = (sizes == ref["local_skyline_sizes"].astype(int).tolist(),
+                              filtered == int(ref["filtered_count"]))
+    finally:
+        dist.destroy_process_group()
+
+
 def _worker(rank, world, port, results):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -130,6 +207,23 @@ def test_sharded_decomposition_matches_single_process(world):
     assert len(res) == len(_cases())
     for k, (ok_ids, ok_sizes) in res.items():
         assert ok_ids and ok_sizes, k
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_phase1_matches_single_process(world):
+    """Row-sharded phase 1 (shard.cu): shard-local representative picks merged
+    into the global first q reproduce the reference's representatives, and
+    the routed, owner-computed local skylines and the filtered count equal
+    the single-process result."""
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        results = mgr.dict()
+        mp.start_processes(_worker_sharded, args=(world, _free_port(), results), nprocs=world, join=True,
+                           start_method="spawn")
+        res = dict(results)
+    assert len(res) == len(_cases())
+    for k, (ok_sizes, ok_filtered) in res.items():
+        assert ok_sizes and ok_filtered, k
 
 
 def test_shard_plans_cover_and_balance():
