@@ -72,6 +72,26 @@ def ncu_traffic(tag):
     return None, None
 
 
+def ncu_pipe_mix(tag):
+    """alu / fma pipe utilisation, warps active and SM clock of the dominance
+    kernel (k_relsky3, duration-weighted over the launches) from the
+    committed `ncu --set full` summary, or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                launches = [e for e in (json.load(f).get(tag) or []) if "relsky3" in e.get("kernel", "")]
+        except (OSError, ValueError):
+            continue
+        if launches:
+            w = sum(e.get("duration_ms", 0.0) for e in launches) or 1.0
+            mix = {k: sum(e.get(k, 0.0) * e.get("duration_ms", 0.0) for e in launches) / w
+                   for k in ("alu_pipe_pct", "fma_pipe_pct", "warps_active_pct", "sm_throughput_pct")}
+            mix["source"] = os.path.relpath(path, ROOT) + f" [{tag}, {len(launches)} k_relsky3 launches]"
+            return mix
+    return None
+
+
 def ncu_stream_traffic(tag):
     """DRAM bytes (read + write) per step of the HBM streaming passes from the
     committed ncu summary (`stream` entries), or (None, None)."""
@@ -433,6 +453,7 @@ def run_ours(args):
         },
         "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / statistics.mean(dev_ms),
         "tests_per_step": dom_tests,
+        "ncu_pipe_mix": ncu_pipe_mix(f"c{args.config}"),
     }
 
     # HBM streaming passes (prep, representative prefilter, candidate pass):
