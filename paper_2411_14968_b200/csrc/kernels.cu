@@ -194,8 +194,12 @@ __device__ __forceinline__ uint32_t angular_slice_exact(double y, double x, cons
             continue;          \
     }
 
-template <int DMAX, class Row>
+// ST >= 0: the strategy as a compile-time constant (the streamed kernels are
+// instantiated per strategy, so no other strategy's code is on the row
+// path); ST < 0: a.strategy at run time.
+template <int DMAX, class Row, int ST = -1>
 __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, const Row& R) {
+    const int strategy = ST >= 0 ? ST : a.strategy;
     constexpr int U = Row::kUnroll;
     const int d = (int)a.d;
     double sum = 0.0;
@@ -216,8 +220,8 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
         return e;
     };
-    const float upper = a.normalized || a.strategy == SKY_GRID ? 1.0f : 3.402823466e38f;
-    if (a.strategy == SKY_GRID && Row::kF32) {
+    const float upper = a.normalized || strategy == SKY_GRID ? 1.0f : 3.402823466e38f;
+    if (strategy == SKY_GRID && Row::kF32) {
         // float rows: the comparisons give the same answers in FP32 as on the
         // exact upcast; cell = floor(x * m) from the product rounded toward
         // zero (floor(x*m) < m <= 2^22 is representable, so rz(x*m) lies in
@@ -238,7 +242,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
         if (!ok) err = f32_errors(true);
         pid = pid32;
-    } else if (a.strategy == SKY_GRID) {
+    } else if (strategy == SKY_GRID) {
         // m^d <= kMaxPartitions (2^22): 32-bit cell arithmetic
         uint32_t stride = 1, pid32 = 0;
         const uint32_t m32 = (uint32_t)a.m;
@@ -257,7 +261,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
             stride *= m32;
         }
         pid = pid32;
-    } else if (a.strategy == SKY_ANGULAR) {
+    } else if (strategy == SKY_ANGULAR) {
         bool ok = true;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
@@ -389,8 +393,8 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
             if ((uint32_t)j == a.slice_dim) sv = R.f(j);
         }
         if (Row::kF32 && !ok) err = f32_errors(false);
-        if (a.strategy == SKY_RANDOM) pid = a.pid_in[i];
-        if (a.strategy == SKY_SLICED) a.slice_key[i] = canon_bits(sv);
+        if (strategy == SKY_RANDOM) pid = a.pid_in[i];
+        if (strategy == SKY_SLICED) a.slice_key[i] = canon_bits(sv);
     }
     if (err) {
         atomicOr(a.err, err);
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 // moves from the staged tile into registers with the widest shared load its
 // stride allows. With a.gmin set, also the per-CTA minimum key of every
 // partition (gmin[p * gridDim.x + blockIdx.x]; the stream path's representative bound).
-template <int DP>
+template <int DP, int ST>
 __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
     extern __shared__ __align__(16) char s_prep[];
     char* smem = s_prep;
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
 #pragma unroll
                 for (int j = 0; j < DP; ++j) R.v[j] = j < (int)d ? x[j] : 0.0f;
             }
-            const uint64_t key = prep_row<DP>(a, i, R);
+            const uint64_t key = prep_row<DP, RegRow<DP>, ST>(a, i, R);
             if (a.gmin) {
                 // read first: after the first rows most keys are above the minimum
                 const uint32_t p = (uint32_t)(key >> 32), k = (uint32_t)key;
@@ -473,8 +477,10 @@ uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count) {
     const size_t smem = stream_smem_bytes(d) + (size_t)P * sizeof(uint32_t);
     int per_sm = 4;
     SKY_DISPATCH_D(padded_dim(d), {
-        ensure_smem_attr((const void*)k_prep_stream<DT>, smem);
-        per_sm = occupancy_cached((const void*)k_prep_stream<DT>, (int)kStreamRows, smem);
+        ensure_smem_attr((const void*)k_prep_stream<DT, SKY_GRID>, smem);
+        ensure_smem_attr((const void*)k_prep_stream<DT, SKY_ANGULAR>, smem);
+        ensure_smem_attr((const void*)k_prep_stream<DT, -1>, smem);
+        per_sm = occupancy_cached((const void*)k_prep_stream<DT, -1>, (int)kStreamRows, smem);
     });
     per_sm = std::max(1, std::min(per_sm, 8));
     return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows), (uint32_t)per_sm * (uint32_t)sm_count));
@@ -486,7 +492,15 @@ void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
         // float rows, 16-byte aligned: persistent CTAs, bulk-copied row tiles
         const size_t smem = stream_smem_bytes(a.d) + (size_t)a.P * sizeof(uint32_t);
         const uint32_t grid = prep_stream_grid(a.n, a.d, a.P, sm_count);  // sets the smem attribute
-        SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT><<<grid, kStreamRows, smem, st>>>(a)));
+        // grid and angular rows get their own instantiations (the row path
+        // then holds only that strategy's code); random / sliced share one
+        if (a.strategy == SKY_GRID) {
+            SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT, SKY_GRID><<<grid, kStreamRows, smem, st>>>(a)));
+        } else if (a.strategy == SKY_ANGULAR) {
+            SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT, SKY_ANGULAR><<<grid, kStreamRows, smem, st>>>(a)));
+        } else {
+            SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT, -1><<<grid, kStreamRows, smem, st>>>(a)));
+        }
     } else {
         if (a.gmin) throw Error(SKY_E_INTERNAL, "partition minima need the streamed prep");
         k_prep<<<ceil_div(a.n, 256), 256, 0, st>>>(a);
