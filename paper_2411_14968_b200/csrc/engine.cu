@@ -156,7 +156,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     }
     // stream path: the prep pass also leaves each CTA's minimum key per
     // partition (the representative candidate bound)
-    const uint32_t prep_grid = stream ? prep_stream_grid(n, d, P, c->sm_count) : 0;
+    const uint32_t prep_grid = stream ? prep_stream_grid(n, d, P, c->sm_count, cfg->strategy) : 0;
     uint32_t* gmin = stream ? R.dev<uint32_t>(S_GMIN, (size_t)prep_grid * P) : nullptr;
     PartitionOut po = partition_phase(R, pts, n, d, normalized, cfg->strategy, P, m, cfg, pid_dev,
                                       &out->angular_host_fixups, eager,
@@ -267,7 +267,10 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             if (!launch_prefilter_append(D, pts, d, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.id, reps.n,
                                          nrep_dev, pthr, app, count_tests ? R.tests(1) : nullptr, c->smem_optin, st))
                 throw Error(SKY_E_INTERNAL, "stream prefilter not applicable");
-            R.hbm_end((uint64_t)n * (4ull * d + 8));  // rows + keys (survivor writes are few)
+            // rows (the rows' keys are staged too only when the device count
+            // of representatives calls for codes: not counted; survivor
+            // writes are few)
+            R.hbm_end((uint64_t)n * 4ull * d);
             R.count();
         } else if (reps.n > 0 && (R.hbm_begin(),  // an unmatched begin is overwritten by the next
                                   launch_prefilter(D, pts, d, po.idx, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr,

@@ -197,11 +197,12 @@ __device__ __forceinline__ uint32_t angular_slice_exact(double y, double x, cons
 // ST >= 0: the strategy as a compile-time constant (the streamed kernels are
 // instantiated per strategy, so no other strategy's code is on the row
 // path); ST < 0: a.strategy at run time.
-template <int DMAX, class Row, int ST = -1>
+template <int DMAX, class Row, int ST = -1, bool XD = false>
 __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, const Row& R) {
     const int strategy = ST >= 0 ? ST : a.strategy;
     constexpr int U = Row::kUnroll;
-    const int d = (int)a.d;
+    // XD: d == DMAX (every coordinate test below folds away at compile time)
+    const int d = XD ? DMAX : (int)a.d;
     double sum = 0.0;
     uint32_t err = 0;
     uint64_t pid = 0;
@@ -220,27 +221,35 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
         return e;
     };
+    // the range test on raw bits: a float lies in [+0, upper] iff its bits
+    // are <= upper's (negatives, -0.0 included, and NaN/inf have larger
+    // bits); -0.0 fails it and is then accepted by f32_errors
     const float upper = a.normalized || strategy == SKY_GRID ? 1.0f : 3.402823466e38f;
+    const uint32_t upper_bits = __float_as_uint(upper);
     if (strategy == SKY_GRID && Row::kF32) {
         // float rows: the comparisons give the same answers in FP32 as on the
         // exact upcast; cell = floor(x * m) from the product rounded toward
         // zero (floor(x*m) < m <= 2^22 is representable, so rz(x*m) lies in
         // [floor(x*m), x*m] and has the same floor)
-        uint32_t stride = 1, pid32 = 0;
         const uint32_t m32 = (uint32_t)a.m;
         const float mf = (float)a.m;
-        bool ok = true;
+        uint32_t mx = 0, pid32 = 0;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) SKY_ROW_END;
             const float v = R.f(j);
-            ok &= (v >= 0.0f) & (v <= 1.0f);
+            mx = max(mx, __float_as_uint(v));
             sum = __dadd_rn(sum, (double)v);
-            const uint32_t cell = min(__float2uint_rz(__fmul_rz(v, mf)), m32 - 1);
-            pid32 += cell * stride;
-            stride *= m32;
         }
-        if (!ok) err = f32_errors(true);
+        // pid = sum_j cell_j * m^j by Horner from the last coordinate (the
+        // registers row is unrolled, so skipping j >= d keeps it exact)
+#pragma unroll U
+        for (int j = DMAX - 1; j >= 0; --j) {
+            if (j >= d) continue;
+            const uint32_t cell = min(__float2uint_rz(__fmul_rz(R.f(j), mf)), m32 - 1);
+            pid32 = pid32 * m32 + cell;
+        }
+        if (mx > upper_bits) err = f32_errors(true);
         pid = pid32;
     } else if (strategy == SKY_GRID) {
         // m^d <= kMaxPartitions (2^22): 32-bit cell arithmetic
@@ -262,14 +271,14 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
         pid = pid32;
     } else if (strategy == SKY_ANGULAR) {
-        bool ok = true;
+        uint32_t mx = 0;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) SKY_ROW_END;
             if (Row::kF32) {
                 // float rows: the same answers as on the exact upcast
                 const float v = R.f(j);
-                ok &= (v >= 0.0f) & (v <= upper);
+                mx = max(mx, __float_as_uint(v));
                 sum = __dadd_rn(sum, (double)v);
             } else {
                 const double v = R.X(j);
@@ -278,7 +287,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
                 sum = __dadd_rn(sum, v);
             }
         }
-        if (Row::kF32 && !ok) err = f32_errors(false);
+        if (Row::kF32 && mx > upper_bits) err = f32_errors(false);
         // hyperspherical_angles: tail sums of squares back to front; the
         // partition index sum_i slice_i * m^i (angular_index) by Horner's rule
         // over i = d-2 .. 0 (m^(d-1) <= 2^22: 32-bit arithmetic, no division)
@@ -376,13 +385,13 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
         }
     } else {
         float sv = 0.0f;
-        bool ok = true;
+        uint32_t mx = 0;
 #pragma unroll U
         for (int j = 0; j < DMAX; ++j) {
             if (j >= d) SKY_ROW_END;
             if (Row::kF32) {
                 const float v = R.f(j);
-                ok &= (v >= 0.0f) & (v <= upper);
+                mx = max(mx, __float_as_uint(v));
                 sum = __dadd_rn(sum, (double)v);
             } else {
                 const double v = R.X(j);
@@ -392,7 +401,7 @@ __device__ __forceinline__ uint64_t prep_row(const PrepArgs& a, uint32_t i, cons
             }
             if ((uint32_t)j == a.slice_dim) sv = R.f(j);
         }
-        if (Row::kF32 && !ok) err = f32_errors(false);
+        if (Row::kF32 && mx > upper_bits) err = f32_errors(false);
         if (strategy == SKY_RANDOM) pid = a.pid_in[i];
         if (strategy == SKY_SLICED) a.slice_key[i] = canon_bits(sv);
     }
@@ -420,19 +429,20 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 // moves from the staged tile into registers with the widest shared load its
 // stride allows. With a.gmin set, also the per-CTA minimum key of every
 // partition (gmin[p * gridDim.x + blockIdx.x]; the stream path's representative bound).
-template <int DP, int ST>
-__global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
+template <int DP, int ST, bool XD>
+__global__ void __launch_bounds__(kStreamThreads) k_prep_stream(PrepArgs a) {
     extern __shared__ __align__(16) char s_prep[];
     char* smem = s_prep;
     uint32_t* s_min = reinterpret_cast<uint32_t*>(smem + stream_smem_bytes(a.d));
     if (a.gmin) {
         for (uint32_t p = threadIdx.x; p < a.P; p += blockDim.x) s_min[p] = 0xFFFFFFFFu;
     }
-    const uint32_t d = a.d;
+    const uint32_t d = XD ? DP : a.d;  // XD: every row is exactly DP wide
     stream_row_tiles(a.pts, a.n, d, smem, [&](const float* tile, uint32_t r0, uint32_t nr, const uint64_t*) {
-        if (threadIdx.x < nr) {
-            const uint32_t i = a.row_base + r0 + threadIdx.x;
-            const float* x = tile + (size_t)threadIdx.x * d;
+#pragma unroll 1
+        for (uint32_t rr = threadIdx.x; rr < nr; rr += kStreamThreads) {
+            const uint32_t i = a.row_base + r0 + rr;
+            const float* x = tile + (size_t)rr * d;
             RegRow<DP> R;
             if ((d & 3) == 0) {
 #pragma unroll
@@ -455,7 +465,7 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
 #pragma unroll
                 for (int j = 0; j < DP; ++j) R.v[j] = j < (int)d ? x[j] : 0.0f;
             }
-            const uint64_t key = prep_row<DP, RegRow<DP>, ST>(a, i, R);
+            const uint64_t key = prep_row<DP, RegRow<DP>, ST, XD>(a, i, R);
             if (a.gmin) {
                 // read first: after the first rows most keys are above the minimum
                 const uint32_t p = (uint32_t)(key >> 32), k = (uint32_t)key;
@@ -469,21 +479,31 @@ __global__ void __launch_bounds__(kStreamRows) k_prep_stream(PrepArgs a) {
     }
 }
 
-// Persistent grid of the streamed prep: as many CTAs as fit on the SMs (the
-// per-tile work is a dependent chain; resident warps hide it), at most one
-// per tile. Deterministic for (n, d, P) on a device, so callers can size
+// Persistent grid of the streamed prep: as many CTAs of the instantiation
+// launched for (d, strategy) as fit on the SMs (the per-tile work is a
+// dependent chain; resident warps hide it), at most one per tile.
+// Deterministic for (n, d, P, strategy) on a device, so callers can size
 // per-CTA outputs (gmin) with it.
-uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count) {
+template <int DT>
+static const void* prep_stream_kernel(int strategy, bool xd) {
+    if (strategy == SKY_GRID)
+        return xd ? (const void*)k_prep_stream<DT, SKY_GRID, true> : (const void*)k_prep_stream<DT, SKY_GRID, false>;
+    if (strategy == SKY_ANGULAR)
+        return xd ? (const void*)k_prep_stream<DT, SKY_ANGULAR, true>
+                  : (const void*)k_prep_stream<DT, SKY_ANGULAR, false>;
+    return xd ? (const void*)k_prep_stream<DT, -1, true> : (const void*)k_prep_stream<DT, -1, false>;
+}
+
+uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count, int strategy) {
     const size_t smem = stream_smem_bytes(d) + (size_t)P * sizeof(uint32_t);
     int per_sm = 4;
     SKY_DISPATCH_D(padded_dim(d), {
-        ensure_smem_attr((const void*)k_prep_stream<DT, SKY_GRID>, smem);
-        ensure_smem_attr((const void*)k_prep_stream<DT, SKY_ANGULAR>, smem);
-        ensure_smem_attr((const void*)k_prep_stream<DT, -1>, smem);
-        per_sm = occupancy_cached((const void*)k_prep_stream<DT, -1>, (int)kStreamRows, smem);
+        const void* k = prep_stream_kernel<DT>(strategy, padded_dim(d) == (int)d);
+        ensure_smem_attr(k, smem);
+        per_sm = occupancy_cached(k, (int)kStreamThreads, smem);
     });
     per_sm = std::max(1, std::min(per_sm, 8));
-    return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows), (uint32_t)per_sm * (uint32_t)sm_count));
+    return std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, stream_tile_rows(d)), (uint32_t)per_sm * (uint32_t)sm_count));
 }
 
 void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
@@ -491,16 +511,27 @@ void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
     if (!a.pts64 && a.d <= 32 && ((uintptr_t)a.pts & 15) == 0 && sm_count > 0) {
         // float rows, 16-byte aligned: persistent CTAs, bulk-copied row tiles
         const size_t smem = stream_smem_bytes(a.d) + (size_t)a.P * sizeof(uint32_t);
-        const uint32_t grid = prep_stream_grid(a.n, a.d, a.P, sm_count);  // sets the smem attribute
+        const uint32_t grid = prep_stream_grid(a.n, a.d, a.P, sm_count, a.strategy);  // sets the smem attribute
         // grid and angular rows get their own instantiations (the row path
         // then holds only that strategy's code); random / sliced share one
+        // and rows exactly as wide as the instantiation get one more (no
+        // per-coordinate width tests)
+        const bool xd = padded_dim(a.d) == (int)a.d;
+#define SKY_PREP_LAUNCH(STRAT)                                              \
+    SKY_DISPATCH_D(padded_dim(a.d), {                                       \
+        if (xd)                                                             \
+            k_prep_stream<DT, STRAT, true><<<grid, kStreamThreads, smem, st>>>(a);  \
+        else                                                                \
+            k_prep_stream<DT, STRAT, false><<<grid, kStreamThreads, smem, st>>>(a); \
+    })
         if (a.strategy == SKY_GRID) {
-            SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT, SKY_GRID><<<grid, kStreamRows, smem, st>>>(a)));
+            SKY_PREP_LAUNCH(SKY_GRID);
         } else if (a.strategy == SKY_ANGULAR) {
-            SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT, SKY_ANGULAR><<<grid, kStreamRows, smem, st>>>(a)));
+            SKY_PREP_LAUNCH(SKY_ANGULAR);
         } else {
-            SKY_DISPATCH_D(padded_dim(a.d), (k_prep_stream<DT, -1><<<grid, kStreamRows, smem, st>>>(a)));
+            SKY_PREP_LAUNCH(-1);
         }
+#undef SKY_PREP_LAUNCH
     } else {
         if (a.gmin) throw Error(SKY_E_INTERNAL, "partition minima need the streamed prep");
         k_prep<<<ceil_div(a.n, 256), 256, 0, st>>>(a);

@@ -81,7 +81,7 @@ struct PrepArgs {
 // sm_count > 0: persistent streamed prep when the rows allow it (float,
 // aligned); required when a.gmin is set (grid = prep_stream_grid chunks)
 void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count = 0);
-uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count);
+uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count, int strategy);
 
 // Partition boundaries of a (pid << 32 | skey)-sorted key array: off[P+1].
 void launch_seg_offsets(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t* off, cudaStream_t st);

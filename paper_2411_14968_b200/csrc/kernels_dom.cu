@@ -830,6 +830,53 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         (reinterpret_cast<uintptr_t>(s_thr + (CODES ? D * kThr : 0)) + 15) & ~uintptr_t{15});
     __syncthreads();
     unsigned long long nt = 0;
+    // APPEND: a warp's kept rows take consecutive output slots
+    auto append_row = [&](const bool keep, const uint32_t row) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (!bal) return;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(app.count, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep)
+            app.out[base + __popc(bal & ((1u << lane) - 1u))] =
+                ((app.key64[row] >> app.key_shift) << app.row_bits) | row;
+    };
+    // APPEND without codes (fewer than 32 representatives), all of them in
+    // shared memory: each row is tested against them in key order (the strongest
+    // first) until one dominates it, a warp vote before each; no key bound
+    // (a representative's key is below a row's it dominates anyway), so the
+    // rows' keys are not staged
+    auto few_reps = [&](const float* tile, const uint32_t r0, const uint32_t nr) {
+#pragma unroll 1
+        for (uint32_t r1 = 0; r1 < stream_tile_rows(d); r1 += kStreamThreads) {
+            const uint32_t rr = threadIdx.x + r1;
+            const bool valid = rr < nr;
+            const float* x = tile + (size_t)rr * d;
+            float4 t[V];
+            if ((d & 3) == 0) {
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    t[v] = (valid && 4 * v < (int)d) ? reinterpret_cast<const float4*>(x)[v]
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                float xs[4 * V];
+#pragma unroll
+                for (int j = 0; j < 4 * V; ++j) xs[j] = (valid && (uint32_t)j < d) ? x[j] : 0.0f;
+#pragma unroll
+                for (int v = 0; v < V; ++v) t[v] = make_float4(xs[4 * v], xs[4 * v + 1], xs[4 * v + 2], xs[4 * v + 3]);
+            }
+            bool alive = valid;
+#pragma unroll 1
+            for (uint32_t r = 0; r < nrep && __any_sync(0xffffffffu, alive); ++r) {
+                if (alive) {
+                    ++nt;
+                    if (dom_f4<D>(s_rep_smem + r * V, t)) alive = false;
+                }
+            }
+            append_row(alive, r0 + rr);
+        }
+    };
     auto process = [&](const float* x, const uint32_t slot, const bool valid, const uint32_t row,
                        const uint64_t* key_in) {
     float4 t[V];
@@ -1006,15 +1053,7 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         if (alive) nt += r;
     }
     if (APPEND) {
-        const bool keep = valid && alive;
-        const uint32_t lane = threadIdx.x & 31;
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        uint32_t base = 0;
-        if (lane == 0 && bal) base = atomicAdd(app.count, (uint32_t)__popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep)
-            app.out[base + __popc(bal & ((1u << lane) - 1u))] =
-                ((app.key64[row] >> app.key_shift) << app.row_bits) | row;
+        append_row(valid && alive, row);
     } else if (POSORDER) {
         if (valid && !alive && !flags_done) dead_row[slot] = 1;
     } else if (valid) {
@@ -1025,10 +1064,18 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
         stream_row_tiles(
             pts, n, d, s_stage,
             [&](const float* tile, uint32_t r0, uint32_t nr, const uint64_t* keys) {
-                const uint32_t r = r0 + threadIdx.x;
-                process(tile + (size_t)threadIdx.x * d, r, threadIdx.x < nr, r, keys + threadIdx.x);
+                if (!use_codes && !greps) {
+                    few_reps(tile, r0, nr);
+                    return;
+                }
+                // warp-uniform trip count: the warp votes stay converged
+#pragma unroll 1
+                for (uint32_t r1 = 0; r1 < stream_tile_rows(d); r1 += kStreamThreads) {
+                    const uint32_t rr = threadIdx.x + r1;
+                    process(tile + (size_t)rr * d, r0 + rr, rr < nr, r0 + rr, keys + rr);
+                }
             },
-            app.key64);
+            use_codes || greps ? app.key64 : nullptr);  // CTA-uniform; the ring is sized for the keys
     } else {
         const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
         const bool valid = slot < n && (!POSORDER || !dead_row[slot]);
@@ -1177,11 +1224,11 @@ bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, co
     // persistent CTAs: as many as fit, capped by the tile count
     auto go = [&](auto kern, const uint2* qc, const float* th) {
         ensure_smem_attr((const void*)kern, smem);
-        const int per_sm = occupancy_cached((const void*)kern, (int)kStreamRows, smem);
+        const int per_sm = occupancy_cached((const void*)kern, (int)kStreamThreads, smem);
         const int sms = device_sm_count();
-        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, kStreamRows),
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(n, stream_tile_rows(d)),
                                                                        (uint32_t)std::max(1, per_sm) * sms));
-        kern<<<grid, kStreamRows, smem, st>>>(pts, d, n, nullptr, reinterpret_cast<const float4*>(rep_xyz), rep_key,
+        kern<<<grid, kStreamThreads, smem, st>>>(pts, d, n, nullptr, reinterpret_cast<const float4*>(rep_xyz), rep_key,
                                               qc, rep_id, nrep, nrep_dev, th, nullptr, tests, X64{}, app);
     };
     SKY_DISPATCH_D16(D, {

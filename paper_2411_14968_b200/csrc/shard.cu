@@ -258,7 +258,7 @@ void run_sharded(sky_ctx* c, const float* src, uint32_t nl, uint32_t row0, const
     // the own rows) when the rows are many
     bool stream_reps = reps_on && strategy != SKY_SLICED && (uint64_t)nl * d * sizeof(float) > (32ull << 20) &&
                        (uint64_t)P * kRepBucket <= (1ull << 31);
-    const uint32_t prep_grid = stream_reps ? prep_stream_grid(nl, d, P, c->sm_count) : 0;
+    const uint32_t prep_grid = stream_reps ? prep_stream_grid(nl, d, P, c->sm_count, strategy) : 0;
     uint64_t* keyA = R.dev<uint64_t>(S_KEY_A, nl);
     uint32_t* skA = strategy == SKY_SLICED ? R.dev<uint32_t>(S_SK_A, nl) : nullptr;
     const uint32_t amb_cap = strategy == SKY_ANGULAR ? std::max<uint32_t>(nl, 1) : 1u;

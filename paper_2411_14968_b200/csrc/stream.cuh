@@ -1,11 +1,13 @@
 // stream.cuh — persistent row-tile streaming for the HBM-bound passes.
 //
-// Rows are float32, row-major n x d. A CTA walks tiles of kStreamRows rows
+// Rows are float32, row-major n x d. A CTA walks tiles of stream_tile_rows(d) rows
 // (tile t, t + gridDim.x, ...); each tile is one contiguous span, copied
 // global -> shared memory by the bulk-copy engine (cp.async.bulk, completion
 // counted on an mbarrier), kStreamStages tiles in flight per CTA, so the SMs
 // keep enough bytes in flight to stream at HBM rate while they compute on the
-// current tile. Thread i of the CTA takes row i of a tile.
+// current tile. A CTA has kStreamThreads threads; thread i takes rows
+// i, i + kStreamThreads, ... of a tile (the per-tile wait, barrier and copy
+// issue are shared by the tile rows / kStreamThreads rows per thread).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -14,8 +16,12 @@
 
 namespace sky {
 
-constexpr uint32_t kStreamRows = 256;   // rows per tile (= threads per CTA)
-constexpr uint32_t kStreamStages = 4;   // tiles in flight per CTA
+constexpr uint32_t kStreamThreads = 256;  // threads per CTA
+constexpr uint32_t kStreamStages = 2;     // tiles in flight per CTA
+// rows per tile: two per thread while a stage stays <= 32 KB
+__host__ __device__ constexpr uint32_t stream_tile_rows(uint32_t d) {
+    return d <= 16 ? 2 * kStreamThreads : kStreamThreads;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -49,17 +55,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-// Shared memory of the ring: kStreamStages stages of (kStreamRows * d
-// floats [+ kStreamRows u64 of the optional per-row aux array]), then the
+// Shared memory of the ring: kStreamStages stages of (tile rows * d
+// floats [+ tile rows u64 of the optional per-row aux array]), then the
 // barriers.
 __host__ __device__ inline size_t stream_stage_bytes(uint32_t d, bool aux) {
-    return (size_t)kStreamRows * d * sizeof(float) + (aux ? kStreamRows * sizeof(uint64_t) : 0);
+    const size_t tr = stream_tile_rows(d);
+    return tr * d * sizeof(float) + (aux ? tr * sizeof(uint64_t) : 0);
 }
 __host__ __device__ inline size_t stream_smem_bytes(uint32_t d, bool aux = false) {
     return (size_t)kStreamStages * stream_stage_bytes(d, aux) + kStreamStages * sizeof(uint64_t) + 16;
 }
 
-// Walk this CTA's tiles. `body(tile, row0, nrows, aux_tile)` runs on every
+// Walk this CTA's tiles (stream_tile_rows(d) rows each). `body(tile, row0, nrows, aux_tile)` runs on every
 // thread with the tile's rows in shared memory (row r of the tile at
 // tile + r * d) and, if `aux` is given, aux[row0 .. row0 + nrows) at
 // aux_tile; it must not call __syncthreads. `smem` is 16-byte aligned,
@@ -68,9 +75,10 @@ template <class Body>
 __device__ __forceinline__ void stream_row_tiles(const float* __restrict__ pts, uint32_t n, uint32_t d, char* smem,
                                                  Body&& body, const uint64_t* __restrict__ aux = nullptr) {
     const size_t stage_bytes = stream_stage_bytes(d, aux != nullptr);
-    const size_t row_bytes = (size_t)kStreamRows * d * sizeof(float);
+    const uint32_t TR = stream_tile_rows(d);
+    const size_t row_bytes = (size_t)TR * d * sizeof(float);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStreamStages * stage_bytes);
-    const uint32_t tiles = (n + kStreamRows - 1) / kStreamRows;
+    const uint32_t tiles = (n + TR - 1) / TR;
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
         for (uint32_t s = 0; s < kStreamStages; ++s) mbar_init(bars + s, 1);
@@ -80,8 +88,8 @@ __device__ __forceinline__ void stream_row_tiles(const float* __restrict__ pts, 
     // the bulk copies take the 16-byte multiples of a tile; the few words of
     // an odd-sized last tile past them are loaded by the threads
     auto issue = [&](uint32_t t, uint32_t s) {
-        const uint32_t r0 = t * kStreamRows;
-        const uint32_t nr = min(kStreamRows, n - r0);
+        const uint32_t r0 = t * TR;
+        const uint32_t nr = min(TR, n - r0);
         const uint32_t bytes = (nr * d * (uint32_t)sizeof(float)) & ~15u;
         const uint32_t abytes = aux ? (nr * (uint32_t)sizeof(uint64_t)) & ~15u : 0u;
         char* st = smem + s * stage_bytes;
@@ -102,8 +110,8 @@ __device__ __forceinline__ void stream_row_tiles(const float* __restrict__ pts, 
         char* st = smem + s * stage_bytes;
         float* tile = reinterpret_cast<float*>(st);
         uint64_t* atile = aux ? reinterpret_cast<uint64_t*>(st + row_bytes) : nullptr;
-        const uint32_t r0 = t * kStreamRows;
-        const uint32_t nr = min(kStreamRows, n - r0);
+        const uint32_t r0 = t * TR;
+        const uint32_t nr = min(TR, n - r0);
         const uint32_t nf = nr * d, done = (nf * (uint32_t)sizeof(float) & ~15u) / (uint32_t)sizeof(float);
         const uint32_t adone = (nr * (uint32_t)sizeof(uint64_t) & ~15u) / (uint32_t)sizeof(uint64_t);
         if (done != nf || (aux && adone != nr)) {  // last tile only (uniform branch)
