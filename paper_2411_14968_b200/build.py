@@ -50,8 +50,8 @@ COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibilit
           "-I", os.path.join(ROOT, "include")] + NCCL_INC
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcudafe", "--diag_suppress=177", "-diag-suppress", "1444"]
-SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "shard.cu", "comm.cpp", "host.cpp", "dataio.cpp", "mtjump.cpp", "angular.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "stream.cuh", "comm.hpp", "engine_impl.cuh"]
+SOURCES = ["kernels.cu", "kernels_dom.cu", "kernels_rand.cu", "engine.cu", "shard.cu", "small.cu", "comm.cpp", "host.cpp", "dataio.cpp", "mtjump.cpp", "angular.cpp"]
+HEADERS = ["common.cuh", "kernels.cuh", "stream.cuh", "dom.cuh", "comm.hpp", "engine_impl.cuh"]
 
 
 def _newer(src_list, target):

@@ -330,33 +330,38 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
                                cfg->filter == SKY_FILTER_REPRESENTATIVE &&
                                !c->opt.host_merge;
     auto dev_merge_ok = [&](uint32_t capacity) { return dev_merge_cfg && capacity >= 8192; };
-    auto finish_dev_merge = [&](const DevSet& Ucap, uint32_t ns_host) {
-        SKY_CUDA(cudaEventRecord(c->ev[2], st));
-        uint8_t* fdead = nullptr;
-        DevSet US = R.merge_all_dev(D, Ucap, offu_dev, P, misc + M_U, count_tests, &fdead);
-        SKY_CUDA(cudaEventRecord(c->ev[3], st));
-        // ascending ids written by the emit kernel straight into pinned host
-        // memory (mapped under UVA): no copy of a capacity-sized buffer
-        const uint32_t cap = Ucap.n;
-        uint32_t* hid = R.pin<uint32_t>(P_IDS, std::max<uint32_t>(cap, 1));
-        uint32_t* bm = R.dev<uint32_t>(S_BM, (size_t)n / 32 + 1);
-        uint32_t* bt = R.dev<uint32_t>(S_BMT, bm_blocks(n));
-        launch_ids_bitmap(US.id, fdead, cap, n, bm, bt, hid, misc + M_TOTAL, st, misc + M_U);
-        R.count(cap ? 3 : 2);
-        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 1 + 32 + 16);
+    // The only round trip of a run finished on the device: union offsets,
+    // counters and test counts into pinned memory (the ids are already in
+    // `hid`), then the result. `small`: the fused small tail, which may have
+    // declined (too many survivors): false, with the counters left in
+    // P_MISC for the general tail.
+    // The small tail's last kernel writes the offsets and counter words
+    // into the same pinned block itself (pin_block()).
+    auto pin_block = [&]() { return R.pin<uint32_t>(P_OFF, P + 1 + kSmallMiscWords); };
+    auto publish = [&](const uint32_t* hid, uint32_t ns_host, bool small) -> bool {
+        static_assert(M_TESTS + 6 <= (int)kSmallMiscWords && M_HITS + 8 <= (int)kSmallMiscWords,
+                      "test counters inside the copied counter words");
+        uint32_t* h = pin_block();
         uint32_t* hmisc = h + P + 1;
-        unsigned long long* ht = reinterpret_cast<unsigned long long*>(hmisc + 32);
-        SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        SKY_CUDA(cudaMemcpyAsync(hmisc, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        SKY_CUDA(cudaMemcpyAsync(ht, R.tests(0), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        SKY_CUDA(cudaMemcpyAsync(ht + 3, misc + M_HITS, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        // test counters (3 x u64) and exact-check counters (4 x u64) are
+        // counter words themselves
+        const unsigned long long* hts = reinterpret_cast<const unsigned long long*>(hmisc + M_TESTS);
+        const unsigned long long* hhits = reinterpret_cast<const unsigned long long*>(hmisc + M_HITS);
+        if (!small) {
+            SKY_CUDA(cudaMemcpyAsync(h, offu_dev, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            SKY_CUDA(cudaMemcpyAsync(hmisc, misc, kSmallMiscWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        }
         SKY_CUDA(cudaEventRecord(c->ev[4], st));
         R.sync();
+        if (small && hmisc[M_S0] > kSmallCap) {
+            std::memcpy(R.pin<uint32_t>(P_MISC, 32), hmisc, 32 * sizeof(uint32_t));
+            return false;
+        }
         check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
         if (defer_rand && hmisc[M_RFLAG]) throw RedoEager{};
         if (hmisc[M_OVF]) throw RedoEager{};
         if (cfg->filter == SKY_FILTER_REPRESENTATIVE) out->n_reps = hmisc[M_NREP];
-        const uint32_t ns = stream ? ns_host : hmisc[M_S0];
+        const uint32_t ns = stream && !small ? ns_host : hmisc[M_S0];
         out->filtered_count = (uint64_t)n - ns;
         for (uint32_t p = 0; p < P; ++p) out->local_skyline_sizes[p] = h[p + 1] - h[p];
         out->union_size = hmisc[M_U];
@@ -365,9 +370,9 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         out->ids = static_cast<int64_t*>(std::malloc((nf ? nf : 1) * sizeof(int64_t)));
         for (uint32_t i = 0; i < nf; ++i) out->ids[i] = hid[i];
         out->n_ids = out->final_size = nf;
-        out->tests_reps = ht[0];
-        out->tests_local = ht[1];
-        out->tests_merge = ht[2];
+        out->tests_reps = hts[0];
+        out->tests_local = hts[1];
+        out->tests_merge = hts[2];
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
         out->partition_ms = ms;
@@ -385,9 +390,56 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         out->stream_launches = c->hbm_used;
         R.timeline_dump();
         out->dom_kernel_ms = c->dom_ms;
-        out->dom_tests = ht[0] + ht[1] + ht[2];
-        out->dom_exact_checks = ht[3] + ht[4] + ht[5] + ht[6];
-        out->exact_checks_merge = ht[5];
+        out->dom_tests = hts[0] + hts[1] + hts[2];
+        out->dom_exact_checks = hhits[0] + hhits[1] + hhits[2] + hhits[3];
+        out->exact_checks_merge = hhits[2];
+        return true;
+    };
+    auto finish_dev_merge = [&](const DevSet& Ucap, uint32_t ns_host) {
+        SKY_CUDA(cudaEventRecord(c->ev[2], st));
+        uint8_t* fdead = nullptr;
+        DevSet US = R.merge_all_dev(D, Ucap, offu_dev, P, misc + M_U, count_tests, &fdead);
+        SKY_CUDA(cudaEventRecord(c->ev[3], st));
+        // ascending ids written by the emit kernel straight into pinned host
+        // memory (mapped under UVA): no copy of a capacity-sized buffer
+        const uint32_t cap = Ucap.n;
+        uint32_t* hid = R.pin<uint32_t>(P_IDS, std::max<uint32_t>(cap, 1));
+        uint32_t* bm = R.dev<uint32_t>(S_BM, (size_t)n / 32 + 1);
+        uint32_t* bt = R.dev<uint32_t>(S_BMT, bm_blocks(n));
+        launch_ids_bitmap(US.id, fdead, cap, n, bm, bt, hid, misc + M_TOTAL, st, misc + M_U);
+        R.count(cap ? 3 : 2);
+        publish(hid, ns_host, false);
+    };
+    // stream path, few survivors: sort, local skylines, union, merge and ids
+    // in five capacity-sized launches and one round trip (small.cu); false
+    // when the survivors exceed the capacity (nothing was changed)
+    auto finish_small = [&]() -> bool {
+        SmallTail t;
+        t.surv = R.dev<uint64_t>(S_SURV, n);
+        t.count = misc + M_S0;
+        t.pts = pts;
+        t.d = d;
+        t.P = P;
+        t.row_bits = (uint32_t)std::max(1, bits_for(n));
+        t.key_shift = key_shift_for(P);
+        t.cap = kSmallCap;
+        t.flags = R.dev<uint32_t>(S_SM_W, (size_t)3 * kSmallCap);
+        t.cnt = R.dev<uint32_t>(S_SM_CNT, P);
+        t.u_count = misc + M_U;
+        t.total = misc + M_TOTAL;
+        t.offu = offu_dev;
+        t.hid = R.pin<uint32_t>(P_IDS, kSmallCap);
+        t.tests = count_tests ? R.tests(1) : nullptr;
+        t.misc = misc;
+        t.hoffu = pin_block();
+        t.hmisc = t.hoffu + P + 1;
+        launch_small_tail(D, t, st);
+        R.count(2);
+        // one pass gives the local skylines and the merge: the merge phase
+        // is empty
+        SKY_CUDA(cudaEventRecord(c->ev[2], st));
+        SKY_CUDA(cudaEventRecord(c->ev[3], st));
+        return publish(t.hid, 0, true);
     };
     auto early_merge = [&](const DevSet& Ucap) {
         if (!(all_mode_merge && P > 1)) return;
@@ -397,11 +449,17 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         us_early = true;
     };
     if (W == 1 && stream) {
+        // few survivors: the fused tail (its round trip also brings the
+        // counters when it declines)
+        const bool small_tried = c->opt.small_tail != 0 && (uint64_t)P <= kSmallMaxParts;
+        if (small_tried && finish_small()) return;
         // survivors of the stream prefilter: count (round trip), sort by
         // (partition, key, row), unpack into partition order
         uint32_t* hc = R.pin<uint32_t>(P_MISC, 32);
-        SKY_CUDA(cudaMemcpyAsync(hc, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        R.sync();
+        if (!small_tried) {
+            SKY_CUDA(cudaMemcpyAsync(hc, misc, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            R.sync();
+        }
         check_prep(hc[M_ERR], hc[M_AMB], cfg->strategy, eager);
         if (hc[M_OVF]) throw RedoEager{};  // a candidate bucket filled up: sorted path
         const uint32_t ns = hc[M_S0];
@@ -998,6 +1056,7 @@ int sky_ctx_set_option(sky_ctx* c, const char* name, int64_t v) {
     else if (k == "wave_split_mpairs") o.wave_split_mpairs = u;
     else if (k == "profile_host") o.profile_host = s > 0;
     else if (k == "timeline") o.timeline = s > 0;
+    else if (k == "small_tail") o.small_tail = s > 0;
     else {
         c->err = "unknown option or value: " + k;
         return SKY_E_CONFIG;

@@ -48,6 +48,7 @@ struct sky_options {
     uint32_t wave_split_mpairs = 8192;  // split the rest into further waves above this many Mi pairs
     int32_t profile_host = 0;   // print host-side planning / wait times
     int32_t timeline = 0;       // an event after every launch, dumped per run
+    int32_t small_tail = 1;     // stream path: the fused tail when <= kSmallCap rows survive the prefilter
 };
 
 struct sky_ctx {
@@ -123,6 +124,7 @@ enum Slot {
     S_SETS, S_SETS_K, S_SETS_I, S_SETS_Q,  // rows sent to their partition owners
     S_SETR, S_SETR_K, S_SETR_I, S_SETR_Q,  // rows received from the other ranks
     S_DEAD2, S_SOFF, S_SH_OFFU, S_OFFM,
+    S_SM_W, S_SM_CNT,  // the fused small tail (small.cu)
     S_COUNT
 };
 // pinned slots
@@ -150,6 +152,8 @@ enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, 
        M_OVF = 29 /* stream path: a representative candidate bucket overflowed */ };
 // stream path (representative filter over large inputs): candidate bucket size
 constexpr uint32_t kRepBucket = 1024;
+// the fused small tail writes P + 1 union offsets from one CTA
+constexpr uint32_t kSmallMaxParts = 1u << 16;
 
 inline uint64_t checked_pow(uint64_t base, uint64_t e) {  // partition.cpp:15-22
     uint64_t r = 1;

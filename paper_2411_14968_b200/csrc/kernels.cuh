@@ -373,6 +373,31 @@ struct PrefilterAppend {
     uint32_t key_shift = 0, row_bits = 0;
     uint32_t regroup = 64;  // POSORDER: representatives before the CTA regroups its live rows
 };
+// Fused tail of a stream-path run with few prefilter survivors (small.cu).
+constexpr uint32_t kSmallCap = 4096;
+struct SmallTail {
+    const uint64_t* surv = nullptr;  // packed survivor keys (prefilter append order)
+    const uint32_t* count = nullptr; // their device count
+    const float* pts = nullptr;
+    uint32_t d = 0, P = 0, row_bits = 0, key_shift = 0, cap = kSmallCap;
+    uint32_t* flags = nullptr;       // 3 x cap words, zeroed by the launcher: local dead, dead, rank
+    uint32_t* cnt = nullptr;         // P words: local skyline size per partition
+    uint32_t* u_count = nullptr;     // |union| (device)
+    uint32_t* total = nullptr;       // final count (device)
+    uint32_t* offu = nullptr;        // P + 1 union offsets per partition (device)
+    uint32_t* hid = nullptr;         // final rows ascending (mapped pinned host memory)
+    unsigned long long* tests = nullptr;
+    // copied into mapped pinned memory by the last kernel (also when it
+    // declines): the run's counter words and the union offsets
+    const uint32_t* misc = nullptr;  // kSmallMiscWords device words
+    uint32_t* hmisc = nullptr;
+    uint32_t* hoffu = nullptr;       // P + 1
+};
+constexpr uint32_t kSmallMiscWords = 32;
+// all pairs of survivors (local + global dominance, ranks), then the counts,
+// offsets and ascending ids (one memset + 2 launches)
+void launch_small_tail(int D, const SmallTail& t, cudaStream_t st);
+
 // false: not applicable (d > 16, unaligned rows, shared memory)
 bool launch_prefilter_append(int D, const float* pts, uint32_t d, uint32_t n, const float* rep_xyz,
                              const uint32_t* rep_key, const uint2* rep_qc, const uint32_t* rep_id, uint32_t nrep,

@@ -20,17 +20,13 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "dom.cuh"
 #include "kernels.cuh"
 #include "stream.cuh"
 
 namespace sky {
 
 namespace {
-
-template <int D>
-struct Dims2 {
-    static constexpr int V = (D + 3) / 4;  // float4 per row == code words
-};
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 #pragma unroll
@@ -434,19 +430,6 @@ size_t bnl2_smem(uint32_t cap) {
     // window: codes (8) + key (4) + pos (4) + ts (4) + pass (1) + kill (1)
     // batch: coords (16V) + codes (8) + key (4)
     return (size_t)cap * 22 + (size_t)BNL2_B * (V * 16 + 12) + 256;
-}
-
-template <int D>
-__device__ __forceinline__ bool dom_f4(const float4* __restrict__ s, const float4* __restrict__ t) {
-    constexpr int V = Dims2<D>::V;
-    bool gt = false, lt = false;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-        const float4 a = s[v], b = t[v];
-        gt |= (a.x > b.x) | (a.y > b.y) | (a.z > b.z) | (a.w > b.w);
-        lt |= (a.x < b.x) | (a.y < b.y) | (a.z < b.z) | (a.w < b.w);
-    }
-    return !gt && lt;
 }
 
 // dom_f4, or for FP64 input: s <= t on the float image (necessary), then

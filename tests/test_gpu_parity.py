@@ -483,3 +483,32 @@ def test_repeated_runs_reuse_buffers(engine):
         r = engine.run(y, ecfg, True)
         assert np.array_equal(r.skyline, exp2["ids"]), ("y", it)
         check_metrics(r, exp2, ("y", it))
+
+
+@pytest.mark.parametrize("small_tail", ["1", "0"])
+def test_stream_small_tail_vs_oracle(engine, options, small_tail):
+    """Stream path whose prefilter leaves at most kSmallCap (4096) rows: the
+    fused tail (small.cu: sort, local skylines, union, merge, ids in five
+    launches and one round trip) against the oracle, and the general tail
+    (small_tail=0) on the same inputs; inputs with more survivors make the
+    fused tail decline and hand over to the general one."""
+    options(stream=1, small_tail=int(small_tail))
+    rng = np.random.default_rng(11)
+    cases = [
+        (generate(3, 200_000, 8, 3), 1, 2, 256),                           # C3-like: correlated, grid 2^8
+        (np.zeros((3000, 3), np.float32), 1, 2, 8),                         # identical rows: all survive, no dominance
+        ((rng.integers(0, 3, (20000, 5)) / 2).astype(np.float32), 1, 3, 243),  # lattice ties
+        (generate(2, 50_000, 4, 4), 1, 4, 256),                             # anticorrelated: > 4096 survivors
+        (generate(1, 100_000, 5, 5), 0, 0, 32),                             # random partitions
+        (generate(1, 100_000, 6, 6), 2, 2, 32),                             # angular
+        (generate(5, 100_000, 5, 7), 0, 0, 16),                             # integer rows, one dominator
+    ]
+    for k, (x, strat, m, p) in enumerate(cases):
+        cfg = SkyConfig.make(strategy=strat, p=p, m=m, seed=k, filter=2, rep_q=5, merge=1, workers=1)
+        normalized = bool(x.max() <= 1.0)
+        exp = O.oracle_run(x, cfg, normalized)
+        r = engine.run(x, to_engine_config(cfg.as_dict()), normalized)
+        tag = (k, small_tail)
+        assert np.array_equal(r.skyline, exp["ids"]), tag
+        check_metrics(r, exp, tag)
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
