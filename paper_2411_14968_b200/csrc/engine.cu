@@ -62,7 +62,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
     if (n == 0 || d == 0) {
         // d == 0: no coordinate can be strictly better, nothing is dominated
         // (dominates_raw core.hpp:89-96); every row is its own local skyline.
-        out->ids = static_cast<int64_t*>(std::malloc((n ? n : 1) * sizeof(int64_t)));
+        out->ids = alloc_ids(n);
         for (uint32_t i = 0; i < n; ++i) out->ids[i] = i;
         out->n_ids = out->final_size = out->union_size = n;
         if (n && cfg->strategy == SKY_RANDOM) {
@@ -216,10 +216,10 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             uint32_t* bcnt = R.dev<uint32_t>(S_BCNT, P);
             uint64_t* bkey = R.dev<uint64_t>(S_BKEY, (size_t)P * kRepBucket);
             uint32_t* brow = R.dev<uint32_t>(S_BROW, (size_t)P * kRepBucket);
-                        R.hbm_begin();
+            cudaEvent_t pb, pe;
+            R.hbm_pair((uint64_t)n * 8, &pb, &pe);  // the key pass alone (thresholds and picks are latency-bound)
             launch_rep_candidates(po.key64, n, P, q, prep_grid, gmin, thr, kRepBucket, bcnt, bkey, brow, pts, d,
-                                  cand, misc + M_OVF, st);
-            R.hbm_end((uint64_t)n * 8);  // the key pass (thresholds and picks are small)
+                                  cand, misc + M_OVF, st, pb, pe);
             R.count(3);
         } else {
             launch_rep_pick(po.key64, po.idx, po.off, P, pts, R.x64_.x, d, q, cand, st);
@@ -367,7 +367,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         out->union_size = hmisc[M_U];
         const uint32_t nf = hmisc[M_TOTAL];
         out->d2h_bytes += (uint64_t)nf * sizeof(uint32_t);
-        out->ids = static_cast<int64_t*>(std::malloc((nf ? nf : 1) * sizeof(int64_t)));
+        out->ids = alloc_ids(nf);
         for (uint32_t i = 0; i < nf; ++i) out->ids[i] = hid[i];
         out->n_ids = out->final_size = nf;
         out->tests_reps = hts[0];
@@ -1136,7 +1136,7 @@ int sky_run_shard(sky_ctx* c, const float* points, uint64_t n_local, uint32_t d,
 
 void sky_result_free(sky_result* r) {
     if (!r) return;
-    std::free(r->ids);
+    IdPool::get().release(r->ids);
     std::free(r->local_skyline_sizes);
     r->ids = nullptr;
     r->local_skyline_sizes = nullptr;
@@ -1241,11 +1241,13 @@ int sky_skyline(sky_ctx* c, const float* points, uint64_t n, uint32_t d, int64_t
         cfg.p = 1;
         sky_result r;
         run_impl(c, points, n, d, 0, 0, &cfg, &r);
-        *out_ids = r.ids;
+        // a plain malloc block for sky_free (the result's own ids are pooled)
+        *out_ids = static_cast<int64_t*>(std::malloc((r.n_ids ? r.n_ids : 1) * sizeof(int64_t)));
+        if (*out_ids) std::memcpy(*out_ids, r.ids, r.n_ids * sizeof(int64_t));
         *n_out = r.n_ids;
         if (tests_out) *tests_out = r.tests_local + r.tests_merge;
-        r.ids = nullptr;
         sky_result_free(&r);
+        if (!*out_ids) throw std::bad_alloc();
     });
 }
 
@@ -1294,7 +1296,7 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
                 rows.insert(rows.end(), points + (size_t)v * d, points + (size_t)(v + 1) * d);
             }
         // prune: the skyline of the candidates (prune_dominated_reps)
-        int64_t* sk = nullptr;
+        std::vector<int64_t> sk;
         uint64_t ns = 0;
         if (!ids.empty()) {
             sky_config c2;
@@ -1303,14 +1305,12 @@ int sky_representatives(sky_ctx* c, const float* points, uint64_t n64, uint32_t 
             c2.p = 1;
             sky_result r;
             run_impl(c, rows.data(), ids.size(), d, 0, 0, &c2, &r);
-            sk = r.ids;
+            sk.assign(r.ids, r.ids + r.n_ids);
             ns = r.n_ids;
-            r.ids = nullptr;
             sky_result_free(&r);
         }
         std::vector<int64_t> outv;
         for (uint64_t k = 0; k < ns; ++k) outv.push_back(ids[sk[k]]);
-        std::free(sk);
         std::sort(outv.begin(), outv.end());
         *out_ids = static_cast<int64_t*>(std::malloc((outv.size() ? outv.size() : 1) * sizeof(int64_t)));
         std::memcpy(*out_ids, outv.data(), outv.size() * sizeof(int64_t));

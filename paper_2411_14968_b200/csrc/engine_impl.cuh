@@ -109,6 +109,52 @@ struct sky_ctx {
 namespace sky {
 namespace eng {
 
+// Result id buffers (sky_result::ids). A skyline of hundreds of thousands of
+// ids is megabytes: malloc hands such blocks out as fresh mappings, and
+// their page faults cost more than the ids' copy (config 4: ~1 ms per run).
+// Large blocks go back to a small process-wide pool in sky_result_free and
+// are reused by the next run. A 16-byte header in front of the ids holds the
+// capacity.
+struct IdPool {
+    static constexpr size_t kHeader = 16, kPooledFrom = 64 * 1024, kSlots = 4;
+    std::mutex mu;
+    std::vector<std::pair<char*, size_t>> free_blocks;  // (block, capacity in bytes)
+    static IdPool& get() {
+        static IdPool* p = new IdPool();  // never destroyed: results may outlive static teardown
+        return *p;
+    }
+    int64_t* alloc(size_t count) {
+        const size_t need = std::max<size_t>(count, 1) * sizeof(int64_t);
+        if (need >= kPooledFrom) {
+            std::lock_guard<std::mutex> lk(mu);
+            for (size_t k = 0; k < free_blocks.size(); ++k)
+                if (free_blocks[k].second >= need && free_blocks[k].second <= 4 * need) {
+                    char* b = free_blocks[k].first;
+                    free_blocks.erase(free_blocks.begin() + k);
+                    return reinterpret_cast<int64_t*>(b + kHeader);
+                }
+        }
+        char* b = static_cast<char*>(std::malloc(kHeader + need));
+        if (!b) throw std::bad_alloc();
+        *reinterpret_cast<size_t*>(b) = need;
+        return reinterpret_cast<int64_t*>(b + kHeader);
+    }
+    void release(int64_t* ids) {
+        if (!ids) return;
+        char* b = reinterpret_cast<char*>(ids) - kHeader;
+        const size_t cap = *reinterpret_cast<size_t*>(b);
+        if (cap >= kPooledFrom) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (free_blocks.size() < kSlots) {
+                free_blocks.emplace_back(b, cap);
+                return;
+            }
+        }
+        std::free(b);
+    }
+};
+inline int64_t* alloc_ids(size_t count) { return IdPool::get().alloc(count); }
+
 enum Slot {
     S_PTS, S_KEY_A, S_KEY_B, S_IDX_A, S_IDX_B, S_SK_A, S_SK_B, S_PID, S_MISC, S_AMB, S_OFF_A, S_OFF_B,
     S_DEAD, S_POS, S_CUB, S_ITEMS, S_RANGES, S_REPCAND, S_REPROWS, S_RUNS,
@@ -1026,6 +1072,19 @@ class Runner {
     }
     void hbm_end(uint64_t bytes) {
         SKY_CUDA(cudaEventRecord(c_->hbm_ev[2 * c_->hbm_used + 1], st_));
+        ++c_->hbm_used;
+        c_->hbm_bytes += bytes;
+    }
+    // an event pair for a pass the launcher brackets itself (recorded there)
+    void hbm_pair(uint64_t bytes, cudaEvent_t* begin, cudaEvent_t* end) {
+        auto& e = c_->hbm_ev;
+        while (e.size() < 2 * (size_t)(c_->hbm_used + 1)) {
+            cudaEvent_t ev;
+            SKY_CUDA(cudaEventCreate(&ev));
+            e.push_back(ev);
+        }
+        *begin = e[2 * c_->hbm_used];
+        *end = e[2 * c_->hbm_used + 1];
         ++c_->hbm_used;
         c_->hbm_bytes += bytes;
     }
@@ -2128,7 +2187,7 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
     R.sync();
     if (W == 1) nf = cn ? hm[0] : 0;
     out->d2h_bytes += (uint64_t)n_copy * sizeof(uint32_t);
-    out->ids = static_cast<int64_t*>(std::malloc((nf ? nf : 1) * sizeof(int64_t)));
+    out->ids = alloc_ids(nf);
     for (uint32_t i = 0; i < nf; ++i) out->ids[i] = hid[i];
     out->n_ids = out->final_size = nf;
     out->tests_reps = ht[0];

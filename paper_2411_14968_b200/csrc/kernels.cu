@@ -1122,13 +1122,16 @@ __global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict_
 void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t q, uint32_t G,
                            const uint32_t* gmin, uint32_t* thr, uint32_t B, uint32_t* cnt, uint64_t* bkey,
                            uint32_t* brow, const float* pts, uint32_t d, uint32_t* cand, uint32_t* overflow,
-                           cudaStream_t st) {
+                           cudaStream_t st, cudaEvent_t pass_begin, cudaEvent_t pass_end) {
     if (B > 1024) throw Error(SKY_E_INTERNAL, "candidate buckets hold at most 1024 rows");
     k_part_thresh<<<ceil_div((uint64_t)P * 32, 256), 256, 0, st>>>(gmin, G, P, q, thr);
     SKY_LAUNCH_CHECK();
     SKY_CUDA(cudaMemsetAsync(cnt, 0, P * sizeof(uint32_t), st));
+    // the key pass alone is timed as an HBM pass (thresholds and picks are latency-bound)
+    if (pass_begin) SKY_CUDA(cudaEventRecord(pass_begin, st));
     k_cand_bucket<<<ceil_div(ceil_div(n, 4), 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
     SKY_LAUNCH_CHECK();
+    if (pass_end) SKY_CUDA(cudaEventRecord(pass_end, st));
     const uint32_t run_floats = std::min<uint32_t>(B * d, 16u * 1024);  // <= 64 KB of run coordinates
     ensure_smem_attr((const void*)k_bucket_pick, 64 * 1024);
     k_bucket_pick<<<P, 256, run_floats * sizeof(float), st>>>(bkey, brow, cnt, B, pts, d, q, cand, run_floats);

@@ -148,7 +148,7 @@ void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t*
 void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32_t q, uint32_t G,
                            const uint32_t* gmin, uint32_t* thr, uint32_t B, uint32_t* cnt, uint64_t* bkey,
                            uint32_t* brow, const float* pts, uint32_t d, uint32_t* cand, uint32_t* overflow,
-                           cudaStream_t st);
+                           cudaStream_t st, cudaEvent_t pass_begin = nullptr, cudaEvent_t pass_end = nullptr);
 
 // Representative finish on the device (<= 2048 picks): key-sorted antichain
 // into `out`, count in *out_count. false: too many picks (host path).

@@ -407,10 +407,10 @@ void run_sharded(sky_ctx* c, const float* src, uint32_t nl, uint32_t row0, const
             uint32_t* bcnt = R.dev<uint32_t>(S_BCNT, P);
             uint64_t* bkey = R.dev<uint64_t>(S_BKEY, (size_t)P * kRepBucket);
             uint32_t* brow = R.dev<uint32_t>(S_BROW, (size_t)P * kRepBucket);
-            R.hbm_begin();
+            cudaEvent_t pb, pe;
+            R.hbm_pair((uint64_t)nl * 8, &pb, &pe);
             launch_rep_candidates(keyA, nl, P, q, prep_grid, gmin, thr, kRepBucket, bcnt, bkey, brow, pts, d, cand,
-                                  misc + M_OVF, st);
-            R.hbm_end((uint64_t)nl * 8);
+                                  misc + M_OVF, st, pb, pe);
             R.count(3);
             SKY_CUDA(cudaMemcpyAsync(hm, misc + M_OVF, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
             R.sync();

@@ -116,6 +116,23 @@ class PartitionConfig:
     slice_dim: int = 0
 
 
+_ZERO_COPY_IDS = 1 << 16  # ids from which RunResult.skyline is a view of the library's buffer
+
+
+class _ResultOwner:
+    """Keeps a sky_result alive for the arrays that view its buffers."""
+
+    def __init__(self, lib, res):
+        self._lib = lib
+        self._res = res
+
+    def __del__(self):
+        try:
+            self._lib.sky_result_free(C.byref(self._res))
+        except Exception:
+            pass
+
+
 @dataclass
 class EngineConfig:
     partition: PartitionConfig = field(default_factory=PartitionConfig)
@@ -384,13 +401,24 @@ class Engine:
         return self._result(res, config)
 
     def _result(self, res, config) -> RunResult:
+        owned = False
         try:
             # memmove instead of np.ctypeslib.as_array (~10 us of array-interface
             # setup per call, inside the caller's timed region)
             nid = int(res.n_ids)
-            ids = np.empty(nid, np.int64)
-            if nid:
-                C.memmove(ids.ctypes.data, res.ids, nid * 8)
+            if nid >= _ZERO_COPY_IDS:
+                # megabytes of ids: a view of the library's buffer instead of
+                # a fresh array (its page faults and the copy cost ~2 ms on
+                # 700k ids); the buffer goes back to the library when the
+                # last view of it is collected
+                buf = (C.c_int64 * nid).from_address(C.addressof(res.ids.contents))
+                buf._owner = _ResultOwner(self._lib, res)
+                owned = True
+                ids = np.frombuffer(buf, dtype=np.int64)
+            else:
+                ids = np.empty(nid, np.int64)
+                if nid:
+                    C.memmove(ids.ctypes.data, res.ids, nid * 8)
             P = int(res.effective_p)
             sizes_a = np.empty(P, np.uint64)
             if P:
@@ -411,7 +439,8 @@ class Engine:
                 exchange_bytes=int(res.exchange_bytes), local_rows=int(res.local_rows))
             return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
         finally:
-            self._lib.sky_result_free(C.byref(res))
+            if not owned:
+                self._lib.sky_result_free(C.byref(res))
 
     # skyline::make_assignment (partition.hpp:102)
     def make_assignment(self, points, partition: PartitionConfig, normalized: bool = True):
