@@ -163,33 +163,25 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
                                       rep_random && cfg->strategy == SKY_SLICED ? &scan_rows : nullptr, !stream,
                                       gmin, &in_chunks);
 
-    std::vector<uint32_t> off0(P + 1);
     uint8_t* dead = R.dev<uint8_t>(S_DEAD, n);
     uint64_t grid_filtered = 0;
     bool any_dead = false;
     if (cfg->filter == SKY_FILTER_GRID) {
-        // grid_filter over non-empty cells (filter.cpp:37-50, engine.cpp:150-163)
-        uint32_t* h = R.pin<uint32_t>(P_OFF, P + 2);
-        SKY_CUDA(cudaMemcpyAsync(h, po.off, (P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        R.sync();
-        std::vector<uint32_t> nonempty;
-        for (uint32_t p = 0; p < P; ++p)
-            if (h[p + 1] > h[p]) nonempty.push_back(p);
-        uint8_t* cd = R.pin<uint8_t>(P_PCOUNT, P);
-        std::memset(cd, 0, P);
-        for (uint32_t a : nonempty)
-            for (uint32_t b : nonempty)
-                if (grid_dom(b, a, m, d)) {
-                    cd[a] = 1;
-                    grid_filtered += h[a + 1] - h[a];
-                    break;
-                }
+        // grid_filter over non-empty cells (filter.cpp:37-50, engine.cpp:150-163):
+        // the cell antichain from the partition offsets on the device (a prefix
+        // OR of the occupancy along each axis); only the filtered row count
+        // travels to the host
         uint8_t* cdd = R.dev<uint8_t>(S_CELLDEAD, P);
-        SKY_CUDA(cudaMemcpyAsync(cdd, cd, P, cudaMemcpyHostToDevice, st));
+        uint8_t* occ = R.dev<uint8_t>(S_GRIDOCC, P);
+        unsigned long long* gcnt = R.dev<unsigned long long>(S_GRIDCNT, 1);
+        R.count(launch_grid_filter(po.off, P, (uint32_t)m, d, occ, cdd, gcnt, st));
         launch_mark_cells_dead(po.key64, n, cdd, dead, st);
         R.count();
-        any_dead = grid_filtered > 0;
+        unsigned long long* hg = R.pin<unsigned long long>(P_PCOUNT, 1);
+        SKY_CUDA(cudaMemcpyAsync(hg, gcnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         R.sync();
+        grid_filtered = *hg;
+        any_dead = grid_filtered > 0;
     } else if (!stream) {
         launch_fill_u8(dead, 0, n, st);
     }

@@ -171,6 +171,7 @@ enum Slot {
     S_SETR, S_SETR_K, S_SETR_I, S_SETR_Q,  // rows received from the other ranks
     S_DEAD2, S_SOFF, S_SH_OFFU, S_OFFM,
     S_SM_W, S_SM_CNT,  // the fused small tail (small.cu)
+    S_GRIDOCC, S_GRIDCNT,  // grid filter: occupancy prefix OR, filtered rows
     S_COUNT
 };
 // pinned slots
@@ -714,6 +715,24 @@ class Runner {
     //   s0: n = capacity, *n0 live rows, partitions off0_dev[P+1].
     DevSet local_sfs_dev(int D, const DevSet& s0, const uint32_t* n0, const uint32_t* off0_dev, uint32_t P,
                          uint32_t* off_u_dev, uint32_t* n_u, bool count_tests) {
+        if (D > 16) {
+            // wider rows run on the exact-compare core, which the device
+            // planner's packed-code launches do not cover: offsets and count
+            // to the host (one round trip), then the host-planned SFS
+            uint32_t* h = pin<uint32_t>(P_OFF, (size_t)P + 2);
+            SKY_CUDA(cudaMemcpyAsync(h, off0_dev, ((size_t)P + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+            SKY_CUDA(cudaMemcpyAsync(h + P + 1, n0, sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+            sync();
+            const std::vector<uint32_t> off0(h, h + P + 1);
+            DevSet live = s0;
+            live.n = h[P + 1];
+            std::vector<uint32_t> off_u;
+            DevSet U = local_sfs(D, live, off0, const_cast<uint32_t*>(off0_dev), P, off_u_dev, off_u, count_tests);
+            uint32_t* hn = stage<uint32_t>(1);
+            *hn = U.n;
+            SKY_CUDA(cudaMemcpyAsync(n_u, hn, sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+            return U;
+        }
         const uint32_t cap = s0.n;
         uint32_t* misc = dev<uint32_t>(S_MISC, 64);
         uint8_t* dead = dev<uint8_t>(S_DEAD, cap);
@@ -1592,14 +1611,6 @@ inline bool weak_grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d) {
         b /= m;
     }
     return !equal;
-}
-inline bool grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d) {
-    for (uint32_t j = 0; j < d; ++j) {
-        if (a % m >= b % m) return false;
-        a /= m;
-        b /= m;
-    }
-    return true;
 }
 
 struct RedoEager {};  // angular boundary points seen by a deferred prep

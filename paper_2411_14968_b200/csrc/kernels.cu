@@ -1915,6 +1915,103 @@ __global__ void k_mark_cells_dead(const uint64_t* __restrict__ key64, uint32_t n
     dead[i] = cell_dead[(uint32_t)(key64[i] >> 32)];
 }
 
+// grid_filter (filter.cpp:37-50, engine.cpp:150-163) on the device. A
+// non-empty cell a is filtered iff some non-empty cell b has b_j < a_j on
+// every axis, i.e. iff a_j >= 1 everywhere and occ(a - (1,..,1)) holds, where
+// occ(c) = "a non-empty cell b <= c exists" is the d-dimensional prefix OR of
+// the occupancy: one running OR along each axis in turn, O(P d) instead of
+// the reference's O(nonempty^2) pair loop. Cells are mixed radix m, axis 0
+// the lowest digit (grid_index, partition.cpp:66-75).
+__device__ __forceinline__ void grid_prefix_axis(uint8_t* e, uint32_t P, uint32_t m, uint32_t stride, uint32_t t,
+                                                 uint32_t nthreads) {
+    const uint32_t lines = P / m;
+    for (uint32_t l = t; l < lines; l += nthreads) {
+        const uint32_t base = (l / stride) * stride * m + (l % stride);
+        uint8_t acc = 0;
+        for (uint32_t k = 0; k < m; ++k) {
+            acc |= e[base + k * stride];
+            e[base + k * stride] = acc;
+        }
+    }
+}
+__device__ __forceinline__ unsigned long long grid_dead_cells(const uint32_t* off, const uint8_t* e, uint32_t P,
+                                                              uint32_t m, uint32_t d, uint32_t diag, uint8_t* cell_dead,
+                                                              uint32_t t, uint32_t nthreads) {
+    unsigned long long rows = 0;
+    for (uint32_t c = t; c < P; c += nthreads) {
+        const uint32_t sz = off[c + 1] - off[c];
+        bool inner = sz > 0;  // every digit >= 1
+        uint32_t x = c;
+        for (uint32_t j = 0; j < d && inner; ++j) {
+            inner = x % m != 0;
+            x /= m;
+        }
+        const bool dead = inner && e[c - diag];
+        cell_dead[c] = dead ? 1 : 0;
+        if (dead) rows += sz;
+    }
+    return rows;
+}
+// one CTA does every step (P <= kGridCtaCells): occupancy, d axis passes, dead cells
+__global__ void __launch_bounds__(1024) k_grid_filter_cta(const uint32_t* __restrict__ off, uint32_t P, uint32_t m,
+                                                          uint32_t d, uint32_t diag, uint8_t* e, uint8_t* cell_dead,
+                                                          unsigned long long* filtered_rows) {
+    for (uint32_t c = threadIdx.x; c < P; c += blockDim.x) e[c] = off[c + 1] > off[c] ? 1 : 0;
+    __syncthreads();
+    uint32_t stride = 1;
+    for (uint32_t j = 0; j < d; ++j) {
+        grid_prefix_axis(e, P, m, stride, threadIdx.x, blockDim.x);
+        __syncthreads();
+        stride *= m;
+    }
+    unsigned long long rows = grid_dead_cells(off, e, P, m, d, diag, cell_dead, threadIdx.x, blockDim.x);
+    rows = warp_sum_u64(rows);
+    if ((threadIdx.x & 31) == 0 && rows) atomicAdd(filtered_rows, rows);
+}
+__global__ void k_grid_occupancy(const uint32_t* __restrict__ off, uint32_t P, uint8_t* e) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < P) e[c] = off[c + 1] > off[c] ? 1 : 0;
+}
+__global__ void k_grid_prefix_axis(uint8_t* e, uint32_t P, uint32_t m, uint32_t stride) {
+    grid_prefix_axis(e, P, m, stride, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+__global__ void k_grid_dead_cells(const uint32_t* __restrict__ off, const uint8_t* __restrict__ e, uint32_t P, uint32_t m,
+                                  uint32_t d, uint32_t diag, uint8_t* cell_dead, unsigned long long* filtered_rows) {
+    unsigned long long rows = grid_dead_cells(off, e, P, m, d, diag, cell_dead, blockIdx.x * blockDim.x + threadIdx.x,
+                                              gridDim.x * blockDim.x);
+    rows = warp_sum_u64(rows);
+    if ((threadIdx.x & 31) == 0 && rows) atomicAdd(filtered_rows, rows);
+}
+
+uint32_t launch_grid_filter(const uint32_t* off, uint32_t P, uint32_t m, uint32_t d, uint8_t* occ, uint8_t* cell_dead,
+                            unsigned long long* filtered_rows, cudaStream_t st) {
+    SKY_CUDA(cudaMemsetAsync(filtered_rows, 0, sizeof(unsigned long long), st));
+    if (!P) return 0;
+    // P = m^d; the all-ones cell (1,..,1) = sum_j m^j
+    uint32_t diag = 0, stride = 1;
+    for (uint32_t j = 0; j < d; ++j) {
+        diag += stride;
+        stride *= m;
+    }
+    constexpr uint32_t kGridCtaCells = 1u << 15;
+    if (P <= kGridCtaCells) {
+        k_grid_filter_cta<<<1, 1024, 0, st>>>(off, P, m, d, diag, occ, cell_dead, filtered_rows);
+        SKY_LAUNCH_CHECK();
+        return 1;
+    }
+    k_grid_occupancy<<<ceil_div(P, 256), 256, 0, st>>>(off, P, occ);
+    SKY_LAUNCH_CHECK();
+    stride = 1;
+    for (uint32_t j = 0; j < d; ++j) {
+        k_grid_prefix_axis<<<ceil_div(P / m, 256), 256, 0, st>>>(occ, P, m, stride);
+        SKY_LAUNCH_CHECK();
+        stride *= m;
+    }
+    k_grid_dead_cells<<<ceil_div(P, 256), 256, 0, st>>>(off, occ, P, m, d, diag, cell_dead, filtered_rows);
+    SKY_LAUNCH_CHECK();
+    return d + 2;
+}
+
 void launch_mark_cells_dead(const uint64_t* key64, uint32_t n, const uint8_t* cell_dead, uint8_t* dead,
                             cudaStream_t st) {
     if (!n) return;

@@ -193,6 +193,11 @@ void launch_fill_live_u8(uint8_t* p, const uint32_t* count, uint32_t cap, cudaSt
 // out[pos[i]] = base + i for live i (dense list of live positions)
 void launch_compact_pos(const uint8_t* dead, const uint32_t* pos, uint32_t n, uint32_t base, uint32_t* out,
                         cudaStream_t st);
+// grid_filter (filter.cpp:37-50) over the P = m^d cells from their row
+// offsets: cell_dead[P] and the rows in filtered cells; occ[P] is scratch.
+// Returns the number of launches.
+uint32_t launch_grid_filter(const uint32_t* off, uint32_t P, uint32_t m, uint32_t d, uint8_t* occ, uint8_t* cell_dead,
+                            unsigned long long* filtered_rows, cudaStream_t st);
 void launch_mark_cells_dead(const uint64_t* key64, uint32_t n, const uint8_t* cell_dead, uint8_t* dead,
                             cudaStream_t st);
 

@@ -1115,7 +1115,7 @@ __global__ void __launch_bounds__(1024) k_small_skyline(const float4* __restrict
         case 10: { constexpr int DT = 10; __VA_ARGS__; break; } \
         case 12: { constexpr int DT = 12; __VA_ARGS__; break; } \
         case 16: { constexpr int DT = 16; __VA_ARGS__; break; } \
-        default: throw Error(SKY_E_INTERNAL, "packed-code kernel needs D <= 16"); \
+        default: throw Error(SKY_E_INTERNAL, std::string("packed-code kernel needs D <= 16 (") + __func__ + ")"); \
     }
 
 template <int D, int K>

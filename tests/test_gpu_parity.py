@@ -512,3 +512,54 @@ def test_stream_small_tail_vs_oracle(engine, options, small_tail):
         assert np.array_equal(r.skyline, exp["ids"]), tag
         check_metrics(r, exp, tag)
         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+
+
+@pytest.mark.parametrize("m,d", [(2, 3), (3, 4), (5, 3), (1, 4), (2, 10), (4, 9), (2, 17)])
+def test_grid_filter_cell_antichain_vs_oracle(engine, m, d):
+    """grid_filter (filter.cpp:37-50) on the device: the per-axis prefix OR of
+    the cell occupancy against the reference's pair loop, from a handful of
+    cells up to m^d = 262,144 (the multi-launch path, above 32,768 cells)."""
+    rng = np.random.default_rng(m * 100 + d)
+    for n, spread in ((400, 1.0), (3000, 1.0), (3000, 0.45)):
+        x = rng.random((n, d), dtype=np.float32)
+        # rows pushed towards the far corner leave the near cells empty, so
+        # few cells are filtered; the full spread filters most of them
+        x = (1.0 - spread + spread * x).astype(np.float32)
+        for merge in (0, 1):
+            cfg = SkyConfig.make(strategy=1, p=m ** d, filter=1, merge=merge, workers=1)
+            exp = O.oracle_run(x, cfg, True)
+            r = engine.run(x, to_engine_config(cfg.as_dict()), True)
+            tag = (m, d, n, spread, merge)
+            assert np.array_equal(r.skyline, exp["ids"]), tag
+            assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+            check_metrics(r, exp, tag)
+
+
+@pytest.mark.parametrize("d", [17, 24, 32])
+def test_wide_rows_vs_oracle(engine, d):
+    """16 < d <= 32 runs on the exact-compare core (no packed codes): every
+    strategy x filter x merge x local algorithm against the oracle."""
+    rng = np.random.default_rng(d)
+    for n in (1, 1500):
+        x = rng.random((n, d), dtype=np.float32)
+        x[:, : d - 3] = np.round(x[:, : d - 3] * 2) / 2  # few distinct values: the skyline is a fraction of the rows
+        for strat in range(4):
+            for filt in ((0, 1, 2) if strat == 1 else (0, 2)):
+                for merge in (0, 1):
+                    for algo in (0, 1):
+                        sel = (strat + merge + algo) % 3 if filt == 2 else 0
+                        p = 2 ** 17 if strat == 1 and d == 17 else 9
+                        cfg = SkyConfig.make(strategy=strat, p=p, seed=3, slice_dim=d - 1, filter=filt, rep_q=4,
+                                             merge=merge, workers=1, rep_selection=sel)
+                        try:
+                            exp = O.oracle_run(x, cfg, True)
+                        except O.CpuError:
+                            continue  # e.g. a grid whose m^d overflows: covered by test_edge_cases
+                        ecfg = to_engine_config(cfg.as_dict())
+                        ecfg.local_algo = LocalAlgo(algo)
+                        ecfg.bnl_window_cap = 64
+                        r = engine.run(x, ecfg, True)
+                        tag = (d, n, strat, filt, merge, algo, sel)
+                        assert np.array_equal(r.skyline, exp["ids"]), tag
+                        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+                        check_metrics(r, exp, tag)
