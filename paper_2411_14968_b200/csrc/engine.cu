@@ -600,6 +600,7 @@ template <class F>
 int guarded(sky_ctx* c, F&& f) {
     try {
         if (c) SKY_CUDA(cudaSetDevice(c->device));
+        cudaGetLastError();  // a failed call of an earlier run must not fail this one's launch checks
         f();
         if (c) c->err.clear();
         return SKY_OK;

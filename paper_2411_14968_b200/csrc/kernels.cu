@@ -7,9 +7,11 @@
 // and warps leave a tile as soon as their coordinate-sum bound is passed or
 // all their candidates are dominated.
 #include <cub/cub.cuh>
+#include <dlfcn.h>
 
 #include <map>
 #include <mutex>
+#include <string>
 #include <tuple>
 
 #include "kernels.cuh"
@@ -35,7 +37,14 @@ void ensure_smem_attr(const void* func, size_t smem) {
     std::lock_guard<std::mutex> lk(mu);
     size_t& cur = done[std::make_pair(dev, func)];
     if (cur >= smem) return;
-    SKY_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // not sticky: leave no stale error for the next launch check
+        Dl_info info{};
+        const char* name = dladdr(func, &info) && info.dli_sname ? info.dli_sname : "?";
+        throw Error(SKY_E_INTERNAL, std::string("shared memory request of ") + std::to_string(smem) + " bytes refused for " +
+                                        name + ": " + cudaGetErrorString(e));
+    }
     cur = smem;
 }
 int occupancy_cached(const void* func, int threads, size_t smem) {
@@ -494,6 +503,8 @@ static const void* prep_stream_kernel(int strategy, bool xd) {
     return xd ? (const void*)k_prep_stream<DT, -1, true> : (const void*)k_prep_stream<DT, -1, false>;
 }
 
+// P: partitions whose per-CTA minima the pass keeps in shared memory (the
+// stream path's a.gmin), 0 without them.
 uint32_t prep_stream_grid(uint32_t n, uint32_t d, uint32_t P, int sm_count, int strategy) {
     const size_t smem = stream_smem_bytes(d) + (size_t)P * sizeof(uint32_t);
     int per_sm = 4;
@@ -510,8 +521,9 @@ void launch_prep(const PrepArgs& a, cudaStream_t st, int sm_count) {
     if (a.n == 0) return;
     if (!a.pts64 && a.d <= 32 && ((uintptr_t)a.pts & 15) == 0 && sm_count > 0) {
         // float rows, 16-byte aligned: persistent CTAs, bulk-copied row tiles
-        const size_t smem = stream_smem_bytes(a.d) + (size_t)a.P * sizeof(uint32_t);
-        const uint32_t grid = prep_stream_grid(a.n, a.d, a.P, sm_count, a.strategy);  // sets the smem attribute
+        const uint32_t pmin = a.gmin ? a.P : 0;  // minima slots only on the stream path
+        const size_t smem = stream_smem_bytes(a.d) + (size_t)pmin * sizeof(uint32_t);
+        const uint32_t grid = prep_stream_grid(a.n, a.d, pmin, sm_count, a.strategy);  // sets the smem attribute
         // grid and angular rows get their own instantiations (the row path
         // then holds only that strategy's code); random / sliced share one
         // and rows exactly as wide as the instantiation get one more (no
@@ -2243,7 +2255,7 @@ __global__ void __launch_bounds__(BNL_B) k_bnl(BnlArgs a, uint32_t cap, uint32_t
                     const uint32_t wn = s_wn;
                     for (uint32_t w = tid; w < wn; w += BNL_B) {
                         const uint32_t meta = win_meta[w];
-                        const bool prev = (int)(meta >> 24) == pass - 1;
+                        const bool prev = (meta >> 24) == ((uint32_t)(pass - 1) & 0xFFu);
                         w_kill[w] = (prev && (meta & 0xFFFFFFu) <= k0) ? 2 : 0;
                     }
                 } else {
@@ -2385,6 +2397,7 @@ __global__ void __launch_bounds__(BNL_B) k_bnl(BnlArgs a, uint32_t cap, uint32_t
                             for (int v = 0; v < V; ++v) w_xyz[slot * V + v] = b_xyz[tid * V + v];
                             win_pos[slot] = mypos;
                             // timestamp: overflow writes in this pass so far
+                            // the pass modulo 256: a window tuple lives two passes at most
                             win_meta[slot] = ((uint32_t)pass << 24) | min(ow, 0xFFFFFFu);
                         } else {
                             ovf[ow + (rank - room)] = mypos;  // ow + ... <= k0 + tid (in place)
@@ -2409,9 +2422,9 @@ __global__ void __launch_bounds__(BNL_B) k_bnl(BnlArgs a, uint32_t cap, uint32_t
                 const uint32_t wn0 = s_wn;
                 for (uint32_t w = tid; w < wn0; w += BNL_B) {
                     const uint32_t meta = win_meta[w];
-                    const bool cur = (int)(meta >> 24) == pass;
+                    const bool cur = (meta >> 24) == ((uint32_t)pass & 0xFFu);
                     const bool confirm = ovf_n == 0 || (cur && (meta & 0xFFFFFFu) == 0) ||
-                                         (!cur && (int)(meta >> 24) == pass - 1);
+                                         (!cur && (meta >> 24) == ((uint32_t)(pass - 1) & 0xFFu));
                     w_kill[w] = confirm ? 2 : 0;
                 }
                 __syncthreads();

@@ -1161,7 +1161,10 @@ bool launch_prefilter(int D, const float* pts, uint32_t d, const uint32_t* idx, 
     const bool codes = rep_qc && thr && nrep >= 32;
     const size_t npad = (nrep + 7) & ~7u;
     const size_t smem = npad * ((D + 3) / 4) * 16 + npad * 12 + (codes ? (size_t)D * kThr * 4 : 0) + 64;
-    if (smem + 1024 > (size_t)smem_optin) return false;
+    // the sorted-position variant also holds its regrouping tables in static
+    // shared memory (256 rows x (V float4 + 5 words), under 24 KB)
+    const size_t stat = codes && posorder ? 24 * 1024 : 1024;
+    if (smem + stat > (size_t)smem_optin) return false;
     if (!n) return true;
     SKY_DISPATCH_D16(D, {
         if (codes && posorder) {

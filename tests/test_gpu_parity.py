@@ -563,3 +563,54 @@ def test_wide_rows_vs_oracle(engine, d):
                         assert np.array_equal(r.skyline, exp["ids"]), tag
                         assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
                         check_metrics(r, exp, tag)
+
+
+@pytest.mark.parametrize("d", [16, 20])
+def test_bnl_many_passes(engine, d):
+    """BNL with a 16-tuple window over one partition of mostly incomparable
+    rows: more than 256 overflow passes (the window records its tuples' pass
+    modulo 256; the d > 16 kernel used to spin forever past pass 255)."""
+    rng = np.random.default_rng(7)
+    x = (rng.integers(0, 4, (12000 if d == 16 else 6000, d)) / 3).astype(np.float32)
+    cfg = SkyConfig.make(strategy=3, p=1, slice_dim=0, merge=1, workers=1)
+    exp = O.oracle_run(x, cfg, True)
+    assert len(exp["ids"]) > 256 * 16
+    ecfg = to_engine_config(cfg.as_dict())
+    ecfg.local_algo = LocalAlgo.BNL
+    ecfg.bnl_window_cap = 16
+    r = engine.run(x, ecfg, True)
+    assert np.array_equal(r.skyline, exp["ids"])
+    check_metrics(r, exp, d)
+
+
+@pytest.mark.parametrize("case", [
+    # (d, data, strategy, p, q, rep_selection): thousands of representatives (past the prefilter's shared
+    # memory) and partition counts past the streamed prep pass's per-partition tables
+    (11, "uniform", 1, 3 ** 11, 1, 0),
+    (16, "lattice", 1, 2 ** 16, 30, 1),
+    (16, "lattice", 1, 2 ** 16, 8, 2),
+    (11, "f64", 3, 1000, 30, 2),
+    (8, "uniform", 0, 5000, 100, 0),
+])
+def test_many_representatives_and_partitions(engine, case):
+    d, data, strat, p, q, sel = case
+    rng = np.random.default_rng(d * 1000 + q)
+    n = 5000
+    if data == "uniform":
+        x = rng.random((n, d), dtype=np.float32)
+    elif data == "lattice":
+        x = (rng.integers(0, 4, (n, d)) / 3).astype(np.float32)
+    else:
+        x = np.clip(rng.integers(0, 1 << 12, (n, d)) / float(1 << 12) + rng.integers(-2, 3, (n, d)) * 2.0 ** -40, 0, 1)
+    for merge in (0, 1):
+        cfg = SkyConfig.make(strategy=strat, p=p, seed=9, slice_dim=d - 1, filter=2, rep_q=q, merge=merge, workers=1,
+                             rep_selection=sel)
+        exp = O.oracle_run(x, cfg, True)
+        for algo in (LocalAlgo.SFS, LocalAlgo.BNL):
+            ecfg = to_engine_config(cfg.as_dict())
+            ecfg.local_algo = algo
+            r = engine.run(x, ecfg, True)
+            tag = (case, merge, algo)
+            assert np.array_equal(r.skyline, exp["ids"]), tag
+            assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+            check_metrics(r, exp, tag)
