@@ -15,7 +15,8 @@ cases = int(sys.argv[1]) if len(sys.argv) > 1 else 600
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 budget_s = float(sys.argv[3]) if len(sys.argv) > 3 else 1e9
 rng = np.random.default_rng(seed)
-eng = Engine(0)
+world = int(os.environ.get("FUZZ_WORLD", "1"))  # > 1: a loopback group of ranks on GPU 0 (the multi-rank engine)
+eng = Engine(0) if world == 1 else Engine.group([0] * world, loopback=True)
 bad = 0
 only = {int(v) for v in os.environ.get("FUZZ_ONLY", "").split(",") if v}  # rerun these iterations only
 t_start = time.time()
@@ -65,9 +66,10 @@ for it in range(cases):
     opts = {"stream": int(rng.choice([-1, 0, 1])), "host_merge": int(rng.integers(0, 2)),
             "cap_sync": int(rng.choice([-1, 0, 1])), "small_tail": int(rng.integers(0, 2)),
             "merge_index": int(rng.integers(0, 2))}
-    eng.reset_options()
-    for k, v in opts.items():
-        eng.set_option(k, v)
+    if world == 1:
+        eng.reset_options()
+        for k, v in opts.items():
+            eng.set_option(k, v)
     tag = dict(it=it, n=n, d=d, kind=kind, strat=strat, p=p, filt=filt, q=q, sel=sel, merge=merge, algo=it % 2,
                win=ecfg.bnl_window_cap, **opts)
     if only and it not in only:
