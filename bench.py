@@ -386,6 +386,12 @@ def run_ours(args):
             ev1.record(stream)
             ev1.synchronize()
             ms.append(ev0.elapsed_time(ev1))
+            if len(res) > 1:
+                # every step must return the same ids; the previous step's id
+                # array is then dropped (a caller does not hoard results, and
+                # the library reuses the buffer), its metrics are kept
+                assert np.array_equal(res[-2].skyline, res[-1].skyline), "non-deterministic skyline across steps"
+                res[-2].skyline = None
             barrier()
         torch.cuda.synchronize()
         return ms, res
@@ -408,8 +414,6 @@ def run_ours(args):
     jobs = 1
     r = dev_res[-1]
     m = r.metrics
-    for rr in dev_res:
-        assert np.array_equal(rr.skyline, r.skyline), "non-deterministic skyline across steps"
     value = w.n * args.steps * jobs / (total_dev / 1e3)
     tests_per_step = statistics.mean(rr.metrics.tests_total for rr in dev_res)
     dom_ms = statistics.mean(rr.metrics.dom_kernel_ms for rr in dev_res)
