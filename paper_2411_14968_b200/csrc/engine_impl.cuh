@@ -2090,13 +2090,15 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
         std::vector<uint64_t> cmp_rows(ncell, 0);
         for (uint32_t cell = 0; cell < ncell; ++cell) {
             if (coff[cell + 1] == coff[cell]) continue;
+            lists[cell].reserve(dom[cell].size());  // one allocation per cell (the device idles while this runs)
             for (uint32_t id : dom[cell])
                 if (coff[id + 1] > coff[id]) {
                     lists[cell].push_back(make_uint2(coff[id], coff[id + 1]));
                     cmp_rows[cell] += coff[id + 1] - coff[id];
                 }
         }
-        auto comps_of = [&](uint32_t cell, std::vector<uint2>& out) { out = lists[cell]; };
+        // each cell's list is asked for once (relsky_waves): handed over, not copied
+        auto comps_of = [&](uint32_t cell, std::vector<uint2>& out) { out = std::move(lists[cell]); };
         // cells split over the ranks by test volume (candidates x comparators)
         const std::vector<uint32_t> cr = plan_ranges(coff, ncell, W, [&](uint32_t cell) -> uint64_t {
             const uint64_t nc = coff[cell + 1] - coff[cell];
