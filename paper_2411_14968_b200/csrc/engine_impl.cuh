@@ -40,7 +40,7 @@ struct sky_options {
     uint32_t merge_tile = 0;    // candidates per merge item (0: from the union size)
     uint32_t merge_head = 4096; // merge wave 0 length
     uint32_t grain_items = 4;   // work items per resident CTA
-    uint32_t bnl_block = 2048;  // BNL: rows per block (one CTA each), 0 = one CTA per partition
+    uint32_t bnl_block = 1024;  // BNL: rows per block (one CTA each), 0 = one CTA per partition (512-1024 measured best on config 4)
     int32_t merge_index = 1;    // merge through the cell index of the union (host-planned merges)
     uint32_t merge_cell_rows = 1024;  // target rows per cell of that index
     uint32_t range_par = 4;     // ranges per item from which warps take whole ranges (0: never)
