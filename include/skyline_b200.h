@@ -94,7 +94,8 @@ typedef struct sky_config {
 } sky_config;
 
 /* RunResult + PhaseMetrics (engine.hpp:40-57). Owned by the library until
- * sky_result_free. */
+ * sky_result_free: `ids` comes from the library's own pool (do not free() it,
+ * do not hand it to sky_free). */
 typedef struct sky_result {
     int64_t* ids;               /* skyline ids, ascending (engine.cpp:132) */
     uint64_t n_ids;
