@@ -90,6 +90,22 @@ class SkyResult(C.Structure):
     ]
 
 
+def _struct_of(cstruct):
+    """struct.Struct with the C layout of a ctypes.Structure of scalars and
+    pointers: one unpack reads every field (a ctypes attribute fetch per field
+    costs ~20 us per result, inside a caller's timed region)."""
+    import struct
+    codes = {C.c_double: "d", C.c_float: "f", C.c_uint64: "Q", C.c_int64: "q", C.c_uint32: "I", C.c_int32: "i"}
+    fmt = "@" + "".join(codes.get(t, "P") for _, t in cstruct._fields_)
+    st = struct.Struct(fmt)
+    assert st.size == C.sizeof(cstruct), (st.size, C.sizeof(cstruct))
+    return st
+
+
+SKY_RESULT_STRUCT = _struct_of(SkyResult)
+SKY_RESULT_FIELDS = {name: k for k, (name, _) in enumerate(SkyResult._fields_)}
+
+
 # Every symbol include/skyline_b200.h declares; tests check the library
 # exports all of them.
 EXPORTED = [

@@ -116,6 +116,7 @@ class PartitionConfig:
     slice_dim: int = 0
 
 
+_RF = abi.SKY_RESULT_FIELDS
 _ZERO_COPY_IDS = 1 << 16  # ids from which RunResult.skyline is a view of the library's buffer
 
 
@@ -403,41 +404,39 @@ class Engine:
     def _result(self, res, config) -> RunResult:
         owned = False
         try:
-            # memmove instead of np.ctypeslib.as_array (~10 us of array-interface
-            # setup per call, inside the caller's timed region)
-            nid = int(res.n_ids)
+            # every scalar of the result in one unpack (no per-field ctypes
+            # fetch); ids by memmove instead of np.ctypeslib.as_array (~10 us
+            # of array-interface setup per call, inside the caller's timed
+            # region)
+            v = abi.SKY_RESULT_STRUCT.unpack_from(res)
+            f = _RF
+            nid = v[f["n_ids"]]
             if nid >= _ZERO_COPY_IDS:
                 # megabytes of ids: a view of the library's buffer instead of
                 # a fresh array (its page faults and the copy cost ~2 ms on
                 # 700k ids); the buffer goes back to the library when the
                 # last view of it is collected
-                buf = (C.c_int64 * nid).from_address(C.addressof(res.ids.contents))
+                buf = (C.c_int64 * nid).from_address(v[f["ids"]])
                 buf._owner = _ResultOwner(self._lib, res)
                 owned = True
                 ids = np.frombuffer(buf, dtype=np.int64)
             else:
                 ids = np.empty(nid, np.int64)
                 if nid:
-                    C.memmove(ids.ctypes.data, res.ids, nid * 8)
-            P = int(res.effective_p)
+                    C.memmove(ids.ctypes.data, v[f["ids"]], nid * 8)
+            P = v[f["effective_p"]]
             sizes_a = np.empty(P, np.uint64)
             if P:
-                C.memmove(sizes_a.ctypes.data, res.local_skyline_sizes, P * 8)
-            sizes = sizes_a.astype(np.int64).tolist()
+                C.memmove(sizes_a.ctypes.data, v[f["local_skyline_sizes"]], P * 8)
             m = PhaseMetrics(
-                partition_ms=res.partition_ms, local_ms=res.local_ms, merge_ms=res.merge_ms,
-                local_skyline_sizes=sizes, union_size=int(res.union_size),
-                filtered_count=int(res.filtered_count), final_size=int(res.final_size),
-                total_ms=res.total_ms, tests_reps=int(res.tests_reps), tests_local=int(res.tests_local),
-                tests_merge=int(res.tests_merge), n_reps=int(res.n_reps),
-                angular_host_fixups=int(res.angular_host_fixups), kernel_launches=int(res.kernel_launches),
-                h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
-                dom_launches=int(res.dom_launches), dom_kernel_ms=float(res.dom_kernel_ms),
-                dom_tests=int(res.dom_tests), dom_exact_checks=int(res.dom_exact_checks),
-                stream_launches=int(res.stream_launches), stream_kernel_ms=float(res.stream_kernel_ms),
-                stream_bytes=int(res.stream_bytes), world=int(res.world) or 1, sharded=bool(res.sharded),
-                exchange_bytes=int(res.exchange_bytes), local_rows=int(res.local_rows))
-            return RunResult(ids, m, config, P, int(res.input_size), int(res.input_dim))
+                v[f["partition_ms"]], v[f["local_ms"]], v[f["merge_ms"]], sizes_a.tolist(), v[f["union_size"]],
+                v[f["filtered_count"]], v[f["final_size"]], v[f["total_ms"]], v[f["tests_reps"]],
+                v[f["tests_local"]], v[f["tests_merge"]], v[f["n_reps"]], v[f["angular_host_fixups"]],
+                v[f["kernel_launches"]], v[f["h2d_bytes"]], v[f["d2h_bytes"]], v[f["dom_launches"]],
+                v[f["dom_kernel_ms"]], v[f["dom_tests"]], v[f["stream_launches"]], v[f["stream_kernel_ms"]],
+                v[f["stream_bytes"]], v[f["dom_exact_checks"]], v[f["world"]] or 1, bool(v[f["sharded"]]),
+                v[f["exchange_bytes"]], v[f["local_rows"]])
+            return RunResult(ids, m, config, P, v[f["input_size"]], v[f["input_dim"]])
         finally:
             if not owned:
                 self._lib.sky_result_free(C.byref(res))
