@@ -113,13 +113,13 @@ typedef struct sky_result {
     uint64_t h2d_bytes, d2h_bytes;
     uint32_t kernel_launches;   /* kernels this library launched for the run */
     uint32_t dom_launches;      /* dominance-kernel (k_relsky/k_bnl) launches */
-    double dom_kernel_ms;       /* summed CUDA-event time of those launches */
+    double dom_kernel_ms;       /* summed CUDA-event time of those launches (option kernel_events = 1, else 0) */
     uint64_t dom_tests;         /* dominance tests they executed */
     uint64_t dom_exact_checks;  /* pairs the packed codes could not rule out */
     uint64_t exact_checks_merge;
     /* HBM streaming passes (prep, representative prefilter, candidate pass) */
     uint32_t stream_launches;
-    double stream_kernel_ms;    /* summed CUDA-event time of those launches */
+    double stream_kernel_ms;    /* summed CUDA-event time of those launches (option kernel_events = 1, else 0) */
     uint64_t stream_bytes;      /* algorithmic bytes they move (reads + writes) */
     /* multi-GPU (ABI v3) */
     uint32_t world;             /* ranks that computed the result (1: one GPU) */

@@ -379,7 +379,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         R.dom_collect();
         out->stream_kernel_ms = R.hbm_collect();
         out->stream_bytes = c->hbm_bytes;
-        out->stream_launches = c->hbm_used;
+        out->stream_launches = c->hbm_launches;
         R.timeline_dump();
         out->dom_kernel_ms = c->dom_ms;
         out->dom_tests = hts[0] + hts[1] + hts[2];
@@ -1050,6 +1050,7 @@ int sky_ctx_set_option(sky_ctx* c, const char* name, int64_t v) {
     else if (k == "profile_host") o.profile_host = s > 0;
     else if (k == "timeline") o.timeline = s > 0;
     else if (k == "small_tail") o.small_tail = s > 0;
+    else if (k == "kernel_events") o.kernel_events = s > 0;
     else {
         c->err = "unknown option or value: " + k;
         return SKY_E_CONFIG;

@@ -49,6 +49,8 @@ struct sky_options {
     int32_t profile_host = 0;   // print host-side planning / wait times
     int32_t timeline = 0;       // an event after every launch, dumped per run
     int32_t small_tail = 1;     // stream path: the fused tail when <= kSmallCap rows survive the prefilter
+    int32_t kernel_events = 0;  // CUDA events around the dominance launches and HBM passes (dom_kernel_ms / stream_kernel_ms of
+                                // sky_result; off by default: the records between kernels cost 25-55 us per run)
 };
 
 struct sky_ctx {
@@ -71,6 +73,7 @@ struct sky_ctx {
     uint32_t dom_used = 0;
     std::vector<cudaEvent_t> hbm_ev;  // (start, end) pairs of the HBM streaming passes of a run
     uint32_t hbm_used = 0;
+    uint32_t hbm_launches = 0;  // passes of the run (counted with or without their events)
     uint64_t hbm_bytes = 0;
     // pinned staging for async H2D copies: bump-allocated per run, never
     // reused within a run, so no launch has to wait for its copy to drain
@@ -468,6 +471,7 @@ class Runner {
         c->stage_cur = c->stage_off = 0;
         c->dom_used = 0;
         c->hbm_used = 0;
+        c->hbm_launches = 0;
         c->hbm_bytes = 0;
     }
 
@@ -1066,6 +1070,7 @@ class Runner {
 
     // CUDA events around each dominance launch; summed once the run drained
     void dom_begin() {
+        if (!c_->opt.kernel_events) return;
         auto& e = c_->dom_ev;
         while (e.size() < 2 * (size_t)(c_->dom_used + 1)) {
             cudaEvent_t ev;
@@ -1075,12 +1080,15 @@ class Runner {
         SKY_CUDA(cudaEventRecord(e[2 * c_->dom_used], st_));
     }
     void dom_end() {
+        c_->dom_launches += c_->opt.kernel_events ? 0 : 1;
+        if (!c_->opt.kernel_events) return;
         SKY_CUDA(cudaEventRecord(c_->dom_ev[2 * c_->dom_used + 1], st_));
         ++c_->dom_used;
         c_->dom_launches += 1;
     }
     // the same for the HBM streaming passes, with their algorithmic bytes
     void hbm_begin() {
+        if (!c_->opt.kernel_events) return;
         auto& e = c_->hbm_ev;
         while (e.size() < 2 * (size_t)(c_->hbm_used + 1)) {
             cudaEvent_t ev;
@@ -1090,12 +1098,18 @@ class Runner {
         SKY_CUDA(cudaEventRecord(e[2 * c_->hbm_used], st_));
     }
     void hbm_end(uint64_t bytes) {
+        ++c_->hbm_launches;
+        c_->hbm_bytes += bytes;
+        if (!c_->opt.kernel_events) return;
         SKY_CUDA(cudaEventRecord(c_->hbm_ev[2 * c_->hbm_used + 1], st_));
         ++c_->hbm_used;
-        c_->hbm_bytes += bytes;
     }
     // an event pair for a pass the launcher brackets itself (recorded there)
     void hbm_pair(uint64_t bytes, cudaEvent_t* begin, cudaEvent_t* end) {
+        *begin = *end = nullptr;
+        ++c_->hbm_launches;
+        c_->hbm_bytes += bytes;
+        if (!c_->opt.kernel_events) return;
         auto& e = c_->hbm_ev;
         while (e.size() < 2 * (size_t)(c_->hbm_used + 1)) {
             cudaEvent_t ev;
@@ -1105,7 +1119,6 @@ class Runner {
         *begin = e[2 * c_->hbm_used];
         *end = e[2 * c_->hbm_used + 1];
         ++c_->hbm_used;
-        c_->hbm_bytes += bytes;
     }
     double hbm_collect() {
         double t = 0.0;
@@ -2220,7 +2233,7 @@ inline void merge_phase(Runner& R, sky_ctx* c, const sky_config* cfg, DevSet U, 
     R.dom_collect();
     out->stream_kernel_ms = R.hbm_collect();
     out->stream_bytes = c->hbm_bytes;
-    out->stream_launches = c->hbm_used;
+    out->stream_launches = c->hbm_launches;
     R.timeline_dump();
     out->dom_kernel_ms = c->dom_ms;
     out->dom_tests = ht[0] + ht[1] + ht[2];

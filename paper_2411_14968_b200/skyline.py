@@ -298,7 +298,7 @@ class Engine:
 
     DEFAULT_OPTIONS = {"stream": -1, "host_merge": 0, "cap_sync": -1, "sfs_tile": 0, "sfs_chunk": 2048,
                        "sfs_head": 2048, "merge_tile": 0, "merge_head": 4096, "grain_items": 4, "bnl_block": 1024, "merge_index": 1, "merge_cell_rows": 1024, "range_par": 4, "sfs_auto_chunk": 1, "wave_growth": 4, "wave_split_mpairs": 8192, "profile_host": 0,
-                       "timeline": 0, "small_tail": 1}
+                       "timeline": 0, "small_tail": 1, "kernel_events": 0}
 
     def reset_options(self):
         for k, v in self.DEFAULT_OPTIONS.items():

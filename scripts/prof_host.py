@@ -5,6 +5,7 @@ from paper_2411_14968_b200.configs import make_config
 import torch
 eng = Engine(0)
 eng.set_option("profile_host", 1)
+eng.set_option("kernel_events", 1)
 w = make_config(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 x = generate(w.kind, w.n, w.d, 42)
 xd = torch.from_numpy(x).cuda()

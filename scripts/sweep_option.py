@@ -28,6 +28,7 @@ e = Engine(0)
 st = torch.cuda.current_stream()
 e.set_stream(st.cuda_stream)
 ref = None
+e.set_option("kernel_events", 1)  # dom_kernel_ms in the output (25-55 us per step of event records)
 for v in a.values:
     e.set_option(a.option, v)
     run = lambda: e.run(None, w.config, w.normalized, device_ptr=xd.data_ptr(), n=w.n, d=w.d)
