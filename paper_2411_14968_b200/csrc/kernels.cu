@@ -915,9 +915,10 @@ __global__ void k_rep_pick(const uint64_t* __restrict__ key64, const uint32_t* _
 // thr[p] = q-th smallest of gmin[., p] (0xFFFFFFFF when fewer than q chunks
 // hold rows of p: then every row of p is a candidate). A warp per partition.
 __global__ void k_part_thresh(const uint32_t* __restrict__ gmin, uint32_t G, uint32_t P, uint32_t q,
-                              uint32_t* __restrict__ thr) {
+                              uint32_t* __restrict__ thr, uint32_t* __restrict__ bucket_count) {
     const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (p >= P) return;
+    if (lane == 0) bucket_count[p] = 0;  // the candidate pass counts from zero (no memset between the launches)
     uint64_t last = 0;
     for (uint32_t r = 0; r < q; ++r) {
         uint64_t best = ~0ull;
@@ -1136,9 +1137,8 @@ void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32
                            uint32_t* brow, const float* pts, uint32_t d, uint32_t* cand, uint32_t* overflow,
                            cudaStream_t st, cudaEvent_t pass_begin, cudaEvent_t pass_end) {
     if (B > 1024) throw Error(SKY_E_INTERNAL, "candidate buckets hold at most 1024 rows");
-    k_part_thresh<<<ceil_div((uint64_t)P * 32, 256), 256, 0, st>>>(gmin, G, P, q, thr);
+    k_part_thresh<<<ceil_div((uint64_t)P * 32, 256), 256, 0, st>>>(gmin, G, P, q, thr, cnt);
     SKY_LAUNCH_CHECK();
-    SKY_CUDA(cudaMemsetAsync(cnt, 0, P * sizeof(uint32_t), st));
     // the key pass alone is timed as an HBM pass (thresholds and picks are latency-bound)
     if (pass_begin) SKY_CUDA(cudaEventRecord(pass_begin, st));
     k_cand_bucket<<<ceil_div(ceil_div(n, 4), 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
