@@ -189,6 +189,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
 
     // ---------------------------------------------- representatives + filter
     uint64_t rep_filtered = 0;
+    uint32_t* small_flags = nullptr;  // the small tail's flags when the stream prefilter cleared them
     if (cfg->filter == SKY_FILTER_REPRESENTATIVE) {
         const uint32_t q = (uint32_t)std::min<uint64_t>(cfg->rep_q, n);
         uint32_t* cand = R.dev<uint32_t>(S_REPCAND, (size_t)P * q);
@@ -255,6 +256,11 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             app.count = misc + M_S0;
             app.key_shift = key_shift_for(P);
             app.row_bits = (uint32_t)std::max(1, bits_for(n));
+            // the fused small tail follows this pass: it clears the tail's flags on the way
+            small_flags = c->world == 1 && c->opt.small_tail != 0 && (uint64_t)P <= kSmallMaxParts
+                              ? R.dev<uint32_t>(S_SM_W, (size_t)3 * kSmallCap) : nullptr;
+            app.zero = small_flags;
+            app.zero_words = small_flags ? 3 * kSmallCap : 0;
             R.hbm_begin();
             if (!launch_prefilter_append(D, pts, d, n, reps.xyz, reps.skey, pthr ? reps.qc : nullptr, reps.id, reps.n,
                                          nrep_dev, pthr, app, count_tests ? R.tests(1) : nullptr, c->smem_optin, st))
@@ -368,9 +374,12 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
         out->partition_ms = ms;
-        cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+        // the fused small tail ends the local phase at the end of the run (no
+        // merge phase, no events of its own)
+        cudaEventElapsedTime(&ms, c->ev[1], c->ev[small ? 4 : 2]);
         out->local_ms = ms;
-        cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+        ms = 0;
+        if (!small) cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
         out->merge_ms = ms;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]);
         out->total_ms = ms;
@@ -416,6 +425,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         t.key_shift = key_shift_for(P);
         t.cap = kSmallCap;
         t.flags = R.dev<uint32_t>(S_SM_W, (size_t)3 * kSmallCap);
+        t.flags_zeroed = small_flags == t.flags;
         t.cnt = R.dev<uint32_t>(S_SM_CNT, P);
         t.u_count = misc + M_U;
         t.total = misc + M_TOTAL;
@@ -428,9 +438,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         launch_small_tail(D, t, st);
         R.count(2);
         // one pass gives the local skylines and the merge: the merge phase
-        // is empty
-        SKY_CUDA(cudaEventRecord(c->ev[2], st));
-        SKY_CUDA(cudaEventRecord(c->ev[3], st));
+        // is empty and the local phase ends with the run (publish)
         return publish(t.hid, 0, true);
     };
     auto early_merge = [&](const DevSet& Ucap) {

@@ -377,6 +377,10 @@ struct PrefilterAppend {
     uint32_t* count = nullptr;
     uint32_t key_shift = 0, row_bits = 0;
     uint32_t regroup = 64;  // POSORDER: representatives before the CTA regroups its live rows
+    // APPEND: words the pass clears on the way (the fused small tail's flags:
+    // no memset between the prefilter and the tail)
+    uint32_t* zero = nullptr;
+    uint32_t zero_words = 0;
 };
 // Fused tail of a stream-path run with few prefilter survivors (small.cu).
 constexpr uint32_t kSmallCap = 4096;
@@ -385,7 +389,8 @@ struct SmallTail {
     const uint32_t* count = nullptr; // their device count
     const float* pts = nullptr;
     uint32_t d = 0, P = 0, row_bits = 0, key_shift = 0, cap = kSmallCap;
-    uint32_t* flags = nullptr;       // 3 x cap words, zeroed by the launcher: local dead, dead, rank
+    uint32_t* flags = nullptr;       // 3 x cap words: local dead, dead, rank; zeroed by the launcher unless
+    bool flags_zeroed = false;       // the prefilter pass already cleared them (PrefilterAppend::zero)
     uint32_t* cnt = nullptr;         // P words: local skyline size per partition
     uint32_t* u_count = nullptr;     // |union| (device)
     uint32_t* total = nullptr;       // final count (device)

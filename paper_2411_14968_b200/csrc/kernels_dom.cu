@@ -808,6 +808,9 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ pts
     };
     if (CODES)
         for (uint32_t i = threadIdx.x; i < D * kThr; i += blockDim.x) s_thr[i] = thr[i];
+    if (APPEND && app.zero)
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < app.zero_words; i += gridDim.x * blockDim.x)
+            app.zero[i] = 0;
     // APPEND: the row tiles stream through shared memory after the tables
     char* s_stage = reinterpret_cast<char*>(
         (reinterpret_cast<uintptr_t>(s_thr + (CODES ? D * kThr : 0)) + 15) & ~uintptr_t{15});

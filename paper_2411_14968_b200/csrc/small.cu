@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_small_finish(SmallTail t) {
 }  // namespace
 
 void launch_small_tail(int D, const SmallTail& t, cudaStream_t st) {
-    SKY_CUDA(cudaMemsetAsync(t.flags, 0, (size_t)3 * t.cap * sizeof(uint32_t), st));
+    if (!t.flags_zeroed) SKY_CUDA(cudaMemsetAsync(t.flags, 0, (size_t)3 * t.cap * sizeof(uint32_t), st));
     const uint32_t grid = kPairCtasPerSm * (uint32_t)device_sm_count();
     SKY_DISPATCH_DOM(D, (k_small_pairs<DT><<<grid, kPairRows, 0, st>>>(t)));
     const size_t smem = (size_t)t.cap * sizeof(uint32_t);
