@@ -405,7 +405,7 @@ struct SmallTail {
 };
 constexpr uint32_t kSmallMiscWords = 32;
 // all pairs of survivors (local + global dominance, ranks), then the counts,
-// offsets and ascending ids (one memset + 2 launches)
+// offsets and ascending ids (2 launches; a memset before them unless flags_zeroed)
 void launch_small_tail(int D, const SmallTail& t, cudaStream_t st);
 
 // false: not applicable (d > 16, unaligned rows, shared memory)

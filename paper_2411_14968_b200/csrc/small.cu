@@ -14,8 +14,9 @@
 //     U (dominance is transitive and S is finite), and rows outside U are
 //     dominated within S;
 //   * the ascending ids are the final rows ordered by their rank among S.
-// So the tail is one memset and two launches sized by the capacity, every
-// count staying on the device, and one round trip at the end:
+// So the tail is two launches sized by the capacity (its flag words are
+// cleared by the prefilter pass before it, else by one memset), every count
+// staying on the device, and one round trip at the end:
 //
 //   k_small_pairs   tiles of 128 x 32 pairs (i, j) of S over resident CTAs: row
 //                   i is locally dead when a row j of its partition dominates
