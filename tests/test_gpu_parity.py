@@ -614,3 +614,41 @@ def test_many_representatives_and_partitions(engine, case):
             assert np.array_equal(r.skyline, exp["ids"]), tag
             assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
             check_metrics(r, exp, tag)
+
+
+def test_baseline_sized_random_configs_vs_reference(engine):
+    """Random configurations at BASELINE-like sizes (100k-1.5M rows of the
+    BASELINE generators) with the engine's default options, so the stream
+    path (inputs over 32 MB), the device-planned merges and the indexed merge
+    take their production branches, against the reference itself
+    (oracle/_ref, all host threads). scripts/fuzz_gpu_big.py runs the long
+    version of this sweep."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref/libskyref.so was not built")
+    import os
+    rng = np.random.default_rng(2411)
+    for it in range(16):
+        d = int(rng.choice([3, 4, 5, 6, 8]))
+        n = int(rng.choice([100_000, 300_000, 1_000_000, 1_500_000]))
+        kind = int(rng.choice([1, 3, 3, 5, 2]))
+        if kind == 2 and n > 300_000:
+            kind = 3
+        x = generate(kind, n, d, int(rng.integers(1 << 30)))
+        norm = kind != 5
+        strat = int(rng.integers(0, 4))
+        filt = int(rng.choice([0, 2, 2] + ([1] if strat == 1 else [])))
+        p = int(rng.choice([2, 3])) ** d if strat == 1 else int(rng.choice([8, 32, 128, 500]))
+        if kind == 5 and strat == 1:  # integers are outside [0, 1]: the grid raises (test_edge_cases)
+            strat, p, filt = 0, 32, 2 if filt == 1 else filt
+        sel = int(rng.choice([0, 0, 1, 2])) if filt == 2 and norm else 0
+        cfg = SkyConfig.make(strategy=strat, p=p, seed=int(rng.integers(0, 1000)), slice_dim=int(rng.integers(0, d)),
+                             filter=filt, rep_q=int(rng.choice([1, 5, 8, 20])), merge=int(rng.integers(0, 2)),
+                             workers=os.cpu_count() or 8, rep_selection=sel)
+        exp = O.ref_run(x, cfg, norm)
+        ecfg = to_engine_config(cfg.as_dict())
+        ecfg.local_algo = LocalAlgo(it % 2)
+        r = engine.run(x, ecfg, norm)
+        tag = (it, n, d, kind, strat, p, filt, sel, cfg.merge, it % 2)
+        assert np.array_equal(r.skyline, exp["ids"]), tag
+        assert r.metrics.local_skyline_sizes == exp["local_skyline_sizes"].astype(int).tolist(), tag
+        check_metrics(r, exp, tag)
