@@ -151,7 +151,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         stream = want && !eager && c->world == 1 && !f64 && cfg->filter == SKY_FILTER_REPRESENTATIVE &&
                  cfg->rep_selection == SKY_REPS_SORTED && cfg->strategy != SKY_SLICED && pb <= 12 &&
                  (uint64_t)P * std::min<uint64_t>(cfg->rep_q, n) <= 2048 && cfg->rep_q <= 64 && D <= 16 &&
-                 ((uintptr_t)pts & 15) == 0 && (uint64_t)P * kRepBucket <= (1ull << 31) &&
+                 ((uintptr_t)pts & 15) == 0 && (uint64_t)P * c->rep_bucket <= (1ull << 24) &&
                  32 + bits_for(n) <= 64;
     }
     // stream path: the prep pass also leaves each CTA's minimum key per
@@ -207,11 +207,11 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             // each sorted by (key, row), then the same exact pick
             uint32_t* thr = R.dev<uint32_t>(S_PTHR2, P);
             uint32_t* bcnt = R.dev<uint32_t>(S_BCNT, P);
-            uint64_t* bkey = R.dev<uint64_t>(S_BKEY, (size_t)P * kRepBucket);
-            uint32_t* brow = R.dev<uint32_t>(S_BROW, (size_t)P * kRepBucket);
+            uint64_t* bkey = R.dev<uint64_t>(S_BKEY, (size_t)P * c->rep_bucket);
+            uint32_t* brow = R.dev<uint32_t>(S_BROW, (size_t)P * c->rep_bucket);
             cudaEvent_t pb, pe;
             R.hbm_pair((uint64_t)n * 8, &pb, &pe);  // the key pass alone (thresholds and picks are latency-bound)
-            launch_rep_candidates(po.key64, n, P, q, prep_grid, gmin, thr, kRepBucket, bcnt, bkey, brow, pts, d,
+            launch_rep_candidates(po.key64, n, P, q, prep_grid, gmin, thr, c->rep_bucket, bcnt, bkey, brow, pts, d,
                                   cand, misc + M_OVF, st, pb, pe);
             R.count(3);
         } else {
@@ -357,7 +357,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
         }
         check_prep(hmisc[M_ERR], hmisc[M_AMB], cfg->strategy, eager);
         if (defer_rand && hmisc[M_RFLAG]) throw RedoEager{};
-        if (hmisc[M_OVF]) throw RedoEager{};
+        if (hmisc[M_OVF]) throw_bucket_overflow(c);
         if (cfg->filter == SKY_FILTER_REPRESENTATIVE) out->n_reps = hmisc[M_NREP];
         const uint32_t ns = stream && !small ? ns_host : hmisc[M_S0];
         out->filtered_count = (uint64_t)n - ns;
@@ -461,7 +461,7 @@ void run_impl(sky_ctx* c, const void* points, uint64_t n64, uint32_t d, int norm
             R.sync();
         }
         check_prep(hc[M_ERR], hc[M_AMB], cfg->strategy, eager);
-        if (hc[M_OVF]) throw RedoEager{};  // a candidate bucket filled up: sorted path
+        if (hc[M_OVF]) throw_bucket_overflow(c);  // a candidate bucket filled up: larger buckets, then the sorted path
         const uint32_t ns = hc[M_S0];
         const uint32_t rb = (uint32_t)std::max(1, bits_for(n));
         uint64_t* surv = R.dev<uint64_t>(S_SURV, n);
@@ -628,10 +628,25 @@ int guarded(sky_ctx* c, F&& f) {
 // run_impl with its eager retry (angular boundary rows, rejected random draws)
 void run_impl_retry(sky_ctx* c, const void* points, uint64_t n, uint32_t d, int normalized, int on_device,
                     const sky_config* cfg, sky_result* out, bool f64) {
+    struct BucketReset {  // whatever happens, the next run starts with the normal buckets
+        sky_ctx* c;
+        ~BucketReset() { c->rep_bucket = sky::kRepBucket; }
+    } reset{c};
     try {
-        run_impl(c, points, n, d, normalized, on_device, cfg, out, false, f64);
+        // a relation whose last run overflowed the normal buckets (queried
+        // again, same size) starts with the large ones
+        if (n && c->big_bucket_rows == n) c->rep_bucket = kRepBucketBig;
+        try {
+            run_impl(c, points, n, d, normalized, on_device, cfg, out, false, f64);
+        } catch (const RedoBigBuckets&) {
+            sky_result_free(out);
+            c->rep_bucket = kRepBucketBig;
+            c->big_bucket_rows = n;
+            run_impl(c, points, n, d, normalized, on_device, cfg, out, false, f64);
+        }
     } catch (const RedoEager&) {
         sky_result_free(out);
+        if (c->rep_bucket == kRepBucketBig) c->big_bucket_rows = 0;  // the large buckets did not help either
         run_impl(c, points, n, d, normalized, on_device, cfg, out, true, f64);
     }
 }

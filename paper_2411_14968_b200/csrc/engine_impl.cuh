@@ -81,6 +81,8 @@ struct sky_ctx {
     size_t stage_cur = 0, stage_off = 0;
     uint32_t launches = 0;
     uint32_t dom_launches = 0;
+    uint32_t rep_bucket = sky::kRepBucket;  // candidate bucket slots of the current run (run_impl_retry)
+    uint64_t big_bucket_rows = 0;  // row count of the last run that needed the large buckets: runs of that size start with them
     double dom_ms = 0.0;
     // multi-GPU: this context is rank `rank` of `world` (one GPU each); the
     // exchanges go through `comm` (NCCL over NVLink/NVSwitch, or loopback
@@ -200,8 +202,6 @@ enum { M_ERR = 0, M_AMB = 1, M_RUNS = 2, M_TOTAL = 3, M_BNLCTR = 4, M_WORK = 5, 
        M_S0 = 24, M_U = 26, M_NP = 27 /* device-side set counts (single-GPU path) */,
        M_RFLAG = 28 /* random partitioner: a draw the reference would reject */,
        M_OVF = 29 /* stream path: a representative candidate bucket overflowed */ };
-// stream path (representative filter over large inputs): candidate bucket size
-constexpr uint32_t kRepBucket = 1024;
 // the fused small tail writes P + 1 union offsets from one CTA
 constexpr uint32_t kSmallMaxParts = 1u << 16;
 
@@ -1627,6 +1627,15 @@ inline bool weak_grid_dom(uint64_t a, uint64_t b, uint64_t m, uint32_t d) {
 }
 
 struct RedoEager {};  // angular boundary points seen by a deferred prep
+// stream path: a candidate bucket of kRepBucket slots filled up (a tie run of
+// more than 1,024 minimum keys in one partition, e.g. duplicates clipped to
+// a corner): the run is redone on the stream path with kRepBucketBig slots;
+// if that overflows too, on the sorted path (RedoEager)
+struct RedoBigBuckets {};
+[[noreturn]] inline void throw_bucket_overflow(const sky_ctx* c) {
+    if (c->rep_bucket < kRepBucketBig) throw RedoBigBuckets{};
+    throw RedoEager{};
+}
 
 inline void check_prep(uint32_t err, uint32_t amb, int strategy, bool eager) {
     if (err & kErrNonFinite) throw Error(SKY_E_DATA, "coordinate must be finite and >= 0");

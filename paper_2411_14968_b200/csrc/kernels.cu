@@ -996,13 +996,16 @@ __global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict_
                                                      const uint32_t* __restrict__ cnt, uint32_t B,
                                                      const float* __restrict__ pts, uint32_t d, uint32_t q,
                                                      uint32_t* __restrict__ cand, uint32_t run_floats) {
-    constexpr uint32_t MAXB = 1024;
-    __shared__ uint64_t s_c[MAXB];  // (key << 32 | row)
-    __shared__ double s_sum[MAXB];
-    __shared__ uint8_t s_taken[MAXB];
+    // dynamic shared memory: the tie run's coordinates (run_floats floats),
+    // then B slots of (key << 32 | row), FP64 sums and taken flags (B = 1,024
+    // normally; the retry after a bucket overflow runs with larger buckets)
+    extern __shared__ float4 s_run4[];
+    uint64_t* s_c = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(s_run4) + run_floats);
+    double* s_sum = reinterpret_cast<double*>(s_c + B);
+    uint8_t* s_taken = reinterpret_cast<uint8_t*>(s_sum + B);
     __shared__ uint32_t s_ra, s_rb, s_best[8];
     const uint32_t p = blockIdx.x;
-    const uint32_t c = min(cnt[p], min(B, MAXB));
+    const uint32_t c = min(cnt[p], B);
     uint32_t* out = cand + (size_t)p * q;
     for (uint32_t k = threadIdx.x; k < q; k += blockDim.x) out[k] = kNone;
     if (c == 0) return;
@@ -1035,8 +1038,7 @@ __global__ void __launch_bounds__(256) k_bucket_pick(const uint64_t* __restrict_
     }
     // the run's rows (coordinates, FP64 sums) in shared memory: a run of
     // duplicates compares every coordinate of every pair
-    extern __shared__ float4 s_run4[];  // [L][d4] when in_smem (rows padded to float4s)
-    float* s_run = reinterpret_cast<float*>(s_run4);
+    float* s_run = reinterpret_cast<float*>(s_run4);  // [L][d4] when in_smem (rows padded to float4s)
     const uint32_t d4 = (d + 3) & ~3u;
     const bool in_smem = (size_t)L * d4 <= run_floats;
     if (in_smem) {
@@ -1136,7 +1138,7 @@ void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32
                            const uint32_t* gmin, uint32_t* thr, uint32_t B, uint32_t* cnt, uint64_t* bkey,
                            uint32_t* brow, const float* pts, uint32_t d, uint32_t* cand, uint32_t* overflow,
                            cudaStream_t st, cudaEvent_t pass_begin, cudaEvent_t pass_end) {
-    if (B > 1024) throw Error(SKY_E_INTERNAL, "candidate buckets hold at most 1024 rows");
+    if (B > kRepBucketBig || (B & (B - 1))) throw Error(SKY_E_INTERNAL, "candidate buckets: a power of two up to 8192 rows");
     k_part_thresh<<<ceil_div((uint64_t)P * 32, 256), 256, 0, st>>>(gmin, G, P, q, thr, cnt);
     SKY_LAUNCH_CHECK();
     // the key pass alone is timed as an HBM pass (thresholds and picks are latency-bound)
@@ -1144,9 +1146,11 @@ void launch_rep_candidates(const uint64_t* key64, uint32_t n, uint32_t P, uint32
     k_cand_bucket<<<ceil_div(ceil_div(n, 4), 256), 256, 0, st>>>(key64, n, thr, B, cnt, bkey, brow, overflow);
     SKY_LAUNCH_CHECK();
     if (pass_end) SKY_CUDA(cudaEventRecord(pass_end, st));
-    const uint32_t run_floats = std::min<uint32_t>(B * d, 16u * 1024);  // <= 64 KB of run coordinates
-    ensure_smem_attr((const void*)k_bucket_pick, 64 * 1024);
-    k_bucket_pick<<<P, 256, run_floats * sizeof(float), st>>>(bkey, brow, cnt, B, pts, d, q, cand, run_floats);
+    // <= 64 KB of run coordinates (a multiple of 4 floats: the slots after them stay 16-byte aligned)
+    const uint32_t run_floats = std::min<uint32_t>(B * d, 16u * 1024) & ~3u;
+    const size_t smem = run_floats * sizeof(float) + (size_t)B * (sizeof(uint64_t) + sizeof(double) + 1) + 16;
+    ensure_smem_attr((const void*)k_bucket_pick, smem);
+    k_bucket_pick<<<P, 256, smem, st>>>(bkey, brow, cnt, B, pts, d, q, cand, run_floats);
     SKY_LAUNCH_CHECK();
 }
 

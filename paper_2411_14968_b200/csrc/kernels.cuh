@@ -140,6 +140,9 @@ void launch_pick_gather(const uint32_t* rows, const uint32_t* gpos, uint32_t slo
 void launch_rep_pick(const uint64_t* key64, const uint32_t* idx, const uint32_t* off, uint32_t P,
                      const float* pts, const double* pts64, uint32_t d, uint32_t q, uint32_t* cand, cudaStream_t st,
                      const uint32_t* off_end = nullptr);
+// stream path (representative filter over large inputs): candidate bucket slots per partition
+constexpr uint32_t kRepBucket = 1024;
+constexpr uint32_t kRepBucketBig = 8192;  // bucket slots of the retry after an overflow (shared memory bound)
 // Stream path of the sorted representatives (select_representatives_sorted,
 // filter.cpp:66-86): per-partition key bound = q-th smallest of the prep
 // CTAs' minima gmin[P][G] -> rows under the bound in B-slot buckets (overflow

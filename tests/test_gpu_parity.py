@@ -338,11 +338,14 @@ def test_filtered_capacity_modes(engine, golden, options, cap_sync):
 
 def test_stream_path_bucket_overflow(engine, options):
     """Candidate buckets that fill up (duplicate-heavy rows, rows sorted by
-    partition) fall back to the sorted path with identical results."""
+    partition): the run is redone with 8,192-slot buckets, and on the sorted
+    path when those overflow too (20,000 identical rows), with identical
+    results."""
     options(stream=1)
     rng = np.random.default_rng(3)
     cases = [
         np.zeros((6000, 3), np.float32),                                   # every row identical
+        np.zeros((20000, 3), np.float32),                                  # more duplicates than the large buckets hold
         np.repeat(rng.random((3, 4), dtype=np.float32), 3000, axis=0),     # three values, 3000 copies
         np.sort(rng.random((20000, 4), dtype=np.float32), axis=0),         # partitions concentrated by row
         rng.integers(0, 3, (20000, 5)).astype(np.float32) / 2,             # lattice ties
